@@ -1,0 +1,380 @@
+#!/usr/bin/env python
+"""Benchmark: Landau point-pair evaluations/s at N = 2^16 (BASELINE.json).
+
+Workload: BASELINE config 5 ("pure kernel sweep") at N = 65536 points, S = 2
+species, outer = inner, seeded synthetic recipe (paper_1702_08880_b200/
+synthetic.py).  One step = one D/K evaluation of all N^2 ordered pairs:
+each rank packs its shard of the inner field state, one all-gather
+replicates it (N > 1), each rank sweeps its N/G outer points against all N
+inner points.  `value` = N^2 * steps / (max over ranks of the summed
+device-timed step durations).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+`--impl reference` times the reference algorithm's CPU implementation (the
+C restatement in oracle/, all host threads; the reference itself is Python +
+numba and is not installable on the GPU box) on a bounded outer sample of
+the same workload, rank 0 only.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+import numpy as np  # noqa: E402
+
+METRIC = "Landau point-pair evals/s at N=2^16"
+UNIT = "pairs/s"
+FLOPS_PER_PAIR = lambda S: 165 + 20 * S * S  # noqa: E731  (kernel.py:560-574)
+
+
+def env_int(name, default):
+    try:
+        return int(os.environ.get(name, default))
+    except ValueError:
+        return default
+
+
+# ----------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled every 100 ms while active."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.idx = gpu_index
+        self.proc = None
+        self.lines = []
+        self.t = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100", "-i", str(self.idx)],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+            time.sleep(0.3)
+        except (OSError, FileNotFoundError):
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append((time.time(), line.strip()))
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        time.sleep(0.15)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        self.t.join(timeout=2)
+        return self.summary()
+
+    def summary(self):
+        rows = []
+        for _, ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                rows.append((float(parts[1]), float(parts[2]), float(parts[3]), parts[5:9]))
+            except ValueError:
+                continue
+        if not rows:
+            return None
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for r in rows for k, v in enumerate(r[3]) if v == "Active"})
+        return {"sm_mhz": statistics.median(r[0] for r in rows),
+                "sm_max_mhz": max(r[1] for r in rows),
+                "power_w_max": max(r[2] for r in rows),
+                "samples": len(rows), "reasons": reasons}
+
+
+def physical_gpu(local_rank: int) -> int:
+    vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+    if vis:
+        ids = [v for v in vis.split(",") if v.strip()]
+        if local_rank < len(ids) and ids[local_rank].strip().isdigit():
+            return int(ids[local_rank])
+    return local_rank
+
+
+# ----------------------------------------------------------------- CPU side
+def cpu_sample(wl, seconds: float, threads: int, min_outer: int = 128):
+    """Time the oracle (reference algorithm restated in C, OpenMP) on a
+    bounded sample: k evenly spaced outer points x all N inner points."""
+    from oracle import oracle as O
+
+    N = wl.N
+
+    def run(k):
+        idx = np.linspace(0, N - 1, k).astype(np.int64)
+        t0 = time.perf_counter()
+        K, D = O.fused_sweep(wl.r[idx], wl.z[idx], wl.r, wl.z, wl.w, wl.f, wl.df_r, wl.df_z,
+                             wl.nu_hat, wl.mass_ratio_o, eps_d=wl.eps_d, threads=threads)
+        return time.perf_counter() - t0, idx, K, D
+
+    t, *_ = run(min_outer)  # warm (page-in, thread pool)
+    rate = min_outer * N / max(t, 1e-9)
+    k = int(min(N, max(min_outer, rate * seconds / N)))
+    return k, run
+
+
+def reference_arm(args):
+    rank = env_int("RANK", 0)
+    if rank != 0:
+        return 0
+    from oracle import oracle as O
+    from paper_1702_08880_b200 import synthetic
+
+    O.build()
+    wl = synthetic.cfg5(args.n)
+    threads = O.max_threads()
+    k, run = cpu_sample(wl, args.ref_step_seconds, threads)
+    for _ in range(args.warmup):
+        run(k)
+    times = [run(k)[0] for _ in range(args.steps)]
+    pairs = k * wl.N
+    value = pairs * len(times) / sum(times)
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "impl": "reference",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * sum(times) / len(times), "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"cfg5 pure kernel sweep N={wl.N} S={wl.S} (BASELINE configs[4])",
+                   "N": wl.N, "S": wl.S, "sample_outer_points": k},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
+                         "sample": f"{k} evenly spaced outer points x all {wl.N} inner points "
+                                   f"per step (oracle/ C restatement of kernel.py:306-493, "
+                                   f"OpenMP {threads} threads)"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "model_gflops": value * FLOPS_PER_PAIR(wl.S) / 1e9,
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ----------------------------------------------------------------- GPU side
+def ours_arm(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_1702_08880_b200 as pkg
+    from paper_1702_08880_b200 import _lib, synthetic
+    from paper_1702_08880_b200.shard import ShardedSweep, local_fields
+
+    world = env_int("WORLD_SIZE", 1)
+    rank = env_int("RANK", 0)
+    local_rank = env_int("LOCAL_RANK", 0)
+    if world != args.gpus and world > 1:
+        print(f"warning: WORLD_SIZE={world} but --gpus={args.gpus}", file=sys.stderr)
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def allmax(vals):
+        t = torch.tensor(vals, dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return t.tolist()
+
+    wl = synthetic.cfg5(args.n)
+    N, S = wl.N, wl.S
+    params = pkg.CollisionParams(nu_hat=wl.nu_hat, mass_ratio_o=wl.mass_ratio_o)
+    sh = ShardedSweep(N, S, params, wl.eps_d, dev, align=1)
+    nloc = sh.hi - sh.lo
+    host = local_fields(wl, sh.lo, sh.hi)
+    d_fields = [torch.from_numpy(a).to(dev) for a in host]
+    lib = _lib.load()
+    ctx = _lib.context(local_rank)
+
+    # FP64 peak at this box's clocks (DFMA microbenchmark; MEASURED_PEAKS.json has none)
+    tf, ms = _lib.C.c_double(), _lib.C.c_double()
+    bursts = []
+    t_end = time.time() + 1.0
+    while time.time() < t_end:
+        _lib.check(lib.lb_fp64_peak(ctx.handle, _lib.C.byref(tf), _lib.C.byref(ms)))
+        bursts.append(tf.value)
+    fp64_burst = max(bursts)
+    fp64_sustained = statistics.median(bursts[len(bursts) // 2:])
+
+    flush = torch.empty(64 << 20, dtype=torch.float32, device=dev)  # 256 MiB > 126 MB L2
+    st = torch.cuda.current_stream(dev)
+
+    def step(ev=None):
+        sh.pack_local(*d_fields)
+        sh.all_gather()
+        if ev is not None:
+            ev[0].record(st)
+        sh.sweep_local(d_fields[0], d_fields[1])
+        if ev is not None:
+            ev[1].record(st)
+
+    for _ in range(args.warmup):
+        step()
+    barrier()
+
+    sampler = ClockSampler(physical_gpu(local_rank)) if args.clocks else None
+    if sampler:
+        sampler.start()
+    E = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
+    sh.launches = 0
+    barrier()
+    for k in range(args.steps):
+        flush.fill_(float(k))  # evict L2 between timed steps (outside the step events)
+        E[k][0].record(st)
+        step(ev=(E[k][1], E[k][2]))
+        E[k][3].record(st)
+    barrier()
+    clocks = sampler.stop() if sampler else None
+    launches = sh.launches
+    step_ms = [E[k][0].elapsed_time(E[k][3]) for k in range(args.steps)]
+    sweep_ms = [E[k][1].elapsed_time(E[k][2]) for k in range(args.steps)]
+    tot_ms, tot_sweep_ms = allmax([sum(step_ms), sum(sweep_ms)])
+    pairs_step = N * N
+    value = pairs_step * args.steps / (tot_ms * 1e-3)
+    # roofline of the dominant kernel on this rank: model flops per launch / launch time
+    sweep_avg_s = sum(sweep_ms) / len(sweep_ms) * 1e-3
+    flops_launch = pkg.flop_count(N, S, nloc)
+    achieved_tf = flops_launch / sweep_avg_s / 1e12
+
+    # e2e through the public API with pinned host buffers (copies inside the timed region)
+    e2e = None
+    if world == 1:
+        pin = [torch.from_numpy(a).pin_memory() for a in host]
+        hp = [t.numpy() for t in pin]
+        data = pkg.QuadPointData(N=N, r=hp[0], z=hp[1], w=hp[2], f=hp[3], df_r=hp[4], df_z=hp[5])
+        pkg.fused_sweep(hp[0], hp[1], data, params, eps_d=wl.eps_d)  # warm
+        ts = []
+        for _ in range(args.e2e_steps):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            K, D = pkg.fused_sweep(hp[0], hp[1], data, params, eps_d=wl.eps_d)
+            ts.append(time.perf_counter() - t0)
+        h2d = 8 * ((3 + 3 * S) * N + 2 * N)
+        d2h = 8 * 6 * S * N
+        e2e = {"value": pairs_step * len(ts) / sum(ts), "unit": UNIT,
+               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+               "api": "paper_1702_08880_b200.fused_sweep (numpy in/out, pinned host)"}
+    else:
+        pin = [torch.from_numpy(a).pin_memory() for a in host]
+        Kh = torch.empty((nloc, S, 2), dtype=torch.float64).pin_memory()
+        Dh = torch.empty((nloc, S, 2, 2), dtype=torch.float64).pin_memory()
+        ts = []
+        for it in range(args.e2e_steps + 1):
+            barrier()
+            t0 = time.perf_counter()
+            for dst, src in zip(d_fields, pin):
+                dst.copy_(src, non_blocking=True)
+            K, D = sh.step(*d_fields)
+            Kh.copy_(K, non_blocking=True)
+            Dh.copy_(D, non_blocking=True)
+            torch.cuda.synchronize()
+            if it:
+                ts.append(time.perf_counter() - t0)
+        tmax = allmax([sum(ts)])[0]
+        e2e = {"value": pairs_step * len(ts) / tmax, "unit": UNIT,
+               "h2d_bytes_per_step": 8 * (3 + 3 * S) * nloc,
+               "d2h_bytes_per_step": 8 * 6 * S * nloc,
+               "api": "paper_1702_08880_b200.shard.ShardedSweep (pinned host in/out)"}
+
+    # CPU baseline (rank 0, N=1): oracle on a bounded sample; doubles as a parity check
+    cpu = None
+    parity = None
+    if world == 1 and rank == 0 and args.cpu_seconds > 0:
+        from oracle import oracle as O
+
+        O.build()
+        threads = O.max_threads()
+        k, run = cpu_sample(wl, args.cpu_seconds, threads)
+        t, idx, Kr, Dr = run(k)
+        cpu = {"value": k * N / t, "unit": UNIT, "cores": threads, "kind": "port",
+               "sample": f"{k} evenly spaced outer points x all {N} inner points "
+                         f"(oracle/ C restatement of kernel.py:306-493, OpenMP, {t:.1f} s)"}
+        parity = O.per_component_scaled_error(K[idx], D[idx], Kr, Dr)
+
+    traffic = None
+    tf_file = ROOT / "profiles" / "sweep_traffic.json"
+    if tf_file.exists():
+        try:
+            traffic = json.loads(tf_file.read_text()).get("bytes_per_launch")
+        except (OSError, ValueError):
+            traffic = None
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": tot_ms / args.steps, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (BASELINE config 5 recipe, seeded)",
+            "config": {"workload": f"cfg5 pure kernel sweep N={N} S={S} (BASELINE configs[4])",
+                       "N": N, "S": S, "outer_per_gpu": nloc, "pairs_per_step": pairs_step,
+                       "parallelism": f"outer-point shards x{world}" + (
+                           " + NCCL all-gather of packed field state" if world > 1 else ""),
+                       "l2": "flushed between timed steps (256 MiB write, outside step events)"},
+            "roofline": {"bound": "fp64", "achieved": achieved_tf, "peak": fp64_sustained,
+                         "unit": "TFLOP/s", "frac": achieved_tf / fp64_sustained,
+                         "traffic": traffic,
+                         "kernel": "lb_sweep_kernel<2> (+ lb_combine_kernel, <1%)",
+                         "flops": "model 165+20*S^2 per pair (kernel.py:560-574)",
+                         "peak_source": "measured DFMA microbenchmark on this GPU "
+                                        "(lb_fp64_peak, median of the last half of 1 s)",
+                         "peak_burst": fp64_burst, "frac_of_nominal_37.2": achieved_tf / 37.2},
+            "e2e": e2e,
+            "gpu_launches": launches,
+            "clocks": clocks,
+            "kernel_ms_per_step": tot_sweep_ms / args.steps,
+        }
+        if cpu:
+            line["cpu_baseline"] = cpu
+            line["parity_scaled_err_vs_oracle"] = parity
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser(description=__doc__.split("\n")[0])
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--n", type=int, default=65536)
+    ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--ref-step-seconds", type=float, default=6.0)
+    ap.add_argument("--no-clocks", dest="clocks", action="store_false")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        print("note: raising --warmup to the required minimum of 3", file=sys.stderr)
+        args.warmup = 3
+    return reference_arm(args) if args.impl == "reference" else ours_arm(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

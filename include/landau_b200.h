@@ -1,0 +1,148 @@
+/*
+ * landau_b200.h -- C ABI of the B200-native Landau pair-integration path.
+ *
+ * This is the drop-in boundary for the hot path of the reference package
+ * `axlandau` (arXiv 1702.08880): the O(N^2) FP64 pair integral that gives
+ * every outer quadrature point its per-species friction vector K and
+ * diffusion tensor D, and the per-element Jacobian contraction B^T[D,K]B.
+ * Citations are `file:line` into the reference tree (pkg/src/axlandau/).
+ *
+ * Conventions
+ *  - All arrays are float64, C order.  Host entry points (no `_dev` suffix)
+ *    take caller-owned HOST pointers, copy in, run, copy out and block until
+ *    the outputs are written (the reference's synchronous semantics).
+ *    `_dev` entry points take DEVICE pointers and a cudaStream_t (passed as
+ *    void*; NULL = the context's own stream) and are asynchronous.
+ *  - Return value: LB_OK (0) or an LB_E* code; `lb_last_error()` returns a
+ *    thread-local message for the most recent failure.  LB_EINVAL maps to
+ *    Python ValueError, everything else to RuntimeError.  There is no CPU
+ *    fallback: without a CUDA device every compute entry fails with
+ *    LB_ENODEV.
+ *  - Species count S: 1 <= S <= LB_MAX_SPECIES.
+ *  - Output layouts match the reference exactly:
+ *      K    (nout, S, 2)        friction  (kernel.py:520)
+ *      D    (nout, S, 2, 2)     diffusion, D[..,0,1] == D[..,1,0] bitwise
+ *                               (kernel.py:521, 437-440)
+ *      elem (S, ncell, 9, 9)    element matrices, row = test i, col = trial j
+ *                               (assembly.py:163-165)
+ *  - Results are deterministic (bitwise run to run) and independent of how
+ *    the outer points are split across calls / GPUs: the inner-point chunking
+ *    depends only on n (the inner count) and every chunk is reduced in a
+ *    fixed order.
+ */
+#ifndef LANDAU_B200_H
+#define LANDAU_B200_H
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define LB_OK 0
+#define LB_EINVAL 1  /* bad argument: maps to ValueError */
+#define LB_ECUDA 2   /* CUDA runtime / launch failure */
+#define LB_ENODEV 3  /* no CUDA device visible */
+#define LB_ENOMEM 4  /* device allocation failed */
+
+#define LB_MAX_SPECIES 8
+
+typedef struct lb_ctx lb_ctx;
+
+/* ABI version (major*100 + minor). */
+int lb_version(void);
+
+/* Thread-local description of the last failure on this thread ("" if none). */
+const char *lb_last_error(void);
+
+/* Number of visible CUDA devices (0 when none); never fails. */
+int lb_device_count(void);
+
+/* One context per (host thread, device): owns a stream and grow-only device
+ * scratch.  Replaces the numba thread pool of kernel.py:524-533. */
+int lb_ctx_create(int device, lb_ctx **out);
+int lb_ctx_destroy(lb_ctx *ctx);
+
+/* Doubles per packed inner-point record for S species (r, z, r^2, 1/r,
+ * then (w*df_r, w*df_z, w*f) per species, padded to an even count). */
+int lb_record_stride(int S);
+
+/* Inner-point chunk length the sweep uses for n inner points (a function of
+ * n only; exposed so tests can check the decomposition). */
+int lb_chunk_len(int n);
+
+/* ---------------------------------------------------------------------
+ * Kernel-level entry: replaces `fused_sweep` (kernel.py:504-536) and the
+ * numba loops under it (_lanes 306-389, _accumulate_block 392-415,
+ * _combine 418-440, _sweep_serial/_sweep_parallel 443-493).
+ *   outer_r/outer_z (nout)            outer points (any points, nout != n ok)
+ *   r, z, w (n); f, df_r, df_z (S, n)  QuadPointData fields (fem.py:133-149)
+ *   coK, coD (S, S)                   coupling from _coupling (kernel.py:496-501)
+ *   eps_d                             exclusion radius; pairs with
+ *                                     d^2 < eps_d^2 or d^2 == 0 are skipped
+ *   K_out (nout,S,2), D_out (nout,S,2,2)
+ * --------------------------------------------------------------------- */
+int lb_fused_sweep(lb_ctx *ctx, int nout, const double *outer_r, const double *outer_z,
+                   int n, int S, const double *r, const double *z, const double *w,
+                   const double *f, const double *df_r, const double *df_z,
+                   const double *coK, const double *coD, double eps_d,
+                   double *K_out, double *D_out);
+
+/* Operator-level entry: replaces the kernel call plus the vectorized outer
+ * point transform and 9x9 element contraction of `assemble_collision`
+ * (assembly.py:148-165).  Points are the mesh's quadrature points in the
+ * order n = 9*cell + q (fem.py:137-140), so n == 9*ncell.
+ *   cell_sizes (ncell, 2)  (dr, dz) per cell (mesh.py VelocityMesh.sizes)
+ *   B (9,9), dB (9,9,2)    reference basis tables (fem.py:66-81)
+ *   K_out, D_out may be NULL (not copied back); elem_out (S, ncell, 9, 9).
+ *   phase_ms (3) may be NULL; else device times (CUDA events) of
+ *   [upload + pack, sweep + coupling, element contraction + download].
+ * The CSR scatter + hanging-node condensation (assembly.py:168-169) stays
+ * with the caller. */
+int lb_assemble_elements(lb_ctx *ctx, int ncell, const double *cell_sizes, int S,
+                         const double *r, const double *z, const double *w,
+                         const double *f, const double *df_r, const double *df_z,
+                         const double *coK, const double *coD, double eps_d,
+                         const double *B, const double *dB,
+                         double *K_out, double *D_out, double *elem_out, double *phase_ms);
+
+/* Per-pair closed form on the device: replaces `axisym_tensor_pair`
+ * (kernel.py:206-235) for npair independent (r, z, rbar, zbar) tuples, with
+ * the same device arithmetic the sweep uses.  UK, UD: (npair, 2, 2).
+ * Coincident pairs (d^2 == 0) return zeros (the sweep's mask). */
+int lb_tensor_pairs(lb_ctx *ctx, int npair, const double *r, const double *z,
+                    const double *rbar, const double *zbar, double *UK, double *UD);
+
+/* ---------------------------------------------------------------------
+ * Device-pointer pieces, used by the multi-GPU layer and the benchmark.
+ * --------------------------------------------------------------------- */
+
+/* Pack n inner points (SoA device arrays) into records of lb_record_stride(S)
+ * doubles: the per-point field state that the sharded path all-gathers. */
+int lb_pack_records_dev(lb_ctx *ctx, int n, int S, const double *r, const double *z,
+                        const double *w, const double *f, const double *df_r,
+                        const double *df_z, double *rec, void *stream);
+
+/* Pair sweep + species coupling over packed records (device pointers).
+ * `n` is the total inner count (all shards), `rec` its packed records. */
+int lb_sweep_dev(lb_ctx *ctx, int nout, const double *outer_r, const double *outer_z,
+                 int n, int S, const double *rec, const double *coK, const double *coD,
+                 double eps_d, double *K_out, double *D_out, void *stream);
+
+/* Outer-point transform + element contraction from device K/D
+ * (assembly.py:151-165).  w (9*ncell) outer weights, cell_sizes (ncell,2). */
+int lb_elements_dev(lb_ctx *ctx, int ncell, int S, const double *cell_sizes,
+                    const double *w, const double *K, const double *D,
+                    const double *B, const double *dB, double *elem_out, void *stream);
+
+/* Number of kernels the most recent lb_sweep_dev / lb_elements_dev /
+ * lb_pack_records_dev call launched (for the benchmark's launch count). */
+int lb_last_launch_count(lb_ctx *ctx);
+
+/* FP64 DFMA throughput microbenchmark on the context's device: a grid of
+ * independent DFMA chains sized to fill every SM, timed with CUDA events.
+ * Writes achieved TFLOP/s (2 flops per DFMA) and the kernel time in ms. */
+int lb_fp64_peak(lb_ctx *ctx, double *tflops, double *ms);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LANDAU_B200_H */

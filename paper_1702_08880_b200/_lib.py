@@ -1,0 +1,142 @@
+"""ctypes binding of liblandau_b200.so (include/landau_b200.h).
+
+Error mapping follows the reference: argument errors raise ValueError (as
+`fused_sweep` does for a species mismatch, kernel.py:517-518), CUDA failures
+and a missing device raise RuntimeError.  There is no CPU fallback: if the
+library or the GPU is missing, every compute call fails loudly.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import threading
+from pathlib import Path
+
+import numpy as np
+
+_PKG = Path(__file__).resolve().parent
+LIB_PATH = _PKG / "liblandau_b200.so"
+
+LB_OK, LB_EINVAL, LB_ECUDA, LB_ENODEV, LB_ENOMEM = 0, 1, 2, 3, 4
+MAX_SPECIES = 8
+
+_dp = C.POINTER(C.c_double)
+_vp = C.c_void_p
+_i = C.c_int
+_d = C.c_double
+
+# symbol -> (restype, argtypes); mirrors include/landau_b200.h one to one
+SIGNATURES = {
+    "lb_version": (_i, []),
+    "lb_last_error": (C.c_char_p, []),
+    "lb_device_count": (_i, []),
+    "lb_ctx_create": (_i, [_i, C.POINTER(_vp)]),
+    "lb_ctx_destroy": (_i, [_vp]),
+    "lb_record_stride": (_i, [_i]),
+    "lb_chunk_len": (_i, [_i]),
+    "lb_fused_sweep": (_i, [_vp, _i, _dp, _dp, _i, _i, _dp, _dp, _dp, _dp, _dp, _dp,
+                            _dp, _dp, _d, _dp, _dp]),
+    "lb_assemble_elements": (_i, [_vp, _i, _dp, _i, _dp, _dp, _dp, _dp, _dp, _dp,
+                                  _dp, _dp, _d, _dp, _dp, _dp, _dp, _dp, _dp]),
+    "lb_tensor_pairs": (_i, [_vp, _i, _dp, _dp, _dp, _dp, _dp, _dp]),
+    "lb_pack_records_dev": (_i, [_vp, _i, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
+    "lb_sweep_dev": (_i, [_vp, _i, _vp, _vp, _i, _i, _vp, _dp, _dp, _d, _vp, _vp, _vp]),
+    "lb_elements_dev": (_i, [_vp, _i, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
+    "lb_last_launch_count": (_i, [_vp]),
+    "lb_fp64_peak": (_i, [_vp, _dp, _dp]),
+}
+
+_lib = None
+_lib_lock = threading.Lock()
+
+
+def load(path: Path | None = None):
+    """Load (once) and type the shared library; raise if it is missing."""
+    global _lib
+    with _lib_lock:
+        if _lib is not None:
+            return _lib
+        p = Path(path) if path else LIB_PATH
+        if not p.exists():
+            raise RuntimeError(
+                f"{p} not built: run `python -m paper_1702_08880_b200.build` "
+                "(there is no CPU fallback for the B200 path)")
+        lib = C.CDLL(str(p))
+        for name, (res, args) in SIGNATURES.items():
+            fn = getattr(lib, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = lib
+        return lib
+
+
+def check(rc: int) -> None:
+    if rc == LB_OK:
+        return
+    msg = load().lb_last_error().decode(errors="replace")
+    if rc == LB_EINVAL:
+        raise ValueError(msg)
+    raise RuntimeError(f"liblandau_b200 error {rc}: {msg}")
+
+
+def dptr(a: np.ndarray):
+    """ctypes double* to a C-contiguous float64 array (caller keeps it alive)."""
+    assert a.dtype == np.float64 and a.flags.c_contiguous
+    return a.ctypes.data_as(_dp)
+
+
+class Context:
+    """One lb_ctx (stream + device scratch) bound to a device."""
+
+    def __init__(self, device: int = 0):
+        lib = load()
+        h = _vp()
+        check(lib.lb_ctx_create(int(device), C.byref(h)))
+        self.handle = h
+        self.device = int(device)
+        self._lib = lib
+
+    def close(self):
+        if getattr(self, "handle", None):
+            self._lib.lb_ctx_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):  # pragma: no cover - interpreter teardown order varies
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+_tls = threading.local()
+
+
+def context(device: int | None = None) -> Context:
+    """Per-(thread, device) cached context (the reference is single-threaded
+    per call; contexts are not shared across host threads)."""
+    if device is None:
+        device = current_device()
+    cache = getattr(_tls, "ctx", None)
+    if cache is None:
+        cache = _tls.ctx = {}
+    if device not in cache:
+        cache[device] = Context(device)
+    return cache[device]
+
+
+def current_device() -> int:
+    """Device for the calling thread: torch's current device if torch is
+    already imported and initialised, else 0."""
+    import sys
+    torch = sys.modules.get("torch")
+    if torch is not None:
+        try:
+            if torch.cuda.is_available() and torch.cuda.is_initialized():
+                return int(torch.cuda.current_device())
+        except Exception:
+            pass
+    return 0
+
+
+def device_count() -> int:
+    return int(load().lb_device_count())

@@ -1,0 +1,817 @@
+// landau_b200.cu -- sm_100a kernels and the C ABI of include/landau_b200.h.
+//
+// Kernels
+//   K0 lb_pack_kernel      SoA QuadPointData -> packed inner records
+//                          (r, z, r^2, 1/r, (w df_r, w df_z, w f) x S)
+//   K1 lb_sweep_kernel<S>  FP64 pair sweep: persistent CTAs walk work items
+//                          (128 outer points x one inner chunk); inner
+//                          records stream through a 2-stage shared-memory
+//                          ring filled by cp.async.bulk (TMA bulk copies)
+//                          completing on mbarriers; each thread holds one
+//                          outer point and its 5S accumulators in registers;
+//                          per-chunk partial sums go to HBM.
+//   K1b lb_combine_kernel<S>  fixed-order reduction of the chunk partials +
+//                          S x S species coupling (kernel.py:418-440).
+//   K2 lb_elements_kernel  outer-point transform G2/G3 + 9x9 element
+//                          contraction per (cell, species) (assembly.py:151-165).
+//   lb_pairs_kernel        per-pair closed form (axisym_tensor_pair).
+//   lb_dfma_kernel         FP64 DFMA peak microbenchmark (the roofline peak).
+//
+// Determinism: inner chunk boundaries depend only on n; within a chunk the
+// inner points are summed in index order, chunks are summed in index order;
+// no atomics.  Results are bitwise reproducible and independent of how outer
+// points are split across calls or GPUs.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdint>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/landau_b200.h"
+#include "landau_pair.cuh"
+
+namespace lb {
+
+constexpr int kTI = 128;        // outer points per CTA (one per thread)
+constexpr int kMinBlocks = 4;   // CTAs per SM the register budget targets
+constexpr int kMaxChunks = 64;  // inner chunks per sweep (sets the JC length)
+constexpr int kChunkAlign = 128;
+constexpr size_t kPartialBudget = size_t(2) << 30;  // bytes of chunk partials per pass
+
+__host__ __device__ constexpr int rec_stride(int S) { return ((4 + 3 * S) + 1) & ~1; }
+template <int S>
+struct TileCfg {
+  static constexpr int RS = rec_stride(S);
+  static constexpr int TJ = S <= 4 ? 128 : 64;  // inner records per stage
+};
+
+struct Coupling {
+  double coK4[LB_MAX_SPECIES * LB_MAX_SPECIES];  // 4 * coK (the pulled-out 4)
+  double coD4[LB_MAX_SPECIES * LB_MAX_SPECIES];
+};
+
+// ------------------------------------------------------------------ PTX helpers
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "LB_WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra LB_WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+// 1-D TMA bulk copy global -> shared, completion counted on `bar`.
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// ------------------------------------------------------------------ K0 pack
+__global__ void lb_pack_kernel(int n, int S, int RS, const double* __restrict__ r,
+                               const double* __restrict__ z, const double* __restrict__ w,
+                               const double* __restrict__ f, const double* __restrict__ dfr,
+                               const double* __restrict__ dfz, double* __restrict__ rec) {
+  for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < n; p += gridDim.x * blockDim.x) {
+    const double rn = r[p], wn = w[p];
+    double* o = rec + (size_t)p * RS;
+    o[0] = rn;
+    o[1] = z[p];
+    o[2] = rn * rn;
+    o[3] = rn > 0.0 ? 1.0 / rn : 0.0;
+    for (int b = 0; b < S; ++b) {
+      // same products as _accumulate_block (kernel.py:408-410)
+      o[4 + 3 * b + 0] = dfr[(size_t)b * n + p] * wn;
+      o[4 + 3 * b + 1] = dfz[(size_t)b * n + p] * wn;
+      o[4 + 3 * b + 2] = f[(size_t)b * n + p] * wn;
+    }
+    for (int k = 4 + 3 * S; k < RS; ++k) o[k] = 0.0;
+  }
+}
+
+// ------------------------------------------------------------------ K1 sweep
+struct SweepArgs {
+  const double* ro;   // outer r (nout)
+  const double* zo;   // outer z (nout)
+  const double* rec;  // packed inner records (n x RS)
+  double* partial;    // [nchunk][5S][nout_pad]
+  int nout, nout_pad, n, jc, nchunk;
+  long long gthr;     // mask threshold on bits(d^2)
+};
+
+template <int S>
+__global__ void __launch_bounds__(kTI, kMinBlocks) lb_sweep_kernel(const SweepArgs a) {
+  constexpr int RS = TileCfg<S>::RS;
+  constexpr int TJ = TileCfg<S>::TJ;
+  extern __shared__ __align__(128) double lb_smem[];
+  __shared__ __align__(8) uint64_t bar[2];
+
+  const int tid = threadIdx.x;
+  const int nib = a.nout_pad / kTI;
+  const long long nitems = (long long)nib * a.nchunk;
+
+  if (tid == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  // producer cursor (meaningful on thread 0 only): next (item, tile) to load
+  long long p_item = blockIdx.x;
+  int p_tile = 0;
+  uint32_t p_k = 0;
+  auto issue_next = [&]() {
+    if (p_item >= nitems) return;
+    const int c = (int)(p_item / nib);
+    const int j0 = c * a.jc + p_tile * TJ;
+    const int jend = min(a.n, (c + 1) * a.jc);
+    const int cnt = min(TJ, jend - j0);
+    const uint32_t bytes = (uint32_t)cnt * RS * sizeof(double);
+    uint64_t* b = &bar[p_k & 1];
+    mbar_expect_tx(b, bytes);
+    bulk_g2s(lb_smem + (p_k & 1) * (TJ * RS), a.rec + (size_t)j0 * RS, bytes, b);
+    ++p_k;
+    if (j0 + TJ >= jend) {
+      p_tile = 0;
+      p_item += gridDim.x;
+    } else {
+      ++p_tile;
+    }
+  };
+  if (tid == 0) issue_next();
+
+  uint32_t k = 0;  // consumer tile counter (same sequence as the producer)
+  for (long long item = blockIdx.x; item < nitems; item += gridDim.x) {
+    const int ib = (int)(item % nib);
+    const int c = (int)(item / nib);
+    const int i = ib * kTI + tid;
+    const int il = min(i, a.nout - 1);
+    const Outer o = make_outer(a.ro[il], a.zo[il]);
+    double acc[S][5];
+#pragma unroll
+    for (int b = 0; b < S; ++b)
+#pragma unroll
+      for (int q = 0; q < 5; ++q) acc[b][q] = 0.0;
+
+    const int jbeg = c * a.jc;
+    const int jend = min(a.n, jbeg + a.jc);
+    for (int j0 = jbeg; j0 < jend; j0 += TJ, ++k) {
+      if (tid == 0) issue_next();
+      mbar_wait(&bar[k & 1], (k >> 1) & 1);
+      const double* tile = lb_smem + (k & 1) * (TJ * RS);
+      const int cnt = min(TJ, jend - j0);
+#pragma unroll 1
+      for (int jj = 0; jj < cnt; ++jj) {
+        const double* rp = tile + jj * RS;
+        const double2 rz = *reinterpret_cast<const double2*>(rp);
+        const double2 aux = *reinterpret_cast<const double2*>(rp + 2);
+        const T5 t = pair_tensor(o, rz.x, rz.y, aux.x, aux.y, a.gthr);
+#pragma unroll
+        for (int b = 0; b < S; ++b) {
+          const double gr = rp[4 + 3 * b], gz = rp[5 + 3 * b], fw = rp[6 + 3 * b];
+          // _accumulate_block (kernel.py:411-415)
+          acc[b][0] = fma(t.xz, gz, fma(t.kr, gr, acc[b][0]));
+          acc[b][1] = fma(t.zz, gz, fma(t.zr, gr, acc[b][1]));
+          acc[b][2] = fma(fw, t.xx, acc[b][2]);
+          acc[b][3] = fma(fw, t.xz, acc[b][3]);
+          acc[b][4] = fma(fw, t.zz, acc[b][4]);
+        }
+      }
+      __syncthreads();  // stage (k & 1) free for the producer
+    }
+    if (i < a.nout) {
+      double* dst = a.partial + (size_t)c * (5 * S) * a.nout_pad + i;
+#pragma unroll
+      for (int b = 0; b < S; ++b)
+#pragma unroll
+        for (int q = 0; q < 5; ++q) dst[(size_t)(b * 5 + q) * a.nout_pad] = acc[b][q];
+    }
+  }
+}
+
+// ------------------------------------------------------------------ K1b combine
+template <int S>
+__global__ void lb_combine_kernel(const double* __restrict__ partial, int nchunk, int nout,
+                                  int nout_pad, const Coupling cp, double* __restrict__ K,
+                                  double* __restrict__ D) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= nout) return;
+  double A[S][5];
+#pragma unroll
+  for (int b = 0; b < S; ++b)
+#pragma unroll
+    for (int q = 0; q < 5; ++q) A[b][q] = 0.0;
+  for (int c = 0; c < nchunk; ++c) {
+    const double* src = partial + (size_t)c * (5 * S) * nout_pad + i;
+#pragma unroll
+    for (int b = 0; b < S; ++b)
+#pragma unroll
+      for (int q = 0; q < 5; ++q) A[b][q] = __dadd_rn(A[b][q], src[(size_t)(b * 5 + q) * nout_pad]);
+  }
+  // _combine (kernel.py:419-440): strict order, no contraction
+#pragma unroll
+  for (int a = 0; a < S; ++a) {
+    double k0 = 0.0, k1 = 0.0, d0 = 0.0, d1 = 0.0, d2 = 0.0;
+#pragma unroll
+    for (int b = 0; b < S; ++b) {
+      const double ck = cp.coK4[a * S + b], cd = cp.coD4[a * S + b];
+      k0 = __dadd_rn(k0, __dmul_rn(ck, A[b][0]));
+      k1 = __dadd_rn(k1, __dmul_rn(ck, A[b][1]));
+      d0 = __dadd_rn(d0, __dmul_rn(cd, A[b][2]));
+      d1 = __dadd_rn(d1, __dmul_rn(cd, A[b][3]));
+      d2 = __dadd_rn(d2, __dmul_rn(cd, A[b][4]));
+    }
+    double* Ko = K + ((size_t)i * S + a) * 2;
+    double* Do = D + ((size_t)i * S + a) * 4;
+    Ko[0] = k0;
+    Ko[1] = k1;
+    Do[0] = d0;
+    Do[1] = d1;
+    Do[2] = d1;
+    Do[3] = d2;
+  }
+}
+
+// ------------------------------------------------------------------ K2 elements
+// One warp per (species a, cell e).  G2 = K Jinv w, G3 = Jinv D Jinv w
+// (assembly.py:159-160), then
+//   elem[a,e,i,j] = sum_q dB[i,q,:].G2[q] B[j,q] + sum_q dB[i,q,:].G3[q].dB[j,q,:]
+// computed as u[i,q] = dB[i,q,:].G2[q], v[i,q,:] = dB[i,q,:].G3[q] followed
+// by a 27-term dot product per entry.
+constexpr int kElemWarps = 4;
+__global__ void __launch_bounds__(32 * kElemWarps) lb_elements_kernel(
+    int ncell, int S, const double* __restrict__ sizes, const double* __restrict__ w,
+    const double* __restrict__ K, const double* __restrict__ D, const double* __restrict__ Bt,
+    const double* __restrict__ dBt, double* __restrict__ elem) {
+  __shared__ double sB[81], sdB[162];
+  __shared__ double sG[kElemWarps][9][6];  // G2 r,z ; G3 rr, rz, zr, zz
+  __shared__ double su[kElemWarps][81], sv[kElemWarps][162];
+  for (int t = threadIdx.x; t < 81; t += blockDim.x) sB[t] = Bt[t];
+  for (int t = threadIdx.x; t < 162; t += blockDim.x) sdB[t] = dBt[t];
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const long long nwork = (long long)ncell * S;
+  for (long long wk = (long long)blockIdx.x * kElemWarps + warp; wk < nwork;
+       wk += (long long)gridDim.x * kElemWarps) {
+    const int a = (int)(wk / ncell);
+    const int e = (int)(wk % ncell);
+    const double jr = 2.0 / sizes[2 * e], jz = 2.0 / sizes[2 * e + 1];
+    if (lane < 9) {
+      const int pnt = 9 * e + lane;
+      const double wp = w[pnt];
+      const double* Kp = K + ((size_t)pnt * S + a) * 2;
+      const double* Dp = D + ((size_t)pnt * S + a) * 4;
+      // same factor grouping as assembly.py:159-160
+      sG[warp][lane][0] = Kp[0] * (jr * wp);
+      sG[warp][lane][1] = Kp[1] * (jz * wp);
+      sG[warp][lane][2] = Dp[0] * ((jr * jr) * wp);
+      sG[warp][lane][3] = Dp[1] * ((jr * jz) * wp);
+      sG[warp][lane][4] = Dp[2] * ((jz * jr) * wp);
+      sG[warp][lane][5] = Dp[3] * ((jz * jz) * wp);
+    }
+    __syncwarp();
+    for (int t = lane; t < 81; t += 32) {  // t = 9*i + q
+      const int q = t % 9;
+      const double* g = sG[warp][q];
+      const double b0 = sdB[2 * t], b1 = sdB[2 * t + 1];
+      su[warp][t] = fma(b1, g[1], b0 * g[0]);
+      sv[warp][2 * t] = fma(b1, g[4], b0 * g[2]);
+      sv[warp][2 * t + 1] = fma(b1, g[5], b0 * g[3]);
+    }
+    __syncwarp();
+    double* out = elem + ((size_t)a * ncell + e) * 81;
+    for (int t = lane; t < 81; t += 32) {  // t = 9*i + j
+      const int ii = t / 9, jj = t % 9;
+      double s = 0.0;
+#pragma unroll
+      for (int q = 0; q < 9; ++q) {
+        s = fma(su[warp][9 * ii + q], sB[9 * jj + q], s);
+        s = fma(sv[warp][2 * (9 * ii + q)], sdB[2 * (9 * jj + q)], s);
+        s = fma(sv[warp][2 * (9 * ii + q) + 1], sdB[2 * (9 * jj + q) + 1], s);
+      }
+      out[t] = s;
+    }
+    __syncwarp();
+  }
+}
+
+// ------------------------------------------------------------------ per-pair
+__global__ void lb_pairs_kernel(int npair, const double* __restrict__ r, const double* __restrict__ z,
+                                const double* __restrict__ rb, const double* __restrict__ zb,
+                                double* __restrict__ UK, double* __restrict__ UD) {
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= npair) return;
+  const Outer o = make_outer(r[p], z[p]);
+  const double rn = rb[p];
+  const T5 t = pair_tensor(o, rn, zb[p], rn * rn, rn > 0.0 ? 1.0 / rn : 0.0, 1LL);
+  // restore the pulled-out factor 4 (exact) and lay out as kernel.py:227-234
+  UD[4 * p + 0] = 4.0 * t.xx;
+  UD[4 * p + 1] = 4.0 * t.xz;
+  UD[4 * p + 2] = 4.0 * t.xz;
+  UD[4 * p + 3] = 4.0 * t.zz;
+  UK[4 * p + 0] = 4.0 * t.kr;
+  UK[4 * p + 1] = 4.0 * t.xz;
+  UK[4 * p + 2] = 4.0 * t.zr;
+  UK[4 * p + 3] = 4.0 * t.zz;
+}
+
+// ------------------------------------------------------------------ FP64 peak
+constexpr int kDfmaChains = 8;
+constexpr int kDfmaIters = 4096;
+__global__ void __launch_bounds__(256) lb_dfma_kernel(double seed, double* sink) {
+  double v[kDfmaChains];
+#pragma unroll
+  for (int c = 0; c < kDfmaChains; ++c) v[c] = seed + threadIdx.x * 1e-9 + c;
+  const double m = 0.999999, add = 1e-7;
+#pragma unroll 4
+  for (int it = 0; it < kDfmaIters; ++it) {
+#pragma unroll
+    for (int c = 0; c < kDfmaChains; ++c) v[c] = fma(v[c], m, add);
+  }
+  double s = 0.0;
+#pragma unroll
+  for (int c = 0; c < kDfmaChains; ++c) s += v[c];
+  if (s == 12345.6789) sink[threadIdx.x] = s;  // never true; keeps the chains live
+}
+
+// ------------------------------------------------------------------ host side
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+#define LB_CUDA(call)                                                                     \
+  do {                                                                                    \
+    cudaError_t e_ = (call);                                                              \
+    if (e_ != cudaSuccess)                                                                \
+      return fail(e_ == cudaErrorMemoryAllocation ? LB_ENOMEM : LB_ECUDA,                 \
+                  std::string(#call) + ": " + cudaGetErrorString(e_));                    \
+  } while (0)
+
+struct DevBuf {
+  void* p = nullptr;
+  size_t cap = 0;
+};
+
+}  // namespace lb
+
+struct lb_ctx {
+  int device = 0;
+  int num_sms = 0;
+  cudaStream_t stream = nullptr;
+  int last_launches = 0;
+  cudaEvent_t ev[4] = {};
+  // grow-only scratch
+  lb::DevBuf in, rec, partial, out, elem, outer, aux;
+};
+
+namespace lb {
+
+int ensure(DevBuf& b, size_t bytes) {
+  if (bytes <= b.cap) return LB_OK;
+  if (b.p) cudaFree(b.p);
+  b.p = nullptr;
+  b.cap = 0;
+  size_t want = std::max(bytes, size_t(1) << 20);
+  cudaError_t e = cudaMalloc(&b.p, want);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return fail(LB_ENOMEM, std::string("cudaMalloc(") + std::to_string(want) + "): " +
+                               cudaGetErrorString(e));
+  }
+  b.cap = want;
+  return LB_OK;
+}
+
+int use_ctx(lb_ctx* ctx) {
+  if (!ctx) return fail(LB_EINVAL, "null lb_ctx");
+  LB_CUDA(cudaSetDevice(ctx->device));
+  return LB_OK;
+}
+
+int chunk_len(int n) {
+  int per = (n + kMaxChunks - 1) / kMaxChunks;
+  per = ((per + kChunkAlign - 1) / kChunkAlign) * kChunkAlign;
+  return std::max(per, kChunkAlign);
+}
+
+long long mask_threshold(double eps_d) {
+  const double eps2 = eps_d * eps_d;
+  long long bits;
+  std::memcpy(&bits, &eps2, sizeof(bits));
+  return std::max(bits, 1LL);
+}
+
+int make_coupling(int S, const double* coK, const double* coD, Coupling& cp) {
+  std::memset(&cp, 0, sizeof(cp));
+  for (int t = 0; t < S * S; ++t) {
+    cp.coK4[t] = 4.0 * coK[t];
+    cp.coD4[t] = 4.0 * coD[t];
+  }
+  return LB_OK;
+}
+
+template <int S>
+int launch_sweep(lb_ctx* ctx, int nout, const double* ro, const double* zo, int n,
+                 const double* rec, const Coupling& cp, long long gthr, double* K, double* D,
+                 cudaStream_t st) {
+  constexpr int RS = TileCfg<S>::RS;
+  constexpr int TJ = TileCfg<S>::TJ;
+  const size_t smem = size_t(2) * TJ * RS * sizeof(double);
+  static bool attr_done[64] = {};
+  if (!attr_done[ctx->device & 63]) {
+    LB_CUDA(cudaFuncSetAttribute(lb_sweep_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)smem));
+    attr_done[ctx->device & 63] = true;
+  }
+  int per_sm = 0;
+  LB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, lb_sweep_kernel<S>, kTI, smem));
+  per_sm = std::max(per_sm, 1);
+  const int jc = chunk_len(n);
+  const int nchunk = (n + jc - 1) / jc;
+  // outer batches bounded by the partial-buffer budget
+  const size_t per_outer = size_t(nchunk) * 5 * S * sizeof(double);
+  int batch = (int)std::min<size_t>((size_t)nout, std::max<size_t>(kTI, kPartialBudget / per_outer));
+  batch = std::max(kTI, (batch / kTI) * kTI);
+  int launches = 0;
+  for (int o0 = 0; o0 < nout; o0 += batch) {
+    const int nb = std::min(batch, nout - o0);
+    const int nout_pad = ((nb + kTI - 1) / kTI) * kTI;
+    int rc = ensure(ctx->partial, size_t(nchunk) * 5 * S * nout_pad * sizeof(double));
+    if (rc) return rc;
+    SweepArgs a;
+    a.ro = ro + o0;
+    a.zo = zo + o0;
+    a.rec = rec;
+    a.partial = static_cast<double*>(ctx->partial.p);
+    a.nout = nb;
+    a.nout_pad = nout_pad;
+    a.n = n;
+    a.jc = jc;
+    a.nchunk = nchunk;
+    a.gthr = gthr;
+    const long long nitems = (long long)(nout_pad / kTI) * nchunk;
+    const int grid = (int)std::min<long long>(nitems, (long long)ctx->num_sms * per_sm);
+    lb_sweep_kernel<S><<<grid, kTI, smem, st>>>(a);
+    LB_CUDA(cudaGetLastError());
+    lb_combine_kernel<S><<<(nb + 127) / 128, 128, 0, st>>>(a.partial, nchunk, nb, nout_pad, cp,
+                                                           K + (size_t)o0 * S * 2,
+                                                           D + (size_t)o0 * S * 4);
+    LB_CUDA(cudaGetLastError());
+    launches += 2;
+  }
+  ctx->last_launches = launches;
+  return LB_OK;
+}
+
+int sweep_dispatch(lb_ctx* ctx, int nout, const double* ro, const double* zo, int n, int S,
+                   const double* rec, const Coupling& cp, long long gthr, double* K, double* D,
+                   cudaStream_t st) {
+  switch (S) {
+    case 1: return launch_sweep<1>(ctx, nout, ro, zo, n, rec, cp, gthr, K, D, st);
+    case 2: return launch_sweep<2>(ctx, nout, ro, zo, n, rec, cp, gthr, K, D, st);
+    case 3: return launch_sweep<3>(ctx, nout, ro, zo, n, rec, cp, gthr, K, D, st);
+    case 4: return launch_sweep<4>(ctx, nout, ro, zo, n, rec, cp, gthr, K, D, st);
+    case 5: return launch_sweep<5>(ctx, nout, ro, zo, n, rec, cp, gthr, K, D, st);
+    case 6: return launch_sweep<6>(ctx, nout, ro, zo, n, rec, cp, gthr, K, D, st);
+    case 7: return launch_sweep<7>(ctx, nout, ro, zo, n, rec, cp, gthr, K, D, st);
+    case 8: return launch_sweep<8>(ctx, nout, ro, zo, n, rec, cp, gthr, K, D, st);
+    default: return fail(LB_EINVAL, "species count must be in [1, 8]");
+  }
+}
+
+int check_species(int S) {
+  if (S < 1 || S > LB_MAX_SPECIES)
+    return fail(LB_EINVAL, "species count " + std::to_string(S) + " outside [1, " +
+                               std::to_string(LB_MAX_SPECIES) + "]");
+  return LB_OK;
+}
+
+int launch_pack(lb_ctx* ctx, int n, int S, const double* r, const double* z, const double* w,
+                const double* f, const double* dfr, const double* dfz, double* rec,
+                cudaStream_t st) {
+  if (n == 0) return LB_OK;
+  const int threads = 256;
+  const int blocks = std::min((n + threads - 1) / threads, ctx->num_sms * 8);
+  lb_pack_kernel<<<blocks, threads, 0, st>>>(n, S, rec_stride(S), r, z, w, f, dfr, dfz, rec);
+  LB_CUDA(cudaGetLastError());
+  return LB_OK;
+}
+
+int launch_elements(lb_ctx* ctx, int ncell, int S, const double* sizes, const double* w,
+                    const double* K, const double* D, const double* B, const double* dB,
+                    double* elem, cudaStream_t st) {
+  if (ncell == 0) return LB_OK;
+  const long long nwork = (long long)ncell * S;
+  const int blocks =
+      (int)std::min<long long>((nwork + kElemWarps - 1) / kElemWarps, (long long)ctx->num_sms * 16);
+  lb_elements_kernel<<<blocks, 32 * kElemWarps, 0, st>>>(ncell, S, sizes, w, K, D, B, dB, elem);
+  LB_CUDA(cudaGetLastError());
+  return LB_OK;
+}
+
+}  // namespace lb
+
+using namespace lb;
+
+// ====================================================================== C ABI
+extern "C" {
+
+int lb_version(void) { return 100; }
+
+const char* lb_last_error(void) { return g_err.c_str(); }
+
+int lb_device_count(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return n;
+}
+
+int lb_ctx_create(int device, lb_ctx** out) {
+  if (!out) return fail(LB_EINVAL, "null output pointer");
+  *out = nullptr;
+  int ndev = lb_device_count();
+  if (ndev <= 0) return fail(LB_ENODEV, "no CUDA device visible (the B200 path has no CPU fallback)");
+  if (device < 0 || device >= ndev)
+    return fail(LB_EINVAL, "device " + std::to_string(device) + " not in [0, " +
+                               std::to_string(ndev) + ")");
+  LB_CUDA(cudaSetDevice(device));
+  lb_ctx* c = new lb_ctx();
+  c->device = device;
+  cudaDeviceProp prop;
+  cudaError_t e = cudaGetDeviceProperties(&prop, device);
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
+  if (e != cudaSuccess) {
+    delete c;
+    return fail(LB_ECUDA, std::string("context setup: ") + cudaGetErrorString(e));
+  }
+  if (prop.major < 10) {
+    cudaStreamDestroy(c->stream);
+    delete c;
+    return fail(LB_ENODEV, std::string("device ") + prop.name + " is sm_" +
+                               std::to_string(prop.major * 10 + prop.minor) +
+                               "; this library is built for sm_100a (B200) only");
+  }
+  c->num_sms = prop.multiProcessorCount;
+  for (auto& ev : c->ev) cudaEventCreate(&ev);
+  *out = c;
+  return LB_OK;
+}
+
+int lb_ctx_destroy(lb_ctx* ctx) {
+  if (!ctx) return LB_OK;
+  cudaSetDevice(ctx->device);
+  for (DevBuf* b : {&ctx->in, &ctx->rec, &ctx->partial, &ctx->out, &ctx->elem, &ctx->outer, &ctx->aux})
+    if (b->p) cudaFree(b->p);
+  for (auto& ev : ctx->ev)
+    if (ev) cudaEventDestroy(ev);
+  if (ctx->stream) cudaStreamDestroy(ctx->stream);
+  delete ctx;
+  return LB_OK;
+}
+
+int lb_record_stride(int S) {
+  if (check_species(S)) return -1;
+  return rec_stride(S);
+}
+
+int lb_chunk_len(int n) { return chunk_len(std::max(n, 0)); }
+
+int lb_last_launch_count(lb_ctx* ctx) { return ctx ? ctx->last_launches : 0; }
+
+int lb_pack_records_dev(lb_ctx* ctx, int n, int S, const double* r, const double* z,
+                        const double* w, const double* f, const double* df_r,
+                        const double* df_z, double* rec, void* stream) {
+  int rc = use_ctx(ctx);
+  if (rc) return rc;
+  if ((rc = check_species(S))) return rc;
+  if (n < 0) return fail(LB_EINVAL, "negative point count");
+  cudaStream_t st = stream ? (cudaStream_t)stream : ctx->stream;
+  rc = launch_pack(ctx, n, S, r, z, w, f, df_r, df_z, rec, st);
+  ctx->last_launches = n > 0 ? 1 : 0;
+  return rc;
+}
+
+int lb_sweep_dev(lb_ctx* ctx, int nout, const double* outer_r, const double* outer_z, int n,
+                 int S, const double* rec, const double* coK, const double* coD, double eps_d,
+                 double* K_out, double* D_out, void* stream) {
+  int rc = use_ctx(ctx);
+  if (rc) return rc;
+  if ((rc = check_species(S))) return rc;
+  if (nout < 0 || n < 0) return fail(LB_EINVAL, "negative point count");
+  if (!coK || !coD) return fail(LB_EINVAL, "null coupling table");
+  cudaStream_t st = stream ? (cudaStream_t)stream : ctx->stream;
+  ctx->last_launches = 0;
+  if (nout == 0) return LB_OK;
+  if (n == 0) {  // empty inner set: all sums are +0
+    LB_CUDA(cudaMemsetAsync(K_out, 0, sizeof(double) * nout * S * 2, st));
+    LB_CUDA(cudaMemsetAsync(D_out, 0, sizeof(double) * nout * S * 4, st));
+    return LB_OK;
+  }
+  Coupling cp;
+  make_coupling(S, coK, coD, cp);
+  return sweep_dispatch(ctx, nout, outer_r, outer_z, n, S, rec, cp, mask_threshold(eps_d), K_out,
+                        D_out, st);
+}
+
+int lb_elements_dev(lb_ctx* ctx, int ncell, int S, const double* cell_sizes, const double* w,
+                    const double* K, const double* D, const double* B, const double* dB,
+                    double* elem_out, void* stream) {
+  int rc = use_ctx(ctx);
+  if (rc) return rc;
+  if ((rc = check_species(S))) return rc;
+  if (ncell < 0) return fail(LB_EINVAL, "negative cell count");
+  cudaStream_t st = stream ? (cudaStream_t)stream : ctx->stream;
+  rc = launch_elements(ctx, ncell, S, cell_sizes, w, K, D, B, dB, elem_out, st);
+  ctx->last_launches = ncell > 0 ? 1 : 0;
+  return rc;
+}
+
+int lb_fused_sweep(lb_ctx* ctx, int nout, const double* outer_r, const double* outer_z, int n,
+                   int S, const double* r, const double* z, const double* w, const double* f,
+                   const double* df_r, const double* df_z, const double* coK, const double* coD,
+                   double eps_d, double* K_out, double* D_out) {
+  int rc = use_ctx(ctx);
+  if (rc) return rc;
+  if ((rc = check_species(S))) return rc;
+  if (nout < 0 || n < 0) return fail(LB_EINVAL, "negative point count");
+  if (nout == 0) return LB_OK;
+  if (!outer_r || !outer_z || !K_out || !D_out || !coK || !coD)
+    return fail(LB_EINVAL, "null argument");
+  if (n > 0 && (!r || !z || !w || !f || !df_r || !df_z)) return fail(LB_EINVAL, "null inner field");
+  cudaStream_t st = ctx->stream;
+  const size_t nin = (size_t)(3 + 3 * S) * n;
+  if ((rc = ensure(ctx->in, std::max<size_t>(nin, 1) * sizeof(double)))) return rc;
+  if ((rc = ensure(ctx->rec, std::max<size_t>((size_t)n * rec_stride(S), 1) * sizeof(double)))) return rc;
+  if ((rc = ensure(ctx->outer, (size_t)2 * nout * sizeof(double)))) return rc;
+  if ((rc = ensure(ctx->out, (size_t)6 * S * nout * sizeof(double)))) return rc;
+  double* din = static_cast<double*>(ctx->in.p);
+  double *dr = din, *dz = dr + n, *dw = dz + n, *df = dw + n, *dfr = df + (size_t)S * n,
+         *dfz = dfr + (size_t)S * n;
+  double* dro = static_cast<double*>(ctx->outer.p);
+  double* dzo = dro + nout;
+  double* dK = static_cast<double*>(ctx->out.p);
+  double* dD = dK + (size_t)2 * S * nout;
+  const size_t bn = sizeof(double) * n, bsn = sizeof(double) * S * n;
+  if (n > 0) {
+    LB_CUDA(cudaMemcpyAsync(dr, r, bn, cudaMemcpyHostToDevice, st));
+    LB_CUDA(cudaMemcpyAsync(dz, z, bn, cudaMemcpyHostToDevice, st));
+    LB_CUDA(cudaMemcpyAsync(dw, w, bn, cudaMemcpyHostToDevice, st));
+    LB_CUDA(cudaMemcpyAsync(df, f, bsn, cudaMemcpyHostToDevice, st));
+    LB_CUDA(cudaMemcpyAsync(dfr, df_r, bsn, cudaMemcpyHostToDevice, st));
+    LB_CUDA(cudaMemcpyAsync(dfz, df_z, bsn, cudaMemcpyHostToDevice, st));
+  }
+  LB_CUDA(cudaMemcpyAsync(dro, outer_r, sizeof(double) * nout, cudaMemcpyHostToDevice, st));
+  LB_CUDA(cudaMemcpyAsync(dzo, outer_z, sizeof(double) * nout, cudaMemcpyHostToDevice, st));
+  double* drec = static_cast<double*>(ctx->rec.p);
+  if ((rc = launch_pack(ctx, n, S, dr, dz, dw, df, dfr, dfz, drec, st))) return rc;
+  if ((rc = lb_sweep_dev(ctx, nout, dro, dzo, n, S, drec, coK, coD, eps_d, dK, dD, st))) return rc;
+  LB_CUDA(cudaMemcpyAsync(K_out, dK, sizeof(double) * 2 * S * nout, cudaMemcpyDeviceToHost, st));
+  LB_CUDA(cudaMemcpyAsync(D_out, dD, sizeof(double) * 4 * S * nout, cudaMemcpyDeviceToHost, st));
+  LB_CUDA(cudaStreamSynchronize(st));
+  return LB_OK;
+}
+
+int lb_assemble_elements(lb_ctx* ctx, int ncell, const double* cell_sizes, int S, const double* r,
+                         const double* z, const double* w, const double* f, const double* df_r,
+                         const double* df_z, const double* coK, const double* coD, double eps_d,
+                         const double* B, const double* dB, double* K_out, double* D_out,
+                         double* elem_out, double* phase_ms) {
+  int rc = use_ctx(ctx);
+  if (rc) return rc;
+  if ((rc = check_species(S))) return rc;
+  if (ncell < 0) return fail(LB_EINVAL, "negative cell count");
+  if (ncell == 0) return LB_OK;
+  if (!cell_sizes || !r || !z || !w || !f || !df_r || !df_z || !coK || !coD || !B || !dB ||
+      !elem_out)
+    return fail(LB_EINVAL, "null argument");
+  const int n = 9 * ncell;
+  cudaStream_t st = ctx->stream;
+  const size_t nin = (size_t)(3 + 3 * S) * n;
+  if ((rc = ensure(ctx->in, nin * sizeof(double)))) return rc;
+  if ((rc = ensure(ctx->rec, (size_t)n * rec_stride(S) * sizeof(double)))) return rc;
+  if ((rc = ensure(ctx->out, (size_t)6 * S * n * sizeof(double)))) return rc;
+  if ((rc = ensure(ctx->elem, (size_t)81 * S * ncell * sizeof(double)))) return rc;
+  if ((rc = ensure(ctx->aux, (size_t)(2 * ncell + 81 + 162) * sizeof(double)))) return rc;
+  double* din = static_cast<double*>(ctx->in.p);
+  double *dr = din, *dz = dr + n, *dw = dz + n, *df = dw + n, *dfr = df + (size_t)S * n,
+         *dfz = dfr + (size_t)S * n;
+  double* dK = static_cast<double*>(ctx->out.p);
+  double* dD = dK + (size_t)2 * S * n;
+  double* dsz = static_cast<double*>(ctx->aux.p);
+  double* dB_ = dsz + 2 * ncell;
+  double* ddB = dB_ + 81;
+  double* delem = static_cast<double*>(ctx->elem.p);
+  const size_t bn = sizeof(double) * n, bsn = sizeof(double) * S * n;
+  LB_CUDA(cudaEventRecord(ctx->ev[0], st));
+  LB_CUDA(cudaMemcpyAsync(dr, r, bn, cudaMemcpyHostToDevice, st));
+  LB_CUDA(cudaMemcpyAsync(dz, z, bn, cudaMemcpyHostToDevice, st));
+  LB_CUDA(cudaMemcpyAsync(dw, w, bn, cudaMemcpyHostToDevice, st));
+  LB_CUDA(cudaMemcpyAsync(df, f, bsn, cudaMemcpyHostToDevice, st));
+  LB_CUDA(cudaMemcpyAsync(dfr, df_r, bsn, cudaMemcpyHostToDevice, st));
+  LB_CUDA(cudaMemcpyAsync(dfz, df_z, bsn, cudaMemcpyHostToDevice, st));
+  LB_CUDA(cudaMemcpyAsync(dsz, cell_sizes, sizeof(double) * 2 * ncell, cudaMemcpyHostToDevice, st));
+  LB_CUDA(cudaMemcpyAsync(dB_, B, sizeof(double) * 81, cudaMemcpyHostToDevice, st));
+  LB_CUDA(cudaMemcpyAsync(ddB, dB, sizeof(double) * 162, cudaMemcpyHostToDevice, st));
+  double* drec = static_cast<double*>(ctx->rec.p);
+  if ((rc = launch_pack(ctx, n, S, dr, dz, dw, df, dfr, dfz, drec, st))) return rc;
+  LB_CUDA(cudaEventRecord(ctx->ev[1], st));
+  if ((rc = lb_sweep_dev(ctx, n, dr, dz, n, S, drec, coK, coD, eps_d, dK, dD, st))) return rc;
+  LB_CUDA(cudaEventRecord(ctx->ev[2], st));
+  if ((rc = launch_elements(ctx, ncell, S, dsz, dw, dK, dD, dB_, ddB, delem, st))) return rc;
+  if (K_out) LB_CUDA(cudaMemcpyAsync(K_out, dK, sizeof(double) * 2 * S * n, cudaMemcpyDeviceToHost, st));
+  if (D_out) LB_CUDA(cudaMemcpyAsync(D_out, dD, sizeof(double) * 4 * S * n, cudaMemcpyDeviceToHost, st));
+  LB_CUDA(cudaMemcpyAsync(elem_out, delem, sizeof(double) * 81 * S * ncell, cudaMemcpyDeviceToHost, st));
+  LB_CUDA(cudaEventRecord(ctx->ev[3], st));
+  LB_CUDA(cudaStreamSynchronize(st));
+  if (phase_ms) {
+    float t = 0.f;
+    for (int p = 0; p < 3; ++p) {
+      LB_CUDA(cudaEventElapsedTime(&t, ctx->ev[p], ctx->ev[p + 1]));
+      phase_ms[p] = t;
+    }
+  }
+  return LB_OK;
+}
+
+int lb_tensor_pairs(lb_ctx* ctx, int npair, const double* r, const double* z, const double* rbar,
+                    const double* zbar, double* UK, double* UD) {
+  int rc = use_ctx(ctx);
+  if (rc) return rc;
+  if (npair < 0) return fail(LB_EINVAL, "negative pair count");
+  if (npair == 0) return LB_OK;
+  if (!r || !z || !rbar || !zbar || !UK || !UD) return fail(LB_EINVAL, "null argument");
+  cudaStream_t st = ctx->stream;
+  if ((rc = ensure(ctx->aux, sizeof(double) * 12 * (size_t)npair))) return rc;
+  double* d = static_cast<double*>(ctx->aux.p);
+  const size_t b = sizeof(double) * npair;
+  LB_CUDA(cudaMemcpyAsync(d, r, b, cudaMemcpyHostToDevice, st));
+  LB_CUDA(cudaMemcpyAsync(d + npair, z, b, cudaMemcpyHostToDevice, st));
+  LB_CUDA(cudaMemcpyAsync(d + 2 * (size_t)npair, rbar, b, cudaMemcpyHostToDevice, st));
+  LB_CUDA(cudaMemcpyAsync(d + 3 * (size_t)npair, zbar, b, cudaMemcpyHostToDevice, st));
+  double* dUK = d + 4 * (size_t)npair;
+  double* dUD = dUK + 4 * (size_t)npair;
+  lb_pairs_kernel<<<(npair + 127) / 128, 128, 0, st>>>(npair, d, d + npair, d + 2 * (size_t)npair,
+                                                       d + 3 * (size_t)npair, dUK, dUD);
+  LB_CUDA(cudaGetLastError());
+  LB_CUDA(cudaMemcpyAsync(UK, dUK, 4 * b, cudaMemcpyDeviceToHost, st));
+  LB_CUDA(cudaMemcpyAsync(UD, dUD, 4 * b, cudaMemcpyDeviceToHost, st));
+  LB_CUDA(cudaStreamSynchronize(st));
+  return LB_OK;
+}
+
+int lb_fp64_peak(lb_ctx* ctx, double* tflops, double* ms) {
+  int rc = use_ctx(ctx);
+  if (rc) return rc;
+  if (!tflops || !ms) return fail(LB_EINVAL, "null output");
+  cudaStream_t st = ctx->stream;
+  if ((rc = ensure(ctx->aux, 256 * sizeof(double)))) return rc;
+  int per_sm = 0;
+  LB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, lb_dfma_kernel, 256, 0));
+  const int blocks = ctx->num_sms * std::max(per_sm, 1) * 4;
+  cudaEvent_t e0, e1;
+  LB_CUDA(cudaEventCreate(&e0));
+  LB_CUDA(cudaEventCreate(&e1));
+  double best = 1e30;
+  for (int rep = 0; rep < 6; ++rep) {  // first rep is warm-up
+    LB_CUDA(cudaEventRecord(e0, st));
+    lb_dfma_kernel<<<blocks, 256, 0, st>>>(1.0 + rep, static_cast<double*>(ctx->aux.p));
+    LB_CUDA(cudaGetLastError());
+    LB_CUDA(cudaEventRecord(e1, st));
+    LB_CUDA(cudaEventSynchronize(e1));
+    float t = 0.f;
+    LB_CUDA(cudaEventElapsedTime(&t, e0, e1));
+    if (rep > 0) best = std::min(best, (double)t);
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  const double flops = 2.0 * kDfmaChains * (double)kDfmaIters * 256.0 * blocks;
+  *ms = best;
+  *tflops = flops / (best * 1e-3) / 1e12;
+  return LB_OK;
+}
+
+}  // extern "C"

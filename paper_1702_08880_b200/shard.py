@@ -1,0 +1,178 @@
+"""Multi-GPU layer: outer-point sharding + all-gather of the inner field state.
+
+One process per GPU (torch.distributed, backend "nccl"; "gloo" on CPU for
+the host-logic tests).  Each rank owns a contiguous, cell-aligned block of
+quadrature points (`synthetic.shard_bounds`): it samples / receives the
+fields of its own points, packs them into inner records on its device
+(`lb_pack_records_dev`), and one all-gather per operator evaluation
+replicates the packed records of every point to every rank -- the paper's
+per-point field state (w f, w grad f) plus coordinates, 10 doubles per point
+at S = 2, 5.2 MB at N = 2^16.  Each rank then sweeps its own outer points
+against all inner points (`lb_sweep_dev`).  No collective follows: the
+outputs K, D are per outer point.
+
+Because the sweep's inner chunking depends only on the global inner count
+and the record order is the global point order, every rank's K/D rows are
+bitwise identical to the single-GPU result for the same points.
+
+The reference has no distributed code; the paper ran
+redundant MPI replicas.  This layer is the B200 design
+from BASELINE.json's north_star.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+from typing import Callable
+
+import numpy as np
+
+from . import _lib
+from .kernel import coupling
+from .synthetic import shard_bounds
+
+__all__ = ["ShardPlan", "ShardedSweep"]
+
+
+@dataclass(frozen=True)
+class ShardPlan:
+    """Contiguous cell-aligned partition of n points over `world` ranks."""
+
+    n: int
+    world: int
+    align: int = 9
+
+    def bounds(self, rank: int):
+        return shard_bounds(self.n, self.world, rank, self.align)
+
+    @property
+    def counts(self):
+        return [hi - lo for lo, hi in (self.bounds(r) for r in range(self.world))]
+
+    @property
+    def max_count(self) -> int:
+        return max(self.counts) if self.world else 0
+
+    @property
+    def even(self) -> bool:
+        return len(set(self.counts)) == 1
+
+
+def _dist():
+    import torch.distributed as dist
+
+    return dist
+
+
+class ShardedSweep:
+    """Per-rank driver of one distributed D/K evaluation.
+
+    Parameters
+    ----------
+    n, S : global inner point count and species count
+    params : object with nu_hat / mass_ratio_o (CollisionParams-like)
+    eps_d : exclusion radius
+    device : torch device of this rank ("cuda:k", or "cpu" with injected
+             pack/sweep functions for the CPU tests)
+    align : shard alignment in points (9 = whole Q2 cells; 1 for point clouds)
+    pack_fn, sweep_fn : injectable for CPU testing; default to the CUDA
+             library (lb_pack_records_dev / lb_sweep_dev on torch tensors)
+    """
+
+    def __init__(self, n: int, S: int, params, eps_d: float, device, align: int = 9,
+                 group=None, pack_fn: Callable | None = None,
+                 sweep_fn: Callable | None = None):
+        import torch
+
+        dist = _dist()
+        self.group = group
+        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+        self.world = dist.get_world_size(group) if dist.is_initialized() else 1
+        self.n, self.S = int(n), int(S)
+        self.plan = ShardPlan(self.n, self.world, align)
+        self.lo, self.hi = self.plan.bounds(self.rank)
+        self.device = torch.device(device)
+        self.eps_d = float(eps_d)
+        self.coK, self.coD = coupling(params)
+        if pack_fn is None or sweep_fn is None:
+            lib = _lib.load()
+            self._lib = lib
+            self._ctx = _lib.context(self.device.index or 0)
+            self.RS = lib.lb_record_stride(self.S)
+            if self.RS < 0:
+                _lib.check(1)
+        else:
+            self.RS = ((4 + 3 * self.S) + 1) & ~1
+        self._pack = pack_fn or self._pack_cuda
+        self._sweep = sweep_fn or self._sweep_cuda
+        mc = self.plan.max_count
+        f64 = torch.float64
+        self.send = torch.zeros((mc, self.RS), dtype=f64, device=self.device)
+        self.recv = (self.send if self.world == 1 else
+                     torch.zeros((self.world * mc, self.RS), dtype=f64, device=self.device))
+        self.rec = (self.recv if self.plan.even else
+                    torch.zeros((self.n, self.RS), dtype=f64, device=self.device))
+        nl = self.hi - self.lo
+        self.K = torch.empty((nl, self.S, 2), dtype=f64, device=self.device)
+        self.D = torch.empty((nl, self.S, 2, 2), dtype=f64, device=self.device)
+        self.launches = 0
+
+    # ---------------------------------------------------------------- CUDA
+    def _stream(self):
+        import torch
+
+        return torch.cuda.current_stream(self.device).cuda_stream
+
+    def _pack_cuda(self, r, z, w, f, dfr, dfz, out):
+        n = r.shape[0]
+        _lib.check(self._lib.lb_pack_records_dev(
+            self._ctx.handle, n, self.S, r.data_ptr(), z.data_ptr(), w.data_ptr(), f.data_ptr(),
+            dfr.data_ptr(), dfz.data_ptr(), out.data_ptr(), self._stream()))
+        self.launches += self._lib.lb_last_launch_count(self._ctx.handle)
+
+    def _sweep_cuda(self, ro, zo, rec, K, D):
+        p = _lib.dptr
+        _lib.check(self._lib.lb_sweep_dev(
+            self._ctx.handle, ro.shape[0], ro.data_ptr(), zo.data_ptr(), self.n, self.S,
+            rec.data_ptr(), p(self.coK), p(self.coD), self.eps_d, K.data_ptr(), D.data_ptr(),
+            self._stream()))
+        self.launches += self._lib.lb_last_launch_count(self._ctx.handle)
+
+    # ---------------------------------------------------------------- steps
+    def pack_local(self, r, z, w, f, dfr, dfz):
+        """Pack this rank's points (device tensors: r,z,w (nl,), f.. (S,nl))."""
+        nl = self.hi - self.lo
+        if r.shape[0] != nl:
+            raise ValueError(f"rank {self.rank} owns {nl} points, got {r.shape[0]}")
+        self._pack(r, z, w, f, dfr, dfz, self.send[:nl])
+
+    def all_gather(self):
+        """Replicate every rank's packed records (one collective)."""
+        if self.world > 1:
+            _dist().all_gather_into_tensor(self.recv, self.send, group=self.group)
+        if not self.plan.even:  # compact the padded slots into global order
+            mc = self.plan.max_count
+            for k in range(self.world):
+                lo, hi = self.plan.bounds(k)
+                self.rec[lo:hi].copy_(self.recv[k * mc:k * mc + (hi - lo)])
+
+    def sweep_local(self, ro, zo):
+        """K, D for this rank's outer points (device tensors ro, zo)."""
+        self._sweep(ro, zo, self.rec, self.K, self.D)
+        return self.K, self.D
+
+    def step(self, r, z, w, f, dfr, dfz):
+        """One distributed evaluation from this rank's local fields; the local
+        points are also the outer points (assemble_collision's all-points
+        sweep, assembly.py:148)."""
+        self.pack_local(r, z, w, f, dfr, dfz)
+        self.all_gather()
+        return self.sweep_local(r, z)
+
+
+def local_fields(wl, lo: int, hi: int):
+    """Slice a host workload (QuadPointData-like) to points [lo, hi)."""
+    sl = slice(lo, hi)
+    return (np.ascontiguousarray(wl.r[sl]), np.ascontiguousarray(wl.z[sl]),
+            np.ascontiguousarray(wl.w[sl]), np.ascontiguousarray(wl.f[:, sl]),
+            np.ascontiguousarray(wl.df_r[:, sl]), np.ascontiguousarray(wl.df_z[:, sl]))

@@ -1,0 +1,116 @@
+"""Seeded synthetic workloads (BASELINE.json configs) for the bench and tests.
+
+The reference publishes no dataset; BASELINE.json config 5 ("pure kernel
+sweep") is defined by a recipe, restated here from SURVEY.md section 8(d):
+
+  N points uniform in the (v_r > 0, v_z) half-disk of radius R = 5:
+      rng = default_rng(1702 + log2 N); u1, u2 ~ U(0,1), c ~ U(0.5, 1.5)
+      rho = R sqrt(u1), theta = pi (u2 - 1/2), r = rho cos theta, z = rho sin theta
+  weights w = r c normalised to sum (2/3) R^3 (the r-weighted half-disk
+  area; the reference drops 2 pi, fem.py:8-10);
+  S = 2 species, electrons (m=1, q=-1, T=0.5, shift 0.5) and ions
+  (m=4, q=+1, T=0.25, shift 0): f = (pi s2)^-3/2 exp(-(r^2+(z-s)^2)/s2),
+  s2 = 2T/m, grad f analytic; nu_hat from the charges (all 1 here),
+  mass_ratio_o = (1, 1/4); eps_d = 1e-14 R.
+
+All arrays are float64 C-contiguous in the QuadPointData layout.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+
+import numpy as np
+
+R_DISK = 5.0
+
+
+@dataclass(frozen=True)
+class SpeciesSpec:
+    name: str
+    mass: float
+    charge: float
+    temperature: float
+    shift: float = 0.0
+
+    @property
+    def sigma2(self) -> float:
+        return 2.0 * self.temperature / self.mass
+
+
+CFG5_SPECIES = (
+    SpeciesSpec("e", 1.0, -1.0, 0.5, 0.5),
+    SpeciesSpec("i", 4.0, 1.0, 0.25, 0.0),
+)
+
+
+def collision_tables(species):
+    """nu_hat = (e_a e_b / e_0^2)^2 and m_o/m_a (physics.py:77-94 with a
+    shared Coulomb logarithm)."""
+    e = np.array([s.charge for s in species], dtype=float)
+    nu = (e[:, None] ** 2) * (e[None, :] ** 2)
+    nu = nu / nu[0, 0]
+    mro = np.array([1.0 / s.mass for s in species])
+    return nu, mro
+
+
+@dataclass
+class Workload:
+    N: int
+    r: np.ndarray
+    z: np.ndarray
+    w: np.ndarray
+    f: np.ndarray
+    df_r: np.ndarray
+    df_z: np.ndarray
+    nu_hat: np.ndarray
+    mass_ratio_o: np.ndarray
+    eps_d: float
+
+    @property
+    def S(self) -> int:
+        return self.f.shape[0]
+
+    def checksum(self) -> float:
+        return float(sum(np.abs(a).sum() for a in (self.r, self.z, self.w, self.f,
+                                                  self.df_r, self.df_z)))
+
+
+def cfg5(N: int, species=CFG5_SPECIES, seed: int | None = None) -> Workload:
+    """BASELINE config 5 input at N points (recipe above)."""
+    if seed is None:
+        seed = 1702 + int(round(math.log2(N)))
+    rng = np.random.default_rng(seed)
+    u1 = rng.random(N)
+    u2 = rng.random(N)
+    c = rng.uniform(0.5, 1.5, N)
+    rho = R_DISK * np.sqrt(u1)
+    theta = math.pi * (u2 - 0.5)
+    r = rho * np.cos(theta)
+    z = rho * np.sin(theta)
+    w = r * c
+    w = w * ((2.0 / 3.0) * R_DISK**3 / w.sum())
+    S = len(species)
+    f = np.empty((S, N))
+    dfr = np.empty((S, N))
+    dfz = np.empty((S, N))
+    for a, sp in enumerate(species):
+        s2 = sp.sigma2
+        fa = (math.pi * s2) ** -1.5 * np.exp(-(r * r + (z - sp.shift) ** 2) / s2)
+        f[a] = fa
+        dfr[a] = -2.0 * r * fa / s2
+        dfz[a] = -2.0 * (z - sp.shift) * fa / s2
+    nu, mro = collision_tables(species)
+    return Workload(N=N, r=np.ascontiguousarray(r), z=np.ascontiguousarray(z),
+                    w=np.ascontiguousarray(w), f=f, df_r=dfr, df_z=dfz,
+                    nu_hat=nu, mass_ratio_o=mro, eps_d=1e-14 * R_DISK)
+
+
+def shard_bounds(n: int, world: int, rank: int, align: int = 9):
+    """Contiguous [lo, hi) block of `n` points for `rank` of `world`, with
+    boundaries on multiples of `align` (whole Q2 cells) where possible."""
+    units = (n + align - 1) // align
+    lo_u = (units * rank) // world
+    hi_u = (units * (rank + 1)) // world
+    return min(lo_u * align, n), min(hi_u * align, n)

@@ -1,0 +1,303 @@
+"""Generate the golden fixtures by running the REFERENCE implementation.
+
+Run in the build container (where the read-only reference tree exists):
+
+    NUMBA_CACHE_DIR=/tmp/numba_cache PYTHONDONTWRITEBYTECODE=1 \
+        python tests/golden/make_golden.py
+
+It imports `axlandau` from /root/reference/pkg/src, evaluates the reference's
+own public functions (`axisym_tensor_pair`, `elliptic_KE`, `fused_sweep`
+with workers=1, `assemble_collision`, `assemble_naive`, `mass_matrix`,
+`linear_cn_step`, `moments`) on seeded inputs, and writes compressed .npz
+fixtures next to this script.  Nothing at test / bench time reads the
+reference tree; the tests compare the oracle and the CUDA path against these
+files.  Case recipes mirror the reference tests they are named after.
+"""
+
+from __future__ import annotations
+
+import math
+import os
+import sys
+from pathlib import Path
+
+import numpy as np
+
+REF_SRC = "/root/reference/pkg/src"
+HERE = Path(__file__).resolve().parent
+sys.path.insert(0, REF_SRC)
+sys.path.insert(0, str(HERE.parents[1]))
+os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/numba_cache")
+
+import axlandau as ax  # noqa: E402
+from axlandau import kernel as axk  # noqa: E402
+from axlandau.solver import linear_cn_step  # noqa: E402
+import scipy.sparse as sp  # noqa: E402
+import scipy.sparse.linalg as spla  # noqa: E402
+
+from paper_1702_08880_b200 import synthetic  # noqa: E402
+
+
+def csr_parts(prefix, m):
+    m = sp.csr_matrix(m)
+    m.sort_indices()
+    return {f"{prefix}_data": m.data, f"{prefix}_indices": m.indices.astype(np.int64),
+            f"{prefix}_indptr": m.indptr.astype(np.int64),
+            f"{prefix}_shape": np.array(m.shape, dtype=np.int64)}
+
+
+def mesh_parts(mesh, ref):
+    out = {"mesh_sizes": mesh.sizes, "mesh_cell_nodes": mesh.cell_nodes.astype(np.int64),
+           "mesh_n_nodes": np.int64(mesh.n_nodes), "mesh_L": np.float64(mesh.domain.L),
+           "mesh_free_r": mesh.nodes[mesh.free_nodes, 0],
+           "mesh_free_z": mesh.nodes[mesh.free_nodes, 1],
+           "ref_B": ref.B, "ref_dB": ref.dB}
+    out.update(csr_parts("mesh_P", mesh.prolongation))
+    return out
+
+
+def data_parts(data):
+    return {"r": data.r, "z": data.z, "w": data.w, "f": data.f, "df_r": data.df_r,
+            "df_z": data.df_z}
+
+
+def params_parts(params):
+    return {"nu_hat": params.nu_hat, "mass_ratio_o": params.mass_ratio_o}
+
+
+def blocks_parts(prefix, cm):
+    out = {}
+    for a, b in enumerate(cm.blocks):
+        out.update(csr_parts(f"{prefix}{a}", b))
+    out[f"{prefix}_count"] = np.int64(len(cm.blocks))
+    return out
+
+
+def moment_matrix(mesh, ref):
+    """Rows (n, z, v^2/2, v^2 z/2) x free dofs with 2 pi restored, so that
+    moments(species a) = mass_a-scaled rows @ coeffs[a] (physics.py:130-146)."""
+    eye = ax.StateVector(np.eye(mesh.n_free))
+    d = ax.sample_state(mesh, ref, eye)
+    wf = d.f * d.w[None, :] * (2.0 * np.pi)
+    v2 = d.r ** 2 + d.z ** 2
+    return np.stack([wf.sum(axis=1), wf @ d.z, 0.5 * (wf @ v2), 0.5 * (wf @ (v2 * d.z))])
+
+
+def save(name, **arrays):
+    path = HERE / f"{name}.npz"
+    np.savez_compressed(path, **arrays)
+    print(f"{path.name}: {path.stat().st_size / 1024:.0f} KiB")
+
+
+def case_pairs():
+    """Known-answer pairs for axisym_tensor_pair (test_kernel.py:94-146) and
+    elliptic_KE (test_kernel.py:30-46)."""
+    rng = np.random.default_rng(20260814)
+    rows = []
+    # generic, like test_pair_matches_azimuthal_quadrature / symmetries
+    n = 600
+    r = rng.uniform(0.01, 2.0, n); rb = rng.uniform(0.01, 2.0, n)
+    z = rng.uniform(-2.0, 2.0, n); zb = rng.uniform(-2.0, 2.0, n)
+    rows.append(np.stack([r, z, rb, zb], 1))
+    # straddling the series switch m = 0.01 (test_pair_series_branch_continuous)
+    rr = rng.uniform(0.02, 0.5, 100)
+    mt = 0.01 * (1.0 + rng.uniform(-0.05, 0.05, 100))
+    dz = np.sqrt(4 * rr * rr * (1 - mt) / mt)
+    rows.append(np.stack([rr, np.zeros(100), rr, dz], 1))
+    # on-axis inner / outer points (test_pair_on_axis_inner_point)
+    k = 50
+    rows.append(np.stack([rng.uniform(0.05, 2, k), rng.uniform(-2, 2, k), np.zeros(k),
+                          rng.uniform(-2, 2, k)], 1))
+    rows.append(np.stack([np.zeros(k), rng.uniform(-2, 2, k), rng.uniform(0.05, 2, k),
+                          rng.uniform(-2, 2, k)], 1))
+    # near-coincident pairs (x -> 0, K log-singular)
+    k = 100
+    r0 = rng.uniform(0.1, 2.0, k); z0 = rng.uniform(-2, 2, k)
+    eps = 10.0 ** rng.uniform(-7, -2, k)
+    ang = rng.uniform(0, 2 * np.pi, k)
+    rows.append(np.stack([r0, z0, r0 + eps * np.cos(ang), z0 + eps * np.sin(ang)], 1))
+    # far apart (small m via separation)
+    k = 100
+    rows.append(np.stack([rng.uniform(0.01, 0.3, k), rng.uniform(-5, -4, k),
+                          rng.uniform(0.01, 0.3, k), rng.uniform(4, 5, k)], 1))
+    P = np.concatenate(rows)
+    UK = np.empty((len(P), 2, 2)); UD = np.empty((len(P), 2, 2))
+    for t, (a, b, c, d) in enumerate(P):
+        pr = ax.axisym_tensor_pair(a, b, c, d)
+        UK[t] = pr.UK; UD[t] = pr.UD
+    ms = np.concatenate([np.linspace(0.0, 0.98, 400), 1.0 - np.geomspace(1e-12, 0.02, 100)])
+    K, E = ax.elliptic_KE(ms)
+    save("pairs", pairs=P, UK=UK, UD=UD, m=ms, K=K, E=E)
+
+
+def case_sweep_small():
+    """test_kernel.py:161-231: 2x4 mesh on DomainSpec() (L=2), e/i species."""
+    domain = ax.DomainSpec()
+    ref = ax.build_reference_element()
+    mesh = ax.cartesian_mesh(domain, 2, 4)
+    sp_ = [ax.Species("e", 1.0, -1.0, 0.2, shift=-0.5), ax.Species("i", 4.0, 1.0, 0.1)]
+    state = ax.maxwellian_init(mesh, ref, sp_, neutralize=True)
+    data = ax.sample_state(mesh, ref, state)
+    params = ax.collision_params(sp_)
+    K, D = ax.fused_sweep(data.r, data.z, data, params, workers=1)
+    # single species + proximity mask (test_kernel.py:223-231)
+    state1 = ax.maxwellian_init(mesh, ref, sp_[:1], neutralize=False)
+    data1 = ax.sample_state(mesh, ref, state1)
+    params1 = ax.collision_params(sp_[:1])
+    r0, z0 = data1.r[10] + 1e-9, data1.z[10]
+    Kw, Dw = ax.fused_sweep(np.array([r0]), np.array([z0]), data1, params1)
+    Km, Dm = ax.fused_sweep(np.array([r0]), np.array([z0]), data1, params1, eps_d=1e-6)
+    # scalar reduction pin for 4 outer points (test_kernel.py:173-194)
+    save("sweep_small", **data_parts(data), **params_parts(params), K=K, D=D,
+         r1=data1.r, z1=data1.z, w1=data1.w, f1=data1.f, df_r1=data1.df_r, df_z1=data1.df_z,
+         nu1=params1.nu_hat, mro1=params1.mass_ratio_o, prox_outer=np.array([r0, z0]),
+         K_with=Kw, D_with=Dw, K_masked=Km, D_masked=Dm)
+
+
+def case_cfg1():
+    """BASELINE config 1: L=5, 8x16 Q2 mesh (N=1152), drifting Maxwellian
+    electrons (n=1 -> 2x maxwellian_init, whose prefactor is 1/2), eps_d=5e-14;
+    full D/K, the assembled operator, and one CN step / composed BE step."""
+    domain = ax.DomainSpec(L=5.0)
+    ref = ax.build_reference_element()
+    mesh = ax.cartesian_mesh(domain, 8, 16)
+    sp_ = [ax.Species("e", 1.0, -1.0, 0.5, shift=0.5)]
+    state = ax.maxwellian_init(mesh, ref, sp_, neutralize=False)
+    state.coeffs *= 2.0
+    data = ax.sample_state(mesh, ref, state)
+    params = ax.collision_params(sp_)
+    eps_d = ax.assembly.default_eps_d(mesh)
+    K, D = ax.fused_sweep(data.r, data.z, data, params, eps_d=eps_d, workers=1)
+    cm = ax.assemble_collision(mesh, ref, data, params)
+    M = ax.mass_matrix(mesh, ref)
+    dt = 0.1
+    cn = linear_cn_step(M, cm, dt, state)
+    be = spla.splu((M - dt * cm.blocks[0]).tocsc()).solve(M @ state.coeffs[0])
+    moms0 = ax.moments(mesh, ref, state, sp_)
+    moms_cn = ax.moments(mesh, ref, cn, sp_)
+    save("cfg1", **mesh_parts(mesh, ref), **data_parts(data), **params_parts(params),
+         eps_d=np.float64(eps_d), K=K, D=D, **blocks_parts("C", cm), **csr_parts("M", M),
+         coeffs=state.coeffs, dt=np.float64(dt), cn_coeffs=cn.coeffs, be_coeffs=be[None, :],
+         Wm=moment_matrix(mesh, ref), masses=np.array([s.mass for s in sp_]),
+         moms0=np.stack([moms0.n, moms0.p_z, moms0.E, moms0.q_z]),
+         moms_cn=np.stack([moms_cn.n, moms_cn.p_z, moms_cn.E, moms_cn.q_z]))
+
+
+def case_hanging():
+    """test_assembly.py:43-51: hanging-node mesh, two species, random state;
+    fused and naive reference assemblies."""
+    domain = ax.DomainSpec()
+    ref = ax.build_reference_element()
+    mesh = ax.refine(ax.cartesian_mesh(domain, 2, 2), [3])
+    sp_ = [ax.Species("e", mass=1.0, charge=-1.0, temperature=0.2, shift=-1.0),
+           ax.Species("i", mass=4.0, charge=1.0, temperature=0.02)]
+    params = ax.collision_params(sp_)
+    rng = np.random.default_rng(20260814)
+    state = ax.StateVector(rng.standard_normal((2, mesh.n_free)))
+    data = ax.sample_state(mesh, ref, state)
+    fused = ax.assemble_collision(mesh, ref, data, params)
+    naive = ax.assemble_naive(mesh, ref, state, params)
+    K, D = ax.fused_sweep(data.r, data.z, data, params, eps_d=ax.assembly.default_eps_d(mesh))
+    save("hanging", **mesh_parts(mesh, ref), **data_parts(data), **params_parts(params),
+         coeffs=state.coeffs, K=K, D=D, **blocks_parts("C", fused),
+         **blocks_parts("N", naive))
+
+
+def case_cons():
+    """test_assembly.py:79-97: perturbed two-species Maxwellian on 8x16 (L=2)."""
+    domain = ax.DomainSpec()
+    ref = ax.build_reference_element()
+    mesh = ax.cartesian_mesh(domain, 8, 16)
+    sp_ = [ax.Species("e", mass=1.0, charge=-1.0, temperature=0.2, shift=-1.0),
+           ax.Species("i", mass=4.0, charge=1.0, temperature=0.02)]
+    r = mesh.nodes[mesh.free_nodes, 0]
+    z = mesh.nodes[mesh.free_nodes, 1]
+    state = ax.maxwellian_init(mesh, ref, sp_)
+    state.coeffs[:] *= 1.0 + 0.1 * np.sin(3 * z) * np.cos(2 * r)
+    data = ax.sample_state(mesh, ref, state)
+    params = ax.collision_params(sp_)
+    cm = ax.assemble_collision(mesh, ref, data, params)
+    save("cons", **mesh_parts(mesh, ref), **data_parts(data), **params_parts(params),
+         coeffs=state.coeffs, masses=np.array([s.mass for s in sp_]),
+         **blocks_parts("C", cm))
+
+
+def case_cfg2():
+    """BASELINE config 2 (reference-native reading): electrons + deuterium
+    (m=3670), T_e = 2 T_i, one shared 16x32 mesh on L=5, S=2."""
+    domain = ax.DomainSpec(L=5.0)
+    ref = ax.build_reference_element()
+    mesh = ax.cartesian_mesh(domain, 16, 32)
+    sp_ = [ax.Species("e", 1.0, -1.0, 0.5), ax.Species("D", 3670.0, 1.0, 0.25)]
+    state = ax.maxwellian_init(mesh, ref, sp_)
+    data = ax.sample_state(mesh, ref, state)
+    params = ax.collision_params(sp_)
+    eps_d = ax.assembly.default_eps_d(mesh)
+    K, D = ax.fused_sweep(data.r, data.z, data, params, eps_d=eps_d, workers=1)
+    cm = ax.assemble_collision(mesh, ref, data, params)
+    save("cfg2", **mesh_parts(mesh, ref), **data_parts(data), **params_parts(params),
+         eps_d=np.float64(eps_d), K=K, D=D, coeffs=state.coeffs,
+         masses=np.array([s.mass for s in sp_]), **blocks_parts("C", cm))
+
+
+def case_cfg4_species():
+    """BASELINE config 4 species set (e, D, C6+, W10+; n = 1/0.8/0.02/0.001,
+    T = 1/1/0.5/0.5; non-neutral, so the state is built directly with a
+    seeded 1% perturbation) on a 16x32 mesh, S = 4, 512 outer points."""
+    domain = ax.DomainSpec(L=5.0)
+    ref = ax.build_reference_element()
+    mesh = ax.cartesian_mesh(domain, 16, 32)
+    spec = [("e", 1.0, -1.0, 1.0, 1.0), ("D", 3670.0, 1.0, 0.8, 1.0),
+            ("C", 21900.0, 6.0, 0.02, 0.5), ("W", 335000.0, 10.0, 0.001, 0.5)]
+    sp_ = [ax.Species(nm, m, q, T) for nm, m, q, _, T in spec]
+    r = mesh.nodes[mesh.free_nodes, 0]
+    z = mesh.nodes[mesh.free_nodes, 1]
+    rng = np.random.default_rng(4)
+    coeffs = []
+    for (nm, m, q, dens, T), s in zip(spec, sp_):
+        s2 = s.sigma2
+        vals = dens * (math.pi * s2) ** -1.5 * np.exp(-(r * r + z * z) / s2)
+        coeffs.append(vals * (1.0 + 0.01 * rng.standard_normal(vals.shape)))
+    state = ax.StateVector(np.stack(coeffs))
+    data = ax.sample_state(mesh, ref, state)
+    params = ax.collision_params(sp_)
+    eps_d = ax.assembly.default_eps_d(mesh)
+    idx = np.unique(np.linspace(0, data.N - 1, 512).astype(np.int64))
+    K, D = ax.fused_sweep(data.r[idx], data.z[idx], data, params, eps_d=eps_d, workers=1)
+    save("cfg4s", **data_parts(data), **params_parts(params), eps_d=np.float64(eps_d),
+         idx=idx, K=K, D=D)
+
+
+def case_cfg5(N, n_sub=None):
+    """BASELINE config 5 recipe (paper_1702_08880_b200/synthetic.py).  Full
+    N^2 when n_sub is None, else n_sub evenly spaced outer points plus the 64
+    owners of the globally closest pairs."""
+    wl = synthetic.cfg5(N)
+    params = axk.CollisionParams(nu_hat=wl.nu_hat, mass_ratio_o=wl.mass_ratio_o)
+    data = ax.QuadPointData(N=N, r=wl.r, z=wl.z, w=wl.w, f=wl.f, df_r=wl.df_r, df_z=wl.df_z)
+    if n_sub is None:
+        idx = np.arange(N)
+    else:
+        from scipy.spatial import cKDTree
+        dist, _ = cKDTree(np.stack([wl.r, wl.z], 1)).query(np.stack([wl.r, wl.z], 1), k=2)
+        close = np.argsort(dist[:, 1])[:64]
+        idx = np.unique(np.concatenate([np.linspace(0, N - 1, n_sub).astype(np.int64), close]))
+    K, D = ax.fused_sweep(wl.r[idx], wl.z[idx], data, params, eps_d=wl.eps_d, workers=1)
+    extra = {} if n_sub is not None else {"r": wl.r, "z": wl.z}
+    save(f"cfg5_{N}", idx=idx, K=K, D=D, checksum=np.float64(wl.checksum()), **extra)
+
+
+def main():
+    which = set(sys.argv[1:])
+    cases = {"pairs": case_pairs, "sweep_small": case_sweep_small, "cfg1": case_cfg1,
+             "hanging": case_hanging, "cons": case_cons, "cfg2": case_cfg2,
+             "cfg4s": case_cfg4_species,
+             "cfg5_4096": lambda: case_cfg5(4096),
+             "cfg5_65536": lambda: case_cfg5(65536, n_sub=192)}
+    for name, fn in cases.items():
+        if not which or name in which:
+            fn()
+
+
+if __name__ == "__main__":
+    main()

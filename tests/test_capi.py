@@ -1,0 +1,85 @@
+"""The C-ABI library loads and exports every symbol include/*.h declares;
+without a GPU the product path fails loudly (no CPU fallback).  CPU only."""
+
+import re
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+from conftest import ROOT, cuda_ok
+
+
+def declared_symbols():
+    syms = set()
+    for h in (ROOT / "include").glob("*.h"):
+        text = re.sub(r"/\*.*?\*/", "", h.read_text(), flags=re.S)
+        syms |= set(re.findall(r"\b(lb_[a-z0-9_]+)\s*\(", text))
+    return syms
+
+
+def test_library_built_and_exports_header():
+    from paper_1702_08880_b200 import _lib
+
+    lib = _lib.load()
+    syms = declared_symbols()
+    assert len(syms) >= 15
+    for s in sorted(syms):
+        assert hasattr(lib, s), s
+    # and the Python binding types every declared symbol
+    assert syms == set(_lib.SIGNATURES)
+
+
+def test_pure_queries():
+    from paper_1702_08880_b200 import _lib
+
+    lib = _lib.load()
+    assert lib.lb_version() == 100
+    assert lib.lb_record_stride(1) == 8
+    assert lib.lb_record_stride(2) == 10
+    assert lib.lb_record_stride(4) == 16
+    assert lib.lb_record_stride(0) == -1 and lib.lb_record_stride(9) == -1
+    # inner chunking is a function of n only, whole 128-point tiles, <= 64 chunks
+    for n in (1, 72, 1152, 4096, 65536, 1 << 20):
+        jc = lib.lb_chunk_len(n)
+        assert jc % 128 == 0 and -(-n // jc) <= 64
+
+
+def test_symbols_listed_in_sass():
+    """The built .so carries sm_100a SASS (not just PTX)."""
+    so = ROOT / "paper_1702_08880_b200" / "liblandau_b200.so"
+    data = so.read_bytes()
+    assert b"sm_100a" in data or b"sm_100" in data
+
+
+@pytest.mark.skipif(cuda_ok(), reason="checks the no-GPU behaviour")
+def test_no_device_fails_loudly():
+    import paper_1702_08880_b200 as pkg
+    from paper_1702_08880_b200 import _lib
+
+    assert _lib.load().lb_device_count() == 0
+    with pytest.raises(RuntimeError, match="no CUDA device"):
+        _lib.Context(0)
+    data = pkg.QuadPointData(N=3, r=np.ones(3), z=np.arange(3.0), w=np.ones(3),
+                             f=np.ones((1, 3)), df_r=np.ones((1, 3)), df_z=np.ones((1, 3)))
+    params = pkg.CollisionParams(nu_hat=np.ones((1, 1)), mass_ratio_o=np.ones(1))
+    with pytest.raises(RuntimeError):
+        pkg.fused_sweep(data.r, data.z, data, params)
+
+
+def test_argument_errors_precede_device():
+    import paper_1702_08880_b200 as pkg
+
+    data = pkg.QuadPointData(N=3, r=np.ones(3), z=np.arange(3.0), w=np.ones(3),
+                             f=np.ones((1, 3)), df_r=np.ones((1, 3)), df_z=np.ones((1, 3)))
+    params2 = pkg.CollisionParams(nu_hat=np.ones((2, 2)), mass_ratio_o=np.ones(2))
+    with pytest.raises(ValueError, match="species count mismatch"):
+        pkg.fused_sweep(data.r, data.z, data, params2)
+    with pytest.raises(ValueError):
+        pkg.CollisionParams(nu_hat=np.ones((2, 3)), mass_ratio_o=np.ones(2))
+    with pytest.raises(ValueError):
+        pkg.CollisionParams(nu_hat=-np.ones((1, 1)), mass_ratio_o=np.ones(1))
+    with pytest.raises(ValueError):
+        pkg.axisym_tensor_pair(-0.1, 0.0, 0.5, 0.0)
+    with pytest.raises(ValueError):
+        pkg.axisym_tensor_pair(0.5, 0.1, 0.5, 0.1)

@@ -1,0 +1,207 @@
+"""Parity of the sm_100a pair sweep (through the C ABI) with the reference
+goldens and the CPU oracle.  Bar: per species / component scaled error
+max|dX|/max|X_ref| <= 1e-10 (BASELINE.json north_star); measured values are
+printed (-s) and sit near 1e-14."""
+
+import numpy as np
+import pytest
+
+from conftest import data_from, golden, params_from, scaled, worst_component
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-10
+
+
+def _rel_pairs(UK, UD, UKr, UDr):
+    s = np.maximum(np.abs(UKr).reshape(len(UKr), -1).max(1), np.abs(UDr).reshape(len(UDr), -1).max(1))
+    e = np.maximum(np.abs(UK - UKr).reshape(len(UK), -1).max(1), np.abs(UD - UDr).reshape(len(UD), -1).max(1))
+    return e / s
+
+
+def test_tensor_pairs_match_reference(gpu):
+    g = golden("pairs")
+    P = g["pairs"]
+    UK, UD = gpu.axisym_tensor_pairs(P[:, 0], P[:, 1], P[:, 2], P[:, 3])
+    err = _rel_pairs(UK, UD, g["UK"], g["UD"])
+    # well-separated pairs agree to rounding; the near-coincident band
+    # (|d| down to 1e-7) has UD_xx cancellation ~ulp * (r/|d|)^2
+    d = np.hypot(P[:, 0] - P[:, 2], P[:, 1] - P[:, 3])
+    sep = d > 1e-2
+    print("pairs worst (separated)", err[sep].max(), "worst (all)", err.max())
+    assert err[sep].max() < 1e-13
+    assert np.all(err <= 1e-15 * (1.0 + (P[:, 0] / d) ** 2) * 50)
+
+
+def test_tensor_pair_structure(gpu):
+    g = golden("pairs")
+    P = g["pairs"][:600]
+    UK, UD = gpu.axisym_tensor_pairs(P[:, 0], P[:, 1], P[:, 2], P[:, 3])
+    assert np.array_equal(UD[:, 0, 1], UD[:, 1, 0])            # UD symmetric
+    assert np.array_equal(UK[:, :, 1], UD[:, :, 1])            # UK z-column == UD z-column
+    t = gpu.axisym_tensor_pair(0.5, 0.3, 0.0, -0.2)            # on-axis inner point
+    assert np.all(np.isfinite(t.UK)) and np.all(np.isfinite(t.UD))
+
+
+def test_sweep_small_all_outer(gpu):
+    g = golden("sweep_small")
+    K, D = gpu.fused_sweep(g["r"], g["z"], data_from(g), params_from(g))
+    err = worst_component(K, D, g["K"], g["D"])
+    print("sweep_small", err)
+    assert err < TOL
+    assert np.array_equal(D[..., 0, 1], D[..., 1, 0])
+
+
+def test_proximity_mask(gpu):
+    g = golden("sweep_small")
+    data = data_from(g, "1")
+    params = params_from(g, "nu1", "mro1")
+    ro, zo = np.array([g["prox_outer"][0]]), np.array([g["prox_outer"][1]])
+    Kw, Dw = gpu.fused_sweep(ro, zo, data, params)
+    Km, Dm = gpu.fused_sweep(ro, zo, data, params, eps_d=1e-6)
+    assert scaled(Km, g["K_masked"]) < TOL and scaled(Dm, g["D_masked"]) < TOL
+    assert scaled(Kw, g["K_with"]) < TOL
+    assert np.all(np.isfinite(Dw)) and not np.allclose(Kw, Km, rtol=1e-8)
+
+
+def test_fused_inner_loop_single_point(gpu):
+    g = golden("sweep_small")
+    data, params = data_from(g, "1"), params_from(g, "nu1", "mro1")
+    acc = gpu.fused_inner_loop((data.r[5], data.z[5], data.w[5]), data, params)
+    K, D = gpu.fused_sweep(data.r[5:6], data.z[5:6], data, params)
+    assert np.array_equal(acc.K, K[0]) and np.array_equal(acc.D, D[0])
+
+
+@pytest.mark.parametrize("case", ["cfg1", "cfg2", "hanging"])
+def test_mesh_sweeps(gpu, case):
+    g = golden(case)
+    eps = float(g["eps_d"]) if "eps_d" in g else 1e-14 * float(g["mesh_L"])
+    K, D = gpu.fused_sweep(g["r"], g["z"], data_from(g), params_from(g), eps_d=eps)
+    err = worst_component(K, D, g["K"], g["D"])
+    print(case, err)
+    assert err < TOL
+
+
+def test_four_species(gpu):
+    g = golden("cfg4s")
+    idx = g["idx"]
+    K, D = gpu.fused_sweep(g["r"][idx], g["z"][idx], data_from(g), params_from(g),
+                           eps_d=float(g["eps_d"]))
+    err = worst_component(K, D, g["K"], g["D"])
+    print("cfg4 species S=4", err)
+    assert err < TOL
+
+
+def _cfg5(N):
+    from paper_1702_08880_b200 import synthetic
+
+    wl = synthetic.cfg5(N)
+    data = pytest.importorskip("paper_1702_08880_b200").QuadPointData(
+        N=N, r=wl.r, z=wl.z, w=wl.w, f=wl.f, df_r=wl.df_r, df_z=wl.df_z)
+    params = pytest.importorskip("paper_1702_08880_b200").CollisionParams(
+        nu_hat=wl.nu_hat, mass_ratio_o=wl.mass_ratio_o)
+    return wl, data, params
+
+
+def test_cfg5_4096_full(gpu):
+    g = golden("cfg5_4096")
+    wl, data, params = _cfg5(4096)
+    assert wl.checksum() == float(g["checksum"])
+    K, D = gpu.fused_sweep(wl.r, wl.z, data, params, eps_d=wl.eps_d)
+    err = worst_component(K, D, g["K"], g["D"])
+    print("cfg5 N=4096", err)
+    assert err < TOL
+
+
+def test_cfg5_headline_subset_with_closest_pairs(gpu):
+    """N = 2^16: evenly spaced outer points + the 64 closest-pair owners."""
+    g = golden("cfg5_65536")
+    wl, data, params = _cfg5(65536)
+    assert wl.checksum() == float(g["checksum"])
+    idx = g["idx"]
+    K, D = gpu.fused_sweep(wl.r[idx], wl.z[idx], data, params, eps_d=wl.eps_d)
+    err = worst_component(K, D, g["K"], g["D"])
+    print("cfg5 N=65536 subset", err)
+    assert err < TOL
+
+
+def test_cfg5_headline_full_properties(gpu):
+    """Full N = 2^16 evaluation: outer-split invariance (bitwise), run-to-run
+    determinism (bitwise), finiteness -- size-independent properties."""
+    wl, data, params = _cfg5(65536)
+    K, D = gpu.fused_sweep(wl.r, wl.z, data, params, eps_d=wl.eps_d)
+    assert np.all(np.isfinite(K)) and np.all(np.isfinite(D))
+    K2, D2 = gpu.fused_sweep(wl.r, wl.z, data, params, eps_d=wl.eps_d)
+    assert np.array_equal(K, K2) and np.array_equal(D, D2)
+    for lo, hi in ((0, 8192), (8192 * 3 + 17, 8192 * 5), (65536 - 129, 65536)):
+        Ks, Ds = gpu.fused_sweep(wl.r[lo:hi], wl.z[lo:hi], data, params, eps_d=wl.eps_d)
+        assert np.array_equal(Ks, K[lo:hi]) and np.array_equal(Ds, D[lo:hi])
+
+
+@pytest.mark.parametrize("S", [1, 3, 5, 8])
+def test_species_counts_vs_oracle(gpu, oracle, S):
+    rng = np.random.default_rng(100 + S)
+    n = 1000 + 37 * S  # ragged (not a multiple of the 128-point tile)
+    r = rng.uniform(0.0, 3.0, n)
+    z = rng.uniform(-3.0, 3.0, n)
+    w = rng.uniform(0.1, 1.0, n)
+    f, dfr, dfz = (rng.standard_normal((S, n)) for _ in range(3))
+    nu = rng.uniform(0.5, 2.0, (S, S))
+    nu = nu + nu.T
+    mro = rng.uniform(0.01, 1.0, S)
+    import paper_1702_08880_b200 as pkg
+
+    data = pkg.QuadPointData(N=n, r=r, z=z, w=w, f=f, df_r=dfr, df_z=dfz)
+    params = pkg.CollisionParams(nu_hat=nu, mass_ratio_o=mro)
+    ro, zo = r[::7], z[::7]
+    K, D = gpu.fused_sweep(ro, zo, data, params, eps_d=1e-13)
+    Kr, Dr = oracle.fused_sweep(ro, zo, r, z, w, f, dfr, dfz, nu, mro, eps_d=1e-13)
+    err = worst_component(K, D, Kr, Dr)
+    print(f"S={S} random", err)
+    assert err < TOL
+
+
+def test_edge_sizes(gpu, oracle):
+    import paper_1702_08880_b200 as pkg
+
+    g = golden("cfg1")
+    data, params = data_from(g), params_from(g)
+    # empty outer set
+    K, D = gpu.fused_sweep(np.zeros(0), np.zeros(0), data, params)
+    assert K.shape == (0, 1, 2) and D.shape == (0, 1, 2, 2)
+    # one outer point, 129 outer points (tile + 1), arbitrary off-grid points
+    for m in (1, 129):
+        ro = np.linspace(0.01, 4.9, m)
+        zo = np.linspace(-4.9, 4.9, m)
+        K, D = gpu.fused_sweep(ro, zo, data, params, eps_d=5e-14)
+        Kr, Dr = oracle.fused_sweep(ro, zo, g["r"], g["z"], g["w"], g["f"], g["df_r"],
+                                    g["df_z"], g["nu_hat"], g["mass_ratio_o"], eps_d=5e-14)
+        assert worst_component(K, D, Kr, Dr) < TOL
+    # empty inner set: all sums zero
+    empty = pkg.QuadPointData(N=0, r=np.zeros(0), z=np.zeros(0), w=np.zeros(0),
+                              f=np.zeros((1, 0)), df_r=np.zeros((1, 0)), df_z=np.zeros((1, 0)))
+    K, D = gpu.fused_sweep(np.ones(3), np.zeros(3), empty, params)
+    assert not K.any() and not D.any()
+    # outer point on the axis (r = 0) and coincident with an inner point
+    ro = np.array([0.0, g["r"][3]])
+    zo = np.array([0.7, g["z"][3]])
+    K, D = gpu.fused_sweep(ro, zo, data, params, eps_d=5e-14)
+    Kr, Dr = oracle.fused_sweep(ro, zo, g["r"], g["z"], g["w"], g["f"], g["df_r"], g["df_z"],
+                                g["nu_hat"], g["mass_ratio_o"], eps_d=5e-14)
+    assert np.all(np.isfinite(K)) and worst_component(K, D, Kr, Dr) < TOL
+
+
+def test_workers_and_block_size_do_not_change_results(gpu):
+    # test_kernel.py:197-212 asserts bitwise invariance to both
+    g = golden("sweep_small")
+    data, params = data_from(g), params_from(g)
+    base = gpu.fused_sweep(g["r"], g["z"], data, params)
+    for kw in ({"workers": 4}, {"block_size": 16}, {"block_size": 1000}):
+        other = gpu.fused_sweep(g["r"], g["z"], data, params, **kw)
+        assert np.array_equal(base[0], other[0]) and np.array_equal(base[1], other[1])
+
+
+def test_species_mismatch_raises(gpu):
+    g = golden("sweep_small")
+    with pytest.raises(ValueError):
+        gpu.fused_sweep(g["r"], g["z"], data_from(g), params_from(g, "nu1", "mro1"))

@@ -1,0 +1,104 @@
+"""Host-side logic of the drop-in mirror (CPU only)."""
+
+import numpy as np
+import pytest
+from hypothesis import given, settings
+from hypothesis import strategies as st
+
+import paper_1702_08880_b200 as pkg
+from paper_1702_08880_b200 import synthetic
+from paper_1702_08880_b200.shard import ShardPlan
+
+
+def test_flop_count_pinned_values():
+    # test_kernel.py:239-244
+    assert pkg.flop_count(1, 1, 1) == 185
+    assert pkg.flop_count(1, 2, 1) == 245
+    assert pkg.flop_count(10, 1, 3) == 3 * 10 * 185
+    assert pkg.flop_count(5, 2, 2, overhead_per_outer=7) == 2 * (5 * 245 + 7)
+    assert pkg.flop_count(0, 3, 4) == 0
+    with pytest.raises(ValueError):
+        pkg.flop_count(-1, 1, 1)
+
+
+@settings(max_examples=50, deadline=None)
+@given(st.integers(0, 10**6), st.integers(0, 8), st.integers(0, 100))
+def test_flop_count_linear_in_outer(N, S, outer):
+    assert pkg.flop_count(N, S, outer) == outer * pkg.flop_count(N, S, 1)
+
+
+def test_coupling_matches_reference_expression():
+    from conftest import golden
+
+    g = golden("cfg4s")
+    params = pkg.CollisionParams(nu_hat=g["nu_hat"], mass_ratio_o=g["mass_ratio_o"])
+    coK, coD = pkg.coupling(params)
+    nu, mro = g["nu_hat"], g["mass_ratio_o"]
+    np.testing.assert_array_equal(coK, nu * mro[:, None] * mro[None, :])
+    np.testing.assert_array_equal(coD, -nu * (mro**2)[:, None])
+
+
+def test_params_properties():
+    p = pkg.CollisionParams(nu_hat=[[1.0, 2.0], [2.0, 4.0]], mass_ratio_o=[1.0, 0.5])
+    assert p.n_species == 2 and p.nu_hat.flags.c_contiguous
+
+
+@settings(max_examples=100, deadline=None)
+@given(st.integers(0, 100000), st.integers(1, 8), st.sampled_from([1, 9]))
+def test_shard_plan_partitions(n, world, align):
+    plan = ShardPlan(n, world, align)
+    cover = []
+    for r in range(world):
+        lo, hi = plan.bounds(r)
+        assert 0 <= lo <= hi <= n
+        if align > 1 and hi < n:
+            assert hi % align == 0
+        cover.extend(range(lo, hi))
+    assert cover == list(range(n))
+    assert max(plan.counts) - min(plan.counts) <= align
+
+
+def test_cfg5_recipe_properties():
+    wl = synthetic.cfg5(4096)
+    assert wl.S == 2 and wl.r.shape == (4096,) and wl.f.shape == (2, 4096)
+    assert np.all(wl.r >= 0) and np.all(wl.r ** 2 + wl.z ** 2 <= 25.0 + 1e-12)
+    assert np.isclose(wl.w.sum(), (2.0 / 3.0) * 125.0, rtol=1e-13)
+    np.testing.assert_array_equal(wl.nu_hat, np.ones((2, 2)))
+    np.testing.assert_array_equal(wl.mass_ratio_o, [1.0, 0.25])
+    # deterministic per seed
+    assert synthetic.cfg5(4096).checksum() == wl.checksum()
+
+
+def test_install_patches_every_importer():
+    """install() routes an axlandau-shaped package through the B200 names."""
+    import sys
+    import types
+
+    root = types.ModuleType("fakeax")
+    root.__path__ = []
+    mods = {}
+    for sub in ("kernel", "assembly", "solver", "cli"):
+        m = types.ModuleType(f"fakeax.{sub}")
+        mods[sub] = m
+        sys.modules[f"fakeax.{sub}"] = m
+    sys.modules["fakeax"] = root
+    try:
+        sentinel = object()
+        mods["kernel"].fused_sweep = sentinel
+        mods["kernel"].fused_inner_loop = sentinel
+        mods["assembly"].fused_sweep = sentinel
+        mods["assembly"].assemble_collision = sentinel
+        mods["solver"].assemble_collision = sentinel
+        mods["cli"].assemble_collision = sentinel
+        mods["cli"].fused_sweep = sentinel
+        root.fused_sweep = sentinel
+        saved = pkg.install(root)
+        assert mods["solver"].assemble_collision is pkg.assemble_collision
+        assert mods["cli"].fused_sweep is pkg.fused_sweep
+        assert root.fused_sweep is pkg.fused_sweep
+        pkg.uninstall(root, saved)
+        assert mods["solver"].assemble_collision is sentinel
+        assert root.fused_sweep is sentinel
+    finally:
+        for k in [k for k in sys.modules if k == "fakeax" or k.startswith("fakeax.")]:
+            del sys.modules[k]
