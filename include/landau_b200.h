@@ -12,7 +12,8 @@
  *    take caller-owned HOST pointers, copy in, run, copy out and block until
  *    the outputs are written (the reference's synchronous semantics).
  *    `_dev` entry points take DEVICE pointers and a cudaStream_t (passed as
- *    void*; NULL = the context's own stream) and are asynchronous.
+ *    void*; NULL = the legacy default stream, as in the CUDA runtime) and
+ *    are asynchronous with respect to the host.
  *  - Return value: LB_OK (0) or an LB_E* code; `lb_last_error()` returns a
  *    thread-local message for the most recent failure.  LB_EINVAL maps to
  *    Python ValueError, everything else to RuntimeError.  There is no CPU

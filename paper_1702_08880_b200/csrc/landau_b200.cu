@@ -609,7 +609,7 @@ int lb_pack_records_dev(lb_ctx* ctx, int n, int S, const double* r, const double
   if (rc) return rc;
   if ((rc = check_species(S))) return rc;
   if (n < 0) return fail(LB_EINVAL, "negative point count");
-  cudaStream_t st = stream ? (cudaStream_t)stream : ctx->stream;
+  cudaStream_t st = (cudaStream_t)stream;  // NULL = legacy default stream
   rc = launch_pack(ctx, n, S, r, z, w, f, df_r, df_z, rec, st);
   ctx->last_launches = n > 0 ? 1 : 0;
   return rc;
@@ -623,7 +623,7 @@ int lb_sweep_dev(lb_ctx* ctx, int nout, const double* outer_r, const double* out
   if ((rc = check_species(S))) return rc;
   if (nout < 0 || n < 0) return fail(LB_EINVAL, "negative point count");
   if (!coK || !coD) return fail(LB_EINVAL, "null coupling table");
-  cudaStream_t st = stream ? (cudaStream_t)stream : ctx->stream;
+  cudaStream_t st = (cudaStream_t)stream;  // NULL = legacy default stream
   ctx->last_launches = 0;
   if (nout == 0) return LB_OK;
   if (n == 0) {  // empty inner set: all sums are +0
@@ -644,7 +644,7 @@ int lb_elements_dev(lb_ctx* ctx, int ncell, int S, const double* cell_sizes, con
   if (rc) return rc;
   if ((rc = check_species(S))) return rc;
   if (ncell < 0) return fail(LB_EINVAL, "negative cell count");
-  cudaStream_t st = stream ? (cudaStream_t)stream : ctx->stream;
+  cudaStream_t st = (cudaStream_t)stream;  // NULL = legacy default stream
   rc = launch_elements(ctx, ncell, S, cell_sizes, w, K, D, B, dB, elem_out, st);
   ctx->last_launches = ncell > 0 ? 1 : 0;
   return rc;

