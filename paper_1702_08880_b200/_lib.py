@@ -9,6 +9,7 @@ library or the GPU is missing, every compute call fails loudly.
 from __future__ import annotations
 
 import ctypes as C
+import os
 import threading
 from pathlib import Path
 
@@ -56,7 +57,8 @@ def load(path: Path | None = None):
     with _lib_lock:
         if _lib is not None:
             return _lib
-        p = Path(path) if path else LIB_PATH
+        # LB_LIB overrides the in-tree library (used to A/B kernel variants)
+        p = Path(path) if path else Path(os.environ.get("LB_LIB", LIB_PATH))
         if not p.exists():
             raise RuntimeError(
                 f"{p} not built: run `python -m paper_1702_08880_b200.build` "

@@ -44,15 +44,20 @@ def needs_build() -> bool:
     return any(p.stat().st_mtime > t for p in DEPS)
 
 
-def build(force: bool = False, verbose: bool = False) -> Path:
-    if not force and not needs_build():
+def build(force: bool = False, verbose: bool = False, out: Path | None = None,
+          defines: dict | None = None) -> Path:
+    """Build the library (or, with `out`/`defines`, a tuning variant of it)."""
+    target = Path(out) if out else LIB
+    if out is None and not force and not needs_build():
         return LIB
-    cmd = [nvcc(), *NVCC_FLAGS, "-o", str(LIB), *map(str, SOURCES)]
+    extra = [f"-D{k}={v}" for k, v in (defines or {}).items()]
+    target.parent.mkdir(parents=True, exist_ok=True)
+    cmd = [nvcc(), *NVCC_FLAGS, *extra, "-o", str(target), *map(str, SOURCES)]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
         print(" ".join(cmd), file=sys.stderr)
     subprocess.run(cmd, check=True)
-    return LIB
+    return target
 
 
 if __name__ == "__main__":

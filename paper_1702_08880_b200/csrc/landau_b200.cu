@@ -21,6 +21,7 @@
 // inner points are summed in index order, chunks are summed in index order;
 // no atomics.  Results are bitwise reproducible and independent of how outer
 // points are split across calls or GPUs.
+#include <cub/device/device_radix_sort.cuh>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -36,7 +37,14 @@
 namespace lb {
 
 constexpr int kTI = 128;        // outer points per CTA (one per thread)
-constexpr int kMinBlocks = 4;   // CTAs per SM the register budget targets
+#ifndef LB_MINB
+#define LB_MINB 4
+#endif
+#ifndef LB_UNROLL
+#define LB_UNROLL 1
+#endif
+constexpr int kMinBlocks = LB_MINB;  // CTAs per SM the register budget targets
+constexpr int kUnroll = LB_UNROLL;   // inner pairs interleaved per loop trip
 constexpr int kMaxChunks = 64;  // inner chunks per sweep (sets the JC length)
 constexpr int kChunkAlign = 128;
 constexpr size_t kPartialBudget = size_t(2) << 30;  // bytes of chunk partials per pass
@@ -117,38 +125,64 @@ struct SweepArgs {
   long long gthr;     // mask threshold on bits(d^2)
 };
 
+constexpr int kStages = 4;     // shared-memory ring depth
+constexpr int kLookahead = 2;  // tiles in flight ahead of the consumer
+constexpr int kWarps = kTI / 32;
+
+template <int S>
+constexpr size_t sweep_smem_bytes() {
+  return size_t(kStages) * TileCfg<S>::TJ * TileCfg<S>::RS * sizeof(double) +
+         size_t(2 << LB_LOGT_BITS) * sizeof(double);
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+// Persistent CTAs walk work items (128 outer points x one inner chunk of jc
+// points).  Inner records flow through a kStages ring: thread 0 issues the
+// 1-D TMA bulk copy of tile k+kLookahead once every warp has released tile
+// k+kLookahead-kStages (per-stage "empty" mbarriers, one arrival per warp),
+// so warps drift independently instead of meeting at a CTA barrier per tile.
 template <int S>
 __global__ void __launch_bounds__(kTI, kMinBlocks) lb_sweep_kernel(const SweepArgs a) {
   constexpr int RS = TileCfg<S>::RS;
   constexpr int TJ = TileCfg<S>::TJ;
   extern __shared__ __align__(128) double lb_smem[];
-  __shared__ __align__(8) uint64_t bar[2];
+  __shared__ __align__(8) uint64_t full[kStages], empty[kStages];
+  double2* logt = reinterpret_cast<double2*>(lb_smem + kStages * TJ * RS);
 
   const int tid = threadIdx.x;
+  const int lane = tid & 31;
   const int nib = a.nout_pad / kTI;
   const long long nitems = (long long)nib * a.nchunk;
 
+  for (int t = tid; t < (2 << LB_LOGT_BITS); t += kTI) lb_smem[kStages * TJ * RS + t] = c_logt[t];
   if (tid == 0) {
-    mbar_init(&bar[0], 1);
-    mbar_init(&bar[1], 1);
+#pragma unroll
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kWarps);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
 
-  // producer cursor (meaningful on thread 0 only): next (item, tile) to load
+  // producer cursor (thread 0 only): next (item, tile) to load, flat tile index
   long long p_item = blockIdx.x;
   int p_tile = 0;
   uint32_t p_k = 0;
   auto issue_next = [&]() {
     if (p_item >= nitems) return;
+    const uint32_t s = p_k % kStages;
+    if (p_k >= kStages) mbar_wait(&empty[s], ((p_k / kStages) - 1) & 1);
     const int c = (int)(p_item / nib);
     const int j0 = c * a.jc + p_tile * TJ;
     const int jend = min(a.n, (c + 1) * a.jc);
     const int cnt = min(TJ, jend - j0);
     const uint32_t bytes = (uint32_t)cnt * RS * sizeof(double);
-    uint64_t* b = &bar[p_k & 1];
-    mbar_expect_tx(b, bytes);
-    bulk_g2s(lb_smem + (p_k & 1) * (TJ * RS), a.rec + (size_t)j0 * RS, bytes, b);
+    mbar_expect_tx(&full[s], bytes);
+    bulk_g2s(lb_smem + s * (TJ * RS), a.rec + (size_t)j0 * RS, bytes, &full[s]);
     ++p_k;
     if (j0 + TJ >= jend) {
       p_tile = 0;
@@ -157,9 +191,10 @@ __global__ void __launch_bounds__(kTI, kMinBlocks) lb_sweep_kernel(const SweepAr
       ++p_tile;
     }
   };
-  if (tid == 0) issue_next();
+  if (tid == 0)
+    for (int q = 0; q < kLookahead; ++q) issue_next();
 
-  uint32_t k = 0;  // consumer tile counter (same sequence as the producer)
+  uint32_t k = 0;  // consumer flat tile index (same sequence as the producer)
   for (long long item = blockIdx.x; item < nitems; item += gridDim.x) {
     const int ib = (int)(item % nib);
     const int c = (int)(item / nib);
@@ -176,15 +211,16 @@ __global__ void __launch_bounds__(kTI, kMinBlocks) lb_sweep_kernel(const SweepAr
     const int jend = min(a.n, jbeg + a.jc);
     for (int j0 = jbeg; j0 < jend; j0 += TJ, ++k) {
       if (tid == 0) issue_next();
-      mbar_wait(&bar[k & 1], (k >> 1) & 1);
-      const double* tile = lb_smem + (k & 1) * (TJ * RS);
+      const uint32_t s = k % kStages;
+      mbar_wait(&full[s], (k / kStages) & 1);
+      const double* tile = lb_smem + s * (TJ * RS);
       const int cnt = min(TJ, jend - j0);
-#pragma unroll 1
+#pragma unroll kUnroll
       for (int jj = 0; jj < cnt; ++jj) {
         const double* rp = tile + jj * RS;
         const double2 rz = *reinterpret_cast<const double2*>(rp);
         const double2 aux = *reinterpret_cast<const double2*>(rp + 2);
-        const T5 t = pair_tensor(o, rz.x, rz.y, aux.x, aux.y, a.gthr);
+        const T5 t = pair_tensor(o, rz.x, rz.y, aux.x, aux.y, a.gthr, logt);
 #pragma unroll
         for (int b = 0; b < S; ++b) {
           const double gr = rp[4 + 3 * b], gz = rp[5 + 3 * b], fw = rp[6 + 3 * b];
@@ -196,7 +232,8 @@ __global__ void __launch_bounds__(kTI, kMinBlocks) lb_sweep_kernel(const SweepAr
           acc[b][4] = fma(fw, t.zz, acc[b][4]);
         }
       }
-      __syncthreads();  // stage (k & 1) free for the producer
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);  // this warp is done with stage s
     }
     if (i < a.nout) {
       double* dst = a.partial + (size_t)c * (5 * S) * a.nout_pad + i;
@@ -211,10 +248,11 @@ __global__ void __launch_bounds__(kTI, kMinBlocks) lb_sweep_kernel(const SweepAr
 // ------------------------------------------------------------------ K1b combine
 template <int S>
 __global__ void lb_combine_kernel(const double* __restrict__ partial, int nchunk, int nout,
-                                  int nout_pad, const Coupling cp, double* __restrict__ K,
-                                  double* __restrict__ D) {
+                                  int nout_pad, const Coupling cp, const int* __restrict__ perm,
+                                  double* __restrict__ K, double* __restrict__ D) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= nout) return;
+  const int io = perm ? perm[i] : i;  // output row of this (possibly reordered) outer point
   double A[S][5];
 #pragma unroll
   for (int b = 0; b < S; ++b)
@@ -240,8 +278,8 @@ __global__ void lb_combine_kernel(const double* __restrict__ partial, int nchunk
       d1 = __dadd_rn(d1, __dmul_rn(cd, A[b][3]));
       d2 = __dadd_rn(d2, __dmul_rn(cd, A[b][4]));
     }
-    double* Ko = K + ((size_t)i * S + a) * 2;
-    double* Do = D + ((size_t)i * S + a) * 4;
+    double* Ko = K + ((size_t)io * S + a) * 2;
+    double* Do = D + ((size_t)io * S + a) * 4;
     Ko[0] = k0;
     Ko[1] = k1;
     Do[0] = d0;
@@ -249,6 +287,76 @@ __global__ void lb_combine_kernel(const double* __restrict__ partial, int nchunk
     Do[2] = d1;
     Do[3] = d2;
   }
+}
+
+// ------------------------------------------------------------------ outer ordering
+// Outer points are visited in Morton (Z-curve) order of (r, z) so the 32
+// outer points of a warp are spatial neighbours: the m < 0.01 series /
+// closed-form branch of pair_tensor is then warp-coherent (random point
+// clouds otherwise diverge on ~half the warps).  Each outer point's sum is
+// computed identically wherever it lands, so the order changes no bit of
+// the result; the combine kernel scatters rows back through `perm`.
+__global__ void lb_bbox_kernel(int n, const double* __restrict__ r, const double* __restrict__ z,
+                               double* __restrict__ box) {
+  __shared__ double red[4][32];
+  double v[4] = {1e308, -1e308, 1e308, -1e308};
+  for (int p = threadIdx.x; p < n; p += blockDim.x) {
+    v[0] = fmin(v[0], r[p]);
+    v[1] = fmax(v[1], r[p]);
+    v[2] = fmin(v[2], z[p]);
+    v[3] = fmax(v[3], z[p]);
+  }
+  for (int o = 16; o; o >>= 1) {
+    v[0] = fmin(v[0], __shfl_xor_sync(0xffffffffu, v[0], o));
+    v[1] = fmax(v[1], __shfl_xor_sync(0xffffffffu, v[1], o));
+    v[2] = fmin(v[2], __shfl_xor_sync(0xffffffffu, v[2], o));
+    v[3] = fmax(v[3], __shfl_xor_sync(0xffffffffu, v[3], o));
+  }
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  if (l == 0)
+    for (int q = 0; q < 4; ++q) red[q][w] = v[q];
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int ww = 1; ww < (int)(blockDim.x >> 5); ++ww) {
+      v[0] = fmin(v[0], red[0][ww]);
+      v[1] = fmax(v[1], red[1][ww]);
+      v[2] = fmin(v[2], red[2][ww]);
+      v[3] = fmax(v[3], red[3][ww]);
+    }
+    for (int q = 0; q < 4; ++q) box[q] = v[q];
+  }
+}
+
+__device__ __forceinline__ uint32_t spread16(uint32_t x) {
+  x &= 0xFFFFu;
+  x = (x | (x << 8)) & 0x00FF00FFu;
+  x = (x | (x << 4)) & 0x0F0F0F0Fu;
+  x = (x | (x << 2)) & 0x33333333u;
+  x = (x | (x << 1)) & 0x55555555u;
+  return x;
+}
+
+__global__ void lb_morton_kernel(int n, const double* __restrict__ r, const double* __restrict__ z,
+                                 const double* __restrict__ box, uint32_t* __restrict__ key,
+                                 int* __restrict__ idx) {
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= n) return;
+  const double sr = 65535.0 / fmax(box[1] - box[0], 1e-300);
+  const double sz = 65535.0 / fmax(box[3] - box[2], 1e-300);
+  const uint32_t qr = (uint32_t)fmin(fmax((r[p] - box[0]) * sr, 0.0), 65535.0);
+  const uint32_t qz = (uint32_t)fmin(fmax((z[p] - box[2]) * sz, 0.0), 65535.0);
+  key[p] = spread16(qr) | (spread16(qz) << 1);
+  idx[p] = p;
+}
+
+__global__ void lb_gather_kernel(int n, const int* __restrict__ perm, const double* __restrict__ r,
+                                 const double* __restrict__ z, double* __restrict__ rs,
+                                 double* __restrict__ zs) {
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= n) return;
+  const int q = perm[p];
+  rs[p] = r[q];
+  zs[p] = z[q];
 }
 
 // ------------------------------------------------------------------ K2 elements
@@ -318,11 +426,15 @@ __global__ void __launch_bounds__(32 * kElemWarps) lb_elements_kernel(
 __global__ void lb_pairs_kernel(int npair, const double* __restrict__ r, const double* __restrict__ z,
                                 const double* __restrict__ rb, const double* __restrict__ zb,
                                 double* __restrict__ UK, double* __restrict__ UD) {
+  __shared__ double2 logt[1 << LB_LOGT_BITS];
+  for (int t = threadIdx.x; t < (1 << LB_LOGT_BITS); t += blockDim.x)
+    logt[t] = make_double2(c_logt[2 * t], c_logt[2 * t + 1]);
+  __syncthreads();
   const int p = blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= npair) return;
   const Outer o = make_outer(r[p], z[p]);
   const double rn = rb[p];
-  const T5 t = pair_tensor(o, rn, zb[p], rn * rn, rn > 0.0 ? 1.0 / rn : 0.0, 1LL);
+  const T5 t = pair_tensor(o, rn, zb[p], rn * rn, rn > 0.0 ? 1.0 / rn : 0.0, 1LL, logt);
   // restore the pulled-out factor 4 (exact) and lay out as kernel.py:227-234
   UD[4 * p + 0] = 4.0 * t.xx;
   UD[4 * p + 1] = 4.0 * t.xz;
@@ -382,7 +494,7 @@ struct lb_ctx {
   int last_launches = 0;
   cudaEvent_t ev[4] = {};
   // grow-only scratch
-  lb::DevBuf in, rec, partial, out, elem, outer, aux;
+  lb::DevBuf in, rec, partial, out, elem, outer, aux, order;
 };
 
 namespace lb {
@@ -431,13 +543,46 @@ int make_coupling(int S, const double* coK, const double* coD, Coupling& cp) {
   return LB_OK;
 }
 
+constexpr int kOrderMin = 4096;  // outer sets at least this large are Morton-ordered
+
+// Morton order of the outer points: writes perm (sorted -> original index)
+// and the reordered coordinates into ctx->order; returns pointers into it.
+int order_outer(lb_ctx* ctx, int nout, const double* ro, const double* zo, cudaStream_t st,
+                const double** rs, const double** zs, const int** perm) {
+  auto al = [](size_t b) { return (b + 255) & ~size_t(255); };
+  size_t temp = 0;
+  LB_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, temp, (uint32_t*)nullptr, (uint32_t*)nullptr,
+                                          (int*)nullptr, (int*)nullptr, nout, 0, 32, st));
+  const size_t bk = al(sizeof(uint32_t) * nout), bi = al(sizeof(int) * nout),
+               bd = al(sizeof(double) * nout);
+  const size_t total = 2 * bk + 2 * bi + 2 * bd + al(4 * sizeof(double)) + al(temp);
+  int rc = ensure(ctx->order, total);
+  if (rc) return rc;
+  char* p = static_cast<char*>(ctx->order.p);
+  uint32_t* k0 = reinterpret_cast<uint32_t*>(p);
+  uint32_t* k1 = reinterpret_cast<uint32_t*>(p + bk);
+  int* i0 = reinterpret_cast<int*>(p + 2 * bk);
+  int* i1 = reinterpret_cast<int*>(p + 2 * bk + bi);
+  double* r1 = reinterpret_cast<double*>(p + 2 * bk + 2 * bi);
+  double* z1 = reinterpret_cast<double*>(p + 2 * bk + 2 * bi + bd);
+  double* box = reinterpret_cast<double*>(p + 2 * bk + 2 * bi + 2 * bd);
+  void* tmp = p + 2 * bk + 2 * bi + 2 * bd + al(4 * sizeof(double));
+  lb_bbox_kernel<<<1, 1024, 0, st>>>(nout, ro, zo, box);
+  lb_morton_kernel<<<(nout + 255) / 256, 256, 0, st>>>(nout, ro, zo, box, k0, i0);
+  LB_CUDA(cub::DeviceRadixSort::SortPairs(tmp, temp, k0, k1, i0, i1, nout, 0, 32, st));
+  lb_gather_kernel<<<(nout + 255) / 256, 256, 0, st>>>(nout, i1, ro, zo, r1, z1);
+  LB_CUDA(cudaGetLastError());
+  *rs = r1;
+  *zs = z1;
+  *perm = i1;
+  return LB_OK;
+}
+
 template <int S>
 int launch_sweep(lb_ctx* ctx, int nout, const double* ro, const double* zo, int n,
                  const double* rec, const Coupling& cp, long long gthr, double* K, double* D,
                  cudaStream_t st) {
-  constexpr int RS = TileCfg<S>::RS;
-  constexpr int TJ = TileCfg<S>::TJ;
-  const size_t smem = size_t(2) * TJ * RS * sizeof(double);
+  const size_t smem = sweep_smem_bytes<S>();
   static bool attr_done[64] = {};
   if (!attr_done[ctx->device & 63]) {
     LB_CUDA(cudaFuncSetAttribute(lb_sweep_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -447,13 +592,19 @@ int launch_sweep(lb_ctx* ctx, int nout, const double* ro, const double* zo, int 
   int per_sm = 0;
   LB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, lb_sweep_kernel<S>, kTI, smem));
   per_sm = std::max(per_sm, 1);
+  int launches = 0;
+  const int* perm = nullptr;
+  if (nout >= kOrderMin) {
+    int rc = order_outer(ctx, nout, ro, zo, st, &ro, &zo, &perm);
+    if (rc) return rc;
+    launches += 4;  // bbox, morton, radix sort (counted once), gather
+  }
   const int jc = chunk_len(n);
   const int nchunk = (n + jc - 1) / jc;
   // outer batches bounded by the partial-buffer budget
   const size_t per_outer = size_t(nchunk) * 5 * S * sizeof(double);
   int batch = (int)std::min<size_t>((size_t)nout, std::max<size_t>(kTI, kPartialBudget / per_outer));
   batch = std::max(kTI, (batch / kTI) * kTI);
-  int launches = 0;
   for (int o0 = 0; o0 < nout; o0 += batch) {
     const int nb = std::min(batch, nout - o0);
     const int nout_pad = ((nb + kTI - 1) / kTI) * kTI;
@@ -474,9 +625,9 @@ int launch_sweep(lb_ctx* ctx, int nout, const double* ro, const double* zo, int 
     const int grid = (int)std::min<long long>(nitems, (long long)ctx->num_sms * per_sm);
     lb_sweep_kernel<S><<<grid, kTI, smem, st>>>(a);
     LB_CUDA(cudaGetLastError());
-    lb_combine_kernel<S><<<(nb + 127) / 128, 128, 0, st>>>(a.partial, nchunk, nb, nout_pad, cp,
-                                                           K + (size_t)o0 * S * 2,
-                                                           D + (size_t)o0 * S * 4);
+    lb_combine_kernel<S><<<(nb + 127) / 128, 128, 0, st>>>(
+        a.partial, nchunk, nb, nout_pad, cp, perm ? perm + o0 : nullptr,
+        perm ? K : K + (size_t)o0 * S * 2, perm ? D : D + (size_t)o0 * S * 4);
     LB_CUDA(cudaGetLastError());
     launches += 2;
   }
@@ -584,7 +735,8 @@ int lb_ctx_create(int device, lb_ctx** out) {
 int lb_ctx_destroy(lb_ctx* ctx) {
   if (!ctx) return LB_OK;
   cudaSetDevice(ctx->device);
-  for (DevBuf* b : {&ctx->in, &ctx->rec, &ctx->partial, &ctx->out, &ctx->elem, &ctx->outer, &ctx->aux})
+  for (DevBuf* b : {&ctx->in, &ctx->rec, &ctx->partial, &ctx->out, &ctx->elem, &ctx->outer, &ctx->aux,
+                    &ctx->order})
     if (b->p) cudaFree(b->p);
   for (auto& ev : ctx->ev)
     if (ev) cudaEventDestroy(ev);

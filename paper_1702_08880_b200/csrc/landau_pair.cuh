@@ -12,15 +12,14 @@
 //
 // What differs (the arithmetic, not the math):
 //  * no IEEE divides: 1/sqrt(P) is MUFU.RSQ64H + one cubic Newton step,
-//    1/P = (1/sqrt P)^2, 1/d^2 and the log's 1/(mant+1) are MUFU.RCP64H + one
-//    cubic step, 1/m = P * (1/(4 ri)) * (1/rn) from per-point reciprocals;
+//    1/P = (1/sqrt P)^2, 1/d^2 is MUFU.RCP64H + one cubic step, 1/m = P * (1/(4 ri)) * (1/rn) from per-point reciprocals;
 //  * the common factor 4 of B1..B5 is pulled out (an exact power-of-two
 //    scaling) and folded into the species coupling coefficients;
 //  * the m < 0.01 series and the closed form are a real branch instead of
 //    computing both and selecting (kernel.py:366-378 always computes both);
-//  * the log keeps the reference's exponent/mantissa split + atanh series
-//    (kernel.py:317-337) but does the exponent/mantissa work on the integer
-//    pipe and converts the exponent with a magic-number add;
+//  * the log is table-driven (no divide) instead of the reference's
+//    exponent/mantissa split + atanh series (kernel.py:317-337); both are
+//    accurate to ~1 ulp;
 //  * the mask and the d^2 guard are 64-bit integer compares on the bit
 //    pattern (d^2 >= 0, so IEEE order == integer order).
 // Every change is a re-association or a <= 1-ulp reciprocal; the parity
@@ -39,15 +38,20 @@ __constant__ double c_pe[11] = LB_PE;
 __constant__ double c_qe[11] = LB_QEX;
 __constant__ double c_s2[10] = LB_S2C;
 __constant__ double c_s3[10] = LB_S3C;
-// atanh series 2/(2k+1), k = 8..0 (kernel.py:328-336), then ln2, 0.01
-__constant__ double c_misc[12] = {2.0 / 17.0, 2.0 / 15.0, 2.0 / 13.0, 2.0 / 11.0, 2.0 / 9.0,
-                                  2.0 / 7.0,  0.4,        2.0 / 3.0,  2.0,        LB_LN2,
+// log1p tail coefficients (-1/8, 1/7, -1/6, 1/5, 1/3), spare, spare, spare,
+// spare, ln2, the series switch 0.01, the 2^52 + 2^31 magic
+__constant__ double c_misc[12] = {-1.0 / 8.0, 1.0 / 7.0, -1.0 / 6.0, 1.0 / 5.0, 1.0 / 3.0,
+                                  0.0,        0.0,       0.0,        0.0,       LB_LN2,
                                   LB_M_SWITCH, 4503601774854144.0};
+// (invc, logc) table of log_table(), copied to shared memory by the kernels
+__constant__ double c_logt[2 << LB_LOGT_BITS] = LB_LOGT;
 
 // bit pattern of 1e-300 (the reference's d^2 guard, kernel.py:315,345)
 constexpr long long kTinyBits = 0x01A56E1FC2F8F359LL;
 // bit pattern of sqrt(2) (mantissa fold threshold, kernel.py:324)
 constexpr long long kSqrt2Bits = 0x3FF6A09E667F3BCDLL;
+// bit pattern of 0.01, the series / closed-form switch (kernel.py:151)
+constexpr long long kMSwitchBits = 0x3F847AE147AE147BLL;
 
 __device__ __forceinline__ double rcp_approx(double a) {
   double r;
@@ -78,29 +82,33 @@ __device__ __forceinline__ double rsqrt_nr(double a) {
   return fma(ye, c, y);
 }
 
-// ln(x) for normal positive x: the reference's split (kernel.py:317-337).
-__device__ __forceinline__ double log_split(double x) {
-  long long bits = __double_as_longlong(x);
-  long long mb = (bits & 0x000FFFFFFFFFFFFFLL) | 0x3FF0000000000000LL;
-  int e = (int)(bits >> 52) - 1023;
-  if (mb > kSqrt2Bits) {  // mant > sqrt2: halve it, bump the exponent
-    mb -= 0x0010000000000000LL;
-    e += 1;
-  }
-  double mant = __longlong_as_double(mb);
-  double s = (mant - 1.0) * rcp_nr(mant + 1.0);
-  double u = s * s;
-  double p = fma(u, c_misc[0], c_misc[1]);
-  p = fma(p, u, c_misc[2]);
-  p = fma(p, u, c_misc[3]);
-  p = fma(p, u, c_misc[4]);
-  p = fma(p, u, c_misc[5]);
-  p = fma(p, u, c_misc[6]);
-  p = fma(p, u, c_misc[7]);
-  p = fma(p, u, 2.0);
-  // exact int -> double: 2^52 + 2^31 + e, minus the same magic
-  double ed = __longlong_as_double(0x4330000080000000LL + (long long)e) - c_misc[11];
-  return fma(ed, c_misc[9], s * p);
+// ln(x) for normal positive x (the reference uses an exponent/mantissa split
+// + atanh series, kernel.py:317-337; any log accurate to ~1 ulp agrees to
+// 1e-16).  Here: table-driven reduction, no divide.  The mantissa is folded
+// around 1 (z in [0.6875, 1.375)), a 128-entry table gives invc ~ 1/z and
+// logc = -ln(invc) (invc == 1 exactly on the two bins touching 1.0, so ln x
+// keeps full relative accuracy as x -> 1), r = z*invc - 1 (|r| < 2^-7, one
+// FMA), ln(1+r) = r + r^2 q(r) with q the degree-6 Taylor tail.
+// Measured max relative error 2.2e-16 (tools/gen_coefs.py table).
+constexpr long long kLogOff = 0x3FE6000000000000LL;
+__device__ __forceinline__ double log_table(double x, const double2* __restrict__ tab) {
+  const long long ix = __double_as_longlong(x);
+  const long long tmp = ix - kLogOff;
+  const int i = (int)((tmp >> (52 - LB_LOGT_BITS)) & ((1 << LB_LOGT_BITS) - 1));
+  const int k = (int)(tmp >> 52);
+  const double z = __longlong_as_double(ix - (tmp & (long long)0xFFF0000000000000ULL));
+  const double2 t = tab[i];  // (invc, logc)
+  const double r = fma(z, t.x, -1.0);
+  double q = fma(r, c_misc[0], c_misc[1]);  // -1/8 r + 1/7
+  q = fma(q, r, c_misc[2]);                 // -1/6
+  q = fma(q, r, c_misc[3]);                 //  1/5
+  q = fma(q, r, -0.25);
+  q = fma(q, r, c_misc[4]);                 //  1/3
+  q = fma(q, r, -0.5);
+  const double l1p = fma(r * r, q, r);
+  // exact int -> double: 2^52 + 2^31 + k, minus the same magic
+  const double kd = __longlong_as_double(0x4330000080000000LL + (long long)k) - c_misc[11];
+  return fma(kd, c_misc[9], t.y + l1p);
 }
 
 // Per-outer-point invariants (hoisted out of the pair loop).
@@ -133,7 +141,8 @@ struct T5 {
 // One (outer, inner) pair.  gthr = max(bits(eps^2), 1): the pair contributes
 // iff bits(d^2) >= gthr, i.e. d^2 >= eps^2 and d^2 > 0 (kernel.py:344).
 __device__ __forceinline__ T5 pair_tensor(const Outer& o, double rn, double zn, double rn2,
-                                          double rcpr, long long gthr) {
+                                          double rcpr, long long gthr,
+                                          const double2* __restrict__ logt) {
   const double dr = o.ri - rn;
   const double dz = o.zi - zn;
   const double dz2 = dz * dz;
@@ -147,7 +156,7 @@ __device__ __forceinline__ T5 pair_tensor(const Outer& o, double rn, double zn, 
   const double invP = isP * isP;
   const double x = d2 * invP;
   const double m = tq * invP;
-  const double lx = log_split(x);
+  const double lx = log_table(x, logt);
 
   // four Horner chains in x (kernel.py:351-359); QK[10] = QEx[10] = QEx[0] = 0
   double pk = fma(c_pk[10], x, c_pk[9]);
@@ -168,7 +177,7 @@ __device__ __forceinline__ T5 pair_tensor(const Outer& o, double rn, double zn, 
   const double Em1 = EE * (P * rcp_nr(d2));  // E/(1-m)
 
   double S2, S3;
-  if (m < c_misc[10]) {
+  if (__double_as_longlong(m) < kMSwitchBits) {  // m < 0.01 (m >= 0: integer order)
     // hypergeometric series (kernel.py:369-375)
     double s2 = c_s2[9], s3 = c_s3[9];
     s2 = fma(s2, m, c_s2[8]);  s3 = fma(s3, m, c_s3[8]);
