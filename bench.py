@@ -228,11 +228,21 @@ def ours_arm(args):
     def step(ev=None):
         sh.pack_local(*d_fields)
         sh.all_gather()
-        if ev is not None:
-            ev[0].record(st)
-        sh.sweep_local(d_fields[0], d_fields[1])
-        if ev is not None:
-            ev[1].record(st)
+        if sh.symmetric:  # each unordered pair once; tile pairs split over ranks
+            sh.sym_prepare()
+            if ev is not None:
+                ev[0].record(st)
+            sh.sym_partial()  # lb_symsweep_kernel + its fixed-order reduction
+            if ev is not None:
+                ev[1].record(st)
+            sh.sym_reduce()
+            sh.sym_finish()
+        else:
+            if ev is not None:
+                ev[0].record(st)
+            sh.sweep_local(d_fields[0], d_fields[1])
+            if ev is not None:
+                ev[1].record(st)
 
     for _ in range(args.warmup):
         step()
@@ -259,7 +269,9 @@ def ours_arm(args):
     value = pairs_step * args.steps / (tot_ms * 1e-3)
     # roofline of the dominant kernel on this rank: model flops per launch / launch time
     sweep_avg_s = sum(sweep_ms) / len(sweep_ms) * 1e-3
-    flops_launch = pkg.flop_count(N, S, nloc)
+    # ordered pairs this rank's sweep delivers: its outer points x N (general
+    # path) or its 1/world share of the tile pairs, each feeding both points
+    flops_launch = pkg.flop_count(N, S, N / world if sh.symmetric else nloc)
     achieved_tf = flops_launch / sweep_avg_s / 1e12
 
     # e2e through the public API with pinned host buffers (copies inside the timed region)
@@ -339,8 +351,13 @@ def ours_arm(args):
             "roofline": {"bound": "fp64", "achieved": achieved_tf, "peak": fp64_sustained,
                          "unit": "TFLOP/s", "frac": achieved_tf / fp64_sustained,
                          "traffic": traffic,
-                         "kernel": "lb_sweep_kernel<2> (+ lb_combine_kernel, <1%)",
-                         "flops": "model 165+20*S^2 per pair (kernel.py:560-574)",
+                         "kernel": ("lb_symsweep_kernel<2> + lb_symreduce_kernel" if sh.symmetric
+                                    else "lb_sweep_kernel<2> (+ lb_combine_kernel, <1%)"),
+                         "flops": "model 165+20*S^2 per ordered pair (kernel.py:560-574)"
+                                  + ("; symmetric path evaluates each unordered pair once, "
+                                     "so model flops per executed flop is ~1.7 and frac may "
+                                     "exceed 1 (see executed-flop fraction from ncu in "
+                                     "profiles/)" if sh.symmetric else ""),
                          "peak_source": "measured DFMA microbenchmark on this GPU "
                                         "(lb_fp64_peak, median of the last half of 1 s)",
                          "peak_burst": fp64_burst, "frac_of_nominal_37.2": achieved_tf / 37.2},
@@ -348,6 +365,7 @@ def ours_arm(args):
             "gpu_launches": launches,
             "clocks": clocks,
             "kernel_ms_per_step": tot_sweep_ms / args.steps,
+            "path": "symmetric (unordered pairs)" if sh.symmetric else "general (ordered pairs)",
         }
         if cpu:
             line["cpu_baseline"] = cpu

@@ -105,6 +105,17 @@ int lb_assemble_elements(lb_ctx *ctx, int ncell, const double *cell_sizes, int S
                          const double *B, const double *dB,
                          double *K_out, double *D_out, double *elem_out, double *phase_ms);
 
+/* All-points entry (outer set == inner set == the n points): the call
+ * `assemble_collision` makes (assembly.py:148, fused_sweep(data.r, data.z,
+ * data, ...)).  For S <= 2 it evaluates each unordered pair once (all
+ * expensive terms are symmetric in i <-> j; only UD_xx differs for the
+ * swapped pair) and feeds both points' accumulators; larger S uses the
+ * general sweep.  K_out (n,S,2), D_out (n,S,2,2) in the input point order. */
+int lb_fused_sweep_all(lb_ctx *ctx, int n, int S, const double *r, const double *z,
+                       const double *w, const double *f, const double *df_r,
+                       const double *df_z, const double *coK, const double *coD,
+                       double eps_d, double *K_out, double *D_out);
+
 /* Per-pair closed form on the device: replaces `axisym_tensor_pair`
  * (kernel.py:206-235) for npair independent (r, z, rbar, zbar) tuples, with
  * the same device arithmetic the sweep uses.  UK, UD: (npair, 2, 2).
@@ -133,6 +144,26 @@ int lb_sweep_dev(lb_ctx *ctx, int nout, const double *outer_r, const double *out
 int lb_elements_dev(lb_ctx *ctx, int ncell, int S, const double *cell_sizes,
                     const double *w, const double *K, const double *D,
                     const double *B, const double *dB, double *elem_out, void *stream);
+
+/* Symmetric all-points sweep in three device steps, for the multi-GPU
+ * layer (the per-rank partial sums are added across ranks by the caller,
+ * e.g. an NCCL all-reduce, between steps 2 and 3):
+ *  1 lb_sym_prepare_dev  Morton-order the n packed records (all points, the
+ *                        same on every rank) into the context;
+ *  2 lb_sym_partial_dev  this rank's share of the unordered tile pairs ->
+ *                        tot[5S][lb_sym_npad(n)] partial accumulators (sorted
+ *                        point order; zero where the rank contributed none);
+ *  3 lb_sym_combine_dev  K/D for original points [q0, q1) from the summed tot
+ *                        (K_out/D_out hold q1-q0 rows).
+ * lb_sym_supported(S) is 1 for the species counts this path implements. */
+int lb_sym_supported(int S);
+int lb_sym_npad(int n);
+int lb_sym_prepare_dev(lb_ctx *ctx, int n, int S, const double *rec, void *stream);
+int lb_sym_partial_dev(lb_ctx *ctx, int S, double eps_d, int rank, int world, double *tot,
+                       void *stream);
+int lb_sym_combine_dev(lb_ctx *ctx, int S, const double *tot, const double *coK,
+                       const double *coD, int q0, int q1, double *K_out, double *D_out,
+                       void *stream);
 
 /* Number of kernels the most recent lb_sweep_dev / lb_elements_dev /
  * lb_pack_records_dev call launched (for the benchmark's launch count). */

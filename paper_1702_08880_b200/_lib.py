@@ -39,7 +39,14 @@ SIGNATURES = {
                             _dp, _dp, _d, _dp, _dp]),
     "lb_assemble_elements": (_i, [_vp, _i, _dp, _i, _dp, _dp, _dp, _dp, _dp, _dp,
                                   _dp, _dp, _d, _dp, _dp, _dp, _dp, _dp, _dp]),
+    "lb_fused_sweep_all": (_i, [_vp, _i, _i, _dp, _dp, _dp, _dp, _dp, _dp, _dp, _dp, _d,
+                                _dp, _dp]),
     "lb_tensor_pairs": (_i, [_vp, _i, _dp, _dp, _dp, _dp, _dp, _dp]),
+    "lb_sym_supported": (_i, [_i]),
+    "lb_sym_npad": (_i, [_i]),
+    "lb_sym_prepare_dev": (_i, [_vp, _i, _i, _vp, _vp]),
+    "lb_sym_partial_dev": (_i, [_vp, _i, _d, _i, _i, _vp, _vp]),
+    "lb_sym_combine_dev": (_i, [_vp, _i, _vp, _dp, _dp, _i, _i, _vp, _vp, _vp]),
     "lb_pack_records_dev": (_i, [_vp, _i, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
     "lb_sweep_dev": (_i, [_vp, _i, _vp, _vp, _i, _i, _vp, _dp, _dp, _d, _vp, _vp, _vp]),
     "lb_elements_dev": (_i, [_vp, _i, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),

@@ -289,6 +289,8 @@ __global__ void lb_combine_kernel(const double* __restrict__ partial, int nchunk
   }
 }
 
+#include "landau_sym.cuh"  // symmetric all-points sweep (kernels)
+
 // ------------------------------------------------------------------ outer ordering
 // Outer points are visited in Morton (Z-curve) order of (r, z) so the 32
 // outer points of a warp are spatial neighbours: the m < 0.01 series /
@@ -297,14 +299,15 @@ __global__ void lb_combine_kernel(const double* __restrict__ partial, int nchunk
 // computed identically wherever it lands, so the order changes no bit of
 // the result; the combine kernel scatters rows back through `perm`.
 __global__ void lb_bbox_kernel(int n, const double* __restrict__ r, const double* __restrict__ z,
-                               double* __restrict__ box) {
+                               int stride, double* __restrict__ box) {
   __shared__ double red[4][32];
   double v[4] = {1e308, -1e308, 1e308, -1e308};
   for (int p = threadIdx.x; p < n; p += blockDim.x) {
-    v[0] = fmin(v[0], r[p]);
-    v[1] = fmax(v[1], r[p]);
-    v[2] = fmin(v[2], z[p]);
-    v[3] = fmax(v[3], z[p]);
+    const double rp = r[(size_t)p * stride], zp = z[(size_t)p * stride];
+    v[0] = fmin(v[0], rp);
+    v[1] = fmax(v[1], rp);
+    v[2] = fmin(v[2], zp);
+    v[3] = fmax(v[3], zp);
   }
   for (int o = 16; o; o >>= 1) {
     v[0] = fmin(v[0], __shfl_xor_sync(0xffffffffu, v[0], o));
@@ -337,14 +340,15 @@ __device__ __forceinline__ uint32_t spread16(uint32_t x) {
 }
 
 __global__ void lb_morton_kernel(int n, const double* __restrict__ r, const double* __restrict__ z,
-                                 const double* __restrict__ box, uint32_t* __restrict__ key,
-                                 int* __restrict__ idx) {
+                                 int stride, const double* __restrict__ box,
+                                 uint32_t* __restrict__ key, int* __restrict__ idx) {
   const int p = blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= n) return;
+  const double rp = r[(size_t)p * stride], zp = z[(size_t)p * stride];
   const double sr = 65535.0 / fmax(box[1] - box[0], 1e-300);
   const double sz = 65535.0 / fmax(box[3] - box[2], 1e-300);
-  const uint32_t qr = (uint32_t)fmin(fmax((r[p] - box[0]) * sr, 0.0), 65535.0);
-  const uint32_t qz = (uint32_t)fmin(fmax((z[p] - box[2]) * sz, 0.0), 65535.0);
+  const uint32_t qr = (uint32_t)fmin(fmax((rp - box[0]) * sr, 0.0), 65535.0);
+  const uint32_t qz = (uint32_t)fmin(fmax((zp - box[2]) * sz, 0.0), 65535.0);
   key[p] = spread16(qr) | (spread16(qz) << 1);
   idx[p] = p;
 }
@@ -495,6 +499,9 @@ struct lb_ctx {
   cudaEvent_t ev[4] = {};
   // grow-only scratch
   lb::DevBuf in, rec, partial, out, elem, outer, aux, order;
+  // symmetric all-points sweep state (lb_sym_*): sorted records, order, partials
+  lb::DevBuf symord, symrec, syminv, symi, symj, symtot;
+  int sym_n = -1, sym_S = 0, sym_nt = 0;
 };
 
 namespace lb {
@@ -545,10 +552,11 @@ int make_coupling(int S, const double* coK, const double* coD, Coupling& cp) {
 
 constexpr int kOrderMin = 4096;  // outer sets at least this large are Morton-ordered
 
-// Morton order of the outer points: writes perm (sorted -> original index)
-// and the reordered coordinates into ctx->order; returns pointers into it.
-int order_outer(lb_ctx* ctx, int nout, const double* ro, const double* zo, cudaStream_t st,
-                const double** rs, const double** zs, const int** perm) {
+// Morton order of n points (r, z at the given stride): perm (sorted ->
+// original index) in `buf`; when rs/zs are requested the reordered
+// coordinates too.  Returns pointers into `buf`.
+int morton_order(DevBuf& buf, int nout, const double* ro, const double* zo, int stride,
+                 cudaStream_t st, const int** perm, const double** rs, const double** zs) {
   auto al = [](size_t b) { return (b + 255) & ~size_t(255); };
   size_t temp = 0;
   LB_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, temp, (uint32_t*)nullptr, (uint32_t*)nullptr,
@@ -556,9 +564,9 @@ int order_outer(lb_ctx* ctx, int nout, const double* ro, const double* zo, cudaS
   const size_t bk = al(sizeof(uint32_t) * nout), bi = al(sizeof(int) * nout),
                bd = al(sizeof(double) * nout);
   const size_t total = 2 * bk + 2 * bi + 2 * bd + al(4 * sizeof(double)) + al(temp);
-  int rc = ensure(ctx->order, total);
+  int rc = ensure(buf, total);
   if (rc) return rc;
-  char* p = static_cast<char*>(ctx->order.p);
+  char* p = static_cast<char*>(buf.p);
   uint32_t* k0 = reinterpret_cast<uint32_t*>(p);
   uint32_t* k1 = reinterpret_cast<uint32_t*>(p + bk);
   int* i0 = reinterpret_cast<int*>(p + 2 * bk);
@@ -567,13 +575,15 @@ int order_outer(lb_ctx* ctx, int nout, const double* ro, const double* zo, cudaS
   double* z1 = reinterpret_cast<double*>(p + 2 * bk + 2 * bi + bd);
   double* box = reinterpret_cast<double*>(p + 2 * bk + 2 * bi + 2 * bd);
   void* tmp = p + 2 * bk + 2 * bi + 2 * bd + al(4 * sizeof(double));
-  lb_bbox_kernel<<<1, 1024, 0, st>>>(nout, ro, zo, box);
-  lb_morton_kernel<<<(nout + 255) / 256, 256, 0, st>>>(nout, ro, zo, box, k0, i0);
+  lb_bbox_kernel<<<1, 1024, 0, st>>>(nout, ro, zo, stride, box);
+  lb_morton_kernel<<<(nout + 255) / 256, 256, 0, st>>>(nout, ro, zo, stride, box, k0, i0);
   LB_CUDA(cub::DeviceRadixSort::SortPairs(tmp, temp, k0, k1, i0, i1, nout, 0, 32, st));
-  lb_gather_kernel<<<(nout + 255) / 256, 256, 0, st>>>(nout, i1, ro, zo, r1, z1);
+  if (rs) {
+    lb_gather_kernel<<<(nout + 255) / 256, 256, 0, st>>>(nout, i1, ro, zo, r1, z1);
+    *rs = r1;
+    *zs = z1;
+  }
   LB_CUDA(cudaGetLastError());
-  *rs = r1;
-  *zs = z1;
   *perm = i1;
   return LB_OK;
 }
@@ -595,7 +605,7 @@ int launch_sweep(lb_ctx* ctx, int nout, const double* ro, const double* zo, int 
   int launches = 0;
   const int* perm = nullptr;
   if (nout >= kOrderMin) {
-    int rc = order_outer(ctx, nout, ro, zo, st, &ro, &zo, &perm);
+    int rc = morton_order(ctx->order, nout, ro, zo, 1, st, &perm, &ro, &zo);
     if (rc) return rc;
     launches += 4;  // bbox, morton, radix sort (counted once), gather
   }
@@ -656,6 +666,131 @@ int check_species(int S) {
     return fail(LB_EINVAL, "species count " + std::to_string(S) + " outside [1, " +
                                std::to_string(LB_MAX_SPECIES) + "]");
   return LB_OK;
+}
+
+
+// ------------------------------------------------------------------ symmetric path (host)
+constexpr size_t kSymBudget = size_t(2) << 30;  // bytes of i/j-side partials per row batch
+
+int sym_prepare(lb_ctx* ctx, int n, int S, const double* rec, cudaStream_t st) {
+  const int RS = rec_stride(S);
+  const int nt = (n + kSymTile - 1) / kSymTile;
+  const int npad = nt * kSymTile;
+  const int* perm = nullptr;
+  int rc = morton_order(ctx->symord, n, rec, rec + 1, RS, st, &perm, nullptr, nullptr);
+  if (rc) return rc;
+  if ((rc = ensure(ctx->symrec, (size_t)npad * RS * sizeof(double)))) return rc;
+  if ((rc = ensure(ctx->syminv, (size_t)n * sizeof(int)))) return rc;
+  lb_sym_gather_kernel<<<(npad + 255) / 256, 256, 0, st>>>(n, npad, RS, perm, rec,
+                                                          static_cast<double*>(ctx->symrec.p));
+  lb_invert_perm_kernel<<<(n + 255) / 256, 256, 0, st>>>(n, perm, static_cast<int*>(ctx->syminv.p));
+  LB_CUDA(cudaGetLastError());
+  ctx->sym_n = n;
+  ctx->sym_S = S;
+  ctx->sym_nt = nt;
+  ctx->last_launches = 6;  // bbox, morton, radix sort (1), gather, records gather, invert
+  return LB_OK;
+}
+
+template <int S>
+int sym_partial(lb_ctx* ctx, long long gthr, int rank, int world, double* tot, cudaStream_t st) {
+  const int nt = ctx->sym_nt;
+  const int npad = nt * kSymTile;
+  const int R0 = (int)((long long)nt * rank / world), R1 = (int)((long long)nt * (rank + 1) / world);
+  const int nseg = sym_nseg(nt), hmax = sym_hmax(nt);
+  int launches = 0;
+  if (R0 >= R1) {
+    LB_CUDA(cudaMemsetAsync(tot, 0, sizeof(double) * 5 * S * npad, st));
+    ctx->last_launches = 0;
+    return LB_OK;
+  }
+  const size_t smem = sym_smem_bytes<S>();
+  static bool attr_done[64] = {};
+  if (!attr_done[ctx->device & 63]) {
+    LB_CUDA(cudaFuncSetAttribute(lb_symsweep_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)smem));
+    attr_done[ctx->device & 63] = true;
+  }
+  int per_sm = 0;
+  LB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, lb_symsweep_kernel<S>, kSymTile, smem));
+  per_sm = std::max(per_sm, 1);
+  const size_t row_i = (size_t)nseg * 5 * S * kSymTile * sizeof(double);
+  const size_t row_j = (size_t)std::max(hmax, 1) * 5 * S * kSymTile * sizeof(double);
+  const int RB = (int)std::max<size_t>(1, std::min<size_t>(R1 - R0, kSymBudget / (row_i + row_j)));
+  int rc;
+  if ((rc = ensure(ctx->symi, row_i * RB))) return rc;
+  if ((rc = ensure(ctx->symj, row_j * RB))) return rc;
+  for (int b0 = R0; b0 < R1; b0 += RB) {
+    const int b1 = std::min(R1, b0 + RB);
+    SymArgs a;
+    a.rec = static_cast<const double*>(ctx->symrec.p);
+    a.iside = static_cast<double*>(ctx->symi.p);
+    a.jside = static_cast<double*>(ctx->symj.p);
+    a.nt = nt;
+    a.row0 = b0;
+    a.row1 = b1;
+    a.nseg = nseg;
+    a.hmax = hmax;
+    a.gthr = gthr;
+    const long long nitems = (long long)(b1 - b0) * nseg;
+    const int grid = (int)std::min<long long>(nitems, (long long)ctx->num_sms * per_sm);
+    lb_symsweep_kernel<S><<<grid, kSymTile, smem, st>>>(a);
+    LB_CUDA(cudaGetLastError());
+    lb_symreduce_kernel<S><<<(npad + 127) / 128, 128, 0, st>>>(a.iside, a.jside, nt, b0, b1, nseg,
+                                                               hmax, b0 == R0 ? 1 : 0, tot);
+    LB_CUDA(cudaGetLastError());
+    launches += 2;
+  }
+  ctx->last_launches = launches;
+  return LB_OK;
+}
+
+template <int S>
+int sym_combine(lb_ctx* ctx, const double* tot, const Coupling& cp, int q0, int q1, double* K,
+                double* D, cudaStream_t st) {
+  if (q1 <= q0) return LB_OK;
+  const int npad = ctx->sym_nt * kSymTile;
+  lb_sym_combine_kernel<S><<<(q1 - q0 + 127) / 128, 128, 0, st>>>(
+      tot, npad, static_cast<const int*>(ctx->syminv.p), q0, q1, cp, K, D);
+  LB_CUDA(cudaGetLastError());
+  ctx->last_launches = 1;
+  return LB_OK;
+}
+
+int sym_partial_dispatch(lb_ctx* ctx, int S, long long gthr, int rank, int world, double* tot,
+                         cudaStream_t st) {
+  switch (S) {
+    case 1: return sym_partial<1>(ctx, gthr, rank, world, tot, st);
+    case 2: return sym_partial<2>(ctx, gthr, rank, world, tot, st);
+    default: return fail(LB_EINVAL, "symmetric sweep supports S <= 2");
+  }
+}
+
+int sym_combine_dispatch(lb_ctx* ctx, int S, const double* tot, const Coupling& cp, int q0, int q1,
+                         double* K, double* D, cudaStream_t st) {
+  switch (S) {
+    case 1: return sym_combine<1>(ctx, tot, cp, q0, q1, K, D, st);
+    case 2: return sym_combine<2>(ctx, tot, cp, q0, q1, K, D, st);
+    default: return fail(LB_EINVAL, "symmetric sweep supports S <= 2");
+  }
+}
+
+// All-points sweep (outer == inner == the n packed records) on one device:
+// symmetric path when S <= kSymMaxS, else the general sweep.
+int all_points_sweep(lb_ctx* ctx, int n, int S, const double* rec, const double* r, const double* z,
+                     const Coupling& cp, long long gthr, double* K, double* D, cudaStream_t st) {
+  if (S > kSymMaxS || n < kSymTile)
+    return sweep_dispatch(ctx, n, r, z, n, S, rec, cp, gthr, K, D, st);
+  int rc = sym_prepare(ctx, n, S, rec, st);
+  if (rc) return rc;
+  const int npad = ctx->sym_nt * kSymTile;
+  if ((rc = ensure(ctx->symtot, (size_t)5 * S * npad * sizeof(double)))) return rc;
+  double* tot = static_cast<double*>(ctx->symtot.p);
+  if ((rc = sym_partial_dispatch(ctx, S, gthr, 0, 1, tot, st))) return rc;
+  int l = ctx->last_launches;
+  rc = sym_combine_dispatch(ctx, S, tot, cp, 0, n, K, D, st);
+  ctx->last_launches += l + 6;
+  return rc;
 }
 
 int launch_pack(lb_ctx* ctx, int n, int S, const double* r, const double* z, const double* w,
@@ -736,7 +871,8 @@ int lb_ctx_destroy(lb_ctx* ctx) {
   if (!ctx) return LB_OK;
   cudaSetDevice(ctx->device);
   for (DevBuf* b : {&ctx->in, &ctx->rec, &ctx->partial, &ctx->out, &ctx->elem, &ctx->outer, &ctx->aux,
-                    &ctx->order})
+                    &ctx->order, &ctx->symord, &ctx->symrec, &ctx->syminv, &ctx->symi, &ctx->symj,
+                    &ctx->symtot})
     if (b->p) cudaFree(b->p);
   for (auto& ev : ctx->ev)
     if (ev) cudaEventDestroy(ev);
@@ -891,7 +1027,12 @@ int lb_assemble_elements(lb_ctx* ctx, int ncell, const double* cell_sizes, int S
   double* drec = static_cast<double*>(ctx->rec.p);
   if ((rc = launch_pack(ctx, n, S, dr, dz, dw, df, dfr, dfz, drec, st))) return rc;
   LB_CUDA(cudaEventRecord(ctx->ev[1], st));
-  if ((rc = lb_sweep_dev(ctx, n, dr, dz, n, S, drec, coK, coD, eps_d, dK, dD, st))) return rc;
+  {
+    Coupling cp;
+    make_coupling(S, coK, coD, cp);
+    if ((rc = all_points_sweep(ctx, n, S, drec, dr, dz, cp, mask_threshold(eps_d), dK, dD, st)))
+      return rc;
+  }
   LB_CUDA(cudaEventRecord(ctx->ev[2], st));
   if ((rc = launch_elements(ctx, ncell, S, dsz, dw, dK, dD, dB_, ddB, delem, st))) return rc;
   if (K_out) LB_CUDA(cudaMemcpyAsync(K_out, dK, sizeof(double) * 2 * S * n, cudaMemcpyDeviceToHost, st));
@@ -907,6 +1048,78 @@ int lb_assemble_elements(lb_ctx* ctx, int ncell, const double* cell_sizes, int S
     }
   }
   return LB_OK;
+}
+
+int lb_fused_sweep_all(lb_ctx* ctx, int n, int S, const double* r, const double* z, const double* w,
+                       const double* f, const double* df_r, const double* df_z, const double* coK,
+                       const double* coD, double eps_d, double* K_out, double* D_out) {
+  int rc = use_ctx(ctx);
+  if (rc) return rc;
+  if ((rc = check_species(S))) return rc;
+  if (n < 0) return fail(LB_EINVAL, "negative point count");
+  if (n == 0) return LB_OK;
+  if (!r || !z || !w || !f || !df_r || !df_z || !coK || !coD || !K_out || !D_out)
+    return fail(LB_EINVAL, "null argument");
+  cudaStream_t st = ctx->stream;
+  const size_t nin = (size_t)(3 + 3 * S) * n;
+  if ((rc = ensure(ctx->in, nin * sizeof(double)))) return rc;
+  if ((rc = ensure(ctx->rec, (size_t)n * rec_stride(S) * sizeof(double)))) return rc;
+  if ((rc = ensure(ctx->out, (size_t)6 * S * n * sizeof(double)))) return rc;
+  double* din = static_cast<double*>(ctx->in.p);
+  double *dr = din, *dz = dr + n, *dw = dz + n, *df = dw + n, *dfr = df + (size_t)S * n,
+         *dfz = dfr + (size_t)S * n;
+  double* dK = static_cast<double*>(ctx->out.p);
+  double* dD = dK + (size_t)2 * S * n;
+  const size_t bn = sizeof(double) * n, bsn = sizeof(double) * S * n;
+  LB_CUDA(cudaMemcpyAsync(dr, r, bn, cudaMemcpyHostToDevice, st));
+  LB_CUDA(cudaMemcpyAsync(dz, z, bn, cudaMemcpyHostToDevice, st));
+  LB_CUDA(cudaMemcpyAsync(dw, w, bn, cudaMemcpyHostToDevice, st));
+  LB_CUDA(cudaMemcpyAsync(df, f, bsn, cudaMemcpyHostToDevice, st));
+  LB_CUDA(cudaMemcpyAsync(dfr, df_r, bsn, cudaMemcpyHostToDevice, st));
+  LB_CUDA(cudaMemcpyAsync(dfz, df_z, bsn, cudaMemcpyHostToDevice, st));
+  double* drec = static_cast<double*>(ctx->rec.p);
+  if ((rc = launch_pack(ctx, n, S, dr, dz, dw, df, dfr, dfz, drec, st))) return rc;
+  Coupling cp;
+  make_coupling(S, coK, coD, cp);
+  if ((rc = all_points_sweep(ctx, n, S, drec, dr, dz, cp, mask_threshold(eps_d), dK, dD, st)))
+    return rc;
+  LB_CUDA(cudaMemcpyAsync(K_out, dK, sizeof(double) * 2 * S * n, cudaMemcpyDeviceToHost, st));
+  LB_CUDA(cudaMemcpyAsync(D_out, dD, sizeof(double) * 4 * S * n, cudaMemcpyDeviceToHost, st));
+  LB_CUDA(cudaStreamSynchronize(st));
+  return LB_OK;
+}
+
+int lb_sym_supported(int S) { return (S >= 1 && S <= kSymMaxS) ? 1 : 0; }
+
+int lb_sym_npad(int n) { return ((std::max(n, 0) + kSymTile - 1) / kSymTile) * kSymTile; }
+
+int lb_sym_prepare_dev(lb_ctx* ctx, int n, int S, const double* rec, void* stream) {
+  int rc = use_ctx(ctx);
+  if (rc) return rc;
+  if (!lb_sym_supported(S)) return fail(LB_EINVAL, "symmetric sweep supports 1 <= S <= 2");
+  if (n < 1) return fail(LB_EINVAL, "symmetric sweep needs n >= 1");
+  return sym_prepare(ctx, n, S, rec, (cudaStream_t)stream);
+}
+
+int lb_sym_partial_dev(lb_ctx* ctx, int S, double eps_d, int rank, int world, double* tot,
+                       void* stream) {
+  int rc = use_ctx(ctx);
+  if (rc) return rc;
+  if (ctx->sym_n < 0 || ctx->sym_S != S) return fail(LB_EINVAL, "lb_sym_prepare_dev not called for this S");
+  if (world < 1 || rank < 0 || rank >= world) return fail(LB_EINVAL, "bad rank / world");
+  return sym_partial_dispatch(ctx, S, mask_threshold(eps_d), rank, world, tot, (cudaStream_t)stream);
+}
+
+int lb_sym_combine_dev(lb_ctx* ctx, int S, const double* tot, const double* coK, const double* coD,
+                       int q0, int q1, double* K_out, double* D_out, void* stream) {
+  int rc = use_ctx(ctx);
+  if (rc) return rc;
+  if (ctx->sym_n < 0 || ctx->sym_S != S) return fail(LB_EINVAL, "lb_sym_prepare_dev not called for this S");
+  if (q0 < 0 || q1 > ctx->sym_n || q0 > q1) return fail(LB_EINVAL, "bad point range");
+  if (!coK || !coD) return fail(LB_EINVAL, "null coupling table");
+  Coupling cp;
+  make_coupling(S, coK, coD, cp);
+  return sym_combine_dispatch(ctx, S, tot, cp, q0, q1, K_out, D_out, (cudaStream_t)stream);
 }
 
 int lb_tensor_pairs(lb_ctx* ctx, int npair, const double* r, const double* z, const double* rbar,

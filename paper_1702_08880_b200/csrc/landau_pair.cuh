@@ -138,11 +138,16 @@ struct T5 {
   double xx, zz, xz, kr, zr;
 };
 
-// One (outer, inner) pair.  gthr = max(bits(eps^2), 1): the pair contributes
-// iff bits(d^2) >= gthr, i.e. d^2 >= eps^2 and d^2 > 0 (kernel.py:344).
-__device__ __forceinline__ T5 pair_tensor(const Outer& o, double rn, double zn, double rn2,
-                                          double rcpr, long long gthr,
-                                          const double2* __restrict__ logt) {
+// The symmetric part of one pair: B1..B5 (each / 4), dz, dz^2 and the mask.
+struct PairB {
+  double B1, B3, B4, B5, dz, dz2;
+  bool g;
+};
+
+// gthr = max(bits(eps^2), 1): the pair contributes iff bits(d^2) >= gthr,
+// i.e. d^2 >= eps^2 and d^2 > 0 (kernel.py:344).
+__device__ __forceinline__ PairB pair_core(const Outer& o, double rn, double zn, double rcpr,
+                                           long long gthr, const double2* __restrict__ logt) {
   const double dr = o.ri - rn;
   const double dz = o.zi - zn;
   const double dz2 = dz * dz;
@@ -199,22 +204,52 @@ __device__ __forceinline__ T5 pair_tensor(const Outer& o, double rn, double zn, 
     S3 = fma(4.0, fma(c, invm, -a) * invm, Em1);
   }
   const double c3 = isP * invP;  // P^-3/2 (the 4 is folded into the coupling)
-  const double B1 = EK * isP;
-  const double B3 = Em1 * c3;
-  const double B4 = S2 * c3;
-  const double B5 = S3 * c3;
+  PairB p;
+  p.B1 = EK * isP;
+  p.B3 = Em1 * c3;
+  p.B4 = S2 * c3;
+  p.B5 = S3 * c3;
+  p.dz = dz;
+  p.dz2 = dz2;
+  p.g = g;
+  return p;
+}
+
+// Direct-pair tensor components from the symmetric part.
+__device__ __forceinline__ T5 pair_tensors(const Outer& o, double rn, double rn2, const PairB& p) {
   const double rr = o.ri * rn;
   const double rr2 = o.tri * rn;
   T5 t;
-  t.xx = fma(-rn2, B5, fma(rr2, B4, fma(-o.ri2, B3, B1)));
-  t.zz = fma(-dz2, B3, B1);
-  t.xz = dz * fma(rn, B4, -(o.ri * B3));
-  t.kr = fma(rr, B3 - B5, dz2 * B4);
-  t.zr = dz * fma(rn, B3, -(o.ri * B4));
-  if (!g) {
+  t.xx = fma(-rn2, p.B5, fma(rr2, p.B4, fma(-o.ri2, p.B3, p.B1)));
+  t.zz = fma(-p.dz2, p.B3, p.B1);
+  t.xz = p.dz * fma(rn, p.B4, -(o.ri * p.B3));
+  t.kr = fma(rr, p.B3 - p.B5, p.dz2 * p.B4);
+  t.zr = p.dz * fma(rn, p.B3, -(o.ri * p.B4));
+  if (!p.g) {
     t.xx = 0.0; t.zz = 0.0; t.xz = 0.0; t.kr = 0.0; t.zr = 0.0;
   }
   return t;
+}
+
+// One (outer, inner) pair: the five tensor components / 4.
+__device__ __forceinline__ T5 pair_tensor(const Outer& o, double rn, double zn, double rn2,
+                                          double rcpr, long long gthr,
+                                          const double2* __restrict__ logt) {
+  const PairB p = pair_core(o, rn, zn, rcpr, gthr, logt);
+  return pair_tensors(o, rn, rn2, p);
+}
+
+// One unordered pair: the direct components in `t` and, returned, the one
+// new component of the swapped pair, UD_xx(j,i) / 4 = (B1 - rn^2 B3 +
+// 2 ri rn B4 - ri^2 B5) / 4; the others are permutations of `t`.
+__device__ __forceinline__ double pair_tensor_sym(const Outer& o, double rn, double zn, double rn2,
+                                                  double rcpr, long long gthr,
+                                                  const double2* __restrict__ logt, T5& t) {
+  const PairB p = pair_core(o, rn, zn, rcpr, gthr, logt);
+  t = pair_tensors(o, rn, rn2, p);
+  const double rr2 = o.tri * rn;
+  const double xx2 = fma(-o.ri2, p.B5, fma(rr2, p.B4, fma(-rn2, p.B3, p.B1)));
+  return p.g ? xx2 : 0.0;
 }
 
 }  // namespace lb

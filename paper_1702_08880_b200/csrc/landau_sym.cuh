@@ -1,0 +1,319 @@
+// landau_sym.cuh -- symmetric all-points sweep (outer set == inner set).
+//
+// The reference evaluates every ordered pair (i, j) independently
+// (kernel.py:443-493).  Everything expensive in a pair -- d^2, P, m, x, ln x,
+// K, E, Em1, S2, S3 and B1, B3, B4, B5 -- is symmetric under i <-> j, and the
+// swapped pair's tensors are permutations of the direct ones except UD_xx
+// (SURVEY section 0 fact 4):
+//   UK_rr(j,i) = UK_rr(i,j)   UD_zz(j,i) = UD_zz(i,j)
+//   UD_xz(j,i) = UK_zr(i,j)   UK_zr(j,i) = UD_xz(i,j)
+//   UD_xx(j,i) = B1 - rj^2 B3 + 2 ri rj B4 - ri^2 B5
+// so each unordered pair is evaluated once and feeds both accumulators.
+//
+// Decomposition (points Morton-sorted, tiles of 128):
+//  * tile pairs {I, J} are enumerated by the circular schedule: row I takes
+//    partners J = I + d (mod nt), d = 1..H(I) with H = floor((nt-1)/2), plus
+//    d = nt/2 for I < nt/2 when nt is even -- every unordered tile pair once,
+//    every row the same length (balanced across CTAs and GPUs);
+//  * d = 0 is the diagonal tile, evaluated as ordered pairs (i-side only);
+//  * a work item is (row I, a segment of kSegLen consecutive d);
+//  * inside a CTA each thread owns one i of I (registers), each warp walks
+//    the 128 j of J as 4 blocks of 32 in a rotated ("diagonal") order: at
+//    step s lane l takes j = (l + s) mod 32, so the 32 lanes touch 32
+//    distinct j and the j-side accumulators travel one lane per step with a
+//    register shuffle -- no cross-lane reduction trees;
+//  * the four warps' j-side sums meet in shared memory (fixed warp order) and
+//    are written per (I, d) to HBM; the i-side sums per (I, segment);
+//  * a reduction kernel adds, per point and in a fixed order, its i-side
+//    segments and the j-side blocks of every row that has its tile as a
+//    partner.  No atomics: results are bitwise reproducible.
+#pragma once
+// (included by landau_b200.cu inside namespace lb, after the sweep helpers)
+
+constexpr int kSymTile = 128;   // points per tile (== threads per CTA)
+constexpr int kSymStages = 2;   // TMA ring depth (one J tile per stage)
+constexpr int kSegLen = 8;      // partner tiles per work item
+constexpr int kSymMinBlocks = 3;
+constexpr int kSymMaxS = 2;     // the shared-memory j-side buffer bounds S
+
+// partner count of row I (d = 1..H(I)); nt tiles
+__host__ __device__ __forceinline__ int sym_h(int I, int nt) {
+  const int h = (nt - 1) / 2;
+  return ((nt & 1) == 0 && I < nt / 2) ? h + 1 : h;
+}
+__host__ __device__ __forceinline__ int sym_hmax(int nt) { return nt / 2; }
+__host__ __device__ __forceinline__ int sym_nseg(int nt) {
+  return (sym_hmax(nt) + 1 + kSegLen - 1) / kSegLen;
+}
+
+template <int S>
+constexpr size_t sym_smem_bytes() {
+  return size_t(kSymStages) * kSymTile * rec_stride(S) * sizeof(double) +
+         size_t(2 << LB_LOGT_BITS) * sizeof(double) +
+         size_t(kSymTile / 32) * kSymTile * 5 * S * sizeof(double);
+}
+
+struct SymArgs {
+  const double* rec;  // sorted records, nt*128 x RS (padding records are inert)
+  double* iside;      // [row - row0][nseg][5S][128]
+  double* jside;      // [row - row0][hmax][5S][128]
+  int nt, row0, row1, nseg, hmax;
+  long long gthr;
+};
+
+template <int S>
+__device__ __forceinline__ void load_point(const double* rp, Outer& o, double (&gi)[S][3]) {
+  o = make_outer(rp[0], rp[1]);
+#pragma unroll
+  for (int b = 0; b < S; ++b) {
+    gi[b][0] = rp[4 + 3 * b];
+    gi[b][1] = rp[5 + 3 * b];
+    gi[b][2] = rp[6 + 3 * b];
+  }
+}
+
+template <int S>
+__global__ void __launch_bounds__(kSymTile, kSymMinBlocks) lb_symsweep_kernel(const SymArgs a) {
+  constexpr int RS = rec_stride(S);
+  constexpr int NW = kSymTile / 32;
+  extern __shared__ __align__(128) double lb_smem[];
+  __shared__ __align__(8) uint64_t full[kSymStages], empty[kSymStages];
+  double2* logt = reinterpret_cast<double2*>(lb_smem + kSymStages * kSymTile * RS);
+  double* jred = lb_smem + kSymStages * kSymTile * RS + (2 << LB_LOGT_BITS);  // [NW][128][5S]
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int nrows = a.row1 - a.row0;
+  const long long nitems = (long long)nrows * a.nseg;
+
+  for (int t = tid; t < (2 << LB_LOGT_BITS); t += kSymTile)
+    lb_smem[kSymStages * kSymTile * RS + t] = c_logt[t];
+  if (tid == 0) {
+#pragma unroll
+    for (int s = 0; s < kSymStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], NW);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  // producer cursor (thread 0): flat sequence of (item, d) tiles
+  long long p_item = blockIdx.x;
+  int p_d = -1;
+  uint32_t p_k = 0;
+  auto seg_range = [&](long long item, int& I, int& d0, int& d1) {
+    I = a.row0 + (int)(item / a.nseg);
+    const int seg = (int)(item % a.nseg);
+    d0 = seg * kSegLen;
+    d1 = min(sym_h(I, a.nt) + 1, d0 + kSegLen);
+  };
+  auto issue_next = [&]() {
+    int I, d0, d1;
+    while (p_item < nitems) {
+      seg_range(p_item, I, d0, d1);
+      if (p_d < 0) p_d = d0;
+      if (p_d < d1) break;
+      p_item += gridDim.x;  // empty segment or exhausted: next item
+      p_d = -1;
+    }
+    if (p_item >= nitems) return;
+    const uint32_t s = p_k % kSymStages;
+    if (p_k >= kSymStages) mbar_wait(&empty[s], ((p_k / kSymStages) - 1) & 1);
+    const int J = (I + p_d) % a.nt;
+    const uint32_t bytes = kSymTile * RS * sizeof(double);
+    mbar_expect_tx(&full[s], bytes);
+    bulk_g2s(lb_smem + s * (kSymTile * RS), a.rec + (size_t)J * kSymTile * RS, bytes, &full[s]);
+    ++p_k;
+    ++p_d;
+  };
+  if (tid == 0) issue_next();
+
+  uint32_t k = 0;
+  for (long long item = blockIdx.x; item < nitems; item += gridDim.x) {
+    int I, d0, d1;
+    seg_range(item, I, d0, d1);
+    if (d0 >= d1) continue;
+    Outer o;
+    double gi[S][3];
+    load_point<S>(a.rec + ((size_t)I * kSymTile + tid) * RS, o, gi);
+    double acc[S][5];
+#pragma unroll
+    for (int b = 0; b < S; ++b)
+#pragma unroll
+      for (int q = 0; q < 5; ++q) acc[b][q] = 0.0;
+
+    for (int d = d0; d < d1; ++d, ++k) {
+      if (tid == 0) issue_next();
+      const uint32_t s = k % kSymStages;
+      mbar_wait(&full[s], (k / kSymStages) & 1);
+      const double* tile = lb_smem + s * (kSymTile * RS);
+      const bool diag = (d == 0);
+#pragma unroll 1
+      for (int jb = 0; jb < kSymTile / 32; ++jb) {
+        double jacc[S][5];
+#pragma unroll
+        for (int b = 0; b < S; ++b)
+#pragma unroll
+          for (int q = 0; q < 5; ++q) jacc[b][q] = 0.0;
+#pragma unroll 1
+        for (int st = 0; st < 32; ++st) {
+          const int jl = (lane + st) & 31;
+          const double* rp = tile + (jb * 32 + jl) * RS;
+          const double2 rz = *reinterpret_cast<const double2*>(rp);
+          const double2 aux = *reinterpret_cast<const double2*>(rp + 2);
+          T5 t;
+          const double txx2 = pair_tensor_sym(o, rz.x, rz.y, aux.x, aux.y, a.gthr, logt, t);
+#pragma unroll
+          for (int b = 0; b < S; ++b) {
+            const double gr = rp[4 + 3 * b], gz = rp[5 + 3 * b], fw = rp[6 + 3 * b];
+            acc[b][0] = fma(t.xz, gz, fma(t.kr, gr, acc[b][0]));
+            acc[b][1] = fma(t.zz, gz, fma(t.zr, gr, acc[b][1]));
+            acc[b][2] = fma(fw, t.xx, acc[b][2]);
+            acc[b][3] = fma(fw, t.xz, acc[b][3]);
+            acc[b][4] = fma(fw, t.zz, acc[b][4]);
+          }
+          if (!diag) {
+            // outer j, inner i (kernel.py:411-415 with the swapped tensors)
+#pragma unroll
+            for (int b = 0; b < S; ++b) {
+              jacc[b][0] = fma(t.zr, gi[b][1], fma(t.kr, gi[b][0], jacc[b][0]));
+              jacc[b][1] = fma(t.zz, gi[b][1], fma(t.xz, gi[b][0], jacc[b][1]));
+              jacc[b][2] = fma(gi[b][2], txx2, jacc[b][2]);
+              jacc[b][3] = fma(gi[b][2], t.zr, jacc[b][3]);
+              jacc[b][4] = fma(gi[b][2], t.zz, jacc[b][4]);
+            }
+            // the accumulator of j = (lane + st + 1) mod 32 comes from lane + 1
+#pragma unroll
+            for (int b = 0; b < S; ++b)
+#pragma unroll
+              for (int q = 0; q < 5; ++q)
+                jacc[b][q] = __shfl_sync(0xffffffffu, jacc[b][q], (lane + 1) & 31);
+          }
+        }
+        if (!diag) {  // lane now holds the warp's sum for j = jb*32 + lane
+          double* dst = jred + ((size_t)warp * kSymTile + jb * 32 + lane) * (5 * S);
+#pragma unroll
+          for (int b = 0; b < S; ++b)
+#pragma unroll
+            for (int q = 0; q < 5; ++q) dst[b * 5 + q] = jacc[b][q];
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);
+      if (!diag) {
+        __syncthreads();
+        double* out = a.jside + ((size_t)(I - a.row0) * a.hmax + (d - 1)) * (5 * S) * kSymTile + tid;
+#pragma unroll
+        for (int c = 0; c < 5 * S; ++c) {
+          double v = jred[(size_t)tid * (5 * S) + c];
+#pragma unroll
+          for (int w = 1; w < NW; ++w) v = __dadd_rn(v, jred[((size_t)w * kSymTile + tid) * (5 * S) + c]);
+          out[(size_t)c * kSymTile] = v;
+        }
+        __syncthreads();
+      }
+    }
+    double* dst = a.iside + ((size_t)(I - a.row0) * a.nseg + (item % a.nseg)) * (5 * S) * kSymTile + tid;
+#pragma unroll
+    for (int b = 0; b < S; ++b)
+#pragma unroll
+      for (int q = 0; q < 5; ++q) dst[(size_t)(b * 5 + q) * kSymTile] = acc[b][q];
+  }
+}
+
+// Fixed-order reduction of one row batch into the running totals
+// tot[5S][nt*128] (SoA): per point, its own row's i-side segments (if the
+// row is in the batch), then the j-side blocks of every batch row having
+// this tile as a partner, by increasing d.
+template <int S>
+__global__ void lb_symreduce_kernel(const double* __restrict__ iside, const double* __restrict__ jside,
+                                    int nt, int row0, int row1, int nseg, int hmax, int first,
+                                    double* __restrict__ tot) {
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  const int npad = nt * kSymTile;
+  if (p >= npad) return;
+  const int P = p / kSymTile, t = p % kSymTile;
+  double v[5 * S];
+#pragma unroll
+  for (int c = 0; c < 5 * S; ++c) v[c] = first ? 0.0 : tot[(size_t)c * npad + p];
+  if (P >= row0 && P < row1) {
+    for (int sg = 0; sg < nseg; ++sg) {
+      const double* src = iside + ((size_t)(P - row0) * nseg + sg) * (5 * S) * kSymTile + t;
+      if (sg * kSegLen > sym_h(P, nt)) break;
+#pragma unroll
+      for (int c = 0; c < 5 * S; ++c) v[c] = __dadd_rn(v[c], src[(size_t)c * kSymTile]);
+    }
+  }
+  for (int d = 1; d <= hmax; ++d) {
+    const int I = (P - d + nt) % nt;
+    if (I < row0 || I >= row1 || d > sym_h(I, nt)) continue;
+    const double* src = jside + ((size_t)(I - row0) * hmax + (d - 1)) * (5 * S) * kSymTile + t;
+#pragma unroll
+    for (int c = 0; c < 5 * S; ++c) v[c] = __dadd_rn(v[c], src[(size_t)c * kSymTile]);
+  }
+#pragma unroll
+  for (int c = 0; c < 5 * S; ++c) tot[(size_t)c * npad + p] = v[c];
+}
+
+// Sorted, padded records: rec_s[p] = rec[perm[p]] for p < n, inert records
+// beyond (far away on the axis side, zero fields: they add exact zeros).
+__global__ void lb_sym_gather_kernel(int n, int npad, int RS, const int* __restrict__ perm,
+                                     const double* __restrict__ rec, double* __restrict__ rec_s) {
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= npad) return;
+  double* o = rec_s + (size_t)p * RS;
+  if (p < n) {
+    const double* src = rec + (size_t)perm[p] * RS;
+    for (int c = 0; c < RS; ++c) o[c] = src[c];
+  } else {
+    o[0] = 1.0;
+    o[1] = 1.0e6;
+    o[2] = 1.0;
+    o[3] = 1.0;
+    for (int c = 4; c < RS; ++c) o[c] = 0.0;
+  }
+}
+
+// K/D for original points [q0, q1) from the totals (sorted order) through
+// the inverse permutation; coupling as _combine (kernel.py:419-440).
+template <int S>
+__global__ void lb_sym_combine_kernel(const double* __restrict__ tot, int npad,
+                                      const int* __restrict__ inv, int q0, int q1, const Coupling cp,
+                                      double* __restrict__ K, double* __restrict__ D) {
+  const int q = q0 + blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= q1) return;
+  const int p = inv[q];
+  double A[S][5];
+#pragma unroll
+  for (int b = 0; b < S; ++b)
+#pragma unroll
+    for (int c = 0; c < 5; ++c) A[b][c] = tot[(size_t)(b * 5 + c) * npad + p];
+  const int io = q - q0;
+#pragma unroll
+  for (int a = 0; a < S; ++a) {
+    double k0 = 0.0, k1 = 0.0, d0 = 0.0, d1 = 0.0, d2 = 0.0;
+#pragma unroll
+    for (int b = 0; b < S; ++b) {
+      const double ck = cp.coK4[a * S + b], cd = cp.coD4[a * S + b];
+      k0 = __dadd_rn(k0, __dmul_rn(ck, A[b][0]));
+      k1 = __dadd_rn(k1, __dmul_rn(ck, A[b][1]));
+      d0 = __dadd_rn(d0, __dmul_rn(cd, A[b][2]));
+      d1 = __dadd_rn(d1, __dmul_rn(cd, A[b][3]));
+      d2 = __dadd_rn(d2, __dmul_rn(cd, A[b][4]));
+    }
+    double* Ko = K + ((size_t)io * S + a) * 2;
+    double* Do = D + ((size_t)io * S + a) * 4;
+    Ko[0] = k0;
+    Ko[1] = k1;
+    Do[0] = d0;
+    Do[1] = d1;
+    Do[2] = d1;
+    Do[3] = d2;
+  }
+}
+
+__global__ void lb_invert_perm_kernel(int n, const int* __restrict__ perm, int* __restrict__ inv) {
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p < n) inv[perm[p]] = p;
+}
+

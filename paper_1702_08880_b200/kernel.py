@@ -150,6 +150,13 @@ def fused_sweep(outer_r, outer_z, data, params, eps_d: float = 0.0,
         return K, D
     ctx = _lib.context()
     p = _lib.dptr
+    if nout == n and np.array_equal(ro, r) and np.array_equal(zo, z):
+        # all-points sweep (assemble_collision's call, assembly.py:148): each
+        # unordered pair is evaluated once on the device (symmetric path)
+        _lib.check(_lib.load().lb_fused_sweep_all(
+            ctx.handle, n, S, p(r), p(z), p(w), p(f), p(dfr), p(dfz), p(coK), p(coD),
+            float(eps_d), p(K), p(D)))
+        return K, D
     _lib.check(_lib.load().lb_fused_sweep(
         ctx.handle, nout, p(ro), p(zo), n, S, p(r), p(z), p(w), p(f), p(dfr), p(dfz),
         p(coK), p(coD), float(eps_d), p(K), p(D)))

@@ -7,13 +7,16 @@ fields of its own points, packs them into inner records on its device
 (`lb_pack_records_dev`), and one all-gather per operator evaluation
 replicates the packed records of every point to every rank -- the paper's
 per-point field state (w f, w grad f) plus coordinates, 10 doubles per point
-at S = 2, 5.2 MB at N = 2^16.  Each rank then sweeps its own outer points
-against all inner points (`lb_sweep_dev`).  No collective follows: the
-outputs K, D are per outer point.
-
-Because the sweep's inner chunking depends only on the global inner count
-and the record order is the global point order, every rank's K/D rows are
-bitwise identical to the single-GPU result for the same points.
+at S = 2, 5.2 MB at N = 2^16.  Then, either
+ * symmetric path (S <= 2, outer set == inner set, the default here): every
+   rank Morton-orders all records identically, evaluates its share of the
+   unordered tile pairs (each pair once, feeding both points), and one
+   all-reduce adds the ranks' 5S partial sums per point (5.2 MB); each rank
+   applies the coupling to its own points; or
+ * general path: each rank sweeps its own outer points against all inner
+   points (`lb_sweep_dev`); no collective follows.  Because the inner
+   chunking depends only on the global inner count, every rank's K/D rows
+   are bitwise identical to the single-GPU result.
 
 The reference has no distributed code; the paper ran
 redundant MPI replicas.  This layer is the B200 design
@@ -81,7 +84,8 @@ class ShardedSweep:
 
     def __init__(self, n: int, S: int, params, eps_d: float, device, align: int = 9,
                  group=None, pack_fn: Callable | None = None,
-                 sweep_fn: Callable | None = None):
+                 sweep_fn: Callable | None = None, symmetric: bool | None = None,
+                 sym_fns: tuple | None = None):
         import torch
 
         dist = _dist()
@@ -105,6 +109,20 @@ class ShardedSweep:
             self.RS = ((4 + 3 * self.S) + 1) & ~1
         self._pack = pack_fn or self._pack_cuda
         self._sweep = sweep_fn or self._sweep_cuda
+        # symmetric all-points path (each unordered pair once, tile pairs split
+        # over ranks, one all-reduce of the 5S partial sums per point)
+        if sym_fns is not None:
+            self._sym_prepare, self._sym_partial, self._sym_combine = sym_fns
+            sym_ok = True
+        else:
+            self._sym_prepare, self._sym_partial = self._sym_prepare_cuda, self._sym_partial_cuda
+            self._sym_combine = self._sym_combine_cuda
+            sym_ok = (pack_fn is None and sweep_fn is None
+                      and bool(self._lib.lb_sym_supported(self.S)) and self.n >= 128)
+        self.symmetric = sym_ok if symmetric is None else (bool(symmetric) and sym_ok)
+        if self.symmetric:
+            npad = -(-self.n // 128) * 128
+            self.tot = torch.zeros((5 * self.S, npad), dtype=torch.float64, device=self.device)
         mc = self.plan.max_count
         f64 = torch.float64
         self.send = torch.zeros((mc, self.RS), dtype=f64, device=self.device)
@@ -138,6 +156,23 @@ class ShardedSweep:
             self._stream()))
         self.launches += self._lib.lb_last_launch_count(self._ctx.handle)
 
+    def _sym_prepare_cuda(self, rec):
+        _lib.check(self._lib.lb_sym_prepare_dev(self._ctx.handle, self.n, self.S, rec.data_ptr(),
+                                                self._stream()))
+        self.launches += self._lib.lb_last_launch_count(self._ctx.handle)
+
+    def _sym_partial_cuda(self, tot):
+        _lib.check(self._lib.lb_sym_partial_dev(self._ctx.handle, self.S, self.eps_d, self.rank,
+                                                self.world, tot.data_ptr(), self._stream()))
+        self.launches += self._lib.lb_last_launch_count(self._ctx.handle)
+
+    def _sym_combine_cuda(self, tot, q0, q1, K, D):
+        p = _lib.dptr
+        _lib.check(self._lib.lb_sym_combine_dev(self._ctx.handle, self.S, tot.data_ptr(),
+                                                p(self.coK), p(self.coD), q0, q1, K.data_ptr(),
+                                                D.data_ptr(), self._stream()))
+        self.launches += self._lib.lb_last_launch_count(self._ctx.handle)
+
     # ---------------------------------------------------------------- steps
     def pack_local(self, r, z, w, f, dfr, dfz):
         """Pack this rank's points (device tensors: r,z,w (nl,), f.. (S,nl))."""
@@ -161,12 +196,37 @@ class ShardedSweep:
         self._sweep(ro, zo, self.rec, self.K, self.D)
         return self.K, self.D
 
+    def sym_prepare(self):
+        """Symmetric path, step 1: order all n gathered records (same on
+        every rank)."""
+        self._sym_prepare(self.rec[:self.n])
+
+    def sym_partial(self):
+        """Step 2: this rank's share of the unordered tile pairs -> tot."""
+        self._sym_partial(self.tot)
+
+    def sym_reduce(self):
+        """Step 3: add the ranks' partial sums (one all-reduce of 5S doubles
+        per point, 5.2 MB at N = 2^16, S = 2)."""
+        if self.world > 1:
+            _dist().all_reduce(self.tot, group=self.group)
+
+    def sym_finish(self):
+        """Step 4: coupling -> K, D for this rank's own points."""
+        self._sym_combine(self.tot, self.lo, self.hi, self.K, self.D)
+        return self.K, self.D
+
     def step(self, r, z, w, f, dfr, dfz):
         """One distributed evaluation from this rank's local fields; the local
         points are also the outer points (assemble_collision's all-points
         sweep, assembly.py:148)."""
         self.pack_local(r, z, w, f, dfr, dfz)
         self.all_gather()
+        if self.symmetric:
+            self.sym_prepare()
+            self.sym_partial()
+            self.sym_reduce()
+            return self.sym_finish()
         return self.sweep_local(r, z)
 
 

@@ -25,27 +25,90 @@ def test_dev_path_on_torch_stream_equals_host_entry(gpu):
     torch, pkg, wl, params, data = _setup(8192)
     from paper_1702_08880_b200.shard import ShardedSweep, local_fields
 
-    K0, D0 = pkg.fused_sweep(wl.r, wl.z, data, params, eps_d=wl.eps_d)
+    K0, D0 = pkg.fused_sweep(wl.r[:-1], wl.z[:-1], data, params, eps_d=wl.eps_d)
     dev = torch.device("cuda", 0)
-    sh = ShardedSweep(wl.N, wl.S, params, wl.eps_d, dev, align=1)
+    sh = ShardedSweep(wl.N, wl.S, params, wl.eps_d, dev, align=1, symmetric=False)
     f = [torch.from_numpy(a).to(dev) for a in local_fields(wl, 0, wl.N)]
     s = torch.cuda.Stream()
     with torch.cuda.stream(s):  # a non-default stream: results must be ordered on it
         K, D = sh.step(*f)
         Kh, Dh = K.cpu(), D.cpu()
     torch.cuda.synchronize()
-    assert np.array_equal(Kh.numpy(), K0) and np.array_equal(Dh.numpy(), D0)
+    assert np.array_equal(Kh.numpy()[:-1], K0) and np.array_equal(Dh.numpy()[:-1], D0)
     assert sh.launches == 7  # pack + Morton ordering (4) + sweep + combine
 
 
 @pytest.mark.parametrize("world", [2, 3, 8])
 def test_emulated_ranks_reproduce_full_result(gpu, world):
+    """General path: per-rank outer shards, run one after another on one GPU
+    (no cross-rank waiting), equal the single-call rows bitwise."""
     torch, pkg, wl, params, data = _setup(4608)
     from paper_1702_08880_b200.shard import ShardPlan
 
-    K0, D0 = pkg.fused_sweep(wl.r, wl.z, data, params, eps_d=wl.eps_d)
-    plan = ShardPlan(wl.N, world, 9)
+    half = wl.N - 1  # not the all-points call: the general (ordered-pair) path
+    K0, D0 = pkg.fused_sweep(wl.r[:half], wl.z[:half], data, params, eps_d=wl.eps_d)
+    plan = ShardPlan(half, world, 9)
     for r in range(world):
         lo, hi = plan.bounds(r)
         K, D = pkg.fused_sweep(wl.r[lo:hi], wl.z[lo:hi], data, params, eps_d=wl.eps_d)
         assert np.array_equal(K, K0[lo:hi]) and np.array_equal(D, D0[lo:hi])
+
+
+def test_symmetric_dev_path_matches_general(gpu, oracle):
+    """Symmetric all-points path (tile pairs, each unordered pair once) vs the
+    general sweep and the oracle, on a ragged N (not a multiple of 128)."""
+    torch, pkg, wl, params, data = _setup(5000)
+    from paper_1702_08880_b200.shard import ShardedSweep, local_fields
+
+    dev = torch.device("cuda", 0)
+    f = [torch.from_numpy(a).to(dev) for a in local_fields(wl, 0, wl.N)]
+    sym = ShardedSweep(wl.N, wl.S, params, wl.eps_d, dev, align=1)
+    gen = ShardedSweep(wl.N, wl.S, params, wl.eps_d, dev, align=1, symmetric=False)
+    assert sym.symmetric and not gen.symmetric
+    Ks, Ds = (t.cpu().numpy() for t in sym.step(*f))
+    Kg, Dg = (t.cpu().numpy() for t in gen.step(*f))
+    Kr, Dr = oracle.fused_sweep(wl.r, wl.z, wl.r, wl.z, wl.w, wl.f, wl.df_r, wl.df_z,
+                                wl.nu_hat, wl.mass_ratio_o, eps_d=wl.eps_d)
+    from conftest import worst_component
+
+    e_sg = worst_component(Ks, Ds, Kg, Dg)
+    e_so = worst_component(Ks, Ds, Kr, Dr)
+    print("sym vs general", e_sg, "sym vs oracle", e_so)
+    assert e_sg < 1e-12 and e_so < 1e-10
+    # deterministic run to run
+    K2, D2 = (t.cpu().numpy() for t in sym.step(*f))
+    assert np.array_equal(K2, Ks) and np.array_equal(D2, Ds)
+    # host all-points entry == device symmetric path, bitwise
+    Kh, Dh = pkg.fused_sweep(wl.r, wl.z, data, params, eps_d=wl.eps_d)
+    assert np.array_equal(Kh, Ks) and np.array_equal(Dh, Ds)
+
+
+@pytest.mark.parametrize("world", [2, 3, 8])
+def test_symmetric_rank_partials_sum_to_single(gpu, world):
+    """Emulate `world` ranks on one GPU one after another: each rank's partial
+    sums (its share of tile pairs) added on the host reproduce the
+    single-rank totals (the all-reduce the multi-GPU path performs)."""
+    torch, pkg, wl, params, data = _setup(4096 + 77)
+    from paper_1702_08880_b200 import _lib
+    from paper_1702_08880_b200.shard import ShardedSweep, local_fields
+
+    dev = torch.device("cuda", 0)
+    f = [torch.from_numpy(a).to(dev) for a in local_fields(wl, 0, wl.N)]
+    sh = ShardedSweep(wl.N, wl.S, params, wl.eps_d, dev, align=1)
+    sh.pack_local(*f)
+    sh.all_gather()
+    sh.sym_prepare()
+    sh.sym_partial()
+    full = sh.tot.clone()
+    acc = torch.zeros_like(full)
+    lib, ctx = _lib.load(), _lib.context(0)
+    st = torch.cuda.current_stream().cuda_stream
+    part = torch.empty_like(full)
+    for r in range(world):
+        _lib.check(lib.lb_sym_partial_dev(ctx.handle, wl.S, wl.eps_d, r, world, part.data_ptr(), st))
+        acc += part
+    torch.cuda.synchronize()
+    scale = full.abs().max(dim=1).values.clamp_min(1e-300)
+    err = ((acc - full).abs().max(dim=1).values / scale).max().item()
+    print(f"world={world} rank-sum vs single", err)
+    assert err < 1e-13
