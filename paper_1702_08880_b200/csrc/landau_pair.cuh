@@ -28,6 +28,10 @@
 #include <cstdint>
 #include "landau_coefs.h"
 
+#ifndef LB_ESTRIN
+#define LB_ESTRIN 0  // 1: Estrin-form polynomials (shorter dependency chains)
+#endif
+
 namespace lb {
 
 // Coefficient tables live in the constant bank so DFMA reads them as
@@ -99,6 +103,13 @@ __device__ __forceinline__ double log_table(double x, const double2* __restrict_
   const double z = __longlong_as_double(ix - (tmp & (long long)0xFFF0000000000000ULL));
   const double2 t = tab[i];  // (invc, logc)
   const double r = fma(z, t.x, -1.0);
+#if LB_ESTRIN
+  // q(r) = -1/2 + r/3 - r^2/4 + r^3/5 - r^4/6 + r^5/7 - r^6/8, depth 3
+  const double r2 = r * r;
+  const double q = fma(fma(-0.125, r2, fma(r, c_misc[1], c_misc[2])), r2 * r2,
+                       fma(fma(r, c_misc[3], -0.25), r2, fma(r, c_misc[4], -0.5)));
+  const double l1p = fma(r2, q, r);
+#else
   double q = fma(r, c_misc[0], c_misc[1]);  // -1/8 r + 1/7
   q = fma(q, r, c_misc[2]);                 // -1/6
   q = fma(q, r, c_misc[3]);                 //  1/5
@@ -106,6 +117,7 @@ __device__ __forceinline__ double log_table(double x, const double2* __restrict_
   q = fma(q, r, c_misc[4]);                 //  1/3
   q = fma(q, r, -0.5);
   const double l1p = fma(r * r, q, r);
+#endif
   // exact int -> double: 2^52 + 2^31 + k, minus the same magic
   const double kd = __longlong_as_double(0x4330000080000000LL + (long long)k) - c_misc[11];
   return fma(kd, c_misc[9], t.y + l1p);
@@ -163,6 +175,24 @@ __device__ __forceinline__ PairB pair_core(const Outer& o, double rn, double zn,
   const double m = tq * invP;
   const double lx = log_table(x, logt);
 
+#if LB_ESTRIN
+  // the reference's four degree-10 polynomials (kernel.py:351-359; QK[10] =
+  // QEx[10] = QEx[0] = 0) in Estrin form: depth 4 instead of 10, sharing
+  // x^2, x^4, x^8 -- same coefficients, re-associated evaluation
+  const double x2 = x * x, x4 = x2 * x2, x8 = x4 * x4;
+  const double pk = fma(fma(c_pk[10], x2, fma(c_pk[9], x, c_pk[8])), x8,
+                        fma(fma(fma(c_pk[7], x, c_pk[6]), x2, fma(c_pk[5], x, c_pk[4])), x4,
+                            fma(fma(c_pk[3], x, c_pk[2]), x2, fma(c_pk[1], x, c_pk[0]))));
+  const double pe = fma(fma(c_pe[10], x2, fma(c_pe[9], x, c_pe[8])), x8,
+                        fma(fma(fma(c_pe[7], x, c_pe[6]), x2, fma(c_pe[5], x, c_pe[4])), x4,
+                            fma(fma(c_pe[3], x, c_pe[2]), x2, fma(c_pe[1], x, c_pe[0]))));
+  const double qk = fma(fma(c_qk[9], x, c_qk[8]), x8,
+                        fma(fma(fma(c_qk[7], x, c_qk[6]), x2, fma(c_qk[5], x, c_qk[4])), x4,
+                            fma(fma(c_qk[3], x, c_qk[2]), x2, fma(c_qk[1], x, c_qk[0]))));
+  const double qe = x * fma(c_qe[9], x8,
+                            fma(fma(fma(c_qe[8], x, c_qe[7]), x2, fma(c_qe[6], x, c_qe[5])), x4,
+                                fma(fma(c_qe[4], x, c_qe[3]), x2, fma(c_qe[2], x, c_qe[1]))));
+#else
   // four Horner chains in x (kernel.py:351-359); QK[10] = QEx[10] = QEx[0] = 0
   double pk = fma(c_pk[10], x, c_pk[9]);
   double qk = c_qk[9];
@@ -177,6 +207,7 @@ __device__ __forceinline__ PairB pair_core(const Outer& o, double rn, double zn,
   pk = fma(pk, x, c_pk[2]);  qk = fma(qk, x, c_qk[2]);  pe = fma(pe, x, c_pe[2]);  qe = fma(qe, x, c_qe[2]);
   pk = fma(pk, x, c_pk[1]);  qk = fma(qk, x, c_qk[1]);  pe = fma(pe, x, c_pe[1]);  qe = fma(qe, x, c_qe[1]);
   pk = fma(pk, x, c_pk[0]);  qk = fma(qk, x, c_qk[0]);  pe = fma(pe, x, c_pe[0]);  qe = qe * x;
+#endif
   const double EK = fma(-lx, qk, pk);
   const double EE = fma(-lx, qe, pe);
   const double Em1 = EE * (P * rcp_nr(d2));  // E/(1-m)

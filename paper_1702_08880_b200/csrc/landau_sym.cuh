@@ -33,7 +33,14 @@
 constexpr int kSymTile = 128;   // points per tile (== threads per CTA)
 constexpr int kSymStages = 2;   // TMA ring depth (one J tile per stage)
 constexpr int kSegLen = 8;      // partner tiles per work item
-constexpr int kSymMinBlocks = 3;
+#ifndef LB_SYM_MINB
+#define LB_SYM_MINB 4
+#endif
+#ifndef LB_SYM_UNROLL
+#define LB_SYM_UNROLL 1
+#endif
+constexpr int kSymMinBlocks = LB_SYM_MINB;
+constexpr int kSymUnroll = LB_SYM_UNROLL;
 constexpr int kSymMaxS = 2;     // the shared-memory j-side buffer bounds S
 
 // partner count of row I (d = 1..H(I)); nt tiles
@@ -46,11 +53,12 @@ __host__ __device__ __forceinline__ int sym_nseg(int nt) {
   return (sym_hmax(nt) + 1 + kSegLen - 1) / kSegLen;
 }
 
+// j-side exchange buffer: 2 (double buffer) x 4 warps x 32 j x 5S doubles
 template <int S>
 constexpr size_t sym_smem_bytes() {
   return size_t(kSymStages) * kSymTile * rec_stride(S) * sizeof(double) +
          size_t(2 << LB_LOGT_BITS) * sizeof(double) +
-         size_t(kSymTile / 32) * kSymTile * 5 * S * sizeof(double);
+         size_t(2) * (kSymTile / 32) * 32 * 5 * S * sizeof(double);
 }
 
 struct SymArgs {
@@ -79,7 +87,7 @@ __global__ void __launch_bounds__(kSymTile, kSymMinBlocks) lb_symsweep_kernel(co
   extern __shared__ __align__(128) double lb_smem[];
   __shared__ __align__(8) uint64_t full[kSymStages], empty[kSymStages];
   double2* logt = reinterpret_cast<double2*>(lb_smem + kSymStages * kSymTile * RS);
-  double* jred = lb_smem + kSymStages * kSymTile * RS + (2 << LB_LOGT_BITS);  // [NW][128][5S]
+  double* jred = lb_smem + kSymStages * kSymTile * RS + (2 << LB_LOGT_BITS);  // [2][NW][32][5S]
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int nrows = a.row1 - a.row0;
@@ -155,7 +163,7 @@ __global__ void __launch_bounds__(kSymTile, kSymMinBlocks) lb_symsweep_kernel(co
         for (int b = 0; b < S; ++b)
 #pragma unroll
           for (int q = 0; q < 5; ++q) jacc[b][q] = 0.0;
-#pragma unroll 1
+#pragma unroll kSymUnroll
         for (int st = 0; st < 32; ++st) {
           const int jl = (lane + st) & 31;
           const double* rp = tile + (jb * 32 + jl) * RS;
@@ -190,28 +198,30 @@ __global__ void __launch_bounds__(kSymTile, kSymMinBlocks) lb_symsweep_kernel(co
                 jacc[b][q] = __shfl_sync(0xffffffffu, jacc[b][q], (lane + 1) & 31);
           }
         }
-        if (!diag) {  // lane now holds the warp's sum for j = jb*32 + lane
-          double* dst = jred + ((size_t)warp * kSymTile + jb * 32 + lane) * (5 * S);
+        if (!diag) {
+          // lane holds this warp's sum for j = jb*32 + lane; the four warps'
+          // sums meet in a double-buffered exchange slot and are added in
+          // fixed warp order (one CTA barrier per 32 j)
+          double* slot = jred + (size_t)(jb & 1) * NW * 32 * (5 * S);
+          double* dst = slot + ((size_t)warp * 32 + lane) * (5 * S);
 #pragma unroll
           for (int b = 0; b < S; ++b)
 #pragma unroll
             for (int q = 0; q < 5; ++q) dst[b * 5 + q] = jacc[b][q];
+          __syncthreads();
+          double* out = a.jside + ((size_t)(I - a.row0) * a.hmax + (d - 1)) * (5 * S) * kSymTile +
+                        jb * 32;
+          for (int v = tid; v < 32 * 5 * S; v += kSymTile) {
+            const int c = v >> 5, jj = v & 31;
+            double x = slot[(size_t)jj * (5 * S) + c];
+#pragma unroll
+            for (int w = 1; w < NW; ++w) x = __dadd_rn(x, slot[((size_t)w * 32 + jj) * (5 * S) + c]);
+            out[(size_t)c * kSymTile + jj] = x;
+          }
         }
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[s]);
-      if (!diag) {
-        __syncthreads();
-        double* out = a.jside + ((size_t)(I - a.row0) * a.hmax + (d - 1)) * (5 * S) * kSymTile + tid;
-#pragma unroll
-        for (int c = 0; c < 5 * S; ++c) {
-          double v = jred[(size_t)tid * (5 * S) + c];
-#pragma unroll
-          for (int w = 1; w < NW; ++w) v = __dadd_rn(v, jred[((size_t)w * kSymTile + tid) * (5 * S) + c]);
-          out[(size_t)c * kSymTile] = v;
-        }
-        __syncthreads();
-      }
     }
     double* dst = a.iside + ((size_t)(I - a.row0) * a.nseg + (item % a.nseg)) * (5 * S) * kSymTile + tid;
 #pragma unroll

@@ -15,20 +15,29 @@ from paper_1702_08880_b200.shard import ShardedSweep, local_fields  # noqa: E402
 
 
 def main():
-    n = int(sys.argv[1]) if len(sys.argv) > 1 else 65536
-    reps = int(sys.argv[2]) if len(sys.argv) > 2 else 4
+    args = [a for a in sys.argv[1:] if not a.startswith("--")]
+    n = int(args[0]) if len(args) > 0 else 65536
+    reps = int(args[1]) if len(args) > 1 else 4
     dev = torch.device("cuda", 0)
     wl = synthetic.cfg5(n)
     params = pkg.CollisionParams(nu_hat=wl.nu_hat, mass_ratio_o=wl.mass_ratio_o)
-    sh = ShardedSweep(n, wl.S, params, wl.eps_d, dev, align=1)
+    sym = "--general" not in sys.argv
+    sh = ShardedSweep(n, wl.S, params, wl.eps_d, dev, align=1, symmetric=sym)
     f = [torch.from_numpy(a).to(dev) for a in local_fields(wl, 0, n)]
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     for k in range(reps):
         sh.pack_local(*f)
         sh.all_gather()
-        e0.record()
-        sh.sweep_local(f[0], f[1])
-        e1.record()
+        if sh.symmetric:
+            sh.sym_prepare()
+            e0.record()
+            sh.sym_partial()
+            e1.record()
+            sh.sym_finish()
+        else:
+            e0.record()
+            sh.sweep_local(f[0], f[1])
+            e1.record()
         torch.cuda.synchronize()
         ms = e0.elapsed_time(e1)
         print(f"rep {k}: sweep {ms:.3f} ms, {n * n / ms / 1e6:.3e} Gpairs/s... "
