@@ -47,6 +47,7 @@ extern "C" {
 #define LB_MAX_SPECIES 8
 
 typedef struct lb_ctx lb_ctx;
+typedef struct lb_mesh lb_mesh;
 
 /* ABI version (major*100 + minor). */
 int lb_version(void);
@@ -115,6 +116,27 @@ int lb_fused_sweep_all(lb_ctx *ctx, int n, int S, const double *r, const double 
                        const double *w, const double *f, const double *df_r,
                        const double *df_z, const double *coK, const double *coD,
                        double eps_d, double *K_out, double *D_out);
+
+/* Device-resident mesh for the operator path: cell sizes, the Q2 basis
+ * tables and the gather map of the CSR scatter + hanging-node condensation
+ * (assembly.py:115-129, mesh.py:233-241), built once per mesh on the host
+ * (paper_1702_08880_b200/scatter.py): for each of the nslots stored entries
+ * of C_free = P^T C P, slot_ptr[s]..slot_ptr[s+1] index (gather_idx,
+ * gather_w) pairs = (element entry (e*9+i)*9+j, P[n_ei,p] * P[n_ej,q]). */
+int lb_mesh_create(lb_ctx *ctx, int ncell, const double *cell_sizes, const double *B,
+                   const double *dB, int nslots, const int *slot_ptr, int ncontrib,
+                   const int *gather_idx, const double *gather_w, lb_mesh **out);
+int lb_mesh_destroy(lb_mesh *mesh);
+
+/* Whole operator on the device: replaces assembly.py:148-169 (kernel,
+ * transform, contraction, scatter, condensation).  Writes the CSR values of
+ * the S species blocks, csr_out (S, nslots), in the map's pattern; K_out /
+ * D_out / phase_ms may be NULL (phase_ms as lb_assemble_elements, the last
+ * phase also covering the scatter). */
+int lb_assemble_csr(lb_ctx *ctx, const lb_mesh *mesh, int S, const double *r, const double *z,
+                    const double *w, const double *f, const double *df_r, const double *df_z,
+                    const double *coK, const double *coD, double eps_d, double *csr_out,
+                    double *K_out, double *D_out, double *phase_ms);
 
 /* Per-pair closed form on the device: replaces `axisym_tensor_pair`
  * (kernel.py:206-235) for npair independent (r, z, rbar, zbar) tuples, with

@@ -22,6 +22,7 @@ LB_OK, LB_EINVAL, LB_ECUDA, LB_ENODEV, LB_ENOMEM = 0, 1, 2, 3, 4
 MAX_SPECIES = 8
 
 _dp = C.POINTER(C.c_double)
+_ip = C.POINTER(C.c_int)
 _vp = C.c_void_p
 _i = C.c_int
 _d = C.c_double
@@ -42,6 +43,10 @@ SIGNATURES = {
     "lb_fused_sweep_all": (_i, [_vp, _i, _i, _dp, _dp, _dp, _dp, _dp, _dp, _dp, _dp, _d,
                                 _dp, _dp]),
     "lb_tensor_pairs": (_i, [_vp, _i, _dp, _dp, _dp, _dp, _dp, _dp]),
+    "lb_mesh_create": (_i, [_vp, _i, _dp, _dp, _dp, _i, _ip, _i, _ip, _dp, C.POINTER(_vp)]),
+    "lb_mesh_destroy": (_i, [_vp]),
+    "lb_assemble_csr": (_i, [_vp, _vp, _i, _dp, _dp, _dp, _dp, _dp, _dp, _dp, _dp, _d, _dp,
+                             _dp, _dp, _dp]),
     "lb_sym_supported": (_i, [_i]),
     "lb_sym_npad": (_i, [_i]),
     "lb_sym_prepare_dev": (_i, [_vp, _i, _i, _vp, _vp]),
@@ -86,6 +91,12 @@ def check(rc: int) -> None:
     if rc == LB_EINVAL:
         raise ValueError(msg)
     raise RuntimeError(f"liblandau_b200 error {rc}: {msg}")
+
+
+def iptr(a: np.ndarray):
+    """ctypes int* to a C-contiguous int32 array (caller keeps it alive)."""
+    assert a.dtype == np.int32 and a.flags.c_contiguous
+    return a.ctypes.data_as(_ip)
 
 
 def dptr(a: np.ndarray):

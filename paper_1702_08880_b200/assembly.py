@@ -1,10 +1,12 @@
 """Drop-in mirror of `axlandau.assembly.assemble_collision` on the B200.
 
-`assemble_collision` (assembly.py:132-175) = pair sweep (K1) + outer-point
-transform and 9x9 element contraction (K2), both on the device in one C-ABI
-call (`lb_assemble_elements`), followed by the reference's COO->CSR scatter
-and hanging-node condensation P^T C P on the host (assembly.py:115-129; the
-device scatter is the next row of the build plan).
+`assemble_collision` (assembly.py:132-175) runs entirely on the device in one
+C-ABI call (`lb_assemble_csr`): pair sweep (K1, symmetric all-points path),
+outer-point transform and 9x9 element contraction (K2), and the CSR scatter
+with hanging-node condensation P^T C P (K3, a per-slot gather-sum through a
+map built once per mesh by `scatter.build_gather_map`).  Only the CSR values
+come back; the host wraps them in scipy CSR matrices with the mesh's fixed
+pattern.
 
 `mesh` is duck-typed on the attributes the reference reads: n_cells, sizes,
 cell_nodes, n_nodes, prolongation (scipy CSR), domain.L.  `ref` needs Nq, B,
@@ -15,6 +17,7 @@ dB (fem.py:50-63).  `data` must come from sampling on the same mesh
 from __future__ import annotations
 
 import time
+from collections import OrderedDict
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -22,8 +25,10 @@ import scipy.sparse as sp
 
 from . import _lib
 from .kernel import _f64, _inner_fields, _n_species, coupling
+from .scatter import build_gather_map
 
-__all__ = ["CollisionMatrix", "assemble_collision", "default_eps_d", "element_matrices"]
+__all__ = ["CollisionMatrix", "DeviceMesh", "assemble_collision", "default_eps_d",
+           "device_mesh", "element_matrices"]
 
 
 def default_eps_d(mesh) -> float:
@@ -84,40 +89,100 @@ def element_matrices(mesh, ref, data, params, eps_d: float | None = None,
     return elem, phase * 1e-3
 
 
-def _scatter_indices(mesh):
-    cn = np.asarray(mesh.cell_nodes)
-    rows = np.repeat(cn, 9, axis=1).ravel()
-    cols = np.tile(cn, (1, 9)).ravel()
-    return rows, cols
+class DeviceMesh:
+    """A mesh resident on one device: cell sizes, Q2 basis tables and the
+    CSR gather map (`lb_mesh_create`)."""
+
+    def __init__(self, mesh, ref, device: int):
+        self.map = build_gather_map(mesh.cell_nodes, int(mesh.n_nodes), mesh.prolongation)
+        ctx = _lib.context(device)
+        lib = _lib.load()
+        self._lib = lib
+        self.ncell = int(mesh.n_cells)
+        sizes, B, dB = _f64(mesh.sizes), _f64(ref.B), _f64(ref.dB)
+        gm = self.map
+        h = _lib.C.c_void_p()
+        _lib.check(lib.lb_mesh_create(
+            ctx.handle, self.ncell, _lib.dptr(sizes), _lib.dptr(B), _lib.dptr(dB), gm.nnz,
+            _lib.iptr(gm.slot_ptr), int(gm.gather_idx.shape[0]), _lib.iptr(gm.gather_idx),
+            _lib.dptr(gm.gather_w), _lib.C.byref(h)))
+        self.handle = h
+
+    def close(self):
+        if getattr(self, "handle", None):
+            self._lib.lb_mesh_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):  # pragma: no cover
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
-def _condense(mesh, elem, rows, cols) -> list:
-    nn = int(mesh.n_nodes)
-    P = mesh.prolongation
-    blocks = []
-    for a in range(elem.shape[0]):
-        Cm = sp.csr_matrix((elem[a].ravel(), (rows, cols)), shape=(nn, nn))
-        blocks.append((P.T @ Cm @ P).tocsr())
-    return blocks
+_MESH_CACHE: "OrderedDict[tuple, tuple]" = OrderedDict()
+_MESH_CACHE_SIZE = 8
+
+
+def device_mesh(mesh, ref, device: int | None = None) -> DeviceMesh:
+    """Cached DeviceMesh for (mesh, ref, device).  Meshes are immutable in the
+    reference (mesh.py:54-56); the cache holds a reference to the mesh so its
+    id cannot be reused while cached."""
+    dev = _lib.current_device() if device is None else int(device)
+    key = (id(mesh), id(ref), dev)
+    hit = _MESH_CACHE.get(key)
+    if hit is not None and hit[0] is mesh and hit[1] is ref:
+        _MESH_CACHE.move_to_end(key)
+        return hit[2]
+    dm = DeviceMesh(mesh, ref, dev)
+    _MESH_CACHE[key] = (mesh, ref, dm)
+    while len(_MESH_CACHE) > _MESH_CACHE_SIZE:
+        _MESH_CACHE.popitem(last=False)
+    return dm
 
 
 def assemble_collision(mesh, ref, data, params, eps_d: float | None = None,
                        workers: int = 1) -> CollisionMatrix:
-    """C[f] per species (assembly.py:132-175) with K1/K2 on the B200.
+    """C[f] per species (assembly.py:132-175), every phase on the B200.
 
     `workers` is accepted for signature compatibility; results are bitwise
-    deterministic regardless (test_assembly.py:100-111).
+    deterministic regardless (test_assembly.py:100-111).  `timings` holds the
+    device-event times of kernel (upload + pair sweep) and fe_transform
+    (contraction + scatter + download); the host CSR wrap goes to scatter.
     """
+    if eps_d is None:
+        eps_d = default_eps_d(mesh)
+    S = _n_species(params)
+    if np.asarray(data.f).shape[0] != S:
+        raise ValueError("species count mismatch between data and params")
+    if int(ref.Nq) != 9:
+        raise ValueError("the B200 path implements the Q2 / 3x3 Gauss element (Nq = 9)")
+    ncell = int(mesh.n_cells)
+    r, z, w, f, dfr, dfz = _inner_fields(data, S)
+    if r.shape[0] != 9 * ncell:
+        raise ValueError(f"data has {r.shape[0]} points, mesh has {9 * ncell} quadrature points")
     t0 = time.perf_counter()
-    elem, phase = element_matrices(mesh, ref, data, params, eps_d=eps_d)
+    dm = device_mesh(mesh, ref)
+    gm = dm.map
+    coK, coD = coupling(params)
+    csr = np.empty((S, gm.nnz))
+    phase = np.zeros(3)
     t1 = time.perf_counter()
-    rows, cols = _scatter_indices(mesh)
-    blocks = _condense(mesh, elem, rows, cols)
+    if ncell:
+        ctx = _lib.context()
+        p = _lib.dptr
+        _lib.check(_lib.load().lb_assemble_csr(
+            ctx.handle, dm.handle, S, p(r), p(z), p(w), p(f), p(dfr), p(dfz), p(coK), p(coD),
+            float(eps_d), p(csr), None, None, p(phase)))
     t2 = time.perf_counter()
-    host = max(t1 - t0 - float(phase.sum()), 0.0)  # ctypes + staging overhead
+    n_free = gm.n_free
+    blocks = [sp.csr_matrix((csr[a], gm.indices, gm.indptr), shape=(n_free, n_free))
+              for a in range(S)]
+    t3 = time.perf_counter()
+    host = max(t2 - t1 - float(phase.sum()) * 1e-3, 0.0)
     return CollisionMatrix(
         blocks=blocks,
-        timings={"kernel": float(phase[0] + phase[1]) + host,
-                 "fe_transform": float(phase[2]),
-                 "scatter": t2 - t1},
+        timings={"kernel": float(phase[0] + phase[1]) * 1e-3 + host,
+                 "fe_transform": float(phase[2]) * 1e-3,
+                 "scatter": (t1 - t0) + (t3 - t2)},
     )

@@ -426,6 +426,25 @@ __global__ void __launch_bounds__(32 * kElemWarps) lb_elements_kernel(
   }
 }
 
+// ------------------------------------------------------------------ K3 CSR gather
+// One thread per stored slot of C_free = P^T C P: the weighted sum of the
+// element-matrix entries that land on it, in the map's fixed order
+// (scatter.py builds the map once per mesh; assembly.py:115-129 is the
+// reference's scipy COO->CSR + condensation).  HBM-bound gather.
+__global__ void lb_csr_gather_kernel(int nslots, int nent, int S, const int* __restrict__ slot_ptr,
+                                     const int* __restrict__ gidx, const double* __restrict__ gw,
+                                     const double* __restrict__ elem, double* __restrict__ out) {
+  const int slot = blockIdx.x * blockDim.x + threadIdx.x;
+  if (slot >= nslots) return;
+  const int k0 = slot_ptr[slot], k1 = slot_ptr[slot + 1];
+  for (int a = 0; a < S; ++a) {
+    const double* ea = elem + (size_t)a * nent;
+    double v = 0.0;
+    for (int k = k0; k < k1; ++k) v = fma(gw[k], ea[gidx[k]], v);
+    out[(size_t)a * nslots + slot] = v;
+  }
+}
+
 // ------------------------------------------------------------------ per-pair
 __global__ void lb_pairs_kernel(int npair, const double* __restrict__ r, const double* __restrict__ z,
                                 const double* __restrict__ rb, const double* __restrict__ zb,
@@ -502,6 +521,16 @@ struct lb_ctx {
   // symmetric all-points sweep state (lb_sym_*): sorted records, order, partials
   lb::DevBuf symord, symrec, syminv, symi, symj, symtot;
   int sym_n = -1, sym_S = 0, sym_nt = 0;
+};
+
+struct lb_mesh {
+  int device = 0;
+  int ncell = 0, nslots = 0, ncontrib = 0;
+  double* sizes = nullptr;    // (ncell, 2)
+  double* basis = nullptr;    // B (81) then dB (162)
+  int* slot_ptr = nullptr;    // (nslots + 1)
+  int* gidx = nullptr;        // (ncontrib)
+  double* gw = nullptr;       // (ncontrib)
 };
 
 namespace lb {
@@ -1120,6 +1149,120 @@ int lb_sym_combine_dev(lb_ctx* ctx, int S, const double* tot, const double* coK,
   Coupling cp;
   make_coupling(S, coK, coD, cp);
   return sym_combine_dispatch(ctx, S, tot, cp, q0, q1, K_out, D_out, (cudaStream_t)stream);
+}
+
+int lb_mesh_create(lb_ctx* ctx, int ncell, const double* cell_sizes, const double* B,
+                   const double* dB, int nslots, const int* slot_ptr, int ncontrib,
+                   const int* gather_idx, const double* gather_w, lb_mesh** out) {
+  int rc = use_ctx(ctx);
+  if (rc) return rc;
+  if (!out) return fail(LB_EINVAL, "null output pointer");
+  *out = nullptr;
+  if (ncell < 0 || nslots < 0 || ncontrib < 0) return fail(LB_EINVAL, "negative size");
+  if (!cell_sizes || !B || !dB || !slot_ptr || (ncontrib && (!gather_idx || !gather_w)))
+    return fail(LB_EINVAL, "null argument");
+  lb_mesh* m = new lb_mesh();
+  m->device = ctx->device;
+  m->ncell = ncell;
+  m->nslots = nslots;
+  m->ncontrib = ncontrib;
+  cudaError_t e = cudaSuccess;
+  auto alloc = [&](void** p, size_t b) {
+    if (e == cudaSuccess) e = cudaMalloc(p, std::max<size_t>(b, 8));
+  };
+  alloc((void**)&m->sizes, sizeof(double) * 2 * ncell);
+  alloc((void**)&m->basis, sizeof(double) * 243);
+  alloc((void**)&m->slot_ptr, sizeof(int) * (nslots + 1));
+  alloc((void**)&m->gidx, sizeof(int) * ncontrib);
+  alloc((void**)&m->gw, sizeof(double) * ncontrib);
+  if (e == cudaSuccess) e = cudaMemcpy(m->sizes, cell_sizes, sizeof(double) * 2 * ncell, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMemcpy(m->basis, B, sizeof(double) * 81, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMemcpy(m->basis + 81, dB, sizeof(double) * 162, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMemcpy(m->slot_ptr, slot_ptr, sizeof(int) * (nslots + 1), cudaMemcpyHostToDevice);
+  if (e == cudaSuccess && ncontrib) e = cudaMemcpy(m->gidx, gather_idx, sizeof(int) * ncontrib, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess && ncontrib) e = cudaMemcpy(m->gw, gather_w, sizeof(double) * ncontrib, cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) {
+    lb_mesh_destroy(m);
+    cudaGetLastError();
+    return fail(e == cudaErrorMemoryAllocation ? LB_ENOMEM : LB_ECUDA,
+                std::string("lb_mesh_create: ") + cudaGetErrorString(e));
+  }
+  *out = m;
+  return LB_OK;
+}
+
+int lb_mesh_destroy(lb_mesh* m) {
+  if (!m) return LB_OK;
+  cudaSetDevice(m->device);
+  for (void* p : {(void*)m->sizes, (void*)m->basis, (void*)m->slot_ptr, (void*)m->gidx, (void*)m->gw})
+    if (p) cudaFree(p);
+  delete m;
+  return LB_OK;
+}
+
+int lb_assemble_csr(lb_ctx* ctx, const lb_mesh* mesh, int S, const double* r, const double* z,
+                    const double* w, const double* f, const double* df_r, const double* df_z,
+                    const double* coK, const double* coD, double eps_d, double* csr_out,
+                    double* K_out, double* D_out, double* phase_ms) {
+  int rc = use_ctx(ctx);
+  if (rc) return rc;
+  if ((rc = check_species(S))) return rc;
+  if (!mesh || mesh->device != ctx->device) return fail(LB_EINVAL, "mesh handle missing or on another device");
+  const int ncell = mesh->ncell, n = 9 * ncell;
+  if (ncell == 0) return LB_OK;
+  if (!r || !z || !w || !f || !df_r || !df_z || !coK || !coD || !csr_out)
+    return fail(LB_EINVAL, "null argument");
+  cudaStream_t st = ctx->stream;
+  const size_t nin = (size_t)(3 + 3 * S) * n;
+  if ((rc = ensure(ctx->in, nin * sizeof(double)))) return rc;
+  if ((rc = ensure(ctx->rec, (size_t)n * rec_stride(S) * sizeof(double)))) return rc;
+  if ((rc = ensure(ctx->out, (size_t)6 * S * n * sizeof(double)))) return rc;
+  if ((rc = ensure(ctx->elem, ((size_t)81 * S * ncell + (size_t)S * mesh->nslots) * sizeof(double))))
+    return rc;
+  double* din = static_cast<double*>(ctx->in.p);
+  double *dr = din, *dz = dr + n, *dw = dz + n, *df = dw + n, *dfr = df + (size_t)S * n,
+         *dfz = dfr + (size_t)S * n;
+  double* dK = static_cast<double*>(ctx->out.p);
+  double* dD = dK + (size_t)2 * S * n;
+  double* delem = static_cast<double*>(ctx->elem.p);
+  double* dcsr = delem + (size_t)81 * S * ncell;
+  const size_t bn = sizeof(double) * n, bsn = sizeof(double) * S * n;
+  LB_CUDA(cudaEventRecord(ctx->ev[0], st));
+  LB_CUDA(cudaMemcpyAsync(dr, r, bn, cudaMemcpyHostToDevice, st));
+  LB_CUDA(cudaMemcpyAsync(dz, z, bn, cudaMemcpyHostToDevice, st));
+  LB_CUDA(cudaMemcpyAsync(dw, w, bn, cudaMemcpyHostToDevice, st));
+  LB_CUDA(cudaMemcpyAsync(df, f, bsn, cudaMemcpyHostToDevice, st));
+  LB_CUDA(cudaMemcpyAsync(dfr, df_r, bsn, cudaMemcpyHostToDevice, st));
+  LB_CUDA(cudaMemcpyAsync(dfz, df_z, bsn, cudaMemcpyHostToDevice, st));
+  double* drec = static_cast<double*>(ctx->rec.p);
+  if ((rc = launch_pack(ctx, n, S, dr, dz, dw, df, dfr, dfz, drec, st))) return rc;
+  LB_CUDA(cudaEventRecord(ctx->ev[1], st));
+  Coupling cp;
+  make_coupling(S, coK, coD, cp);
+  if ((rc = all_points_sweep(ctx, n, S, drec, dr, dz, cp, mask_threshold(eps_d), dK, dD, st)))
+    return rc;
+  LB_CUDA(cudaEventRecord(ctx->ev[2], st));
+  if ((rc = launch_elements(ctx, ncell, S, mesh->sizes, dw, dK, dD, mesh->basis, mesh->basis + 81,
+                            delem, st)))
+    return rc;
+  if (mesh->nslots) {
+    lb_csr_gather_kernel<<<(mesh->nslots + 255) / 256, 256, 0, st>>>(
+        mesh->nslots, 81 * ncell, S, mesh->slot_ptr, mesh->gidx, mesh->gw, delem, dcsr);
+    LB_CUDA(cudaGetLastError());
+  }
+  LB_CUDA(cudaMemcpyAsync(csr_out, dcsr, sizeof(double) * S * mesh->nslots, cudaMemcpyDeviceToHost, st));
+  if (K_out) LB_CUDA(cudaMemcpyAsync(K_out, dK, sizeof(double) * 2 * S * n, cudaMemcpyDeviceToHost, st));
+  if (D_out) LB_CUDA(cudaMemcpyAsync(D_out, dD, sizeof(double) * 4 * S * n, cudaMemcpyDeviceToHost, st));
+  LB_CUDA(cudaEventRecord(ctx->ev[3], st));
+  LB_CUDA(cudaStreamSynchronize(st));
+  if (phase_ms) {
+    float t = 0.f;
+    for (int p = 0; p < 3; ++p) {
+      LB_CUDA(cudaEventElapsedTime(&t, ctx->ev[p], ctx->ev[p + 1]));
+      phase_ms[p] = t;
+    }
+  }
+  return LB_OK;
 }
 
 int lb_tensor_pairs(lb_ctx* ctx, int npair, const double* r, const double* z, const double* rbar,

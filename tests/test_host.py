@@ -102,3 +102,28 @@ def test_install_patches_every_importer():
     finally:
         for k in [k for k in sys.modules if k == "fakeax" or k.startswith("fakeax.")]:
             del sys.modules[k]
+
+
+@pytest.mark.parametrize("case", ["cfg1", "hanging", "cfg2"])
+def test_gather_map_reproduces_scipy_condensation(case):
+    """The per-mesh CSR gather map (device scatter K3) evaluated on the host
+    equals the reference's COO->CSR + P^T C P (assembly.py:115-129) on the
+    reference's own element matrices, with the same sparsity pattern."""
+    from conftest import blocks_from, csr_from, golden
+    from oracle import oracle as O
+    from paper_1702_08880_b200.scatter import build_gather_map
+
+    g = golden(case)
+    P = csr_from(g, "mesh_P")
+    gm = build_gather_map(g["mesh_cell_nodes"], int(g["mesh_n_nodes"]), P)
+    elem = O.element_matrices(g["K"], g["D"], g["w"], g["mesh_sizes"], g["ref_B"], g["ref_dB"])
+    mine = gm.apply(elem)
+    ref = O.condense(elem, g["mesh_cell_nodes"], int(g["mesh_n_nodes"]), P)
+    for x, y, z in zip(mine, ref, blocks_from(g)):
+        assert x.nnz == z.nnz
+        assert np.array_equal(np.sort(x.indices), np.sort(z.indices))
+        yd = y.toarray()
+        assert np.abs(x.toarray() - yd).max() <= 1e-14 * np.abs(yd).max()
+        assert np.abs(x.toarray() - z.toarray()).max() <= 1e-13 * np.abs(z.toarray()).max()
+    assert gm.slot_ptr[-1] == gm.gather_idx.shape[0]
+    assert gm.gather_idx.max() < elem[0].size
