@@ -791,7 +791,10 @@ int sym_partial_dispatch(lb_ctx* ctx, int S, long long gthr, int rank, int world
   switch (S) {
     case 1: return sym_partial<1>(ctx, gthr, rank, world, tot, st);
     case 2: return sym_partial<2>(ctx, gthr, rank, world, tot, st);
-    default: return fail(LB_EINVAL, "symmetric sweep supports S <= 2");
+#if LB_SYM_MAXS >= 3
+    case 3: return sym_partial<3>(ctx, gthr, rank, world, tot, st);
+#endif
+    default: return fail(LB_EINVAL, "symmetric sweep supports S <= " + std::to_string(kSymMaxS));
   }
 }
 
@@ -800,7 +803,10 @@ int sym_combine_dispatch(lb_ctx* ctx, int S, const double* tot, const Coupling& 
   switch (S) {
     case 1: return sym_combine<1>(ctx, tot, cp, q0, q1, K, D, st);
     case 2: return sym_combine<2>(ctx, tot, cp, q0, q1, K, D, st);
-    default: return fail(LB_EINVAL, "symmetric sweep supports S <= 2");
+#if LB_SYM_MAXS >= 3
+    case 3: return sym_combine<3>(ctx, tot, cp, q0, q1, K, D, st);
+#endif
+    default: return fail(LB_EINVAL, "symmetric sweep supports S <= " + std::to_string(kSymMaxS));
   }
 }
 
@@ -1125,7 +1131,8 @@ int lb_sym_npad(int n) { return ((std::max(n, 0) + kSymTile - 1) / kSymTile) * k
 int lb_sym_prepare_dev(lb_ctx* ctx, int n, int S, const double* rec, void* stream) {
   int rc = use_ctx(ctx);
   if (rc) return rc;
-  if (!lb_sym_supported(S)) return fail(LB_EINVAL, "symmetric sweep supports 1 <= S <= 2");
+  if (!lb_sym_supported(S))
+    return fail(LB_EINVAL, "symmetric sweep supports 1 <= S <= " + std::to_string(kSymMaxS));
   if (n < 1) return fail(LB_EINVAL, "symmetric sweep needs n >= 1");
   return sym_prepare(ctx, n, S, rec, (cudaStream_t)stream);
 }

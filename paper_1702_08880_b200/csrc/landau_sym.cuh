@@ -41,7 +41,10 @@ constexpr int kSegLen = 8;      // partner tiles per work item
 #endif
 constexpr int kSymMinBlocks = LB_SYM_MINB;
 constexpr int kSymUnroll = LB_SYM_UNROLL;
-constexpr int kSymMaxS = 2;     // the shared-memory j-side buffer bounds S
+#ifndef LB_SYM_MAXS
+#define LB_SYM_MAXS 3  // measured: S = 4 symmetric (210 regs, 2 CTAs/SM) loses to the general sweep
+#endif
+constexpr int kSymMaxS = LB_SYM_MAXS;  // register / shared-memory budget bounds S
 
 // partner count of row I (d = 1..H(I)); nt tiles
 __host__ __device__ __forceinline__ int sym_h(int I, int nt) {
@@ -81,7 +84,7 @@ __device__ __forceinline__ void load_point(const double* rp, Outer& o, double (&
 }
 
 template <int S>
-__global__ void __launch_bounds__(kSymTile, kSymMinBlocks) lb_symsweep_kernel(const SymArgs a) {
+__global__ void __launch_bounds__(kSymTile, S <= 2 ? kSymMinBlocks : 2) lb_symsweep_kernel(const SymArgs a) {
   constexpr int RS = rec_stride(S);
   constexpr int NW = kSymTile / 32;
   extern __shared__ __align__(128) double lb_smem[];

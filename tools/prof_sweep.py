@@ -19,7 +19,12 @@ def main():
     n = int(args[0]) if len(args) > 0 else 65536
     reps = int(args[1]) if len(args) > 1 else 4
     dev = torch.device("cuda", 0)
-    wl = synthetic.cfg5(n)
+    S = int(next((a.split("=")[1] for a in sys.argv if a.startswith("--S=")), 2))
+    sp = synthetic.CFG5_SPECIES if S == 2 else tuple(
+        synthetic.SpeciesSpec(f"s{k}", m, q, T) for k, (m, q, T) in enumerate(
+            [(1.0, -1.0, 1.0), (3670.0, 1.0, 1.0), (21900.0, 6.0, 0.5), (335000.0, 10.0, 0.5),
+             (2.0, 1.0, 1.0), (3.0, 1.0, 1.0), (4.0, 1.0, 1.0), (5.0, 1.0, 1.0)][:S]))
+    wl = synthetic.cfg5(n, species=sp)
     params = pkg.CollisionParams(nu_hat=wl.nu_hat, mass_ratio_o=wl.mass_ratio_o)
     sym = "--general" not in sys.argv
     sh = ShardedSweep(n, wl.S, params, wl.eps_d, dev, align=1, symmetric=sym)
@@ -41,7 +46,8 @@ def main():
         torch.cuda.synchronize()
         ms = e0.elapsed_time(e1)
         print(f"rep {k}: sweep {ms:.3f} ms, {n * n / ms / 1e6:.3e} Gpairs/s... "
-              f"model {pkg.flop_count(n, wl.S, n) / ms / 1e9:.2f} TFLOP/s")
+              f"model {pkg.flop_count(n, wl.S, n) / ms / 1e9:.2f} TFLOP/s, S={wl.S}, "
+              f"{'symmetric' if sh.symmetric else 'general'}")
 
 
 if __name__ == "__main__":
