@@ -138,6 +138,30 @@ int lb_assemble_csr(lb_ctx *ctx, const lb_mesh *mesh, int S, const double *r, co
                     const double *coK, const double *coD, double eps_d, double *csr_out,
                     double *K_out, double *D_out, double *phase_ms);
 
+/* Sampling geometry of a mesh (fem.py:84-113, mesh.py:54-106): cell
+ * origins (ncell,2), reference quadrature points qpts (9,2) / weights qwts
+ * (9), cell_nodes (ncell,9), and the prolongation P (n_nodes x n_free) as
+ * CSR (P_ptr (n_nodes+1), P_idx, P_w). */
+int lb_mesh_set_geometry(lb_mesh *mesh, const double *origins, const double *qpts,
+                         const double *qwts, const int *cell_nodes, int n_nodes, int n_free,
+                         const int *P_ptr, const int *P_idx, const double *P_w);
+
+/* Device `sample_state` (fem.py:170-199) for cells [c0, c1): coeffs
+ * (S, n_free) on the device -> r, z, w (9*(c1-c0)) and f, df_r, df_z
+ * (S, 9*(c1-c0)), the QuadPointData layout of those cells' points (what
+ * each rank feeds into the all-gather). */
+int lb_sample_state_dev(lb_ctx *ctx, const lb_mesh *mesh, int S, int c0, int c1,
+                        const double *coeffs, double *r, double *z, double *w, double *f,
+                        double *df_r, double *df_z, void *stream);
+
+/* State-level operator: replaces solver._assemble_at (solver.py:81-84) =
+ * sample_state + assemble_collision.  Host coeffs (S, n_free) in, CSR
+ * values csr_out (S, nslots) out; data_out ((3+3S) x 9*ncell: r, z, w, f,
+ * df_r, df_z) and phase_ms may be NULL. */
+int lb_assemble_state(lb_ctx *ctx, const lb_mesh *mesh, int S, const double *coeffs,
+                      const double *coK, const double *coD, double eps_d, double *csr_out,
+                      double *data_out, double *phase_ms);
+
 /* Per-pair closed form on the device: replaces `axisym_tensor_pair`
  * (kernel.py:206-235) for npair independent (r, z, rbar, zbar) tuples, with
  * the same device arithmetic the sweep uses.  UK, UD: (npair, 2, 2).

@@ -15,7 +15,14 @@ point sharding with an NCCL all-gather of the field state lives in
 `paper_1702_08880_b200.shard`.
 """
 
-from .assembly import CollisionMatrix, assemble_collision, default_eps_d, element_matrices
+from .assembly import (
+    CollisionMatrix,
+    assemble_at,
+    assemble_collision,
+    default_eps_d,
+    element_matrices,
+    sample_state,
+)
 from .kernel import (
     Accumulators,
     CollisionParams,
@@ -34,9 +41,15 @@ __version__ = "0.1.0"
 _PATCH = {
     "kernel": ("fused_sweep", "fused_inner_loop"),
     "assembly": ("fused_sweep", "assemble_collision"),
-    "solver": ("assemble_collision",),
+    "solver": ("assemble_collision", "_assemble_at"),
     "cli": ("assemble_collision", "fused_sweep"),
 }
+
+
+def _assemble_at_cfg(mesh, ref, state, params, cfg):
+    """solver._assemble_at signature (solver.py:81-84): device sampling +
+    operator in one call."""
+    return assemble_at(mesh, ref, state, params, eps_d=getattr(cfg, "eps_d", None))
 
 
 def install(axlandau_pkg) -> dict:
@@ -49,7 +62,7 @@ def install(axlandau_pkg) -> dict:
     import importlib
 
     here = {"fused_sweep": fused_sweep, "fused_inner_loop": fused_inner_loop,
-            "assemble_collision": assemble_collision}
+            "assemble_collision": assemble_collision, "_assemble_at": _assemble_at_cfg}
     saved = {}
     for mod_name, names in _PATCH.items():
         mod = importlib.import_module(f"{axlandau_pkg.__name__}.{mod_name}")
@@ -75,7 +88,7 @@ def uninstall(axlandau_pkg, saved: dict) -> None:
 
 __all__ = [
     "Accumulators", "CollisionMatrix", "CollisionParams", "LandauTensorPair",
-    "QuadPointData", "assemble_collision", "axisym_tensor_pair", "axisym_tensor_pairs",
+    "QuadPointData", "assemble_at", "assemble_collision", "sample_state", "axisym_tensor_pair", "axisym_tensor_pairs",
     "coupling", "default_eps_d", "element_matrices", "flop_count", "fused_inner_loop",
     "fused_sweep", "install", "uninstall",
 ]

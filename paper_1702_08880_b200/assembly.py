@@ -27,8 +27,8 @@ from . import _lib
 from .kernel import _f64, _inner_fields, _n_species, coupling
 from .scatter import build_gather_map
 
-__all__ = ["CollisionMatrix", "DeviceMesh", "assemble_collision", "default_eps_d",
-           "device_mesh", "element_matrices"]
+__all__ = ["CollisionMatrix", "DeviceMesh", "assemble_at", "assemble_collision",
+           "default_eps_d", "device_mesh", "element_matrices", "sample_state"]
 
 
 def default_eps_d(mesh) -> float:
@@ -107,6 +107,20 @@ class DeviceMesh:
             _lib.iptr(gm.slot_ptr), int(gm.gather_idx.shape[0]), _lib.iptr(gm.gather_idx),
             _lib.dptr(gm.gather_w), _lib.C.byref(h)))
         self.handle = h
+        self.n_free = gm.n_free
+        self.has_geometry = all(hasattr(mesh, a) for a in ("origins",)) and all(
+            hasattr(ref, a) for a in ("qpts", "qwts"))
+        if self.has_geometry:  # enables device sampling (sample_state / assemble_at)
+            P = sp.csr_matrix(mesh.prolongation)
+            P.sum_duplicates()
+            ptr = np.ascontiguousarray(P.indptr, dtype=np.int32)
+            idx = np.ascontiguousarray(P.indices, dtype=np.int32)
+            pw = _f64(P.data)
+            cn = np.ascontiguousarray(mesh.cell_nodes, dtype=np.int32)
+            _lib.check(lib.lb_mesh_set_geometry(
+                h, _lib.dptr(_f64(mesh.origins)), _lib.dptr(_f64(ref.qpts)),
+                _lib.dptr(_f64(ref.qwts)), _lib.iptr(cn), int(mesh.n_nodes), P.shape[1],
+                _lib.iptr(ptr), _lib.iptr(idx), _lib.dptr(pw)))
 
     def close(self):
         if getattr(self, "handle", None):
@@ -186,3 +200,83 @@ def assemble_collision(mesh, ref, data, params, eps_d: float | None = None,
                  "fe_transform": float(phase[2]) * 1e-3,
                  "scatter": (t1 - t0) + (t3 - t2)},
     )
+
+
+def _coeffs(state, S_expected: int | None, n_free: int) -> np.ndarray:
+    c = np.atleast_2d(np.ascontiguousarray(getattr(state, "coeffs", state), dtype=np.float64))
+    if c.shape[1] != n_free:
+        raise ValueError(f"state has {c.shape[1]} dofs, mesh has {n_free} free nodes")
+    if S_expected is not None and c.shape[0] != S_expected:
+        raise ValueError("species count mismatch between state and params")
+    return c
+
+
+def assemble_at(mesh, ref, state, params, eps_d: float | None = None,
+                return_data: bool = False):
+    """State-level operator: `solver._assemble_at` (solver.py:81-84) =
+    `sample_state` + `assemble_collision`, in one device call
+    (`lb_assemble_state`): nodal coefficients in, CSR blocks out."""
+    if eps_d is None:
+        eps_d = default_eps_d(mesh)
+    S = _n_species(params)
+    dm = device_mesh(mesh, ref)
+    if not dm.has_geometry:
+        raise ValueError("mesh/ref lack origins/qpts/qwts needed for device sampling")
+    c = _coeffs(state, S, dm.n_free)
+    gm = dm.map
+    coK, coD = coupling(params)
+    csr = np.empty((S, gm.nnz))
+    n = 9 * dm.ncell
+    data = np.empty((3 + 3 * S, n)) if return_data else None
+    phase = np.zeros(3)
+    t0 = time.perf_counter()
+    if dm.ncell:
+        ctx = _lib.context()
+        p = _lib.dptr
+        _lib.check(_lib.load().lb_assemble_state(
+            ctx.handle, dm.handle, S, p(c), p(coK), p(coD), float(eps_d), p(csr),
+            p(data) if return_data else None, p(phase)))
+    t1 = time.perf_counter()
+    blocks = [sp.csr_matrix((csr[a], gm.indices, gm.indptr), shape=(gm.n_free, gm.n_free))
+              for a in range(S)]
+    t2 = time.perf_counter()
+    host = max(t1 - t0 - float(phase.sum()) * 1e-3, 0.0)
+    cm = CollisionMatrix(blocks=blocks, timings={
+        "kernel": float(phase[0] + phase[1]) * 1e-3 + host,
+        "fe_transform": float(phase[2]) * 1e-3, "scatter": t2 - t1})
+    if return_data:
+        from .kernel import QuadPointData
+
+        qd = QuadPointData(N=n, r=data[0], z=data[1], w=data[2], f=data[3:3 + S],
+                           df_r=data[3 + S:3 + 2 * S], df_z=data[3 + 2 * S:3 + 3 * S])
+        return cm, qd
+    return cm
+
+
+def sample_state(mesh, ref, state):
+    """Device `sample_state` (fem.py:170-199): QuadPointData of the state at
+    all quadrature points (r, z, w bitwise the reference's)."""
+    import torch
+
+    dm = device_mesh(mesh, ref)
+    if not dm.has_geometry:
+        raise ValueError("mesh/ref lack origins/qpts/qwts needed for device sampling")
+    c = _coeffs(state, None, dm.n_free)
+    S = c.shape[0]
+    n = 9 * dm.ncell
+    dev = torch.device("cuda", _lib.current_device())
+    dc = torch.from_numpy(c).to(dev)
+    out = torch.empty((3 + 3 * S, n), dtype=torch.float64, device=dev)
+    if n:
+        ctx = _lib.context(dev.index)
+        o = out.data_ptr()
+        row = 8 * n
+        _lib.check(_lib.load().lb_sample_state_dev(
+            ctx.handle, dm.handle, S, 0, dm.ncell, dc.data_ptr(), o, o + row, o + 2 * row,
+            o + 3 * row, o + (3 + S) * row, o + (3 + 2 * S) * row,
+            torch.cuda.current_stream(dev).cuda_stream))
+    h = out.cpu().numpy()
+    from .kernel import QuadPointData
+
+    return QuadPointData(N=n, r=h[0], z=h[1], w=h[2], f=h[3:3 + S], df_r=h[3 + S:3 + 2 * S],
+                         df_z=h[3 + 2 * S:3 + 3 * S])

@@ -445,6 +445,51 @@ __global__ void lb_csr_gather_kernel(int nslots, int nent, int S, const int* __r
   }
 }
 
+// ------------------------------------------------------------------ K4 sampling
+// sample_state (fem.py:170-199) + element_geometry (fem.py:103-113) on the
+// device: one thread per quadrature point (e, q) of cells [c0, c1).
+// Coordinates / weights use the reference's exact operation order (no
+// contraction), so r, z, w are bitwise those of the reference; nodal values
+// go through the prolongation rows (hanging nodes: 3 weights).
+__global__ void lb_sample_kernel(int c0, int c1, int S, int n_free, const double* __restrict__ origins,
+                                 const double* __restrict__ sizes, const double* __restrict__ qgeo,
+                                 const double* __restrict__ basis, const int* __restrict__ cell_nodes,
+                                 const int* __restrict__ P_ptr, const int* __restrict__ P_idx,
+                                 const double* __restrict__ P_w, const double* __restrict__ coeffs,
+                                 double* __restrict__ r, double* __restrict__ z, double* __restrict__ w,
+                                 double* __restrict__ f, double* __restrict__ dfr,
+                                 double* __restrict__ dfz) {
+  const int nloc = 9 * (c1 - c0);
+  const int pl = blockIdx.x * blockDim.x + threadIdx.x;
+  if (pl >= nloc) return;
+  const int e = c0 + pl / 9, q = pl % 9;
+  const double sr = sizes[2 * e], sz = sizes[2 * e + 1];
+  // coords = origins + (qpts + 1) * 0.5 * sizes (fem.py:109-111)
+  const double rq = __dadd_rn(origins[2 * e], __dmul_rn(__dmul_rn(__dadd_rn(qgeo[2 * q], 1.0), 0.5), sr));
+  const double zq =
+      __dadd_rn(origins[2 * e + 1], __dmul_rn(__dmul_rn(__dadd_rn(qgeo[2 * q + 1], 1.0), 0.5), sz));
+  const double detJ = __ddiv_rn(__dmul_rn(sr, sz), 4.0);   // fem.py:105
+  r[pl] = rq;
+  z[pl] = zq;
+  w[pl] = __dmul_rn(__dmul_rn(qgeo[18 + q], detJ), rq);   // fem.py:112
+  const double jr = __ddiv_rn(2.0, sr), jz = __ddiv_rn(2.0, sz);  // fem.py:107-108
+  for (int s = 0; s < S; ++s) {
+    const double* cs = coeffs + (size_t)s * n_free;
+    double fv = 0.0, gr = 0.0, gz = 0.0;
+    for (int i = 0; i < 9; ++i) {
+      const int node = cell_nodes[9 * e + i];
+      double v = 0.0;  // (P @ coeffs^T)[node] (fem.py:182)
+      for (int k = P_ptr[node]; k < P_ptr[node + 1]; ++k) v = __dadd_rn(v, __dmul_rn(P_w[k], cs[P_idx[k]]));
+      fv = fma(v, basis[9 * i + q], fv);
+      gr = fma(v, basis[81 + 2 * (9 * i + q)], gr);
+      gz = fma(v, basis[81 + 2 * (9 * i + q) + 1], gz);
+    }
+    f[(size_t)s * nloc + pl] = fv;
+    dfr[(size_t)s * nloc + pl] = __dmul_rn(gr, jr);  // fem.py:188-189
+    dfz[(size_t)s * nloc + pl] = __dmul_rn(gz, jz);
+  }
+}
+
 // ------------------------------------------------------------------ per-pair
 __global__ void lb_pairs_kernel(int npair, const double* __restrict__ r, const double* __restrict__ z,
                                 const double* __restrict__ rb, const double* __restrict__ zb,
@@ -531,6 +576,14 @@ struct lb_mesh {
   int* slot_ptr = nullptr;    // (nslots + 1)
   int* gidx = nullptr;        // (ncontrib)
   double* gw = nullptr;       // (ncontrib)
+  // sampling geometry (lb_mesh_set_geometry)
+  int n_nodes = 0, n_free = 0, nnzP = 0;
+  double* origins = nullptr;  // (ncell, 2)
+  double* qgeo = nullptr;     // qpts (9, 2) then qwts (9)
+  int* cell_nodes = nullptr;  // (ncell, 9)
+  int* P_ptr = nullptr;       // (n_nodes + 1)
+  int* P_idx = nullptr;       // (nnzP)
+  double* P_w = nullptr;      // (nnzP)
 };
 
 namespace lb {
@@ -1201,7 +1254,9 @@ int lb_mesh_create(lb_ctx* ctx, int ncell, const double* cell_sizes, const doubl
 int lb_mesh_destroy(lb_mesh* m) {
   if (!m) return LB_OK;
   cudaSetDevice(m->device);
-  for (void* p : {(void*)m->sizes, (void*)m->basis, (void*)m->slot_ptr, (void*)m->gidx, (void*)m->gw})
+  for (void* p : {(void*)m->sizes, (void*)m->basis, (void*)m->slot_ptr, (void*)m->gidx, (void*)m->gw,
+                  (void*)m->origins, (void*)m->qgeo, (void*)m->cell_nodes, (void*)m->P_ptr,
+                  (void*)m->P_idx, (void*)m->P_w})
     if (p) cudaFree(p);
   delete m;
   return LB_OK;
@@ -1260,6 +1315,125 @@ int lb_assemble_csr(lb_ctx* ctx, const lb_mesh* mesh, int S, const double* r, co
   LB_CUDA(cudaMemcpyAsync(csr_out, dcsr, sizeof(double) * S * mesh->nslots, cudaMemcpyDeviceToHost, st));
   if (K_out) LB_CUDA(cudaMemcpyAsync(K_out, dK, sizeof(double) * 2 * S * n, cudaMemcpyDeviceToHost, st));
   if (D_out) LB_CUDA(cudaMemcpyAsync(D_out, dD, sizeof(double) * 4 * S * n, cudaMemcpyDeviceToHost, st));
+  LB_CUDA(cudaEventRecord(ctx->ev[3], st));
+  LB_CUDA(cudaStreamSynchronize(st));
+  if (phase_ms) {
+    float t = 0.f;
+    for (int p = 0; p < 3; ++p) {
+      LB_CUDA(cudaEventElapsedTime(&t, ctx->ev[p], ctx->ev[p + 1]));
+      phase_ms[p] = t;
+    }
+  }
+  return LB_OK;
+}
+
+int lb_mesh_set_geometry(lb_mesh* m, const double* origins, const double* qpts, const double* qwts,
+                         const int* cell_nodes, int n_nodes, int n_free, const int* P_ptr,
+                         const int* P_idx, const double* P_w) {
+  if (!m) return fail(LB_EINVAL, "null mesh");
+  if (!origins || !qpts || !qwts || !cell_nodes || !P_ptr || n_nodes < 0 || n_free < 0)
+    return fail(LB_EINVAL, "bad geometry argument");
+  LB_CUDA(cudaSetDevice(m->device));
+  int nnzP = 0;
+  std::memcpy(&nnzP, P_ptr + n_nodes, sizeof(int));
+  if (nnzP < 0 || (nnzP && (!P_idx || !P_w))) return fail(LB_EINVAL, "bad prolongation");
+  for (void* p : {(void*)m->origins, (void*)m->qgeo, (void*)m->cell_nodes, (void*)m->P_ptr,
+                  (void*)m->P_idx, (void*)m->P_w})
+    if (p) cudaFree(p);
+  m->origins = m->qgeo = m->P_w = nullptr;
+  m->cell_nodes = m->P_ptr = m->P_idx = nullptr;
+  cudaError_t e = cudaSuccess;
+  auto up = [&](void** dst, const void* src, size_t b) {
+    if (e == cudaSuccess) e = cudaMalloc(dst, std::max<size_t>(b, 8));
+    if (e == cudaSuccess && b) e = cudaMemcpy(*dst, src, b, cudaMemcpyHostToDevice);
+  };
+  up((void**)&m->origins, origins, sizeof(double) * 2 * m->ncell);
+  if (e == cudaSuccess) e = cudaMalloc((void**)&m->qgeo, sizeof(double) * 27);
+  if (e == cudaSuccess) e = cudaMemcpy(m->qgeo, qpts, sizeof(double) * 18, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMemcpy(m->qgeo + 18, qwts, sizeof(double) * 9, cudaMemcpyHostToDevice);
+  up((void**)&m->cell_nodes, cell_nodes, sizeof(int) * 9 * m->ncell);
+  up((void**)&m->P_ptr, P_ptr, sizeof(int) * (n_nodes + 1));
+  up((void**)&m->P_idx, P_idx, sizeof(int) * nnzP);
+  up((void**)&m->P_w, P_w, sizeof(double) * nnzP);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return fail(e == cudaErrorMemoryAllocation ? LB_ENOMEM : LB_ECUDA,
+                std::string("lb_mesh_set_geometry: ") + cudaGetErrorString(e));
+  }
+  m->n_nodes = n_nodes;
+  m->n_free = n_free;
+  m->nnzP = nnzP;
+  return LB_OK;
+}
+
+int lb_sample_state_dev(lb_ctx* ctx, const lb_mesh* m, int S, int c0, int c1, const double* coeffs,
+                        double* r, double* z, double* w, double* f, double* df_r, double* df_z,
+                        void* stream) {
+  int rc = use_ctx(ctx);
+  if (rc) return rc;
+  if ((rc = check_species(S))) return rc;
+  if (!m || !m->cell_nodes) return fail(LB_EINVAL, "mesh has no sampling geometry (lb_mesh_set_geometry)");
+  if (c0 < 0 || c1 > m->ncell || c0 > c1) return fail(LB_EINVAL, "bad cell range");
+  const int nloc = 9 * (c1 - c0);
+  ctx->last_launches = 0;
+  if (nloc == 0) return LB_OK;
+  lb_sample_kernel<<<(nloc + 127) / 128, 128, 0, (cudaStream_t)stream>>>(
+      c0, c1, S, m->n_free, m->origins, m->sizes, m->qgeo, m->basis, m->cell_nodes, m->P_ptr,
+      m->P_idx, m->P_w, coeffs, r, z, w, f, df_r, df_z);
+  LB_CUDA(cudaGetLastError());
+  ctx->last_launches = 1;
+  return LB_OK;
+}
+
+int lb_assemble_state(lb_ctx* ctx, const lb_mesh* m, int S, const double* coeffs, const double* coK,
+                      const double* coD, double eps_d, double* csr_out, double* data_out,
+                      double* phase_ms) {
+  int rc = use_ctx(ctx);
+  if (rc) return rc;
+  if ((rc = check_species(S))) return rc;
+  if (!m || !m->cell_nodes || m->device != ctx->device)
+    return fail(LB_EINVAL, "mesh handle missing, on another device, or without geometry");
+  if (!coeffs || !coK || !coD || !csr_out) return fail(LB_EINVAL, "null argument");
+  const int ncell = m->ncell, n = 9 * ncell;
+  if (ncell == 0) return LB_OK;
+  cudaStream_t st = ctx->stream;
+  const size_t nin = (size_t)(3 + 3 * S) * n + (size_t)S * m->n_free;
+  if ((rc = ensure(ctx->in, nin * sizeof(double)))) return rc;
+  if ((rc = ensure(ctx->rec, (size_t)n * rec_stride(S) * sizeof(double)))) return rc;
+  if ((rc = ensure(ctx->out, (size_t)6 * S * n * sizeof(double)))) return rc;
+  if ((rc = ensure(ctx->elem, ((size_t)81 * S * ncell + (size_t)S * m->nslots) * sizeof(double))))
+    return rc;
+  double* din = static_cast<double*>(ctx->in.p);
+  double *dr = din, *dz = dr + n, *dw = dz + n, *df = dw + n, *dfr = df + (size_t)S * n,
+         *dfz = dfr + (size_t)S * n, *dco = dfz + (size_t)S * n;
+  double* dK = static_cast<double*>(ctx->out.p);
+  double* dD = dK + (size_t)2 * S * n;
+  double* delem = static_cast<double*>(ctx->elem.p);
+  double* dcsr = delem + (size_t)81 * S * ncell;
+  LB_CUDA(cudaEventRecord(ctx->ev[0], st));
+  LB_CUDA(cudaMemcpyAsync(dco, coeffs, sizeof(double) * S * m->n_free, cudaMemcpyHostToDevice, st));
+  lb_sample_kernel<<<(n + 127) / 128, 128, 0, st>>>(0, ncell, S, m->n_free, m->origins, m->sizes,
+                                                    m->qgeo, m->basis, m->cell_nodes, m->P_ptr,
+                                                    m->P_idx, m->P_w, dco, dr, dz, dw, df, dfr, dfz);
+  LB_CUDA(cudaGetLastError());
+  double* drec = static_cast<double*>(ctx->rec.p);
+  if ((rc = launch_pack(ctx, n, S, dr, dz, dw, df, dfr, dfz, drec, st))) return rc;
+  LB_CUDA(cudaEventRecord(ctx->ev[1], st));
+  Coupling cp;
+  make_coupling(S, coK, coD, cp);
+  if ((rc = all_points_sweep(ctx, n, S, drec, dr, dz, cp, mask_threshold(eps_d), dK, dD, st)))
+    return rc;
+  LB_CUDA(cudaEventRecord(ctx->ev[2], st));
+  if ((rc = launch_elements(ctx, ncell, S, m->sizes, dw, dK, dD, m->basis, m->basis + 81, delem, st)))
+    return rc;
+  if (m->nslots) {
+    lb_csr_gather_kernel<<<(m->nslots + 255) / 256, 256, 0, st>>>(m->nslots, 81 * ncell, S, m->slot_ptr,
+                                                                   m->gidx, m->gw, delem, dcsr);
+    LB_CUDA(cudaGetLastError());
+  }
+  LB_CUDA(cudaMemcpyAsync(csr_out, dcsr, sizeof(double) * S * m->nslots, cudaMemcpyDeviceToHost, st));
+  if (data_out)  // r, z, w, f, df_r, df_z as one (3 + 3S) x n block
+    LB_CUDA(cudaMemcpyAsync(data_out, din, sizeof(double) * (3 + 3 * S) * n, cudaMemcpyDeviceToHost, st));
   LB_CUDA(cudaEventRecord(ctx->ev[3], st));
   LB_CUDA(cudaStreamSynchronize(st));
   if (phase_ms) {

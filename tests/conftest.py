@@ -41,13 +41,14 @@ def mesh_from(g):
     attributes assemble_collision reads (assembly.py:153-169)."""
     cn = g["mesh_cell_nodes"]
     return SimpleNamespace(
-        n_cells=cn.shape[0], sizes=g["mesh_sizes"], cell_nodes=cn,
+        n_cells=cn.shape[0], sizes=g["mesh_sizes"], cell_nodes=cn, origins=g["mesh_origins"],
         n_nodes=int(g["mesh_n_nodes"]), prolongation=csr_from(g, "mesh_P"),
         domain=SimpleNamespace(L=float(g["mesh_L"])))
 
 
 def ref_from(g):
-    return SimpleNamespace(Nq=9, B=g["ref_B"], dB=g["ref_dB"])
+    return SimpleNamespace(Nq=9, B=g["ref_B"], dB=g["ref_dB"], qpts=g["ref_qpts"],
+                           qwts=g["ref_qwts"])
 
 
 def data_from(g, suffix=""):

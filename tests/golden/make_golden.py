@@ -51,6 +51,7 @@ def mesh_parts(mesh, ref):
            "mesh_n_nodes": np.int64(mesh.n_nodes), "mesh_L": np.float64(mesh.domain.L),
            "mesh_free_r": mesh.nodes[mesh.free_nodes, 0],
            "mesh_free_z": mesh.nodes[mesh.free_nodes, 1],
+           "mesh_origins": mesh.origins, "ref_qpts": ref.qpts, "ref_qwts": ref.qwts,
            "ref_B": ref.B, "ref_dB": ref.dB}
     out.update(csr_parts("mesh_P", mesh.prolongation))
     return out

@@ -114,3 +114,30 @@ def test_assembly_deterministic(gpu):
                                workers=2)
     for x, y in zip(a.blocks, b.blocks):
         assert np.array_equal(x.toarray(), y.toarray())
+
+
+@pytest.mark.parametrize("case", ["cfg1", "hanging", "cfg2", "cons"])
+def test_device_sampling_matches_reference(gpu, case):
+    """Device sample_state (fem.py:170-199): r, z, w bitwise the reference's,
+    f and grad f to rounding."""
+    g = golden(case)
+    qd = gpu.sample_state(mesh_from(g), ref_from(g), g["coeffs"])
+    for k in ("r", "z", "w"):
+        assert np.array_equal(getattr(qd, k), g[k]), k
+    for k in ("f", "df_r", "df_z"):
+        ref = g[k]
+        err = np.abs(getattr(qd, k) - ref).max() / np.abs(ref).max()
+        assert err < 1e-14, (k, err)
+
+
+@pytest.mark.parametrize("case", ["cfg1", "hanging", "cfg2"])
+def test_state_level_operator(gpu, case):
+    """assemble_at = solver._assemble_at (solver.py:81-84) in one device call:
+    nodal coefficients in, CSR blocks out, matching the reference operator."""
+    g = golden(case)
+    cm, qd = gpu.assemble_at(mesh_from(g), ref_from(g), g["coeffs"], params_from(g),
+                             return_data=True)
+    err = _block_err(cm, blocks_from(g, "C"))
+    print(case, "state-level jacobian", err)
+    assert err < TOL
+    assert np.array_equal(qd.r, g["r"]) and np.array_equal(qd.w, g["w"])
