@@ -689,7 +689,7 @@ int launch_sweep(lb_ctx* ctx, int nout, const double* ro, const double* zo, int 
   if (nout >= kOrderMin) {
     int rc = morton_order(ctx->order, nout, ro, zo, 1, st, &perm, &ro, &zo);
     if (rc) return rc;
-    launches += 4;  // bbox, morton, radix sort (counted once), gather
+    launches += 3;  // own kernels: bbox, morton, gather (+ CUB radix sort)
   }
   const int jc = chunk_len(n);
   const int nchunk = (n + jc - 1) / jc;
@@ -770,7 +770,7 @@ int sym_prepare(lb_ctx* ctx, int n, int S, const double* rec, cudaStream_t st) {
   ctx->sym_n = n;
   ctx->sym_S = S;
   ctx->sym_nt = nt;
-  ctx->last_launches = 6;  // bbox, morton, radix sort (1), gather, records gather, invert
+  ctx->last_launches = 4;  // own kernels: bbox, morton, records gather, invert (+ CUB radix sort)
   return LB_OK;
 }
 
@@ -875,9 +875,9 @@ int all_points_sweep(lb_ctx* ctx, int n, int S, const double* rec, const double*
   if ((rc = ensure(ctx->symtot, (size_t)5 * S * npad * sizeof(double)))) return rc;
   double* tot = static_cast<double*>(ctx->symtot.p);
   if ((rc = sym_partial_dispatch(ctx, S, gthr, 0, 1, tot, st))) return rc;
-  int l = ctx->last_launches;
+  const int l = ctx->last_launches;  // sweep + reduce launches
   rc = sym_combine_dispatch(ctx, S, tot, cp, 0, n, K, D, st);
-  ctx->last_launches += l + 6;
+  ctx->last_launches += l + 4;        // + combine (set above) + 4 ordering kernels
   return rc;
 }
 

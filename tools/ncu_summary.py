@@ -64,6 +64,24 @@ def summarise(report):
                     stalls[h[len("smsp__average_warps_issue_stalled_"):-len(
                         "_per_issue_active.ratio")]] = fv
         s["stalls_per_issue"] = dict(sorted(stalls.items(), key=lambda kv: -kv[1]))
+        # executed FP64 work: thread-level DFMA (2 flops) + DMUL + DADD per SMSP-cycle
+        try:
+            per = {op: float(d[f"smsp__sass_thread_inst_executed_op_{op}_pred_on.sum.per_cycle_elapsed"][0])
+                   for op in ("dfma", "dmul", "dadd")}
+            clk = float(d["sm__cycles_elapsed.avg.per_second"][0]) * 1e9
+            if d["sm__cycles_elapsed.avg.per_second"][1].lower().startswith("mhz"):
+                clk = float(d["sm__cycles_elapsed.avg.per_second"][0]) * 1e6
+            flops_per_cycle = 2 * per["dfma"] + per["dmul"] + per["dadd"]   # whole GPU
+            insts_per_cycle = per["dfma"] + per["dmul"] + per["dadd"]
+            nsm = 148
+            s["executed_fp64"] = {
+                "thread_ops_per_cycle_gpu": insts_per_cycle,
+                "tflops": flops_per_cycle * clk / 1e12,
+                "frac_of_issue_peak": insts_per_cycle / (64.0 * nsm),
+                "frac_of_flop_peak": flops_per_cycle / (128.0 * nsm),
+                "note": "DFMA counted as 2 flops; peak 64 DFMA/clk/SM (148 SMs)"}
+        except (KeyError, ValueError):
+            pass
         res.append(s)
     return res
 
