@@ -63,9 +63,13 @@ int lb_device_count(void);
 int lb_ctx_create(int device, lb_ctx **out);
 int lb_ctx_destroy(lb_ctx *ctx);
 
-/* Doubles per packed inner-point record for S species (r, z, r^2, 1/r,
- * then (w*df_r, w*df_z, w*f) per species, padded to an even count). */
-int lb_record_stride(int S);
+/* Doubles per packed inner-point record for S species and the coupling
+ * coK/coD (NULL: per-species layout): r, z, r^2, 1/r, then (w*df_r, w*df_z,
+ * w*f) per species -- or, when coK and coD are rank one (always so for the
+ * reference's collision_params, nu_ab ~ e_a^2 e_b^2, physics.py:77-94), the
+ * species-collapsed triple (sum_b k_b w df_r, sum_b k_b w df_z,
+ * sum_b be_b w f) -- padded to an even count. */
+int lb_record_stride(int S, const double *coK, const double *coD);
 
 /* Inner-point chunk length the sweep uses for n inner points (a function of
  * n only; exposed so tests can check the decomposition). */
@@ -177,7 +181,8 @@ int lb_tensor_pairs(lb_ctx *ctx, int npair, const double *r, const double *z,
  * doubles: the per-point field state that the sharded path all-gathers. */
 int lb_pack_records_dev(lb_ctx *ctx, int n, int S, const double *r, const double *z,
                         const double *w, const double *f, const double *df_r,
-                        const double *df_z, double *rec, void *stream);
+                        const double *df_z, const double *coK, const double *coD,
+                        double *rec, void *stream);
 
 /* Pair sweep + species coupling over packed records (device pointers).
  * `n` is the total inner count (all shards), `rec` its packed records. */
@@ -201,10 +206,12 @@ int lb_elements_dev(lb_ctx *ctx, int ncell, int S, const double *cell_sizes,
  *                        point order; zero where the rank contributed none);
  *  3 lb_sym_combine_dev  K/D for original points [q0, q1) from the summed tot
  *                        (K_out/D_out hold q1-q0 rows).
- * lb_sym_supported(S) is 1 for the species counts this path implements. */
-int lb_sym_supported(int S);
+ * lb_sym_supported(S, coK, coD) is 1 when this path implements the
+ * coupling (any S with a rank-one coupling, else S <= 3). */
+int lb_sym_supported(int S, const double *coK, const double *coD);
 int lb_sym_npad(int n);
-int lb_sym_prepare_dev(lb_ctx *ctx, int n, int S, const double *rec, void *stream);
+int lb_sym_prepare_dev(lb_ctx *ctx, int n, int S, const double *coK, const double *coD,
+                       const double *rec, void *stream);
 int lb_sym_partial_dev(lb_ctx *ctx, int S, double eps_d, int rank, int world, double *tot,
                        void *stream);
 int lb_sym_combine_dev(lb_ctx *ctx, int S, const double *tot, const double *coK,

@@ -34,7 +34,7 @@ SIGNATURES = {
     "lb_device_count": (_i, []),
     "lb_ctx_create": (_i, [_i, C.POINTER(_vp)]),
     "lb_ctx_destroy": (_i, [_vp]),
-    "lb_record_stride": (_i, [_i]),
+    "lb_record_stride": (_i, [_i, _dp, _dp]),
     "lb_chunk_len": (_i, [_i]),
     "lb_fused_sweep": (_i, [_vp, _i, _dp, _dp, _i, _i, _dp, _dp, _dp, _dp, _dp, _dp,
                             _dp, _dp, _d, _dp, _dp]),
@@ -50,12 +50,12 @@ SIGNATURES = {
     "lb_assemble_state": (_i, [_vp, _vp, _i, _dp, _dp, _dp, _d, _dp, _dp, _dp]),
     "lb_assemble_csr": (_i, [_vp, _vp, _i, _dp, _dp, _dp, _dp, _dp, _dp, _dp, _dp, _d, _dp,
                              _dp, _dp, _dp]),
-    "lb_sym_supported": (_i, [_i]),
+    "lb_sym_supported": (_i, [_i, _dp, _dp]),
     "lb_sym_npad": (_i, [_i]),
-    "lb_sym_prepare_dev": (_i, [_vp, _i, _i, _vp, _vp]),
+    "lb_sym_prepare_dev": (_i, [_vp, _i, _i, _dp, _dp, _vp, _vp]),
     "lb_sym_partial_dev": (_i, [_vp, _i, _d, _i, _i, _vp, _vp]),
     "lb_sym_combine_dev": (_i, [_vp, _i, _vp, _dp, _dp, _i, _i, _vp, _vp, _vp]),
-    "lb_pack_records_dev": (_i, [_vp, _i, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
+    "lb_pack_records_dev": (_i, [_vp, _i, _i, _vp, _vp, _vp, _vp, _vp, _vp, _dp, _dp, _vp, _vp]),
     "lb_sweep_dev": (_i, [_vp, _i, _vp, _vp, _i, _i, _vp, _dp, _dp, _d, _vp, _vp, _vp]),
     "lb_elements_dev": (_i, [_vp, _i, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
     "lb_last_launch_count": (_i, [_vp]),

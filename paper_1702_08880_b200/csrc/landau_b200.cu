@@ -56,9 +56,24 @@ struct TileCfg {
   static constexpr int TJ = S <= 4 ? 128 : 64;  // inner records per stage
 };
 
+// Species coupling (kernel.py:496-501) and the record layout it implies.
+// When coK and coD are rank one -- always for the reference's own tables:
+// nu_ab ~ e_a^2 e_b^2 (physics.py:77-94), so coK_ab = k_a k_b with
+// k_a = sqrt(nu_aa) m_o/m_a and coD_ab = al_a be_b -- the S species collapse
+// into ONE accumulator set: each inner point carries the pre-weighted fields
+// gr' = sum_b k_b w df_r,b, gz' = sum_b k_b w df_z,b, f' = sum_b be_b w f_b
+// (formed once per point in K0), the pair loop runs at S = 1 cost, and the
+// combine expands K[a] = k_a A'_{0:2}, D[a] = al_a A'_{2:5}.  Algebraically
+// identical to summing per species then coupling (the reference's order);
+// the rank-one test admits only tables factoring to ~4 ulp.
 struct Coupling {
+  int S = 1;          // species
+  int Se = 1;         // accumulator species sets (1 when collapsed)
+  int collapsed = 0;
   double coK4[LB_MAX_SPECIES * LB_MAX_SPECIES];  // 4 * coK (the pulled-out 4)
   double coD4[LB_MAX_SPECIES * LB_MAX_SPECIES];
+  double kw[LB_MAX_SPECIES], dw[LB_MAX_SPECIES];      // per-point field weights
+  double kout[LB_MAX_SPECIES], dout[LB_MAX_SPECIES];  // 4 k_a, 4 al_a
 };
 
 // ------------------------------------------------------------------ PTX helpers
@@ -94,10 +109,16 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 }
 
 // ------------------------------------------------------------------ K0 pack
+struct PackW {
+  int collapsed;
+  double kw[LB_MAX_SPECIES], dw[LB_MAX_SPECIES];
+};
+
 __global__ void lb_pack_kernel(int n, int S, int RS, const double* __restrict__ r,
                                const double* __restrict__ z, const double* __restrict__ w,
                                const double* __restrict__ f, const double* __restrict__ dfr,
-                               const double* __restrict__ dfz, double* __restrict__ rec) {
+                               const double* __restrict__ dfz, const PackW pw,
+                               double* __restrict__ rec) {
   for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < n; p += gridDim.x * blockDim.x) {
     const double rn = r[p], wn = w[p];
     double* o = rec + (size_t)p * RS;
@@ -105,13 +126,26 @@ __global__ void lb_pack_kernel(int n, int S, int RS, const double* __restrict__ 
     o[1] = z[p];
     o[2] = rn * rn;
     o[3] = rn > 0.0 ? 1.0 / rn : 0.0;
-    for (int b = 0; b < S; ++b) {
-      // same products as _accumulate_block (kernel.py:408-410)
-      o[4 + 3 * b + 0] = dfr[(size_t)b * n + p] * wn;
-      o[4 + 3 * b + 1] = dfz[(size_t)b * n + p] * wn;
-      o[4 + 3 * b + 2] = f[(size_t)b * n + p] * wn;
+    if (pw.collapsed) {  // species-collapsed record (see Coupling)
+      double gr = 0.0, gz = 0.0, fw = 0.0;
+      for (int b = 0; b < S; ++b) {
+        gr = fma(pw.kw[b], dfr[(size_t)b * n + p] * wn, gr);
+        gz = fma(pw.kw[b], dfz[(size_t)b * n + p] * wn, gz);
+        fw = fma(pw.dw[b], f[(size_t)b * n + p] * wn, fw);
+      }
+      o[4] = gr;
+      o[5] = gz;
+      o[6] = fw;
+      for (int k = 7; k < RS; ++k) o[k] = 0.0;
+    } else {
+      for (int b = 0; b < S; ++b) {
+        // same products as _accumulate_block (kernel.py:408-410)
+        o[4 + 3 * b + 0] = dfr[(size_t)b * n + p] * wn;
+        o[4 + 3 * b + 1] = dfz[(size_t)b * n + p] * wn;
+        o[4 + 3 * b + 2] = f[(size_t)b * n + p] * wn;
+      }
+      for (int k = 4 + 3 * S; k < RS; ++k) o[k] = 0.0;
     }
-    for (int k = 4 + 3 * S; k < RS; ++k) o[k] = 0.0;
   }
 }
 
@@ -246,40 +280,33 @@ __global__ void __launch_bounds__(kTI, kMinBlocks) lb_sweep_kernel(const SweepAr
 }
 
 // ------------------------------------------------------------------ K1b combine
-template <int S>
-__global__ void lb_combine_kernel(const double* __restrict__ partial, int nchunk, int nout,
-                                  int nout_pad, const Coupling cp, const int* __restrict__ perm,
-                                  double* __restrict__ K, double* __restrict__ D) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= nout) return;
-  const int io = perm ? perm[i] : i;  // output row of this (possibly reordered) outer point
-  double A[S][5];
-#pragma unroll
-  for (int b = 0; b < S; ++b)
-#pragma unroll
-    for (int q = 0; q < 5; ++q) A[b][q] = 0.0;
-  for (int c = 0; c < nchunk; ++c) {
-    const double* src = partial + (size_t)c * (5 * S) * nout_pad + i;
-#pragma unroll
-    for (int b = 0; b < S; ++b)
-#pragma unroll
-      for (int q = 0; q < 5; ++q) A[b][q] = __dadd_rn(A[b][q], src[(size_t)(b * 5 + q) * nout_pad]);
-  }
-  // _combine (kernel.py:419-440): strict order, no contraction
-#pragma unroll
+// Shared by both combine kernels: accumulators A[Se][5] -> K, D rows.
+template <int Se>
+__device__ __forceinline__ void write_kd(const double (&A)[Se][5], const Coupling& cp, size_t io,
+                                         double* __restrict__ K, double* __restrict__ D) {
+  const int S = cp.S;
   for (int a = 0; a < S; ++a) {
-    double k0 = 0.0, k1 = 0.0, d0 = 0.0, d1 = 0.0, d2 = 0.0;
+    double k0, k1, d0, d1, d2;
+    if (cp.collapsed) {  // rank-one coupling: expand the single accumulator set
+      k0 = __dmul_rn(cp.kout[a], A[0][0]);
+      k1 = __dmul_rn(cp.kout[a], A[0][1]);
+      d0 = __dmul_rn(cp.dout[a], A[0][2]);
+      d1 = __dmul_rn(cp.dout[a], A[0][3]);
+      d2 = __dmul_rn(cp.dout[a], A[0][4]);
+    } else {  // _combine (kernel.py:419-440): strict order, no contraction
+      k0 = 0.0, k1 = 0.0, d0 = 0.0, d1 = 0.0, d2 = 0.0;
 #pragma unroll
-    for (int b = 0; b < S; ++b) {
-      const double ck = cp.coK4[a * S + b], cd = cp.coD4[a * S + b];
-      k0 = __dadd_rn(k0, __dmul_rn(ck, A[b][0]));
-      k1 = __dadd_rn(k1, __dmul_rn(ck, A[b][1]));
-      d0 = __dadd_rn(d0, __dmul_rn(cd, A[b][2]));
-      d1 = __dadd_rn(d1, __dmul_rn(cd, A[b][3]));
-      d2 = __dadd_rn(d2, __dmul_rn(cd, A[b][4]));
+      for (int b = 0; b < Se; ++b) {
+        const double ck = cp.coK4[a * Se + b], cd = cp.coD4[a * Se + b];
+        k0 = __dadd_rn(k0, __dmul_rn(ck, A[b][0]));
+        k1 = __dadd_rn(k1, __dmul_rn(ck, A[b][1]));
+        d0 = __dadd_rn(d0, __dmul_rn(cd, A[b][2]));
+        d1 = __dadd_rn(d1, __dmul_rn(cd, A[b][3]));
+        d2 = __dadd_rn(d2, __dmul_rn(cd, A[b][4]));
+      }
     }
-    double* Ko = K + ((size_t)io * S + a) * 2;
-    double* Do = D + ((size_t)io * S + a) * 4;
+    double* Ko = K + (io * S + a) * 2;
+    double* Do = D + (io * S + a) * 4;
     Ko[0] = k0;
     Ko[1] = k1;
     Do[0] = d0;
@@ -287,6 +314,28 @@ __global__ void lb_combine_kernel(const double* __restrict__ partial, int nchunk
     Do[2] = d1;
     Do[3] = d2;
   }
+}
+
+template <int Se>
+__global__ void lb_combine_kernel(const double* __restrict__ partial, int nchunk, int nout,
+                                  int nout_pad, const Coupling cp, const int* __restrict__ perm,
+                                  double* __restrict__ K, double* __restrict__ D) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= nout) return;
+  const int io = perm ? perm[i] : i;  // output row of this (possibly reordered) outer point
+  double A[Se][5];
+#pragma unroll
+  for (int b = 0; b < Se; ++b)
+#pragma unroll
+    for (int q = 0; q < 5; ++q) A[b][q] = 0.0;
+  for (int c = 0; c < nchunk; ++c) {
+    const double* src = partial + (size_t)c * (5 * Se) * nout_pad + i;
+#pragma unroll
+    for (int b = 0; b < Se; ++b)
+#pragma unroll
+      for (int q = 0; q < 5; ++q) A[b][q] = __dadd_rn(A[b][q], src[(size_t)(b * 5 + q) * nout_pad]);
+  }
+  write_kd<Se>(A, cp, (size_t)io, K, D);
 }
 
 #include "landau_sym.cuh"  // symmetric all-points sweep (kernels)
@@ -565,7 +614,7 @@ struct lb_ctx {
   lb::DevBuf in, rec, partial, out, elem, outer, aux, order;
   // symmetric all-points sweep state (lb_sym_*): sorted records, order, partials
   lb::DevBuf symord, symrec, syminv, symi, symj, symtot;
-  int sym_n = -1, sym_S = 0, sym_nt = 0;
+  int sym_n = -1, sym_S = 0, sym_Se = 0, sym_nt = 0;
 };
 
 struct lb_mesh {
@@ -624,13 +673,43 @@ long long mask_threshold(double eps_d) {
 }
 
 int make_coupling(int S, const double* coK, const double* coD, Coupling& cp) {
-  std::memset(&cp, 0, sizeof(cp));
+  cp = Coupling();
+  cp.S = S;
+  cp.Se = S;
   for (int t = 0; t < S * S; ++t) {
     cp.coK4[t] = 4.0 * coK[t];
     cp.coD4[t] = 4.0 * coD[t];
   }
+  if (S < 2) return LB_OK;
+  // rank-one test (to ~4 ulp): coK_ab = k_a k_b, coD_ab = al_a be_b
+  const double tol = 1e-15;
+  double k[LB_MAX_SPECIES], al[LB_MAX_SPECIES], be[LB_MAX_SPECIES];
+  if (!(coD[0] != 0.0)) return LB_OK;
+  for (int a = 0; a < S; ++a) {
+    if (!(coK[a * S + a] > 0.0)) return LB_OK;
+    k[a] = std::sqrt(coK[a * S + a]);
+    al[a] = coD[a * S + 0];
+    be[a] = coD[0 * S + a] / coD[0];
+  }
+  for (int a = 0; a < S; ++a)
+    for (int b = 0; b < S; ++b) {
+      const double kk = k[a] * k[b], cK = coK[a * S + b];
+      const double dd = al[a] * be[b], cD = coD[a * S + b];
+      if (std::fabs(kk - cK) > tol * std::fabs(cK) || std::fabs(dd - cD) > tol * std::fabs(cD))
+        return LB_OK;
+    }
+  cp.collapsed = 1;
+  cp.Se = 1;
+  for (int a = 0; a < S; ++a) {
+    cp.kw[a] = k[a];
+    cp.dw[a] = be[a];
+    cp.kout[a] = 4.0 * k[a];
+    cp.dout[a] = 4.0 * al[a];
+  }
   return LB_OK;
 }
+
+int record_stride(const Coupling& cp) { return rec_stride(cp.Se); }
 
 constexpr int kOrderMin = 4096;  // outer sets at least this large are Morton-ordered
 
@@ -719,7 +798,7 @@ int launch_sweep(lb_ctx* ctx, int nout, const double* ro, const double* zo, int 
     LB_CUDA(cudaGetLastError());
     lb_combine_kernel<S><<<(nb + 127) / 128, 128, 0, st>>>(
         a.partial, nchunk, nb, nout_pad, cp, perm ? perm + o0 : nullptr,
-        perm ? K : K + (size_t)o0 * S * 2, perm ? D : D + (size_t)o0 * S * 4);
+        perm ? K : K + (size_t)o0 * cp.S * 2, perm ? D : D + (size_t)o0 * cp.S * 4);
     LB_CUDA(cudaGetLastError());
     launches += 2;
   }
@@ -730,7 +809,7 @@ int launch_sweep(lb_ctx* ctx, int nout, const double* ro, const double* zo, int 
 int sweep_dispatch(lb_ctx* ctx, int nout, const double* ro, const double* zo, int n, int S,
                    const double* rec, const Coupling& cp, long long gthr, double* K, double* D,
                    cudaStream_t st) {
-  switch (S) {
+  switch (cp.Se) {  // template = accumulator species sets
     case 1: return launch_sweep<1>(ctx, nout, ro, zo, n, rec, cp, gthr, K, D, st);
     case 2: return launch_sweep<2>(ctx, nout, ro, zo, n, rec, cp, gthr, K, D, st);
     case 3: return launch_sweep<3>(ctx, nout, ro, zo, n, rec, cp, gthr, K, D, st);
@@ -754,8 +833,8 @@ int check_species(int S) {
 // ------------------------------------------------------------------ symmetric path (host)
 constexpr size_t kSymBudget = size_t(2) << 30;  // bytes of i/j-side partials per row batch
 
-int sym_prepare(lb_ctx* ctx, int n, int S, const double* rec, cudaStream_t st) {
-  const int RS = rec_stride(S);
+int sym_prepare(lb_ctx* ctx, int n, const Coupling& cp, const double* rec, cudaStream_t st) {
+  const int RS = record_stride(cp);
   const int nt = (n + kSymTile - 1) / kSymTile;
   const int npad = nt * kSymTile;
   const int* perm = nullptr;
@@ -768,7 +847,8 @@ int sym_prepare(lb_ctx* ctx, int n, int S, const double* rec, cudaStream_t st) {
   lb_invert_perm_kernel<<<(n + 255) / 256, 256, 0, st>>>(n, perm, static_cast<int*>(ctx->syminv.p));
   LB_CUDA(cudaGetLastError());
   ctx->sym_n = n;
-  ctx->sym_S = S;
+  ctx->sym_S = cp.S;
+  ctx->sym_Se = cp.Se;
   ctx->sym_nt = nt;
   ctx->last_launches = 4;  // own kernels: bbox, morton, records gather, invert (+ CUB radix sort)
   return LB_OK;
@@ -865,29 +945,35 @@ int sym_combine_dispatch(lb_ctx* ctx, int S, const double* tot, const Coupling& 
 
 // All-points sweep (outer == inner == the n packed records) on one device:
 // symmetric path when S <= kSymMaxS, else the general sweep.
-int all_points_sweep(lb_ctx* ctx, int n, int S, const double* rec, const double* r, const double* z,
+int all_points_sweep(lb_ctx* ctx, int n, const double* rec, const double* r, const double* z,
                      const Coupling& cp, long long gthr, double* K, double* D, cudaStream_t st) {
-  if (S > kSymMaxS || n < kSymTile)
-    return sweep_dispatch(ctx, n, r, z, n, S, rec, cp, gthr, K, D, st);
-  int rc = sym_prepare(ctx, n, S, rec, st);
+  if (cp.Se > kSymMaxS || n < kSymTile)
+    return sweep_dispatch(ctx, n, r, z, n, cp.S, rec, cp, gthr, K, D, st);
+  int rc = sym_prepare(ctx, n, cp, rec, st);
   if (rc) return rc;
   const int npad = ctx->sym_nt * kSymTile;
-  if ((rc = ensure(ctx->symtot, (size_t)5 * S * npad * sizeof(double)))) return rc;
+  if ((rc = ensure(ctx->symtot, (size_t)5 * cp.Se * npad * sizeof(double)))) return rc;
   double* tot = static_cast<double*>(ctx->symtot.p);
-  if ((rc = sym_partial_dispatch(ctx, S, gthr, 0, 1, tot, st))) return rc;
+  if ((rc = sym_partial_dispatch(ctx, cp.Se, gthr, 0, 1, tot, st))) return rc;
   const int l = ctx->last_launches;  // sweep + reduce launches
-  rc = sym_combine_dispatch(ctx, S, tot, cp, 0, n, K, D, st);
+  rc = sym_combine_dispatch(ctx, cp.Se, tot, cp, 0, n, K, D, st);
   ctx->last_launches += l + 4;        // + combine (set above) + 4 ordering kernels
   return rc;
 }
 
 int launch_pack(lb_ctx* ctx, int n, int S, const double* r, const double* z, const double* w,
-                const double* f, const double* dfr, const double* dfz, double* rec,
-                cudaStream_t st) {
+                const double* f, const double* dfr, const double* dfz, const Coupling& cp,
+                double* rec, cudaStream_t st) {
   if (n == 0) return LB_OK;
+  PackW pw;
+  pw.collapsed = cp.collapsed;
+  for (int b = 0; b < LB_MAX_SPECIES; ++b) {
+    pw.kw[b] = cp.kw[b];
+    pw.dw[b] = cp.dw[b];
+  }
   const int threads = 256;
   const int blocks = std::min((n + threads - 1) / threads, ctx->num_sms * 8);
-  lb_pack_kernel<<<blocks, threads, 0, st>>>(n, S, rec_stride(S), r, z, w, f, dfr, dfz, rec);
+  lb_pack_kernel<<<blocks, threads, 0, st>>>(n, S, record_stride(cp), r, z, w, f, dfr, dfz, pw, rec);
   LB_CUDA(cudaGetLastError());
   return LB_OK;
 }
@@ -969,9 +1055,12 @@ int lb_ctx_destroy(lb_ctx* ctx) {
   return LB_OK;
 }
 
-int lb_record_stride(int S) {
+int lb_record_stride(int S, const double* coK, const double* coD) {
   if (check_species(S)) return -1;
-  return rec_stride(S);
+  if (!coK || !coD) return rec_stride(S);
+  Coupling cp;
+  make_coupling(S, coK, coD, cp);
+  return record_stride(cp);
 }
 
 int lb_chunk_len(int n) { return chunk_len(std::max(n, 0)); }
@@ -980,13 +1069,17 @@ int lb_last_launch_count(lb_ctx* ctx) { return ctx ? ctx->last_launches : 0; }
 
 int lb_pack_records_dev(lb_ctx* ctx, int n, int S, const double* r, const double* z,
                         const double* w, const double* f, const double* df_r,
-                        const double* df_z, double* rec, void* stream) {
+                        const double* df_z, const double* coK, const double* coD, double* rec,
+                        void* stream) {
   int rc = use_ctx(ctx);
   if (rc) return rc;
   if ((rc = check_species(S))) return rc;
   if (n < 0) return fail(LB_EINVAL, "negative point count");
+  if (!coK || !coD) return fail(LB_EINVAL, "null coupling table");
+  Coupling cp;
+  make_coupling(S, coK, coD, cp);
   cudaStream_t st = (cudaStream_t)stream;  // NULL = legacy default stream
-  rc = launch_pack(ctx, n, S, r, z, w, f, df_r, df_z, rec, st);
+  rc = launch_pack(ctx, n, S, r, z, w, f, df_r, df_z, cp, rec, st);
   ctx->last_launches = n > 0 ? 1 : 0;
   return rc;
 }
@@ -1038,10 +1131,12 @@ int lb_fused_sweep(lb_ctx* ctx, int nout, const double* outer_r, const double* o
   if (!outer_r || !outer_z || !K_out || !D_out || !coK || !coD)
     return fail(LB_EINVAL, "null argument");
   if (n > 0 && (!r || !z || !w || !f || !df_r || !df_z)) return fail(LB_EINVAL, "null inner field");
+  Coupling cp;
+  make_coupling(S, coK, coD, cp);
   cudaStream_t st = ctx->stream;
   const size_t nin = (size_t)(3 + 3 * S) * n;
   if ((rc = ensure(ctx->in, std::max<size_t>(nin, 1) * sizeof(double)))) return rc;
-  if ((rc = ensure(ctx->rec, std::max<size_t>((size_t)n * rec_stride(S), 1) * sizeof(double)))) return rc;
+  if ((rc = ensure(ctx->rec, std::max<size_t>((size_t)n * record_stride(cp), 1) * sizeof(double)))) return rc;
   if ((rc = ensure(ctx->outer, (size_t)2 * nout * sizeof(double)))) return rc;
   if ((rc = ensure(ctx->out, (size_t)6 * S * nout * sizeof(double)))) return rc;
   double* din = static_cast<double*>(ctx->in.p);
@@ -1063,7 +1158,7 @@ int lb_fused_sweep(lb_ctx* ctx, int nout, const double* outer_r, const double* o
   LB_CUDA(cudaMemcpyAsync(dro, outer_r, sizeof(double) * nout, cudaMemcpyHostToDevice, st));
   LB_CUDA(cudaMemcpyAsync(dzo, outer_z, sizeof(double) * nout, cudaMemcpyHostToDevice, st));
   double* drec = static_cast<double*>(ctx->rec.p);
-  if ((rc = launch_pack(ctx, n, S, dr, dz, dw, df, dfr, dfz, drec, st))) return rc;
+  if ((rc = launch_pack(ctx, n, S, dr, dz, dw, df, dfr, dfz, cp, drec, st))) return rc;
   if ((rc = lb_sweep_dev(ctx, nout, dro, dzo, n, S, drec, coK, coD, eps_d, dK, dD, st))) return rc;
   LB_CUDA(cudaMemcpyAsync(K_out, dK, sizeof(double) * 2 * S * nout, cudaMemcpyDeviceToHost, st));
   LB_CUDA(cudaMemcpyAsync(D_out, dD, sizeof(double) * 4 * S * nout, cudaMemcpyDeviceToHost, st));
@@ -1084,11 +1179,13 @@ int lb_assemble_elements(lb_ctx* ctx, int ncell, const double* cell_sizes, int S
   if (!cell_sizes || !r || !z || !w || !f || !df_r || !df_z || !coK || !coD || !B || !dB ||
       !elem_out)
     return fail(LB_EINVAL, "null argument");
+  Coupling cp;
+  make_coupling(S, coK, coD, cp);
   const int n = 9 * ncell;
   cudaStream_t st = ctx->stream;
   const size_t nin = (size_t)(3 + 3 * S) * n;
   if ((rc = ensure(ctx->in, nin * sizeof(double)))) return rc;
-  if ((rc = ensure(ctx->rec, (size_t)n * rec_stride(S) * sizeof(double)))) return rc;
+  if ((rc = ensure(ctx->rec, (size_t)n * record_stride(cp) * sizeof(double)))) return rc;
   if ((rc = ensure(ctx->out, (size_t)6 * S * n * sizeof(double)))) return rc;
   if ((rc = ensure(ctx->elem, (size_t)81 * S * ncell * sizeof(double)))) return rc;
   if ((rc = ensure(ctx->aux, (size_t)(2 * ncell + 81 + 162) * sizeof(double)))) return rc;
@@ -1113,14 +1210,10 @@ int lb_assemble_elements(lb_ctx* ctx, int ncell, const double* cell_sizes, int S
   LB_CUDA(cudaMemcpyAsync(dB_, B, sizeof(double) * 81, cudaMemcpyHostToDevice, st));
   LB_CUDA(cudaMemcpyAsync(ddB, dB, sizeof(double) * 162, cudaMemcpyHostToDevice, st));
   double* drec = static_cast<double*>(ctx->rec.p);
-  if ((rc = launch_pack(ctx, n, S, dr, dz, dw, df, dfr, dfz, drec, st))) return rc;
+  if ((rc = launch_pack(ctx, n, S, dr, dz, dw, df, dfr, dfz, cp, drec, st))) return rc;
   LB_CUDA(cudaEventRecord(ctx->ev[1], st));
-  {
-    Coupling cp;
-    make_coupling(S, coK, coD, cp);
-    if ((rc = all_points_sweep(ctx, n, S, drec, dr, dz, cp, mask_threshold(eps_d), dK, dD, st)))
-      return rc;
-  }
+  if ((rc = all_points_sweep(ctx, n, drec, dr, dz, cp, mask_threshold(eps_d), dK, dD, st)))
+    return rc;
   LB_CUDA(cudaEventRecord(ctx->ev[2], st));
   if ((rc = launch_elements(ctx, ncell, S, dsz, dw, dK, dD, dB_, ddB, delem, st))) return rc;
   if (K_out) LB_CUDA(cudaMemcpyAsync(K_out, dK, sizeof(double) * 2 * S * n, cudaMemcpyDeviceToHost, st));
@@ -1148,10 +1241,12 @@ int lb_fused_sweep_all(lb_ctx* ctx, int n, int S, const double* r, const double*
   if (n == 0) return LB_OK;
   if (!r || !z || !w || !f || !df_r || !df_z || !coK || !coD || !K_out || !D_out)
     return fail(LB_EINVAL, "null argument");
+  Coupling cp;
+  make_coupling(S, coK, coD, cp);
   cudaStream_t st = ctx->stream;
   const size_t nin = (size_t)(3 + 3 * S) * n;
   if ((rc = ensure(ctx->in, nin * sizeof(double)))) return rc;
-  if ((rc = ensure(ctx->rec, (size_t)n * rec_stride(S) * sizeof(double)))) return rc;
+  if ((rc = ensure(ctx->rec, (size_t)n * record_stride(cp) * sizeof(double)))) return rc;
   if ((rc = ensure(ctx->out, (size_t)6 * S * n * sizeof(double)))) return rc;
   double* din = static_cast<double*>(ctx->in.p);
   double *dr = din, *dz = dr + n, *dw = dz + n, *df = dw + n, *dfr = df + (size_t)S * n,
@@ -1166,10 +1261,8 @@ int lb_fused_sweep_all(lb_ctx* ctx, int n, int S, const double* r, const double*
   LB_CUDA(cudaMemcpyAsync(dfr, df_r, bsn, cudaMemcpyHostToDevice, st));
   LB_CUDA(cudaMemcpyAsync(dfz, df_z, bsn, cudaMemcpyHostToDevice, st));
   double* drec = static_cast<double*>(ctx->rec.p);
-  if ((rc = launch_pack(ctx, n, S, dr, dz, dw, df, dfr, dfz, drec, st))) return rc;
-  Coupling cp;
-  make_coupling(S, coK, coD, cp);
-  if ((rc = all_points_sweep(ctx, n, S, drec, dr, dz, cp, mask_threshold(eps_d), dK, dD, st)))
+  if ((rc = launch_pack(ctx, n, S, dr, dz, dw, df, dfr, dfz, cp, drec, st))) return rc;
+  if ((rc = all_points_sweep(ctx, n, drec, dr, dz, cp, mask_threshold(eps_d), dK, dD, st)))
     return rc;
   LB_CUDA(cudaMemcpyAsync(K_out, dK, sizeof(double) * 2 * S * n, cudaMemcpyDeviceToHost, st));
   LB_CUDA(cudaMemcpyAsync(D_out, dD, sizeof(double) * 4 * S * n, cudaMemcpyDeviceToHost, st));
@@ -1177,17 +1270,29 @@ int lb_fused_sweep_all(lb_ctx* ctx, int n, int S, const double* r, const double*
   return LB_OK;
 }
 
-int lb_sym_supported(int S) { return (S >= 1 && S <= kSymMaxS) ? 1 : 0; }
+int lb_sym_supported(int S, const double* coK, const double* coD) {
+  if (S < 1 || S > LB_MAX_SPECIES) return 0;
+  if (!coK || !coD) return S <= kSymMaxS ? 1 : 0;
+  Coupling cp;
+  make_coupling(S, coK, coD, cp);
+  return cp.Se <= kSymMaxS ? 1 : 0;
+}
 
 int lb_sym_npad(int n) { return ((std::max(n, 0) + kSymTile - 1) / kSymTile) * kSymTile; }
 
-int lb_sym_prepare_dev(lb_ctx* ctx, int n, int S, const double* rec, void* stream) {
+int lb_sym_prepare_dev(lb_ctx* ctx, int n, int S, const double* coK, const double* coD,
+                       const double* rec, void* stream) {
   int rc = use_ctx(ctx);
   if (rc) return rc;
-  if (!lb_sym_supported(S))
-    return fail(LB_EINVAL, "symmetric sweep supports 1 <= S <= " + std::to_string(kSymMaxS));
+  if ((rc = check_species(S))) return rc;
   if (n < 1) return fail(LB_EINVAL, "symmetric sweep needs n >= 1");
-  return sym_prepare(ctx, n, S, rec, (cudaStream_t)stream);
+  if (!coK || !coD) return fail(LB_EINVAL, "null coupling table");
+  Coupling cp;
+  make_coupling(S, coK, coD, cp);
+  if (cp.Se > kSymMaxS)
+    return fail(LB_EINVAL, "symmetric sweep supports at most " + std::to_string(kSymMaxS) +
+                               " accumulator species sets");
+  return sym_prepare(ctx, n, cp, rec, (cudaStream_t)stream);
 }
 
 int lb_sym_partial_dev(lb_ctx* ctx, int S, double eps_d, int rank, int world, double* tot,
@@ -1196,7 +1301,8 @@ int lb_sym_partial_dev(lb_ctx* ctx, int S, double eps_d, int rank, int world, do
   if (rc) return rc;
   if (ctx->sym_n < 0 || ctx->sym_S != S) return fail(LB_EINVAL, "lb_sym_prepare_dev not called for this S");
   if (world < 1 || rank < 0 || rank >= world) return fail(LB_EINVAL, "bad rank / world");
-  return sym_partial_dispatch(ctx, S, mask_threshold(eps_d), rank, world, tot, (cudaStream_t)stream);
+  return sym_partial_dispatch(ctx, ctx->sym_Se, mask_threshold(eps_d), rank, world, tot,
+                              (cudaStream_t)stream);
 }
 
 int lb_sym_combine_dev(lb_ctx* ctx, int S, const double* tot, const double* coK, const double* coD,
@@ -1208,7 +1314,8 @@ int lb_sym_combine_dev(lb_ctx* ctx, int S, const double* tot, const double* coK,
   if (!coK || !coD) return fail(LB_EINVAL, "null coupling table");
   Coupling cp;
   make_coupling(S, coK, coD, cp);
-  return sym_combine_dispatch(ctx, S, tot, cp, q0, q1, K_out, D_out, (cudaStream_t)stream);
+  if (cp.Se != ctx->sym_Se) return fail(LB_EINVAL, "coupling differs from lb_sym_prepare_dev's");
+  return sym_combine_dispatch(ctx, cp.Se, tot, cp, q0, q1, K_out, D_out, (cudaStream_t)stream);
 }
 
 int lb_mesh_create(lb_ctx* ctx, int ncell, const double* cell_sizes, const double* B,
@@ -1274,10 +1381,12 @@ int lb_assemble_csr(lb_ctx* ctx, const lb_mesh* mesh, int S, const double* r, co
   if (ncell == 0) return LB_OK;
   if (!r || !z || !w || !f || !df_r || !df_z || !coK || !coD || !csr_out)
     return fail(LB_EINVAL, "null argument");
+  Coupling cp;
+  make_coupling(S, coK, coD, cp);
   cudaStream_t st = ctx->stream;
   const size_t nin = (size_t)(3 + 3 * S) * n;
   if ((rc = ensure(ctx->in, nin * sizeof(double)))) return rc;
-  if ((rc = ensure(ctx->rec, (size_t)n * rec_stride(S) * sizeof(double)))) return rc;
+  if ((rc = ensure(ctx->rec, (size_t)n * record_stride(cp) * sizeof(double)))) return rc;
   if ((rc = ensure(ctx->out, (size_t)6 * S * n * sizeof(double)))) return rc;
   if ((rc = ensure(ctx->elem, ((size_t)81 * S * ncell + (size_t)S * mesh->nslots) * sizeof(double))))
     return rc;
@@ -1297,11 +1406,9 @@ int lb_assemble_csr(lb_ctx* ctx, const lb_mesh* mesh, int S, const double* r, co
   LB_CUDA(cudaMemcpyAsync(dfr, df_r, bsn, cudaMemcpyHostToDevice, st));
   LB_CUDA(cudaMemcpyAsync(dfz, df_z, bsn, cudaMemcpyHostToDevice, st));
   double* drec = static_cast<double*>(ctx->rec.p);
-  if ((rc = launch_pack(ctx, n, S, dr, dz, dw, df, dfr, dfz, drec, st))) return rc;
+  if ((rc = launch_pack(ctx, n, S, dr, dz, dw, df, dfr, dfz, cp, drec, st))) return rc;
   LB_CUDA(cudaEventRecord(ctx->ev[1], st));
-  Coupling cp;
-  make_coupling(S, coK, coD, cp);
-  if ((rc = all_points_sweep(ctx, n, S, drec, dr, dz, cp, mask_threshold(eps_d), dK, dD, st)))
+  if ((rc = all_points_sweep(ctx, n, drec, dr, dz, cp, mask_threshold(eps_d), dK, dD, st)))
     return rc;
   LB_CUDA(cudaEventRecord(ctx->ev[2], st));
   if ((rc = launch_elements(ctx, ncell, S, mesh->sizes, dw, dK, dD, mesh->basis, mesh->basis + 81,
@@ -1396,10 +1503,12 @@ int lb_assemble_state(lb_ctx* ctx, const lb_mesh* m, int S, const double* coeffs
   if (!coeffs || !coK || !coD || !csr_out) return fail(LB_EINVAL, "null argument");
   const int ncell = m->ncell, n = 9 * ncell;
   if (ncell == 0) return LB_OK;
+  Coupling cp;
+  make_coupling(S, coK, coD, cp);
   cudaStream_t st = ctx->stream;
   const size_t nin = (size_t)(3 + 3 * S) * n + (size_t)S * m->n_free;
   if ((rc = ensure(ctx->in, nin * sizeof(double)))) return rc;
-  if ((rc = ensure(ctx->rec, (size_t)n * rec_stride(S) * sizeof(double)))) return rc;
+  if ((rc = ensure(ctx->rec, (size_t)n * record_stride(cp) * sizeof(double)))) return rc;
   if ((rc = ensure(ctx->out, (size_t)6 * S * n * sizeof(double)))) return rc;
   if ((rc = ensure(ctx->elem, ((size_t)81 * S * ncell + (size_t)S * m->nslots) * sizeof(double))))
     return rc;
@@ -1417,11 +1526,9 @@ int lb_assemble_state(lb_ctx* ctx, const lb_mesh* m, int S, const double* coeffs
                                                     m->P_idx, m->P_w, dco, dr, dz, dw, df, dfr, dfz);
   LB_CUDA(cudaGetLastError());
   double* drec = static_cast<double*>(ctx->rec.p);
-  if ((rc = launch_pack(ctx, n, S, dr, dz, dw, df, dfr, dfz, drec, st))) return rc;
+  if ((rc = launch_pack(ctx, n, S, dr, dz, dw, df, dfr, dfz, cp, drec, st))) return rc;
   LB_CUDA(cudaEventRecord(ctx->ev[1], st));
-  Coupling cp;
-  make_coupling(S, coK, coD, cp);
-  if ((rc = all_points_sweep(ctx, n, S, drec, dr, dz, cp, mask_threshold(eps_d), dK, dD, st)))
+  if ((rc = all_points_sweep(ctx, n, drec, dr, dz, cp, mask_threshold(eps_d), dK, dD, st)))
     return rc;
   LB_CUDA(cudaEventRecord(ctx->ev[2], st));
   if ((rc = launch_elements(ctx, ncell, S, m->sizes, dw, dK, dD, m->basis, m->basis + 81, delem, st)))

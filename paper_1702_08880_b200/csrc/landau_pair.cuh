@@ -152,8 +152,7 @@ struct T5 {
 
 // The symmetric part of one pair: B1..B5 (each / 4), dz, dz^2 and the mask.
 struct PairB {
-  double B1, B3, B4, B5, dz, dz2;
-  bool g;
+  double B1, B3, B4, B5, dz, dz2;  // B's are zero for masked pairs
 };
 
 // gthr = max(bits(eps^2), 1): the pair contributes iff bits(d^2) >= gthr,
@@ -234,15 +233,17 @@ __device__ __forceinline__ PairB pair_core(const Outer& o, double rn, double zn,
     const double c = fma(-2.0, EK, Em1 + EE);
     S3 = fma(4.0, fma(c, invm, -a) * invm, Em1);
   }
-  const double c3 = isP * invP;  // P^-3/2 (the 4 is folded into the coupling)
+  // mask (kernel.py:344) applied once: with isP := 0 every B, hence every
+  // tensor component of both orientations, is an exact (signed) zero
+  const double isPm = g ? isP : 0.0;
+  const double c3 = isPm * invP;  // P^-3/2 (the 4 is folded into the coupling)
   PairB p;
-  p.B1 = EK * isP;
+  p.B1 = EK * isPm;
   p.B3 = Em1 * c3;
   p.B4 = S2 * c3;
   p.B5 = S3 * c3;
   p.dz = dz;
   p.dz2 = dz2;
-  p.g = g;
   return p;
 }
 
@@ -256,10 +257,7 @@ __device__ __forceinline__ T5 pair_tensors(const Outer& o, double rn, double rn2
   t.xz = p.dz * fma(rn, p.B4, -(o.ri * p.B3));
   t.kr = fma(rr, p.B3 - p.B5, p.dz2 * p.B4);
   t.zr = p.dz * fma(rn, p.B3, -(o.ri * p.B4));
-  if (!p.g) {
-    t.xx = 0.0; t.zz = 0.0; t.xz = 0.0; t.kr = 0.0; t.zr = 0.0;
-  }
-  return t;
+  return t;  // masked pairs: all B are zero (pair_core), so is every component
 }
 
 // One (outer, inner) pair: the five tensor components / 4.
@@ -279,8 +277,7 @@ __device__ __forceinline__ double pair_tensor_sym(const Outer& o, double rn, dou
   const PairB p = pair_core(o, rn, zn, rcpr, gthr, logt);
   t = pair_tensors(o, rn, rn2, p);
   const double rr2 = o.tri * rn;
-  const double xx2 = fma(-o.ri2, p.B5, fma(rr2, p.B4, fma(-rn2, p.B3, p.B1)));
-  return p.g ? xx2 : 0.0;
+  return fma(-o.ri2, p.B5, fma(rr2, p.B4, fma(-rn2, p.B3, p.B1)));
 }
 
 }  // namespace lb

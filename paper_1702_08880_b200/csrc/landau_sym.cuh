@@ -289,40 +289,19 @@ __global__ void lb_sym_gather_kernel(int n, int npad, int RS, const int* __restr
 
 // K/D for original points [q0, q1) from the totals (sorted order) through
 // the inverse permutation; coupling as _combine (kernel.py:419-440).
-template <int S>
+template <int Se>
 __global__ void lb_sym_combine_kernel(const double* __restrict__ tot, int npad,
                                       const int* __restrict__ inv, int q0, int q1, const Coupling cp,
                                       double* __restrict__ K, double* __restrict__ D) {
   const int q = q0 + blockIdx.x * blockDim.x + threadIdx.x;
   if (q >= q1) return;
   const int p = inv[q];
-  double A[S][5];
+  double A[Se][5];
 #pragma unroll
-  for (int b = 0; b < S; ++b)
+  for (int b = 0; b < Se; ++b)
 #pragma unroll
     for (int c = 0; c < 5; ++c) A[b][c] = tot[(size_t)(b * 5 + c) * npad + p];
-  const int io = q - q0;
-#pragma unroll
-  for (int a = 0; a < S; ++a) {
-    double k0 = 0.0, k1 = 0.0, d0 = 0.0, d1 = 0.0, d2 = 0.0;
-#pragma unroll
-    for (int b = 0; b < S; ++b) {
-      const double ck = cp.coK4[a * S + b], cd = cp.coD4[a * S + b];
-      k0 = __dadd_rn(k0, __dmul_rn(ck, A[b][0]));
-      k1 = __dadd_rn(k1, __dmul_rn(ck, A[b][1]));
-      d0 = __dadd_rn(d0, __dmul_rn(cd, A[b][2]));
-      d1 = __dadd_rn(d1, __dmul_rn(cd, A[b][3]));
-      d2 = __dadd_rn(d2, __dmul_rn(cd, A[b][4]));
-    }
-    double* Ko = K + ((size_t)io * S + a) * 2;
-    double* Do = D + ((size_t)io * S + a) * 4;
-    Ko[0] = k0;
-    Ko[1] = k1;
-    Do[0] = d0;
-    Do[1] = d1;
-    Do[2] = d1;
-    Do[3] = d2;
-  }
+  write_kd<Se>(A, cp, (size_t)(q - q0), K, D);
 }
 
 __global__ void lb_invert_perm_kernel(int n, const int* __restrict__ perm, int* __restrict__ inv) {

@@ -102,7 +102,8 @@ class ShardedSweep:
             lib = _lib.load()
             self._lib = lib
             self._ctx = _lib.context(self.device.index or 0)
-            self.RS = lib.lb_record_stride(self.S)
+            p = _lib.dptr
+            self.RS = lib.lb_record_stride(self.S, p(self.coK), p(self.coD))
             if self.RS < 0:
                 _lib.check(1)
         else:
@@ -117,12 +118,14 @@ class ShardedSweep:
         else:
             self._sym_prepare, self._sym_partial = self._sym_prepare_cuda, self._sym_partial_cuda
             self._sym_combine = self._sym_combine_cuda
-            sym_ok = (pack_fn is None and sweep_fn is None
-                      and bool(self._lib.lb_sym_supported(self.S)) and self.n >= 128)
+            sym_ok = (pack_fn is None and sweep_fn is None and self.n >= 128 and bool(
+                self._lib.lb_sym_supported(self.S, _lib.dptr(self.coK), _lib.dptr(self.coD))))
         self.symmetric = sym_ok if symmetric is None else (bool(symmetric) and sym_ok)
-        if self.symmetric:
+        if self.symmetric:  # partial sums: 5 per accumulator set (1 set when collapsed)
             npad = -(-self.n // 128) * 128
-            self.tot = torch.zeros((5 * self.S, npad), dtype=torch.float64, device=self.device)
+            nacc = (self.RS - 4) // 3 if sym_fns is None else self.S
+            self.tot = torch.zeros((5 * max(nacc, 1), npad), dtype=torch.float64,
+                                   device=self.device)
         mc = self.plan.max_count
         f64 = torch.float64
         self.send = torch.zeros((mc, self.RS), dtype=f64, device=self.device)
@@ -143,9 +146,11 @@ class ShardedSweep:
 
     def _pack_cuda(self, r, z, w, f, dfr, dfz, out):
         n = r.shape[0]
+        p = _lib.dptr
         _lib.check(self._lib.lb_pack_records_dev(
             self._ctx.handle, n, self.S, r.data_ptr(), z.data_ptr(), w.data_ptr(), f.data_ptr(),
-            dfr.data_ptr(), dfz.data_ptr(), out.data_ptr(), self._stream()))
+            dfr.data_ptr(), dfz.data_ptr(), p(self.coK), p(self.coD), out.data_ptr(),
+            self._stream()))
         self.launches += self._lib.lb_last_launch_count(self._ctx.handle)
 
     def _sweep_cuda(self, ro, zo, rec, K, D):
@@ -157,8 +162,9 @@ class ShardedSweep:
         self.launches += self._lib.lb_last_launch_count(self._ctx.handle)
 
     def _sym_prepare_cuda(self, rec):
-        _lib.check(self._lib.lb_sym_prepare_dev(self._ctx.handle, self.n, self.S, rec.data_ptr(),
-                                                self._stream()))
+        p = _lib.dptr
+        _lib.check(self._lib.lb_sym_prepare_dev(self._ctx.handle, self.n, self.S, p(self.coK),
+                                                p(self.coD), rec.data_ptr(), self._stream()))
         self.launches += self._lib.lb_last_launch_count(self._ctx.handle)
 
     def _sym_partial_cuda(self, tot):

@@ -219,3 +219,33 @@ def test_species_mismatch_raises(gpu):
     g = golden("sweep_small")
     with pytest.raises(ValueError):
         gpu.fused_sweep(g["r"], g["z"], data_from(g), params_from(g, "nu1", "mro1"))
+
+
+@pytest.mark.parametrize("S,rank1", [(2, False), (3, False), (2, True), (4, True), (6, True)])
+def test_all_points_coupling_layouts(gpu, oracle, S, rank1):
+    """All-points sweep (symmetric path) for per-species accumulation (a
+    coupling that is not rank one) and for the species-collapsed layout (rank
+    one, the reference's own collision_params structure), vs the oracle."""
+    import paper_1702_08880_b200 as pkg
+
+    rng = np.random.default_rng(300 + S)
+    n = 3000 + 11 * S
+    r = rng.uniform(0.0, 3.0, n)
+    z = rng.uniform(-3.0, 3.0, n)
+    w = rng.uniform(0.1, 1.0, n)
+    f, dfr, dfz = (rng.standard_normal((S, n)) for _ in range(3))
+    if rank1:
+        e = rng.uniform(0.5, 3.0, S)
+        nu = np.outer(e**2, e**2)
+        nu = nu / nu[0, 0]
+    else:
+        nu = rng.uniform(0.5, 2.0, (S, S))
+    mro = rng.uniform(0.01, 1.0, S)
+    data = pkg.QuadPointData(N=n, r=r, z=z, w=w, f=f, df_r=dfr, df_z=dfz)
+    params = pkg.CollisionParams(nu_hat=nu, mass_ratio_o=mro)
+    K, D = gpu.fused_sweep(r, z, data, params, eps_d=1e-13)
+    Kr, Dr = oracle.fused_sweep(r, z, r, z, w, f, dfr, dfz, nu, mro, eps_d=1e-13)
+    err = worst_component(K, D, Kr, Dr)
+    print(f"all-points S={S} rank1={rank1}", err)
+    assert err < 1e-10
+    assert np.array_equal(D[..., 0, 1], D[..., 1, 0])
