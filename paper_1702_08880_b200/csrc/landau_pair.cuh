@@ -54,8 +54,9 @@ __constant__ double c_logt[2 << LB_LOGT_BITS] = LB_LOGT;
 constexpr long long kTinyBits = 0x01A56E1FC2F8F359LL;
 // bit pattern of sqrt(2) (mantissa fold threshold, kernel.py:324)
 constexpr long long kSqrt2Bits = 0x3FF6A09E667F3BCDLL;
-// bit pattern of 0.01, the series / closed-form switch (kernel.py:151)
-constexpr long long kMSwitchBits = 0x3F847AE147AE147BLL;
+// bit pattern of 0.99 = 1 - 0.01, the series / closed-form switch
+// (kernel.py:151) expressed on x = 1 - m
+constexpr long long kXSwitchBits = 0x3FEFAE147AE147AELL;
 
 __device__ __forceinline__ double rcp_approx(double a) {
   double r;
@@ -153,6 +154,7 @@ struct T5 {
 // The symmetric part of one pair: B1..B5 (each / 4), dz, dz^2 and the mask.
 struct PairB {
   double B1, B3, B4, B5, dz, dz2;  // B's are zero for masked pairs
+  double u;                         // B1 + 2 ri rn B4 (shared by UD_xx of both orientations)
 };
 
 // gthr = max(bits(eps^2), 1): the pair contributes iff bits(d^2) >= gthr,
@@ -171,7 +173,6 @@ __device__ __forceinline__ PairB pair_core(const Outer& o, double rn, double zn,
   const double isP = rsqrt_nr(P);
   const double invP = isP * isP;
   const double x = d2 * invP;
-  const double m = tq * invP;
   const double lx = log_table(x, logt);
 
 #if LB_ESTRIN
@@ -209,11 +210,14 @@ __device__ __forceinline__ PairB pair_core(const Outer& o, double rn, double zn,
 #endif
   const double EK = fma(-lx, qk, pk);
   const double EE = fma(-lx, qe, pe);
-  const double Em1 = EE * (P * rcp_nr(d2));  // E/(1-m)
+  const double Em1 = EE * rcp_nr(x);  // E/(1-m) = E P/d^2
 
   double S2, S3;
-  if (__double_as_longlong(m) < kMSwitchBits) {  // m < 0.01 (m >= 0: integer order)
+  // m < 0.01 (kernel.py:376) tested as x = 1 - m > 0.99 on the bit pattern;
+  // m itself is only needed by the series
+  if (__double_as_longlong(x) > kXSwitchBits) {
     // hypergeometric series (kernel.py:369-375)
+    const double m = tq * invP;
     double s2 = c_s2[9], s3 = c_s3[9];
     s2 = fma(s2, m, c_s2[8]);  s3 = fma(s3, m, c_s3[8]);
     s2 = fma(s2, m, c_s2[7]);  s3 = fma(s3, m, c_s3[7]);
@@ -244,15 +248,15 @@ __device__ __forceinline__ PairB pair_core(const Outer& o, double rn, double zn,
   p.B5 = S3 * c3;
   p.dz = dz;
   p.dz2 = dz2;
+  p.u = fma(o.tri * rn, p.B4, p.B1);
   return p;
 }
 
 // Direct-pair tensor components from the symmetric part.
 __device__ __forceinline__ T5 pair_tensors(const Outer& o, double rn, double rn2, const PairB& p) {
   const double rr = o.ri * rn;
-  const double rr2 = o.tri * rn;
   T5 t;
-  t.xx = fma(-rn2, p.B5, fma(rr2, p.B4, fma(-o.ri2, p.B3, p.B1)));
+  t.xx = fma(-rn2, p.B5, fma(-o.ri2, p.B3, p.u));
   t.zz = fma(-p.dz2, p.B3, p.B1);
   t.xz = p.dz * fma(rn, p.B4, -(o.ri * p.B3));
   t.kr = fma(rr, p.B3 - p.B5, p.dz2 * p.B4);
@@ -276,8 +280,7 @@ __device__ __forceinline__ double pair_tensor_sym(const Outer& o, double rn, dou
                                                   const double2* __restrict__ logt, T5& t) {
   const PairB p = pair_core(o, rn, zn, rcpr, gthr, logt);
   t = pair_tensors(o, rn, rn2, p);
-  const double rr2 = o.tri * rn;
-  return fma(-o.ri2, p.B5, fma(rr2, p.B4, fma(-rn2, p.B3, p.B1)));
+  return fma(-o.ri2, p.B5, fma(-rn2, p.B3, p.u));
 }
 
 }  // namespace lb
