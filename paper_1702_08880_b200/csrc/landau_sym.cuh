@@ -166,11 +166,15 @@ __global__ void __launch_bounds__(kSymTile, S <= 2 ? kSymMinBlocks : 2) lb_symsw
         for (int b = 0; b < S; ++b)
 #pragma unroll
           for (int q = 0; q < 5; ++q) jacc[b][q] = 0.0;
+        // (r, z) of the next step's record are loaded one step ahead so the
+        // shared-memory latency is off the pair's dependency chain
+        double2 rz_next = *reinterpret_cast<const double2*>(tile + (jb * 32 + lane) * RS);
 #pragma unroll kSymUnroll
         for (int st = 0; st < 32; ++st) {
           const int jl = (lane + st) & 31;
           const double* rp = tile + (jb * 32 + jl) * RS;
-          const double2 rz = *reinterpret_cast<const double2*>(rp);
+          const double2 rz = rz_next;
+          rz_next = *reinterpret_cast<const double2*>(tile + (jb * 32 + ((jl + 1) & 31)) * RS);
           const double2 aux = *reinterpret_cast<const double2*>(rp + 2);
           T5 t;
           const double txx2 = pair_tensor_sym(o, rz.x, rz.y, aux.x, aux.y, a.gthr, logt, t);
