@@ -269,6 +269,7 @@ def ours_arm(args):
     value = pairs_step * args.steps / (tot_ms * 1e-3)
     # roofline of the dominant kernel on this rank: model flops per launch / launch time
     sweep_avg_s = sum(sweep_ms) / len(sweep_ms) * 1e-3
+    nacc = (sh.RS - 4) // 3  # accumulator species sets (1: rank-one species collapse)
     # ordered pairs this rank's sweep delivers: its outer points x N (general
     # path) or its 1/world share of the tile pairs, each feeding both points
     flops_launch = pkg.flop_count(N, S, N / world if sh.symmetric else nloc)
@@ -351,8 +352,9 @@ def ours_arm(args):
             "roofline": {"bound": "fp64", "achieved": achieved_tf, "peak": fp64_sustained,
                          "unit": "TFLOP/s", "frac": achieved_tf / fp64_sustained,
                          "traffic": traffic,
-                         "kernel": ("lb_symsweep_kernel<2> + lb_symreduce_kernel" if sh.symmetric
-                                    else "lb_sweep_kernel<2> (+ lb_combine_kernel, <1%)"),
+                         "kernel": (f"lb_symsweep_kernel<{nacc}> + lb_symreduce_kernel" if sh.symmetric
+                                    else f"lb_sweep_kernel<{nacc}> (+ lb_combine_kernel, <1%)"),
+                         "species_collapsed": nacc == 1 and S > 1,
                          "flops": "model 165+20*S^2 per ordered pair (kernel.py:560-574)"
                                   + ("; symmetric path evaluates each unordered pair once, "
                                      "so model flops per executed flop is ~1.7 and frac may "
