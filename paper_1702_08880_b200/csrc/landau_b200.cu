@@ -27,6 +27,7 @@
 #include <algorithm>
 #include <cstdint>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -47,7 +48,19 @@ constexpr int kMinBlocks = LB_MINB;  // CTAs per SM the register budget targets
 constexpr int kUnroll = LB_UNROLL;   // inner pairs interleaved per loop trip
 constexpr int kMaxChunks = 64;  // inner chunks per sweep (sets the JC length)
 constexpr int kChunkAlign = 128;
-constexpr size_t kPartialBudget = size_t(2) << 30;  // bytes of chunk partials per pass
+// Scratch budgets for partial sums (bytes): general-path chunk partials per
+// outer batch and symmetric-path i/j-side partials per row batch.  The
+// batch sizes only depend on the problem size and these budgets; the
+// LB_PARTIAL_BUDGET_MB environment variable lowers them (tests use it to
+// exercise multi-batch runs at moderate N).
+size_t partial_budget() {
+  static size_t b = [] {
+    const char* e = std::getenv("LB_PARTIAL_BUDGET_MB");
+    const long long mb = e ? std::atoll(e) : 0;
+    return mb > 0 ? size_t(mb) << 20 : size_t(2) << 30;
+  }();
+  return b;
+}
 
 __host__ __device__ constexpr int rec_stride(int S) { return ((4 + 3 * S) + 1) & ~1; }
 template <int S>
@@ -774,7 +787,7 @@ int launch_sweep(lb_ctx* ctx, int nout, const double* ro, const double* zo, int 
   const int nchunk = (n + jc - 1) / jc;
   // outer batches bounded by the partial-buffer budget
   const size_t per_outer = size_t(nchunk) * 5 * S * sizeof(double);
-  int batch = (int)std::min<size_t>((size_t)nout, std::max<size_t>(kTI, kPartialBudget / per_outer));
+  int batch = (int)std::min<size_t>((size_t)nout, std::max<size_t>(kTI, partial_budget() / per_outer));
   batch = std::max(kTI, (batch / kTI) * kTI);
   for (int o0 = 0; o0 < nout; o0 += batch) {
     const int nb = std::min(batch, nout - o0);
@@ -831,7 +844,6 @@ int check_species(int S) {
 
 
 // ------------------------------------------------------------------ symmetric path (host)
-constexpr size_t kSymBudget = size_t(2) << 30;  // bytes of i/j-side partials per row batch
 
 int sym_prepare(lb_ctx* ctx, int n, const Coupling& cp, const double* rec, cudaStream_t st) {
   const int RS = record_stride(cp);
@@ -878,7 +890,7 @@ int sym_partial(lb_ctx* ctx, long long gthr, int rank, int world, double* tot, c
   per_sm = std::max(per_sm, 1);
   const size_t row_i = (size_t)nseg * 5 * S * kSymTile * sizeof(double);
   const size_t row_j = (size_t)std::max(hmax, 1) * 5 * S * kSymTile * sizeof(double);
-  const int RB = (int)std::max<size_t>(1, std::min<size_t>(R1 - R0, kSymBudget / (row_i + row_j)));
+  const int RB = (int)std::max<size_t>(1, std::min<size_t>(R1 - R0, partial_budget() / (row_i + row_j)));
   int rc;
   if ((rc = ensure(ctx->symi, row_i * RB))) return rc;
   if ((rc = ensure(ctx->symj, row_j * RB))) return rc;

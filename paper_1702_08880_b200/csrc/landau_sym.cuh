@@ -238,10 +238,12 @@ __global__ void __launch_bounds__(kSymTile, S <= 2 ? kSymMinBlocks : 2) lb_symsw
   }
 }
 
-// Fixed-order reduction of one row batch into the running totals
-// tot[5S][nt*128] (SoA): per point, its own row's i-side segments (if the
-// row is in the batch), then the j-side blocks of every batch row having
-// this tile as a partner, by increasing d.
+// Fixed-order reduction of one row batch [row0, row1) into the running
+// totals tot[5S][nt*128] (SoA): per point, its own row's i-side segments (if
+// the row is in the batch), then the j-side block of every batch row I that
+// has this tile as a partner (d = P - I mod nt in 1..H(I)), by increasing I.
+// Batches are processed in increasing row order, so each point's sum order
+// is a function of n (and the row-batch size) only.
 template <int S>
 __global__ void lb_symreduce_kernel(const double* __restrict__ iside, const double* __restrict__ jside,
                                     int nt, int row0, int row1, int nseg, int hmax, int first,
@@ -261,9 +263,9 @@ __global__ void lb_symreduce_kernel(const double* __restrict__ iside, const doub
       for (int c = 0; c < 5 * S; ++c) v[c] = __dadd_rn(v[c], src[(size_t)c * kSymTile]);
     }
   }
-  for (int d = 1; d <= hmax; ++d) {
-    const int I = (P - d + nt) % nt;
-    if (I < row0 || I >= row1 || d > sym_h(I, nt)) continue;
+  for (int I = row0; I < row1; ++I) {
+    const int d = (P - I + nt) % nt;
+    if (d < 1 || d > sym_h(I, nt)) continue;
     const double* src = jside + ((size_t)(I - row0) * hmax + (d - 1)) * (5 * S) * kSymTile + t;
 #pragma unroll
     for (int c = 0; c < 5 * S; ++c) v[c] = __dadd_rn(v[c], src[(size_t)c * kSymTile]);

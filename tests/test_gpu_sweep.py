@@ -249,3 +249,50 @@ def test_all_points_coupling_layouts(gpu, oracle, S, rank1):
     print(f"all-points S={S} rank1={rank1}", err)
     assert err < 1e-10
     assert np.array_equal(D[..., 0, 1], D[..., 1, 0])
+
+
+def test_multibatch_runs_match(gpu, oracle):
+    """Scratch-bounded batching (outer batches on the general path, row
+    batches on the symmetric path) at N = 2^15, forced with a 1 MiB budget in
+    a subprocess, agrees with the single-batch run and the oracle."""
+    import json
+    import os
+    import subprocess
+    import sys
+
+    code = r"""
+import json, sys, numpy as np
+sys.path.insert(0, '.')
+import paper_1702_08880_b200 as pkg
+from paper_1702_08880_b200 import synthetic
+wl = synthetic.cfg5(32768)
+d = pkg.QuadPointData(N=wl.N, r=wl.r, z=wl.z, w=wl.w, f=wl.f, df_r=wl.df_r, df_z=wl.df_z)
+p = pkg.CollisionParams(nu_hat=wl.nu_hat, mass_ratio_o=wl.mass_ratio_o)
+K, D = pkg.fused_sweep(wl.r, wl.z, d, p, eps_d=wl.eps_d)
+Kg, Dg = pkg.fused_sweep(wl.r[:-1], wl.z[:-1], d, p, eps_d=wl.eps_d)
+np.savez(sys.argv[1], K=K, D=D, Kg=Kg, Dg=Dg)
+"""
+    import tempfile
+
+    outs = []
+    for budget in (None, "1"):
+        env = dict(os.environ)
+        if budget:
+            env["LB_PARTIAL_BUDGET_MB"] = budget
+        with tempfile.NamedTemporaryFile(suffix=".npz", delete=False) as fh:
+            path = fh.name
+        subprocess.run([sys.executable, "-c", code, path], check=True, env=env,
+                       cwd=str(__import__("conftest").ROOT))
+        outs.append(np.load(path))
+    a, b = outs
+    e_sym = worst_component(b["K"], b["D"], a["K"], a["D"])
+    e_gen = worst_component(b["Kg"], b["Dg"], a["Kg"], a["Dg"])
+    print("multi-batch vs single: symmetric", e_sym, "general", e_gen)
+    assert e_sym < 1e-13 and e_gen < 1e-13
+    from paper_1702_08880_b200 import synthetic
+
+    wl = synthetic.cfg5(32768)
+    idx = np.arange(0, 32768, 97)
+    Kr, Dr = oracle.fused_sweep(wl.r[idx], wl.z[idx], wl.r, wl.z, wl.w, wl.f, wl.df_r, wl.df_z,
+                                wl.nu_hat, wl.mass_ratio_o, eps_d=wl.eps_d)
+    assert worst_component(b["K"][idx], b["D"][idx], Kr, Dr) < 1e-10
