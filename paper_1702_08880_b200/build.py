@@ -18,7 +18,7 @@ ROOT = PKG.parent
 CSRC = PKG / "csrc"
 LIB = PKG / "liblandau_b200.so"
 SOURCES = [CSRC / "landau_b200.cu"]
-DEPS = SOURCES + [CSRC / "landau_pair.cuh", CSRC / "landau_coefs.h", ROOT / "include" / "landau_b200.h"]
+DEPS = SOURCES + sorted(CSRC.glob("*.cuh")) + sorted(CSRC.glob("*.h")) + [ROOT / "include" / "landau_b200.h"]
 
 NVCC_FLAGS = [
     "-O3", "-std=c++17",

@@ -16,7 +16,7 @@
 //    d = nt/2 for I < nt/2 when nt is even -- every unordered tile pair once,
 //    every row the same length (balanced across CTAs and GPUs);
 //  * d = 0 is the diagonal tile, evaluated as ordered pairs (i-side only);
-//  * a work item is (row I, a segment of kSegLen consecutive d);
+//  * a work item is (row I, a segment of sym_seglen(nt) consecutive d);
 //  * inside a CTA each thread owns one i of I (registers), each warp walks
 //    the 128 j of J as 4 blocks of 32 in a rotated ("diagonal") order: at
 //    step s lane l takes j = (l + s) mod 32, so the 32 lanes touch 32
@@ -32,7 +32,7 @@
 
 constexpr int kSymTile = 128;   // points per tile (== threads per CTA)
 constexpr int kSymStages = 2;   // TMA ring depth (one J tile per stage)
-constexpr int kSegLen = 8;      // partner tiles per work item
+constexpr int kSegLenMax = 8;   // partner tiles per work item (large n)
 #ifndef LB_SYM_MINB
 #define LB_SYM_MINB 4
 #endif
@@ -52,8 +52,15 @@ __host__ __device__ __forceinline__ int sym_h(int I, int nt) {
   return ((nt & 1) == 0 && I < nt / 2) ? h + 1 : h;
 }
 __host__ __device__ __forceinline__ int sym_hmax(int nt) { return nt / 2; }
+// Segment length: 8 partner tiles per item for large n, shorter for small n
+// so there are enough items to fill the GPU (a function of n only, so the
+// summation order -- hence every bit of the result -- depends on n alone).
+__host__ __device__ __forceinline__ int sym_seglen(int nt) {
+  return max(1, min(kSegLenMax, nt / 64));
+}
 __host__ __device__ __forceinline__ int sym_nseg(int nt) {
-  return (sym_hmax(nt) + 1 + kSegLen - 1) / kSegLen;
+  const int L = sym_seglen(nt);
+  return (sym_hmax(nt) + 1 + L - 1) / L;
 }
 
 // j-side exchange buffer: 2 (double buffer) x 4 warps x 32 j x 5S doubles
@@ -115,8 +122,9 @@ __global__ void __launch_bounds__(kSymTile, S <= 2 ? kSymMinBlocks : 2) lb_symsw
   auto seg_range = [&](long long item, int& I, int& d0, int& d1) {
     I = a.row0 + (int)(item / a.nseg);
     const int seg = (int)(item % a.nseg);
-    d0 = seg * kSegLen;
-    d1 = min(sym_h(I, a.nt) + 1, d0 + kSegLen);
+    const int L = sym_seglen(a.nt);
+    d0 = seg * L;
+    d1 = min(sym_h(I, a.nt) + 1, d0 + L);
   };
   auto issue_next = [&]() {
     int I, d0, d1;
@@ -258,7 +266,7 @@ __global__ void lb_symreduce_kernel(const double* __restrict__ iside, const doub
   if (P >= row0 && P < row1) {
     for (int sg = 0; sg < nseg; ++sg) {
       const double* src = iside + ((size_t)(P - row0) * nseg + sg) * (5 * S) * kSymTile + t;
-      if (sg * kSegLen > sym_h(P, nt)) break;
+      if (sg * sym_seglen(nt) > sym_h(P, nt)) break;
 #pragma unroll
       for (int c = 0; c < 5 * S; ++c) v[c] = __dadd_rn(v[c], src[(size_t)c * kSymTile]);
     }
