@@ -148,7 +148,9 @@ def reference_arm(args):
     O.build()
     wl = synthetic.cfg5(args.n)
     threads = O.max_threads()
-    k, run = cpu_sample(wl, args.ref_step_seconds, threads)
+    # each step is a bounded sample sized so the whole run stays ~2 minutes
+    per_step = min(args.ref_step_seconds, 120.0 / max(args.steps + args.warmup, 1))
+    k, run = cpu_sample(wl, per_step, threads, min_outer=16)
     for _ in range(args.warmup):
         run(k)
     times = [run(k)[0] for _ in range(args.steps)]

@@ -241,6 +241,52 @@ def case_cfg2():
          masses=np.array([s.mass for s in sp_]), **blocks_parts("C", cm))
 
 
+def case_cfg3():
+    """BASELINE config 3, reference-native reading: Q2 on an
+    8x16 base (L=5) refined 3 rounds toward the origin and the thermal shell
+    |v| ~ 1 (hanging nodes), bi-Maxwellian electrons (T_par = 1.5 T_perp)
+    plus Maxwellian ions built directly as a StateVector; D/K, the operator,
+    and one frozen-coefficient Newton step (solver.py:103-134)."""
+    from axlandau.solver import StepConfig, newton_step
+
+    domain = ax.DomainSpec(L=5.0)
+    ref = ax.build_reference_element()
+    mesh = ax.cartesian_mesh(domain, 8, 16)
+    for _ in range(3):
+        o, sz = mesh.origins, mesh.sizes
+        rmin, rmax = o[:, 0], o[:, 0] + sz[:, 0]
+        zlo, zhi = o[:, 1], o[:, 1] + sz[:, 1]
+        zn = np.where((zlo <= 0) & (zhi >= 0), 0.0, np.minimum(abs(zlo), abs(zhi)))
+        vmin = np.hypot(rmin, zn)
+        vmax = np.hypot(rmax, np.maximum(abs(zlo), abs(zhi)))
+        mesh = ax.refine(mesh, np.where((vmin <= 0.7) | ((vmax >= 0.6) & (vmin <= 1.6)))[0])
+    sp_ = [ax.Species("e", 1.0, -1.0, 0.4), ax.Species("i", 4.0, 1.0, 0.2)]
+    r = mesh.nodes[mesh.free_nodes, 0]
+    z = mesh.nodes[mesh.free_nodes, 1]
+    s_perp, s_par = 2.0 * 0.4, 2.0 * 0.6  # sigma^2 = 2T/m, T_par = 1.5 T_perp
+    fe = 0.5 * (math.pi ** 1.5 * s_perp * math.sqrt(s_par)) ** -1 * np.exp(-r * r / s_perp - z * z / s_par)
+    fi = ax.physics.maxwellian_values(sp_[1], r, z)
+    state = ax.StateVector(np.stack([fe, fi]))
+    data = ax.sample_state(mesh, ref, state)
+    params = ax.collision_params(sp_)
+    eps_d = ax.assembly.default_eps_d(mesh)
+    idx = np.unique(np.linspace(0, data.N - 1, 1024).astype(np.int64))
+    K, D = ax.fused_sweep(data.r[idx], data.z[idx], data, params, eps_d=eps_d, workers=1)
+    cm = ax.assemble_collision(mesh, ref, data, params)
+    cfg = StepConfig(dt=0.1, max_newton=1)
+    M = ax.mass_matrix(mesh, ref)
+    nxt, rnorm = newton_step(state, state, mesh, ref, params, cfg, M=M)
+    moms0 = ax.moments(mesh, ref, state, sp_)
+    moms1 = ax.moments(mesh, ref, nxt, sp_)
+    save("cfg3", **mesh_parts(mesh, ref), **data_parts(data), **params_parts(params),
+         eps_d=np.float64(eps_d), idx=idx, K=K, D=D, coeffs=state.coeffs,
+         masses=np.array([s.mass for s in sp_]), **blocks_parts("C", cm), **csr_parts("M", M),
+         dt=np.float64(cfg.dt), newton_coeffs=nxt.coeffs, newton_rnorm=np.float64(rnorm),
+         Wm=moment_matrix(mesh, ref),
+         moms0=np.stack([moms0.n, moms0.p_z, moms0.E, moms0.q_z]),
+         moms1=np.stack([moms1.n, moms1.p_z, moms1.E, moms1.q_z]))
+
+
 def case_cfg4_species():
     """BASELINE config 4 species set (e, D, C6+, W10+; n = 1/0.8/0.02/0.001,
     T = 1/1/0.5/0.5; non-neutral, so the state is built directly with a
@@ -292,7 +338,7 @@ def main():
     which = set(sys.argv[1:])
     cases = {"pairs": case_pairs, "sweep_small": case_sweep_small, "cfg1": case_cfg1,
              "hanging": case_hanging, "cons": case_cons, "cfg2": case_cfg2,
-             "cfg4s": case_cfg4_species,
+             "cfg3": case_cfg3, "cfg4s": case_cfg4_species,
              "cfg5_4096": lambda: case_cfg5(4096),
              "cfg5_65536": lambda: case_cfg5(65536, n_sub=192)}
     for name, fn in cases.items():

@@ -29,7 +29,7 @@ def _block_err(cm, blocks_ref):
     return worst
 
 
-@pytest.mark.parametrize("case", ["cfg1", "hanging", "cfg2", "cons"])
+@pytest.mark.parametrize("case", ["cfg1", "hanging", "cfg2", "cons", "cfg3"])
 def test_blocks_match_reference(gpu, case):
     g, cm = _assemble(gpu, case)
     assert cm.n_species == int(g["C_count"])
@@ -116,7 +116,7 @@ def test_assembly_deterministic(gpu):
         assert np.array_equal(x.toarray(), y.toarray())
 
 
-@pytest.mark.parametrize("case", ["cfg1", "hanging", "cfg2", "cons"])
+@pytest.mark.parametrize("case", ["cfg1", "hanging", "cfg2", "cons", "cfg3"])
 def test_device_sampling_matches_reference(gpu, case):
     """Device sample_state (fem.py:170-199): r, z, w bitwise the reference's,
     f and grad f to rounding."""
@@ -141,3 +141,30 @@ def test_state_level_operator(gpu, case):
     print(case, "state-level jacobian", err)
     assert err < TOL
     assert np.array_equal(qd.r, g["r"]) and np.array_equal(qd.w, g["w"])
+
+
+def test_cfg3_newton_step(gpu):
+    """BASELINE config 3 (refined mesh with 168 hanging nodes, bi-Maxwellian
+    electrons + ions): one frozen-coefficient Newton step (solver.py:103-134)
+    with the device operator reproduces the reference's next state and
+    moments to 1e-10."""
+    g = golden("cfg3")
+    cm = gpu.assemble_at(mesh_from(g), ref_from(g), g["coeffs"], params_from(g))
+    assert _block_err(cm, blocks_from(g, "C")) < TOL
+    M = csr_from(g, "M")
+    dt = float(g["dt"])
+    f0 = g["coeffs"]
+    nxt = np.empty_like(f0)
+    for a in range(f0.shape[0]):
+        C = cm.blocks[a]
+        R = -0.5 * dt * (C @ f0[a] + C @ f0[a])  # residual(f, f, C, C, M, dt)
+        delta = spla.splu((M - 0.5 * dt * C).tocsc()).solve(-R)
+        nxt[a] = f0[a] + delta
+    ref = g["newton_coeffs"]
+    assert np.abs(nxt - ref).max() <= 1e-10 * np.abs(ref).max()
+    m = g["masses"]
+    moms = np.stack([g["Wm"] @ nxt[a] * np.array([1.0, m[a], m[a], m[a]]) for a in range(2)], 1)
+    rel = np.abs(moms - g["moms1"]) / np.maximum(np.abs(g["moms1"]), 1e-300)
+    print("cfg3 post-Newton moments rel", rel.max())
+    assert np.all(rel[[0, 2]] <= 1e-10)             # density, energy
+    assert np.all(np.abs(moms - g["moms1"])[[1, 3]] <= 1e-10 * np.abs(g["moms1"][[0, 2]]))

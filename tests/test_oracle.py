@@ -100,11 +100,11 @@ def test_proximity_mask(oracle):
     assert not np.allclose(Kw, Km, rtol=1e-8)
 
 
-@pytest.mark.parametrize("case", ["cfg1", "cfg2", "hanging"])
+@pytest.mark.parametrize("case", ["cfg1", "cfg2", "hanging", "cfg3"])
 def test_mesh_sweeps_match_reference(oracle, case):
     g = golden(case)
     eps = float(g["eps_d"]) if "eps_d" in g else 1e-14 * float(g["mesh_L"])
-    K, D = _sweep(oracle, g, eps_d=eps)
+    K, D = _sweep(oracle, g, idx=g["idx"] if "idx" in g else None, eps_d=eps)
     assert worst_component(K, D, g["K"], g["D"]) < TOL_SWEEP
 
 
