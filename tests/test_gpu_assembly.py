@@ -165,6 +165,7 @@ def test_cfg3_newton_step(gpu):
     m = g["masses"]
     moms = np.stack([g["Wm"] @ nxt[a] * np.array([1.0, m[a], m[a], m[a]]) for a in range(2)], 1)
     rel = np.abs(moms - g["moms1"]) / np.maximum(np.abs(g["moms1"]), 1e-300)
-    print("cfg3 post-Newton moments rel", rel.max())
+    print("cfg3 post-Newton density/energy rel", rel[[0, 2]].max(),
+          "p_z/q_z abs (scaled)", (np.abs(moms - g["moms1"])[[1, 3]] / np.abs(g["moms1"][[0, 2]])).max())
     assert np.all(rel[[0, 2]] <= 1e-10)             # density, energy
     assert np.all(np.abs(moms - g["moms1"])[[1, 3]] <= 1e-10 * np.abs(g["moms1"][[0, 2]]))
