@@ -166,6 +166,15 @@ int lb_assemble_state(lb_ctx *ctx, const lb_mesh *mesh, int S, const double *coe
                       const double *coK, const double *coD, double eps_d, double *csr_out,
                       double *data_out, double *phase_ms);
 
+/* Element contraction + CSR scatter/condensation from given accumulators:
+ * w (9*ncell) outer weights, K (9*ncell,S,2), D (9*ncell,S,2,2) host arrays
+ * of the mesh's points -> csr_out (S, nslots).  With per-species meshes the
+ * accumulators come from one all-points sweep over the union of the
+ * species' point sets; each species' block is assembled on
+ * its own mesh (assembly.py:151-169). */
+int lb_elements_csr(lb_ctx *ctx, const lb_mesh *mesh, int S, const double *w, const double *K,
+                    const double *D, double *csr_out);
+
 /* Per-pair closed form on the device: replaces `axisym_tensor_pair`
  * (kernel.py:206-235) for npair independent (r, z, rbar, zbar) tuples, with
  * the same device arithmetic the sweep uses.  UK, UD: (npair, 2, 2).

@@ -19,6 +19,7 @@ from .assembly import (
     CollisionMatrix,
     assemble_at,
     assemble_collision,
+    assemble_species_meshes,
     default_eps_d,
     element_matrices,
     sample_state,
@@ -88,7 +89,7 @@ def uninstall(axlandau_pkg, saved: dict) -> None:
 
 __all__ = [
     "Accumulators", "CollisionMatrix", "CollisionParams", "LandauTensorPair",
-    "QuadPointData", "assemble_at", "assemble_collision", "sample_state", "axisym_tensor_pair", "axisym_tensor_pairs",
+    "QuadPointData", "assemble_at", "assemble_collision", "assemble_species_meshes", "sample_state", "axisym_tensor_pair", "axisym_tensor_pairs",
     "coupling", "default_eps_d", "element_matrices", "flop_count", "fused_inner_loop",
     "fused_sweep", "install", "uninstall",
 ]

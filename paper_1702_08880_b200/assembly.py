@@ -28,7 +28,8 @@ from .kernel import _f64, _inner_fields, _n_species, coupling
 from .scatter import build_gather_map
 
 __all__ = ["CollisionMatrix", "DeviceMesh", "assemble_at", "assemble_collision",
-           "default_eps_d", "device_mesh", "element_matrices", "sample_state"]
+           "assemble_species_meshes", "default_eps_d", "device_mesh", "element_matrices",
+           "sample_state", "union_point_data"]
 
 
 def default_eps_d(mesh) -> float:
@@ -280,3 +281,65 @@ def sample_state(mesh, ref, state):
 
     return QuadPointData(N=n, r=h[0], z=h[1], w=h[2], f=h[3:3 + S], df_r=h[3 + S:3 + 2 * S],
                          df_z=h[3 + 2 * S:3 + 3 * S])
+
+
+def union_point_data(datas):
+    """Species-tagged union of per-species point sets:
+    datas[a] is species a's QuadPointData on its own mesh (one species row,
+    or S rows of which row a is used); the union carries species a's fields
+    on its own points and exact zeros elsewhere, so one all-points sweep over
+    the union is the exact multi-mesh D/K.  Returns (QuadPointData, offsets)."""
+    from .kernel import QuadPointData
+
+    S = len(datas)
+    ns = [int(np.asarray(d.r).shape[0]) for d in datas]
+    off = np.concatenate([[0], np.cumsum(ns)]).astype(np.int64)
+    n = int(off[-1])
+    f = np.zeros((S, n))
+    dfr = np.zeros((S, n))
+    dfz = np.zeros((S, n))
+    for a, d in enumerate(datas):
+        row = 0 if np.atleast_2d(d.f).shape[0] == 1 else a
+        sl = slice(off[a], off[a + 1])
+        f[a, sl] = np.atleast_2d(d.f)[row]
+        dfr[a, sl] = np.atleast_2d(d.df_r)[row]
+        dfz[a, sl] = np.atleast_2d(d.df_z)[row]
+    cat = lambda k: np.ascontiguousarray(np.concatenate([np.asarray(getattr(d, k)) for d in datas]))  # noqa: E731
+    return QuadPointData(N=n, r=cat("r"), z=cat("z"), w=cat("w"), f=f, df_r=dfr, df_z=dfz), off
+
+
+def assemble_species_meshes(meshes, ref, datas, params, eps_d: float | None = None):
+    """C_a for species a on its OWN mesh (the paper's per-species meshes,
+    PAPER.md section 3.0.2; BASELINE configs 2 and 4 as worded).  One
+    all-points sweep over the species-tagged union point set (symmetric,
+    species-collapsed) gives every point's K/D; species a's block is then the
+    element contraction + scatter on mesh a with its points' K[:, a], D[:, a]
+    (`lb_elements_csr`).  eps_d defaults to 1e-14 * min_a L_a.
+    Returns (list of S CSR blocks, (K, D) of the union points)."""
+    from .kernel import fused_sweep
+
+    S = _n_species(params)
+    if len(meshes) != S or len(datas) != S:
+        raise ValueError("need one mesh and one QuadPointData per species")
+    if eps_d is None:
+        eps_d = min(default_eps_d(m) for m in meshes)
+    union, off = union_point_data(datas)
+    K, D = fused_sweep(union.r, union.z, union, params, eps_d=eps_d)
+    blocks = []
+    for a, mesh in enumerate(meshes):
+        dm = device_mesh(mesh, ref)
+        gm = dm.map
+        sl = slice(off[a], off[a + 1])
+        if off[a + 1] - off[a] != 9 * dm.ncell:
+            raise ValueError(f"species {a}: data points do not match its mesh")
+        w = np.ascontiguousarray(union.w[sl])
+        Ka = np.ascontiguousarray(K[sl, a:a + 1])
+        Da = np.ascontiguousarray(D[sl, a:a + 1])
+        csr = np.empty((1, gm.nnz))
+        if dm.ncell:
+            ctx = _lib.context()
+            p = _lib.dptr
+            _lib.check(_lib.load().lb_elements_csr(ctx.handle, dm.handle, 1, p(w), p(Ka), p(Da),
+                                                   p(csr)))
+        blocks.append(sp.csr_matrix((csr[0], gm.indices, gm.indptr), shape=(gm.n_free, gm.n_free)))
+    return blocks, (K, D)

@@ -1565,6 +1565,39 @@ int lb_assemble_state(lb_ctx* ctx, const lb_mesh* m, int S, const double* coeffs
   return LB_OK;
 }
 
+int lb_elements_csr(lb_ctx* ctx, const lb_mesh* m, int S, const double* w, const double* K,
+                    const double* D, double* csr_out) {
+  int rc = use_ctx(ctx);
+  if (rc) return rc;
+  if ((rc = check_species(S))) return rc;
+  if (!m || m->device != ctx->device) return fail(LB_EINVAL, "mesh handle missing or on another device");
+  if (!w || !K || !D || !csr_out) return fail(LB_EINVAL, "null argument");
+  const int ncell = m->ncell, n = 9 * ncell;
+  if (ncell == 0) return LB_OK;
+  cudaStream_t st = ctx->stream;
+  if ((rc = ensure(ctx->in, (size_t)(1 + 6 * S) * n * sizeof(double)))) return rc;
+  if ((rc = ensure(ctx->elem, ((size_t)81 * S * ncell + (size_t)S * m->nslots) * sizeof(double))))
+    return rc;
+  double* dw = static_cast<double*>(ctx->in.p);
+  double* dK = dw + n;
+  double* dD = dK + (size_t)2 * S * n;
+  double* delem = static_cast<double*>(ctx->elem.p);
+  double* dcsr = delem + (size_t)81 * S * ncell;
+  LB_CUDA(cudaMemcpyAsync(dw, w, sizeof(double) * n, cudaMemcpyHostToDevice, st));
+  LB_CUDA(cudaMemcpyAsync(dK, K, sizeof(double) * 2 * S * n, cudaMemcpyHostToDevice, st));
+  LB_CUDA(cudaMemcpyAsync(dD, D, sizeof(double) * 4 * S * n, cudaMemcpyHostToDevice, st));
+  if ((rc = launch_elements(ctx, ncell, S, m->sizes, dw, dK, dD, m->basis, m->basis + 81, delem, st)))
+    return rc;
+  if (m->nslots) {
+    lb_csr_gather_kernel<<<(m->nslots + 255) / 256, 256, 0, st>>>(m->nslots, 81 * ncell, S, m->slot_ptr,
+                                                                   m->gidx, m->gw, delem, dcsr);
+    LB_CUDA(cudaGetLastError());
+  }
+  LB_CUDA(cudaMemcpyAsync(csr_out, dcsr, sizeof(double) * S * m->nslots, cudaMemcpyDeviceToHost, st));
+  LB_CUDA(cudaStreamSynchronize(st));
+  return LB_OK;
+}
+
 int lb_tensor_pairs(lb_ctx* ctx, int npair, const double* r, const double* z, const double* rbar,
                     const double* zbar, double* UK, double* UD) {
   int rc = use_ctx(ctx);

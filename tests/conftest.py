@@ -26,6 +26,19 @@ def golden(name: str):
     return np.load(GOLDEN / f"{name}.npz")
 
 
+class Prefixed:
+    """View of a fixture with keys 'prefix' + k (per-species mesh fixtures)."""
+
+    def __init__(self, g, prefix):
+        self.g, self.p = g, prefix
+
+    def __getitem__(self, k):
+        return self.g[self.p + k]
+
+    def __contains__(self, k):
+        return (self.p + k) in self.g
+
+
 def csr_from(g, prefix):
     shape = tuple(int(v) for v in g[f"{prefix}_shape"])
     return sp.csr_matrix((g[f"{prefix}_data"], g[f"{prefix}_indices"], g[f"{prefix}_indptr"]),

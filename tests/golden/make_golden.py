@@ -315,6 +315,76 @@ def case_cfg4_species():
          idx=idx, K=K, D=D)
 
 
+def _species_meshes_case(name, spec, grid, seed=None):
+    """Per-species meshes (PAPER.md 3.0.2; BASELINE configs 2 / 4 as
+    worded): species a on its own uniform grid over L_a = 5 sigma_a.  The
+    composed reference oracle: one reference fused_sweep
+    over the species-tagged union point set (f_b = 0 off mesh b; exact), then
+    each species' transform + contraction + condensation on its own mesh
+    (assembly.py:151-169 restated in oracle/oracle.py, pinned against the
+    reference by tests/test_oracle.py)."""
+    sys.path.insert(0, str(HERE.parents[1]))
+    from oracle import oracle as O
+
+    ref = ax.build_reference_element()
+    sp_ = [ax.Species(nm, m, q, T) for nm, m, q, _, T in spec]
+    params = ax.collision_params(sp_)
+    rng = np.random.default_rng(seed) if seed is not None else None
+    meshes, datas, coeffs = [], [], []
+    for (nm, m, q, dens, T), s in zip(spec, sp_):
+        mesh = ax.cartesian_mesh(ax.DomainSpec(L=5.0 * math.sqrt(s.sigma2)), *grid)
+        st = ax.maxwellian_init(mesh, ref, [s], neutralize=False)
+        st.coeffs *= 2.0 * dens  # the reference prefactor is 1/2 (physics.py:97-100)
+        if rng is not None:
+            st.coeffs *= 1.0 + 0.01 * rng.standard_normal(st.coeffs.shape)
+        meshes.append(mesh)
+        coeffs.append(st.coeffs[0])
+        datas.append(ax.sample_state(mesh, ref, st))
+    S = len(spec)
+    ns = [d.N for d in datas]
+    off = np.concatenate([[0], np.cumsum(ns)])
+    n = int(off[-1])
+    f = np.zeros((S, n)); dfr = np.zeros((S, n)); dfz = np.zeros((S, n))
+    for a, d in enumerate(datas):
+        f[a, off[a]:off[a + 1]] = d.f[0]
+        dfr[a, off[a]:off[a + 1]] = d.df_r[0]
+        dfz[a, off[a]:off[a + 1]] = d.df_z[0]
+    union = ax.QuadPointData(N=n, r=np.concatenate([d.r for d in datas]),
+                             z=np.concatenate([d.z for d in datas]),
+                             w=np.concatenate([d.w for d in datas]), f=f, df_r=dfr, df_z=dfz)
+    eps_d = min(ax.assembly.default_eps_d(m) for m in meshes)
+    K, D = ax.fused_sweep(union.r, union.z, union, params, eps_d=eps_d, workers=1)
+    out = {"S": np.int64(S), "eps_d": np.float64(eps_d), "offsets": off, "K": K, "D": D,
+           **params_parts(params), "masses": np.array([s.mass for s in sp_])}
+    for a, (mesh, d) in enumerate(zip(meshes, datas)):
+        sl = slice(off[a], off[a + 1])
+        elem = O.element_matrices(K[sl, a:a + 1], D[sl, a:a + 1], d.w, mesh.sizes, ref.B, ref.dB)
+        blk = O.condense(elem, mesh.cell_nodes, mesh.n_nodes, mesh.prolongation)[0]
+        for k, v in mesh_parts(mesh, ref).items():
+            out[f"s{a}_{k}"] = v
+        for k, v in data_parts(d).items():
+            out[f"s{a}_{k}"] = v
+        out.update(csr_parts(f"s{a}_C", blk))
+        out[f"s{a}_coeffs"] = coeffs[a]
+    save(name, **out)
+
+
+def case_cfg2_meshes():
+    """Config 2 as worded: e and D (m = 3670), T_e = 2 T_i, each on its own
+    16x32 mesh scaled to its thermal speed (9216 union points)."""
+    _species_meshes_case("cfg2m", [("e", 1.0, -1.0, 1.0, 0.5), ("D", 3670.0, 1.0, 1.0, 0.25)],
+                         (16, 32))
+
+
+def case_cfg4_meshes():
+    """Config 4 as worded but on 8x16 meshes (the 64x128 union of 294,912
+    points is beyond the reference's CPU budget): e, D, C6+, W10+ each on its
+    own mesh, densities 1/0.8/0.02/0.001, T 1/1/0.5/0.5, 1 % seeded noise."""
+    _species_meshes_case("cfg4m", [("e", 1.0, -1.0, 1.0, 1.0), ("D", 3670.0, 1.0, 0.8, 1.0),
+                                   ("C", 21900.0, 6.0, 0.02, 0.5),
+                                   ("W", 335000.0, 10.0, 0.001, 0.5)], (8, 16), seed=4)
+
+
 def case_cfg5(N, n_sub=None):
     """BASELINE config 5 recipe (paper_1702_08880_b200/synthetic.py).  Full
     N^2 when n_sub is None, else n_sub evenly spaced outer points plus the 64
@@ -338,7 +408,8 @@ def main():
     which = set(sys.argv[1:])
     cases = {"pairs": case_pairs, "sweep_small": case_sweep_small, "cfg1": case_cfg1,
              "hanging": case_hanging, "cons": case_cons, "cfg2": case_cfg2,
-             "cfg3": case_cfg3, "cfg4s": case_cfg4_species,
+             "cfg3": case_cfg3, "cfg4s": case_cfg4_species, "cfg2m": case_cfg2_meshes,
+             "cfg4m": case_cfg4_meshes,
              "cfg5_4096": lambda: case_cfg5(4096),
              "cfg5_65536": lambda: case_cfg5(65536, n_sub=192)}
     for name, fn in cases.items():
