@@ -87,23 +87,26 @@ __device__ __forceinline__ double rsqrt_nr(double a) {
   return fma(ye, c, y);
 }
 
-// ln(x) for normal positive x (the reference uses an exponent/mantissa split
-// + atanh series, kernel.py:317-337; any log accurate to ~1 ulp agrees to
-// 1e-16).  Here: table-driven reduction, no divide.  The mantissa is folded
-// around 1 (z in [0.6875, 1.375)), a 128-entry table gives invc ~ 1/z and
-// logc = -ln(invc) (invc == 1 exactly on the two bins touching 1.0, so ln x
-// keeps full relative accuracy as x -> 1), r = z*invc - 1 (|r| < 2^-7, one
-// FMA), ln(1+r) = r + r^2 q(r) with q the degree-6 Taylor tail.
-// Measured max relative error 2.2e-16 (tools/gen_coefs.py table).
 constexpr long long kLogOff = 0x3FE6000000000000LL;
-__device__ __forceinline__ double log_table(double x, const double2* __restrict__ tab) {
+
+// Stage 1 of the log: table lookup and argument reduction.  Returns r with
+// |r| < 2^-7; logc and the exponent (as a double) are written to the refs.
+__device__ __forceinline__ double log_reduce(double x, const double2* __restrict__ tab,
+                                             double& logc, double& kd) {
   const long long ix = __double_as_longlong(x);
   const long long tmp = ix - kLogOff;
   const int i = (int)((tmp >> (52 - LB_LOGT_BITS)) & ((1 << LB_LOGT_BITS) - 1));
   const int k = (int)(tmp >> 52);
   const double z = __longlong_as_double(ix - (tmp & (long long)0xFFF0000000000000ULL));
   const double2 t = tab[i];  // (invc, logc)
-  const double r = fma(z, t.x, -1.0);
+  logc = t.y;
+  // exact int -> double: 2^52 + 2^31 + k, minus the same magic
+  kd = __longlong_as_double(0x4330000080000000LL + (long long)k) - c_misc[11];
+  return fma(z, t.x, -1.0);
+}
+
+// Stage 2 of the log: ln x = k ln2 + logc + ln(1 + r).
+__device__ __forceinline__ double log_finish(double r, double logc, double kd) {
 #if LB_ESTRIN
   // q(r) = -1/2 + r/3 - r^2/4 + r^3/5 - r^4/6 + r^5/7 - r^6/8, depth 3
   const double r2 = r * r;
@@ -119,9 +122,21 @@ __device__ __forceinline__ double log_table(double x, const double2* __restrict_
   q = fma(q, r, -0.5);
   const double l1p = fma(r * r, q, r);
 #endif
-  // exact int -> double: 2^52 + 2^31 + k, minus the same magic
-  const double kd = __longlong_as_double(0x4330000080000000LL + (long long)k) - c_misc[11];
-  return fma(kd, c_misc[9], t.y + l1p);
+  return fma(kd, c_misc[9], logc + l1p);
+}
+
+// ln(x) for normal positive x (the reference uses an exponent/mantissa split
+// + atanh series, kernel.py:317-337; any log accurate to ~1 ulp agrees to
+// 1e-16).  Here: table-driven reduction, no divide.  The mantissa is folded
+// around 1 (z in [0.6875, 1.375)), a 128-entry table gives invc ~ 1/z and
+// logc = -ln(invc) (invc == 1 exactly on the two bins touching 1.0, so ln x
+// keeps full relative accuracy as x -> 1), r = z*invc - 1 (|r| < 2^-7, one
+// FMA), ln(1+r) = r + r^2 q(r) with q the degree-6 Taylor tail.
+// Measured max relative error 2.2e-16 (tools/gen_coefs.py table).
+__device__ __forceinline__ double log_table(double x, const double2* __restrict__ tab) {
+  double logc, kd;
+  const double r = log_reduce(x, tab, logc, kd);
+  return log_finish(r, logc, kd);
 }
 
 // Per-outer-point invariants (hoisted out of the pair loop).
@@ -159,21 +174,40 @@ struct PairB {
 
 // gthr = max(bits(eps^2), 1): the pair contributes iff bits(d^2) >= gthr,
 // i.e. d^2 >= eps^2 and d^2 > 0 (kernel.py:344).
-__device__ __forceinline__ PairB pair_core(const Outer& o, double rn, double zn, double rcpr,
-                                           long long gthr, const double2* __restrict__ logt) {
+// Stage 1 of a pair: geometry, mask, 1/sqrt(P), x and the log's table
+// lookup -- the long-latency front (MUFU, shared-memory table) that the
+// symmetric sweep issues one step ahead of the rest.
+struct PairS1 {
+  double dz, dz2, P, tq, isPm, invP, x, lr, logc, kd;
+};
+
+__device__ __forceinline__ PairS1 pair_stage1(const Outer& o, double rn, double zn, long long gthr,
+                                              const double2* __restrict__ logt) {
+  PairS1 s;
   const double dr = o.ri - rn;
-  const double dz = o.zi - zn;
-  const double dz2 = dz * dz;
-  const double dist2 = fma(dr, dr, dz2);
+  s.dz = o.zi - zn;
+  s.dz2 = s.dz * s.dz;
+  const double dist2 = fma(dr, dr, s.dz2);
   const long long di = __double_as_longlong(dist2);
-  const bool g = di >= gthr;
+  const bool g = di >= gthr;  // d^2 >= eps^2 and d^2 > 0 (kernel.py:344)
   const double d2 = di > kTinyBits ? dist2 : 1.0;
-  const double tq = o.fri * rn;  // 4 ri rn
-  const double P = d2 + tq;
-  const double isP = rsqrt_nr(P);
-  const double invP = isP * isP;
-  const double x = d2 * invP;
-  const double lx = log_table(x, logt);
+  s.tq = o.fri * rn;  // 4 ri rn
+  s.P = d2 + s.tq;
+  const double isP = rsqrt_nr(s.P);
+  s.invP = isP * isP;
+  s.x = d2 * s.invP;
+  // mask (kernel.py:344) applied once: with isP := 0 every B, hence every
+  // tensor component of both orientations, is an exact (signed) zero
+  s.isPm = g ? isP : 0.0;
+  s.lr = log_reduce(s.x, logt, s.logc, s.kd);
+  return s;
+}
+
+// Stage 2: ln x, K(m), E(m), S2/S3 and B1..B5 (each / 4).
+__device__ __forceinline__ PairB pair_stage2(const Outer& o, double rn, double rcpr, const PairS1& s) {
+  const double x = s.x, P = s.P, tq = s.tq, invP = s.invP;
+  const double lx = log_finish(s.lr, s.logc, s.kd);
+
 
 #if LB_ESTRIN
   // the reference's four degree-10 polynomials (kernel.py:351-359; QK[10] =
@@ -237,19 +271,23 @@ __device__ __forceinline__ PairB pair_core(const Outer& o, double rn, double zn,
     const double c = fma(-2.0, EK, Em1 + EE);
     S3 = fma(4.0, fma(c, invm, -a) * invm, Em1);
   }
-  // mask (kernel.py:344) applied once: with isP := 0 every B, hence every
-  // tensor component of both orientations, is an exact (signed) zero
-  const double isPm = g ? isP : 0.0;
+  const double isPm = s.isPm;
   const double c3 = isPm * invP;  // P^-3/2 (the 4 is folded into the coupling)
   PairB p;
   p.B1 = EK * isPm;
   p.B3 = Em1 * c3;
   p.B4 = S2 * c3;
   p.B5 = S3 * c3;
-  p.dz = dz;
-  p.dz2 = dz2;
+  p.dz = s.dz;
+  p.dz2 = s.dz2;
   p.u = fma(o.tri * rn, p.B4, p.B1);
   return p;
+}
+
+// The symmetric part of one pair (stage 1 + stage 2).
+__device__ __forceinline__ PairB pair_core(const Outer& o, double rn, double zn, double rcpr,
+                                           long long gthr, const double2* __restrict__ logt) {
+  return pair_stage2(o, rn, rcpr, pair_stage1(o, rn, zn, gthr, logt));
 }
 
 // Direct-pair tensor components from the symmetric part.
