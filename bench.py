@@ -188,10 +188,17 @@ def ours_arm(args):
     local_rank = env_int("LOCAL_RANK", 0)
     if world != args.gpus and world > 1:
         print(f"warning: WORLD_SIZE={world} but --gpus={args.gpus}", file=sys.stderr)
-    torch.cuda.set_device(local_rank)
-    dev = torch.device("cuda", local_rank)
+    # one process per GPU; --backend gloo with more ranks than GPUs is a
+    # functional check of the sharded path only (host collectives, ranks
+    # time-share a GPU, no kernel waits on another rank) -- never a timing
+    dev_index = local_rank % max(torch.cuda.device_count(), 1)
+    torch.cuda.set_device(dev_index)
+    dev = torch.device("cuda", dev_index)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if args.backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(args.backend)
 
     def barrier():
         if world > 1:
@@ -212,7 +219,7 @@ def ours_arm(args):
     host = local_fields(wl, sh.lo, sh.hi)
     d_fields = [torch.from_numpy(a).to(dev) for a in host]
     lib = _lib.load()
-    ctx = _lib.context(local_rank)
+    ctx = _lib.context(dev_index)
 
     # FP64 peak at this box's clocks (DFMA microbenchmark; MEASURED_PEAKS.json has none)
     tf, ms = _lib.C.c_double(), _lib.C.c_double()
@@ -250,7 +257,7 @@ def ours_arm(args):
         step()
     barrier()
 
-    sampler = ClockSampler(physical_gpu(local_rank)) if args.clocks else None
+    sampler = ClockSampler(physical_gpu(dev_index)) if args.clocks else None
     if sampler:
         sampler.start()
     E = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
@@ -332,6 +339,16 @@ def ours_arm(args):
                          f"(oracle/ C restatement of kernel.py:306-493, OpenMP, {t:.1f} s)"}
         parity = O.per_component_scaled_error(K[idx], D[idx], Kr, Dr)
 
+    check = None
+    if args.check:  # every rank's own rows vs the oracle on a sample (functional check)
+        from oracle import oracle as O
+
+        Kh_, Dh_ = sh.K.cpu().numpy(), sh.D.cpu().numpy()
+        idx = np.arange(sh.lo, sh.hi, max(1, (sh.hi - sh.lo) // 64))
+        Kr, Dr = O.fused_sweep(wl.r[idx], wl.z[idx], wl.r, wl.z, wl.w, wl.f, wl.df_r, wl.df_z,
+                               wl.nu_hat, wl.mass_ratio_o, eps_d=wl.eps_d)
+        err = O.per_component_scaled_error(Kh_[idx - sh.lo], Dh_[idx - sh.lo], Kr, Dr)
+        check = allmax([err])[0]
     traffic = None
     tf_file = ROOT / "profiles" / "sweep_traffic.json"
     if tf_file.exists():
@@ -374,6 +391,11 @@ def ours_arm(args):
         if cpu:
             line["cpu_baseline"] = cpu
             line["parity_scaled_err_vs_oracle"] = parity
+        if check is not None:
+            line["check_all_ranks_scaled_err_vs_oracle"] = check
+        if args.backend != "nccl" and world > 1:
+            line["note"] = f"functional run over {args.backend} (ranks may share a GPU): not a timing"
+
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
@@ -391,6 +413,9 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--ref-step-seconds", type=float, default=6.0)
     ap.add_argument("--no-clocks", dest="clocks", action="store_false")
+    ap.add_argument("--backend", choices=["nccl", "gloo"], default="nccl")
+    ap.add_argument("--check", action="store_true",
+                    help="compare every rank's rows with the oracle on a sample")
     args = ap.parse_args()
     if args.warmup < 3:
         print("note: raising --warmup to the required minimum of 3", file=sys.stderr)
