@@ -366,7 +366,9 @@ def ours_arm(args):
             "config": {"workload": f"cfg5 pure kernel sweep N={N} S={S} (BASELINE configs[4])",
                        "N": N, "S": S, "outer_per_gpu": nloc, "pairs_per_step": pairs_step,
                        "parallelism": f"outer-point shards x{world}" + (
-                           " + NCCL all-gather of packed field state" if world > 1 else ""),
+                           f" + {args.backend} all-gather of packed field state"
+                           + (" + all-reduce of partial sums" if sh.symmetric else "")
+                           if world > 1 else ""),
                        "l2": "flushed between timed steps (256 MiB write, outside step events)"},
             "roofline": {"bound": "fp64", "achieved": achieved_tf, "peak": fp64_sustained,
                          "unit": "TFLOP/s", "frac": achieved_tf / fp64_sustained,

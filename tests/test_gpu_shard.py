@@ -112,3 +112,31 @@ def test_symmetric_rank_partials_sum_to_single(gpu, world):
     err = ((acc - full).abs().max(dim=1).values / scale).max().item()
     print(f"world={world} rank-sum vs single", err)
     assert err < 1e-13
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_multirank_bench_functional(gpu, world):
+    """The multi-GPU bench path end to end with `world` ranks over gloo on
+    one GPU (ranks time-share the device; no kernel waits on another rank):
+    all-gather of packed records, symmetric tile-pair split, all-reduce of
+    partial sums, per-rank combine -- every rank's rows vs the oracle."""
+    import json
+    import socket
+    import subprocess
+    import sys
+
+    from conftest import ROOT
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={world}", "--master-addr=127.0.0.1", f"--master-port={port}",
+           "bench.py", "--gpus", str(world), "--backend", "gloo", "--check", "--steps", "3",
+           "--warmup", "3", "--points", "12000", "--no-clocks", "--e2e-steps", "1"]
+    out = subprocess.run(cmd, cwd=str(ROOT), capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stderr[-3000:]
+    line = json.loads([l for l in out.stdout.splitlines() if l.startswith("{")][-1])
+    assert line["n_gpus"] == world
+    print("multi-rank", world, "check", line["check_all_ranks_scaled_err_vs_oracle"])
+    assert line["check_all_ranks_scaled_err_vs_oracle"] < 1e-10
