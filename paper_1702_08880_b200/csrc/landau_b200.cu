@@ -652,7 +652,10 @@ namespace lb {
 
 int ensure(DevBuf& b, size_t bytes) {
   if (bytes <= b.cap) return LB_OK;
-  if (b.p) cudaFree(b.p);
+  if (b.p) {  // grow: earlier asynchronous work (any stream) may still read it
+    cudaDeviceSynchronize();
+    cudaFree(b.p);
+  }
   b.p = nullptr;
   b.cap = 0;
   size_t want = std::max(bytes, size_t(1) << 20);
