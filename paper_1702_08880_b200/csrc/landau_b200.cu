@@ -360,16 +360,26 @@ __global__ void lb_combine_kernel(const double* __restrict__ partial, int nchunk
 // clouds otherwise diverge on ~half the warps).  Each outer point's sum is
 // computed identically wherever it lands, so the order changes no bit of
 // the result; the combine kernel scatters rows back through `perm`.
+// Bounding box of (r, z): grid-stride partial min/max per block (stage 1,
+// gridDim.x blocks write part[4*block]), then one block folds the partials
+// (stage 2, n = number of partials, stride 0 selects the partial layout).
 __global__ void lb_bbox_kernel(int n, const double* __restrict__ r, const double* __restrict__ z,
                                int stride, double* __restrict__ box) {
   __shared__ double red[4][32];
   double v[4] = {1e308, -1e308, 1e308, -1e308};
-  for (int p = threadIdx.x; p < n; p += blockDim.x) {
-    const double rp = r[(size_t)p * stride], zp = z[(size_t)p * stride];
-    v[0] = fmin(v[0], rp);
-    v[1] = fmax(v[1], rp);
-    v[2] = fmin(v[2], zp);
-    v[3] = fmax(v[3], zp);
+  for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < n; p += gridDim.x * blockDim.x) {
+    if (stride > 0) {
+      const double rp = r[(size_t)p * stride], zp = z[(size_t)p * stride];
+      v[0] = fmin(v[0], rp);
+      v[1] = fmax(v[1], rp);
+      v[2] = fmin(v[2], zp);
+      v[3] = fmax(v[3], zp);
+    } else {  // fold stage-1 partials: r points at part[], z unused
+      v[0] = fmin(v[0], r[4 * p + 0]);
+      v[1] = fmax(v[1], r[4 * p + 1]);
+      v[2] = fmin(v[2], r[4 * p + 2]);
+      v[3] = fmax(v[3], r[4 * p + 3]);
+    }
   }
   for (int o = 16; o; o >>= 1) {
     v[0] = fmin(v[0], __shfl_xor_sync(0xffffffffu, v[0], o));
@@ -388,7 +398,7 @@ __global__ void lb_bbox_kernel(int n, const double* __restrict__ r, const double
       v[2] = fmin(v[2], red[2][ww]);
       v[3] = fmax(v[3], red[3][ww]);
     }
-    for (int q = 0; q < 4; ++q) box[q] = v[q];
+    for (int q = 0; q < 4; ++q) box[4 * blockIdx.x + q] = v[q];
   }
 }
 
@@ -740,7 +750,8 @@ int morton_order(DevBuf& buf, int nout, const double* ro, const double* zo, int 
                                           (int*)nullptr, (int*)nullptr, nout, 0, 32, st));
   const size_t bk = al(sizeof(uint32_t) * nout), bi = al(sizeof(int) * nout),
                bd = al(sizeof(double) * nout);
-  const size_t total = 2 * bk + 2 * bi + 2 * bd + al(4 * sizeof(double)) + al(temp);
+  constexpr int kBoxBlocks = 64;
+  const size_t total = 2 * bk + 2 * bi + 2 * bd + al(4 * (kBoxBlocks + 1) * sizeof(double)) + al(temp);
   int rc = ensure(buf, total);
   if (rc) return rc;
   char* p = static_cast<char*>(buf.p);
@@ -751,8 +762,10 @@ int morton_order(DevBuf& buf, int nout, const double* ro, const double* zo, int 
   double* r1 = reinterpret_cast<double*>(p + 2 * bk + 2 * bi);
   double* z1 = reinterpret_cast<double*>(p + 2 * bk + 2 * bi + bd);
   double* box = reinterpret_cast<double*>(p + 2 * bk + 2 * bi + 2 * bd);
-  void* tmp = p + 2 * bk + 2 * bi + 2 * bd + al(4 * sizeof(double));
-  lb_bbox_kernel<<<1, 1024, 0, st>>>(nout, ro, zo, stride, box);
+  double* part = box + 4;
+  void* tmp = p + 2 * bk + 2 * bi + 2 * bd + al(4 * (kBoxBlocks + 1) * sizeof(double));
+  lb_bbox_kernel<<<kBoxBlocks, 256, 0, st>>>(nout, ro, zo, stride, part);
+  lb_bbox_kernel<<<1, 64, 0, st>>>(kBoxBlocks, part, nullptr, 0, box);
   lb_morton_kernel<<<(nout + 255) / 256, 256, 0, st>>>(nout, ro, zo, stride, box, k0, i0);
   LB_CUDA(cub::DeviceRadixSort::SortPairs(tmp, temp, k0, k1, i0, i1, nout, 0, 32, st));
   if (rs) {
@@ -784,7 +797,7 @@ int launch_sweep(lb_ctx* ctx, int nout, const double* ro, const double* zo, int 
   if (nout >= kOrderMin) {
     int rc = morton_order(ctx->order, nout, ro, zo, 1, st, &perm, &ro, &zo);
     if (rc) return rc;
-    launches += 3;  // own kernels: bbox, morton, gather (+ CUB radix sort)
+    launches += 4;  // own kernels: bbox (2), morton, gather (+ CUB radix sort)
   }
   const int jc = chunk_len(n);
   const int nchunk = (n + jc - 1) / jc;
@@ -865,7 +878,7 @@ int sym_prepare(lb_ctx* ctx, int n, const Coupling& cp, const double* rec, cudaS
   ctx->sym_S = cp.S;
   ctx->sym_Se = cp.Se;
   ctx->sym_nt = nt;
-  ctx->last_launches = 4;  // own kernels: bbox, morton, records gather, invert (+ CUB radix sort)
+  ctx->last_launches = 5;  // own kernels: bbox (2), morton, records gather, invert (+ CUB sort)
   return LB_OK;
 }
 
@@ -972,7 +985,7 @@ int all_points_sweep(lb_ctx* ctx, int n, const double* rec, const double* r, con
   if ((rc = sym_partial_dispatch(ctx, cp.Se, gthr, 0, 1, tot, st))) return rc;
   const int l = ctx->last_launches;  // sweep + reduce launches
   rc = sym_combine_dispatch(ctx, cp.Se, tot, cp, 0, n, K, D, st);
-  ctx->last_launches += l + 4;        // + combine (set above) + 4 ordering kernels
+  ctx->last_launches += l + 5;        // + combine (set above) + 5 ordering kernels
   return rc;
 }
 

@@ -32,7 +32,10 @@
 
 constexpr int kSymTile = 128;   // points per tile (== threads per CTA)
 constexpr int kSymStages = 2;   // TMA ring depth (one J tile per stage)
-constexpr int kSegLenMax = 8;   // partner tiles per work item (large n)
+#ifndef LB_SEGLEN
+#define LB_SEGLEN 2
+#endif
+constexpr int kSegLenMax = LB_SEGLEN;  // partner tiles per work item (large n)
 #ifndef LB_SYM_MINB
 #define LB_SYM_MINB 4
 #endif

@@ -35,7 +35,7 @@ def test_dev_path_on_torch_stream_equals_host_entry(gpu):
         Kh, Dh = K.cpu(), D.cpu()
     torch.cuda.synchronize()
     assert np.array_equal(Kh.numpy()[:-1], K0) and np.array_equal(Dh.numpy()[:-1], D0)
-    assert sh.launches == 6  # pack + Morton ordering (3 own + CUB sort) + sweep + combine
+    assert sh.launches == 7  # pack + Morton ordering (4 own + CUB sort) + sweep + combine
 
 
 @pytest.mark.parametrize("world", [2, 3, 8])

@@ -10,7 +10,7 @@ sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 import torch  # noqa: E402
 
 import paper_1702_08880_b200 as pkg  # noqa: E402
-from paper_1702_08880_b200 import synthetic  # noqa: E402
+from paper_1702_08880_b200 import _lib, synthetic  # noqa: E402
 from paper_1702_08880_b200.shard import ShardedSweep, local_fields  # noqa: E402
 
 
@@ -27,6 +27,7 @@ def main():
     wl = synthetic.cfg5(n, species=sp)
     params = pkg.CollisionParams(nu_hat=wl.nu_hat, mass_ratio_o=wl.mass_ratio_o)
     sym = "--general" not in sys.argv
+    world = int(next((a.split("=")[1] for a in sys.argv if a.startswith("--world=")), 1))
     sh = ShardedSweep(n, wl.S, params, wl.eps_d, dev, align=1, symmetric=sym)
     f = [torch.from_numpy(a).to(dev) for a in local_fields(wl, 0, n)]
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -36,7 +37,12 @@ def main():
         if sh.symmetric:
             sh.sym_prepare()
             e0.record()
-            sh.sym_partial()
+            if world > 1:  # rank 0's share of a `world`-GPU split (per-rank kernel time)
+                _lib.check(_lib.load().lb_sym_partial_dev(
+                    _lib.context(0).handle, wl.S, wl.eps_d, 0, world, sh.tot.data_ptr(),
+                    torch.cuda.current_stream().cuda_stream))
+            else:
+                sh.sym_partial()
             e1.record()
             sh.sym_finish()
         else:
@@ -45,6 +51,9 @@ def main():
             e1.record()
         torch.cuda.synchronize()
         ms = e0.elapsed_time(e1)
+        if world > 1:
+            print(f"rep {k}: rank 0 of {world}: {ms:.3f} ms (x{world} = {ms * world:.2f} ms single-GPU equiv.)")
+            continue
         print(f"rep {k}: sweep {ms:.3f} ms, {n * n / ms / 1e6:.3e} Gpairs/s... "
               f"model {pkg.flop_count(n, wl.S, n) / ms / 1e9:.2f} TFLOP/s, S={wl.S}, "
               f"{'symmetric' if sh.symmetric else 'general'}")
