@@ -175,6 +175,15 @@ int lb_assemble_state(lb_ctx *ctx, const lb_mesh *mesh, int S, const double *coe
 int lb_elements_csr(lb_ctx *ctx, const lb_mesh *mesh, int S, const double *w, const double *K,
                     const double *D, double *csr_out);
 
+/* Multi-GPU operator piece: element contraction for this rank's cells
+ * [c0, c1) (w, K, D device arrays of those cells' points) and the CSR
+ * gather over ALL slots with the other cells' entries zero -> csr_out
+ * (S, nslots) device partial values; summing them over ranks (all-reduce)
+ * gives the operator (assembly.py:151-169). */
+int lb_operator_partial_dev(lb_ctx *ctx, const lb_mesh *mesh, int S, int c0, int c1,
+                            const double *w, const double *K, const double *D, double *csr_out,
+                            void *stream);
+
 /* Per-pair closed form on the device: replaces `axisym_tensor_pair`
  * (kernel.py:206-235) for npair independent (r, z, rbar, zbar) tuples, with
  * the same device arithmetic the sweep uses.  UK, UD: (npair, 2, 2).

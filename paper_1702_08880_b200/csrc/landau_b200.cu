@@ -445,7 +445,8 @@ constexpr int kElemWarps = 4;
 __global__ void __launch_bounds__(32 * kElemWarps) lb_elements_kernel(
     int ncell, int S, const double* __restrict__ sizes, const double* __restrict__ w,
     const double* __restrict__ K, const double* __restrict__ D, const double* __restrict__ Bt,
-    const double* __restrict__ dBt, double* __restrict__ elem) {
+    const double* __restrict__ dBt, double* __restrict__ elem, int ncell_out, int c_out) {
+  // cells e of this launch land at cell c_out + e of an (S, ncell_out, 81) buffer
   __shared__ double sB[81], sdB[162];
   __shared__ double sG[kElemWarps][9][6];  // G2 r,z ; G3 rr, rz, zr, zz
   __shared__ double su[kElemWarps][81], sv[kElemWarps][162];
@@ -482,7 +483,7 @@ __global__ void __launch_bounds__(32 * kElemWarps) lb_elements_kernel(
       sv[warp][2 * t + 1] = fma(b1, g[5], b0 * g[3]);
     }
     __syncwarp();
-    double* out = elem + ((size_t)a * ncell + e) * 81;
+    double* out = elem + ((size_t)a * ncell_out + c_out + e) * 81;
     for (int t = lane; t < 81; t += 32) {  // t = 9*i + j
       const int ii = t / 9, jj = t % 9;
       double s = 0.0;
@@ -1008,12 +1009,14 @@ int launch_pack(lb_ctx* ctx, int n, int S, const double* r, const double* z, con
 
 int launch_elements(lb_ctx* ctx, int ncell, int S, const double* sizes, const double* w,
                     const double* K, const double* D, const double* B, const double* dB,
-                    double* elem, cudaStream_t st) {
+                    double* elem, cudaStream_t st, int ncell_out = -1, int c_out = 0) {
+  if (ncell_out < 0) ncell_out = ncell;
   if (ncell == 0) return LB_OK;
   const long long nwork = (long long)ncell * S;
   const int blocks =
       (int)std::min<long long>((nwork + kElemWarps - 1) / kElemWarps, (long long)ctx->num_sms * 16);
-  lb_elements_kernel<<<blocks, 32 * kElemWarps, 0, st>>>(ncell, S, sizes, w, K, D, B, dB, elem);
+  lb_elements_kernel<<<blocks, 32 * kElemWarps, 0, st>>>(ncell, S, sizes, w, K, D, B, dB, elem,
+                                                         ncell_out, c_out);
   LB_CUDA(cudaGetLastError());
   return LB_OK;
 }
@@ -1611,6 +1614,36 @@ int lb_elements_csr(lb_ctx* ctx, const lb_mesh* m, int S, const double* w, const
   }
   LB_CUDA(cudaMemcpyAsync(csr_out, dcsr, sizeof(double) * S * m->nslots, cudaMemcpyDeviceToHost, st));
   LB_CUDA(cudaStreamSynchronize(st));
+  return LB_OK;
+}
+
+int lb_operator_partial_dev(lb_ctx* ctx, const lb_mesh* m, int S, int c0, int c1, const double* w,
+                            const double* K, const double* D, double* csr_out, void* stream) {
+  int rc = use_ctx(ctx);
+  if (rc) return rc;
+  if ((rc = check_species(S))) return rc;
+  if (!m || m->device != ctx->device) return fail(LB_EINVAL, "mesh handle missing or on another device");
+  if (c0 < 0 || c1 > m->ncell || c0 > c1) return fail(LB_EINVAL, "bad cell range");
+  cudaStream_t st = (cudaStream_t)stream;
+  const size_t nel = (size_t)81 * S * m->ncell;
+  if ((rc = ensure(ctx->elem, std::max<size_t>(nel, 1) * sizeof(double)))) return rc;
+  double* delem = static_cast<double*>(ctx->elem.p);
+  LB_CUDA(cudaMemsetAsync(delem, 0, nel * sizeof(double), st));
+  int launches = 0;
+  if (c1 > c0) {
+    if ((rc = launch_elements(ctx, c1 - c0, S, m->sizes + 2 * (size_t)c0, w, K, D, m->basis,
+                              m->basis + 81, delem, st, m->ncell, c0)))
+      return rc;
+    ++launches;
+  }
+  if (m->nslots) {
+    lb_csr_gather_kernel<<<(m->nslots + 255) / 256, 256, 0, st>>>(m->nslots, 81 * m->ncell, S,
+                                                                   m->slot_ptr, m->gidx, m->gw, delem,
+                                                                   csr_out);
+    LB_CUDA(cudaGetLastError());
+    ++launches;
+  }
+  ctx->last_launches = launches;
   return LB_OK;
 }
 

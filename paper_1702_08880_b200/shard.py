@@ -242,3 +242,86 @@ def local_fields(wl, lo: int, hi: int):
     return (np.ascontiguousarray(wl.r[sl]), np.ascontiguousarray(wl.z[sl]),
             np.ascontiguousarray(wl.w[sl]), np.ascontiguousarray(wl.f[:, sl]),
             np.ascontiguousarray(wl.df_r[:, sl]), np.ascontiguousarray(wl.df_z[:, sl]))
+
+
+class ShardedOperator:
+    """Multi-GPU state-level operator: `solver._assemble_at` (solver.py:81-84)
+    with cells sharded over ranks, the paper's data flow (BASELINE north_star):
+
+      1. every rank holds the state coefficients (S, n_free) -- the solver's
+         small replicated vector -- and samples ITS cells on the device
+         (`lb_sample_state_dev`, K4);
+      2. packs its points and all-gathers the packed field state (NCCL);
+      3. evaluates its share of the unordered tile pairs (symmetric sweep),
+         one all-reduce of the per-point partial sums, coupling for its own
+         points (K, D of its cells);
+      4. contracts its cells' element matrices and gathers them into a
+         partial CSR value array (`lb_operator_partial_dev`, K2 + K3);
+      5. one all-reduce of the CSR values (S x nnz) gives every rank C.
+    """
+
+    def __init__(self, mesh, ref, params, device, eps_d: float | None = None, group=None):
+        import torch
+
+        from .assembly import default_eps_d, device_mesh
+
+        self.device = torch.device(device)
+        self.group = group
+        self.S = int(np.asarray(params.mass_ratio_o).shape[0])
+        self.dm = device_mesh(mesh, ref, self.device.index or 0)
+        if not self.dm.has_geometry:
+            raise ValueError("mesh/ref lack origins/qpts/qwts needed for device sampling")
+        self.ncell = self.dm.ncell
+        n = 9 * self.ncell
+        eps = default_eps_d(mesh) if eps_d is None else float(eps_d)
+        self.sweep = ShardedSweep(n, self.S, params, eps, self.device, align=9, group=group)
+        self.c0, self.c1 = self.sweep.lo // 9, self.sweep.hi // 9
+        nl = self.sweep.hi - self.sweep.lo
+        f64 = torch.float64
+        self.coeffs = torch.empty((self.S, self.dm.n_free), dtype=f64, device=self.device)
+        self.fields = torch.empty((3 + 3 * self.S, max(nl, 1)), dtype=f64, device=self.device)
+        self.csr = torch.empty((self.S, self.dm.map.nnz), dtype=f64, device=self.device)
+        self._lib = _lib.load()
+        self._ctx = _lib.context(self.device.index or 0)
+
+    def _stream(self):
+        import torch
+
+        return torch.cuda.current_stream(self.device).cuda_stream
+
+    def local_fields(self):
+        """Views (r, z, w, f, df_r, df_z) of this rank's sampled points."""
+        S, F = self.S, self.fields
+        nl = self.sweep.hi - self.sweep.lo
+        return (F[0, :nl], F[1, :nl], F[2, :nl], F[3:3 + S, :nl], F[3 + S:3 + 2 * S, :nl],
+                F[3 + 2 * S:3 + 3 * S, :nl])
+
+    def step(self, coeffs):
+        """C blocks (list of S scipy CSR) for the state `coeffs` (S, n_free):
+        host array or device tensor; identical on every rank."""
+        import scipy.sparse as sp
+        import torch
+
+        c = coeffs if isinstance(coeffs, torch.Tensor) else torch.from_numpy(
+            np.ascontiguousarray(np.atleast_2d(coeffs), dtype=np.float64))
+        self.coeffs.copy_(c)
+        nl = self.sweep.hi - self.sweep.lo
+        st = self._stream()
+        lib, h = self._lib, self._ctx.handle
+        row = self.fields.stride(0) * 8
+        o = self.fields.data_ptr()
+        _lib.check(lib.lb_sample_state_dev(
+            h, self.dm.handle, self.S, self.c0, self.c1, self.coeffs.data_ptr(), o, o + row,
+            o + 2 * row, o + 3 * row, o + (3 + self.S) * row, o + (3 + 2 * self.S) * row, st))
+        r, z, w, f, dfr, dfz = (t.contiguous() for t in self.local_fields())
+        K, D = self.sweep.step(r, z, w, f, dfr, dfz)
+        _lib.check(lib.lb_operator_partial_dev(
+            h, self.dm.handle, self.S, self.c0, self.c1, w.data_ptr(), K.data_ptr(), D.data_ptr(),
+            self.csr.data_ptr(), st))
+        if self.sweep.world > 1:
+            _dist().all_reduce(self.csr, group=self.group)
+        vals = self.csr.cpu().numpy()
+        gm = self.dm.map
+        del nl
+        return [sp.csr_matrix((vals[a], gm.indices, gm.indptr), shape=(gm.n_free, gm.n_free))
+                for a in range(self.S)]

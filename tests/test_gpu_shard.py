@@ -140,3 +140,32 @@ def test_multirank_bench_functional(gpu, world):
     assert line["n_gpus"] == world
     print("multi-rank", world, "check", line["check_all_ranks_scaled_err_vs_oracle"])
     assert line["check_all_ranks_scaled_err_vs_oracle"] < 1e-10
+
+
+@pytest.mark.parametrize("world,case", [(1, "cfg3"), (2, "cfg3"), (3, "hanging"), (2, "cfg2")])
+def test_sharded_operator(gpu, tmp_path, world, case):
+    """Multi-GPU state-level operator (cells sharded, device sampling,
+    all-gather, symmetric sweep split, per-rank element contraction, CSR
+    all-reduce), `world` ranks over gloo on one GPU, vs the reference blocks."""
+    import socket
+    import subprocess
+    import sys
+
+    from conftest import ROOT, blocks_from, golden
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    out = tmp_path / "blocks.npz"
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={world}", "--master-addr=127.0.0.1", f"--master-port={port}",
+           "tools/sharded_operator_check.py", case, str(out), "gloo"]
+    res = subprocess.run(cmd, cwd=str(ROOT), capture_output=True, text=True, timeout=600)
+    assert res.returncode == 0, res.stderr[-3000:]
+    d = np.load(out)
+    worst = 0.0
+    for a, ref in enumerate(blocks_from(golden(case))):
+        r = ref.toarray()
+        worst = max(worst, np.abs(d[f"b{a}"] - r).max() / np.abs(r).max())
+    print(f"sharded operator {case} world={world}", worst)
+    assert worst < 1e-10

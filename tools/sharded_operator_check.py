@@ -1,0 +1,45 @@
+"""Run ShardedOperator on a reference fixture under torchrun (any backend;
+gloo lets several ranks share one GPU for a functional check) and, on rank
+0, save the assembled CSR blocks for comparison.
+
+    torchrun --nproc-per-node 2 tools/sharded_operator_check.py cfg3 out.npz gloo
+"""
+import os
+import sys
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parents[1]
+sys.path.insert(0, str(ROOT))
+sys.path.insert(0, str(ROOT / "tests"))
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+import torch.distributed as dist  # noqa: E402
+
+from conftest import golden, mesh_from, params_from, ref_from  # noqa: E402
+from paper_1702_08880_b200.shard import ShardedOperator  # noqa: E402
+
+
+def main():
+    case, out, backend = sys.argv[1], sys.argv[2], sys.argv[3] if len(sys.argv) > 3 else "gloo"
+    local = int(os.environ.get("LOCAL_RANK", 0))
+    dev = torch.device("cuda", local % torch.cuda.device_count())
+    torch.cuda.set_device(dev)
+    if int(os.environ.get("WORLD_SIZE", 1)) > 1:
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
+    g = golden(case)
+    op = ShardedOperator(mesh_from(g), ref_from(g), params_from(g), dev)
+    blocks = op.step(g["coeffs"])
+    blocks = op.step(g["coeffs"])  # second evaluation reuses every buffer
+    if not dist.is_initialized() or dist.get_rank() == 0:
+        np.savez(out, **{f"b{a}": b.toarray() for a, b in enumerate(blocks)},
+                 world=dist.get_world_size() if dist.is_initialized() else 1)
+    if dist.is_initialized():
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()
