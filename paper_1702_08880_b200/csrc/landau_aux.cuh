@@ -1,0 +1,261 @@
+// landau_aux.cuh -- outer-point Morton ordering, K2 element contraction, K3 CSR
+// gather, K4 state sampling, the per-pair entry and the FP64 peak probe.
+#pragma once
+#include "landau_common.cuh"
+
+namespace lb {
+
+// ------------------------------------------------------------------ outer ordering
+// Outer points are visited in Morton (Z-curve) order of (r, z) so the 32
+// outer points of a warp are spatial neighbours: the m < 0.01 series /
+// closed-form branch of pair_tensor is then warp-coherent (random point
+// clouds otherwise diverge on ~half the warps).  Each outer point's sum is
+// computed identically wherever it lands, so the order changes no bit of
+// the result; the combine kernel scatters rows back through `perm`.
+// Bounding box of (r, z): grid-stride partial min/max per block (stage 1,
+// gridDim.x blocks write part[4*block]), then one block folds the partials
+// (stage 2, n = number of partials, stride 0 selects the partial layout).
+__global__ void lb_bbox_kernel(int n, const double* __restrict__ r, const double* __restrict__ z,
+                               int stride, double* __restrict__ box) {
+  __shared__ double red[4][32];
+  double v[4] = {1e308, -1e308, 1e308, -1e308};
+  for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < n; p += gridDim.x * blockDim.x) {
+    if (stride > 0) {
+      const double rp = r[(size_t)p * stride], zp = z[(size_t)p * stride];
+      v[0] = fmin(v[0], rp);
+      v[1] = fmax(v[1], rp);
+      v[2] = fmin(v[2], zp);
+      v[3] = fmax(v[3], zp);
+    } else {  // fold stage-1 partials: r points at part[], z unused
+      v[0] = fmin(v[0], r[4 * p + 0]);
+      v[1] = fmax(v[1], r[4 * p + 1]);
+      v[2] = fmin(v[2], r[4 * p + 2]);
+      v[3] = fmax(v[3], r[4 * p + 3]);
+    }
+  }
+  for (int o = 16; o; o >>= 1) {
+    v[0] = fmin(v[0], __shfl_xor_sync(0xffffffffu, v[0], o));
+    v[1] = fmax(v[1], __shfl_xor_sync(0xffffffffu, v[1], o));
+    v[2] = fmin(v[2], __shfl_xor_sync(0xffffffffu, v[2], o));
+    v[3] = fmax(v[3], __shfl_xor_sync(0xffffffffu, v[3], o));
+  }
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  if (l == 0)
+    for (int q = 0; q < 4; ++q) red[q][w] = v[q];
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int ww = 1; ww < (int)(blockDim.x >> 5); ++ww) {
+      v[0] = fmin(v[0], red[0][ww]);
+      v[1] = fmax(v[1], red[1][ww]);
+      v[2] = fmin(v[2], red[2][ww]);
+      v[3] = fmax(v[3], red[3][ww]);
+    }
+    for (int q = 0; q < 4; ++q) box[4 * blockIdx.x + q] = v[q];
+  }
+}
+
+__device__ __forceinline__ uint32_t spread16(uint32_t x) {
+  x &= 0xFFFFu;
+  x = (x | (x << 8)) & 0x00FF00FFu;
+  x = (x | (x << 4)) & 0x0F0F0F0Fu;
+  x = (x | (x << 2)) & 0x33333333u;
+  x = (x | (x << 1)) & 0x55555555u;
+  return x;
+}
+
+__global__ void lb_morton_kernel(int n, const double* __restrict__ r, const double* __restrict__ z,
+                                 int stride, const double* __restrict__ box,
+                                 uint32_t* __restrict__ key, int* __restrict__ idx) {
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= n) return;
+  const double rp = r[(size_t)p * stride], zp = z[(size_t)p * stride];
+  const double sr = 65535.0 / fmax(box[1] - box[0], 1e-300);
+  const double sz = 65535.0 / fmax(box[3] - box[2], 1e-300);
+  const uint32_t qr = (uint32_t)fmin(fmax((rp - box[0]) * sr, 0.0), 65535.0);
+  const uint32_t qz = (uint32_t)fmin(fmax((zp - box[2]) * sz, 0.0), 65535.0);
+  key[p] = spread16(qr) | (spread16(qz) << 1);
+  idx[p] = p;
+}
+
+__global__ void lb_gather_kernel(int n, const int* __restrict__ perm, const double* __restrict__ r,
+                                 const double* __restrict__ z, double* __restrict__ rs,
+                                 double* __restrict__ zs) {
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= n) return;
+  const int q = perm[p];
+  rs[p] = r[q];
+  zs[p] = z[q];
+}
+
+// ------------------------------------------------------------------ K2 elements
+// One warp per (species a, cell e).  G2 = K Jinv w, G3 = Jinv D Jinv w
+// (assembly.py:159-160), then
+//   elem[a,e,i,j] = sum_q dB[i,q,:].G2[q] B[j,q] + sum_q dB[i,q,:].G3[q].dB[j,q,:]
+// computed as u[i,q] = dB[i,q,:].G2[q], v[i,q,:] = dB[i,q,:].G3[q] followed
+// by a 27-term dot product per entry.
+constexpr int kElemWarps = 4;
+__global__ void __launch_bounds__(32 * kElemWarps) lb_elements_kernel(
+    int ncell, int S, const double* __restrict__ sizes, const double* __restrict__ w,
+    const double* __restrict__ K, const double* __restrict__ D, const double* __restrict__ Bt,
+    const double* __restrict__ dBt, double* __restrict__ elem, int ncell_out, int c_out) {
+  // cells e of this launch land at cell c_out + e of an (S, ncell_out, 81) buffer
+  __shared__ double sB[81], sdB[162];
+  __shared__ double sG[kElemWarps][9][6];  // G2 r,z ; G3 rr, rz, zr, zz
+  __shared__ double su[kElemWarps][81], sv[kElemWarps][162];
+  for (int t = threadIdx.x; t < 81; t += blockDim.x) sB[t] = Bt[t];
+  for (int t = threadIdx.x; t < 162; t += blockDim.x) sdB[t] = dBt[t];
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const long long nwork = (long long)ncell * S;
+  for (long long wk = (long long)blockIdx.x * kElemWarps + warp; wk < nwork;
+       wk += (long long)gridDim.x * kElemWarps) {
+    const int a = (int)(wk / ncell);
+    const int e = (int)(wk % ncell);
+    const double jr = 2.0 / sizes[2 * e], jz = 2.0 / sizes[2 * e + 1];
+    if (lane < 9) {
+      const int pnt = 9 * e + lane;
+      const double wp = w[pnt];
+      const double* Kp = K + ((size_t)pnt * S + a) * 2;
+      const double* Dp = D + ((size_t)pnt * S + a) * 4;
+      // same factor grouping as assembly.py:159-160
+      sG[warp][lane][0] = Kp[0] * (jr * wp);
+      sG[warp][lane][1] = Kp[1] * (jz * wp);
+      sG[warp][lane][2] = Dp[0] * ((jr * jr) * wp);
+      sG[warp][lane][3] = Dp[1] * ((jr * jz) * wp);
+      sG[warp][lane][4] = Dp[2] * ((jz * jr) * wp);
+      sG[warp][lane][5] = Dp[3] * ((jz * jz) * wp);
+    }
+    __syncwarp();
+    for (int t = lane; t < 81; t += 32) {  // t = 9*i + q
+      const int q = t % 9;
+      const double* g = sG[warp][q];
+      const double b0 = sdB[2 * t], b1 = sdB[2 * t + 1];
+      su[warp][t] = fma(b1, g[1], b0 * g[0]);
+      sv[warp][2 * t] = fma(b1, g[4], b0 * g[2]);
+      sv[warp][2 * t + 1] = fma(b1, g[5], b0 * g[3]);
+    }
+    __syncwarp();
+    double* out = elem + ((size_t)a * ncell_out + c_out + e) * 81;
+    for (int t = lane; t < 81; t += 32) {  // t = 9*i + j
+      const int ii = t / 9, jj = t % 9;
+      double s = 0.0;
+#pragma unroll
+      for (int q = 0; q < 9; ++q) {
+        s = fma(su[warp][9 * ii + q], sB[9 * jj + q], s);
+        s = fma(sv[warp][2 * (9 * ii + q)], sdB[2 * (9 * jj + q)], s);
+        s = fma(sv[warp][2 * (9 * ii + q) + 1], sdB[2 * (9 * jj + q) + 1], s);
+      }
+      out[t] = s;
+    }
+    __syncwarp();
+  }
+}
+
+// ------------------------------------------------------------------ K3 CSR gather
+// One thread per stored slot of C_free = P^T C P: the weighted sum of the
+// element-matrix entries that land on it, in the map's fixed order
+// (scatter.py builds the map once per mesh; assembly.py:115-129 is the
+// reference's scipy COO->CSR + condensation).  HBM-bound gather.
+__global__ void lb_csr_gather_kernel(int nslots, int nent, int S, const int* __restrict__ slot_ptr,
+                                     const int* __restrict__ gidx, const double* __restrict__ gw,
+                                     const double* __restrict__ elem, double* __restrict__ out) {
+  const int slot = blockIdx.x * blockDim.x + threadIdx.x;
+  if (slot >= nslots) return;
+  const int k0 = slot_ptr[slot], k1 = slot_ptr[slot + 1];
+  for (int a = 0; a < S; ++a) {
+    const double* ea = elem + (size_t)a * nent;
+    double v = 0.0;
+    for (int k = k0; k < k1; ++k) v = fma(gw[k], ea[gidx[k]], v);
+    out[(size_t)a * nslots + slot] = v;
+  }
+}
+
+// ------------------------------------------------------------------ K4 sampling
+// sample_state (fem.py:170-199) + element_geometry (fem.py:103-113) on the
+// device: one thread per quadrature point (e, q) of cells [c0, c1).
+// Coordinates / weights use the reference's exact operation order (no
+// contraction), so r, z, w are bitwise those of the reference; nodal values
+// go through the prolongation rows (hanging nodes: 3 weights).
+__global__ void lb_sample_kernel(int c0, int c1, int S, int n_free, const double* __restrict__ origins,
+                                 const double* __restrict__ sizes, const double* __restrict__ qgeo,
+                                 const double* __restrict__ basis, const int* __restrict__ cell_nodes,
+                                 const int* __restrict__ P_ptr, const int* __restrict__ P_idx,
+                                 const double* __restrict__ P_w, const double* __restrict__ coeffs,
+                                 double* __restrict__ r, double* __restrict__ z, double* __restrict__ w,
+                                 double* __restrict__ f, double* __restrict__ dfr,
+                                 double* __restrict__ dfz) {
+  const int nloc = 9 * (c1 - c0);
+  const int pl = blockIdx.x * blockDim.x + threadIdx.x;
+  if (pl >= nloc) return;
+  const int e = c0 + pl / 9, q = pl % 9;
+  const double sr = sizes[2 * e], sz = sizes[2 * e + 1];
+  // coords = origins + (qpts + 1) * 0.5 * sizes (fem.py:109-111)
+  const double rq = __dadd_rn(origins[2 * e], __dmul_rn(__dmul_rn(__dadd_rn(qgeo[2 * q], 1.0), 0.5), sr));
+  const double zq =
+      __dadd_rn(origins[2 * e + 1], __dmul_rn(__dmul_rn(__dadd_rn(qgeo[2 * q + 1], 1.0), 0.5), sz));
+  const double detJ = __ddiv_rn(__dmul_rn(sr, sz), 4.0);   // fem.py:105
+  r[pl] = rq;
+  z[pl] = zq;
+  w[pl] = __dmul_rn(__dmul_rn(qgeo[18 + q], detJ), rq);   // fem.py:112
+  const double jr = __ddiv_rn(2.0, sr), jz = __ddiv_rn(2.0, sz);  // fem.py:107-108
+  for (int s = 0; s < S; ++s) {
+    const double* cs = coeffs + (size_t)s * n_free;
+    double fv = 0.0, gr = 0.0, gz = 0.0;
+    for (int i = 0; i < 9; ++i) {
+      const int node = cell_nodes[9 * e + i];
+      double v = 0.0;  // (P @ coeffs^T)[node] (fem.py:182)
+      for (int k = P_ptr[node]; k < P_ptr[node + 1]; ++k) v = __dadd_rn(v, __dmul_rn(P_w[k], cs[P_idx[k]]));
+      fv = fma(v, basis[9 * i + q], fv);
+      gr = fma(v, basis[81 + 2 * (9 * i + q)], gr);
+      gz = fma(v, basis[81 + 2 * (9 * i + q) + 1], gz);
+    }
+    f[(size_t)s * nloc + pl] = fv;
+    dfr[(size_t)s * nloc + pl] = __dmul_rn(gr, jr);  // fem.py:188-189
+    dfz[(size_t)s * nloc + pl] = __dmul_rn(gz, jz);
+  }
+}
+
+// ------------------------------------------------------------------ per-pair
+__global__ void lb_pairs_kernel(int npair, const double* __restrict__ r, const double* __restrict__ z,
+                                const double* __restrict__ rb, const double* __restrict__ zb,
+                                double* __restrict__ UK, double* __restrict__ UD) {
+  __shared__ double2 logt[1 << LB_LOGT_BITS];
+  for (int t = threadIdx.x; t < (1 << LB_LOGT_BITS); t += blockDim.x)
+    logt[t] = make_double2(c_logt[2 * t], c_logt[2 * t + 1]);
+  __syncthreads();
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= npair) return;
+  const Outer o = make_outer(r[p], z[p]);
+  const double rn = rb[p];
+  const T5 t = pair_tensor(o, rn, zb[p], rn * rn, rn > 0.0 ? 1.0 / rn : 0.0, 1LL, logt);
+  // restore the pulled-out factor 4 (exact) and lay out as kernel.py:227-234
+  UD[4 * p + 0] = 4.0 * t.xx;
+  UD[4 * p + 1] = 4.0 * t.xz;
+  UD[4 * p + 2] = 4.0 * t.xz;
+  UD[4 * p + 3] = 4.0 * t.zz;
+  UK[4 * p + 0] = 4.0 * t.kr;
+  UK[4 * p + 1] = 4.0 * t.xz;
+  UK[4 * p + 2] = 4.0 * t.zr;
+  UK[4 * p + 3] = 4.0 * t.zz;
+}
+
+// ------------------------------------------------------------------ FP64 peak
+constexpr int kDfmaChains = 8;
+constexpr int kDfmaIters = 4096;
+__global__ void __launch_bounds__(256) lb_dfma_kernel(double seed, double* sink) {
+  double v[kDfmaChains];
+#pragma unroll
+  for (int c = 0; c < kDfmaChains; ++c) v[c] = seed + threadIdx.x * 1e-9 + c;
+  const double m = 0.999999, add = 1e-7;
+#pragma unroll 4
+  for (int it = 0; it < kDfmaIters; ++it) {
+#pragma unroll
+    for (int c = 0; c < kDfmaChains; ++c) v[c] = fma(v[c], m, add);
+  }
+  double s = 0.0;
+#pragma unroll
+  for (int c = 0; c < kDfmaChains; ++c) s += v[c];
+  if (s == 12345.6789) sink[threadIdx.x] = s;  // never true; keeps the chains live
+}
+
+}  // namespace lb

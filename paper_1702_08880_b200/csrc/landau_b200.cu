@@ -1,26 +1,19 @@
-// landau_b200.cu -- sm_100a kernels and the C ABI of include/landau_b200.h.
+// landau_b200.cu -- host side and the C ABI of include/landau_b200.h.
 //
-// Kernels
-//   K0 lb_pack_kernel      SoA QuadPointData -> packed inner records
-//                          (r, z, r^2, 1/r, (w df_r, w df_z, w f) x S)
-//   K1 lb_sweep_kernel<S>  FP64 pair sweep: persistent CTAs walk work items
-//                          (128 outer points x one inner chunk); inner
-//                          records stream through a 2-stage shared-memory
-//                          ring filled by cp.async.bulk (TMA bulk copies)
-//                          completing on mbarriers; each thread holds one
-//                          outer point and its 5S accumulators in registers;
-//                          per-chunk partial sums go to HBM.
-//   K1b lb_combine_kernel<S>  fixed-order reduction of the chunk partials +
-//                          S x S species coupling (kernel.py:418-440).
-//   K2 lb_elements_kernel  outer-point transform G2/G3 + 9x9 element
-//                          contraction per (cell, species) (assembly.py:151-165).
-//   lb_pairs_kernel        per-pair closed form (axisym_tensor_pair).
-//   lb_dfma_kernel         FP64 DFMA peak microbenchmark (the roofline peak).
+// Kernels (all sm_100a, all FP64) live in the headers:
+//   landau_pair.cuh    per-pair arithmetic of the axisymmetric Landau tensor
+//   landau_common.cuh  constants, record layout, species coupling, PTX helpers
+//   landau_sweep.cuh   K0 record pack, K1 general pair sweep (any outer points,
+//                      4-stage TMA ring, per-warp mbarrier release), K1b combine
+//   landau_sym.cuh     K1s symmetric all-points sweep (unordered tile pairs,
+//                      rotated j-side accumulators) and its fixed-order reduce
+//   landau_aux.cuh     Morton ordering, K2 element contraction, K3 CSR gather,
+//                      K4 state sampling, per-pair entry, FP64 peak probe
+// This file owns the context (stream, events, grow-only device scratch), the
+// device mesh handle, the launch logic and every extern "C" entry point.
 //
-// Determinism: inner chunk boundaries depend only on n; within a chunk the
-// inner points are summed in index order, chunks are summed in index order;
-// no atomics.  Results are bitwise reproducible and independent of how outer
-// points are split across calls or GPUs.
+// Determinism: every reduction runs in a fixed order that is a function of
+// the problem size (and the Morton order of the points); no atomics.
 #include <cub/device/device_radix_sort.cuh>
 #include <cuda_runtime.h>
 
@@ -33,578 +26,12 @@
 #include <vector>
 
 #include "../../include/landau_b200.h"
-#include "landau_pair.cuh"
+#include "landau_common.cuh"
+#include "landau_sweep.cuh"
+#include "landau_sym.cuh"
+#include "landau_aux.cuh"
 
 namespace lb {
-
-constexpr int kTI = 128;        // outer points per CTA (one per thread)
-#ifndef LB_MINB
-#define LB_MINB 4
-#endif
-#ifndef LB_UNROLL
-#define LB_UNROLL 1
-#endif
-constexpr int kMinBlocks = LB_MINB;  // CTAs per SM the register budget targets
-constexpr int kUnroll = LB_UNROLL;   // inner pairs interleaved per loop trip
-constexpr int kMaxChunks = 64;  // inner chunks per sweep (sets the JC length)
-constexpr int kChunkAlign = 128;
-// Scratch budgets for partial sums (bytes): general-path chunk partials per
-// outer batch and symmetric-path i/j-side partials per row batch.  The
-// batch sizes only depend on the problem size and these budgets; the
-// LB_PARTIAL_BUDGET_MB environment variable lowers them (tests use it to
-// exercise multi-batch runs at moderate N).
-size_t partial_budget() {
-  static size_t b = [] {
-    const char* e = std::getenv("LB_PARTIAL_BUDGET_MB");
-    const long long mb = e ? std::atoll(e) : 0;
-    return mb > 0 ? size_t(mb) << 20 : size_t(2) << 30;
-  }();
-  return b;
-}
-
-__host__ __device__ constexpr int rec_stride(int S) { return ((4 + 3 * S) + 1) & ~1; }
-template <int S>
-struct TileCfg {
-  static constexpr int RS = rec_stride(S);
-  static constexpr int TJ = S <= 4 ? 128 : 64;  // inner records per stage
-};
-
-// Species coupling (kernel.py:496-501) and the record layout it implies.
-// When coK and coD are rank one -- always for the reference's own tables:
-// nu_ab ~ e_a^2 e_b^2 (physics.py:77-94), so coK_ab = k_a k_b with
-// k_a = sqrt(nu_aa) m_o/m_a and coD_ab = al_a be_b -- the S species collapse
-// into ONE accumulator set: each inner point carries the pre-weighted fields
-// gr' = sum_b k_b w df_r,b, gz' = sum_b k_b w df_z,b, f' = sum_b be_b w f_b
-// (formed once per point in K0), the pair loop runs at S = 1 cost, and the
-// combine expands K[a] = k_a A'_{0:2}, D[a] = al_a A'_{2:5}.  Algebraically
-// identical to summing per species then coupling (the reference's order);
-// the rank-one test admits only tables factoring to ~4 ulp.
-struct Coupling {
-  int S = 1;          // species
-  int Se = 1;         // accumulator species sets (1 when collapsed)
-  int collapsed = 0;
-  double coK4[LB_MAX_SPECIES * LB_MAX_SPECIES];  // 4 * coK (the pulled-out 4)
-  double coD4[LB_MAX_SPECIES * LB_MAX_SPECIES];
-  double kw[LB_MAX_SPECIES], dw[LB_MAX_SPECIES];      // per-point field weights
-  double kout[LB_MAX_SPECIES], dout[LB_MAX_SPECIES];  // 4 k_a, 4 al_a
-};
-
-// ------------------------------------------------------------------ PTX helpers
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
-               "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-  asm volatile(
-      "{\n"
-      ".reg .pred p;\n"
-      "LB_WAIT_%=:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-      "@!p bra LB_WAIT_%=;\n"
-      "}\n" ::"r"(smem_u32(bar)),
-      "r"(parity)
-      : "memory");
-}
-// 1-D TMA bulk copy global -> shared, completion counted on `bar`.
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-          smem_u32(dst)),
-      "l"(src), "r"(bytes), "r"(smem_u32(bar))
-      : "memory");
-}
-
-// ------------------------------------------------------------------ K0 pack
-struct PackW {
-  int collapsed;
-  double kw[LB_MAX_SPECIES], dw[LB_MAX_SPECIES];
-};
-
-__global__ void lb_pack_kernel(int n, int S, int RS, const double* __restrict__ r,
-                               const double* __restrict__ z, const double* __restrict__ w,
-                               const double* __restrict__ f, const double* __restrict__ dfr,
-                               const double* __restrict__ dfz, const PackW pw,
-                               double* __restrict__ rec) {
-  for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < n; p += gridDim.x * blockDim.x) {
-    const double rn = r[p], wn = w[p];
-    double* o = rec + (size_t)p * RS;
-    o[0] = rn;
-    o[1] = z[p];
-    o[2] = rn * rn;
-    o[3] = rn > 0.0 ? 1.0 / rn : 0.0;
-    if (pw.collapsed) {  // species-collapsed record (see Coupling)
-      double gr = 0.0, gz = 0.0, fw = 0.0;
-      for (int b = 0; b < S; ++b) {
-        gr = fma(pw.kw[b], dfr[(size_t)b * n + p] * wn, gr);
-        gz = fma(pw.kw[b], dfz[(size_t)b * n + p] * wn, gz);
-        fw = fma(pw.dw[b], f[(size_t)b * n + p] * wn, fw);
-      }
-      o[4] = gr;
-      o[5] = gz;
-      o[6] = fw;
-      for (int k = 7; k < RS; ++k) o[k] = 0.0;
-    } else {
-      for (int b = 0; b < S; ++b) {
-        // same products as _accumulate_block (kernel.py:408-410)
-        o[4 + 3 * b + 0] = dfr[(size_t)b * n + p] * wn;
-        o[4 + 3 * b + 1] = dfz[(size_t)b * n + p] * wn;
-        o[4 + 3 * b + 2] = f[(size_t)b * n + p] * wn;
-      }
-      for (int k = 4 + 3 * S; k < RS; ++k) o[k] = 0.0;
-    }
-  }
-}
-
-// ------------------------------------------------------------------ K1 sweep
-struct SweepArgs {
-  const double* ro;   // outer r (nout)
-  const double* zo;   // outer z (nout)
-  const double* rec;  // packed inner records (n x RS)
-  double* partial;    // [nchunk][5S][nout_pad]
-  int nout, nout_pad, n, jc, nchunk;
-  long long gthr;     // mask threshold on bits(d^2)
-};
-
-constexpr int kStages = 4;     // shared-memory ring depth
-constexpr int kLookahead = 2;  // tiles in flight ahead of the consumer
-constexpr int kWarps = kTI / 32;
-
-template <int S>
-constexpr size_t sweep_smem_bytes() {
-  return size_t(kStages) * TileCfg<S>::TJ * TileCfg<S>::RS * sizeof(double) +
-         size_t(2 << LB_LOGT_BITS) * sizeof(double);
-}
-
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-
-// Persistent CTAs walk work items (128 outer points x one inner chunk of jc
-// points).  Inner records flow through a kStages ring: thread 0 issues the
-// 1-D TMA bulk copy of tile k+kLookahead once every warp has released tile
-// k+kLookahead-kStages (per-stage "empty" mbarriers, one arrival per warp),
-// so warps drift independently instead of meeting at a CTA barrier per tile.
-template <int S>
-__global__ void __launch_bounds__(kTI, kMinBlocks) lb_sweep_kernel(const SweepArgs a) {
-  constexpr int RS = TileCfg<S>::RS;
-  constexpr int TJ = TileCfg<S>::TJ;
-  extern __shared__ __align__(128) double lb_smem[];
-  __shared__ __align__(8) uint64_t full[kStages], empty[kStages];
-  double2* logt = reinterpret_cast<double2*>(lb_smem + kStages * TJ * RS);
-
-  const int tid = threadIdx.x;
-  const int lane = tid & 31;
-  const int nib = a.nout_pad / kTI;
-  const long long nitems = (long long)nib * a.nchunk;
-
-  for (int t = tid; t < (2 << LB_LOGT_BITS); t += kTI) lb_smem[kStages * TJ * RS + t] = c_logt[t];
-  if (tid == 0) {
-#pragma unroll
-    for (int s = 0; s < kStages; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&empty[s], kWarps);
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  __syncthreads();
-
-  // producer cursor (thread 0 only): next (item, tile) to load, flat tile index
-  long long p_item = blockIdx.x;
-  int p_tile = 0;
-  uint32_t p_k = 0;
-  auto issue_next = [&]() {
-    if (p_item >= nitems) return;
-    const uint32_t s = p_k % kStages;
-    if (p_k >= kStages) mbar_wait(&empty[s], ((p_k / kStages) - 1) & 1);
-    const int c = (int)(p_item / nib);
-    const int j0 = c * a.jc + p_tile * TJ;
-    const int jend = min(a.n, (c + 1) * a.jc);
-    const int cnt = min(TJ, jend - j0);
-    const uint32_t bytes = (uint32_t)cnt * RS * sizeof(double);
-    mbar_expect_tx(&full[s], bytes);
-    bulk_g2s(lb_smem + s * (TJ * RS), a.rec + (size_t)j0 * RS, bytes, &full[s]);
-    ++p_k;
-    if (j0 + TJ >= jend) {
-      p_tile = 0;
-      p_item += gridDim.x;
-    } else {
-      ++p_tile;
-    }
-  };
-  if (tid == 0)
-    for (int q = 0; q < kLookahead; ++q) issue_next();
-
-  uint32_t k = 0;  // consumer flat tile index (same sequence as the producer)
-  for (long long item = blockIdx.x; item < nitems; item += gridDim.x) {
-    const int ib = (int)(item % nib);
-    const int c = (int)(item / nib);
-    const int i = ib * kTI + tid;
-    const int il = min(i, a.nout - 1);
-    const Outer o = make_outer(a.ro[il], a.zo[il]);
-    double acc[S][5];
-#pragma unroll
-    for (int b = 0; b < S; ++b)
-#pragma unroll
-      for (int q = 0; q < 5; ++q) acc[b][q] = 0.0;
-
-    const int jbeg = c * a.jc;
-    const int jend = min(a.n, jbeg + a.jc);
-    for (int j0 = jbeg; j0 < jend; j0 += TJ, ++k) {
-      if (tid == 0) issue_next();
-      const uint32_t s = k % kStages;
-      mbar_wait(&full[s], (k / kStages) & 1);
-      const double* tile = lb_smem + s * (TJ * RS);
-      const int cnt = min(TJ, jend - j0);
-#pragma unroll kUnroll
-      for (int jj = 0; jj < cnt; ++jj) {
-        const double* rp = tile + jj * RS;
-        const double2 rz = *reinterpret_cast<const double2*>(rp);
-        const double2 aux = *reinterpret_cast<const double2*>(rp + 2);
-        const T5 t = pair_tensor(o, rz.x, rz.y, aux.x, aux.y, a.gthr, logt);
-#pragma unroll
-        for (int b = 0; b < S; ++b) {
-          const double gr = rp[4 + 3 * b], gz = rp[5 + 3 * b], fw = rp[6 + 3 * b];
-          // _accumulate_block (kernel.py:411-415)
-          acc[b][0] = fma(t.xz, gz, fma(t.kr, gr, acc[b][0]));
-          acc[b][1] = fma(t.zz, gz, fma(t.zr, gr, acc[b][1]));
-          acc[b][2] = fma(fw, t.xx, acc[b][2]);
-          acc[b][3] = fma(fw, t.xz, acc[b][3]);
-          acc[b][4] = fma(fw, t.zz, acc[b][4]);
-        }
-      }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[s]);  // this warp is done with stage s
-    }
-    if (i < a.nout) {
-      double* dst = a.partial + (size_t)c * (5 * S) * a.nout_pad + i;
-#pragma unroll
-      for (int b = 0; b < S; ++b)
-#pragma unroll
-        for (int q = 0; q < 5; ++q) dst[(size_t)(b * 5 + q) * a.nout_pad] = acc[b][q];
-    }
-  }
-}
-
-// ------------------------------------------------------------------ K1b combine
-// Shared by both combine kernels: accumulators A[Se][5] -> K, D rows.
-template <int Se>
-__device__ __forceinline__ void write_kd(const double (&A)[Se][5], const Coupling& cp, size_t io,
-                                         double* __restrict__ K, double* __restrict__ D) {
-  const int S = cp.S;
-  for (int a = 0; a < S; ++a) {
-    double k0, k1, d0, d1, d2;
-    if (cp.collapsed) {  // rank-one coupling: expand the single accumulator set
-      k0 = __dmul_rn(cp.kout[a], A[0][0]);
-      k1 = __dmul_rn(cp.kout[a], A[0][1]);
-      d0 = __dmul_rn(cp.dout[a], A[0][2]);
-      d1 = __dmul_rn(cp.dout[a], A[0][3]);
-      d2 = __dmul_rn(cp.dout[a], A[0][4]);
-    } else {  // _combine (kernel.py:419-440): strict order, no contraction
-      k0 = 0.0, k1 = 0.0, d0 = 0.0, d1 = 0.0, d2 = 0.0;
-#pragma unroll
-      for (int b = 0; b < Se; ++b) {
-        const double ck = cp.coK4[a * Se + b], cd = cp.coD4[a * Se + b];
-        k0 = __dadd_rn(k0, __dmul_rn(ck, A[b][0]));
-        k1 = __dadd_rn(k1, __dmul_rn(ck, A[b][1]));
-        d0 = __dadd_rn(d0, __dmul_rn(cd, A[b][2]));
-        d1 = __dadd_rn(d1, __dmul_rn(cd, A[b][3]));
-        d2 = __dadd_rn(d2, __dmul_rn(cd, A[b][4]));
-      }
-    }
-    double* Ko = K + (io * S + a) * 2;
-    double* Do = D + (io * S + a) * 4;
-    Ko[0] = k0;
-    Ko[1] = k1;
-    Do[0] = d0;
-    Do[1] = d1;
-    Do[2] = d1;
-    Do[3] = d2;
-  }
-}
-
-template <int Se>
-__global__ void lb_combine_kernel(const double* __restrict__ partial, int nchunk, int nout,
-                                  int nout_pad, const Coupling cp, const int* __restrict__ perm,
-                                  double* __restrict__ K, double* __restrict__ D) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= nout) return;
-  const int io = perm ? perm[i] : i;  // output row of this (possibly reordered) outer point
-  double A[Se][5];
-#pragma unroll
-  for (int b = 0; b < Se; ++b)
-#pragma unroll
-    for (int q = 0; q < 5; ++q) A[b][q] = 0.0;
-  for (int c = 0; c < nchunk; ++c) {
-    const double* src = partial + (size_t)c * (5 * Se) * nout_pad + i;
-#pragma unroll
-    for (int b = 0; b < Se; ++b)
-#pragma unroll
-      for (int q = 0; q < 5; ++q) A[b][q] = __dadd_rn(A[b][q], src[(size_t)(b * 5 + q) * nout_pad]);
-  }
-  write_kd<Se>(A, cp, (size_t)io, K, D);
-}
-
-#include "landau_sym.cuh"  // symmetric all-points sweep (kernels)
-
-// ------------------------------------------------------------------ outer ordering
-// Outer points are visited in Morton (Z-curve) order of (r, z) so the 32
-// outer points of a warp are spatial neighbours: the m < 0.01 series /
-// closed-form branch of pair_tensor is then warp-coherent (random point
-// clouds otherwise diverge on ~half the warps).  Each outer point's sum is
-// computed identically wherever it lands, so the order changes no bit of
-// the result; the combine kernel scatters rows back through `perm`.
-// Bounding box of (r, z): grid-stride partial min/max per block (stage 1,
-// gridDim.x blocks write part[4*block]), then one block folds the partials
-// (stage 2, n = number of partials, stride 0 selects the partial layout).
-__global__ void lb_bbox_kernel(int n, const double* __restrict__ r, const double* __restrict__ z,
-                               int stride, double* __restrict__ box) {
-  __shared__ double red[4][32];
-  double v[4] = {1e308, -1e308, 1e308, -1e308};
-  for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < n; p += gridDim.x * blockDim.x) {
-    if (stride > 0) {
-      const double rp = r[(size_t)p * stride], zp = z[(size_t)p * stride];
-      v[0] = fmin(v[0], rp);
-      v[1] = fmax(v[1], rp);
-      v[2] = fmin(v[2], zp);
-      v[3] = fmax(v[3], zp);
-    } else {  // fold stage-1 partials: r points at part[], z unused
-      v[0] = fmin(v[0], r[4 * p + 0]);
-      v[1] = fmax(v[1], r[4 * p + 1]);
-      v[2] = fmin(v[2], r[4 * p + 2]);
-      v[3] = fmax(v[3], r[4 * p + 3]);
-    }
-  }
-  for (int o = 16; o; o >>= 1) {
-    v[0] = fmin(v[0], __shfl_xor_sync(0xffffffffu, v[0], o));
-    v[1] = fmax(v[1], __shfl_xor_sync(0xffffffffu, v[1], o));
-    v[2] = fmin(v[2], __shfl_xor_sync(0xffffffffu, v[2], o));
-    v[3] = fmax(v[3], __shfl_xor_sync(0xffffffffu, v[3], o));
-  }
-  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
-  if (l == 0)
-    for (int q = 0; q < 4; ++q) red[q][w] = v[q];
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    for (int ww = 1; ww < (int)(blockDim.x >> 5); ++ww) {
-      v[0] = fmin(v[0], red[0][ww]);
-      v[1] = fmax(v[1], red[1][ww]);
-      v[2] = fmin(v[2], red[2][ww]);
-      v[3] = fmax(v[3], red[3][ww]);
-    }
-    for (int q = 0; q < 4; ++q) box[4 * blockIdx.x + q] = v[q];
-  }
-}
-
-__device__ __forceinline__ uint32_t spread16(uint32_t x) {
-  x &= 0xFFFFu;
-  x = (x | (x << 8)) & 0x00FF00FFu;
-  x = (x | (x << 4)) & 0x0F0F0F0Fu;
-  x = (x | (x << 2)) & 0x33333333u;
-  x = (x | (x << 1)) & 0x55555555u;
-  return x;
-}
-
-__global__ void lb_morton_kernel(int n, const double* __restrict__ r, const double* __restrict__ z,
-                                 int stride, const double* __restrict__ box,
-                                 uint32_t* __restrict__ key, int* __restrict__ idx) {
-  const int p = blockIdx.x * blockDim.x + threadIdx.x;
-  if (p >= n) return;
-  const double rp = r[(size_t)p * stride], zp = z[(size_t)p * stride];
-  const double sr = 65535.0 / fmax(box[1] - box[0], 1e-300);
-  const double sz = 65535.0 / fmax(box[3] - box[2], 1e-300);
-  const uint32_t qr = (uint32_t)fmin(fmax((rp - box[0]) * sr, 0.0), 65535.0);
-  const uint32_t qz = (uint32_t)fmin(fmax((zp - box[2]) * sz, 0.0), 65535.0);
-  key[p] = spread16(qr) | (spread16(qz) << 1);
-  idx[p] = p;
-}
-
-__global__ void lb_gather_kernel(int n, const int* __restrict__ perm, const double* __restrict__ r,
-                                 const double* __restrict__ z, double* __restrict__ rs,
-                                 double* __restrict__ zs) {
-  const int p = blockIdx.x * blockDim.x + threadIdx.x;
-  if (p >= n) return;
-  const int q = perm[p];
-  rs[p] = r[q];
-  zs[p] = z[q];
-}
-
-// ------------------------------------------------------------------ K2 elements
-// One warp per (species a, cell e).  G2 = K Jinv w, G3 = Jinv D Jinv w
-// (assembly.py:159-160), then
-//   elem[a,e,i,j] = sum_q dB[i,q,:].G2[q] B[j,q] + sum_q dB[i,q,:].G3[q].dB[j,q,:]
-// computed as u[i,q] = dB[i,q,:].G2[q], v[i,q,:] = dB[i,q,:].G3[q] followed
-// by a 27-term dot product per entry.
-constexpr int kElemWarps = 4;
-__global__ void __launch_bounds__(32 * kElemWarps) lb_elements_kernel(
-    int ncell, int S, const double* __restrict__ sizes, const double* __restrict__ w,
-    const double* __restrict__ K, const double* __restrict__ D, const double* __restrict__ Bt,
-    const double* __restrict__ dBt, double* __restrict__ elem, int ncell_out, int c_out) {
-  // cells e of this launch land at cell c_out + e of an (S, ncell_out, 81) buffer
-  __shared__ double sB[81], sdB[162];
-  __shared__ double sG[kElemWarps][9][6];  // G2 r,z ; G3 rr, rz, zr, zz
-  __shared__ double su[kElemWarps][81], sv[kElemWarps][162];
-  for (int t = threadIdx.x; t < 81; t += blockDim.x) sB[t] = Bt[t];
-  for (int t = threadIdx.x; t < 162; t += blockDim.x) sdB[t] = dBt[t];
-  __syncthreads();
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const long long nwork = (long long)ncell * S;
-  for (long long wk = (long long)blockIdx.x * kElemWarps + warp; wk < nwork;
-       wk += (long long)gridDim.x * kElemWarps) {
-    const int a = (int)(wk / ncell);
-    const int e = (int)(wk % ncell);
-    const double jr = 2.0 / sizes[2 * e], jz = 2.0 / sizes[2 * e + 1];
-    if (lane < 9) {
-      const int pnt = 9 * e + lane;
-      const double wp = w[pnt];
-      const double* Kp = K + ((size_t)pnt * S + a) * 2;
-      const double* Dp = D + ((size_t)pnt * S + a) * 4;
-      // same factor grouping as assembly.py:159-160
-      sG[warp][lane][0] = Kp[0] * (jr * wp);
-      sG[warp][lane][1] = Kp[1] * (jz * wp);
-      sG[warp][lane][2] = Dp[0] * ((jr * jr) * wp);
-      sG[warp][lane][3] = Dp[1] * ((jr * jz) * wp);
-      sG[warp][lane][4] = Dp[2] * ((jz * jr) * wp);
-      sG[warp][lane][5] = Dp[3] * ((jz * jz) * wp);
-    }
-    __syncwarp();
-    for (int t = lane; t < 81; t += 32) {  // t = 9*i + q
-      const int q = t % 9;
-      const double* g = sG[warp][q];
-      const double b0 = sdB[2 * t], b1 = sdB[2 * t + 1];
-      su[warp][t] = fma(b1, g[1], b0 * g[0]);
-      sv[warp][2 * t] = fma(b1, g[4], b0 * g[2]);
-      sv[warp][2 * t + 1] = fma(b1, g[5], b0 * g[3]);
-    }
-    __syncwarp();
-    double* out = elem + ((size_t)a * ncell_out + c_out + e) * 81;
-    for (int t = lane; t < 81; t += 32) {  // t = 9*i + j
-      const int ii = t / 9, jj = t % 9;
-      double s = 0.0;
-#pragma unroll
-      for (int q = 0; q < 9; ++q) {
-        s = fma(su[warp][9 * ii + q], sB[9 * jj + q], s);
-        s = fma(sv[warp][2 * (9 * ii + q)], sdB[2 * (9 * jj + q)], s);
-        s = fma(sv[warp][2 * (9 * ii + q) + 1], sdB[2 * (9 * jj + q) + 1], s);
-      }
-      out[t] = s;
-    }
-    __syncwarp();
-  }
-}
-
-// ------------------------------------------------------------------ K3 CSR gather
-// One thread per stored slot of C_free = P^T C P: the weighted sum of the
-// element-matrix entries that land on it, in the map's fixed order
-// (scatter.py builds the map once per mesh; assembly.py:115-129 is the
-// reference's scipy COO->CSR + condensation).  HBM-bound gather.
-__global__ void lb_csr_gather_kernel(int nslots, int nent, int S, const int* __restrict__ slot_ptr,
-                                     const int* __restrict__ gidx, const double* __restrict__ gw,
-                                     const double* __restrict__ elem, double* __restrict__ out) {
-  const int slot = blockIdx.x * blockDim.x + threadIdx.x;
-  if (slot >= nslots) return;
-  const int k0 = slot_ptr[slot], k1 = slot_ptr[slot + 1];
-  for (int a = 0; a < S; ++a) {
-    const double* ea = elem + (size_t)a * nent;
-    double v = 0.0;
-    for (int k = k0; k < k1; ++k) v = fma(gw[k], ea[gidx[k]], v);
-    out[(size_t)a * nslots + slot] = v;
-  }
-}
-
-// ------------------------------------------------------------------ K4 sampling
-// sample_state (fem.py:170-199) + element_geometry (fem.py:103-113) on the
-// device: one thread per quadrature point (e, q) of cells [c0, c1).
-// Coordinates / weights use the reference's exact operation order (no
-// contraction), so r, z, w are bitwise those of the reference; nodal values
-// go through the prolongation rows (hanging nodes: 3 weights).
-__global__ void lb_sample_kernel(int c0, int c1, int S, int n_free, const double* __restrict__ origins,
-                                 const double* __restrict__ sizes, const double* __restrict__ qgeo,
-                                 const double* __restrict__ basis, const int* __restrict__ cell_nodes,
-                                 const int* __restrict__ P_ptr, const int* __restrict__ P_idx,
-                                 const double* __restrict__ P_w, const double* __restrict__ coeffs,
-                                 double* __restrict__ r, double* __restrict__ z, double* __restrict__ w,
-                                 double* __restrict__ f, double* __restrict__ dfr,
-                                 double* __restrict__ dfz) {
-  const int nloc = 9 * (c1 - c0);
-  const int pl = blockIdx.x * blockDim.x + threadIdx.x;
-  if (pl >= nloc) return;
-  const int e = c0 + pl / 9, q = pl % 9;
-  const double sr = sizes[2 * e], sz = sizes[2 * e + 1];
-  // coords = origins + (qpts + 1) * 0.5 * sizes (fem.py:109-111)
-  const double rq = __dadd_rn(origins[2 * e], __dmul_rn(__dmul_rn(__dadd_rn(qgeo[2 * q], 1.0), 0.5), sr));
-  const double zq =
-      __dadd_rn(origins[2 * e + 1], __dmul_rn(__dmul_rn(__dadd_rn(qgeo[2 * q + 1], 1.0), 0.5), sz));
-  const double detJ = __ddiv_rn(__dmul_rn(sr, sz), 4.0);   // fem.py:105
-  r[pl] = rq;
-  z[pl] = zq;
-  w[pl] = __dmul_rn(__dmul_rn(qgeo[18 + q], detJ), rq);   // fem.py:112
-  const double jr = __ddiv_rn(2.0, sr), jz = __ddiv_rn(2.0, sz);  // fem.py:107-108
-  for (int s = 0; s < S; ++s) {
-    const double* cs = coeffs + (size_t)s * n_free;
-    double fv = 0.0, gr = 0.0, gz = 0.0;
-    for (int i = 0; i < 9; ++i) {
-      const int node = cell_nodes[9 * e + i];
-      double v = 0.0;  // (P @ coeffs^T)[node] (fem.py:182)
-      for (int k = P_ptr[node]; k < P_ptr[node + 1]; ++k) v = __dadd_rn(v, __dmul_rn(P_w[k], cs[P_idx[k]]));
-      fv = fma(v, basis[9 * i + q], fv);
-      gr = fma(v, basis[81 + 2 * (9 * i + q)], gr);
-      gz = fma(v, basis[81 + 2 * (9 * i + q) + 1], gz);
-    }
-    f[(size_t)s * nloc + pl] = fv;
-    dfr[(size_t)s * nloc + pl] = __dmul_rn(gr, jr);  // fem.py:188-189
-    dfz[(size_t)s * nloc + pl] = __dmul_rn(gz, jz);
-  }
-}
-
-// ------------------------------------------------------------------ per-pair
-__global__ void lb_pairs_kernel(int npair, const double* __restrict__ r, const double* __restrict__ z,
-                                const double* __restrict__ rb, const double* __restrict__ zb,
-                                double* __restrict__ UK, double* __restrict__ UD) {
-  __shared__ double2 logt[1 << LB_LOGT_BITS];
-  for (int t = threadIdx.x; t < (1 << LB_LOGT_BITS); t += blockDim.x)
-    logt[t] = make_double2(c_logt[2 * t], c_logt[2 * t + 1]);
-  __syncthreads();
-  const int p = blockIdx.x * blockDim.x + threadIdx.x;
-  if (p >= npair) return;
-  const Outer o = make_outer(r[p], z[p]);
-  const double rn = rb[p];
-  const T5 t = pair_tensor(o, rn, zb[p], rn * rn, rn > 0.0 ? 1.0 / rn : 0.0, 1LL, logt);
-  // restore the pulled-out factor 4 (exact) and lay out as kernel.py:227-234
-  UD[4 * p + 0] = 4.0 * t.xx;
-  UD[4 * p + 1] = 4.0 * t.xz;
-  UD[4 * p + 2] = 4.0 * t.xz;
-  UD[4 * p + 3] = 4.0 * t.zz;
-  UK[4 * p + 0] = 4.0 * t.kr;
-  UK[4 * p + 1] = 4.0 * t.xz;
-  UK[4 * p + 2] = 4.0 * t.zr;
-  UK[4 * p + 3] = 4.0 * t.zz;
-}
-
-// ------------------------------------------------------------------ FP64 peak
-constexpr int kDfmaChains = 8;
-constexpr int kDfmaIters = 4096;
-__global__ void __launch_bounds__(256) lb_dfma_kernel(double seed, double* sink) {
-  double v[kDfmaChains];
-#pragma unroll
-  for (int c = 0; c < kDfmaChains; ++c) v[c] = seed + threadIdx.x * 1e-9 + c;
-  const double m = 0.999999, add = 1e-7;
-#pragma unroll 4
-  for (int it = 0; it < kDfmaIters; ++it) {
-#pragma unroll
-    for (int c = 0; c < kDfmaChains; ++c) v[c] = fma(v[c], m, add);
-  }
-  double s = 0.0;
-#pragma unroll
-  for (int c = 0; c < kDfmaChains; ++c) s += v[c];
-  if (s == 12345.6789) sink[threadIdx.x] = s;  // never true; keeps the chains live
-}
 
 // ------------------------------------------------------------------ host side
 thread_local std::string g_err;

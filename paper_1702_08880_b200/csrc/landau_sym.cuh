@@ -28,7 +28,9 @@
 //    segments and the j-side blocks of every row that has its tile as a
 //    partner.  No atomics: results are bitwise reproducible.
 #pragma once
-// (included by landau_b200.cu inside namespace lb, after the sweep helpers)
+#include "landau_sweep.cuh"
+
+namespace lb {
 
 constexpr int kSymTile = 128;   // points per tile (== threads per CTA)
 constexpr int kSymStages = 2;   // TMA ring depth (one J tile per stage)
@@ -326,3 +328,4 @@ __global__ void lb_invert_perm_kernel(int n, const int* __restrict__ perm, int* 
   if (p < n) inv[perm[p]] = p;
 }
 
+}  // namespace lb

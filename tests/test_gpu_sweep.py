@@ -30,7 +30,8 @@ def test_tensor_pairs_match_reference(gpu):
     #    series switch m = 0.01, amplifying rounding by ~1/m^2 (kernel.py:366-367).
     d2 = (P[:, 0] - P[:, 2]) ** 2 + (P[:, 1] - P[:, 3]) ** 2
     m = 4 * P[:, 0] * P[:, 2] / (d2 + 4 * P[:, 0] * P[:, 2])
-    amp = 1.0 + np.maximum(P[:, 0], P[:, 2]) ** 2 / d2 + np.where(m >= 0.01, 1.0 / m**2, 0.0)
+    with np.errstate(divide="ignore"):
+        amp = 1.0 + np.maximum(P[:, 0], P[:, 2]) ** 2 / d2 + np.where(m >= 0.01, 1.0 / m**2, 0.0)
     tol = 64 * np.finfo(float).eps * amp
     benign = amp < 10
     print("pairs worst (benign)", err[benign].max(), "worst err/tol", (err / tol).max())
