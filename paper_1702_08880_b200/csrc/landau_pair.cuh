@@ -90,7 +90,7 @@ __device__ __forceinline__ double rsqrt_nr(double a) {
 constexpr long long kLogOff = 0x3FE6000000000000LL;
 
 // Stage 1 of the log: table lookup and argument reduction.  Returns r with
-// |r| < 2^-7; logc and the exponent (as a double) are written to the refs.
+// |r| < 2^-(LB_LOGT_BITS); logc and the exponent (as a double) are written to the refs.
 __device__ __forceinline__ double log_reduce(double x, const double2* __restrict__ tab,
                                              double& logc, double& kd) {
   const long long ix = __double_as_longlong(x);
@@ -113,6 +113,13 @@ __device__ __forceinline__ double log_finish(double r, double logc, double kd) {
   const double q = fma(fma(-0.125, r2, fma(r, c_misc[1], c_misc[2])), r2 * r2,
                        fma(fma(r, c_misc[3], -0.25), r2, fma(r, c_misc[4], -0.5)));
   const double l1p = fma(r2, q, r);
+#elif LB_LOGT_BITS >= 9
+  // |r| < 2^-9: q(r) = -1/2 + r/3 - r^2/4 + r^3/5 - r^4/6 (terms to r^6)
+  double q = fma(r, c_misc[2], c_misc[3]);  // -1/6 r + 1/5
+  q = fma(q, r, -0.25);
+  q = fma(q, r, c_misc[4]);                 //  1/3
+  q = fma(q, r, -0.5);
+  const double l1p = fma(r * r, q, r);
 #else
   double q = fma(r, c_misc[0], c_misc[1]);  // -1/8 r + 1/7
   q = fma(q, r, c_misc[2]);                 // -1/6
@@ -128,10 +135,10 @@ __device__ __forceinline__ double log_finish(double r, double logc, double kd) {
 // ln(x) for normal positive x (the reference uses an exponent/mantissa split
 // + atanh series, kernel.py:317-337; any log accurate to ~1 ulp agrees to
 // 1e-16).  Here: table-driven reduction, no divide.  The mantissa is folded
-// around 1 (z in [0.6875, 1.375)), a 128-entry table gives invc ~ 1/z and
+// around 1 (z in [0.6875, 1.375)), a 2^LB_LOGT_BITS-entry table gives invc ~ 1/z and
 // logc = -ln(invc) (invc == 1 exactly on the two bins touching 1.0, so ln x
-// keeps full relative accuracy as x -> 1), r = z*invc - 1 (|r| < 2^-7, one
-// FMA), ln(1+r) = r + r^2 q(r) with q the degree-6 Taylor tail.
+// keeps full relative accuracy as x -> 1), r = z*invc - 1 (|r| < 2^-9 with
+// the 512-entry table, one FMA), ln(1+r) = r + r^2 q(r), q the degree-4 Taylor tail.
 // Measured max relative error 2.2e-16 (tools/gen_coefs.py table).
 __device__ __forceinline__ double log_table(double x, const double2* __restrict__ tab) {
   double logc, kd;
