@@ -278,7 +278,7 @@ def ours_arm(args):
     value = pairs_step * args.steps / (tot_ms * 1e-3)
     # roofline of the dominant kernel on this rank: model flops per launch / launch time
     sweep_avg_s = sum(sweep_ms) / len(sweep_ms) * 1e-3
-    nacc = (sh.RS - 4) // 3  # accumulator species sets (1: rank-one species collapse)
+    nacc = sh.nacc  # accumulator species sets (1: rank-one species collapse)
     # ordered pairs this rank's sweep delivers: its outer points x N (general
     # path) or its 1/world share of the tile pairs, each feeding both points
     flops_launch = pkg.flop_count(N, S, N / world if sh.symmetric else nloc)

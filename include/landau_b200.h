@@ -71,6 +71,10 @@ int lb_ctx_destroy(lb_ctx *ctx);
  * sum_b be_b w f) -- padded to an even count. */
 int lb_record_stride(int S, const double *coK, const double *coD);
 
+/* Accumulator species sets the sweep keeps per point: 1 when coK/coD are
+ * rank one (species collapse), else S (-1 for an invalid S). */
+int lb_accumulator_sets(int S, const double *coK, const double *coD);
+
 /* Inner-point chunk length the sweep uses for n inner points (a function of
  * n only; exposed so tests can check the decomposition). */
 int lb_chunk_len(int n);

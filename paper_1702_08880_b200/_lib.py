@@ -35,6 +35,7 @@ SIGNATURES = {
     "lb_ctx_create": (_i, [_i, C.POINTER(_vp)]),
     "lb_ctx_destroy": (_i, [_vp]),
     "lb_record_stride": (_i, [_i, _dp, _dp]),
+    "lb_accumulator_sets": (_i, [_i, _dp, _dp]),
     "lb_chunk_len": (_i, [_i]),
     "lb_fused_sweep": (_i, [_vp, _i, _dp, _dp, _i, _i, _dp, _dp, _dp, _dp, _dp, _dp,
                             _dp, _dp, _d, _dp, _dp]),

@@ -521,6 +521,14 @@ int lb_record_stride(int S, const double* coK, const double* coD) {
   return record_stride(cp);
 }
 
+int lb_accumulator_sets(int S, const double* coK, const double* coD) {
+  if (check_species(S)) return -1;
+  if (!coK || !coD) return S;
+  Coupling cp;
+  make_coupling(S, coK, coD, cp);
+  return cp.Se;
+}
+
 int lb_chunk_len(int n) { return chunk_len(std::max(n, 0)); }
 
 int lb_last_launch_count(lb_ctx* ctx) { return ctx ? ctx->last_launches : 0; }

@@ -39,7 +39,15 @@ inline size_t partial_budget() {
   return b;
 }
 
-__host__ __device__ constexpr int rec_stride(int S) { return ((4 + 3 * S) + 1) & ~1; }
+// Record stride in doubles: the smallest even count >= 4 + 3S whose half is
+// odd.  The symmetric sweep reads records at lane-varying addresses (lane l
+// takes record (l + s) mod 32); a 16-byte load then hits bank group
+// (RS/2 * k) mod 8, so RS/2 odd spreads 32 lanes over all 8 groups (4
+// wavefronts, the minimum) while e.g. RS = 8 would put them on 2 (16-way
+// conflict).
+__host__ __device__ constexpr int rec_stride(int S) {
+  return (((4 + 3 * S) + 1) & ~1) + (((((4 + 3 * S) + 1) & ~1) / 2) % 2 == 0 ? 2 : 0);
+}
 template <int S>
 struct TileCfg {
   static constexpr int RS = rec_stride(S);

@@ -104,10 +104,13 @@ class ShardedSweep:
             self._ctx = _lib.context(self.device.index or 0)
             p = _lib.dptr
             self.RS = lib.lb_record_stride(self.S, p(self.coK), p(self.coD))
+            self.nacc = lib.lb_accumulator_sets(self.S, p(self.coK), p(self.coD))
             if self.RS < 0:
                 _lib.check(1)
         else:
-            self.RS = ((4 + 3 * self.S) + 1) & ~1
+            base = ((4 + 3 * self.S) + 1) & ~1  # rec_stride() of landau_common.cuh
+            self.RS = base + (2 if (base // 2) % 2 == 0 else 0)
+            self.nacc = self.S
         self._pack = pack_fn or self._pack_cuda
         self._sweep = sweep_fn or self._sweep_cuda
         # symmetric all-points path (each unordered pair once, tile pairs split
@@ -123,8 +126,7 @@ class ShardedSweep:
         self.symmetric = sym_ok if symmetric is None else (bool(symmetric) and sym_ok)
         if self.symmetric:  # partial sums: 5 per accumulator set (1 set when collapsed)
             npad = -(-self.n // 128) * 128
-            nacc = (self.RS - 4) // 3 if sym_fns is None else self.S
-            self.tot = torch.zeros((5 * max(nacc, 1), npad), dtype=torch.float64,
+            self.tot = torch.zeros((5 * max(self.nacc, 1), npad), dtype=torch.float64,
                                    device=self.device)
         mc = self.plan.max_count
         f64 = torch.float64

@@ -35,9 +35,9 @@ def test_pure_queries():
 
     lib = _lib.load()
     assert lib.lb_version() == 100
-    assert lib.lb_record_stride(1, None, None) == 8
-    assert lib.lb_record_stride(2, None, None) == 10
-    assert lib.lb_record_stride(4, None, None) == 16
+    # even, >= 4 + 3S, half odd (conflict-free lane-varying 16-byte loads)
+    for S, rs in ((1, 10), (2, 10), (3, 14), (4, 18), (5, 22), (8, 30)):
+        assert lib.lb_record_stride(S, None, None) == rs
     assert lib.lb_record_stride(0, None, None) == -1 and lib.lb_record_stride(9, None, None) == -1
     # rank-one coupling (the reference's own collision_params): species collapse
     import paper_1702_08880_b200 as pkg
@@ -47,13 +47,13 @@ def test_pure_queries():
     nu = np.outer(e**2, e**2)
     p4 = pkg.CollisionParams(nu_hat=nu / nu[0, 0], mass_ratio_o=1.0 / np.array([1, 3670, 21900, 335000.0]))
     coK, coD = pkg.coupling(p4)
-    assert lib.lb_record_stride(4, L.dptr(coK), L.dptr(coD)) == 8
+    assert lib.lb_record_stride(4, L.dptr(coK), L.dptr(coD)) == 10
     assert lib.lb_sym_supported(4, L.dptr(coK), L.dptr(coD)) == 1
     # a coupling that is not rank one keeps the per-species layout
     nu2 = nu.copy()
     nu2[0, 1] *= 1.5
     coK2, coD2 = pkg.coupling(pkg.CollisionParams(nu_hat=nu2, mass_ratio_o=np.ones(4)))
-    assert lib.lb_record_stride(4, L.dptr(coK2), L.dptr(coD2)) == 16
+    assert lib.lb_record_stride(4, L.dptr(coK2), L.dptr(coD2)) == 18
     assert lib.lb_sym_supported(4, L.dptr(coK2), L.dptr(coD2)) == 0
     # inner chunking is a function of n only, whole 128-point tiles, <= 64 chunks
     for n in (1, 72, 1152, 4096, 65536, 1 << 20):
