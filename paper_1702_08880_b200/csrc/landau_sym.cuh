@@ -39,12 +39,17 @@ constexpr int kSymStages = 2;   // TMA ring depth (one J tile per stage)
 #endif
 constexpr int kSegLenMax = LB_SEGLEN;  // partner tiles per work item (large n)
 #ifndef LB_SYM_MINB
-#define LB_SYM_MINB 4
+#define LB_SYM_MINB 5  // CTAs per SM for Se = 1 (94 registers, no spills)
 #endif
 #ifndef LB_SYM_UNROLL
 #define LB_SYM_UNROLL 1
 #endif
 constexpr int kSymMinBlocks = LB_SYM_MINB;
+// register budget per accumulator-set count (measured: Se = 1 at 5 CTAs/SM,
+// Se = 2 spills above 4, Se = 3 needs ~184 registers)
+__host__ __device__ constexpr int sym_min_blocks(int Se) {
+  return Se == 1 ? kSymMinBlocks : (Se == 2 ? 4 : 2);
+}
 constexpr int kSymUnroll = LB_SYM_UNROLL;
 #ifndef LB_SYM_MAXS
 #define LB_SYM_MAXS 3  // measured: S = 4 symmetric (210 regs, 2 CTAs/SM) loses to the general sweep
@@ -96,7 +101,7 @@ __device__ __forceinline__ void load_point(const double* rp, Outer& o, double (&
 }
 
 template <int S>
-__global__ void __launch_bounds__(kSymTile, S <= 2 ? kSymMinBlocks : 2) lb_symsweep_kernel(const SymArgs a) {
+__global__ void __launch_bounds__(kSymTile, sym_min_blocks(S)) lb_symsweep_kernel(const SymArgs a) {
   constexpr int RS = rec_stride(S);
   constexpr int NW = kSymTile / 32;
   extern __shared__ __align__(128) double lb_smem[];
