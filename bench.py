@@ -36,7 +36,9 @@ import numpy as np  # noqa: E402
 
 METRIC = "Landau point-pair evals/s at N=2^16"
 UNIT = "pairs/s"
-FLOPS_PER_PAIR = lambda S: 165 + 20 * S * S  # noqa: E731  (kernel.py:560-574)
+def flops_per_pair(S: int) -> int:
+    """The reference's flop model per ordered pair (kernel.py:560-574)."""
+    return 165 + 20 * S * S
 
 
 def env_int(name, default):
@@ -168,7 +170,7 @@ def reference_arm(args):
                                    f"per step (oracle/ C restatement of kernel.py:306-493, "
                                    f"OpenMP {threads} threads)"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-        "model_gflops": value * FLOPS_PER_PAIR(wl.S) / 1e9,
+        "model_gflops": value * flops_per_pair(wl.S) / 1e9,
     }
     print(json.dumps(line), flush=True)
     return 0

@@ -304,7 +304,9 @@ def union_point_data(datas):
         f[a, sl] = np.atleast_2d(d.f)[row]
         dfr[a, sl] = np.atleast_2d(d.df_r)[row]
         dfz[a, sl] = np.atleast_2d(d.df_z)[row]
-    cat = lambda k: np.ascontiguousarray(np.concatenate([np.asarray(getattr(d, k)) for d in datas]))  # noqa: E731
+    def cat(k):
+        return np.ascontiguousarray(np.concatenate([np.asarray(getattr(d, k)) for d in datas]))
+
     return QuadPointData(N=n, r=cat("r"), z=cat("z"), w=cat("w"), f=f, df_r=dfr, df_z=dfz), off
 
 

@@ -307,7 +307,6 @@ class ShardedOperator:
         c = coeffs if isinstance(coeffs, torch.Tensor) else torch.from_numpy(
             np.ascontiguousarray(np.atleast_2d(coeffs), dtype=np.float64))
         self.coeffs.copy_(c)
-        nl = self.sweep.hi - self.sweep.lo
         st = self._stream()
         lib, h = self._lib, self._ctx.handle
         row = self.fields.stride(0) * 8
@@ -324,6 +323,5 @@ class ShardedOperator:
             _dist().all_reduce(self.csr, group=self.group)
         vals = self.csr.cpu().numpy()
         gm = self.dm.map
-        del nl
         return [sp.csr_matrix((vals[a], gm.indices, gm.indptr), shape=(gm.n_free, gm.n_free))
                 for a in range(self.S)]

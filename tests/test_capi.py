@@ -2,7 +2,6 @@
 without a GPU the product path fails loudly (no CPU fallback).  CPU only."""
 
 import re
-from pathlib import Path
 
 import numpy as np
 import pytest
