@@ -352,10 +352,13 @@ def ours_arm(args):
         err = O.per_component_scaled_error(Kh_[idx - sh.lo], Dh_[idx - sh.lo], Kr, Dr)
         check = allmax([err])[0]
     traffic = None
+    executed = None
     tf_file = ROOT / "profiles" / "sweep_traffic.json"
-    if tf_file.exists():
+    if tf_file.exists():  # committed ncu capture of the same kernel (profiles/)
         try:
-            traffic = json.loads(tf_file.read_text()).get("bytes_per_launch")
+            prof = json.loads(tf_file.read_text())
+            traffic = prof.get("bytes_per_launch")
+            executed = prof.get("executed_fp64_ncu")
         except (OSError, ValueError):
             traffic = None
 
@@ -385,7 +388,8 @@ def ours_arm(args):
                                      "profiles/)" if sh.symmetric else ""),
                          "peak_source": "measured DFMA microbenchmark on this GPU "
                                         "(lb_fp64_peak, median of the last half of 1 s)",
-                         "peak_burst": fp64_burst, "frac_of_nominal_37.2": achieved_tf / 37.2},
+                         "peak_burst": fp64_burst, "frac_of_nominal_37.2": achieved_tf / 37.2,
+                         "executed_fp64_ncu": executed},
             "e2e": e2e,
             "gpu_launches": launches,
             "clocks": clocks,
