@@ -169,3 +169,34 @@ def test_sharded_operator(gpu, tmp_path, world, case):
         worst = max(worst, np.abs(d[f"b{a}"] - r).max() / np.abs(r).max())
     print(f"sharded operator {case} world={world}", worst)
     assert worst < 1e-10
+
+
+def test_bench_json_contract(gpu):
+    """bench.py prints one JSON line with the driver's keys (short run)."""
+    import json
+    import subprocess
+    import sys
+
+    from conftest import ROOT
+
+    out = subprocess.run([sys.executable, "bench.py", "--steps", "3", "--warmup", "3",
+                          "--points", "8192", "--cpu-seconds", "1", "--e2e-steps", "1",
+                          "--peak-seconds", "0.1"], cwd=str(ROOT), capture_output=True,
+                         text=True, timeout=600)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [l for l in out.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step",
+              "higher_is_better", "scaling", "vs_baseline", "dtype", "data", "config",
+              "roofline", "cpu_baseline", "e2e", "gpu_launches", "clocks"):
+        assert k in d, k
+    assert d["steps"] == 3 and d["warmup"] == 3 and d["n_gpus"] == 1
+    assert d["value"] > 0 and d["e2e"]["value"] > 0 and d["gpu_launches"] > 0
+    for k in ("bound", "achieved", "peak", "unit", "frac", "traffic"):
+        assert k in d["roofline"]
+    for k in ("value", "unit", "cores", "kind", "sample"):
+        assert k in d["cpu_baseline"]
+    for k in ("value", "unit", "h2d_bytes_per_step", "d2h_bytes_per_step"):
+        assert k in d["e2e"]
+    assert d["parity_scaled_err_vs_oracle"] < 1e-10
