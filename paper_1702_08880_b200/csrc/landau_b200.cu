@@ -65,7 +65,7 @@ struct lb_ctx {
   // grow-only scratch
   lb::DevBuf in, rec, partial, out, elem, outer, aux, order;
   // symmetric all-points sweep state (lb_sym_*): sorted records, order, partials
-  lb::DevBuf symord, symrec, syminv, symi, symj, symtot;
+  lb::DevBuf symord, symrec, syminv, symi, symj, symtot, symctr;
   int sym_n = -1, sym_S = 0, sym_Se = 0, sym_nt = 0;
   // CUDA graph of the state-level operator's device work (lb_assemble_state):
   // captured on the second call with an unchanged key, replayed after
@@ -358,12 +358,17 @@ int sym_partial(lb_ctx* ctx, long long gthr, int rank, int world, double* tot, c
   int rc;
   if ((rc = ensure(ctx->symi, row_i * RB))) return rc;
   if ((rc = ensure(ctx->symj, row_j * RB))) return rc;
+  const int nbatch = (R1 - R0 + RB - 1) / RB;
+  if ((rc = ensure(ctx->symctr, sizeof(int) * nbatch))) return rc;
+  int* ctr = static_cast<int*>(ctx->symctr.p);
+  LB_CUDA(cudaMemsetAsync(ctr, 0, sizeof(int) * nbatch, st));
   for (int b0 = R0; b0 < R1; b0 += RB) {
     const int b1 = std::min(R1, b0 + RB);
     SymArgs a;
     a.rec = static_cast<const double*>(ctx->symrec.p);
     a.iside = static_cast<double*>(ctx->symi.p);
     a.jside = static_cast<double*>(ctx->symj.p);
+    a.next_item = ctr + (b0 - R0) / RB;
     a.nt = nt;
     a.row0 = b0;
     a.row1 = b1;
@@ -524,7 +529,7 @@ int lb_ctx_destroy(lb_ctx* ctx) {
   cudaSetDevice(ctx->device);
   for (DevBuf* b : {&ctx->in, &ctx->rec, &ctx->partial, &ctx->out, &ctx->elem, &ctx->outer, &ctx->aux,
                     &ctx->order, &ctx->symord, &ctx->symrec, &ctx->syminv, &ctx->symi, &ctx->symj,
-                    &ctx->symtot})
+                    &ctx->symtot, &ctx->symctr})
     if (b->p) cudaFree(b->p);
   for (auto& ev : ctx->ev)
     if (ev) cudaEventDestroy(ev);

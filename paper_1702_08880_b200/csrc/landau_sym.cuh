@@ -85,6 +85,7 @@ struct SymArgs {
   const double* rec;  // sorted records, nt*128 x RS (padding records are inert)
   double* iside;      // [row - row0][nseg][5S][128]
   double* jside;      // [row - row0][hmax][5S][128]
+  int* next_item;     // work counter (zero at launch): items past the first wave
   int nt, row0, row1, nseg, hmax;
   long long gthr;
 };
@@ -106,6 +107,7 @@ __global__ void __launch_bounds__(kSymTile, sym_min_blocks(S)) lb_symsweep_kerne
   constexpr int NW = kSymTile / 32;
   extern __shared__ __align__(128) double lb_smem[];
   __shared__ __align__(8) uint64_t full[kSymStages], empty[kSymStages];
+  __shared__ int stage_item[kSymStages], stage_d[kSymStages];  // what each stage holds (-1: end)
   double2* logt = reinterpret_cast<double2*>(lb_smem + kSymStages * kSymTile * RS);
   double* jred = lb_smem + kSymStages * kSymTile * RS + (2 << LB_LOGT_BITS);  // [2][NW][32][5S]
 
@@ -125,56 +127,79 @@ __global__ void __launch_bounds__(kSymTile, sym_min_blocks(S)) lb_symsweep_kerne
   }
   __syncthreads();
 
-  // producer cursor (thread 0): flat sequence of (item, d) tiles
-  long long p_item = blockIdx.x;
-  int p_d = -1;
+  // Producer (thread 0): walks (item, d) tiles.  Items after the first wave
+  // (item = blockIdx.x) are claimed from a global counter, so CTAs that the
+  // warp schedulers favour take more items and all CTAs of an SM stay
+  // resident until the end.  Every item writes its own partial slot, so the
+  // result does not depend on which CTA ran it.  Each stage carries its
+  // (item, d) to the consumers; item -1 ends the sweep.
+  int p_item = blockIdx.x, p_d = -1;
   uint32_t p_k = 0;
-  auto seg_range = [&](long long item, int& I, int& d0, int& d1) {
-    I = a.row0 + (int)(item / a.nseg);
-    const int seg = (int)(item % a.nseg);
+  bool p_done = false;
+  auto seg_range = [&](int item, int& I, int& d0, int& d1) {
+    I = a.row0 + item / a.nseg;
+    const int seg = item % a.nseg;
     const int L = sym_seglen(a.nt);
     d0 = seg * L;
     d1 = min(sym_h(I, a.nt) + 1, d0 + L);
   };
   auto issue_next = [&]() {
-    int I, d0, d1;
+    if (p_done) return;
+    int I = 0, d0, d1;
     while (p_item < nitems) {
       seg_range(p_item, I, d0, d1);
       if (p_d < 0) p_d = d0;
       if (p_d < d1) break;
-      p_item += gridDim.x;  // empty segment or exhausted: next item
+      p_item = (int)gridDim.x + atomicAdd(a.next_item, 1);  // segment done: claim the next
       p_d = -1;
     }
-    if (p_item >= nitems) return;
     const uint32_t s = p_k % kSymStages;
     if (p_k >= kSymStages) mbar_wait(&empty[s], ((p_k / kSymStages) - 1) & 1);
+    ++p_k;
+    if (p_item >= nitems) {
+      stage_item[s] = -1;
+      mbar_arrive(&full[s]);
+      p_done = true;
+      return;
+    }
+    stage_item[s] = p_item;
+    stage_d[s] = p_d;
     const int J = (I + p_d) % a.nt;
     const uint32_t bytes = kSymTile * RS * sizeof(double);
     mbar_expect_tx(&full[s], bytes);
     bulk_g2s(lb_smem + s * (kSymTile * RS), a.rec + (size_t)J * kSymTile * RS, bytes, &full[s]);
-    ++p_k;
     ++p_d;
   };
   if (tid == 0) issue_next();
 
-  uint32_t k = 0;
-  for (long long item = blockIdx.x; item < nitems; item += gridDim.x) {
-    int I, d0, d1;
-    seg_range(item, I, d0, d1);
-    if (d0 >= d1) continue;
-    Outer o;
-    double gi[S][3];
-    load_point<S>(a.rec + ((size_t)I * kSymTile + tid) * RS, o, gi);
-    double acc[S][5];
+  Outer o;
+  double gi[S][3];
+  double acc[S][5];
+  int cur = -1, I = 0;
+  auto flush_iside = [&]() {
+    double* dst = a.iside + ((size_t)(I - a.row0) * a.nseg + (cur % a.nseg)) * (5 * S) * kSymTile + tid;
 #pragma unroll
     for (int b = 0; b < S; ++b)
 #pragma unroll
-      for (int q = 0; q < 5; ++q) acc[b][q] = 0.0;
-
-    for (int d = d0; d < d1; ++d, ++k) {
-      if (tid == 0) issue_next();
-      const uint32_t s = k % kSymStages;
-      mbar_wait(&full[s], (k / kSymStages) & 1);
+      for (int q = 0; q < 5; ++q) dst[(size_t)(b * 5 + q) * kSymTile] = acc[b][q];
+  };
+  for (uint32_t k = 0;; ++k) {
+    if (tid == 0) issue_next();
+    const uint32_t s = k % kSymStages;
+    mbar_wait(&full[s], (k / kSymStages) & 1);
+    const int item = stage_item[s], d = stage_d[s];
+    if (item < 0) break;
+    if (item != cur) {
+      if (cur >= 0) flush_iside();
+      cur = item;
+      I = a.row0 + item / a.nseg;
+      load_point<S>(a.rec + ((size_t)I * kSymTile + tid) * RS, o, gi);
+#pragma unroll
+      for (int b = 0; b < S; ++b)
+#pragma unroll
+        for (int q = 0; q < 5; ++q) acc[b][q] = 0.0;
+    }
+    {
       const double* tile = lb_smem + s * (kSymTile * RS);
       const bool diag = (d == 0);
 #pragma unroll 1
@@ -248,12 +273,8 @@ __global__ void __launch_bounds__(kSymTile, sym_min_blocks(S)) lb_symsweep_kerne
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[s]);
     }
-    double* dst = a.iside + ((size_t)(I - a.row0) * a.nseg + (item % a.nseg)) * (5 * S) * kSymTile + tid;
-#pragma unroll
-    for (int b = 0; b < S; ++b)
-#pragma unroll
-      for (int q = 0; q < 5; ++q) dst[(size_t)(b * 5 + q) * kSymTile] = acc[b][q];
   }
+  if (cur >= 0) flush_iside();
 }
 
 // Fixed-order reduction of one row batch [row0, row1) into the running
