@@ -328,4 +328,93 @@ __device__ __forceinline__ double pair_tensor_sym(const Outer& o, double rn, dou
   return fma(-o.ri2, p.B5, fma(-rn2, p.B3, p.u));
 }
 
+// U unordered pairs (one outer point, U inner points) evaluated in lockstep:
+// the same arithmetic as pair_tensor_sym, interleaved so every polynomial
+// coefficient is loaded once for U fused multiply-adds and the U dependency
+// chains overlap.  The closed form for S2/S3 is evaluated for every pair and
+// replaced by the series where m < 0.01 (kernel.py:366-378 likewise computes
+// both and selects).
+template <int U>
+__device__ __forceinline__ void pair_tensor_sym_x(const Outer& o, const double (&rn)[U],
+                                                  const double (&zn)[U], const double (&rn2)[U],
+                                                  const double (&rcpr)[U], long long gthr,
+                                                  const double2* __restrict__ logt, T5 (&t)[U],
+                                                  double (&txx2)[U]) {
+  PairS1 s[U];
+  double lx[U], x[U];
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    s[u] = pair_stage1(o, rn[u], zn[u], gthr, logt);
+    x[u] = s[u].x;
+  }
+#pragma unroll
+  for (int u = 0; u < U; ++u) lx[u] = log_finish(s[u].lr, s[u].logc, s[u].kd);
+  // four Horner chains in x per pair (kernel.py:351-359); QK[10] = QEx[10] = QEx[0] = 0
+  double pk[U], qk[U], pe[U], qe[U];
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    pk[u] = fma(c_pk[10], x[u], c_pk[9]);
+    qk[u] = c_qk[9];
+    pe[u] = fma(c_pe[10], x[u], c_pe[9]);
+    qe[u] = c_qe[9];
+  }
+#pragma unroll
+  for (int k = 8; k >= 1; --k) {
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      pk[u] = fma(pk[u], x[u], c_pk[k]);
+      qk[u] = fma(qk[u], x[u], c_qk[k]);
+      pe[u] = fma(pe[u], x[u], c_pe[k]);
+      qe[u] = fma(qe[u], x[u], c_qe[k]);
+    }
+  }
+  double EK[U], EE[U], Em1[U], S2[U], S3[U];
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    pk[u] = fma(pk[u], x[u], c_pk[0]);
+    qk[u] = fma(qk[u], x[u], c_qk[0]);
+    pe[u] = fma(pe[u], x[u], c_pe[0]);
+    qe[u] = qe[u] * x[u];
+    EK[u] = fma(-lx[u], qk[u], pk[u]);
+    EE[u] = fma(-lx[u], qe[u], pe[u]);
+    Em1[u] = EE[u] * rcp_nr(x[u]);  // E/(1-m) = E P/d^2
+    // closed form (kernel.py:366-367); 1/m = P/(4 ri rn)
+    const double invm = s[u].P * o.rfri * rcpr[u];
+    const double a = Em1[u] - EK[u];
+    S2[u] = fma(2.0, a * invm, -Em1[u]);
+    const double c = fma(-2.0, EK[u], Em1[u] + EE[u]);
+    S3[u] = fma(4.0, fma(c, invm, -a) * invm, Em1[u]);
+  }
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    // m < 0.01 (kernel.py:376), tested as x = 1 - m > 0.99 on the bit pattern
+    if (__double_as_longlong(x[u]) > kXSwitchBits) {
+      const double m = s[u].tq * s[u].invP;
+      double s2 = c_s2[9], s3 = c_s3[9];
+#pragma unroll
+      for (int k = 8; k >= 1; --k) {
+        s2 = fma(s2, m, c_s2[k]);
+        s3 = fma(s3, m, c_s3[k]);
+      }
+      S2[u] = s2 * m;
+      S3[u] = fma(s3, m, c_s3[0]);
+    }
+  }
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    const double isPm = s[u].isPm;
+    const double c3 = isPm * s[u].invP;  // P^-3/2 (the 4 is folded into the coupling)
+    PairB p;
+    p.B1 = EK[u] * isPm;
+    p.B3 = Em1[u] * c3;
+    p.B4 = S2[u] * c3;
+    p.B5 = S3[u] * c3;
+    p.dz = s[u].dz;
+    p.dz2 = s[u].dz2;
+    p.u = fma(o.tri * rn[u], p.B4, p.B1);
+    t[u] = pair_tensors(o, rn[u], rn2[u], p);
+    txx2[u] = fma(-o.ri2, p.B5, fma(-rn2[u], p.B3, p.u));
+  }
+}
+
 }  // namespace lb
