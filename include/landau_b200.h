@@ -43,11 +43,13 @@ extern "C" {
 #define LB_ECUDA 2   /* CUDA runtime / launch failure */
 #define LB_ENODEV 3  /* no CUDA device visible */
 #define LB_ENOMEM 4  /* device allocation failed */
+#define LB_ESINGULAR 5 /* singular or non-finite linear solve: maps to solver.StepFailure */
 
 #define LB_MAX_SPECIES 8
 
 typedef struct lb_ctx lb_ctx;
 typedef struct lb_mesh lb_mesh;
+typedef struct lb_cn lb_cn;
 
 /* ABI version (major*100 + minor). */
 int lb_version(void);
@@ -248,6 +250,44 @@ int lb_last_launch_count(lb_ctx *ctx);
  * independent DFMA chains sized to fill every SM, timed with CUDA events.
  * Writes achieved TFLOP/s (2 flops per DFMA) and the kernel time in ms. */
 int lb_fp64_peak(lb_ctx *ctx, double *tflops, double *ms);
+
+/* ---- Crank-Nicolson time step on the device (solver.py:103-150) ----------
+ * The reference solves (M - dt/2 C_a) delta = -R per species with SuperLU
+ * (solver.py:124-133, splu).  Here the free nodes are permuted into a banded
+ * order (perm[p] = free node at band position p, natural or reverse
+ * Cuthill-McKee), cut into blocks of nb rows (nb >= the permuted bandwidth),
+ * and the block-tridiagonal systems of all species are factorised together
+ * on the device (block LU, partial pivoting inside diagonal blocks).
+ *
+ * lb_cn_create     solver with S species for an n x n CSR pattern indptr (n+1)
+ *                  / indices (nnz); with a mesh, n = n_free and the pattern is
+ *                  the mesh's (the order of lb_assemble_csr's values); mesh
+ *                  NULL gives a linear-solve-only instance (lb_cn_linear_step).
+ *                  perm (n), nb the block size; LB_EINVAL if nb is below the
+ *                  permuted bandwidth.
+ * lb_cn_set_mass   mass-matrix values in that pattern (host; fem.py:152-167
+ *                  mass_matrix mapped onto the pattern), or NULL to assemble
+ *                  M on the device from the mesh geometry.
+ * lb_cn_get_mass   download the current mass values (nslots).
+ * lb_cn_newton     newton_step (solver.py:103-134): assemble C at f_guess on
+ *                  the device (and at f_old when C_old is NULL), residual
+ *                  R = M(g - f) - dt/2 (C_g g + C_old f), solve, f_next =
+ *                  f_guess + delta; rnorm = ||R|| / ||M f_old^T||.  States
+ *                  are (S, n_free) host arrays, C_old / C_guess_out (S,
+ *                  nslots).  LB_ESINGULAR: zero pivot or non-finite update.
+ *                  phase_ms (4, optional): assembly, residual+fill, factor,
+ *                  solve+download.
+ * lb_cn_linear_step linear_cn_step (solver.py:137-150): (M - dt/2 C) f+ =
+ *                  (M + dt/2 C) f with C (S, nslots) held fixed. */
+int lb_cn_create(lb_ctx *ctx, const lb_mesh *mesh, int S, int n, const int *indptr,
+                 const int *indices, const int *perm, int nb, lb_cn **out);
+int lb_cn_destroy(lb_cn *cn);
+int lb_cn_set_mass(lb_cn *cn, const double *M_vals);
+int lb_cn_get_mass(lb_cn *cn, double *M_vals);
+int lb_cn_newton(lb_cn *cn, const double *coK, const double *coD, double eps_d, double dt,
+                 const double *f_guess, const double *f_old, const double *C_old,
+                 double *f_next, double *C_guess_out, double *rnorm, double *phase_ms);
+int lb_cn_linear_step(lb_cn *cn, double dt, const double *C, const double *f, double *f_out);
 
 #ifdef __cplusplus
 }

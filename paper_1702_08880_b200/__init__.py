@@ -24,6 +24,7 @@ from .assembly import (
     element_matrices,
     sample_state,
 )
+from .solver import CNSolver, StepFailure, linear_cn_step, newton_step
 from .kernel import (
     Accumulators,
     CollisionParams,
@@ -42,7 +43,7 @@ __version__ = "0.1.0"
 _PATCH = {
     "kernel": ("fused_sweep", "fused_inner_loop"),
     "assembly": ("fused_sweep", "assemble_collision"),
-    "solver": ("assemble_collision", "_assemble_at"),
+    "solver": ("assemble_collision", "_assemble_at", "newton_step", "linear_cn_step"),
     "cli": ("assemble_collision", "fused_sweep"),
 }
 
@@ -62,9 +63,16 @@ def install(axlandau_pkg) -> dict:
     """
     import importlib
 
+    from . import solver as _solver
+
     here = {"fused_sweep": fused_sweep, "fused_inner_loop": fused_inner_loop,
-            "assemble_collision": assemble_collision, "_assemble_at": _assemble_at_cfg}
+            "assemble_collision": assemble_collision, "_assemble_at": _assemble_at_cfg,
+            "newton_step": _solver.newton_step, "linear_cn_step": _solver.linear_cn_step}
     saved = {}
+    ref_solver = importlib.import_module(f"{axlandau_pkg.__name__}.solver")
+    if hasattr(ref_solver, "StepFailure"):  # so the reference's advance() catches ours
+        saved[("@", "StepFailure")] = _solver._StepFailure
+        _solver._StepFailure = ref_solver.StepFailure
     for mod_name, names in _PATCH.items():
         mod = importlib.import_module(f"{axlandau_pkg.__name__}.{mod_name}")
         for nm in names:
@@ -82,6 +90,11 @@ def uninstall(axlandau_pkg, saved: dict) -> None:
     import importlib
 
     for (mod_name, nm), fn in saved.items():
+        if mod_name == "@":  # our solver's failure class
+            from . import solver as _solver
+
+            _solver._StepFailure = fn
+            continue
         mod = axlandau_pkg if not mod_name else importlib.import_module(
             f"{axlandau_pkg.__name__}.{mod_name}")
         setattr(mod, nm, fn)
@@ -91,5 +104,6 @@ __all__ = [
     "Accumulators", "CollisionMatrix", "CollisionParams", "LandauTensorPair",
     "QuadPointData", "assemble_at", "assemble_collision", "assemble_species_meshes", "sample_state", "axisym_tensor_pair", "axisym_tensor_pairs",
     "coupling", "default_eps_d", "element_matrices", "flop_count", "fused_inner_loop",
-    "fused_sweep", "install", "uninstall",
+    "fused_sweep", "install", "uninstall", "CNSolver", "StepFailure", "linear_cn_step",
+    "newton_step",
 ]

@@ -18,7 +18,7 @@ import numpy as np
 _PKG = Path(__file__).resolve().parent
 LIB_PATH = _PKG / "liblandau_b200.so"
 
-LB_OK, LB_EINVAL, LB_ECUDA, LB_ENODEV, LB_ENOMEM = 0, 1, 2, 3, 4
+LB_OK, LB_EINVAL, LB_ECUDA, LB_ENODEV, LB_ENOMEM, LB_ESINGULAR = 0, 1, 2, 3, 4, 5
 MAX_SPECIES = 8
 
 _dp = C.POINTER(C.c_double)
@@ -63,6 +63,12 @@ SIGNATURES = {
     "lb_elements_dev": (_i, [_vp, _i, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
     "lb_last_launch_count": (_i, [_vp]),
     "lb_fp64_peak": (_i, [_vp, _dp, _dp]),
+    "lb_cn_create": (_i, [_vp, _vp, _i, _i, _ip, _ip, _ip, _i, C.POINTER(_vp)]),
+    "lb_cn_destroy": (_i, [_vp]),
+    "lb_cn_set_mass": (_i, [_vp, _dp]),
+    "lb_cn_get_mass": (_i, [_vp, _dp]),
+    "lb_cn_newton": (_i, [_vp, _dp, _dp, _d, _d, _dp, _dp, _dp, _dp, _dp, _dp, _dp]),
+    "lb_cn_linear_step": (_i, [_vp, _d, _dp, _dp, _dp]),
 }
 
 _lib = None
@@ -90,12 +96,19 @@ def load(path: Path | None = None):
         return lib
 
 
+class SingularSystem(RuntimeError):
+    """Zero pivot or non-finite update in a device linear solve (the
+    solver layer re-raises it as solver.StepFailure, solver.py:124-132)."""
+
+
 def check(rc: int) -> None:
     if rc == LB_OK:
         return
     msg = load().lb_last_error().decode(errors="replace")
     if rc == LB_EINVAL:
         raise ValueError(msg)
+    if rc == LB_ESINGULAR:
+        raise SingularSystem(msg)
     raise RuntimeError(f"liblandau_b200 error {rc}: {msg}")
 
 

@@ -28,6 +28,8 @@ NVCC_FLAGS = [
     "-cudart", "static",
     f"-I{ROOT / 'include'}",
 ]
+# cuBLAS (batched dense block LU of the Crank-Nicolson solver, landau_cn.cuh)
+LINK_FLAGS = ["-lcublas"]
 
 
 def nvcc() -> str:
@@ -52,7 +54,7 @@ def build(force: bool = False, verbose: bool = False, out: Path | None = None,
         return LIB
     extra = [f"-D{k}={v}" for k, v in (defines or {}).items()]
     target.parent.mkdir(parents=True, exist_ok=True)
-    cmd = [nvcc(), *NVCC_FLAGS, *extra, "-o", str(target), *map(str, SOURCES)]
+    cmd = [nvcc(), *NVCC_FLAGS, *extra, "-o", str(target), *map(str, SOURCES), *LINK_FLAGS]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
         print(" ".join(cmd), file=sys.stderr)

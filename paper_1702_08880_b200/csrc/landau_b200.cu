@@ -15,9 +15,11 @@
 // Determinism: every reduction runs in a fixed order that is a function of
 // the problem size (and the Morton order of the points); no atomics.
 #include <cub/device/device_radix_sort.cuh>
+#include <cublas_v2.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cmath>
 #include <atomic>
 #include <cstdint>
 #include <cstdio>
@@ -31,6 +33,7 @@
 #include "landau_sweep.cuh"
 #include "landau_sym.cuh"
 #include "landau_aux.cuh"
+#include "landau_cn.cuh"
 
 namespace lb {
 
@@ -986,6 +989,63 @@ int lb_sample_state_dev(lb_ctx* ctx, const lb_mesh* m, int S, int c0, int c1, co
   return LB_OK;
 }
 
+// Scratch of the state-level operator (sampling outputs, records, K/D,
+// element blocks, CSR values) inside the context's grow-only buffers.
+struct StateBufs {
+  double *dr, *dz, *dw, *df, *dfr, *dfz, *dco, *dK, *dD, *delem, *dcsr, *drec;
+};
+
+static int state_bufs(lb_ctx* ctx, const lb_mesh* m, int S, const Coupling& cp, StateBufs& b) {
+  const int ncell = m->ncell, n = 9 * ncell;
+  int rc;
+  const size_t nin = (size_t)(3 + 3 * S) * n + (size_t)S * m->n_free;
+  if ((rc = ensure(ctx->in, nin * sizeof(double)))) return rc;
+  if ((rc = ensure(ctx->rec, (size_t)n * record_stride(cp) * sizeof(double)))) return rc;
+  if ((rc = ensure(ctx->out, (size_t)6 * S * n * sizeof(double)))) return rc;
+  if ((rc = ensure(ctx->elem, ((size_t)81 * S * ncell + (size_t)S * m->nslots) * sizeof(double))))
+    return rc;
+  double* din = static_cast<double*>(ctx->in.p);
+  b.dr = din;
+  b.dz = b.dr + n;
+  b.dw = b.dz + n;
+  b.df = b.dw + n;
+  b.dfr = b.df + (size_t)S * n;
+  b.dfz = b.dfr + (size_t)S * n;
+  b.dco = b.dfz + (size_t)S * n;
+  b.dK = static_cast<double*>(ctx->out.p);
+  b.dD = b.dK + (size_t)2 * S * n;
+  b.delem = static_cast<double*>(ctx->elem.p);
+  b.dcsr = b.delem + (size_t)81 * S * ncell;
+  b.drec = static_cast<double*>(ctx->rec.p);
+  return LB_OK;
+}
+
+// Device work of the state-level operator (solver._assemble_at,
+// solver.py:81-84): sample the nodal coefficients dco -> pack records ->
+// symmetric sweep -> element contraction -> CSR gather into dcsr.
+static int state_issue(lb_ctx* ctx, const lb_mesh* m, int S, const Coupling& cp, long long gthr,
+                       const StateBufs& b, const double* dco, double* dcsr, cudaStream_t st) {
+  const int ncell = m->ncell, n = 9 * ncell;
+  lb_sample_kernel<<<(n + 127) / 128, 128, 0, st>>>(0, ncell, S, m->n_free, m->origins, m->sizes,
+                                                    m->qgeo, m->basis, m->cell_nodes, m->P_ptr,
+                                                    m->P_idx, m->P_w, dco, b.dr, b.dz, b.dw, b.df,
+                                                    b.dfr, b.dfz);
+  LB_CUDA(cudaGetLastError());
+  int r = launch_pack(ctx, n, S, b.dr, b.dz, b.dw, b.df, b.dfr, b.dfz, cp, b.drec, st);
+  if (r) return r;
+  if ((r = all_points_sweep(ctx, n, b.drec, b.dr, b.dz, cp, gthr, b.dK, b.dD, st))) return r;
+  if ((r = launch_elements(ctx, ncell, S, m->sizes, b.dw, b.dK, b.dD, m->basis, m->basis + 81,
+                           b.delem, st)))
+    return r;
+  if (m->nslots) {
+    lb_csr_gather_kernel<<<(m->nslots + 255) / 256, 256, 0, st>>>(m->nslots, 81 * ncell, S,
+                                                                   m->slot_ptr, m->gidx, m->gw,
+                                                                   b.delem, dcsr);
+    LB_CUDA(cudaGetLastError());
+  }
+  return LB_OK;
+}
+
 // Field-wise (padding- and unused-entry-blind) equality of graph keys.
 static bool same_state_key(const lb_ctx::StateKey& a, const lb_ctx::StateKey& b) {
   if (a.m != b.m || a.mesh_uid != b.mesh_uid || a.S != b.S || a.eps != b.eps || a.gen != b.gen)
@@ -1014,40 +1074,12 @@ int lb_assemble_state(lb_ctx* ctx, const lb_mesh* m, int S, const double* coeffs
   Coupling cp;
   make_coupling(S, coK, coD, cp);
   cudaStream_t st = ctx->stream;
-  const size_t nin = (size_t)(3 + 3 * S) * n + (size_t)S * m->n_free;
-  if ((rc = ensure(ctx->in, nin * sizeof(double)))) return rc;
-  if ((rc = ensure(ctx->rec, (size_t)n * record_stride(cp) * sizeof(double)))) return rc;
-  if ((rc = ensure(ctx->out, (size_t)6 * S * n * sizeof(double)))) return rc;
-  if ((rc = ensure(ctx->elem, ((size_t)81 * S * ncell + (size_t)S * m->nslots) * sizeof(double))))
-    return rc;
-  double* din = static_cast<double*>(ctx->in.p);
-  double *dr = din, *dz = dr + n, *dw = dz + n, *df = dw + n, *dfr = df + (size_t)S * n,
-         *dfz = dfr + (size_t)S * n, *dco = dfz + (size_t)S * n;
-  double* dK = static_cast<double*>(ctx->out.p);
-  double* dD = dK + (size_t)2 * S * n;
-  double* delem = static_cast<double*>(ctx->elem.p);
-  double* dcsr = delem + (size_t)81 * S * ncell;
-  double* drec = static_cast<double*>(ctx->rec.p);
+  StateBufs sb;
+  if ((rc = state_bufs(ctx, m, S, cp, sb))) return rc;
+  double *din = sb.dr, *dco = sb.dco, *dcsr = sb.dcsr;
   const long long gthr = mask_threshold(eps_d);
   // device work: sample -> pack -> symmetric sweep -> elements -> CSR gather
-  auto issue = [&]() -> int {
-    lb_sample_kernel<<<(n + 127) / 128, 128, 0, st>>>(0, ncell, S, m->n_free, m->origins, m->sizes,
-                                                      m->qgeo, m->basis, m->cell_nodes, m->P_ptr,
-                                                      m->P_idx, m->P_w, dco, dr, dz, dw, df, dfr, dfz);
-    LB_CUDA(cudaGetLastError());
-    int r = launch_pack(ctx, n, S, dr, dz, dw, df, dfr, dfz, cp, drec, st);
-    if (r) return r;
-    if ((r = all_points_sweep(ctx, n, drec, dr, dz, cp, gthr, dK, dD, st))) return r;
-    if ((r = launch_elements(ctx, ncell, S, m->sizes, dw, dK, dD, m->basis, m->basis + 81, delem, st)))
-      return r;
-    if (m->nslots) {
-      lb_csr_gather_kernel<<<(m->nslots + 255) / 256, 256, 0, st>>>(m->nslots, 81 * ncell, S,
-                                                                     m->slot_ptr, m->gidx, m->gw,
-                                                                     delem, dcsr);
-      LB_CUDA(cudaGetLastError());
-    }
-    return LB_OK;
-  };
+  auto issue = [&]() -> int { return state_issue(ctx, m, S, cp, gthr, sb, dco, dcsr, st); };
   LB_CUDA(cudaEventRecord(ctx->ev[0], st));
   LB_CUDA(cudaMemcpyAsync(dco, coeffs, sizeof(double) * S * m->n_free, cudaMemcpyHostToDevice, st));
   LB_CUDA(cudaEventRecord(ctx->ev[1], st));
@@ -1234,3 +1266,532 @@ int lb_fp64_peak(lb_ctx* ctx, double* tflops, double* ms) {
 }
 
 }  // extern "C"
+
+// ------------------------------------------------------------------ Crank-Nicolson solver
+// Device Newton step / linear CN step (solver.py:103-150): the operator is
+// assembled at the guess on the device (state_issue), the residual and the
+// per-species systems (M - dt/2 C_a) are formed there, and the systems are
+// solved by a block-tridiagonal LU of the permuted banded matrix (batched
+// over species with cuBLAS) instead of SuperLU (solver.py:124-133).
+
+// Block cyclic reduction of the S block-tridiagonal systems.  Level l holds
+// N_l block rows k (original block row r = k 2^l); its odd rows are
+// eliminated in terms of the even ones, which form level l + 1:
+//   odd k:  D_k = P L U (getrf); L_k := D_k^-1 L_k, U_k := D_k^-1 U_k
+//   even k: D_k -= L_k U_{k-1} + U_k L_{k+1}
+//           L'_{k/2} = -L_k L_{k-1},  U'_{k/2} = -U_k U_{k+1}
+// D and the right-hand side live per original row (levels alias them); L and
+// U are stored per level, because the solve needs each level's couplings.
+// Every step is one batched dense call over (rows of the level) x species,
+// so the sequential depth is log2(N) levels instead of N block rows.
+struct CnBatch {  // one batched call: pointer arrays (device) and their count
+  double** A = nullptr;
+  double** B = nullptr;
+  double** C = nullptr;
+  int count = 0;
+};
+
+struct CnLevel {
+  int N = 0;
+  int* piv = nullptr;   // pivots of the odd rows' D, (count x nb), batch order
+  int* info = nullptr;  // getrf info of the odd rows
+  CnBatch getrf;        // A = D (odd rows)
+  CnBatch getrsL, getrsU;  // A = D, B = L / U (odd rows; U: with a right neighbour)
+  CnBatch gemmE, gemmF;    // C = D_even -= A B
+  CnBatch gemmG, gemmH;    // C = next level's L / U = -A B
+  CnBatch solveY;          // B = v (odd rows): v := D^-1 v
+  CnBatch fwdL, fwdU;      // even rows: v_k -= A x (A = L_k / U_k, x = v of the neighbour)
+  CnBatch backL, backU;    // odd rows:  v_k -= A x (A = P^L / P^U)
+};
+
+struct lb_cn {
+  lb_ctx* ctx = nullptr;
+  const lb_mesh* m = nullptr;
+  int S = 0, n = 0, nb = 0, nblk = 0, npad = 0;
+  long long nnz = 0, sstride = 0;  // sstride: block-pool doubles per species
+  bool has_mass = false;
+  cublasHandle_t blas = nullptr;
+  int *indptr = nullptr, *indices = nullptr, *perm = nullptr, *flag = nullptr;
+  long long* off = nullptr;  // CSR slot -> block-pool offset (species 0)
+  double* Mv = nullptr;      // mass values (nnz)
+  double* blk = nullptr;     // block pool: S * sstride
+  long long zero_len = 0;    // level-0 part of the pool (zeroed per fill)
+  std::vector<CnLevel> lv;   // levels 0 .. L (the last has N = 1)
+  double *g = nullptr, *f = nullptr, *d = nullptr, *R = nullptr, *Mf = nullptr, *x = nullptr,
+         *out = nullptr, *Co = nullptr, *Cg = nullptr, *red = nullptr;
+  std::vector<void*> allocs;
+};
+
+#define LB_BLAS(call)                                                                  \
+  do {                                                                                 \
+    cublasStatus_t s_ = (call);                                                        \
+    if (s_ != CUBLAS_STATUS_SUCCESS)                                                   \
+      return fail(LB_ECUDA, std::string(#call) + ": cuBLAS status " + std::to_string((int)s_)); \
+  } while (0)
+
+static int cn_alloc(lb_cn* cn, void** p, size_t bytes) {
+  cudaError_t e = cudaMalloc(p, std::max<size_t>(bytes, 8));
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return fail(e == cudaErrorMemoryAllocation ? LB_ENOMEM : LB_ECUDA,
+                std::string("lb_cn: ") + cudaGetErrorString(e));
+  }
+  cn->allocs.push_back(*p);
+  return LB_OK;
+}
+
+static int cn_factor(lb_cn* cn, cudaStream_t st) {
+  const int nb = cn->nb;
+  const double one = 1.0, mone = -1.0, zero = 0.0;
+  int hinfo = 0;
+  LB_BLAS(cublasSetStream(cn->blas, st));
+  for (const CnLevel& L : cn->lv) {
+    if (L.getrf.count)
+      LB_BLAS(cublasDgetrfBatched(cn->blas, nb, L.getrf.A, nb, L.piv, L.info, L.getrf.count));
+    if (L.getrsL.count)
+      LB_BLAS(cublasDgetrsBatched(cn->blas, CUBLAS_OP_N, nb, nb, L.getrsL.A, nb, L.piv, L.getrsL.B, nb,
+                                  &hinfo, L.getrsL.count));
+    if (L.getrsU.count)
+      LB_BLAS(cublasDgetrsBatched(cn->blas, CUBLAS_OP_N, nb, nb, L.getrsU.A, nb, L.piv, L.getrsU.B, nb,
+                                  &hinfo, L.getrsU.count));
+    const CnBatch* acc[2] = {&L.gemmE, &L.gemmF};
+    for (const CnBatch* b : acc)
+      if (b->count)
+        LB_BLAS(cublasDgemmBatched(cn->blas, CUBLAS_OP_N, CUBLAS_OP_N, nb, nb, nb, &mone, b->A, nb, b->B, nb,
+                                   &one, b->C, nb, b->count));
+    const CnBatch* fresh[2] = {&L.gemmG, &L.gemmH};
+    for (const CnBatch* b : fresh)
+      if (b->count)
+        LB_BLAS(cublasDgemmBatched(cn->blas, CUBLAS_OP_N, CUBLAS_OP_N, nb, nb, nb, &mone, b->A, nb, b->B, nb,
+                                   &zero, b->C, nb, b->count));
+  }
+  // zero pivots anywhere -> singular (splu's RuntimeError, solver.py:127-129)
+  for (size_t l = 0; l < cn->lv.size(); ++l) {
+    const CnLevel& L = cn->lv[l];
+    if (!L.getrf.count) continue;
+    std::vector<int> info(L.getrf.count);
+    LB_CUDA(cudaMemcpyAsync(info.data(), L.info, sizeof(int) * info.size(), cudaMemcpyDeviceToHost, st));
+    LB_CUDA(cudaStreamSynchronize(st));
+    for (size_t k = 0; k < info.size(); ++k)
+      if (info[k] != 0)
+        return fail(LB_ESINGULAR, "singular diagonal block (level " + std::to_string(l) + ", species " +
+                                      std::to_string(k % cn->S) + ", zero pivot " + std::to_string(info[k]) + ")");
+  }
+  return LB_OK;
+}
+
+// x (S x npad, band order) holds the right-hand side on entry, the solution
+// on exit.
+static int cn_solve(lb_cn* cn, cudaStream_t st) {
+  const int nb = cn->nb;
+  const double one = 1.0, mone = -1.0;
+  int hinfo = 0;
+  LB_BLAS(cublasSetStream(cn->blas, st));
+  for (const CnLevel& L : cn->lv) {
+    if (L.solveY.count)
+      LB_BLAS(cublasDgetrsBatched(cn->blas, CUBLAS_OP_N, nb, 1, L.getrf.A, nb, L.piv, L.solveY.B, nb, &hinfo,
+                                  L.solveY.count));
+    const CnBatch* fw[2] = {&L.fwdL, &L.fwdU};
+    for (const CnBatch* b : fw)
+      if (b->count)
+        LB_BLAS(cublasDgemvBatched(cn->blas, CUBLAS_OP_N, nb, nb, &mone, b->A, nb, b->B, 1, &one, b->C, 1,
+                                   b->count));
+  }
+  for (int l = (int)cn->lv.size() - 1; l >= 0; --l) {
+    const CnLevel& L = cn->lv[l];
+    const CnBatch* bk[2] = {&L.backL, &L.backU};
+    for (const CnBatch* b : bk)
+      if (b->count)
+        LB_BLAS(cublasDgemvBatched(cn->blas, CUBLAS_OP_N, nb, nb, &mone, b->A, nb, b->B, 1, &one, b->C, 1,
+                                   b->count));
+  }
+  return LB_OK;
+}
+
+// level-0 blocks = M - h C (C null: M), padded diagonal = identity
+static int cn_fill(lb_cn* cn, const double* C, double h, cudaStream_t st) {
+  for (int a = 0; a < cn->S; ++a)
+    LB_CUDA(cudaMemsetAsync(cn->blk + a * cn->sstride, 0, sizeof(double) * cn->zero_len, st));
+  const long long tot = cn->nnz * cn->S;
+  if (tot)
+    lb_band_fill_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(cn->nnz, cn->S, cn->sstride, cn->off,
+                                                                       cn->Mv, C, h, cn->blk);
+  const int npadrows = cn->S * (cn->npad - cn->n);
+  if (npadrows)
+    lb_band_identity_kernel<<<(npadrows + 255) / 256, 256, 0, st>>>(cn->S, cn->sstride, cn->nb, cn->n,
+                                                                    cn->npad, cn->blk);
+  LB_CUDA(cudaGetLastError());
+  return LB_OK;
+}
+
+static void cn_sumsq(lb_cn* cn, const double* x, long long len, cudaStream_t st, int slot) {
+  lb_sumsq_kernel<<<1, 1024, 0, st>>>(len, x, cn->red + slot);
+}
+
+// Build the level structure and every batched call's pointer arrays.
+static int cn_plan(lb_cn* cn) {
+  const int nb = cn->nb, S = cn->S, N = cn->nblk;
+  const size_t bsz = (size_t)nb * nb;
+  std::vector<int> Ns;
+  for (int Nl = N;; Nl = (Nl + 1) / 2) {
+    Ns.push_back(Nl);
+    if (Nl == 1) break;
+  }
+  // block ids: D[r] = r; level l: L_l[k] = N + 2 (base_l + k), U_l[k] = that + 1
+  std::vector<long long> base(Ns.size() + 1, 0);
+  for (size_t l = 0; l < Ns.size(); ++l) base[l + 1] = base[l] + Ns[l];
+  const long long nblocks = N + 2 * base[Ns.size()];
+  cn->sstride = nblocks * (long long)bsz;
+  cn->zero_len = (long long)(N + 2LL * N) * bsz;  // D and level-0 L, U
+  int rc;
+  if ((rc = cn_alloc(cn, (void**)&cn->blk, sizeof(double) * cn->sstride * S))) return rc;
+  auto D = [&](int r, int a) { return cn->blk + a * cn->sstride + (size_t)r * bsz; };
+  auto Lb = [&](size_t l, int k, int a) {
+    return cn->blk + a * cn->sstride + (size_t)(N + 2 * (base[l] + k)) * bsz;
+  };
+  auto Ub = [&](size_t l, int k, int a) { return Lb(l, k, a) + bsz; };
+  auto V = [&](int r, int a) { return cn->x + (size_t)a * cn->npad + (size_t)r * nb; };
+  // host pointer lists, uploaded at the end into one device pool
+  std::vector<double*> pool;
+  struct Pending {
+    CnBatch* b;
+    size_t a0, b0, c0;
+  };
+  std::vector<Pending> pend;
+  auto make = [&](CnBatch& b, const std::vector<double*>& A, const std::vector<double*>& B,
+                  const std::vector<double*>& C) {
+    b.count = (int)std::max(A.size(), std::max(B.size(), C.size()));
+    Pending p{&b, pool.size(), 0, 0};
+    pool.insert(pool.end(), A.begin(), A.end());
+    p.b0 = pool.size();
+    pool.insert(pool.end(), B.begin(), B.end());
+    p.c0 = pool.size();
+    pool.insert(pool.end(), C.begin(), C.end());
+    pend.push_back(p);
+  };
+  cn->lv.resize(Ns.size());
+  for (size_t l = 0; l < Ns.size(); ++l) {
+    CnLevel& L = cn->lv[l];
+    const int Nl = Ns[l], step = 1 << l;
+    L.N = Nl;
+    std::vector<double*> fA, lB, uA, uB, yB, bLA, bLx, bLy, bUA, bUx, bUy;
+    std::vector<double*> eA, eB, eC, fA2, fB2, fC2, gA, gB, gC, hA, hB, hC;
+    std::vector<double*> wLA, wLx, wLy, wUA, wUx, wUy;
+    // odd rows (or the single row of the last level)
+    for (int k = (Nl == 1 ? 0 : 1); k < Nl; k += 2)
+      for (int a = 0; a < S; ++a) {
+        fA.push_back(D(k * step, a));
+        yB.push_back(V(k * step, a));
+        if (Nl > 1) {
+          lB.push_back(Lb(l, k, a));
+          bLA.push_back(Lb(l, k, a));
+          bLx.push_back(V((k - 1) * step, a));
+          bLy.push_back(V(k * step, a));
+        }
+      }
+    for (int k = 1; k + 1 < Nl; k += 2)  // odd rows with a right neighbour (a prefix)
+      for (int a = 0; a < S; ++a) {
+        uA.push_back(D(k * step, a));
+        uB.push_back(Ub(l, k, a));
+        bUA.push_back(Ub(l, k, a));
+        bUx.push_back(V((k + 1) * step, a));
+        bUy.push_back(V(k * step, a));
+      }
+    if (Nl > 1)
+      for (int k = 0; k < Nl; k += 2)  // even rows
+        for (int a = 0; a < S; ++a) {
+          if (k >= 2) {
+            eA.push_back(Lb(l, k, a));
+            eB.push_back(Ub(l, k - 1, a));
+            eC.push_back(D(k * step, a));
+            gA.push_back(Lb(l, k, a));
+            gB.push_back(Lb(l, k - 1, a));
+            gC.push_back(Lb(l + 1, k / 2, a));
+            wLA.push_back(Lb(l, k, a));
+            wLx.push_back(V((k - 1) * step, a));
+            wLy.push_back(V(k * step, a));
+          }
+          if (k + 1 < Nl) {
+            fA2.push_back(Ub(l, k, a));
+            fB2.push_back(Lb(l, k + 1, a));
+            fC2.push_back(D(k * step, a));
+            wUA.push_back(Ub(l, k, a));
+            wUx.push_back(V((k + 1) * step, a));
+            wUy.push_back(V(k * step, a));
+          }
+          if (k + 2 < Nl) {
+            hA.push_back(Ub(l, k, a));
+            hB.push_back(Ub(l, k + 1, a));
+            hC.push_back(Ub(l + 1, k / 2, a));
+          }
+        }
+    make(L.getrf, fA, {}, {});
+    make(L.getrsL, fA.size() && Nl > 1 ? fA : std::vector<double*>{}, lB, {});
+    make(L.getrsU, uA, uB, {});
+    make(L.gemmE, eA, eB, eC);
+    make(L.gemmF, fA2, fB2, fC2);
+    make(L.gemmG, gA, gB, gC);
+    make(L.gemmH, hA, hB, hC);
+    make(L.solveY, {}, yB, {});
+    make(L.fwdL, wLA, wLx, wLy);
+    make(L.fwdU, wUA, wUx, wUy);
+    make(L.backL, bLA, bLx, bLy);
+    make(L.backU, bUA, bUx, bUy);
+    if ((rc = cn_alloc(cn, (void**)&L.piv, sizeof(int) * std::max<size_t>(fA.size(), 1) * nb))) return rc;
+    if ((rc = cn_alloc(cn, (void**)&L.info, sizeof(int) * std::max<size_t>(fA.size(), 1)))) return rc;
+  }
+  double** dpool = nullptr;
+  if ((rc = cn_alloc(cn, (void**)&dpool, sizeof(double*) * std::max<size_t>(pool.size(), 1)))) return rc;
+  LB_CUDA(cudaMemcpy(dpool, pool.data(), sizeof(double*) * pool.size(), cudaMemcpyHostToDevice));
+  for (const Pending& p : pend) {
+    p.b->A = dpool + p.a0;
+    p.b->B = dpool + p.b0;
+    p.b->C = dpool + p.c0;
+  }
+  return LB_OK;
+}
+
+int lb_cn_create(lb_ctx* ctx, const lb_mesh* m, int S, int n, const int* indptr, const int* indices,
+                 const int* perm, int nb, lb_cn** out) {
+  int rc = use_ctx(ctx);
+  if (rc) return rc;
+  if ((rc = check_species(S))) return rc;
+  if (!out || !indptr || !indices || !perm) return fail(LB_EINVAL, "null argument");
+  *out = nullptr;
+  if (m && (!m->cell_nodes || m->device != ctx->device))
+    return fail(LB_EINVAL, "mesh handle on another device or without geometry");
+  if (n <= 0 || nb <= 0 || indptr[0] != 0) return fail(LB_EINVAL, "bad pattern or block size");
+  const long long nnz = indptr[n];
+  if (m && (n != m->n_free || nnz != m->nslots))
+    return fail(LB_EINVAL, "pattern does not match the mesh (n_free rows, nslots entries)");
+  std::vector<int> inv(n, -1);
+  for (int p = 0; p < n; ++p) {
+    if (perm[p] < 0 || perm[p] >= n || inv[perm[p]] >= 0) return fail(LB_EINVAL, "perm is not a permutation");
+    inv[perm[p]] = p;
+  }
+  const int nblk = (n + nb - 1) / nb;
+  const size_t bsz = (size_t)nb * nb;
+  // slot -> block pool offset (species 0): D[I] = block I, level-0 L_I / U_I
+  // = blocks nblk + 2 I / + 1, column-major inside the block
+  std::vector<long long> off(nnz);
+  for (int row = 0; row < n; ++row)
+    for (int k = indptr[row]; k < indptr[row + 1]; ++k) {
+      const int col = indices[k];
+      if (col < 0 || col >= n) return fail(LB_EINVAL, "column index out of range");
+      const int pi = inv[row], pj = inv[col];
+      const int I = pi / nb, J = pj / nb;
+      long long id;
+      if (J == I) id = I;
+      else if (J == I - 1) id = nblk + 2LL * I;
+      else if (J == I + 1) id = nblk + 2LL * I + 1;
+      else return fail(LB_EINVAL, "block size " + std::to_string(nb) + " is below the permuted bandwidth");
+      off[k] = id * (long long)bsz + (long long)(pj % nb) * nb + (pi % nb);
+    }
+  lb_cn* cn = new lb_cn();
+  cn->ctx = ctx;
+  cn->m = m;
+  cn->S = S;
+  cn->n = n;
+  cn->nnz = nnz;
+  cn->nb = nb;
+  cn->nblk = nblk;
+  cn->npad = nb * nblk;
+  auto bail = [&](int r) {
+    lb_cn_destroy(cn);
+    return r;
+  };
+  const size_t vec = sizeof(double) * S * (size_t)n, vpad = sizeof(double) * S * (size_t)cn->npad;
+  if ((rc = cn_alloc(cn, (void**)&cn->indptr, sizeof(int) * (n + 1))) ||
+      (rc = cn_alloc(cn, (void**)&cn->indices, sizeof(int) * nnz)) ||
+      (rc = cn_alloc(cn, (void**)&cn->perm, sizeof(int) * n)) ||
+      (rc = cn_alloc(cn, (void**)&cn->off, sizeof(long long) * nnz)) ||
+      (rc = cn_alloc(cn, (void**)&cn->Mv, sizeof(double) * nnz)) ||
+      (rc = cn_alloc(cn, (void**)&cn->flag, sizeof(int))) ||
+      (rc = cn_alloc(cn, (void**)&cn->g, vec)) || (rc = cn_alloc(cn, (void**)&cn->f, vec)) ||
+      (rc = cn_alloc(cn, (void**)&cn->d, vec)) || (rc = cn_alloc(cn, (void**)&cn->R, vec)) ||
+      (rc = cn_alloc(cn, (void**)&cn->Mf, vec)) || (rc = cn_alloc(cn, (void**)&cn->out, vec)) ||
+      (rc = cn_alloc(cn, (void**)&cn->x, vpad)) ||
+      (rc = cn_alloc(cn, (void**)&cn->Co, sizeof(double) * S * nnz)) ||
+      (rc = cn_alloc(cn, (void**)&cn->Cg, sizeof(double) * S * nnz)) ||
+      (rc = cn_alloc(cn, (void**)&cn->red, sizeof(double) * 4)) || (rc = cn_plan(cn)))
+    return bail(rc);
+  cudaError_t e = cudaSuccess;
+  auto up = [&](void* dst, const void* src, size_t b) {
+    if (e == cudaSuccess) e = cudaMemcpy(dst, src, b, cudaMemcpyHostToDevice);
+  };
+  up(cn->indptr, indptr, sizeof(int) * (n + 1));
+  up(cn->indices, indices, sizeof(int) * nnz);
+  up(cn->perm, perm, sizeof(int) * n);
+  up(cn->off, off.data(), sizeof(long long) * nnz);
+  if (e != cudaSuccess) return bail(fail(LB_ECUDA, std::string("lb_cn_create: ") + cudaGetErrorString(e)));
+  if (cublasCreate(&cn->blas) != CUBLAS_STATUS_SUCCESS) return bail(fail(LB_ECUDA, "cublasCreate failed"));
+  *out = cn;
+  return LB_OK;
+}
+
+int lb_cn_destroy(lb_cn* cn) {
+  if (!cn) return LB_OK;
+  cudaSetDevice(cn->ctx->device);
+  cudaStreamSynchronize(cn->ctx->stream);
+  if (cn->blas) cublasDestroy(cn->blas);
+  for (void* p : cn->allocs) cudaFree(p);
+  delete cn;
+  return LB_OK;
+}
+
+int lb_cn_set_mass(lb_cn* cn, const double* M_vals) {
+  if (!cn) return fail(LB_EINVAL, "null solver");
+  int rc = use_ctx(cn->ctx);
+  if (rc) return rc;
+  cudaStream_t st = cn->ctx->stream;
+  if (M_vals) {
+    LB_CUDA(cudaMemcpyAsync(cn->Mv, M_vals, sizeof(double) * cn->nnz, cudaMemcpyHostToDevice, st));
+  } else if (!cn->m) {
+    return fail(LB_EINVAL, "device mass matrix needs the solver's mesh");
+  } else {
+    // device mass matrix (fem.py:152-167): sample once for the weights, then
+    // element blocks and the same CSR gather as the operator
+    const lb_mesh* m = cn->m;
+    const int ncell = m->ncell, n9 = 9 * ncell;
+    Coupling cp;
+    const double one = 1.0;
+    make_coupling(1, &one, &one, cp);
+    StateBufs sb;
+    if ((rc = state_bufs(cn->ctx, m, 1, cp, sb))) return rc;
+    LB_CUDA(cudaMemsetAsync(sb.dco, 0, sizeof(double) * m->n_free, st));
+    lb_sample_kernel<<<(n9 + 127) / 128, 128, 0, st>>>(0, ncell, 1, m->n_free, m->origins, m->sizes,
+                                                       m->qgeo, m->basis, m->cell_nodes, m->P_ptr,
+                                                       m->P_idx, m->P_w, sb.dco, sb.dr, sb.dz, sb.dw,
+                                                       sb.df, sb.dfr, sb.dfz);
+    lb_mass_elements_kernel<<<(81 * ncell + 255) / 256, 256, 0, st>>>(ncell, sb.dw, m->basis, sb.delem);
+    if (m->nslots)
+      lb_csr_gather_kernel<<<(m->nslots + 255) / 256, 256, 0, st>>>(m->nslots, 81 * ncell, 1, m->slot_ptr,
+                                                                     m->gidx, m->gw, sb.delem, cn->Mv);
+    LB_CUDA(cudaGetLastError());
+  }
+  LB_CUDA(cudaStreamSynchronize(st));
+  cn->has_mass = true;
+  return LB_OK;
+}
+
+int lb_cn_get_mass(lb_cn* cn, double* M_vals) {
+  if (!cn || !M_vals) return fail(LB_EINVAL, "null argument");
+  if (!cn->has_mass) return fail(LB_EINVAL, "mass matrix not set (lb_cn_set_mass)");
+  int rc = use_ctx(cn->ctx);
+  if (rc) return rc;
+  LB_CUDA(cudaMemcpy(M_vals, cn->Mv, sizeof(double) * cn->nnz, cudaMemcpyDeviceToHost));
+  return LB_OK;
+}
+
+int lb_cn_newton(lb_cn* cn, const double* coK, const double* coD, double eps_d, double dt,
+                 const double* f_guess, const double* f_old, const double* C_old, double* f_next,
+                 double* C_guess_out, double* rnorm, double* phase_ms) {
+  if (!cn) return fail(LB_EINVAL, "null solver");
+  int rc = use_ctx(cn->ctx);
+  if (rc) return rc;
+  if (!coK || !coD || !f_guess || !f_old || !f_next || !rnorm) return fail(LB_EINVAL, "null argument");
+  if (!cn->has_mass) return fail(LB_EINVAL, "mass matrix not set (lb_cn_set_mass)");
+  if (!cn->m) return fail(LB_EINVAL, "lb_cn_newton needs the solver's mesh");
+  if (!(dt > 0.0)) return fail(LB_EINVAL, "dt must be positive");
+  lb_ctx* ctx = cn->ctx;
+  const lb_mesh* m = cn->m;
+  const int S = cn->S, n = cn->n;
+  cudaStream_t st = ctx->stream;
+  cudaEvent_t ev[5];
+  for (auto& x : ev) cudaEventCreate(&x);
+  struct EvGuard {
+    cudaEvent_t* e;
+    ~EvGuard() {
+      for (int i = 0; i < 5; ++i) cudaEventDestroy(e[i]);
+    }
+  } guard{ev};
+  Coupling cp;
+  make_coupling(S, coK, coD, cp);
+  const long long gthr = mask_threshold(eps_d);
+  StateBufs sb;
+  if ((rc = state_bufs(ctx, m, S, cp, sb))) return rc;
+  LB_CUDA(cudaEventRecord(ev[0], st));
+  LB_CUDA(cudaMemcpyAsync(cn->g, f_guess, sizeof(double) * S * n, cudaMemcpyHostToDevice, st));
+  LB_CUDA(cudaMemcpyAsync(cn->f, f_old, sizeof(double) * S * n, cudaMemcpyHostToDevice, st));
+  // C at the guess (and at the old state unless the caller holds it)
+  if ((rc = state_issue(ctx, m, S, cp, gthr, sb, cn->g, cn->Cg, st))) return rc;
+  if (C_old) {
+    LB_CUDA(cudaMemcpyAsync(cn->Co, C_old, sizeof(double) * S * cn->nnz, cudaMemcpyHostToDevice, st));
+  } else if ((rc = state_issue(ctx, m, S, cp, gthr, sb, cn->f, cn->Co, st))) {
+    return rc;
+  }
+  LB_CUDA(cudaEventRecord(ev[1], st));
+  // residual R = M (g - f) - dt/2 (Cg g + Co f) (solver.py:87-100) and its scale
+  const double h = 0.5 * dt;
+  const int nS = S * n;
+  lb_axpby_kernel<<<(nS + 255) / 256, 256, 0, st>>>(nS, cn->g, cn->f, cn->d);
+  lb_cn_residual_kernel<<<(nS + 127) / 128, 128, 0, st>>>(n, S, cn->indptr, cn->indices, cn->nnz, cn->Mv,
+                                                          cn->Cg, cn->Co, cn->g, cn->f, cn->d, h, cn->R,
+                                                          cn->Mf);
+  cn_sumsq(cn, cn->R, nS, st, 0);
+  cn_sumsq(cn, cn->Mf, nS, st, 1);
+  LB_CUDA(cudaGetLastError());
+  // (M - dt/2 Cg) delta = -R per species (solver.py:124-133)
+  if ((rc = cn_fill(cn, cn->Cg, h, st))) return rc;
+  LB_CUDA(cudaEventRecord(ev[2], st));
+  if ((rc = cn_factor(cn, st))) return rc;
+  LB_CUDA(cudaEventRecord(ev[3], st));
+  lb_perm_gather_kernel<<<(S * cn->npad + 255) / 256, 256, 0, st>>>(n, cn->npad, S, cn->perm, cn->R, -1.0,
+                                                                   cn->x);
+  if ((rc = cn_solve(cn, st))) return rc;
+  LB_CUDA(cudaMemsetAsync(cn->flag, 0, sizeof(int), st));
+  lb_perm_update_kernel<<<(nS + 255) / 256, 256, 0, st>>>(n, cn->npad, S, cn->perm, cn->g, cn->x, cn->out,
+                                                          cn->flag);
+  LB_CUDA(cudaGetLastError());
+  double red[2];
+  int bad = 0;
+  LB_CUDA(cudaMemcpyAsync(f_next, cn->out, sizeof(double) * nS, cudaMemcpyDeviceToHost, st));
+  LB_CUDA(cudaMemcpyAsync(red, cn->red, sizeof(double) * 2, cudaMemcpyDeviceToHost, st));
+  LB_CUDA(cudaMemcpyAsync(&bad, cn->flag, sizeof(int), cudaMemcpyDeviceToHost, st));
+  if (C_guess_out)
+    LB_CUDA(cudaMemcpyAsync(C_guess_out, cn->Cg, sizeof(double) * S * cn->nnz, cudaMemcpyDeviceToHost, st));
+  LB_CUDA(cudaEventRecord(ev[4], st));
+  LB_CUDA(cudaStreamSynchronize(st));
+  // rnorm = ||R|| / ||M f_old^T|| (solver.py:118-119)
+  const double scale = std::sqrt(red[1]);
+  *rnorm = scale > 0.0 ? std::sqrt(red[0]) / scale : std::sqrt(red[0]);
+  if (phase_ms)
+    for (int p = 0; p < 4; ++p) {
+      float t = 0.f;
+      LB_CUDA(cudaEventElapsedTime(&t, ev[p], ev[p + 1]));
+      phase_ms[p] = t;
+    }
+  if (bad) return fail(LB_ESINGULAR, "non-finite Newton update");
+  return LB_OK;
+}
+
+int lb_cn_linear_step(lb_cn* cn, double dt, const double* C, const double* f, double* f_out) {
+  if (!cn) return fail(LB_EINVAL, "null solver");
+  int rc = use_ctx(cn->ctx);
+  if (rc) return rc;
+  if (!C || !f || !f_out) return fail(LB_EINVAL, "null argument");
+  if (!cn->has_mass) return fail(LB_EINVAL, "mass matrix not set (lb_cn_set_mass)");
+  const int S = cn->S, n = cn->n, nS = S * n;
+  cudaStream_t st = cn->ctx->stream;
+  const double h = 0.5 * dt;
+  LB_CUDA(cudaMemcpyAsync(cn->Cg, C, sizeof(double) * S * cn->nnz, cudaMemcpyHostToDevice, st));
+  LB_CUDA(cudaMemcpyAsync(cn->f, f, sizeof(double) * nS, cudaMemcpyHostToDevice, st));
+  // rhs = (M + dt/2 C) f (solver.py:146), then (M - dt/2 C) f+ = rhs
+  lb_cn_rhs_kernel<<<(nS + 127) / 128, 128, 0, st>>>(n, S, cn->indptr, cn->indices, cn->nnz, cn->Mv, cn->Cg,
+                                                     cn->f, h, cn->R);
+  if ((rc = cn_fill(cn, cn->Cg, h, st))) return rc;
+  if ((rc = cn_factor(cn, st))) return rc;
+  lb_perm_gather_kernel<<<(S * cn->npad + 255) / 256, 256, 0, st>>>(n, cn->npad, S, cn->perm, cn->R, 1.0,
+                                                                   cn->x);
+  if ((rc = cn_solve(cn, st))) return rc;
+  LB_CUDA(cudaMemsetAsync(cn->flag, 0, sizeof(int), st));
+  lb_perm_update_kernel<<<(nS + 255) / 256, 256, 0, st>>>(n, cn->npad, S, cn->perm, nullptr, cn->x, cn->out,
+                                                          cn->flag);
+  LB_CUDA(cudaGetLastError());
+  int bad = 0;
+  LB_CUDA(cudaMemcpyAsync(f_out, cn->out, sizeof(double) * nS, cudaMemcpyDeviceToHost, st));
+  LB_CUDA(cudaMemcpyAsync(&bad, cn->flag, sizeof(int), cudaMemcpyDeviceToHost, st));
+  LB_CUDA(cudaStreamSynchronize(st));
+  if (bad) return fail(LB_ESINGULAR, "non-finite solution");
+  return LB_OK;
+}

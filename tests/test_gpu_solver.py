@@ -1,0 +1,149 @@
+"""Device Crank-Nicolson step: newton_step and
+linear_cn_step (solver.py:103-150) with the operator assembled and the
+per-species systems (M - dt/2 C_a) solved on the B200 (block-tridiagonal
+LU of the banded matrix), against the reference's SuperLU results.
+Bar: post-step state max|df|/max|f_ref| <= 1e-10, moments relative <= 1e-10."""
+
+from types import SimpleNamespace
+
+import numpy as np
+import pytest
+import scipy.sparse as sp
+import scipy.sparse.linalg as spla
+
+from conftest import blocks_from, csr_from, golden, mesh_from, params_from, ref_from
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-10
+
+
+def _scaled(x, ref):
+    return float(np.abs(x - ref).max() / np.abs(ref).max())
+
+
+def test_newton_step_cfg3(gpu):
+    """BASELINE config 3 (refined mesh, 168 hanging nodes, two species): one
+    newton_step(state, state, ..., M=M) with max_newton=1 (the fixture's
+    reference call) reproduces the reference's next state and residual."""
+    g = golden("cfg3")
+    cfg = SimpleNamespace(dt=float(g["dt"]), eps_d=None)
+    M = csr_from(g, "M")
+    f0 = g["coeffs"]
+    nxt, rnorm = gpu.newton_step(f0, f0, mesh_from(g), ref_from(g), params_from(g), cfg, M=M)
+    err = _scaled(nxt, g["newton_coeffs"])
+    print("cfg3 device newton step", err, "rnorm", rnorm, float(g["newton_rnorm"]))
+    assert err <= TOL
+    assert abs(rnorm - float(g["newton_rnorm"])) <= 1e-8 * float(g["newton_rnorm"])
+    m = g["masses"]
+    moms = np.stack([g["Wm"] @ nxt[a] * np.array([1.0, m[a], m[a], m[a]]) for a in range(2)], 1)
+    ref = g["moms1"]
+    assert np.all(np.abs(moms - ref)[[0, 2]] <= 1e-10 * np.abs(ref[[0, 2]]))
+    assert np.all(np.abs(moms - ref)[[1, 3]] <= 1e-10 * np.abs(ref[[0, 2]]))
+
+
+def test_newton_step_c_old_and_device_mass(gpu):
+    """C_old passed in (as advance() does) and M assembled on the device give
+    the same step as the defaults."""
+    g = golden("cfg3")
+    mesh, ref, params = mesh_from(g), ref_from(g), params_from(g)
+    cfg = SimpleNamespace(dt=float(g["dt"]), eps_d=None)
+    M = csr_from(g, "M")
+    f0 = g["coeffs"]
+    C_old = gpu.assemble_at(mesh, ref, f0, params)
+    a, ra = gpu.newton_step(f0, f0, mesh, ref, params, cfg, M=M, C_old=C_old)
+    b, rb = gpu.newton_step(f0, f0, mesh, ref, params, cfg, M=None)
+    assert _scaled(a, g["newton_coeffs"]) <= TOL
+    assert _scaled(b, g["newton_coeffs"]) <= TOL
+    assert abs(ra - rb) <= 1e-12 * abs(ra)
+
+
+@pytest.mark.parametrize("case", ["cfg1", "cfg3"])
+def test_device_mass_matrix(gpu, case):
+    """Device mass matrix (fem.py:152-167: r-weighted 3x3 Gauss, P^T M P)
+    against the reference's mass_matrix."""
+    g = golden(case)
+    mesh, ref = mesh_from(g), ref_from(g)
+    from paper_1702_08880_b200.solver import _mesh_solver, pattern_values
+
+    s = _mesh_solver(mesh, ref, 1)
+    s.set_mass(None)
+    got = s.mass_values()
+    want = pattern_values(csr_from(g, "M"), s.indptr, s.indices, s.n)
+    err = _scaled(got, want)
+    print(case, "device mass matrix", err, "bandwidth", s.bandwidth)
+    assert err <= 1e-14
+
+
+def test_linear_cn_step_cfg1(gpu):
+    """linear_cn_step (solver.py:137-150) with the reference's own C and M
+    gives the reference's CN state (the fixture's cn_coeffs)."""
+    g = golden("cfg1")
+    C = SimpleNamespace(blocks=blocks_from(g, "C"))
+    out = gpu.linear_cn_step(csr_from(g, "M"), C, float(g["dt"]), g["coeffs"])
+    err = _scaled(out[0], g["cn_coeffs"][0])
+    print("cfg1 device linear CN", err)
+    assert err <= TOL
+
+
+def test_linear_cn_matches_splu_multi_species(gpu):
+    """Banded block LU vs SuperLU on the two-species hanging-node operator,
+    both signs of dt (time reversibility of the frozen-C map)."""
+    g = golden("cfg3")
+    M = csr_from(g, "M")
+    blocks = blocks_from(g, "C")
+    C = SimpleNamespace(blocks=blocks)
+    f0 = g["coeffs"]
+    for dt in (0.1, 1.0, -0.1):
+        out = gpu.linear_cn_step(M, C, dt, f0)
+        for a in range(2):
+            want = spla.splu((M - 0.5 * dt * blocks[a]).tocsc()).solve((M + 0.5 * dt * blocks[a]) @ f0[a])
+            assert _scaled(out[a], want) <= TOL, (dt, a)
+    # test_solver.py:85-91 (reversible to 1e-10) and 73-82 (frozen residual)
+    fwd = gpu.linear_cn_step(M, C, 0.1, f0)
+    back = gpu.linear_cn_step(M, C, -0.1, fwd)
+    assert _scaled(back, f0) < 1e-10
+    R = np.stack([M @ (fwd[a] - f0[a]) - 0.05 * (blocks[a] @ fwd[a] + blocks[a] @ f0[a])
+                  for a in range(2)])
+    assert np.linalg.norm(R) < 1e-10 * np.linalg.norm(M @ f0.T)
+
+
+def test_singular_system_raises_step_failure(gpu):
+    """A singular system (zero matrix) raises StepFailure, as splu's
+    RuntimeError does in the reference (solver.py:127-129)."""
+    g = golden("cfg1")
+    M = csr_from(g, "M")
+    Z = sp.csr_matrix(M.shape)
+    C = SimpleNamespace(blocks=[Z])
+    with pytest.raises(gpu.StepFailure):
+        gpu.linear_cn_step(Z, C, 0.1, g["coeffs"])
+
+
+def test_newton_iterations_contract(gpu):
+    """advance()'s inner loop (solver.py:171-185): repeated device Newton
+    iterations at a fixed old state contract (test_solver.py:94-108: ratios
+    < 0.6), track the same iteration done on the host with SuperLU to 1e-10,
+    and conserve density to the reference's digits at every iterate."""
+    g = golden("cfg3")
+    mesh, ref, params = mesh_from(g), ref_from(g), params_from(g)
+    dt = float(g["dt"])
+    cfg = SimpleNamespace(dt=dt, eps_d=None)
+    M = csr_from(g, "M")
+    f0 = g["coeffs"]
+    C_old = gpu.assemble_at(mesh, ref, f0, params)
+    guess, host, res = f0, f0.copy(), []
+    n0 = g["Wm"][0] @ f0.T
+    for _ in range(5):
+        guess, r = gpu.newton_step(guess, f0, mesh, ref, params, cfg, M=M, C_old=C_old)
+        res.append(r)
+        Cg = gpu.assemble_at(mesh, ref, host, params)
+        nxt = np.empty_like(host)
+        for a in range(2):
+            R = M @ (host[a] - f0[a]) - 0.5 * dt * (Cg.blocks[a] @ host[a] + C_old.blocks[a] @ f0[a])
+            nxt[a] = host[a] + spla.splu((M - 0.5 * dt * Cg.blocks[a]).tocsc()).solve(-R)
+        host = nxt
+        assert _scaled(guess, host) <= TOL
+        n1 = g["Wm"][0] @ guess.T
+        assert np.all(np.abs(n1 - n0) <= 1e-11 * np.abs(n0))
+    print("newton residuals", res)
+    assert np.all(np.array(res[1:]) / np.array(res[:-1]) < 0.6)
