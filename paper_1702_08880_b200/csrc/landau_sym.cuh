@@ -33,7 +33,10 @@
 namespace lb {
 
 constexpr int kSymTile = 128;   // points per tile (== threads per CTA)
-constexpr int kSymStages = 2;   // TMA ring depth (one J tile per stage)
+#ifndef LB_SYM_STAGES
+#define LB_SYM_STAGES 2
+#endif
+constexpr int kSymStages = LB_SYM_STAGES;  // TMA ring depth (one J tile per stage)
 #ifndef LB_SEGLEN
 #define LB_SEGLEN 2
 #endif
