@@ -111,6 +111,28 @@ def _f64(a) -> np.ndarray:
     return np.ascontiguousarray(a, dtype=np.float64)
 
 
+_PINNED = None  # torch module when page-locked output staging is available
+
+
+def _host_out(shape) -> np.ndarray:
+    """Output array for a device->host copy: page-locked memory from torch's
+    caching host allocator when CUDA is up (the copy then runs at full link
+    speed instead of through the driver's pageable staging), else plain
+    numpy.  Either way the caller gets an ordinary float64 ndarray (a
+    pinned one keeps its torch storage alive through `.base`)."""
+    global _PINNED
+    if _PINNED is None:
+        try:
+            import torch
+
+            _PINNED = torch if torch.cuda.is_available() else False
+        except Exception:  # pragma: no cover
+            _PINNED = False
+    if _PINNED is False:
+        return np.empty(shape)
+    return _PINNED.empty(shape, dtype=_PINNED.float64, pin_memory=True).numpy()
+
+
 def _inner_fields(data, S: int):
     r, z, w = _f64(data.r), _f64(data.z), _f64(data.w)
     f, dfr, dfz = _f64(data.f), _f64(data.df_r), _f64(data.df_z)
@@ -144,13 +166,13 @@ def fused_sweep(outer_r, outer_z, data, params, eps_d: float = 0.0,
     r, z, w, f, dfr, dfz = _inner_fields(data, S)
     coK, coD = coupling(params)
     nout, n = ro.shape[0], r.shape[0]
-    K = np.empty((nout, S, 2))
-    D = np.empty((nout, S, 2, 2))
     if nout == 0:
-        return K, D
+        return np.empty((0, S, 2)), np.empty((0, S, 2, 2))
+    K = _host_out((nout, S, 2))
+    D = _host_out((nout, S, 2, 2))
     ctx = _lib.context()
     p = _lib.dptr
-    if nout == n and np.array_equal(ro, r) and np.array_equal(zo, z):
+    if nout == n and (ro is r or np.array_equal(ro, r)) and (zo is z or np.array_equal(zo, z)):
         # all-points sweep (assemble_collision's call, assembly.py:148): each
         # unordered pair is evaluated once on the device (symmetric path)
         _lib.check(_lib.load().lb_fused_sweep_all(
