@@ -24,3 +24,12 @@ for name, f in [("api", lambda: pkg.fused_sweep(hp[0], hp[1], data, params, eps_
     for _ in range(8):
         t0 = time.perf_counter(); f(); ts.append(time.perf_counter() - t0)
     print(name, "%.3f ms" % (1e3 * min(ts)), "median %.3f" % (1e3 * sorted(ts)[4]))
+# the bench's pattern: results kept until the next call returns
+ts = []
+K, D = pkg.fused_sweep(hp[0], hp[1], data, params, eps_d=wl.eps_d)
+for _ in range(8):
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    K, D = pkg.fused_sweep(hp[0], hp[1], data, params, eps_d=wl.eps_d)
+    ts.append(time.perf_counter() - t0)
+print("bench pattern per step ms", [round(1e3 * t, 2) for t in ts])
