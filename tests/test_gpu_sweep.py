@@ -157,6 +157,29 @@ def test_cfg5_headline_full_properties(gpu):
         assert np.array_equal(Ks, Kw[lo:hi]) and np.array_equal(Ds, Dw[lo:hi])
 
 
+def test_cfg5_max_size(gpu, oracle):
+    """BASELINE config 5 at its largest size, N = 2^20 (1.1e12 ordered pairs,
+    scratch-bounded row batches on the symmetric path): finite, D symmetric,
+    and 48 outer points (evenly spaced + the 16 closest-pair owners) agree
+    with the oracle to 1e-10."""
+    from scipy.spatial import cKDTree
+
+    N = 1 << 20
+    wl, data, params = _cfg5(N)
+    K, D = gpu.fused_sweep(wl.r, wl.z, data, params, eps_d=wl.eps_d)
+    assert np.all(np.isfinite(K)) and np.all(np.isfinite(D))
+    assert np.array_equal(D[..., 0, 1], D[..., 1, 0])
+    pts = np.stack([wl.r, wl.z], 1)
+    dist, nn = cKDTree(pts).query(pts, k=2)
+    close = np.argsort(dist[:, 1])[:16]
+    idx = np.unique(np.concatenate([np.linspace(0, N - 1, 32).astype(np.int64), close]))
+    Kr, Dr = oracle.fused_sweep(wl.r[idx], wl.z[idx], wl.r, wl.z, wl.w, wl.f, wl.df_r, wl.df_z,
+                                wl.nu_hat, wl.mass_ratio_o, eps_d=wl.eps_d)
+    err = worst_component(K[idx], D[idx], Kr, Dr)
+    print("cfg5 N=2^20 subset incl. closest pairs", err)
+    assert err < TOL
+
+
 @pytest.mark.parametrize("S", [1, 3, 5, 8])
 def test_species_counts_vs_oracle(gpu, oracle, S):
     rng = np.random.default_rng(100 + S)
