@@ -334,6 +334,12 @@ int sym_prepare(lb_ctx* ctx, int n, const Coupling& cp, const double* rec, cudaS
 }
 
 template <int S>
+auto sym_kernel() {
+  if constexpr (S == 1 && LB_SYM_IB) return lb_symsweep_ib_kernel<S>;
+  else return lb_symsweep_kernel<S>;
+}
+
+template <int S>
 int sym_partial(lb_ctx* ctx, long long gthr, int rank, int world, double* tot, cudaStream_t st) {
   const int nt = ctx->sym_nt;
   const int npad = nt * kSymTile;
@@ -348,12 +354,12 @@ int sym_partial(lb_ctx* ctx, long long gthr, int rank, int world, double* tot, c
   const size_t smem = sym_smem_bytes<S>();
   static bool attr_done[64] = {};
   if (!attr_done[ctx->device & 63]) {
-    LB_CUDA(cudaFuncSetAttribute(lb_symsweep_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    LB_CUDA(cudaFuncSetAttribute(sym_kernel<S>(), cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)smem));
     attr_done[ctx->device & 63] = true;
   }
   int per_sm = 0;
-  LB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, lb_symsweep_kernel<S>, kSymTile, smem));
+  LB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sym_kernel<S>(), sym_threads<S>(), smem));
   per_sm = std::max(per_sm, 1);
   const size_t row_i = (size_t)nseg * 5 * S * kSymTile * sizeof(double);
   const size_t row_j = (size_t)std::max(hmax, 1) * 5 * S * kSymTile * sizeof(double);
@@ -380,7 +386,7 @@ int sym_partial(lb_ctx* ctx, long long gthr, int rank, int world, double* tot, c
     a.gthr = gthr;
     const long long nitems = (long long)(b1 - b0) * nseg;
     const int grid = (int)std::min<long long>(nitems, (long long)ctx->num_sms * per_sm);
-    lb_symsweep_kernel<S><<<grid, kSymTile, smem, st>>>(a);
+    sym_kernel<S>()<<<grid, sym_threads<S>(), smem, st>>>(a);
     LB_CUDA(cudaGetLastError());
     lb_symreduce_kernel<S><<<(npad + 127) / 128, 128, 0, st>>>(a.iside, a.jside, nt, b0, b1, nseg,
                                                                hmax, b0 == R0 ? 1 : 0, tot);

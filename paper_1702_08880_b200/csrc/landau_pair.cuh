@@ -328,14 +328,14 @@ __device__ __forceinline__ double pair_tensor_sym(const Outer& o, double rn, dou
   return fma(-o.ri2, p.B5, fma(-rn2, p.B3, p.u));
 }
 
-// U unordered pairs (one outer point, U inner points) evaluated in lockstep:
+// U unordered pairs (outer point oo[u], inner point u) evaluated in lockstep:
 // the same arithmetic as pair_tensor_sym, interleaved so every polynomial
 // coefficient is loaded once for U fused multiply-adds and the U dependency
 // chains overlap.  The closed form for S2/S3 is evaluated for every pair and
 // replaced by the series where m < 0.01 (kernel.py:366-378 likewise computes
 // both and selects).
 template <int U>
-__device__ __forceinline__ void pair_tensor_sym_x(const Outer& o, const double (&rn)[U],
+__device__ __forceinline__ void pair_tensor_sym_x(const Outer (&oo)[U], const double (&rn)[U],
                                                   const double (&zn)[U], const double (&rn2)[U],
                                                   const double (&rcpr)[U], long long gthr,
                                                   const double2* __restrict__ logt, T5 (&t)[U],
@@ -344,7 +344,7 @@ __device__ __forceinline__ void pair_tensor_sym_x(const Outer& o, const double (
   double lx[U], x[U];
 #pragma unroll
   for (int u = 0; u < U; ++u) {
-    s[u] = pair_stage1(o, rn[u], zn[u], gthr, logt);
+    s[u] = pair_stage1(oo[u], rn[u], zn[u], gthr, logt);
     x[u] = s[u].x;
   }
 #pragma unroll
@@ -379,7 +379,7 @@ __device__ __forceinline__ void pair_tensor_sym_x(const Outer& o, const double (
     EE[u] = fma(-lx[u], qe[u], pe[u]);
     Em1[u] = EE[u] * rcp_nr(x[u]);  // E/(1-m) = E P/d^2
     // closed form (kernel.py:366-367); 1/m = P/(4 ri rn)
-    const double invm = s[u].P * o.rfri * rcpr[u];
+    const double invm = s[u].P * oo[u].rfri * rcpr[u];
     const double a = Em1[u] - EK[u];
     S2[u] = fma(2.0, a * invm, -Em1[u]);
     const double c = fma(-2.0, EK[u], Em1[u] + EE[u]);
@@ -411,9 +411,9 @@ __device__ __forceinline__ void pair_tensor_sym_x(const Outer& o, const double (
     p.B5 = S3[u] * c3;
     p.dz = s[u].dz;
     p.dz2 = s[u].dz2;
-    p.u = fma(o.tri * rn[u], p.B4, p.B1);
-    t[u] = pair_tensors(o, rn[u], rn2[u], p);
-    txx2[u] = fma(-o.ri2, p.B5, fma(-rn2[u], p.B3, p.u));
+    p.u = fma(oo[u].tri * rn[u], p.B4, p.B1);
+    t[u] = pair_tensors(oo[u], rn[u], rn2[u], p);
+    txx2[u] = fma(-oo[u].ri2, p.B5, fma(-rn2[u], p.B3, p.u));
   }
 }
 

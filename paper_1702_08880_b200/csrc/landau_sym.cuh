@@ -89,12 +89,21 @@ __host__ __device__ __forceinline__ int sym_nseg(int nt) {
   return (sym_hmax(nt) + 1 + L - 1) / L;
 }
 
-// TMA stages + log table + j-side exchange (2 x 4 warps x 32 j x 5S doubles)
+#ifndef LB_SYM_IB
+#define LB_SYM_IB 1  // species-collapsed sweep: two outer points per thread (lb_symsweep_ib_kernel)
+#endif
+constexpr int kIbThreads = kSymTile / 2;
+template <int S>
+__host__ __device__ constexpr int sym_threads() {
+  return (S == 1 && LB_SYM_IB) ? kIbThreads : kSymTile;
+}
+
+// TMA stages + log table + j-side exchange (2 x warps x 32 j x 5S doubles)
 template <int S>
 constexpr size_t sym_smem_bytes() {
   return size_t(kSymStages) * kSymTile * rec_stride(S) * sizeof(double) +
          size_t(2 << LB_LOGT_BITS) * sizeof(double) +
-         size_t(2) * (kSymTile / 32) * 32 * 5 * S * sizeof(double);
+         size_t(2) * (sym_threads<S>() / 32) * 32 * 5 * S * sizeof(double);
 }
 
 struct SymArgs {
@@ -259,7 +268,10 @@ __global__ void __launch_bounds__(kSymTile, sym_min_blocks(S)) lb_symsweep_kerne
             }
             T5 t[U];
             double txx2[U];
-            pair_tensor_sym_x<U>(o, rn, zn, rn2, rcpr, a.gthr, logt, t, txx2);
+            Outer oo[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) oo[u] = o;
+            pair_tensor_sym_x<U>(oo, rn, zn, rn2, rcpr, a.gthr, logt, t, txx2);
 #pragma unroll
             for (int u = 0; u < U; ++u) {
 #pragma unroll
@@ -378,6 +390,235 @@ __global__ void __launch_bounds__(kSymTile, sym_min_blocks(S)) lb_symsweep_kerne
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[s]);
     }
+  }
+  if (cur >= 0) flush_iside();
+}
+
+// Species-collapsed variant with two OUTER points per thread (i-blocking):
+// 64 threads own the 128 points of the row tile (lane l of warp w: points
+// 64w + l and 64w + 32 + l) and every step pairs both with the same partner
+// j = (l + s) mod 32, so the partner's record loads, the coefficient loads
+// and the one j-side accumulator shuffle are shared by two pairs.  Same
+// work items, schedule, TMA ring and partial layouts as lb_symsweep_kernel.
+#ifndef LB_IB_PAIRS
+#define LB_IB_PAIRS 2  // partners per step, each paired with both outer points (4 pairs)
+#endif
+#ifndef LB_IB_MINB
+#define LB_IB_MINB (LB_IB_PAIRS == 2 ? 4 : 6)  // CTAs per SM (240 / 168 registers)
+#endif
+
+template <int S>
+__global__ void __launch_bounds__(kIbThreads, LB_IB_MINB) lb_symsweep_ib_kernel(const SymArgs a) {
+  constexpr int RS = rec_stride(S);
+  constexpr int NW = kIbThreads / 32;
+  extern __shared__ __align__(128) double lb_smem[];
+  __shared__ __align__(8) uint64_t full[kSymStages], empty[kSymStages];
+  __shared__ int stage_item[kSymStages], stage_d[kSymStages];
+  double2* logt = reinterpret_cast<double2*>(lb_smem + kSymStages * kSymTile * RS);
+  double* jred = lb_smem + kSymStages * kSymTile * RS + (2 << LB_LOGT_BITS);  // [2][NW][32][5S]
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int nrows = a.row1 - a.row0;
+  const long long nitems = (long long)nrows * a.nseg;
+  for (int t = tid; t < (2 << LB_LOGT_BITS); t += kIbThreads)
+    lb_smem[kSymStages * kSymTile * RS + t] = c_logt[t];
+  if (tid == 0) {
+#pragma unroll
+    for (int s = 0; s < kSymStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], NW);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  int p_item = blockIdx.x, p_d = -1;
+  uint32_t p_k = 0;
+  bool p_done = false;
+  auto seg_range = [&](int item, int& I, int& d0, int& d1) {
+    I = a.row0 + item / a.nseg;
+    const int seg = item % a.nseg;
+    const int L = sym_seglen(a.nt);
+    d0 = seg * L;
+    d1 = min(sym_h(I, a.nt) + 1, d0 + L);
+  };
+  auto issue_next = [&]() {
+    if (p_done) return;
+    int I = 0, d0, d1;
+    while (p_item < nitems) {
+      seg_range(p_item, I, d0, d1);
+      if (p_d < 0) p_d = d0;
+      if (p_d < d1) break;
+      p_item = (int)gridDim.x + atomicAdd(a.next_item, 1);
+      p_d = -1;
+    }
+    const uint32_t s = p_k % kSymStages;
+    if (p_k >= kSymStages) mbar_wait(&empty[s], ((p_k / kSymStages) - 1) & 1);
+    ++p_k;
+    if (p_item >= nitems) {
+      stage_item[s] = -1;
+      mbar_arrive(&full[s]);
+      p_done = true;
+      return;
+    }
+    stage_item[s] = p_item;
+    stage_d[s] = p_d;
+    const int J = (I + p_d) % a.nt;
+    const uint32_t bytes = kSymTile * RS * sizeof(double);
+    mbar_expect_tx(&full[s], bytes);
+    bulk_g2s(lb_smem + s * (kSymTile * RS), a.rec + (size_t)J * kSymTile * RS, bytes, &full[s]);
+    ++p_d;
+  };
+  if (tid == 0) issue_next();
+
+  Outer o[2];
+  double gi[2][S][3];
+  double acc[2][S][5];
+  int cur = -1, I = 0;
+  auto pidx = [&](int ib) { return warp * 64 + ib * 32 + lane; };
+  auto flush_iside = [&]() {
+#pragma unroll
+    for (int ib = 0; ib < 2; ++ib) {
+      double* dst = a.iside + ((size_t)(I - a.row0) * a.nseg + (cur % a.nseg)) * (5 * S) * kSymTile + pidx(ib);
+#pragma unroll
+      for (int b = 0; b < S; ++b)
+#pragma unroll
+        for (int q = 0; q < 5; ++q) dst[(size_t)(b * 5 + q) * kSymTile] = acc[ib][b][q];
+    }
+  };
+  for (uint32_t k = 0;; ++k) {
+    if (tid == 0) issue_next();
+    const uint32_t s = k % kSymStages;
+    mbar_wait(&full[s], (k / kSymStages) & 1);
+    const int item = stage_item[s], d = stage_d[s];
+    if (item < 0) break;
+    if (item != cur) {
+      if (cur >= 0) flush_iside();
+      cur = item;
+      I = a.row0 + item / a.nseg;
+#pragma unroll
+      for (int ib = 0; ib < 2; ++ib) {
+        load_point<S>(a.rec + ((size_t)I * kSymTile + pidx(ib)) * RS, o[ib], gi[ib]);
+#pragma unroll
+        for (int b = 0; b < S; ++b)
+#pragma unroll
+          for (int q = 0; q < 5; ++q) acc[ib][b][q] = 0.0;
+      }
+    }
+    const double* tile = lb_smem + s * (kSymTile * RS);
+    const bool diag = (d == 0);
+#pragma unroll 1
+    for (int jb = 0; jb < kSymTile / 32; ++jb) {
+      // JU partners per step (j = (lane + st + u L) mod 32, L = 32 / JU) for
+      // both outer points: 2 JU pairs in lockstep, JU j-side accumulators
+      constexpr int JU = LB_IB_PAIRS, L = 32 / JU, P2 = 2 * JU;
+      double ju[JU][S][5];
+#pragma unroll
+      for (int u = 0; u < JU; ++u)
+#pragma unroll
+        for (int b = 0; b < S; ++b)
+#pragma unroll
+          for (int q = 0; q < 5; ++q) ju[u][b][q] = 0.0;
+      double2 rzn[JU];
+#pragma unroll
+      for (int u = 0; u < JU; ++u)
+        rzn[u] = *reinterpret_cast<const double2*>(tile + (jb * 32 + ((lane + u * L) & 31)) * RS);
+#pragma unroll 1
+      for (int st = 0; st < L; ++st) {
+        const double* rp[JU];
+        Outer oo[P2];
+        double rn[P2], zn[P2], rn2[P2], rcpr[P2];
+#pragma unroll
+        for (int u = 0; u < JU; ++u) {
+          const int jl = (lane + st + u * L) & 31;
+          rp[u] = tile + (jb * 32 + jl) * RS;
+          const double2 rz = rzn[u];
+          rzn[u] = *reinterpret_cast<const double2*>(tile + (jb * 32 + ((jl + 1) & 31)) * RS);
+          const double2 aux = *reinterpret_cast<const double2*>(rp[u] + 2);
+#pragma unroll
+          for (int ib = 0; ib < 2; ++ib) {
+            oo[2 * u + ib] = o[ib];
+            rn[2 * u + ib] = rz.x;
+            zn[2 * u + ib] = rz.y;
+            rn2[2 * u + ib] = aux.x;
+            rcpr[2 * u + ib] = aux.y;
+          }
+        }
+        T5 t[P2];
+        double txx2[P2];
+        pair_tensor_sym_x<P2>(oo, rn, zn, rn2, rcpr, a.gthr, logt, t, txx2);
+#pragma unroll
+        for (int u = 0; u < JU; ++u)
+#pragma unroll
+          for (int b = 0; b < S; ++b) {
+            const double gr = rp[u][4 + 3 * b], gz = rp[u][5 + 3 * b], fw = rp[u][6 + 3 * b];
+#pragma unroll
+            for (int ib = 0; ib < 2; ++ib) {
+              const T5& tt = t[2 * u + ib];
+              acc[ib][b][0] = fma(tt.xz, gz, fma(tt.kr, gr, acc[ib][b][0]));
+              acc[ib][b][1] = fma(tt.zz, gz, fma(tt.zr, gr, acc[ib][b][1]));
+              acc[ib][b][2] = fma(fw, tt.xx, acc[ib][b][2]);
+              acc[ib][b][3] = fma(fw, tt.xz, acc[ib][b][3]);
+              acc[ib][b][4] = fma(fw, tt.zz, acc[ib][b][4]);
+            }
+          }
+        if (!diag) {
+#pragma unroll
+          for (int u = 0; u < JU; ++u)
+#pragma unroll
+            for (int b = 0; b < S; ++b)
+#pragma unroll
+              for (int ib = 0; ib < 2; ++ib) {
+                const T5& tt = t[2 * u + ib];
+                ju[u][b][0] = fma(tt.zr, gi[ib][b][1], fma(tt.kr, gi[ib][b][0], ju[u][b][0]));
+                ju[u][b][1] = fma(tt.zz, gi[ib][b][1], fma(tt.xz, gi[ib][b][0], ju[u][b][1]));
+                ju[u][b][2] = fma(gi[ib][b][2], txx2[2 * u + ib], ju[u][b][2]);
+                ju[u][b][3] = fma(gi[ib][b][2], tt.zr, ju[u][b][3]);
+                ju[u][b][4] = fma(gi[ib][b][2], tt.zz, ju[u][b][4]);
+              }
+#pragma unroll
+          for (int u = 0; u < JU; ++u)
+#pragma unroll
+            for (int b = 0; b < S; ++b)
+#pragma unroll
+              for (int q = 0; q < 5; ++q) ju[u][b][q] = __shfl_sync(0xffffffffu, ju[u][b][q], (lane + 1) & 31);
+        }
+      }
+      // lane l holds accumulator u of j = l + (u+1)L: gather j = l in u order
+      double jacc[S][5];
+#pragma unroll
+      for (int b = 0; b < S; ++b)
+#pragma unroll
+        for (int q = 0; q < 5; ++q) {
+          double x = 0.0;
+#pragma unroll
+          for (int u = 0; u < JU; ++u) {
+            const double v = (u + 1) * L == 32 ? ju[u][b][q]
+                                               : __shfl_sync(0xffffffffu, ju[u][b][q], (lane - (u + 1) * L) & 31);
+            x = u == 0 ? v : __dadd_rn(x, v);
+          }
+          jacc[b][q] = x;
+        }
+      if (!diag) {
+        double* slot = jred + (size_t)(jb & 1) * NW * 32 * (5 * S);
+        double* dst = slot + ((size_t)warp * 32 + lane) * (5 * S);
+#pragma unroll
+        for (int b = 0; b < S; ++b)
+#pragma unroll
+          for (int q = 0; q < 5; ++q) dst[b * 5 + q] = jacc[b][q];
+        __syncthreads();
+        double* out = a.jside + ((size_t)(I - a.row0) * a.hmax + (d - 1)) * (5 * S) * kSymTile + jb * 32;
+        for (int v = tid; v < 32 * 5 * S; v += kIbThreads) {
+          const int c = v >> 5, jj = v & 31;
+          double x = slot[(size_t)jj * (5 * S) + c];
+#pragma unroll
+          for (int w = 1; w < NW; ++w) x = __dadd_rn(x, slot[((size_t)w * 32 + jj) * (5 * S) + c]);
+          out[(size_t)c * kSymTile + jj] = x;
+        }
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);
   }
   if (cur >= 0) flush_iside();
 }
