@@ -68,7 +68,7 @@ struct lb_ctx {
   // grow-only scratch
   lb::DevBuf in, rec, partial, out, elem, outer, aux, order;
   // symmetric all-points sweep state (lb_sym_*): sorted records, order, partials
-  lb::DevBuf symord, symrec, syminv, symi, symj, symtot, symctr;
+  lb::DevBuf symord, symrec, syminv, symi, symj, symtot, symctr, sweepctr;
   int sym_n = -1, sym_S = 0, sym_Se = 0, sym_nt = 0;
   // CUDA graph of the state-level operator's device work (lb_assemble_state):
   // captured on the second call with an unchanged key, replayed after
@@ -261,7 +261,10 @@ int launch_sweep(lb_ctx* ctx, int nout, const double* ro, const double* zo, int 
     const int nout_pad = ((nb + kTI - 1) / kTI) * kTI;
     int rc = ensure(ctx->partial, size_t(nchunk) * 5 * S * nout_pad * sizeof(double));
     if (rc) return rc;
+    if ((rc = ensure(ctx->sweepctr, sizeof(int)))) return rc;
+    LB_CUDA(cudaMemsetAsync(ctx->sweepctr.p, 0, sizeof(int), st));
     SweepArgs a;
+    a.next_item = static_cast<int*>(ctx->sweepctr.p);
     a.ro = ro + o0;
     a.zo = zo + o0;
     a.rec = rec;
@@ -538,7 +541,7 @@ int lb_ctx_destroy(lb_ctx* ctx) {
   cudaSetDevice(ctx->device);
   for (DevBuf* b : {&ctx->in, &ctx->rec, &ctx->partial, &ctx->out, &ctx->elem, &ctx->outer, &ctx->aux,
                     &ctx->order, &ctx->symord, &ctx->symrec, &ctx->syminv, &ctx->symi, &ctx->symj,
-                    &ctx->symtot, &ctx->symctr})
+                    &ctx->symtot, &ctx->symctr, &ctx->sweepctr})
     if (b->p) cudaFree(b->p);
   for (auto& ev : ctx->ev)
     if (ev) cudaEventDestroy(ev);

@@ -52,6 +52,7 @@ struct SweepArgs {
   const double* zo;   // outer z (nout)
   const double* rec;  // packed inner records (n x RS)
   double* partial;    // [nchunk][5S][nout_pad]
+  int* next_item;     // work counter (zero at launch): items past the first wave
   int nout, nout_pad, n, jc, nchunk;
   long long gthr;     // mask threshold on bits(d^2)
 };
@@ -86,7 +87,7 @@ __global__ void __launch_bounds__(kTI, kMinBlocks) lb_sweep_kernel(const SweepAr
   const int tid = threadIdx.x;
   const int lane = tid & 31;
   const int nib = a.nout_pad / kTI;
-  const long long nitems = (long long)nib * a.nchunk;
+  const int nitems = nib * a.nchunk;
 
   for (int t = tid; t < (2 << LB_LOGT_BITS); t += kTI) lb_smem[kStages * TJ * RS + t] = c_logt[t];
   if (tid == 0) {
@@ -99,25 +100,39 @@ __global__ void __launch_bounds__(kTI, kMinBlocks) lb_sweep_kernel(const SweepAr
   }
   __syncthreads();
 
-  // producer cursor (thread 0 only): next (item, tile) to load, flat tile index
-  long long p_item = blockIdx.x;
-  int p_tile = 0;
+  // Producer (thread 0): walks the tiles of its items; items after the first
+  // wave are claimed from a device counter (CTAs the schedulers favour take
+  // more, every SM keeps its CTAs to the end; each item writes its own
+  // partial slot, so results do not depend on the assignment).  Each stage
+  // carries (item, first inner point, count); item -1 ends the sweep.
+  __shared__ int stage_item[kStages], stage_j0[kStages], stage_cnt[kStages];
+  int p_item = blockIdx.x, p_tile = 0;
   uint32_t p_k = 0;
+  bool p_done = false;
   auto issue_next = [&]() {
-    if (p_item >= nitems) return;
+    if (p_done) return;
     const uint32_t s = p_k % kStages;
     if (p_k >= kStages) mbar_wait(&empty[s], ((p_k / kStages) - 1) & 1);
-    const int c = (int)(p_item / nib);
+    ++p_k;
+    if (p_item >= nitems) {
+      stage_item[s] = -1;
+      mbar_arrive(&full[s]);
+      p_done = true;
+      return;
+    }
+    const int c = p_item / nib;
     const int j0 = c * a.jc + p_tile * TJ;
     const int jend = min(a.n, (c + 1) * a.jc);
     const int cnt = min(TJ, jend - j0);
+    stage_item[s] = p_item;
+    stage_j0[s] = j0;
+    stage_cnt[s] = cnt;
     const uint32_t bytes = (uint32_t)cnt * RS * sizeof(double);
     mbar_expect_tx(&full[s], bytes);
     bulk_g2s(lb_smem + s * (TJ * RS), a.rec + (size_t)j0 * RS, bytes, &full[s]);
-    ++p_k;
     if (j0 + TJ >= jend) {
       p_tile = 0;
-      p_item += gridDim.x;
+      p_item = (int)gridDim.x + atomicAdd(a.next_item, 1);
     } else {
       ++p_tile;
     }
@@ -125,55 +140,83 @@ __global__ void __launch_bounds__(kTI, kMinBlocks) lb_sweep_kernel(const SweepAr
   if (tid == 0)
     for (int q = 0; q < kLookahead; ++q) issue_next();
 
-  uint32_t k = 0;  // consumer flat tile index (same sequence as the producer)
-  for (long long item = blockIdx.x; item < nitems; item += gridDim.x) {
-    const int ib = (int)(item % nib);
-    const int c = (int)(item / nib);
-    const int i = ib * kTI + tid;
-    const int il = min(i, a.nout - 1);
-    const Outer o = make_outer(a.ro[il], a.zo[il]);
-    double acc[S][5];
-#pragma unroll
-    for (int b = 0; b < S; ++b)
-#pragma unroll
-      for (int q = 0; q < 5; ++q) acc[b][q] = 0.0;
-
-    const int jbeg = c * a.jc;
-    const int jend = min(a.n, jbeg + a.jc);
-    for (int j0 = jbeg; j0 < jend; j0 += TJ, ++k) {
-      if (tid == 0) issue_next();
-      const uint32_t s = k % kStages;
-      mbar_wait(&full[s], (k / kStages) & 1);
-      const double* tile = lb_smem + s * (TJ * RS);
-      const int cnt = min(TJ, jend - j0);
-#pragma unroll kUnroll
-      for (int jj = 0; jj < cnt; ++jj) {
-        const double* rp = tile + jj * RS;
-        const double2 rz = *reinterpret_cast<const double2*>(rp);
-        const double2 aux = *reinterpret_cast<const double2*>(rp + 2);
-        const T5 t = pair_tensor(o, rz.x, rz.y, aux.x, aux.y, a.gthr, logt);
-#pragma unroll
-        for (int b = 0; b < S; ++b) {
-          const double gr = rp[4 + 3 * b], gz = rp[5 + 3 * b], fw = rp[6 + 3 * b];
-          // _accumulate_block (kernel.py:411-415)
-          acc[b][0] = fma(t.xz, gz, fma(t.kr, gr, acc[b][0]));
-          acc[b][1] = fma(t.zz, gz, fma(t.zr, gr, acc[b][1]));
-          acc[b][2] = fma(fw, t.xx, acc[b][2]);
-          acc[b][3] = fma(fw, t.xz, acc[b][3]);
-          acc[b][4] = fma(fw, t.zz, acc[b][4]);
-        }
-      }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[s]);  // this warp is done with stage s
-    }
+  // partners per step: two for few accumulator sets (shared coefficient
+  // loads, two overlapping chains), one where registers are short
+  constexpr int GU = S <= 2 ? 2 : 1;
+  Outer o;
+  double acc[S][5];
+  int cur = -1;
+  auto flush = [&]() {
+    const int i = (cur % nib) * kTI + tid;
     if (i < a.nout) {
-      double* dst = a.partial + (size_t)c * (5 * S) * a.nout_pad + i;
+      double* dst = a.partial + (size_t)(cur / nib) * (5 * S) * a.nout_pad + i;
 #pragma unroll
       for (int b = 0; b < S; ++b)
 #pragma unroll
         for (int q = 0; q < 5; ++q) dst[(size_t)(b * 5 + q) * a.nout_pad] = acc[b][q];
     }
+  };
+  auto accumulate = [&](const T5& t, const double* rp) {
+#pragma unroll
+    for (int b = 0; b < S; ++b) {
+      const double gr = rp[4 + 3 * b], gz = rp[5 + 3 * b], fw = rp[6 + 3 * b];
+      // _accumulate_block (kernel.py:411-415)
+      acc[b][0] = fma(t.xz, gz, fma(t.kr, gr, acc[b][0]));
+      acc[b][1] = fma(t.zz, gz, fma(t.zr, gr, acc[b][1]));
+      acc[b][2] = fma(fw, t.xx, acc[b][2]);
+      acc[b][3] = fma(fw, t.xz, acc[b][3]);
+      acc[b][4] = fma(fw, t.zz, acc[b][4]);
+    }
+  };
+  for (uint32_t k = 0;; ++k) {
+    if (tid == 0) issue_next();
+    const uint32_t s = k % kStages;
+    mbar_wait(&full[s], (k / kStages) & 1);
+    const int item = stage_item[s];
+    if (item < 0) break;
+    if (item != cur) {
+      if (cur >= 0) flush();
+      cur = item;
+      const int il = min((item % nib) * kTI + tid, a.nout - 1);
+      o = make_outer(a.ro[il], a.zo[il]);
+#pragma unroll
+      for (int b = 0; b < S; ++b)
+#pragma unroll
+        for (int q = 0; q < 5; ++q) acc[b][q] = 0.0;
+    }
+    const double* tile = lb_smem + s * (TJ * RS);
+    const int cnt = stage_cnt[s];
+    int jj = 0;
+    if constexpr (GU == 2) {
+      const Outer oo[2] = {o, o};
+#pragma unroll 1
+      for (; jj + 1 < cnt; jj += 2) {
+        const double* rp0 = tile + jj * RS;
+        const double* rp1 = rp0 + RS;
+        const double2 rz0 = *reinterpret_cast<const double2*>(rp0);
+        const double2 rz1 = *reinterpret_cast<const double2*>(rp1);
+        const double2 ax0 = *reinterpret_cast<const double2*>(rp0 + 2);
+        const double2 ax1 = *reinterpret_cast<const double2*>(rp1 + 2);
+        const double rn[2] = {rz0.x, rz1.x}, zn[2] = {rz0.y, rz1.y};
+        const double rn2[2] = {ax0.x, ax1.x}, rcpr[2] = {ax0.y, ax1.y};
+        T5 t[2];
+        double txx2[2];  // (unused: the general path has no swapped pair)
+        pair_tensor_sym_x<2>(oo, rn, zn, rn2, rcpr, a.gthr, logt, t, txx2);
+        accumulate(t[0], rp0);
+        accumulate(t[1], rp1);
+      }
+    }
+#pragma unroll 1
+    for (; jj < cnt; ++jj) {
+      const double* rp = tile + jj * RS;
+      const double2 rz = *reinterpret_cast<const double2*>(rp);
+      const double2 aux = *reinterpret_cast<const double2*>(rp + 2);
+      accumulate(pair_tensor(o, rz.x, rz.y, aux.x, aux.y, a.gthr, logt), rp);
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);  // this warp is done with stage s
   }
+  if (cur >= 0) flush();
 }
 
 // ------------------------------------------------------------------ K1b combine
