@@ -648,12 +648,16 @@ __global__ void lb_symreduce_kernel(const double* __restrict__ iside, const doub
       for (int c = 0; c < 5 * S; ++c) v[c] = __dadd_rn(v[c], src[(size_t)c * kSymTile]);
     }
   }
+  // d = (P - I) mod nt, stepped down with I (no integer division per row)
+  int d = (P - row0) % nt;
+  if (d < 0) d += nt;
   for (int I = row0; I < row1; ++I) {
-    const int d = (P - I + nt) % nt;
-    if (d < 1 || d > sym_h(I, nt)) continue;
-    const double* src = jside + ((size_t)(I - row0) * hmax + (d - 1)) * (5 * S) * kSymTile + t;
+    if (d >= 1 && d <= sym_h(I, nt)) {
+      const double* src = jside + ((size_t)(I - row0) * hmax + (d - 1)) * (5 * S) * kSymTile + t;
 #pragma unroll
-    for (int c = 0; c < 5 * S; ++c) v[c] = __dadd_rn(v[c], src[(size_t)c * kSymTile]);
+      for (int c = 0; c < 5 * S; ++c) v[c] = __dadd_rn(v[c], src[(size_t)c * kSymTile]);
+    }
+    d = d == 0 ? nt - 1 : d - 1;
   }
 #pragma unroll
   for (int c = 0; c < 5 * S; ++c) tot[(size_t)c * npad + p] = v[c];
