@@ -648,16 +648,35 @@ __global__ void lb_symreduce_kernel(const double* __restrict__ iside, const doub
       for (int c = 0; c < 5 * S; ++c) v[c] = __dadd_rn(v[c], src[(size_t)c * kSymTile]);
     }
   }
-  // d = (P - I) mod nt, stepped down with I (no integer division per row)
+  // d = (P - I) mod nt, stepped down with I (no integer division per row);
+  // rows in groups of G: the group's loads are issued before its adds, which
+  // stay in increasing-I order (the condition is uniform across the block)
   int d = (P - row0) % nt;
   if (d < 0) d += nt;
-  for (int I = row0; I < row1; ++I) {
-    if (d >= 1 && d <= sym_h(I, nt)) {
-      const double* src = jside + ((size_t)(I - row0) * hmax + (d - 1)) * (5 * S) * kSymTile + t;
+#ifndef LB_RED_G
+#define LB_RED_G 8
+#endif
+  constexpr int G = LB_RED_G;
+  for (int I0 = row0; I0 < row1; I0 += G) {
+    double x[G][5 * S];
+    bool on[G];
 #pragma unroll
-      for (int c = 0; c < 5 * S; ++c) v[c] = __dadd_rn(v[c], src[(size_t)c * kSymTile]);
+    for (int g = 0; g < G; ++g) {
+      const int I = I0 + g;
+      on[g] = I < row1 && d >= 1 && d <= sym_h(I, nt);
+      if (on[g]) {
+        const double* src = jside + ((size_t)(I - row0) * hmax + (d - 1)) * (5 * S) * kSymTile + t;
+#pragma unroll
+        for (int c = 0; c < 5 * S; ++c) x[g][c] = src[(size_t)c * kSymTile];
+      }
+      d = d == 0 ? nt - 1 : d - 1;
     }
-    d = d == 0 ? nt - 1 : d - 1;
+#pragma unroll
+    for (int g = 0; g < G; ++g)
+      if (on[g]) {
+#pragma unroll
+        for (int c = 0; c < 5 * S; ++c) v[c] = __dadd_rn(v[c], x[g][c]);
+      }
   }
 #pragma unroll
   for (int c = 0; c < 5 * S; ++c) tot[(size_t)c * npad + p] = v[c];
