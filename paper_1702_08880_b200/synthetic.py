@@ -114,3 +114,69 @@ def shard_bounds(n: int, world: int, rank: int, align: int = 9):
     lo_u = (units * rank) // world
     hi_u = (units * (rank + 1)) // world
     return min(lo_u * align, n), min(hi_u * align, n)
+
+
+# ---------------------------------------------------------------- config 4 mesh
+# BASELINE config 4's shared uniform Q2 mesh and Maxwellian state, built
+# without the reference (its cartesian_mesh node numbering is not needed for
+# timing or for device-vs-host solver comparisons).
+CFG4_SPECIES = ((1.0, -1.0, 1.0, 1.0), (3670.0, 1.0, 0.8, 1.0), (21900.0, 6.0, 0.02, 0.5),
+                (335000.0, 10.0, 0.001, 0.5))  # (mass, charge, density, temperature)
+
+
+def uniform_q2_mesh(L: float, nr: int, nz: int):
+    """(mesh, nodes): Q2 nodes on a (2nr+1) x (2nz+1) lattice over [0,L] x
+    [-L,L], z-major cells, no hanging nodes (identity prolongation)."""
+    import scipy.sparse as sp
+    from types import SimpleNamespace
+
+    dr, dz = L / nr, 2 * L / nz
+    NR = 2 * nr + 1
+    cells, origins = [], []
+    for j in range(nz):
+        for i in range(nr):
+            base = (2 * j) * NR + 2 * i
+            cells.append([base + a * NR + b for a in range(3) for b in range(3)])
+            origins.append((i * dr, -L + j * dz))
+    nn = NR * (2 * nz + 1)
+    ii, jj = np.meshgrid(np.arange(NR), np.arange(2 * nz + 1))
+    nodes = np.stack([ii.ravel() * dr / 2, -L + jj.ravel() * dz / 2], 1)
+    mesh = SimpleNamespace(n_cells=len(cells), sizes=np.tile([dr, dz], (len(cells), 1)),
+                           cell_nodes=np.array(cells, dtype=np.int64), origins=np.array(origins),
+                           n_nodes=nn, prolongation=sp.identity(nn, format="csr"),
+                           domain=SimpleNamespace(L=L))
+    return mesh, nodes
+
+
+def q2_reference():
+    """3x3 Gauss Q2 reference element (fem.py:33-81 layout: B (9 basis x 9
+    points), dB (.., .., 2), qpts, qwts)."""
+    from types import SimpleNamespace
+
+    g = math.sqrt(3.0 / 5.0) * np.array([-1.0, 0.0, 1.0])
+    w1 = np.array([5.0, 8.0, 5.0]) / 9.0
+    lag = np.stack([0.5 * g * (g - 1), 1 - g * g, 0.5 * g * (g + 1)])
+    dlag = np.stack([g - 0.5, -2 * g, g + 0.5])
+    B = np.empty((9, 9))
+    dB = np.empty((9, 9, 2))
+    for kz in range(3):
+        for kr in range(3):
+            i = 3 * kz + kr
+            B[i] = np.outer(lag[kz], lag[kr]).ravel()
+            dB[i, :, 0] = np.outer(lag[kz], dlag[kr]).ravel()
+            dB[i, :, 1] = np.outer(dlag[kz], lag[kr]).ravel()
+    qr, qz = np.meshgrid(g, g, indexing="xy")
+    return SimpleNamespace(Nq=9, B=B, dB=dB, qpts=np.stack([qr.ravel(), qz.ravel()], 1),
+                           qwts=(w1[None, :] * w1[:, None]).ravel())
+
+
+def cfg4_state(nodes: np.ndarray, species=CFG4_SPECIES, seed: int = 4):
+    """Config 4 Maxwellians at the mesh nodes, perturbed x(1 + 0.01 N(0,1)),
+    and the species' (nu_hat, mass_ratio_o) tables (e^2 e^2 coupling)."""
+    r, z = nodes[:, 0], nodes[:, 1]
+    rng = np.random.default_rng(seed)
+    coeffs = np.stack([n * (math.pi * 2 * T / m) ** -1.5 * np.exp(-(r * r + z * z) / (2 * T / m))
+                       * (1 + 0.01 * rng.standard_normal(r.shape)) for m, q, n, T in species])
+    e = np.array([q for _, q, _, _ in species])
+    nu = np.outer(e**2, e**2)
+    return coeffs, nu / nu[0, 0], np.array([1.0 / m for m, _, _, _ in species])

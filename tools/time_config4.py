@@ -4,73 +4,26 @@ mesh (N = 73,728 points), state-level operator (device sampling + symmetric
 species-collapsed sweep + element contraction + CSR scatter) and the bare
 all-points sweep.  The uniform Q2 mesh arrays are generated here (the
 reference's cartesian_mesh node numbering is not needed for timing)."""
-import math
 import sys
 import time
 from pathlib import Path
-from types import SimpleNamespace
 
 sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 
 import numpy as np  # noqa: E402
-import scipy.sparse as sp  # noqa: E402
 
 import paper_1702_08880_b200 as pkg  # noqa: E402
 
 
-def uniform_q2_mesh(L, nr, nz):
-    """Q2 nodes on a (2nr+1) x (2nz+1) lattice over [0,L] x [-L,L]."""
-    dr, dz = L / nr, 2 * L / nz
-    NR = 2 * nr + 1
-    cells, origins = [], []
-    for j in range(nz):          # z-major cell order
-        for i in range(nr):
-            base = (2 * j) * NR + 2 * i
-            cells.append([base + a * NR + b for a in range(3) for b in range(3)])
-            origins.append((i * dr, -L + j * dz))
-    cn = np.array(cells, dtype=np.int64)
-    nn = NR * (2 * nz + 1)
-    ii, jj = np.meshgrid(np.arange(NR), np.arange(2 * nz + 1))
-    nodes = np.stack([ii.ravel() * dr / 2, -L + jj.ravel() * dz / 2], 1)
-    P = sp.identity(nn, format="csr")
-    mesh = SimpleNamespace(n_cells=len(cells), sizes=np.tile([dr, dz], (len(cells), 1)),
-                           cell_nodes=cn, origins=np.array(origins), n_nodes=nn,
-                           prolongation=P, domain=SimpleNamespace(L=L))
-    return mesh, nodes
-
-
-def q2_reference():
-    g = math.sqrt(3.0 / 5.0) * np.array([-1.0, 0.0, 1.0])
-    w1 = np.array([5.0, 8.0, 5.0]) / 9.0
-    lag = np.stack([0.5 * g * (g - 1), 1 - g * g, 0.5 * g * (g + 1)])
-    dlag = np.stack([g - 0.5, -2 * g, g + 0.5])
-    B = np.empty((9, 9))
-    dB = np.empty((9, 9, 2))
-    for kz in range(3):
-        for kr in range(3):
-            i = 3 * kz + kr
-            B[i] = np.outer(lag[kz], lag[kr]).ravel()
-            dB[i, :, 0] = np.outer(lag[kz], dlag[kr]).ravel()
-            dB[i, :, 1] = np.outer(dlag[kz], lag[kr]).ravel()
-    qr, qz = np.meshgrid(g, g, indexing="xy")
-    return SimpleNamespace(Nq=9, B=B, dB=dB, qpts=np.stack([qr.ravel(), qz.ravel()], 1),
-                           qwts=(w1[None, :] * w1[:, None]).ravel())
+from paper_1702_08880_b200.synthetic import cfg4_state, q2_reference, uniform_q2_mesh  # noqa: E402
 
 
 def main():
     nr, nz = (int(a) for a in (sys.argv[1:3] if len(sys.argv) > 2 else (64, 128)))
     mesh, nodes = uniform_q2_mesh(5.0, nr, nz)
     ref = q2_reference()
-    spec = [(1.0, -1.0, 1.0, 1.0), (3670.0, 1.0, 0.8, 1.0), (21900.0, 6.0, 0.02, 0.5),
-            (335000.0, 10.0, 0.001, 0.5)]
-    r, z = nodes[:, 0], nodes[:, 1]
-    rng = np.random.default_rng(4)
-    coeffs = np.stack([dens * (math.pi * 2 * T / m) ** -1.5 * np.exp(-(r * r + z * z) / (2 * T / m))
-                       * (1 + 0.01 * rng.standard_normal(r.shape)) for m, q, dens, T in spec])
-    e = np.array([q for _, q, _, _ in spec])
-    nu = np.outer(e**2, e**2)
-    params = pkg.CollisionParams(nu_hat=nu / nu[0, 0],
-                                 mass_ratio_o=np.array([1.0 / m for m, _, _, _ in spec]))
+    coeffs, nu_hat, mro = cfg4_state(nodes)
+    params = pkg.CollisionParams(nu_hat=nu_hat, mass_ratio_o=mro)
     N = 9 * mesh.n_cells
     cm = pkg.assemble_at(mesh, ref, coeffs, params)  # warm: mesh upload, gather map
     ts = []

@@ -6,7 +6,6 @@ config 4 shared 64x128 Q2 mesh with four species.
 
     python tools/time_solver.py [cfg1 cfg3 cfg4]
 """
-import math
 import sys
 import time
 from pathlib import Path
@@ -33,20 +32,12 @@ def fixture_case(name):
 
 
 def config4_case():
-    from time_config4 import q2_reference, uniform_q2_mesh
+    from paper_1702_08880_b200.synthetic import cfg4_state, q2_reference, uniform_q2_mesh
 
     mesh, nodes = uniform_q2_mesh(5.0, 64, 128)
     ref = q2_reference()
-    spec = [(1.0, -1.0, 1.0, 1.0), (3670.0, 1.0, 0.8, 1.0), (21900.0, 6.0, 0.02, 0.5),
-            (335000.0, 10.0, 0.001, 0.5)]
-    r, z = nodes[:, 0], nodes[:, 1]
-    rng = np.random.default_rng(4)
-    coeffs = np.stack([dens * (math.pi * 2 * T / m) ** -1.5 * np.exp(-(r * r + z * z) / (2 * T / m))
-                       * (1 + 0.01 * rng.standard_normal(r.shape)) for m, q, dens, T in spec])
-    e = np.array([q for _, q, _, _ in spec])
-    nu = np.outer(e**2, e**2)
-    params = pkg.CollisionParams(nu_hat=nu / nu[0, 0],
-                                 mass_ratio_o=np.array([1.0 / m for m, _, _, _ in spec]))
+    coeffs, nu_hat, mro = cfg4_state(nodes)
+    params = pkg.CollisionParams(nu_hat=nu_hat, mass_ratio_o=mro)
     s = _mesh_solver(mesh, ref, 4)
     s.set_mass(None)  # device mass matrix (the uniform mesh has no reference fixture)
     M = sp.csr_matrix((s.mass_values(), s.indices, s.indptr), shape=(s.n, s.n))
