@@ -279,6 +279,33 @@ def test_all_points_coupling_layouts(gpu, oracle, S, rank1):
     assert np.array_equal(D[..., 0, 1], D[..., 1, 0])
 
 
+@pytest.mark.parametrize("n", [128, 129, 255, 256, 300, 383])
+@pytest.mark.parametrize("rank1", [True, False])
+def test_all_points_tile_boundaries(gpu, oracle, n, rank1):
+    """All-points (symmetric) sweep at tile-count edges: one tile (only the
+    diagonal tile pair), one tile + 1 point (padding), an even tile count
+    (the opposite tile is shared by half the rows), odd counts -- for the
+    collapsed (two points x two partners per thread) and the per-species
+    kernels, vs the oracle."""
+    import paper_1702_08880_b200 as pkg
+
+    S = 2
+    rng = np.random.default_rng(900 + n)
+    r = rng.uniform(0.0, 3.0, n)
+    z = rng.uniform(-3.0, 3.0, n)
+    w = rng.uniform(0.1, 1.0, n)
+    f, dfr, dfz = (rng.standard_normal((S, n)) for _ in range(3))
+    e = np.array([1.0, 2.0])
+    nu = np.outer(e**2, e**2) if rank1 else np.array([[1.0, 0.7], [0.7, 2.0]])
+    mro = np.array([1.0, 0.3])
+    data = pkg.QuadPointData(N=n, r=r, z=z, w=w, f=f, df_r=dfr, df_z=dfz)
+    params = pkg.CollisionParams(nu_hat=nu, mass_ratio_o=mro)
+    K, D = gpu.fused_sweep(r, z, data, params, eps_d=1e-13)
+    Kr, Dr = oracle.fused_sweep(r, z, r, z, w, f, dfr, dfz, nu, mro, eps_d=1e-13)
+    err = worst_component(K, D, Kr, Dr)
+    assert err < TOL, (n, rank1, err)
+
+
 def test_multibatch_runs_match(gpu, oracle):
     """Scratch-bounded batching (outer batches on the general path, row
     batches on the symmetric path) at N = 2^15, forced with a 1 MiB budget in
