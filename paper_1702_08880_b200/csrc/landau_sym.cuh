@@ -640,12 +640,28 @@ __global__ void lb_symreduce_kernel(const double* __restrict__ iside, const doub
   double v[5 * S];
 #pragma unroll
   for (int c = 0; c < 5 * S; ++c) v[c] = first ? 0.0 : tot[(size_t)c * npad + p];
+#ifndef LB_RED_G
+#define LB_RED_G 8
+#endif
+  constexpr int G = LB_RED_G;
   if (P >= row0 && P < row1) {
-    for (int sg = 0; sg < nseg; ++sg) {
-      const double* src = iside + ((size_t)(P - row0) * nseg + sg) * (5 * S) * kSymTile + t;
-      if (sg * sym_seglen(nt) > sym_h(P, nt)) break;
+    // own row's segments, in groups of G loads ahead of their ordered adds
+    const int nsg = min(nseg, sym_h(P, nt) / sym_seglen(nt) + 1);
+    for (int s0 = 0; s0 < nsg; s0 += G) {
+      double x[G][5 * S];
 #pragma unroll
-      for (int c = 0; c < 5 * S; ++c) v[c] = __dadd_rn(v[c], src[(size_t)c * kSymTile]);
+      for (int g = 0; g < G; ++g)
+        if (s0 + g < nsg) {
+          const double* src = iside + ((size_t)(P - row0) * nseg + s0 + g) * (5 * S) * kSymTile + t;
+#pragma unroll
+          for (int c = 0; c < 5 * S; ++c) x[g][c] = src[(size_t)c * kSymTile];
+        }
+#pragma unroll
+      for (int g = 0; g < G; ++g)
+        if (s0 + g < nsg) {
+#pragma unroll
+          for (int c = 0; c < 5 * S; ++c) v[c] = __dadd_rn(v[c], x[g][c]);
+        }
     }
   }
   // d = (P - I) mod nt, stepped down with I (no integer division per row);
@@ -653,10 +669,6 @@ __global__ void lb_symreduce_kernel(const double* __restrict__ iside, const doub
   // stay in increasing-I order (the condition is uniform across the block)
   int d = (P - row0) % nt;
   if (d < 0) d += nt;
-#ifndef LB_RED_G
-#define LB_RED_G 8
-#endif
-  constexpr int G = LB_RED_G;
   for (int I0 = row0; I0 < row1; I0 += G) {
     double x[G][5 * S];
     bool on[G];
