@@ -242,6 +242,10 @@ int lb_sym_combine_dev(lb_ctx *ctx, int S, const double *tot, const double *coK,
                        const double *coD, int q0, int q1, double *K_out, double *D_out,
                        void *stream);
 
+/* elliptic_KE (kernel.py:93-113): K(m), E(m) for n parameters in [0, 1)
+ * (LB_EINVAL outside), with the device's table log and Horner chains. */
+int lb_elliptic_ke(lb_ctx *ctx, int n, const double *m, double *K, double *E);
+
 /* Number of kernels the most recent lb_sweep_dev / lb_elements_dev /
  * lb_pack_records_dev call launched (for the benchmark's launch count). */
 int lb_last_launch_count(lb_ctx *ctx);

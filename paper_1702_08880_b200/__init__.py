@@ -33,6 +33,7 @@ from .kernel import (
     axisym_tensor_pair,
     axisym_tensor_pairs,
     coupling,
+    elliptic_KE,
     flop_count,
     fused_inner_loop,
     fused_sweep,
@@ -103,7 +104,7 @@ def uninstall(axlandau_pkg, saved: dict) -> None:
 __all__ = [
     "Accumulators", "CollisionMatrix", "CollisionParams", "LandauTensorPair",
     "QuadPointData", "assemble_at", "assemble_collision", "assemble_species_meshes", "sample_state", "axisym_tensor_pair", "axisym_tensor_pairs",
-    "coupling", "default_eps_d", "element_matrices", "flop_count", "fused_inner_loop",
+    "coupling", "default_eps_d", "element_matrices", "elliptic_KE", "flop_count", "fused_inner_loop",
     "fused_sweep", "install", "uninstall", "CNSolver", "StepFailure", "linear_cn_step",
     "newton_step",
 ]

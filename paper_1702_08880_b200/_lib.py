@@ -63,6 +63,7 @@ SIGNATURES = {
     "lb_elements_dev": (_i, [_vp, _i, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
     "lb_last_launch_count": (_i, [_vp]),
     "lb_fp64_peak": (_i, [_vp, _dp, _dp]),
+    "lb_elliptic_ke": (_i, [_vp, _i, _dp, _dp, _dp]),
     "lb_cn_create": (_i, [_vp, _vp, _i, _i, _ip, _ip, _ip, _i, C.POINTER(_vp)]),
     "lb_cn_destroy": (_i, [_vp]),
     "lb_cn_set_mass": (_i, [_vp, _dp]),

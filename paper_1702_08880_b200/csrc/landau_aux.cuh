@@ -239,6 +239,32 @@ __global__ void lb_pairs_kernel(int npair, const double* __restrict__ r, const d
   UK[4 * p + 3] = 4.0 * t.zz;
 }
 
+// elliptic_KE (kernel.py:93-113): K(m), E(m) from x = 1 - m with the same
+// table log and Horner chains as the pair kernels (pair_stage2)
+__global__ void lb_elliptic_kernel(int n, const double* __restrict__ m, double* __restrict__ K,
+                                   double* __restrict__ E) {
+  __shared__ double2 logt[1 << LB_LOGT_BITS];
+  for (int t = threadIdx.x; t < (1 << LB_LOGT_BITS); t += blockDim.x)
+    logt[t] = make_double2(c_logt[2 * t], c_logt[2 * t + 1]);
+  __syncthreads();
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= n) return;
+  const double x = 1.0 - m[p];
+  const double lx = log_table(x, logt);
+  double pk = fma(c_pk[10], x, c_pk[9]), qk = c_qk[9];
+  double pe = fma(c_pe[10], x, c_pe[9]), qe = c_qe[9];
+#pragma unroll
+  for (int k = 8; k >= 0; --k) {
+    pk = fma(pk, x, c_pk[k]);
+    qk = fma(qk, x, c_qk[k]);
+    pe = fma(pe, x, c_pe[k]);
+    if (k >= 1) qe = fma(qe, x, c_qe[k]);
+  }
+  qe = qe * x;
+  K[p] = fma(-lx, qk, pk);
+  E[p] = fma(-lx, qe, pe);
+}
+
 // ------------------------------------------------------------------ FP64 peak
 constexpr int kDfmaChains = 8;
 constexpr int kDfmaIters = 4096;

@@ -1243,6 +1243,27 @@ int lb_tensor_pairs(lb_ctx* ctx, int npair, const double* r, const double* z, co
   return LB_OK;
 }
 
+int lb_elliptic_ke(lb_ctx* ctx, int n, const double* m, double* K, double* E) {
+  int rc = use_ctx(ctx);
+  if (rc) return rc;
+  if (n < 0) return fail(LB_EINVAL, "negative count");
+  if (n == 0) return LB_OK;
+  if (!m || !K || !E) return fail(LB_EINVAL, "null argument");
+  for (int i = 0; i < n; ++i)
+    if (!(m[i] >= 0.0 && m[i] < 1.0)) return fail(LB_EINVAL, "elliptic parameter must satisfy 0 <= m < 1");
+  cudaStream_t st = ctx->stream;
+  if ((rc = ensure(ctx->aux, sizeof(double) * 3 * (size_t)n))) return rc;
+  double* d = static_cast<double*>(ctx->aux.p);
+  const size_t b = sizeof(double) * n;
+  LB_CUDA(cudaMemcpyAsync(d, m, b, cudaMemcpyHostToDevice, st));
+  lb_elliptic_kernel<<<(n + 127) / 128, 128, 0, st>>>(n, d, d + n, d + 2 * (size_t)n);
+  LB_CUDA(cudaGetLastError());
+  LB_CUDA(cudaMemcpyAsync(K, d + n, b, cudaMemcpyDeviceToHost, st));
+  LB_CUDA(cudaMemcpyAsync(E, d + 2 * (size_t)n, b, cudaMemcpyDeviceToHost, st));
+  LB_CUDA(cudaStreamSynchronize(st));
+  return LB_OK;
+}
+
 int lb_fp64_peak(lb_ctx* ctx, double* tflops, double* ms) {
   int rc = use_ctx(ctx);
   if (rc) return rc;

@@ -194,6 +194,26 @@ def fused_inner_loop(outer, data, params, eps_d: float = 0.0,
     return Accumulators(K=K[0], D=D[0])
 
 
+def elliptic_KE(m):
+    """Complete elliptic integrals (K(m), E(m)) for m in [0, 1)
+    (kernel.py:93-113) on the device: the reference's polynomial fits in
+    x = 1 - m with the device table log.  Scalars in, floats out; arrays in,
+    arrays out; ValueError outside [0, 1)."""
+    m_arr = np.asarray(m, dtype=np.float64)
+    if np.any(m_arr < 0.0) or np.any(m_arr >= 1.0) or np.any(np.isnan(m_arr)):
+        raise ValueError("elliptic parameter must satisfy 0 <= m < 1")
+    flat = np.ascontiguousarray(m_arr.ravel())
+    K = np.empty_like(flat)
+    E = np.empty_like(flat)
+    if flat.size:
+        ctx = _lib.context()
+        _lib.check(_lib.load().lb_elliptic_ke(ctx.handle, flat.size, _lib.dptr(flat), _lib.dptr(K),
+                                              _lib.dptr(E)))
+    if np.isscalar(m) or np.ndim(m) == 0:
+        return float(K[0]), float(E[0])
+    return K.reshape(m_arr.shape), E.reshape(m_arr.shape)
+
+
 def axisym_tensor_pairs(r, z, rbar, zbar):
     """Vectorized device evaluation of the azimuthally integrated tensors
     (UK, UD), each (npair, 2, 2), with the sweep's own device arithmetic.

@@ -39,6 +39,23 @@ def test_tensor_pairs_match_reference(gpu):
     assert np.all(err <= tol)
 
 
+def test_elliptic_KE_device(gpu):
+    """elliptic_KE (kernel.py:93-113, test_kernel.py:30-46): known values,
+    the reference's own outputs on the 1000-pair fixture to 1e-15 relative
+    (table log and fused Horner vs numpy), scalar/array forms."""
+    K, E = gpu.elliptic_KE(0.5)
+    assert isinstance(K, float)
+    assert abs(K - 1.854074677301369) <= 1e-14 * K and abs(E - 1.350643881047669) <= 1e-14 * E
+    K0, E0 = gpu.elliptic_KE(0.0)
+    # the fits reproduce pi/2 at m = 0 to their accuracy (rtol 1e-14, test_kernel.py:30-36)
+    assert abs(K0 - np.pi / 2) <= 1e-14 * np.pi / 2 and abs(E0 - np.pi / 2) <= 1e-14 * np.pi / 2
+    g = golden("pairs")
+    K, E = gpu.elliptic_KE(g["m"])
+    assert K.shape == g["m"].shape
+    assert np.max(np.abs(K - g["K"]) / np.abs(g["K"])) <= 1e-15
+    assert np.max(np.abs(E - g["E"]) / np.abs(g["E"])) <= 1e-15
+
+
 def test_tensor_pair_structure(gpu):
     g = golden("pairs")
     P = g["pairs"][:600]

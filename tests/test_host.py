@@ -214,3 +214,15 @@ def test_install_into_the_reference_package():
     finally:
         pkg.uninstall(ax, saved)
     assert ax.assembly.fused_sweep is not pkg.fused_sweep
+
+
+def test_elliptic_domain_errors_before_the_device():
+    """elliptic_KE rejects m outside [0, 1) with ValueError (kernel.py:101-102,
+    test_kernel.py:49-57) before any device work."""
+    import pytest
+
+    import paper_1702_08880_b200 as pkg
+
+    for bad in (-0.1, 1.0, 1.5, float("nan")):
+        with pytest.raises(ValueError):
+            pkg.elliptic_KE([bad])
