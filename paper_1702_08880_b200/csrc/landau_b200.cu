@@ -1347,6 +1347,9 @@ struct lb_cn {
   double* blk = nullptr;     // block pool: S * sstride
   long long zero_len = 0;    // level-0 part of the pool (zeroed per fill)
   std::vector<CnLevel> lv;   // levels 0 .. L (the last has N = 1)
+  cudaGraphExec_t factor_graph = nullptr, solve_graph = nullptr;  // captured on first use
+  bool graph_failed = false;
+  void* blas_ws = nullptr;   // cuBLAS workspace (set explicitly so calls can be captured)
   double *g = nullptr, *f = nullptr, *d = nullptr, *R = nullptr, *Mf = nullptr, *x = nullptr,
          *out = nullptr, *Co = nullptr, *Cg = nullptr, *red = nullptr;
   std::vector<void*> allocs;
@@ -1370,7 +1373,7 @@ static int cn_alloc(lb_cn* cn, void** p, size_t bytes) {
   return LB_OK;
 }
 
-static int cn_factor(lb_cn* cn, cudaStream_t st) {
+static int cn_factor_issue(lb_cn* cn, cudaStream_t st) {
   const int nb = cn->nb;
   const double one = 1.0, mone = -1.0, zero = 0.0;
   int hinfo = 0;
@@ -1395,24 +1398,60 @@ static int cn_factor(lb_cn* cn, cudaStream_t st) {
         LB_BLAS(cublasDgemmBatched(cn->blas, CUBLAS_OP_N, CUBLAS_OP_N, nb, nb, nb, &mone, b->A, nb, b->B, nb,
                                    &zero, b->C, nb, b->count));
   }
+  return LB_OK;
+}
+
+// Run a launch sequence through a CUDA graph captured on first use (the
+// solver's level structure and every pointer are fixed per lb_cn, so the
+// graph stays valid); eager if capture is not possible.
+template <class F>
+static int cn_graph_run(cudaGraphExec_t& exec, bool& failed, cudaStream_t st, F&& issue) {
+  static const bool no_graph = std::getenv("LB_NO_GRAPH") != nullptr;
+  if (!exec && !failed && !no_graph) {
+    cudaGraph_t g = nullptr;
+    if (cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal) == cudaSuccess) {
+      const int rc = issue();
+      const cudaError_t ce = cudaStreamEndCapture(st, &g);
+      if (rc != LB_OK || ce != cudaSuccess || cudaGraphInstantiate(&exec, g, 0) != cudaSuccess) {
+        exec = nullptr;
+        failed = true;
+      }
+      if (g) cudaGraphDestroy(g);
+    } else {
+      failed = true;
+    }
+    cudaGetLastError();
+  }
+  if (exec) {
+    LB_CUDA(cudaGraphLaunch(exec, st));
+    return LB_OK;
+  }
+  return issue();
+}
+
+static int cn_factor(lb_cn* cn, cudaStream_t st) {
+  int rc = cn_graph_run(cn->factor_graph, cn->graph_failed, st, [&] { return cn_factor_issue(cn, st); });
+  if (rc) return rc;
   // zero pivots anywhere -> singular (splu's RuntimeError, solver.py:127-129)
+  std::vector<std::vector<int>> info(cn->lv.size());
   for (size_t l = 0; l < cn->lv.size(); ++l) {
     const CnLevel& L = cn->lv[l];
-    if (!L.getrf.count) continue;
-    std::vector<int> info(L.getrf.count);
-    LB_CUDA(cudaMemcpyAsync(info.data(), L.info, sizeof(int) * info.size(), cudaMemcpyDeviceToHost, st));
-    LB_CUDA(cudaStreamSynchronize(st));
-    for (size_t k = 0; k < info.size(); ++k)
-      if (info[k] != 0)
-        return fail(LB_ESINGULAR, "singular diagonal block (level " + std::to_string(l) + ", species " +
-                                      std::to_string(k % cn->S) + ", zero pivot " + std::to_string(info[k]) + ")");
+    info[l].resize(L.getrf.count);
+    if (L.getrf.count)
+      LB_CUDA(cudaMemcpyAsync(info[l].data(), L.info, sizeof(int) * L.getrf.count, cudaMemcpyDeviceToHost, st));
   }
+  LB_CUDA(cudaStreamSynchronize(st));
+  for (size_t l = 0; l < info.size(); ++l)
+    for (size_t k = 0; k < info[l].size(); ++k)
+      if (info[l][k] != 0)
+        return fail(LB_ESINGULAR, "singular diagonal block (level " + std::to_string(l) + ", species " +
+                                      std::to_string(k % cn->S) + ", zero pivot " + std::to_string(info[l][k]) + ")");
   return LB_OK;
 }
 
 // x (S x npad, band order) holds the right-hand side on entry, the solution
 // on exit.
-static int cn_solve(lb_cn* cn, cudaStream_t st) {
+static int cn_solve_issue(lb_cn* cn, cudaStream_t st) {
   const int nb = cn->nb;
   const double one = 1.0, mone = -1.0;
   int hinfo = 0;
@@ -1436,6 +1475,10 @@ static int cn_solve(lb_cn* cn, cudaStream_t st) {
                                    b->count));
   }
   return LB_OK;
+}
+
+static int cn_solve(lb_cn* cn, cudaStream_t st) {
+  return cn_graph_run(cn->solve_graph, cn->graph_failed, st, [&] { return cn_solve_issue(cn, st); });
 }
 
 // level-0 blocks = M - h C (C null: M), padded diagonal = identity
@@ -1655,6 +1698,10 @@ int lb_cn_create(lb_ctx* ctx, const lb_mesh* m, int S, int n, const int* indptr,
   up(cn->off, off.data(), sizeof(long long) * nnz);
   if (e != cudaSuccess) return bail(fail(LB_ECUDA, std::string("lb_cn_create: ") + cudaGetErrorString(e)));
   if (cublasCreate(&cn->blas) != CUBLAS_STATUS_SUCCESS) return bail(fail(LB_ECUDA, "cublasCreate failed"));
+  const size_t ws = size_t(32) << 20;
+  if ((rc = cn_alloc(cn, &cn->blas_ws, ws))) return bail(rc);
+  if (cublasSetWorkspace(cn->blas, cn->blas_ws, ws) != CUBLAS_STATUS_SUCCESS)
+    return bail(fail(LB_ECUDA, "cublasSetWorkspace failed"));
   *out = cn;
   return LB_OK;
 }
@@ -1663,6 +1710,8 @@ int lb_cn_destroy(lb_cn* cn) {
   if (!cn) return LB_OK;
   cudaSetDevice(cn->ctx->device);
   cudaStreamSynchronize(cn->ctx->stream);
+  if (cn->factor_graph) cudaGraphExecDestroy(cn->factor_graph);
+  if (cn->solve_graph) cudaGraphExecDestroy(cn->solve_graph);
   if (cn->blas) cublasDestroy(cn->blas);
   for (void* p : cn->allocs) cudaFree(p);
   delete cn;
