@@ -1373,6 +1373,12 @@ static int cn_alloc(lb_cn* cn, void** p, size_t bytes) {
   return LB_OK;
 }
 
+// factor blocks small enough for the shared-memory vector solve (cuBLAS otherwise)
+static bool cn_small(const lb_cn* cn) {
+  static const bool force_blas = std::getenv("LB_CN_CUBLAS") != nullptr;
+  return cn->nb <= kSmallNb && !force_blas;
+}
+
 static int cn_factor_issue(lb_cn* cn, cudaStream_t st) {
   const int nb = cn->nb;
   const double one = 1.0, mone = -1.0, zero = 0.0;
@@ -1456,10 +1462,16 @@ static int cn_solve_issue(lb_cn* cn, cudaStream_t st) {
   const double one = 1.0, mone = -1.0;
   int hinfo = 0;
   LB_BLAS(cublasSetStream(cn->blas, st));
+  const bool small = cn_small(cn);
   for (const CnLevel& L : cn->lv) {
-    if (L.solveY.count)
+    if (small && L.solveY.count) {
+      lb_small_solve_kernel<<<L.solveY.count, kSmallThreads, small_solve_smem_bytes(nb), st>>>(nb, L.solveY.count, L.getrf.A,
+                                                                              L.piv, L.solveY.B);
+      LB_CUDA(cudaGetLastError());
+    } else if (L.solveY.count) {
       LB_BLAS(cublasDgetrsBatched(cn->blas, CUBLAS_OP_N, nb, 1, L.getrf.A, nb, L.piv, L.solveY.B, nb, &hinfo,
                                   L.solveY.count));
+    }
     const CnBatch* fw[2] = {&L.fwdL, &L.fwdU};
     for (const CnBatch* b : fw)
       if (b->count)
@@ -1698,6 +1710,10 @@ int lb_cn_create(lb_ctx* ctx, const lb_mesh* m, int S, int n, const int* indptr,
   up(cn->off, off.data(), sizeof(long long) * nnz);
   if (e != cudaSuccess) return bail(fail(LB_ECUDA, std::string("lb_cn_create: ") + cudaGetErrorString(e)));
   if (cublasCreate(&cn->blas) != CUBLAS_STATUS_SUCCESS) return bail(fail(LB_ECUDA, "cublasCreate failed"));
+  if (nb <= kSmallNb &&
+      cudaFuncSetAttribute(lb_small_solve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)small_solve_smem_bytes(kSmallNb)) != cudaSuccess)
+    return bail(fail(LB_ECUDA, "cudaFuncSetAttribute(lb_small_solve_kernel) failed"));
   const size_t ws = size_t(32) << 20;
   if ((rc = cn_alloc(cn, &cn->blas_ws, ws))) return bail(rc);
   if (cublasSetWorkspace(cn->blas, cn->blas_ws, ws) != CUBLAS_STATUS_SUCCESS)

@@ -147,3 +147,62 @@ __global__ void lb_perm_update_kernel(int n, int npad, int S, const int* __restr
 }
 
 }  // namespace lb
+
+namespace lb {
+
+// ---------------------------------------------------------------- small-block solve
+// Vector solves with small factor blocks (at most kSmallNb rows), where
+// cuBLAS's batched getrs (1 right-hand side) spends ~0.1 ms per call in
+// latency-bound kernels.  (A one-CTA shared-memory LU of the blocks was also
+// written and measured slower than cuBLAS getrf: 228 vs ~160 us per level at
+// 68 rows -- a latency-bound chain of 68 pivot steps on one SM.)
+constexpr int kSmallNb = 96;
+constexpr int kSmallThreads = 128;
+
+// x := D^-1 x for one vector per matrix with getrf's factors (LAPACK
+// layout, 1-based pivots): one CTA per vector, factors staged in shared memory,
+// right-looking substitution parallel over rows.
+__global__ void __launch_bounds__(kSmallThreads) lb_small_solve_kernel(int nb, int count,
+                                                                       double* const* __restrict__ D,
+                                                                       const int* __restrict__ piv_all,
+                                                                       double* const* __restrict__ V) {
+  extern __shared__ __align__(16) double sm[];
+  double* A = sm;                  // [nb][nb]
+  double* x = sm + (size_t)nb * nb;  // [nb]
+  const int w = blockIdx.x, tid = threadIdx.x;
+  if (w >= count) return;
+  const double* Ag = D[w];
+  const int* piv = piv_all + (size_t)w * nb;
+  double* xg = V[w];
+  for (int t = tid; t < nb * nb; t += kSmallThreads) A[t] = Ag[t];
+  for (int t = tid; t < nb; t += kSmallThreads) x[t] = xg[t];
+  __syncthreads();
+  if (tid == 0)
+    for (int k = 0; k < nb; ++k) {
+      const int p = piv[k] - 1;
+      if (p != k) {
+        const double t0 = x[k];
+        x[k] = x[p];
+        x[p] = t0;
+      }
+    }
+  __syncthreads();
+  for (int k = 0; k < nb - 1; ++k) {
+    const double xk = x[k];
+    const int i = k + 1 + tid;
+    if (i < nb) x[i] = fma(-A[(size_t)k * nb + i], xk, x[i]);
+    __syncthreads();
+  }
+  for (int k = nb - 1; k >= 0; --k) {
+    const double xk = x[k] / A[(size_t)k * nb + k];
+    __syncthreads();
+    if (tid == 0) x[k] = xk;
+    if (tid < k) x[tid] = fma(-A[(size_t)k * nb + tid], xk, x[tid]);
+    __syncthreads();
+  }
+  for (int t = tid; t < nb; t += kSmallThreads) xg[t] = x[t];
+}
+
+inline size_t small_solve_smem_bytes(int nb) { return sizeof(double) * ((size_t)nb * nb + nb); }
+
+}  // namespace lb

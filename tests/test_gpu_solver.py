@@ -149,16 +149,18 @@ def test_newton_iterations_contract(gpu):
     assert np.all(np.array(res[1:]) / np.array(res[:-1]) < 0.6)
 
 
-def test_config4_mesh_newton_step_matches_splu(gpu):
-    """A 32x64 uniform Q2 mesh with BASELINE config 4's four species (8385
-    free nodes, 64 bandwidth blocks: six reduction levels): the device
-    Newton step equals the host step done with SuperLU on the same device
-    operator, and the device mass matrix satisfies M 1 = the r-weighted
-    areas (row sums)."""
+@pytest.mark.parametrize("nr,nz", [(16, 32), (32, 64)])
+def test_config4_mesh_newton_step_matches_splu(gpu, nr, nz):
+    """Uniform Q2 meshes with BASELINE config 4's four species -- 16x32
+    (2145 free nodes, 68-row blocks: the shared-memory block LU) and 32x64
+    (8385 free nodes, 132-row blocks in 64 block rows: cuBLAS, six reduction
+    levels): the device Newton step equals the host step done with SuperLU
+    on the same device operator, and the device mass matrix integrates r
+    over the domain."""
     from paper_1702_08880_b200 import synthetic
     from paper_1702_08880_b200.solver import _mesh_solver
 
-    mesh, nodes = synthetic.uniform_q2_mesh(5.0, 32, 64)
+    mesh, nodes = synthetic.uniform_q2_mesh(5.0, nr, nz)
     ref = synthetic.q2_reference()
     f0, nu, mro = synthetic.cfg4_state(nodes)
     params = gpu.CollisionParams(nu_hat=nu, mass_ratio_o=mro)
