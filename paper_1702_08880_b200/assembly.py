@@ -24,7 +24,7 @@ import numpy as np
 import scipy.sparse as sp
 
 from . import _lib
-from .kernel import _f64, _inner_fields, _n_species, coupling
+from .kernel import _f64, _host_out, _inner_fields, _n_species, coupling
 from .scatter import build_gather_map
 
 __all__ = ["CollisionMatrix", "DeviceMesh", "assemble_at", "assemble_collision",
@@ -180,7 +180,7 @@ def assemble_collision(mesh, ref, data, params, eps_d: float | None = None,
     dm = device_mesh(mesh, ref)
     gm = dm.map
     coK, coD = coupling(params)
-    csr = np.empty((S, gm.nnz))
+    csr = _host_out((S, gm.nnz))
     phase = np.zeros(3)
     t1 = time.perf_counter()
     if ncell:
@@ -226,7 +226,7 @@ def assemble_at(mesh, ref, state, params, eps_d: float | None = None,
     c = _coeffs(state, S, dm.n_free)
     gm = dm.map
     coK, coD = coupling(params)
-    csr = np.empty((S, gm.nnz))
+    csr = _host_out((S, gm.nnz))
     n = 9 * dm.ncell
     data = np.empty((3 + 3 * S, n)) if return_data else None
     phase = np.zeros(3)
