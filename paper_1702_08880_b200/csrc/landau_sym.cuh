@@ -115,6 +115,67 @@ struct SymArgs {
   long long gthr;
 };
 
+// Producer of both symmetric sweeps (thread 0 of the CTA): walks the (item,
+// d) partner tiles of its work items, issuing each tile into the TMA ring
+// once the stage is free.  Items after the first wave (item = blockIdx.x)
+// are claimed from a global counter, so CTAs that the warp schedulers favour
+// take more items and all CTAs of an SM stay resident until the end; every
+// item writes its own partial slot, so the result does not depend on which
+// CTA ran it.  Each stage carries its (item, d) to the consumers; item -1
+// ends the sweep.
+template <int RS>
+struct SymProducer {
+  const SymArgs& a;
+  long long nitems;
+  double* smem;
+  uint64_t *full, *empty;
+  int *stage_item, *stage_d;
+  int p_item, p_d = -1;
+  uint32_t p_k = 0;
+  bool p_done = false;
+
+  __device__ SymProducer(const SymArgs& args, long long n, double* sm, uint64_t* f, uint64_t* e, int* si,
+                         int* sd)
+      : a(args), nitems(n), smem(sm), full(f), empty(e), stage_item(si), stage_d(sd),
+        p_item(blockIdx.x) {}
+
+  __device__ void seg_range(int item, int& I, int& d0, int& d1) const {
+    I = a.row0 + item / a.nseg;
+    const int seg = item % a.nseg;
+    const int L = sym_seglen(a.nt);
+    d0 = seg * L;
+    d1 = min(sym_h(I, a.nt) + 1, d0 + L);
+  }
+
+  __device__ void issue_next() {
+    if (p_done) return;
+    int I = 0, d0, d1;
+    while (p_item < nitems) {
+      seg_range(p_item, I, d0, d1);
+      if (p_d < 0) p_d = d0;
+      if (p_d < d1) break;
+      p_item = (int)gridDim.x + atomicAdd(a.next_item, 1);  // segment done: claim the next
+      p_d = -1;
+    }
+    const uint32_t s = p_k % kSymStages;
+    if (p_k >= kSymStages) mbar_wait(&empty[s], ((p_k / kSymStages) - 1) & 1);
+    ++p_k;
+    if (p_item >= nitems) {
+      stage_item[s] = -1;
+      mbar_arrive(&full[s]);
+      p_done = true;
+      return;
+    }
+    stage_item[s] = p_item;
+    stage_d[s] = p_d;
+    const int J = (I + p_d) % a.nt;
+    const uint32_t bytes = kSymTile * RS * sizeof(double);
+    mbar_expect_tx(&full[s], bytes);
+    bulk_g2s(smem + s * (kSymTile * RS), a.rec + (size_t)J * kSymTile * RS, bytes, &full[s]);
+    ++p_d;
+  }
+};
+
 template <int S>
 __device__ __forceinline__ void load_point(const double* rp, Outer& o, double (&gi)[S][3]) {
   o = make_outer(rp[0], rp[1]);
@@ -152,50 +213,8 @@ __global__ void __launch_bounds__(kSymTile, sym_min_blocks(S)) lb_symsweep_kerne
   }
   __syncthreads();
 
-  // Producer (thread 0): walks (item, d) tiles.  Items after the first wave
-  // (item = blockIdx.x) are claimed from a global counter, so CTAs that the
-  // warp schedulers favour take more items and all CTAs of an SM stay
-  // resident until the end.  Every item writes its own partial slot, so the
-  // result does not depend on which CTA ran it.  Each stage carries its
-  // (item, d) to the consumers; item -1 ends the sweep.
-  int p_item = blockIdx.x, p_d = -1;
-  uint32_t p_k = 0;
-  bool p_done = false;
-  auto seg_range = [&](int item, int& I, int& d0, int& d1) {
-    I = a.row0 + item / a.nseg;
-    const int seg = item % a.nseg;
-    const int L = sym_seglen(a.nt);
-    d0 = seg * L;
-    d1 = min(sym_h(I, a.nt) + 1, d0 + L);
-  };
-  auto issue_next = [&]() {
-    if (p_done) return;
-    int I = 0, d0, d1;
-    while (p_item < nitems) {
-      seg_range(p_item, I, d0, d1);
-      if (p_d < 0) p_d = d0;
-      if (p_d < d1) break;
-      p_item = (int)gridDim.x + atomicAdd(a.next_item, 1);  // segment done: claim the next
-      p_d = -1;
-    }
-    const uint32_t s = p_k % kSymStages;
-    if (p_k >= kSymStages) mbar_wait(&empty[s], ((p_k / kSymStages) - 1) & 1);
-    ++p_k;
-    if (p_item >= nitems) {
-      stage_item[s] = -1;
-      mbar_arrive(&full[s]);
-      p_done = true;
-      return;
-    }
-    stage_item[s] = p_item;
-    stage_d[s] = p_d;
-    const int J = (I + p_d) % a.nt;
-    const uint32_t bytes = kSymTile * RS * sizeof(double);
-    mbar_expect_tx(&full[s], bytes);
-    bulk_g2s(lb_smem + s * (kSymTile * RS), a.rec + (size_t)J * kSymTile * RS, bytes, &full[s]);
-    ++p_d;
-  };
-  if (tid == 0) issue_next();
+  SymProducer<RS> prod(a, nitems, lb_smem, full, empty, stage_item, stage_d);
+  if (tid == 0) prod.issue_next();
 
   Outer o;
   double gi[S][3];
@@ -209,7 +228,7 @@ __global__ void __launch_bounds__(kSymTile, sym_min_blocks(S)) lb_symsweep_kerne
       for (int q = 0; q < 5; ++q) dst[(size_t)(b * 5 + q) * kSymTile] = acc[b][q];
   };
   for (uint32_t k = 0;; ++k) {
-    if (tid == 0) issue_next();
+    if (tid == 0) prod.issue_next();
     const uint32_t s = k % kSymStages;
     mbar_wait(&full[s], (k / kSymStages) & 1);
     const int item = stage_item[s], d = stage_d[s];
@@ -432,44 +451,8 @@ __global__ void __launch_bounds__(kIbThreads, LB_IB_MINB) lb_symsweep_ib_kernel(
   }
   __syncthreads();
 
-  int p_item = blockIdx.x, p_d = -1;
-  uint32_t p_k = 0;
-  bool p_done = false;
-  auto seg_range = [&](int item, int& I, int& d0, int& d1) {
-    I = a.row0 + item / a.nseg;
-    const int seg = item % a.nseg;
-    const int L = sym_seglen(a.nt);
-    d0 = seg * L;
-    d1 = min(sym_h(I, a.nt) + 1, d0 + L);
-  };
-  auto issue_next = [&]() {
-    if (p_done) return;
-    int I = 0, d0, d1;
-    while (p_item < nitems) {
-      seg_range(p_item, I, d0, d1);
-      if (p_d < 0) p_d = d0;
-      if (p_d < d1) break;
-      p_item = (int)gridDim.x + atomicAdd(a.next_item, 1);
-      p_d = -1;
-    }
-    const uint32_t s = p_k % kSymStages;
-    if (p_k >= kSymStages) mbar_wait(&empty[s], ((p_k / kSymStages) - 1) & 1);
-    ++p_k;
-    if (p_item >= nitems) {
-      stage_item[s] = -1;
-      mbar_arrive(&full[s]);
-      p_done = true;
-      return;
-    }
-    stage_item[s] = p_item;
-    stage_d[s] = p_d;
-    const int J = (I + p_d) % a.nt;
-    const uint32_t bytes = kSymTile * RS * sizeof(double);
-    mbar_expect_tx(&full[s], bytes);
-    bulk_g2s(lb_smem + s * (kSymTile * RS), a.rec + (size_t)J * kSymTile * RS, bytes, &full[s]);
-    ++p_d;
-  };
-  if (tid == 0) issue_next();
+  SymProducer<RS> prod(a, nitems, lb_smem, full, empty, stage_item, stage_d);
+  if (tid == 0) prod.issue_next();
 
   Outer o[2];
   double gi[2][S][3];
@@ -487,7 +470,7 @@ __global__ void __launch_bounds__(kIbThreads, LB_IB_MINB) lb_symsweep_ib_kernel(
     }
   };
   for (uint32_t k = 0;; ++k) {
-    if (tid == 0) issue_next();
+    if (tid == 0) prod.issue_next();
     const uint32_t s = k % kSymStages;
     mbar_wait(&full[s], (k / kSymStages) & 1);
     const int item = stage_item[s], d = stage_d[s];
