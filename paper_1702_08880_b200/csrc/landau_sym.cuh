@@ -41,15 +41,8 @@ constexpr int kSymStages = LB_SYM_STAGES;  // TMA ring depth (one J tile per sta
 #define LB_SEGLEN 2
 #endif
 constexpr int kSegLenMax = LB_SEGLEN;  // partner tiles per work item (large n)
-#ifndef LB_SYM_PAIRS
-#define LB_SYM_PAIRS 2  // Se = 1: pairs evaluated in lockstep per thread and step
-#endif
 #ifndef LB_SYM_MINB
-#if LB_SYM_PAIRS == 2
-#define LB_SYM_MINB 4  // CTAs per SM for Se = 1 (128 registers, no spills)
-#else
-#define LB_SYM_MINB 5  // CTAs per SM for Se = 1 (94 registers, no spills)
-#endif
+#define LB_SYM_MINB 5  // CTAs per SM of lb_symsweep_kernel<1> (LB_SYM_IB=0; 94 registers)
 #endif
 #ifndef LB_SYM_UNROLL
 #define LB_SYM_UNROLL 1
@@ -61,12 +54,6 @@ __host__ __device__ constexpr int sym_min_blocks(int Se) {
   return Se == 1 ? kSymMinBlocks : (Se == 2 ? 4 : 2);
 }
 constexpr int kSymUnroll = LB_SYM_UNROLL;
-// partners per thread and step: two for the species-collapsed kernel (shared
-// coefficient loads, two overlapping chains), one where registers are short
-template <int S>
-__host__ __device__ constexpr int sym_pairs() {
-  return S == 1 ? LB_SYM_PAIRS : 1;
-}
 #ifndef LB_SYM_MAXS
 #define LB_SYM_MAXS 3  // measured: S = 4 symmetric (210 regs, 2 CTAs/SM) loses to the general sweep
 #endif
@@ -253,95 +240,6 @@ __global__ void __launch_bounds__(kSymTile, sym_min_blocks(S)) lb_symsweep_kerne
         for (int b = 0; b < S; ++b)
 #pragma unroll
           for (int q = 0; q < 5; ++q) jacc[b][q] = 0.0;
-        if constexpr (sym_pairs<S>() > 1) {
-          // U partners per step: j = (lane + st + u L) mod 32, L = 32 / U,
-          // st < L.  Accumulator u of j visits lanes j - uL .. j - uL - L + 1;
-          // after the L steps lane l holds accumulator u of j = l + (u+1)L,
-          // so j's total is gathered from U lanes in fixed u order below.
-          constexpr int U = sym_pairs<S>(), L = 32 / U;
-          double ju[U][S][5];
-#pragma unroll
-          for (int u = 0; u < U; ++u)
-#pragma unroll
-            for (int b = 0; b < S; ++b)
-#pragma unroll
-              for (int q = 0; q < 5; ++q) ju[u][b][q] = 0.0;
-          double2 rzn[U];
-#pragma unroll
-          for (int u = 0; u < U; ++u)
-            rzn[u] = *reinterpret_cast<const double2*>(tile + (jb * 32 + ((lane + u * L) & 31)) * RS);
-#pragma unroll kSymUnroll
-          for (int st = 0; st < L; ++st) {
-            const double* rp[U];
-            double rn[U], zn[U], rn2[U], rcpr[U];
-#pragma unroll
-            for (int u = 0; u < U; ++u) {
-              const int jl = (lane + st + u * L) & 31;
-              rp[u] = tile + (jb * 32 + jl) * RS;
-              rn[u] = rzn[u].x;
-              zn[u] = rzn[u].y;
-              rzn[u] = *reinterpret_cast<const double2*>(tile + (jb * 32 + ((jl + 1) & 31)) * RS);
-              const double2 aux = *reinterpret_cast<const double2*>(rp[u] + 2);
-              rn2[u] = aux.x;
-              rcpr[u] = aux.y;
-            }
-            T5 t[U];
-            double txx2[U];
-            Outer oo[U];
-#pragma unroll
-            for (int u = 0; u < U; ++u) oo[u] = o;
-            pair_tensor_sym_x<U>(oo, rn, zn, rn2, rcpr, a.gthr, logt, t, txx2);
-#pragma unroll
-            for (int u = 0; u < U; ++u) {
-#pragma unroll
-              for (int b = 0; b < S; ++b) {
-                const double gr = rp[u][4 + 3 * b], gz = rp[u][5 + 3 * b], fw = rp[u][6 + 3 * b];
-                acc[b][0] = fma(t[u].xz, gz, fma(t[u].kr, gr, acc[b][0]));
-                acc[b][1] = fma(t[u].zz, gz, fma(t[u].zr, gr, acc[b][1]));
-                acc[b][2] = fma(fw, t[u].xx, acc[b][2]);
-                acc[b][3] = fma(fw, t[u].xz, acc[b][3]);
-                acc[b][4] = fma(fw, t[u].zz, acc[b][4]);
-              }
-            }
-            if (!diag) {
-#pragma unroll
-              for (int u = 0; u < U; ++u)
-#pragma unroll
-                for (int b = 0; b < S; ++b) {
-                  ju[u][b][0] = fma(t[u].zr, gi[b][1], fma(t[u].kr, gi[b][0], ju[u][b][0]));
-                  ju[u][b][1] = fma(t[u].zz, gi[b][1], fma(t[u].xz, gi[b][0], ju[u][b][1]));
-                  ju[u][b][2] = fma(gi[b][2], txx2[u], ju[u][b][2]);
-                  ju[u][b][3] = fma(gi[b][2], t[u].zr, ju[u][b][3]);
-                  ju[u][b][4] = fma(gi[b][2], t[u].zz, ju[u][b][4]);
-                }
-#pragma unroll
-              for (int u = 0; u < U; ++u)
-#pragma unroll
-                for (int b = 0; b < S; ++b)
-#pragma unroll
-                  for (int q = 0; q < 5; ++q)
-                    ju[u][b][q] = __shfl_sync(0xffffffffu, ju[u][b][q], (lane + 1) & 31);
-            }
-          }
-          if (!diag) {
-#pragma unroll
-            for (int b = 0; b < S; ++b)
-#pragma unroll
-              for (int q = 0; q < 5; ++q) {
-                double x = 0.0;
-#pragma unroll
-                for (int u = 0; u < U; ++u) {
-                  const double v = (u + 1) * L == 32
-                                       ? ju[u][b][q]
-                                       : __shfl_sync(0xffffffffu, ju[u][b][q], (lane - (u + 1) * L) & 31);
-                  x = u == 0 ? v : __dadd_rn(x, v);
-                }
-                jacc[b][q] = x;
-              }
-          }
-        } else {
-        // (r, z) of the next step's record are loaded one step ahead so the
-        // shared-memory latency is off the pair's dependency chain
         // (r, z) of the next step's record are loaded one step ahead so the
         // shared-memory latency is off the pair's dependency chain
         double2 rz_next = *reinterpret_cast<const double2*>(tile + (jb * 32 + lane) * RS);
@@ -380,7 +278,6 @@ __global__ void __launch_bounds__(kSymTile, sym_min_blocks(S)) lb_symsweep_kerne
               for (int q = 0; q < 5; ++q)
                 jacc[b][q] = __shfl_sync(0xffffffffu, jacc[b][q], (lane + 1) & 31);
           }
-        }
         }
         if (!diag) {
           // lane holds this warp's sum for j = jb*32 + lane; the four warps'
