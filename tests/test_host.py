@@ -204,16 +204,26 @@ def test_install_into_the_reference_package():
         assert ax.cli.fused_sweep is pkg.fused_sweep and ax.cli.assemble_collision is pkg.assemble_collision
         assert ax.kernel.fused_inner_loop is pkg.fused_inner_loop
         assert ax.fused_sweep is pkg.fused_sweep
+        assert ax.solver.newton_step is pkg.newton_step
+        assert ax.solver.linear_cn_step is pkg.linear_cn_step
+        from paper_1702_08880_b200 import solver as our_solver
+
+        # failures surface as the reference's own StepFailure (advance catches it)
+        assert our_solver._StepFailure is ax.solver.StepFailure
         import inspect
 
         # the patched entry points accept the reference's call signatures
         for ref_fn, ours in ((saved[("kernel", "fused_sweep")], pkg.fused_sweep),
-                             (saved[("assembly", "assemble_collision")], pkg.assemble_collision)):
+                             (saved[("assembly", "assemble_collision")], pkg.assemble_collision),
+                             (saved[("solver", "newton_step")], pkg.newton_step),
+                             (saved[("solver", "linear_cn_step")], pkg.linear_cn_step)):
             assert list(inspect.signature(ref_fn).parameters) == list(
                 inspect.signature(ours).parameters)
     finally:
         pkg.uninstall(ax, saved)
     assert ax.assembly.fused_sweep is not pkg.fused_sweep
+    assert ax.solver.newton_step is not pkg.newton_step
+    assert our_solver._StepFailure is our_solver.StepFailure
 
 
 def test_elliptic_domain_errors_before_the_device():
