@@ -241,6 +241,38 @@ def case_cfg2():
          masses=np.array([s.mass for s in sp_]), **blocks_parts("C", cm))
 
 
+def case_cfg1_advance():
+    """BASELINE config 1 time integration: the reference's own advance()
+    (solver.py:153-200) on the 8x16 mesh with the drifting Maxwellian of
+    case_cfg1, 10 steps of dt = 0.1, Newton to 1e-12 (at most 4 frozen-
+    coefficient iterations per step); per-step states, moments and residual
+    histories.  (Config 2's deuterium, sigma = 0.012 on an h = 0.3 mesh, makes
+    the reference's iteration diverge, so it is no parity target.)"""
+    from axlandau.solver import StepConfig, advance
+
+    domain = ax.DomainSpec(L=5.0)
+    ref = ax.build_reference_element()
+    mesh = ax.cartesian_mesh(domain, 8, 16)
+    sp_ = [ax.Species("e", 1.0, -1.0, 0.5, shift=0.5)]
+    state = ax.maxwellian_init(mesh, ref, sp_, neutralize=False)
+    state.coeffs *= 2.0
+    params = ax.collision_params(sp_)
+    cfg = StepConfig(dt=0.1, newton_tol=1e-12, max_newton=4)
+    hist = []
+
+    def record(step, t, st, moms, info):
+        hist.append(info["residuals"] + [np.nan] * (cfg.max_newton - len(info["residuals"])))
+
+    traj = advance(mesh, ref, sp_, state, 1.0, cfg, params=params, callback=record)
+    states = np.stack([s.coeffs for _, s, _ in traj])
+    moms = np.stack([np.stack([m.n, m.p_z, m.E, m.q_z]) for _, _, m in traj])
+    M = ax.mass_matrix(mesh, ref)
+    save("cfg1adv", **mesh_parts(mesh, ref), **params_parts(params), **csr_parts("M", M),
+         states=states, moms=moms, residuals=np.array(hist), dt=np.float64(cfg.dt),
+         newton_tol=np.float64(cfg.newton_tol), max_newton=np.int64(cfg.max_newton),
+         masses=np.array([s.mass for s in sp_]), Wm=moment_matrix(mesh, ref))
+
+
 def case_cfg3():
     """BASELINE config 3, reference-native reading: Q2 on an
     8x16 base (L=5) refined 3 rounds toward the origin and the thermal shell
@@ -408,7 +440,7 @@ def main():
     which = set(sys.argv[1:])
     cases = {"pairs": case_pairs, "sweep_small": case_sweep_small, "cfg1": case_cfg1,
              "hanging": case_hanging, "cons": case_cons, "cfg2": case_cfg2,
-             "cfg3": case_cfg3, "cfg4s": case_cfg4_species, "cfg2m": case_cfg2_meshes,
+             "cfg3": case_cfg3, "cfg1adv": case_cfg1_advance, "cfg4s": case_cfg4_species, "cfg2m": case_cfg2_meshes,
              "cfg4m": case_cfg4_meshes,
              "cfg5_4096": lambda: case_cfg5(4096),
              "cfg5_65536": lambda: case_cfg5(65536, n_sub=192)}
