@@ -216,7 +216,7 @@ def ours_arm(args):
     wl = synthetic.cfg5(args.n)
     N, S = wl.N, wl.S
     params = pkg.CollisionParams(nu_hat=wl.nu_hat, mass_ratio_o=wl.mass_ratio_o)
-    sh = ShardedSweep(N, S, params, wl.eps_d, dev, align=1)
+    sh = ShardedSweep(N, S, params, wl.eps_d, dev, align=1, p2p=args.p2p)
     nloc = sh.hi - sh.lo
     host = local_fields(wl, sh.lo, sh.hi)
     d_fields = [torch.from_numpy(a).to(dev) for a in host]
@@ -375,13 +375,15 @@ def ours_arm(args):
                        "N": N, "S": S, "outer_per_gpu": nloc, "pairs_per_step": pairs_step,
                        "parallelism": f"outer-point shards x{world}" + (
                            f" + {args.backend} all-gather of packed field state"
-                           + (" + all-reduce of partial sums" if sh.symmetric else "")
+                           + ((" + peer-memory (CUDA IPC) reduction fused with the combine"
+                              if sh.p2p else " + all-reduce of partial sums") if sh.symmetric else "")
                            if world > 1 else ""),
                        "l2": "flushed between timed steps (256 MiB write, outside step events)"},
             "roofline": {"bound": "fp64", "achieved": achieved_tf, "peak": fp64_sustained,
                          "unit": "TFLOP/s", "frac": achieved_tf / fp64_sustained,
                          "traffic": traffic,
-                         "kernel": (f"lb_symsweep_kernel<{nacc}> + lb_symreduce_kernel" if sh.symmetric
+                         "kernel": ((f"lb_symsweep_ib_kernel<1>" if nacc == 1 else f"lb_symsweep_kernel<{nacc}>")
+                                    + " + lb_symreduce_kernel" if sh.symmetric
                                     else f"lb_sweep_kernel<{nacc}> (+ lb_combine_kernel, <1%)"),
                          "species_collapsed": nacc == 1 and S > 1,
                          "flops": "model 165+20*S^2 per ordered pair (kernel.py:560-574)"
@@ -408,6 +410,7 @@ def ours_arm(args):
             line["note"] = f"functional run over {args.backend} (ranks may share a GPU): not a timing"
 
         print(json.dumps(line), flush=True)
+    sh.close()  # peer-memory mode: unmap the peers' buffers (collective)
     if world > 1:
         dist.destroy_process_group()
     return 0
@@ -428,6 +431,9 @@ def main():
     ap.add_argument("--peak-seconds", type=float, default=1.0,
                     help="duration of the FP64 DFMA peak probe (the roofline denominator)")
     ap.add_argument("--backend", choices=["nccl", "gloo"], default="nccl")
+    ap.add_argument("--p2p", action="store_true",
+                    help="symmetric path: peer-memory (CUDA IPC / NVLink) reduction fused with "
+                         "the combine instead of the NCCL all-reduce")
     ap.add_argument("--check", action="store_true",
                     help="compare every rank's rows with the oracle on a sample")
     args = ap.parse_args()

@@ -34,6 +34,8 @@
 #ifndef LANDAU_B200_H
 #define LANDAU_B200_H
 
+#include <stddef.h>
+
 #ifdef __cplusplus
 extern "C" {
 #endif
@@ -245,6 +247,23 @@ int lb_sym_combine_dev(lb_ctx *ctx, int S, const double *tot, const double *coK,
 /* elliptic_KE (kernel.py:93-113): K(m), E(m) for n parameters in [0, 1)
  * (LB_EINVAL outside), with the device's table log and Horner chains. */
 int lb_elliptic_ke(lb_ctx *ctx, int n, const double *m, double *K, double *E);
+
+/* Peer-memory reduction for the symmetric multi-GPU path: every rank
+ * allocates its partial-sum buffer with lb_ipc_alloc (cudaMalloc + a
+ * 64-byte CUDA IPC handle), the handles are exchanged out of band, and each
+ * rank maps its peers' buffers with lb_ipc_open (peer access over NVLink).
+ * lb_sym_combine_peers_dev is lb_sym_combine_dev reading the G ranks'
+ * partial sums (tots: a DEVICE array of G pointers, rank order) and adding
+ * them for points [q0, q1) only -- the all-reduce and the combine in one
+ * kernel.  The caller orders it after every rank's lb_sym_partial_dev and
+ * before any rank's next one (e.g. a stream-ordered barrier). */
+int lb_sym_combine_peers_dev(lb_ctx *ctx, int S, const double *const *tots, int G,
+                             const double *coK, const double *coD, int q0, int q1,
+                             double *K_out, double *D_out, void *stream);
+int lb_ipc_alloc(lb_ctx *ctx, size_t bytes, void **dptr, unsigned char *handle);
+int lb_ipc_open(lb_ctx *ctx, const unsigned char *handle, void **dptr);
+int lb_ipc_close(lb_ctx *ctx, void *dptr);
+int lb_ipc_free(lb_ctx *ctx, void *dptr);
 
 /* Number of kernels the most recent lb_sweep_dev / lb_elements_dev /
  * lb_pack_records_dev call launched (for the benchmark's launch count). */

@@ -64,6 +64,11 @@ SIGNATURES = {
     "lb_last_launch_count": (_i, [_vp]),
     "lb_fp64_peak": (_i, [_vp, _dp, _dp]),
     "lb_elliptic_ke": (_i, [_vp, _i, _dp, _dp, _dp]),
+    "lb_sym_combine_peers_dev": (_i, [_vp, _i, _vp, _i, _dp, _dp, _i, _i, _vp, _vp, _vp]),
+    "lb_ipc_alloc": (_i, [_vp, C.c_size_t, C.POINTER(_vp), C.c_char_p]),
+    "lb_ipc_open": (_i, [_vp, C.c_char_p, C.POINTER(_vp)]),
+    "lb_ipc_close": (_i, [_vp, _vp]),
+    "lb_ipc_free": (_i, [_vp, _vp]),
     "lb_cn_create": (_i, [_vp, _vp, _i, _i, _ip, _ip, _ip, _i, C.POINTER(_vp)]),
     "lb_cn_destroy": (_i, [_vp]),
     "lb_cn_set_mass": (_i, [_vp, _dp]),

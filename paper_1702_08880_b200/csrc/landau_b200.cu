@@ -822,6 +822,85 @@ int lb_sym_combine_dev(lb_ctx* ctx, int S, const double* tot, const double* coK,
   return sym_combine_dispatch(ctx, cp.Se, tot, cp, q0, q1, K_out, D_out, (cudaStream_t)stream);
 }
 
+int lb_sym_combine_peers_dev(lb_ctx* ctx, int S, const double* const* tots, int G, const double* coK,
+                             const double* coD, int q0, int q1, double* K_out, double* D_out,
+                             void* stream) {
+  int rc = use_ctx(ctx);
+  if (rc) return rc;
+  if (ctx->sym_n < 0 || ctx->sym_S != S) return fail(LB_EINVAL, "lb_sym_prepare_dev not called for this S");
+  if (q0 < 0 || q1 > ctx->sym_n || q0 > q1) return fail(LB_EINVAL, "bad point range");
+  if (!coK || !coD || !tots || G < 1) return fail(LB_EINVAL, "null argument or no ranks");
+  Coupling cp;
+  make_coupling(S, coK, coD, cp);
+  if (cp.Se != ctx->sym_Se) return fail(LB_EINVAL, "coupling differs from lb_sym_prepare_dev's");
+  if (q1 == q0) return LB_OK;
+  const int npad = ctx->sym_nt * kSymTile;
+  const int* inv = static_cast<const int*>(ctx->syminv.p);
+  cudaStream_t st = (cudaStream_t)stream;
+  const int grid = (q1 - q0 + 127) / 128;
+  switch (cp.Se) {
+    case 1: lb_sym_combine_peers_kernel<1><<<grid, 128, 0, st>>>(tots, G, npad, inv, q0, q1, cp, K_out, D_out); break;
+    case 2: lb_sym_combine_peers_kernel<2><<<grid, 128, 0, st>>>(tots, G, npad, inv, q0, q1, cp, K_out, D_out); break;
+#if LB_SYM_MAXS >= 3
+    case 3: lb_sym_combine_peers_kernel<3><<<grid, 128, 0, st>>>(tots, G, npad, inv, q0, q1, cp, K_out, D_out); break;
+#endif
+    default: return fail(LB_EINVAL, "symmetric sweep supports S <= " + std::to_string(kSymMaxS));
+  }
+  LB_CUDA(cudaGetLastError());
+  ctx->last_launches = 1;
+  return LB_OK;
+}
+
+int lb_ipc_alloc(lb_ctx* ctx, size_t bytes, void** dptr, unsigned char* handle) {
+  int rc = use_ctx(ctx);
+  if (rc) return rc;
+  if (!dptr || !handle) return fail(LB_EINVAL, "null argument");
+  *dptr = nullptr;
+  cudaError_t e = cudaMalloc(dptr, std::max<size_t>(bytes, 8));
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return fail(e == cudaErrorMemoryAllocation ? LB_ENOMEM : LB_ECUDA, std::string("lb_ipc_alloc: ") + cudaGetErrorString(e));
+  }
+  cudaIpcMemHandle_t h;
+  e = cudaIpcGetMemHandle(&h, *dptr);
+  if (e != cudaSuccess) {
+    cudaFree(*dptr);
+    *dptr = nullptr;
+    cudaGetLastError();
+    return fail(LB_ECUDA, std::string("cudaIpcGetMemHandle: ") + cudaGetErrorString(e));
+  }
+  std::memcpy(handle, &h, sizeof(h));
+  return LB_OK;
+}
+
+int lb_ipc_open(lb_ctx* ctx, const unsigned char* handle, void** dptr) {
+  int rc = use_ctx(ctx);
+  if (rc) return rc;
+  if (!dptr || !handle) return fail(LB_EINVAL, "null argument");
+  cudaIpcMemHandle_t h;
+  std::memcpy(&h, handle, sizeof(h));
+  const cudaError_t e = cudaIpcOpenMemHandle(dptr, h, cudaIpcMemLazyEnablePeerAccess);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return fail(LB_ECUDA, std::string("cudaIpcOpenMemHandle: ") + cudaGetErrorString(e));
+  }
+  return LB_OK;
+}
+
+int lb_ipc_close(lb_ctx* ctx, void* dptr) {
+  int rc = use_ctx(ctx);
+  if (rc) return rc;
+  if (dptr) LB_CUDA(cudaIpcCloseMemHandle(dptr));
+  return LB_OK;
+}
+
+int lb_ipc_free(lb_ctx* ctx, void* dptr) {
+  int rc = use_ctx(ctx);
+  if (rc) return rc;
+  if (dptr) LB_CUDA(cudaFree(dptr));
+  return LB_OK;
+}
+
 int lb_mesh_create(lb_ctx* ctx, int ncell, const double* cell_sizes, const double* B,
                    const double* dB, int nslots, const int* slot_ptr, int ncontrib,
                    const int* gather_idx, const double* gather_w, lb_mesh** out) {

@@ -610,6 +610,31 @@ __global__ void lb_sym_combine_kernel(const double* __restrict__ tot, int npad,
   write_kd<Se>(A, cp, (size_t)(q - q0), K, D);
 }
 
+// Peer-memory variant fused with the cross-rank reduction: the partial
+// sums of all G ranks are read directly (tots[g] are peer pointers mapped
+// over NVLink with CUDA IPC) for this rank's own points only and added in
+// rank order before the coupling -- the all-reduce + combine of the NCCL
+// path as one kernel, moving only this rank's share of every rank's sums.
+template <int Se>
+__global__ void lb_sym_combine_peers_kernel(const double* const* __restrict__ tots, int G, int npad,
+                                            const int* __restrict__ inv, int q0, int q1,
+                                            const Coupling cp, double* __restrict__ K,
+                                            double* __restrict__ D) {
+  const int q = q0 + blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= q1) return;
+  const int p = inv[q];
+  double A[Se][5];
+#pragma unroll
+  for (int b = 0; b < Se; ++b)
+#pragma unroll
+    for (int c = 0; c < 5; ++c) {
+      double v = tots[0][(size_t)(b * 5 + c) * npad + p];
+      for (int g = 1; g < G; ++g) v = __dadd_rn(v, tots[g][(size_t)(b * 5 + c) * npad + p]);
+      A[b][c] = v;
+    }
+  write_kd<Se>(A, cp, (size_t)(q - q0), K, D);
+}
+
 __global__ void lb_invert_perm_kernel(int n, const int* __restrict__ perm, int* __restrict__ inv) {
   const int p = blockIdx.x * blockDim.x + threadIdx.x;
   if (p < n) inv[perm[p]] = p;

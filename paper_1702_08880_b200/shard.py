@@ -80,12 +80,16 @@ class ShardedSweep:
     align : shard alignment in points (9 = whole Q2 cells; 1 for point clouds)
     pack_fn, sweep_fn : injectable for CPU testing; default to the CUDA
              library (lb_pack_records_dev / lb_sweep_dev on torch tensors)
+    p2p : symmetric path only -- replace the all-reduce of the partial sums
+             and the combine by one kernel that reads every rank's partial
+             sums for this rank's own points through CUDA IPC peer mappings
+             (NVLink), ordered by stream-level barriers
     """
 
     def __init__(self, n: int, S: int, params, eps_d: float, device, align: int = 9,
                  group=None, pack_fn: Callable | None = None,
                  sweep_fn: Callable | None = None, symmetric: bool | None = None,
-                 sym_fns: tuple | None = None):
+                 sym_fns: tuple | None = None, p2p: bool = False):
         import torch
 
         dist = _dist()
@@ -124,10 +128,17 @@ class ShardedSweep:
             sym_ok = (pack_fn is None and sweep_fn is None and self.n >= 128 and bool(
                 self._lib.lb_sym_supported(self.S, _lib.dptr(self.coK), _lib.dptr(self.coD))))
         self.symmetric = sym_ok if symmetric is None else (bool(symmetric) and sym_ok)
+        self.p2p = bool(p2p) and self.symmetric and sym_fns is None
+        self._p2p_pending = False
+        self._opened = []
+        self._ipc_ptr = None
         if self.symmetric:  # partial sums: 5 per accumulator set (1 set when collapsed)
             npad = -(-self.n // 128) * 128
-            self.tot = torch.zeros((5 * max(self.nacc, 1), npad), dtype=torch.float64,
-                                   device=self.device)
+            shape = (5 * max(self.nacc, 1), npad)
+            if self.p2p:
+                self.tot = self._init_p2p(shape)
+            else:
+                self.tot = torch.zeros(shape, dtype=torch.float64, device=self.device)
         mc = self.plan.max_count
         f64 = torch.float64
         self.send = torch.zeros((mc, self.RS), dtype=f64, device=self.device)
@@ -139,6 +150,73 @@ class ShardedSweep:
         self.K = torch.empty((nl, self.S, 2), dtype=f64, device=self.device)
         self.D = torch.empty((nl, self.S, 2, 2), dtype=f64, device=self.device)
         self.launches = 0
+
+    # ---------------------------------------------------------------- peer memory
+    def _init_p2p(self, shape):
+        """Partial-sum buffer in CUDA IPC memory; map every peer's buffer."""
+        import ctypes as C
+
+        import torch
+
+        lib, ctx = self._lib, self._ctx.handle
+        nbytes = 8 * shape[0] * shape[1]
+        ptr = C.c_void_p()
+        handle = C.create_string_buffer(64)
+        _lib.check(lib.lb_ipc_alloc(ctx, nbytes, C.byref(ptr), handle))
+        self._ipc_ptr = ptr.value
+        handles = [bytes(handle.raw)]
+        if self.world > 1:
+            handles = [None] * self.world
+            _dist().all_gather_object(handles, bytes(handle.raw), group=self.group)
+        peers = []
+        for g, h in enumerate(handles):
+            if g == self.rank:
+                peers.append(ptr.value)
+                continue
+            q = C.c_void_p()
+            _lib.check(lib.lb_ipc_open(ctx, h, C.byref(q)))
+            self._opened.append(q.value)
+            peers.append(q.value)
+        self._peer_ptrs = torch.tensor(peers, dtype=torch.int64, device=self.device)
+        self._flag = torch.zeros(1, dtype=torch.float64, device=self.device)
+
+        class _View:  # torch view of the IPC allocation (__cuda_array_interface__)
+            __cuda_array_interface__ = {"shape": tuple(shape), "typestr": "<f8",
+                                        "data": (ptr.value, False), "version": 3,
+                                        "strides": None}
+
+        tot = torch.as_tensor(_View(), device=self.device)
+        tot.zero_()
+        return tot
+
+    def _barrier(self):
+        """Every rank's prior work on its stream is done before any rank's
+        later work: a stream-ordered one-element NCCL all-reduce (no host
+        sync), or host synchronisation + barrier on gloo."""
+        if self.world == 1:
+            return
+        dist = _dist()
+        if dist.get_backend(self.group) == "nccl":
+            dist.all_reduce(self._flag, group=self.group)
+        else:
+            import torch
+
+            torch.cuda.synchronize(self.device)
+            dist.barrier(group=self.group)
+
+    def close(self):
+        if getattr(self, "_ipc_ptr", None) is None:
+            return
+        import torch
+
+        torch.cuda.synchronize(self.device)
+        self._barrier()  # no peer still reads our buffer
+        for q in self._opened:
+            self._lib.lb_ipc_close(self._ctx.handle, q)
+        self._opened = []
+        self.tot = None
+        self._lib.lb_ipc_free(self._ctx.handle, self._ipc_ptr)
+        self._ipc_ptr = None
 
     # ---------------------------------------------------------------- CUDA
     def _stream(self):
@@ -211,16 +289,32 @@ class ShardedSweep:
 
     def sym_partial(self):
         """Step 2: this rank's share of the unordered tile pairs -> tot."""
+        if self.p2p and self._p2p_pending:  # peers may still read our last sums
+            self._barrier()
+            self._p2p_pending = False
         self._sym_partial(self.tot)
 
     def sym_reduce(self):
         """Step 3: add the ranks' partial sums (one all-reduce of 5S doubles
-        per point, 5.2 MB at N = 2^16, S = 2)."""
-        if self.world > 1:
+        per point, 5.2 MB at N = 2^16, S = 2); peer-memory mode: only order
+        every rank's partial sums before the fused combine."""
+        if self.p2p:
+            self._barrier()
+        elif self.world > 1:
             _dist().all_reduce(self.tot, group=self.group)
 
     def sym_finish(self):
-        """Step 4: coupling -> K, D for this rank's own points."""
+        """Step 4: coupling -> K, D for this rank's own points (peer-memory
+        mode: the cross-rank sum for these points, fused)."""
+        if self.p2p:
+            p = _lib.dptr
+            _lib.check(self._lib.lb_sym_combine_peers_dev(
+                self._ctx.handle, self.S, self._peer_ptrs.data_ptr(), self.world, p(self.coK),
+                p(self.coD), self.lo, self.hi, self.K.data_ptr(), self.D.data_ptr(),
+                self._stream()))
+            self.launches += self._lib.lb_last_launch_count(self._ctx.handle)
+            self._p2p_pending = True
+            return self.K, self.D
         self._sym_combine(self.tot, self.lo, self.hi, self.K, self.D)
         return self.K, self.D
 

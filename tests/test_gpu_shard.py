@@ -142,6 +142,34 @@ def test_multirank_bench_functional(gpu, world):
     assert line["check_all_ranks_scaled_err_vs_oracle"] < 1e-10
 
 
+@pytest.mark.parametrize("world", [2, 3])
+def test_multirank_bench_p2p(gpu, world):
+    """The peer-memory reduction (CUDA IPC mappings of every rank's partial
+    sums, read by one fused reduce + combine kernel) with `world` ranks over
+    gloo on one GPU (ordering by host barriers; no kernel waits on another
+    rank): every rank's rows vs the oracle."""
+    import json
+    import socket
+    import subprocess
+    import sys
+
+    from conftest import ROOT
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={world}", "--master-addr=127.0.0.1", f"--master-port={port}",
+           "bench.py", "--gpus", str(world), "--backend", "gloo", "--p2p", "--check", "--steps", "3",
+           "--warmup", "3", "--points", "12000", "--no-clocks", "--e2e-steps", "2"]
+    out = subprocess.run(cmd, cwd=str(ROOT), capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stderr[-3000:]
+    line = json.loads([l for l in out.stdout.splitlines() if l.startswith("{")][-1])
+    assert "peer-memory" in line["config"]["parallelism"]
+    print("p2p multi-rank", world, "check", line["check_all_ranks_scaled_err_vs_oracle"])
+    assert line["check_all_ranks_scaled_err_vs_oracle"] < 1e-10
+
+
 @pytest.mark.parametrize("world,case", [(1, "cfg3"), (2, "cfg3"), (3, "hanging"), (2, "cfg2")])
 def test_sharded_operator(gpu, tmp_path, world, case):
     """Multi-GPU state-level operator (cells sharded, device sampling,
