@@ -1405,7 +1405,7 @@ struct CnLevel {
   int* piv = nullptr;   // pivots of the odd rows' D, (count x nb), batch order
   int* info = nullptr;  // getrf info of the odd rows
   CnBatch getrf;        // A = D (odd rows)
-  CnBatch getrsL, getrsU;  // A = D, B = L / U (odd rows; U: with a right neighbour)
+  CnBatch getrsL;       // A = D, B = [L U] (odd rows; adjacent blocks, one nb x 2nb right-hand side)
   CnBatch gemmE, gemmF;    // C = D_even -= A B
   CnBatch gemmG, gemmH;    // C = next level's L / U = -A B
   CnBatch solveY;          // B = v (odd rows): v := D^-1 v
@@ -1466,12 +1466,12 @@ static int cn_factor_issue(lb_cn* cn, cudaStream_t st) {
   for (const CnLevel& L : cn->lv) {
     if (L.getrf.count)
       LB_BLAS(cublasDgetrfBatched(cn->blas, nb, L.getrf.A, nb, L.piv, L.info, L.getrf.count));
+    // L_l[k] and U_l[k] are adjacent in the pool, so [L U] is one nb x 2nb
+    // column-major right-hand side: P = D^-1 [L U] in a single call (the
+    // last odd row's U slot is unused scratch when it has no right neighbour)
     if (L.getrsL.count)
-      LB_BLAS(cublasDgetrsBatched(cn->blas, CUBLAS_OP_N, nb, nb, L.getrsL.A, nb, L.piv, L.getrsL.B, nb,
-                                  &hinfo, L.getrsL.count));
-    if (L.getrsU.count)
-      LB_BLAS(cublasDgetrsBatched(cn->blas, CUBLAS_OP_N, nb, nb, L.getrsU.A, nb, L.piv, L.getrsU.B, nb,
-                                  &hinfo, L.getrsU.count));
+      LB_BLAS(cublasDgetrsBatched(cn->blas, CUBLAS_OP_N, nb, 2 * nb, L.getrsL.A, nb, L.piv, L.getrsL.B,
+                                  nb, &hinfo, L.getrsL.count));
     const CnBatch* acc[2] = {&L.gemmE, &L.gemmF};
     for (const CnBatch* b : acc)
       if (b->count)
@@ -1638,7 +1638,7 @@ static int cn_plan(lb_cn* cn) {
     CnLevel& L = cn->lv[l];
     const int Nl = Ns[l], step = 1 << l;
     L.N = Nl;
-    std::vector<double*> fA, lB, uA, uB, yB, bLA, bLx, bLy, bUA, bUx, bUy;
+    std::vector<double*> fA, lB, yB, bLA, bLx, bLy, bUA, bUx, bUy;
     std::vector<double*> eA, eB, eC, fA2, fB2, fC2, gA, gB, gC, hA, hB, hC;
     std::vector<double*> wLA, wLx, wLy, wUA, wUx, wUy;
     // odd rows (or the single row of the last level)
@@ -1655,8 +1655,6 @@ static int cn_plan(lb_cn* cn) {
       }
     for (int k = 1; k + 1 < Nl; k += 2)  // odd rows with a right neighbour (a prefix)
       for (int a = 0; a < S; ++a) {
-        uA.push_back(D(k * step, a));
-        uB.push_back(Ub(l, k, a));
         bUA.push_back(Ub(l, k, a));
         bUx.push_back(V((k + 1) * step, a));
         bUy.push_back(V(k * step, a));
@@ -1691,7 +1689,6 @@ static int cn_plan(lb_cn* cn) {
         }
     make(L.getrf, fA, {}, {});
     make(L.getrsL, fA.size() && Nl > 1 ? fA : std::vector<double*>{}, lB, {});
-    make(L.getrsU, uA, uB, {});
     make(L.gemmE, eA, eB, eC);
     make(L.gemmF, fA2, fB2, fC2);
     make(L.gemmG, gA, gB, gC);
