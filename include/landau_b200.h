@@ -293,7 +293,10 @@ int lb_fp64_peak(lb_ctx *ctx, double *tflops, double *ms);
  *                  M on the device from the mesh geometry.
  * lb_cn_get_mass   download the current mass values (nslots).
  * lb_cn_newton     newton_step (solver.py:103-134): assemble C at f_guess on
- *                  the device (and at f_old when C_old is NULL), residual
+ *                  the device; C_old per c_old_mode: 0 = assemble at f_old,
+ *                  1 = upload the caller's C_old, 2 = keep the device copy
+ *                  of the previous call (advance() passes one C_old to every
+ *                  iteration of a step, solver.py:171-181); residual
  *                  R = M(g - f) - dt/2 (C_g g + C_old f), solve, f_next =
  *                  f_guess + delta; rnorm = ||R|| / ||M f_old^T||.  States
  *                  are (S, n_free) host arrays, C_old / C_guess_out (S,
@@ -309,7 +312,8 @@ int lb_cn_set_mass(lb_cn *cn, const double *M_vals);
 int lb_cn_get_mass(lb_cn *cn, double *M_vals);
 int lb_cn_newton(lb_cn *cn, const double *coK, const double *coD, double eps_d, double dt,
                  const double *f_guess, const double *f_old, const double *C_old,
-                 double *f_next, double *C_guess_out, double *rnorm, double *phase_ms);
+                 int c_old_mode, double *f_next, double *C_guess_out, double *rnorm,
+                 double *phase_ms);
 int lb_cn_linear_step(lb_cn *cn, double dt, const double *C, const double *f, double *f_out);
 
 #ifdef __cplusplus

@@ -1419,6 +1419,7 @@ struct lb_cn {
   int S = 0, n = 0, nb = 0, nblk = 0, npad = 0;
   long long nnz = 0, sstride = 0;  // sstride: block-pool doubles per species
   bool has_mass = false;
+  bool co_valid = false;     // Co holds a C_old from an earlier lb_cn_newton
   cublasHandle_t blas = nullptr;
   int *indptr = nullptr, *indices = nullptr, *perm = nullptr, *flag = nullptr;
   long long* off = nullptr;  // CSR slot -> block-pool offset (species 0)
@@ -1855,8 +1856,8 @@ int lb_cn_get_mass(lb_cn* cn, double* M_vals) {
 }
 
 int lb_cn_newton(lb_cn* cn, const double* coK, const double* coD, double eps_d, double dt,
-                 const double* f_guess, const double* f_old, const double* C_old, double* f_next,
-                 double* C_guess_out, double* rnorm, double* phase_ms) {
+                 const double* f_guess, const double* f_old, const double* C_old, int c_old_mode,
+                 double* f_next, double* C_guess_out, double* rnorm, double* phase_ms) {
   if (!cn) return fail(LB_EINVAL, "null solver");
   int rc = use_ctx(cn->ctx);
   if (rc) return rc;
@@ -1886,10 +1887,17 @@ int lb_cn_newton(lb_cn* cn, const double* coK, const double* coD, double eps_d, 
   LB_CUDA(cudaMemcpyAsync(cn->f, f_old, sizeof(double) * S * n, cudaMemcpyHostToDevice, st));
   // C at the guess (and at the old state unless the caller holds it)
   if ((rc = state_issue(ctx, m, S, cp, gthr, sb, cn->g, cn->Cg, st))) return rc;
-  if (C_old) {
+  if (c_old_mode == 1) {  // the caller's C_old
+    if (!C_old) return fail(LB_EINVAL, "c_old_mode 1 needs C_old");
     LB_CUDA(cudaMemcpyAsync(cn->Co, C_old, sizeof(double) * S * cn->nnz, cudaMemcpyHostToDevice, st));
-  } else if ((rc = state_issue(ctx, m, S, cp, gthr, sb, cn->f, cn->Co, st))) {
-    return rc;
+    cn->co_valid = true;
+  } else if (c_old_mode == 2) {  // still resident from the previous call (same step)
+    if (!cn->co_valid) return fail(LB_EINVAL, "c_old_mode 2 without a resident C_old");
+  } else if (c_old_mode == 0) {  // C at f_old, assembled here
+    if ((rc = state_issue(ctx, m, S, cp, gthr, sb, cn->f, cn->Co, st))) return rc;
+    cn->co_valid = true;
+  } else {
+    return fail(LB_EINVAL, "c_old_mode must be 0, 1 or 2");
   }
   LB_CUDA(cudaEventRecord(ev[1], st));
   // residual R = M (g - f) - dt/2 (Cg g + Co f) (solver.py:87-100) and its scale

@@ -115,6 +115,7 @@ class CNSolver:
         self.handle = h
         self.dm = dm
         self._mass_key = None
+        self._c_old_ref = None  # CollisionMatrix whose values are resident as C_old
 
     def set_mass(self, M=None):
         """Mass values: the caller's matrix mapped onto the pattern, or (None)
@@ -193,7 +194,15 @@ def newton_step(f_guess, f_old, mesh, ref, params, cfg, M=None, C_old=None):
     if g.shape[1] != solver.n:
         raise ValueError(f"state has {g.shape[1]} dofs, mesh has {solver.n} free nodes")
     solver.set_mass(M)
-    Cv = None if C_old is None else solver.block_values(C_old.blocks)
+    # C_old: advance() hands the same CollisionMatrix to every Newton
+    # iteration of a step (solver.py:171-181); it is uploaded once and kept
+    # resident on the device for the following iterations
+    Cv, mode = None, 0
+    if C_old is not None:
+        if C_old is solver._c_old_ref:
+            mode = 2
+        else:
+            Cv, mode = solver.block_values(C_old.blocks), 1
     eps = getattr(cfg, "eps_d", None)
     eps = default_eps_d(mesh) if eps is None else float(eps)
     coK, coD = coupling(params)
@@ -203,10 +212,12 @@ def newton_step(f_guess, f_old, mesh, ref, params, cfg, M=None, C_old=None):
     try:
         _lib.check(solver._lib.lb_cn_newton(
             solver.handle, _lib.dptr(coK), _lib.dptr(coD), eps, float(cfg.dt), _lib.dptr(g),
-            _lib.dptr(f), _lib.dptr(Cv) if Cv is not None else None, _lib.dptr(out), None,
+            _lib.dptr(f), _lib.dptr(Cv) if Cv is not None else None, mode, _lib.dptr(out), None,
             _lib.dptr(rnorm), _lib.dptr(phase)))
     except _lib.SingularSystem as err:
+        solver._c_old_ref = None
         raise _StepFailure(-1, f"linear solve failed: {err}") from err
+    solver._c_old_ref = C_old  # held: its identity marks the resident copy
     # device phase times (ms) of the last call: assembly, residual + band
     # fill, block LU, solve + download
     LAST_PHASES_MS[:] = phase
