@@ -236,3 +236,28 @@ def test_elliptic_domain_errors_before_the_device():
     for bad in (-0.1, 1.0, 1.5, float("nan")):
         with pytest.raises(ValueError):
             pkg.elliptic_KE([bad])
+
+
+def test_bench_reference_arm_contract():
+    """`bench.py --impl reference` (the reference algorithm on the host cores)
+    prints one JSON line with the contract's keys: impl, cpu_baseline,
+    e2e with zero transfer bytes, the same metric/unit as our arm."""
+    import json
+    import subprocess
+    import sys
+
+    from conftest import ROOT
+
+    out = subprocess.run([sys.executable, "bench.py", "--impl", "reference", "--steps", "1",
+                          "--warmup", "3", "--points", "1024", "--ref-step-seconds", "0.1"],
+                         cwd=str(ROOT), capture_output=True, text=True, timeout=300)
+    assert out.returncode == 0, out.stderr[-2000:]
+    line = json.loads([l for l in out.stdout.splitlines() if l.startswith("{")][-1])
+    assert line["impl"] == "reference" and line["unit"] == "pairs/s" and line["value"] > 0
+    for k in ("metric", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better",
+              "scaling", "vs_baseline", "dtype", "data", "config"):
+        assert k in line, k
+    cb = line["cpu_baseline"]
+    assert cb["kind"] in ("port", "reference") and cb["cores"] >= 1 and cb["value"] == line["value"]
+    assert line["e2e"]["h2d_bytes_per_step"] == 0 and line["e2e"]["d2h_bytes_per_step"] == 0
+    assert line["warmup"] >= 3
