@@ -1,5 +1,8 @@
+"""End-to-end probe of the public fused_sweep at N = 2^16 (pinned inputs):
+the API call vs the bare library call with pageable / page-locked outputs,
+and the bench's call pattern (results held until the next call)."""
 import sys, time
-sys.path.insert(0, '/root/repo')
+sys.path.insert(0, str(__import__('pathlib').Path(__file__).resolve().parents[1]))
 import numpy as np, torch
 import paper_1702_08880_b200 as pkg
 from paper_1702_08880_b200 import _lib, synthetic
