@@ -324,7 +324,11 @@ __global__ void __launch_bounds__(kSymTile, sym_min_blocks(S)) lb_symsweep_kerne
 #endif
 
 template <int S>
+#ifdef LB_IB_MAXNREG
+__global__ void __maxnreg__(LB_IB_MAXNREG) lb_symsweep_ib_kernel(const SymArgs a) {
+#else
 __global__ void __launch_bounds__(kIbThreads, LB_IB_MINB) lb_symsweep_ib_kernel(const SymArgs a) {
+#endif
   constexpr int RS = rec_stride(S);
   constexpr int NW = kIbThreads / 32;
   extern __shared__ __align__(128) double lb_smem[];
