@@ -165,7 +165,10 @@ __global__ void lb_csr_gather_kernel(int nslots, int nent, int S, const int* __r
   for (int a = 0; a < S; ++a) {
     const double* ea = elem + (size_t)a * nent;
     double v = 0.0;
-    for (int k = k0; k < k1; ++k) v = fma(gw[k], ea[gidx[k]], v);
+    for (int k = k0; k < k1; ++k) {
+      LB_DCHECK(gidx[k] >= 0 && gidx[k] < nent);
+      v = fma(gw[k], ea[gidx[k]], v);
+    }
     out[(size_t)a * nslots + slot] = v;
   }
 }

@@ -118,6 +118,7 @@ __global__ void lb_band_fill_kernel(long long nnz, int S, long long sstride,
   const int a = (int)(t / nnz);
   const long long k = t % nnz;
   const double c = C ? C[t] : 0.0;
+  LB_DCHECK(off[k] >= 0 && off[k] < sstride);
   blk[a * sstride + off[k]] = __dsub_rn(Mv[k], __dmul_rn(h, c));
 }
 

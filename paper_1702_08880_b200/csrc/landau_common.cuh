@@ -9,6 +9,28 @@
 #include <cstring>
 
 #include "../../include/landau_b200.h"
+
+// Device bounds checks for debug builds (-DLB_DEBUG=1): a failed check traps
+// the kernel (the host sees a CUDA error).  Used where compute-sanitizer is
+// not available; compiled out otherwise.
+#ifndef LB_DEBUG
+#define LB_DEBUG 0
+#endif
+#if LB_DEBUG
+#include <cstdio>
+#define LB_DCHECK(cond)                                                              \
+  do {                                                                               \
+    if (!(cond)) {                                                                   \
+      printf("LB_DCHECK failed: %s (%s:%d) block %d thread %d\n", #cond, __FILE__,  \
+             __LINE__, (int)blockIdx.x, (int)threadIdx.x);                           \
+      __trap();                                                                      \
+    }                                                                                \
+  } while (0)
+#else
+#define LB_DCHECK(cond) \
+  do {                  \
+  } while (0)
+#endif
 #include "landau_pair.cuh"
 
 namespace lb {

@@ -127,6 +127,7 @@ __global__ void __launch_bounds__(kTI, kMinBlocks) lb_sweep_kernel(const SweepAr
     stage_item[s] = p_item;
     stage_j0[s] = j0;
     stage_cnt[s] = cnt;
+    LB_DCHECK(j0 >= 0 && cnt >= 1 && cnt <= TJ && j0 + cnt <= a.n);
     const uint32_t bytes = (uint32_t)cnt * RS * sizeof(double);
     mbar_expect_tx(&full[s], bytes);
     bulk_g2s(lb_smem + s * (TJ * RS), a.rec + (size_t)j0 * RS, bytes, &full[s]);

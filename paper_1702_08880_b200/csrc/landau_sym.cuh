@@ -156,6 +156,7 @@ struct SymProducer {
     stage_item[s] = p_item;
     stage_d[s] = p_d;
     const int J = (I + p_d) % a.nt;
+    LB_DCHECK(I >= a.row0 && I < a.row1 && p_d >= 0 && p_d <= sym_h(I, a.nt) && J >= 0 && J < a.nt);
     const uint32_t bytes = kSymTile * RS * sizeof(double);
     mbar_expect_tx(&full[s], bytes);
     bulk_g2s(smem + s * (kSymTile * RS), a.rec + (size_t)J * kSymTile * RS, bytes, &full[s]);
@@ -292,6 +293,7 @@ __global__ void __launch_bounds__(kSymTile, sym_min_blocks(S)) lb_symsweep_kerne
 #pragma unroll
             for (int q = 0; q < 5; ++q) dst[b * 5 + q] = jacc[b][q];
           __syncthreads();
+          LB_DCHECK(d >= 1 && d <= a.hmax);
           double* out = a.jside + ((size_t)(I - a.row0) * a.hmax + (d - 1)) * (5 * S) * kSymTile +
                         jb * 32;
           for (int v = tid; v < 32 * 5 * S; v += kSymTile) {
@@ -363,6 +365,7 @@ __global__ void __launch_bounds__(kIbThreads, LB_IB_MINB) lb_symsweep_ib_kernel(
   auto flush_iside = [&]() {
 #pragma unroll
     for (int ib = 0; ib < 2; ++ib) {
+      LB_DCHECK(pidx(ib) < kSymTile && I >= a.row0 && I < a.row1);
       double* dst = a.iside + ((size_t)(I - a.row0) * a.nseg + (cur % a.nseg)) * (5 * S) * kSymTile + pidx(ib);
 #pragma unroll
       for (int b = 0; b < S; ++b)
@@ -491,6 +494,7 @@ __global__ void __launch_bounds__(kIbThreads, LB_IB_MINB) lb_symsweep_ib_kernel(
 #pragma unroll
           for (int q = 0; q < 5; ++q) dst[b * 5 + q] = jacc[b][q];
         __syncthreads();
+        LB_DCHECK(d >= 1 && d <= a.hmax);
         double* out = a.jside + ((size_t)(I - a.row0) * a.hmax + (d - 1)) * (5 * S) * kSymTile + jb * 32;
         for (int v = tid; v < 32 * 5 * S; v += kIbThreads) {
           const int c = v >> 5, jj = v & 31;
@@ -561,6 +565,7 @@ __global__ void lb_symreduce_kernel(const double* __restrict__ iside, const doub
       const int I = I0 + g;
       on[g] = I < row1 && d >= 1 && d <= sym_h(I, nt);
       if (on[g]) {
+        LB_DCHECK(d >= 1 && d <= hmax);
         const double* src = jside + ((size_t)(I - row0) * hmax + (d - 1)) * (5 * S) * kSymTile + t;
 #pragma unroll
         for (int c = 0; c < 5 * S; ++c) x[g][c] = src[(size_t)c * kSymTile];
