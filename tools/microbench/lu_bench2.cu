@@ -74,8 +74,27 @@ int main() {
         cudaEventSynchronize(e1);
         cudaEventElapsedTime(&tv, e0, e1);
       }
-      printf("n=%4d batch=%4d: getrf %7.3f  getri %7.3f  getrs(nrhs=n) %7.3f  gemm %7.3f  gemv %7.3f ms\n", n,
-             batch, tf, ti, ts, tg, tv);
+      // no pivoting: getrf with a null pivot array + two triangular solves
+      float tfn = 0, tt = 0;
+      for (int rep = 0; rep < 3; ++rep) {
+        cudaMemcpy(A, A0, nn * batch * 8, cudaMemcpyDeviceToDevice);
+        cudaMemcpy(B, A0, nn * batch * 8, cudaMemcpyDeviceToDevice);
+        cudaEventRecord(e0);
+        cublasDgetrfBatched(bl, n, dA, n, nullptr, info, batch);
+        cudaEventRecord(e1);
+        cudaEventSynchronize(e1);
+        cudaEventElapsedTime(&tfn, e0, e1);
+        cudaEventRecord(e0);
+        cublasDtrsmBatched(bl, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N, CUBLAS_DIAG_UNIT, n, n,
+                           &one, dA, n, dB, n, batch);
+        cublasDtrsmBatched(bl, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_UPPER, CUBLAS_OP_N, CUBLAS_DIAG_NON_UNIT, n,
+                           n, &one, dA, n, dB, n, batch);
+        cudaEventRecord(e1);
+        cudaEventSynchronize(e1);
+        cudaEventElapsedTime(&tt, e0, e1);
+      }
+      printf("n=%4d batch=%4d: getrf %7.3f  getri %7.3f  getrs(nrhs=n) %7.3f  gemm %7.3f  gemv %7.3f ms"
+             "  | no-pivot getrf %7.3f  2x trsm(nrhs=n) %7.3f ms\n", n, batch, tf, ti, ts, tg, tv, tfn, tt);
       cudaFree(A); cudaFree(A0); cudaFree(C); cudaFree(B); cudaFree(piv); cudaFree(info);
       cudaFree(dA); cudaFree(dC); cudaFree(dB);
     }
