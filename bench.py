@@ -343,6 +343,10 @@ def ours_arm(args):
                "sample": f"{k} evenly spaced outer points x all {N} inner points "
                          f"(oracle/ C restatement of kernel.py:306-493, OpenMP, {t:.1f} s)"}
         parity = O.per_component_scaled_error(K[idx], D[idx], Kr, Dr)
+        # one core as well (the survey's per-core reference rate)
+        k1, run1 = cpu_sample(wl, min(2.0, args.cpu_seconds / 5), 1, min_outer=16)
+        t1, *_ = run1(k1)
+        cpu["single_core_value"] = k1 * N / t1
 
     check = None
     if args.check:  # every rank's own rows vs the oracle on a sample (functional check)
