@@ -304,7 +304,11 @@ int lb_fp64_peak(lb_ctx *ctx, double *tflops, double *ms);
  *                  phase_ms (4, optional): assembly, residual+fill, factor,
  *                  solve+download.
  * lb_cn_linear_step linear_cn_step (solver.py:137-150): (M - dt/2 C) f+ =
- *                  (M + dt/2 C) f with C (S, nslots) held fixed. */
+ *                  (M + dt/2 C) f with C (S, nslots) held fixed.
+ * Every solve first uses the block LU WITHOUT pivoting (cheaper) and accepts
+ * it only if the relative backward error is <= 1e-12; otherwise the solver
+ * refactorises with partial pivoting inside the diagonal blocks, and keeps
+ * pivoting for later calls (LB_CN_PIVOT=1 in the environment: always). */
 int lb_cn_create(lb_ctx *ctx, const lb_mesh *mesh, int S, int n, const int *indptr,
                  const int *indices, const int *perm, int nb, lb_cn **out);
 int lb_cn_destroy(lb_cn *cn);
@@ -315,6 +319,10 @@ int lb_cn_newton(lb_cn *cn, const double *coK, const double *coD, double eps_d, 
                  int c_old_mode, double *f_next, double *C_guess_out, double *rnorm,
                  double *phase_ms);
 int lb_cn_linear_step(lb_cn *cn, double dt, const double *C, const double *f, double *f_out);
+/* Linear-solve diagnostics: relative backward error ||(M - dt/2 C) x - b|| /
+ * ||b|| of the last solve, how often the unpivoted block LU was rejected
+ * (then refactorised with pivoting), and whether the solver now pivots. */
+int lb_cn_stats(lb_cn *cn, double *last_rel_residual, int *fallbacks, int *pivoting);
 
 #ifdef __cplusplus
 }

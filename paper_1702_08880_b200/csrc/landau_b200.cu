@@ -1427,8 +1427,13 @@ struct lb_cn {
   double* blk = nullptr;     // block pool: S * sstride
   long long zero_len = 0;    // level-0 part of the pool (zeroed per fill)
   std::vector<CnLevel> lv;   // levels 0 .. L (the last has N = 1)
-  cudaGraphExec_t factor_graph = nullptr, solve_graph = nullptr;  // captured on first use
+  cudaGraphExec_t factor_graph[2] = {}, solve_graph[2] = {};  // [pivoted], captured on first use
   bool graph_failed = false;
+  // unpivoted block LU first (cheaper), accepted after a backward-error
+  // check; one failed check makes this solver pivot from then on
+  bool pivot = false;
+  int fallbacks = 0;
+  double last_rel_residual = 0.0;
   void* blas_ws = nullptr;   // cuBLAS workspace (set explicitly so calls can be captured)
   double *g = nullptr, *f = nullptr, *d = nullptr, *R = nullptr, *Mf = nullptr, *x = nullptr,
          *out = nullptr, *Co = nullptr, *Cg = nullptr, *red = nullptr;
@@ -1459,20 +1464,31 @@ static bool cn_small(const lb_cn* cn) {
   return cn->nb <= kSmallNb && !force_blas;
 }
 
-static int cn_factor_issue(lb_cn* cn, cudaStream_t st) {
+static int cn_factor_issue(lb_cn* cn, cudaStream_t st, bool pivot) {
   const int nb = cn->nb;
   const double one = 1.0, mone = -1.0, zero = 0.0;
   int hinfo = 0;
   LB_BLAS(cublasSetStream(cn->blas, st));
   for (const CnLevel& L : cn->lv) {
     if (L.getrf.count)
-      LB_BLAS(cublasDgetrfBatched(cn->blas, nb, L.getrf.A, nb, L.piv, L.info, L.getrf.count));
+      LB_BLAS(cublasDgetrfBatched(cn->blas, nb, L.getrf.A, nb, pivot ? L.piv : nullptr, L.info,
+                                  L.getrf.count));
     // L_l[k] and U_l[k] are adjacent in the pool, so [L U] is one nb x 2nb
     // column-major right-hand side: P = D^-1 [L U] in a single call (the
     // last odd row's U slot is unused scratch when it has no right neighbour)
-    if (L.getrsL.count)
-      LB_BLAS(cublasDgetrsBatched(cn->blas, CUBLAS_OP_N, nb, 2 * nb, L.getrsL.A, nb, L.piv, L.getrsL.B,
-                                  nb, &hinfo, L.getrsL.count));
+    if (L.getrsL.count) {
+      if (pivot) {
+        LB_BLAS(cublasDgetrsBatched(cn->blas, CUBLAS_OP_N, nb, 2 * nb, L.getrsL.A, nb, L.piv, L.getrsL.B,
+                                    nb, &hinfo, L.getrsL.count));
+      } else {
+        LB_BLAS(cublasDtrsmBatched(cn->blas, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N,
+                                   CUBLAS_DIAG_UNIT, nb, 2 * nb, &one, L.getrsL.A, nb, L.getrsL.B, nb,
+                                   L.getrsL.count));
+        LB_BLAS(cublasDtrsmBatched(cn->blas, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_UPPER, CUBLAS_OP_N,
+                                   CUBLAS_DIAG_NON_UNIT, nb, 2 * nb, &one, L.getrsL.A, nb, L.getrsL.B, nb,
+                                   L.getrsL.count));
+      }
+    }
     const CnBatch* acc[2] = {&L.gemmE, &L.gemmF};
     for (const CnBatch* b : acc)
       if (b->count)
@@ -1516,7 +1532,8 @@ static int cn_graph_run(cudaGraphExec_t& exec, bool& failed, cudaStream_t st, F&
 }
 
 static int cn_factor(lb_cn* cn, cudaStream_t st) {
-  int rc = cn_graph_run(cn->factor_graph, cn->graph_failed, st, [&] { return cn_factor_issue(cn, st); });
+  const bool pv = cn->pivot;
+  int rc = cn_graph_run(cn->factor_graph[pv], cn->graph_failed, st, [&] { return cn_factor_issue(cn, st, pv); });
   if (rc) return rc;
   // zero pivots anywhere -> singular (splu's RuntimeError, solver.py:127-129)
   std::vector<std::vector<int>> info(cn->lv.size());
@@ -1537,7 +1554,7 @@ static int cn_factor(lb_cn* cn, cudaStream_t st) {
 
 // x (S x npad, band order) holds the right-hand side on entry, the solution
 // on exit.
-static int cn_solve_issue(lb_cn* cn, cudaStream_t st) {
+static int cn_solve_issue(lb_cn* cn, cudaStream_t st, bool pivot) {
   const int nb = cn->nb;
   const double one = 1.0, mone = -1.0;
   int hinfo = 0;
@@ -1545,12 +1562,18 @@ static int cn_solve_issue(lb_cn* cn, cudaStream_t st) {
   const bool small = cn_small(cn);
   for (const CnLevel& L : cn->lv) {
     if (small && L.solveY.count) {
-      lb_small_solve_kernel<<<L.solveY.count, kSmallThreads, small_solve_smem_bytes(nb), st>>>(nb, L.solveY.count, L.getrf.A,
-                                                                              L.piv, L.solveY.B);
+      lb_small_solve_kernel<<<L.solveY.count, kSmallThreads, small_solve_smem_bytes(nb), st>>>(
+          nb, L.solveY.count, L.getrf.A, pivot ? L.piv : nullptr, L.solveY.B);
       LB_CUDA(cudaGetLastError());
-    } else if (L.solveY.count) {
+    } else if (L.solveY.count && pivot) {
       LB_BLAS(cublasDgetrsBatched(cn->blas, CUBLAS_OP_N, nb, 1, L.getrf.A, nb, L.piv, L.solveY.B, nb, &hinfo,
                                   L.solveY.count));
+    } else if (L.solveY.count) {
+      LB_BLAS(cublasDtrsmBatched(cn->blas, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N,
+                                 CUBLAS_DIAG_UNIT, nb, 1, &one, L.getrf.A, nb, L.solveY.B, nb, L.solveY.count));
+      LB_BLAS(cublasDtrsmBatched(cn->blas, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_UPPER, CUBLAS_OP_N,
+                                 CUBLAS_DIAG_NON_UNIT, nb, 1, &one, L.getrf.A, nb, L.solveY.B, nb,
+                                 L.solveY.count));
     }
     const CnBatch* fw[2] = {&L.fwdL, &L.fwdU};
     for (const CnBatch* b : fw)
@@ -1570,7 +1593,8 @@ static int cn_solve_issue(lb_cn* cn, cudaStream_t st) {
 }
 
 static int cn_solve(lb_cn* cn, cudaStream_t st) {
-  return cn_graph_run(cn->solve_graph, cn->graph_failed, st, [&] { return cn_solve_issue(cn, st); });
+  const bool pv = cn->pivot;
+  return cn_graph_run(cn->solve_graph[pv], cn->graph_failed, st, [&] { return cn_solve_issue(cn, st, pv); });
 }
 
 // level-0 blocks = M - h C (C null: M), padded diagonal = identity
@@ -1592,6 +1616,60 @@ static int cn_fill(lb_cn* cn, const double* C, double h, cudaStream_t st) {
 static void cn_sumsq(lb_cn* cn, const double* x, long long len, cudaStream_t st, int slot) {
   lb_sumsq_kernel<<<1, 1024, 0, st>>>(len, x, cn->red + slot);
 }
+
+// Relative backward error accepted from the unpivoted factorisation (the
+// pivoted one reaches ~1e-15 on the test systems); LB_CN_PIVOT=1 pivots always.
+constexpr double kCnAcceptResidual = 1e-12;
+
+// (M - h C) x = bsign * b for the S species (b: S x n, original order):
+// fill, factor, solve, out = base + x (x alone when base is null), x also in
+// cn->d; then the backward-error check e = (M - h C) x - bsign b.  The
+// unpivoted LU is accepted when ||e|| <= kCnAcceptResidual ||b||; otherwise
+// the solver switches to pivoting (sticky) and redoes the solve.  Leaves
+// cn->red[2] = ||e||^2, cn->red[3] = ||b||^2; *bad = non-finite x.
+static int cn_guarded_solve(lb_cn* cn, const double* C, double h, const double* b, double bsign,
+                            const double* base, cudaStream_t st, cudaEvent_t ev_fill, cudaEvent_t ev_factor,
+                            int* bad) {
+  static const bool force_pivot = std::getenv("LB_CN_PIVOT") != nullptr;
+  if (force_pivot) cn->pivot = true;
+  const int S = cn->S, n = cn->n, nS = S * n;
+  int rc;
+  for (int attempt = 0; attempt < 2; ++attempt) {
+    if ((rc = cn_fill(cn, C, h, st))) return rc;
+    if (ev_fill && attempt == 0) LB_CUDA(cudaEventRecord(ev_fill, st));
+    if ((rc = cn_factor(cn, st))) {
+      if (rc == LB_ESINGULAR && !cn->pivot) {  // a zero pivot without pivoting: retry pivoted
+        cn->pivot = true;
+        ++cn->fallbacks;
+        continue;
+      }
+      return rc;
+    }
+    if (ev_factor && attempt == 0) LB_CUDA(cudaEventRecord(ev_factor, st));
+    lb_perm_gather_kernel<<<(S * cn->npad + 255) / 256, 256, 0, st>>>(n, cn->npad, S, cn->perm, b, bsign,
+                                                                     cn->x);
+    if ((rc = cn_solve(cn, st))) return rc;
+    LB_CUDA(cudaMemsetAsync(cn->flag, 0, sizeof(int), st));
+    lb_perm_update_kernel<<<(nS + 255) / 256, 256, 0, st>>>(n, cn->npad, S, cn->perm, base, cn->x, cn->out,
+                                                            cn->d, cn->flag);
+    lb_cn_check_kernel<<<(nS + 127) / 128, 128, 0, st>>>(n, S, cn->indptr, cn->indices, cn->nnz, cn->Mv, C, h,
+                                                         cn->d, b, bsign, cn->Mf);
+    cn_sumsq(cn, cn->Mf, nS, st, 2);
+    cn_sumsq(cn, b, nS, st, 3);
+    LB_CUDA(cudaGetLastError());
+    double red[2];
+    LB_CUDA(cudaMemcpyAsync(red, cn->red + 2, sizeof(double) * 2, cudaMemcpyDeviceToHost, st));
+    LB_CUDA(cudaMemcpyAsync(bad, cn->flag, sizeof(int), cudaMemcpyDeviceToHost, st));
+    LB_CUDA(cudaStreamSynchronize(st));
+    const double rel = red[1] > 0.0 ? std::sqrt(red[0] / red[1]) : std::sqrt(red[0]);
+    cn->last_rel_residual = rel;
+    if (cn->pivot || (!*bad && rel <= kCnAcceptResidual)) return LB_OK;
+    cn->pivot = true;  // the unpivoted factorisation is not good enough here
+    ++cn->fallbacks;
+  }
+  return LB_OK;
+}
+
 
 // Build the level structure and every batched call's pointer arrays.
 static int cn_plan(lb_cn* cn) {
@@ -1803,8 +1881,10 @@ int lb_cn_destroy(lb_cn* cn) {
   if (!cn) return LB_OK;
   cudaSetDevice(cn->ctx->device);
   cudaStreamSynchronize(cn->ctx->stream);
-  if (cn->factor_graph) cudaGraphExecDestroy(cn->factor_graph);
-  if (cn->solve_graph) cudaGraphExecDestroy(cn->solve_graph);
+  for (int k = 0; k < 2; ++k) {
+    if (cn->factor_graph[k]) cudaGraphExecDestroy(cn->factor_graph[k]);
+    if (cn->solve_graph[k]) cudaGraphExecDestroy(cn->solve_graph[k]);
+  }
   if (cn->blas) cublasDestroy(cn->blas);
   for (void* p : cn->allocs) cudaFree(p);
   delete cn;
@@ -1911,22 +1991,11 @@ int lb_cn_newton(lb_cn* cn, const double* coK, const double* coD, double eps_d, 
   cn_sumsq(cn, cn->Mf, nS, st, 1);
   LB_CUDA(cudaGetLastError());
   // (M - dt/2 Cg) delta = -R per species (solver.py:124-133)
-  if ((rc = cn_fill(cn, cn->Cg, h, st))) return rc;
-  LB_CUDA(cudaEventRecord(ev[2], st));
-  if ((rc = cn_factor(cn, st))) return rc;
-  LB_CUDA(cudaEventRecord(ev[3], st));
-  lb_perm_gather_kernel<<<(S * cn->npad + 255) / 256, 256, 0, st>>>(n, cn->npad, S, cn->perm, cn->R, -1.0,
-                                                                   cn->x);
-  if ((rc = cn_solve(cn, st))) return rc;
-  LB_CUDA(cudaMemsetAsync(cn->flag, 0, sizeof(int), st));
-  lb_perm_update_kernel<<<(nS + 255) / 256, 256, 0, st>>>(n, cn->npad, S, cn->perm, cn->g, cn->x, cn->out,
-                                                          cn->flag);
-  LB_CUDA(cudaGetLastError());
-  double red[2];
   int bad = 0;
+  if ((rc = cn_guarded_solve(cn, cn->Cg, h, cn->R, -1.0, cn->g, st, ev[2], ev[3], &bad))) return rc;
+  double red[2];
   LB_CUDA(cudaMemcpyAsync(f_next, cn->out, sizeof(double) * nS, cudaMemcpyDeviceToHost, st));
   LB_CUDA(cudaMemcpyAsync(red, cn->red, sizeof(double) * 2, cudaMemcpyDeviceToHost, st));
-  LB_CUDA(cudaMemcpyAsync(&bad, cn->flag, sizeof(int), cudaMemcpyDeviceToHost, st));
   if (C_guess_out)
     LB_CUDA(cudaMemcpyAsync(C_guess_out, cn->Cg, sizeof(double) * S * cn->nnz, cudaMemcpyDeviceToHost, st));
   LB_CUDA(cudaEventRecord(ev[4], st));
@@ -1944,6 +2013,14 @@ int lb_cn_newton(lb_cn* cn, const double* coK, const double* coD, double eps_d, 
   return LB_OK;
 }
 
+int lb_cn_stats(lb_cn* cn, double* last_rel_residual, int* fallbacks, int* pivoting) {
+  if (!cn) return fail(LB_EINVAL, "null solver");
+  if (last_rel_residual) *last_rel_residual = cn->last_rel_residual;
+  if (fallbacks) *fallbacks = cn->fallbacks;
+  if (pivoting) *pivoting = cn->pivot ? 1 : 0;
+  return LB_OK;
+}
+
 int lb_cn_linear_step(lb_cn* cn, double dt, const double* C, const double* f, double* f_out) {
   if (!cn) return fail(LB_EINVAL, "null solver");
   int rc = use_ctx(cn->ctx);
@@ -1958,18 +2035,9 @@ int lb_cn_linear_step(lb_cn* cn, double dt, const double* C, const double* f, do
   // rhs = (M + dt/2 C) f (solver.py:146), then (M - dt/2 C) f+ = rhs
   lb_cn_rhs_kernel<<<(nS + 127) / 128, 128, 0, st>>>(n, S, cn->indptr, cn->indices, cn->nnz, cn->Mv, cn->Cg,
                                                      cn->f, h, cn->R);
-  if ((rc = cn_fill(cn, cn->Cg, h, st))) return rc;
-  if ((rc = cn_factor(cn, st))) return rc;
-  lb_perm_gather_kernel<<<(S * cn->npad + 255) / 256, 256, 0, st>>>(n, cn->npad, S, cn->perm, cn->R, 1.0,
-                                                                   cn->x);
-  if ((rc = cn_solve(cn, st))) return rc;
-  LB_CUDA(cudaMemsetAsync(cn->flag, 0, sizeof(int), st));
-  lb_perm_update_kernel<<<(nS + 255) / 256, 256, 0, st>>>(n, cn->npad, S, cn->perm, nullptr, cn->x, cn->out,
-                                                          cn->flag);
-  LB_CUDA(cudaGetLastError());
   int bad = 0;
+  if ((rc = cn_guarded_solve(cn, cn->Cg, h, cn->R, 1.0, nullptr, st, nullptr, nullptr, &bad))) return rc;
   LB_CUDA(cudaMemcpyAsync(f_out, cn->out, sizeof(double) * nS, cudaMemcpyDeviceToHost, st));
-  LB_CUDA(cudaMemcpyAsync(&bad, cn->flag, sizeof(int), cudaMemcpyDeviceToHost, st));
   LB_CUDA(cudaStreamSynchronize(st));
   if (bad) return fail(LB_ESINGULAR, "non-finite solution");
   return LB_OK;

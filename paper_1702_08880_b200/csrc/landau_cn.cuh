@@ -137,7 +137,8 @@ __global__ void lb_perm_gather_kernel(int n, int npad, int S, const int* __restr
 // out[a][perm[p]] = base[a][perm[p]] + x[a][p]  (f_next = guess + delta)
 __global__ void lb_perm_update_kernel(int n, int npad, int S, const int* __restrict__ perm,
                                       const double* __restrict__ base, const double* __restrict__ x,
-                                      double* __restrict__ out, int* __restrict__ nonfinite) {
+                                      double* __restrict__ out, double* __restrict__ dx_out,
+                                      int* __restrict__ nonfinite) {
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= S * n) return;
   const int a = t / n, p = t % n;
@@ -145,6 +146,26 @@ __global__ void lb_perm_update_kernel(int n, int npad, int S, const int* __restr
   if (!isfinite(dx)) atomicOr(nonfinite, 1);
   const size_t o = (size_t)a * n + perm[p];
   out[o] = base ? __dadd_rn(base[o], dx) : dx;
+  if (dx_out) dx_out[o] = dx;
+}
+
+// Backward-error check of a solve of (M - h C_a) x_a = b_a (original order):
+// e = (M - h C) x - b, written for a deterministic sum of squares.  With the
+// unpivoted block LU the solver accepts the result only when ||e|| is at the
+// level a pivoted factorisation reaches, else it refactorises with pivoting.
+__global__ void lb_cn_check_kernel(int n, int S, const int* __restrict__ indptr,
+                                   const int* __restrict__ indices, long long nnz,
+                                   const double* __restrict__ Mv, const double* __restrict__ C, double h,
+                                   const double* __restrict__ x, const double* __restrict__ b, double bsign,
+                                   double* __restrict__ e) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n * S) return;
+  const int a = t / n, row = t % n;
+  const double* Ca = C + (size_t)a * nnz;
+  const double* xa = x + (size_t)a * n;
+  double s = 0.0;
+  for (int k = indptr[row]; k < indptr[row + 1]; ++k) s = fma(Mv[k] - h * Ca[k], xa[indices[k]], s);
+  e[t] = s - bsign * b[t];
 }
 
 }  // namespace lb
@@ -173,12 +194,12 @@ __global__ void __launch_bounds__(kSmallThreads) lb_small_solve_kernel(int nb, i
   const int w = blockIdx.x, tid = threadIdx.x;
   if (w >= count) return;
   const double* Ag = D[w];
-  const int* piv = piv_all + (size_t)w * nb;
+  const int* piv = piv_all ? piv_all + (size_t)w * nb : nullptr;
   double* xg = V[w];
   for (int t = tid; t < nb * nb; t += kSmallThreads) A[t] = Ag[t];
   for (int t = tid; t < nb; t += kSmallThreads) x[t] = xg[t];
   __syncthreads();
-  if (tid == 0)
+  if (tid == 0 && piv_all)  // no pivots: factors of the unpivoted LU
     for (int k = 0; k < nb; ++k) {
       const int p = piv[k] - 1;
       if (p != k) {

@@ -134,6 +134,15 @@ class CNSolver:
         _lib.check(self._lib.lb_cn_get_mass(self.handle, _lib.dptr(out)))
         return out
 
+    def stats(self) -> dict:
+        """Last solve's relative backward error, rejected unpivoted
+        factorisations, and whether the solver pivots now (lb_cn_stats)."""
+        import ctypes as C
+
+        r, nf, pv = C.c_double(), C.c_int(), C.c_int()
+        _lib.check(self._lib.lb_cn_stats(self.handle, C.byref(r), C.byref(nf), C.byref(pv)))
+        return {"rel_residual": r.value, "fallbacks": nf.value, "pivoting": bool(pv.value)}
+
     def block_values(self, blocks) -> np.ndarray:
         return np.stack([pattern_values(b, self.indptr, self.indices, self.n) for b in blocks])
 

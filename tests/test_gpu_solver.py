@@ -217,3 +217,35 @@ def test_cfg1_advance_ten_steps(gpu):
         assert np.all(np.abs(moms - ref_m)[[0, 1, 2]] <= 1e-10 * np.abs(ref_m[[0, 1, 2]]))
     print("cfg1 10-step trajectory: worst state error", worst)
     assert worst <= TOL
+
+
+def test_unpivoted_lu_falls_back_to_pivoting(gpu):
+    """The solver factorises without pivoting first and accepts the result
+    only after a backward-error check; a system whose first diagonal entry
+    is exactly zero (nonsingular, but not factorable without pivoting) must
+    fall back to the pivoted block LU and still equal SuperLU."""
+    from paper_1702_08880_b200 import solver as S
+
+    g = golden("cfg1")
+    M = csr_from(g, "M")
+    C0 = blocks_from(g, "C")[0]
+    dt = float(g["dt"])
+    # the first row of the first eliminated (odd) diagonal block in band
+    # order: its pivot is the raw matrix entry, so zero it
+    pat = (abs(M) + abs(C0)).tocsr()
+    pat.sort_indices()
+    perm, bw = S.band_order(pat.indptr, pat.indices, pat.shape[0])
+    node = int(perm[max(bw, 1)])
+    M = M.tolil()
+    M[node, node] = 0.5 * dt * C0[node, node]  # (M - dt/2 C)[node, node] == 0
+    M = M.tocsr()
+    C = SimpleNamespace(blocks=[C0])
+    f0 = g["coeffs"]
+    out = gpu.linear_cn_step(M, C, dt, f0)
+    A = (M - 0.5 * dt * C0).tocsc()
+    assert A[node, node] == 0.0
+    want = spla.splu(A).solve((M + 0.5 * dt * C0) @ f0[0])
+    assert _scaled(out[0], want) <= TOL
+    stats = [s.stats() for s in S._LINEAR.values()]
+    assert any(st["fallbacks"] >= 1 and st["pivoting"] for st in stats), stats
+    assert min(st["rel_residual"] for st in stats) < 1e-12

@@ -78,7 +78,8 @@ def main():
         print(f"{name}: n_free={s.n} S={f.shape[0]} bandwidth={s.bandwidth} blocks={-(-s.n // s.nb)}  "
               f"device newton_step {min(td) * 1e3:.2f} ms  host (device assembly + splu) "
               f"{min(th) * 1e3:.2f} ms  x{min(th) / min(td):.1f}  rel diff {err:.1e}  rnorm {rnorm:.3e}"
-              f"  device phases (assemble, residual+fill, LU, solve) {np.round(ph, 2).tolist()} ms")
+              f"  device phases (assemble, residual+fill, LU, solve) {np.round(ph, 2).tolist()} ms"
+              f"  solver {s.stats()}")
 
 
 if __name__ == "__main__":
