@@ -273,14 +273,8 @@ def case_cfg1_advance():
          masses=np.array([s.mass for s in sp_]), Wm=moment_matrix(mesh, ref))
 
 
-def case_cfg3():
-    """BASELINE config 3, reference-native reading (SURVEY 8(d)): Q2 on an
-    8x16 base (L=5) refined 3 rounds toward the origin and the thermal shell
-    |v| ~ 1 (hanging nodes), bi-Maxwellian electrons (T_par = 1.5 T_perp)
-    plus Maxwellian ions built directly as a StateVector; D/K, the operator,
-    and one frozen-coefficient Newton step (solver.py:103-134)."""
-    from axlandau.solver import StepConfig, newton_step
-
+def _cfg3_setup():
+    """Config 3's refined mesh and bi-Maxwellian state (see case_cfg3)."""
     domain = ax.DomainSpec(L=5.0)
     ref = ax.build_reference_element()
     mesh = ax.cartesian_mesh(domain, 8, 16)
@@ -299,6 +293,18 @@ def case_cfg3():
     fe = 0.5 * (math.pi ** 1.5 * s_perp * math.sqrt(s_par)) ** -1 * np.exp(-r * r / s_perp - z * z / s_par)
     fi = ax.physics.maxwellian_values(sp_[1], r, z)
     state = ax.StateVector(np.stack([fe, fi]))
+    return mesh, ref, sp_, state
+
+
+def case_cfg3():
+    """BASELINE config 3, reference-native reading (SURVEY 8(d)): Q2 on an
+    8x16 base (L=5) refined 3 rounds toward the origin and the thermal shell
+    |v| ~ 1 (hanging nodes), bi-Maxwellian electrons (T_par = 1.5 T_perp)
+    plus Maxwellian ions built directly as a StateVector; D/K, the operator,
+    and one frozen-coefficient Newton step (solver.py:103-134)."""
+    from axlandau.solver import StepConfig, newton_step
+
+    mesh, ref, sp_, state = _cfg3_setup()
     data = ax.sample_state(mesh, ref, state)
     params = ax.collision_params(sp_)
     eps_d = ax.assembly.default_eps_d(mesh)
@@ -317,6 +323,30 @@ def case_cfg3():
          Wm=moment_matrix(mesh, ref),
          moms0=np.stack([moms0.n, moms0.p_z, moms0.E, moms0.q_z]),
          moms1=np.stack([moms1.n, moms1.p_z, moms1.E, moms1.q_z]))
+
+
+def case_cfg3_advance():
+    """Config 3 time integration (hanging nodes, two species): the reference's
+    advance() for 3 steps of dt = 0.1, Newton to 1e-12 (at most 3 iterations);
+    per-step states, moments and residual histories."""
+    from axlandau.solver import StepConfig, advance
+
+    mesh, ref, sp_, state = _cfg3_setup()
+    params = ax.collision_params(sp_)
+    cfg = StepConfig(dt=0.1, newton_tol=1e-12, max_newton=3)
+    hist = []
+
+    def record(step, t, st, moms, info):
+        hist.append(info["residuals"] + [np.nan] * (cfg.max_newton - len(info["residuals"])))
+
+    traj = advance(mesh, ref, sp_, state, 0.3, cfg, params=params, callback=record)
+    states = np.stack([s.coeffs for _, s, _ in traj])
+    moms = np.stack([np.stack([m.n, m.p_z, m.E, m.q_z]) for _, _, m in traj])
+    M = ax.mass_matrix(mesh, ref)
+    save("cfg3adv", **mesh_parts(mesh, ref), **params_parts(params), **csr_parts("M", M),
+         states=states, moms=moms, residuals=np.array(hist), dt=np.float64(cfg.dt),
+         newton_tol=np.float64(cfg.newton_tol), max_newton=np.int64(cfg.max_newton),
+         masses=np.array([s.mass for s in sp_]), Wm=moment_matrix(mesh, ref))
 
 
 def case_cfg4_species():
@@ -440,7 +470,7 @@ def main():
     which = set(sys.argv[1:])
     cases = {"pairs": case_pairs, "sweep_small": case_sweep_small, "cfg1": case_cfg1,
              "hanging": case_hanging, "cons": case_cons, "cfg2": case_cfg2,
-             "cfg3": case_cfg3, "cfg1adv": case_cfg1_advance, "cfg4s": case_cfg4_species, "cfg2m": case_cfg2_meshes,
+             "cfg3": case_cfg3, "cfg1adv": case_cfg1_advance, "cfg3adv": case_cfg3_advance, "cfg4s": case_cfg4_species, "cfg2m": case_cfg2_meshes,
              "cfg4m": case_cfg4_meshes,
              "cfg5_4096": lambda: case_cfg5(4096),
              "cfg5_65536": lambda: case_cfg5(65536, n_sub=192)}

@@ -183,20 +183,22 @@ def test_config4_mesh_newton_step_matches_splu(gpu, nr, nz):
         assert err <= TOL
 
 
-def test_cfg1_advance_ten_steps(gpu):
-    """BASELINE config 1 time integration: the reference's advance() loop
-    (solver.py:153-200: C_old at each step, up to max_newton frozen-
-    coefficient iterations, early exit below newton_tol) run with the device
-    operator and device Newton step reproduces the reference trajectory --
-    every step's state to 1e-10 scaled, density / momentum / energy to 1e-10
-    relative, and the residual histories."""
-    g = golden("cfg1adv")
+@pytest.mark.parametrize("case", ["cfg1adv", "cfg3adv"])
+def test_advance_trajectory(gpu, case):
+    """BASELINE config 1 (10 steps) and config 3 (3 steps; hanging nodes, two
+    species) time integration: the reference's advance() loop (solver.py:
+    153-200: C_old at each step, up to max_newton frozen-coefficient
+    iterations, early exit below newton_tol) run with the device operator and
+    device Newton step reproduces the reference trajectory -- every step's
+    state to 1e-10 scaled, density / momentum / energy to 1e-10 relative, and
+    the residual histories."""
+    g = golden(case)
     mesh, ref, params = mesh_from(g), ref_from(g), params_from(g)
     M = csr_from(g, "M")
     cfg = SimpleNamespace(dt=float(g["dt"]), eps_d=None)
     tol, max_newton = float(g["newton_tol"]), int(g["max_newton"])
     states, moms_ref, res_ref = g["states"], g["moms"], g["residuals"]
-    Wm, m = g["Wm"], float(g["masses"][0])
+    Wm, masses = g["Wm"], g["masses"]
     state = states[0]
     worst = 0.0
     for step in range(1, states.shape[0]):
@@ -212,10 +214,13 @@ def test_cfg1_advance_ten_steps(gpu):
         want = res_ref[step - 1][~np.isnan(res_ref[step - 1])]
         assert len(res) == len(want)
         assert np.allclose(res, want, rtol=1e-6, atol=0.0)
-        moms = Wm @ state[0] * np.array([1.0, m, m, m])
-        ref_m = moms_ref[step][:, 0]
-        assert np.all(np.abs(moms - ref_m)[[0, 1, 2]] <= 1e-10 * np.abs(ref_m[[0, 1, 2]]))
-    print("cfg1 10-step trajectory: worst state error", worst)
+        for a, m in enumerate(masses):
+            moms = Wm @ state[a] * np.array([1.0, m, m, m])
+            ref_m = moms_ref[step][:, a]
+            # density and energy relative; momentum relative to the density scale
+            assert np.all(np.abs(moms - ref_m)[[0, 2]] <= 1e-10 * np.abs(ref_m[[0, 2]]))
+            assert abs(moms[1] - ref_m[1]) <= 1e-10 * abs(ref_m[0])
+    print(case, "trajectory: worst state error", worst)
     assert worst <= TOL
 
 
