@@ -28,6 +28,14 @@
 #include <cstdint>
 #include "landau_coefs.h"
 
+#ifndef LB_SERIES_MODE
+#define LB_SERIES_MODE 1  // 1: one series branch per lockstep group (selected per pair); 0: one per pair
+#endif
+
+#ifndef LB_KD_I2F
+#define LB_KD_I2F 1  // exponent to double by I2F.F64 (off the FP64 pipe); 0: magic-number DADD
+#endif
+
 #ifndef LB_ESTRIN
 #define LB_ESTRIN 0  // 1: Estrin-form polynomials (shorter dependency chains)
 #endif
@@ -101,7 +109,11 @@ __device__ __forceinline__ double log_reduce(double x, const double2* __restrict
   const double2 t = tab[i];  // (invc, logc)
   logc = t.y;
   // exact int -> double: 2^52 + 2^31 + k, minus the same magic
+#if LB_KD_I2F
+  kd = (double)k;  // I2F.F64 (conversion unit) instead of a DADD on the FP64 pipe
+#else
   kd = __longlong_as_double(0x4330000080000000LL + (long long)k) - c_misc[11];
+#endif
   return fma(z, t.x, -1.0);
 }
 
@@ -150,8 +162,6 @@ __device__ __forceinline__ double log_table(double x, const double2* __restrict_
 struct Outer {
   double ri, zi;
   double ri2;   // ri*ri
-  double fri;   // 4*ri
-  double tri;   // 2*ri
   double rfri;  // 1/(4 ri), 0 when ri == 0 (then m == 0 and the series runs)
 };
 
@@ -160,8 +170,6 @@ __device__ __forceinline__ Outer make_outer(double ri, double zi) {
   o.ri = ri;
   o.zi = zi;
   o.ri2 = ri * ri;
-  o.fri = 4.0 * ri;
-  o.tri = 2.0 * ri;
   o.rfri = ri > 0.0 ? 1.0 / (4.0 * ri) : 0.0;
   return o;
 }
@@ -176,6 +184,7 @@ struct T5 {
 // The symmetric part of one pair: B1..B5 (each / 4), dz, dz^2 and the mask.
 struct PairB {
   double B1, B3, B4, B5, dz, dz2;  // B's are zero for masked pairs
+  double rr;                        // ri rn
   double u;                         // B1 + 2 ri rn B4 (shared by UD_xx of both orientations)
 };
 
@@ -185,7 +194,7 @@ struct PairB {
 // lookup -- the long-latency front (MUFU, shared-memory table) that the
 // symmetric sweep issues one step ahead of the rest.
 struct PairS1 {
-  double dz, dz2, P, tq, isPm, invP, x, lr, logc, kd;
+  double dz, dz2, P, rr, isPm, invP, x, lr, logc, kd;
 };
 
 __device__ __forceinline__ PairS1 pair_stage1(const Outer& o, double rn, double zn, long long gthr,
@@ -198,8 +207,10 @@ __device__ __forceinline__ PairS1 pair_stage1(const Outer& o, double rn, double 
   const long long di = __double_as_longlong(dist2);
   const bool g = di >= gthr;  // d^2 >= eps^2 and d^2 > 0 (kernel.py:344)
   const double d2 = di > kTinyBits ? dist2 : 1.0;
-  s.tq = o.fri * rn;  // 4 ri rn
-  s.P = d2 + s.tq;
+  // ri rn; 4 ri rn and 2 ri rn below are exact scalings of it, so P, m and
+  // u round exactly as with (4 ri) rn and (2 ri) rn
+  s.rr = o.ri * rn;
+  s.P = fma(4.0, s.rr, d2);
   const double isP = rsqrt_nr(s.P);
   s.invP = isP * isP;
   s.x = d2 * s.invP;
@@ -212,7 +223,7 @@ __device__ __forceinline__ PairS1 pair_stage1(const Outer& o, double rn, double 
 
 // Stage 2: ln x, K(m), E(m), S2/S3 and B1..B5 (each / 4).
 __device__ __forceinline__ PairB pair_stage2(const Outer& o, double rn, double rcpr, const PairS1& s) {
-  const double x = s.x, P = s.P, tq = s.tq, invP = s.invP;
+  const double x = s.x, P = s.P, invP = s.invP;
   const double lx = log_finish(s.lr, s.logc, s.kd);
 
 
@@ -258,7 +269,7 @@ __device__ __forceinline__ PairB pair_stage2(const Outer& o, double rn, double r
   // m itself is only needed by the series
   if (__double_as_longlong(x) > kXSwitchBits) {
     // hypergeometric series (kernel.py:369-375)
-    const double m = tq * invP;
+    const double m = (4.0 * s.rr) * invP;
     double s2 = c_s2[9], s3 = c_s3[9];
     s2 = fma(s2, m, c_s2[8]);  s3 = fma(s3, m, c_s3[8]);
     s2 = fma(s2, m, c_s2[7]);  s3 = fma(s3, m, c_s3[7]);
@@ -287,7 +298,8 @@ __device__ __forceinline__ PairB pair_stage2(const Outer& o, double rn, double r
   p.B5 = S3 * c3;
   p.dz = s.dz;
   p.dz2 = s.dz2;
-  p.u = fma(o.tri * rn, p.B4, p.B1);
+  p.rr = s.rr;
+  p.u = fma(s.rr + s.rr, p.B4, p.B1);
   return p;
 }
 
@@ -299,7 +311,7 @@ __device__ __forceinline__ PairB pair_core(const Outer& o, double rn, double zn,
 
 // Direct-pair tensor components from the symmetric part.
 __device__ __forceinline__ T5 pair_tensors(const Outer& o, double rn, double rn2, const PairB& p) {
-  const double rr = o.ri * rn;
+  const double rr = p.rr;
   T5 t;
   t.xx = fma(-rn2, p.B5, fma(-o.ri2, p.B3, p.u));
   t.zz = fma(-p.dz2, p.B3, p.B1);
@@ -385,11 +397,12 @@ __device__ __forceinline__ void pair_tensor_sym_x(const Outer (&oo)[U], const do
     const double c = fma(-2.0, EK[u], Em1[u] + EE[u]);
     S3[u] = fma(4.0, fma(c, invm, -a) * invm, Em1[u]);
   }
+#if LB_SERIES_MODE == 0
 #pragma unroll
   for (int u = 0; u < U; ++u) {
     // m < 0.01 (kernel.py:376), tested as x = 1 - m > 0.99 on the bit pattern
     if (__double_as_longlong(x[u]) > kXSwitchBits) {
-      const double m = s[u].tq * s[u].invP;
+      const double m = (4.0 * s[u].rr) * s[u].invP;
       double s2 = c_s2[9], s3 = c_s3[9];
 #pragma unroll
       for (int k = 8; k >= 1; --k) {
@@ -400,6 +413,38 @@ __device__ __forceinline__ void pair_tensor_sym_x(const Outer (&oo)[U], const do
       S3[u] = fma(s3, m, c_s3[0]);
     }
   }
+#else
+  // one branch for the U pairs: the series (rare: m < 0.01 needs a point
+  // near the axis) runs for all U in lockstep and is selected per pair
+  bool ser[U], any = false;
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    ser[u] = __double_as_longlong(x[u]) > kXSwitchBits;  // m < 0.01 (kernel.py:376)
+    any |= ser[u];
+  }
+  if (any) {
+    double m[U], s2[U], s3[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      m[u] = (4.0 * s[u].rr) * s[u].invP;
+      s2[u] = c_s2[9];
+      s3[u] = c_s3[9];
+    }
+#pragma unroll
+    for (int k = 8; k >= 1; --k)
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        s2[u] = fma(s2[u], m[u], c_s2[k]);
+        s3[u] = fma(s3[u], m[u], c_s3[k]);
+      }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const double a2 = s2[u] * m[u], a3 = fma(s3[u], m[u], c_s3[0]);
+      S2[u] = ser[u] ? a2 : S2[u];
+      S3[u] = ser[u] ? a3 : S3[u];
+    }
+  }
+#endif
 #pragma unroll
   for (int u = 0; u < U; ++u) {
     const double isPm = s[u].isPm;
@@ -411,7 +456,8 @@ __device__ __forceinline__ void pair_tensor_sym_x(const Outer (&oo)[U], const do
     p.B5 = S3[u] * c3;
     p.dz = s[u].dz;
     p.dz2 = s[u].dz2;
-    p.u = fma(oo[u].tri * rn[u], p.B4, p.B1);
+    p.rr = s[u].rr;
+    p.u = fma(s[u].rr + s[u].rr, p.B4, p.B1);
     t[u] = pair_tensors(oo[u], rn[u], rn2[u], p);
     txx2[u] = fma(-oo[u].ri2, p.B5, fma(-rn2[u], p.B3, p.u));
   }

@@ -321,6 +321,9 @@ __global__ void __launch_bounds__(kSymTile, sym_min_blocks(S)) lb_symsweep_kerne
 #ifndef LB_IB_PAIRS
 #define LB_IB_PAIRS 2  // partners per step, each paired with both outer points (4 pairs)
 #endif
+#ifndef LB_IB_ROT_TOP
+#define LB_IB_ROT_TOP 0  // 1: j-side rotation at the top of the next step (measured no gain)
+#endif
 #ifndef LB_IB_MINB
 #define LB_IB_MINB (LB_IB_PAIRS == 2 ? 4 : 6)  // CTAs per SM (240 / 168 registers)
 #endif
@@ -412,6 +415,18 @@ __global__ void __launch_bounds__(kIbThreads, LB_IB_MINB) lb_symsweep_ib_kernel(
         rzn[u] = *reinterpret_cast<const double2*>(tile + (jb * 32 + ((lane + u * L) & 31)) * RS);
 #pragma unroll 1
       for (int st = 0; st < L; ++st) {
+#if LB_IB_ROT_TOP
+        // rotate the j-side sums of the previous step here (a no-op on the
+        // zeros at st == 0) rather than after its accumulation, so the
+        // shuffles share a basic block with, and hide under, this step's
+        // pair arithmetic
+#pragma unroll
+        for (int u = 0; u < JU; ++u)
+#pragma unroll
+          for (int b = 0; b < S; ++b)
+#pragma unroll
+            for (int q = 0; q < 5; ++q) ju[u][b][q] = __shfl_sync(0xffffffffu, ju[u][b][q], (lane + 1) & 31);
+#endif
         const double* rp[JU];
         Outer oo[P2];
         double rn[P2], zn[P2], rn2[P2], rcpr[P2];
@@ -463,14 +478,25 @@ __global__ void __launch_bounds__(kIbThreads, LB_IB_MINB) lb_symsweep_ib_kernel(
                 ju[u][b][3] = fma(gi[ib][b][2], tt.zr, ju[u][b][3]);
                 ju[u][b][4] = fma(gi[ib][b][2], tt.zz, ju[u][b][4]);
               }
+#if !LB_IB_ROT_TOP
 #pragma unroll
           for (int u = 0; u < JU; ++u)
 #pragma unroll
             for (int b = 0; b < S; ++b)
 #pragma unroll
               for (int q = 0; q < 5; ++q) ju[u][b][q] = __shfl_sync(0xffffffffu, ju[u][b][q], (lane + 1) & 31);
+#endif
         }
       }
+#if LB_IB_ROT_TOP
+      // the last step's rotation
+#pragma unroll
+      for (int u = 0; u < JU; ++u)
+#pragma unroll
+        for (int b = 0; b < S; ++b)
+#pragma unroll
+          for (int q = 0; q < 5; ++q) ju[u][b][q] = __shfl_sync(0xffffffffu, ju[u][b][q], (lane + 1) & 31);
+#endif
       // lane l holds accumulator u of j = l + (u+1)L: gather j = l in u order
       double jacc[S][5];
 #pragma unroll
