@@ -12,7 +12,7 @@
 //
 // What differs (the arithmetic, not the math):
 //  * no IEEE divides: 1/sqrt(P) is MUFU.RSQ64H + one cubic Newton step,
-//    1/P = (1/sqrt P)^2, 1/d^2 is MUFU.RCP64H + one cubic step, 1/m = P * (1/(4 ri)) * (1/rn) from per-point reciprocals;
+//    1/P = (1/sqrt P)^2, 1/d^2 is MUFU.RCP64H + one cubic step, 2/m = P * (1/(2 ri)) * (1/rn) from per-point reciprocals;
 //  * the common factor 4 of B1..B5 is pulled out (an exact power-of-two
 //    scaling) and folded into the species coupling coefficients;
 //  * the m < 0.01 series and the closed form are a real branch instead of
@@ -162,7 +162,7 @@ __device__ __forceinline__ double log_table(double x, const double2* __restrict_
 struct Outer {
   double ri, zi;
   double ri2;   // ri*ri
-  double rfri;  // 1/(4 ri), 0 when ri == 0 (then m == 0 and the series runs)
+  double rtri;  // 1/(2 ri), 0 when ri == 0 (then m == 0 and the series runs)
 };
 
 __device__ __forceinline__ Outer make_outer(double ri, double zi) {
@@ -170,7 +170,7 @@ __device__ __forceinline__ Outer make_outer(double ri, double zi) {
   o.ri = ri;
   o.zi = zi;
   o.ri2 = ri * ri;
-  o.rfri = ri > 0.0 ? 1.0 / (4.0 * ri) : 0.0;
+  o.rtri = ri > 0.0 ? 1.0 / (2.0 * ri) : 0.0;
   return o;
 }
 
@@ -282,12 +282,13 @@ __device__ __forceinline__ PairB pair_stage2(const Outer& o, double rn, double r
     S2 = s2 * m;
     S3 = fma(s3, m, c_s3[0]);
   } else {
-    // closed form (kernel.py:366-367); 1/m = P/(4 ri rn), here m >= 0.01 so rn > 0
-    const double invm = P * o.rfri * rcpr;
+    // closed form (kernel.py:366-367) in 2/m = P/(2 ri rn) (m >= 0.01, so rn > 0):
+    // S2 = a (2/m) - Em1, S3 = (c (2/m) - 2a)(2/m) + Em1 = 4c/m^2 - 4a/m + Em1
+    const double invm2 = P * o.rtri * rcpr;  // 2/m
     const double a = Em1 - EK;
-    S2 = fma(2.0, a * invm, -Em1);
+    S2 = fma(a, invm2, -Em1);
     const double c = fma(-2.0, EK, Em1 + EE);
-    S3 = fma(4.0, fma(c, invm, -a) * invm, Em1);
+    S3 = fma(fma(c, invm2, -(a + a)), invm2, Em1);
   }
   const double isPm = s.isPm;
   const double c3 = isPm * invP;  // P^-3/2 (the 4 is folded into the coupling)
@@ -390,12 +391,12 @@ __device__ __forceinline__ void pair_tensor_sym_x(const Outer (&oo)[U], const do
     EK[u] = fma(-lx[u], qk[u], pk[u]);
     EE[u] = fma(-lx[u], qe[u], pe[u]);
     Em1[u] = EE[u] * rcp_nr(x[u]);  // E/(1-m) = E P/d^2
-    // closed form (kernel.py:366-367); 1/m = P/(4 ri rn)
-    const double invm = s[u].P * oo[u].rfri * rcpr[u];
+    // closed form (kernel.py:366-367) in 2/m = P/(2 ri rn), as in pair_stage2
+    const double invm2 = s[u].P * oo[u].rtri * rcpr[u];  // 2/m
     const double a = Em1[u] - EK[u];
-    S2[u] = fma(2.0, a * invm, -Em1[u]);
+    S2[u] = fma(a, invm2, -Em1[u]);
     const double c = fma(-2.0, EK[u], Em1[u] + EE[u]);
-    S3[u] = fma(4.0, fma(c, invm, -a) * invm, Em1[u]);
+    S3[u] = fma(fma(c, invm2, -(a + a)), invm2, Em1[u]);
   }
 #if LB_SERIES_MODE == 0
 #pragma unroll

@@ -86,11 +86,15 @@ __host__ __device__ constexpr int sym_threads() {
 }
 
 // TMA stages + log table + j-side exchange (2 x warps x 32 j x 5S doubles)
+#ifndef LB_IB_ROT_SMEM
+#define LB_IB_ROT_SMEM 0  // 1: j-side rotation through shared memory instead of shuffles
+#endif
 template <int S>
 constexpr size_t sym_smem_bytes() {
   return size_t(kSymStages) * kSymTile * rec_stride(S) * sizeof(double) +
          size_t(2 << LB_LOGT_BITS) * sizeof(double) +
-         size_t(2) * (sym_threads<S>() / 32) * 32 * 5 * S * sizeof(double);
+         size_t(2) * (sym_threads<S>() / 32) * 32 * 5 * S * sizeof(double) +
+         ((S == 1 && LB_SYM_IB && LB_IB_ROT_SMEM) ? size_t(2) * kIbThreads * 10 * sizeof(double) : 0);
 }
 
 struct SymArgs {
@@ -341,6 +345,9 @@ __global__ void __launch_bounds__(kIbThreads, LB_IB_MINB) lb_symsweep_ib_kernel(
   __shared__ int stage_item[kSymStages], stage_d[kSymStages];
   double2* logt = reinterpret_cast<double2*>(lb_smem + kSymStages * kSymTile * RS);
   double* jred = lb_smem + kSymStages * kSymTile * RS + (2 << LB_LOGT_BITS);  // [2][NW][32][5S]
+#if LB_IB_ROT_SMEM
+  double* jrot = jred + 2 * NW * 32 * (5 * S);  // [2][kIbThreads][10]
+#endif
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int nrows = a.row1 - a.row0;
@@ -478,7 +485,26 @@ __global__ void __launch_bounds__(kIbThreads, LB_IB_MINB) lb_symsweep_ib_kernel(
                 ju[u][b][3] = fma(gi[ib][b][2], tt.zr, ju[u][b][3]);
                 ju[u][b][4] = fma(gi[ib][b][2], tt.zz, ju[u][b][4]);
               }
-#if !LB_IB_ROT_TOP
+#if LB_IB_ROT_SMEM
+          {
+            // rotate through a double-buffered per-thread slot (80 B stride:
+            // conflict-free 16-byte accesses); one __syncwarp per step
+            static_assert(JU * S * 5 == 10, "shared-memory rotation assumes 10 j-side sums");
+            double* own = jrot + ((size_t)(st & 1) * kIbThreads + tid) * 10;
+            const double* nb = jrot + ((size_t)(st & 1) * kIbThreads + warp * 32 + ((lane + 1) & 31)) * 10;
+            double* flat = &ju[0][0][0];
+#pragma unroll
+            for (int q = 0; q < 10; q += 2)
+              *reinterpret_cast<double2*>(own + q) = make_double2(flat[q], flat[q + 1]);
+            __syncwarp();
+#pragma unroll
+            for (int q = 0; q < 10; q += 2) {
+              const double2 v = *reinterpret_cast<const double2*>(nb + q);
+              flat[q] = v.x;
+              flat[q + 1] = v.y;
+            }
+          }
+#elif !LB_IB_ROT_TOP
 #pragma unroll
           for (int u = 0; u < JU; ++u)
 #pragma unroll
