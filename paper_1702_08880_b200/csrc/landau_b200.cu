@@ -34,6 +34,7 @@
 #include "landau_sym.cuh"
 #include "landau_aux.cuh"
 #include "landau_cn.cuh"
+#include "landau_lu.cuh"
 
 namespace lb {
 
@@ -1404,6 +1405,8 @@ struct CnLevel {
   int N = 0;
   int* piv = nullptr;   // pivots of the odd rows' D, (count x nb), batch order
   int* info = nullptr;  // getrf info of the odd rows
+  int* perm = nullptr;     // row permutation of each odd-row factorisation (custom LU)
+  double* inv = nullptr;   // inverses of the factors' diagonal blocks (custom LU)
   CnBatch getrf;        // A = D (odd rows)
   CnBatch getrsL;       // A = D, B = [L U] (odd rows; adjacent blocks, one nb x 2nb right-hand side)
   CnBatch gemmE, gemmF;    // C = D_even -= A B
@@ -1458,6 +1461,14 @@ static int cn_alloc(lb_cn* cn, void** p, size_t bytes) {
   return LB_OK;
 }
 
+// block LU + [L U] solve by the custom kernels of landau_lu.cuh (cuBLAS
+// getrf / getrs / trsm otherwise: blocks over 384 rows, or LB_CN_CUBLAS_LU set)
+constexpr int kLuKB = 32, kLuW = 32, kLuMaxNb = 384;
+static bool cn_custom_lu(const lb_cn* cn) {
+  static const bool force_blas = std::getenv("LB_CN_CUBLAS_LU") != nullptr;
+  return cn->nb <= kLuMaxNb && !force_blas;
+}
+
 // factor blocks small enough for the shared-memory vector solve (cuBLAS otherwise)
 static bool cn_small(const lb_cn* cn) {
   static const bool force_blas = std::getenv("LB_CN_CUBLAS") != nullptr;
@@ -1469,14 +1480,30 @@ static int cn_factor_issue(lb_cn* cn, cudaStream_t st, bool pivot) {
   const double one = 1.0, mone = -1.0, zero = 0.0;
   int hinfo = 0;
   LB_BLAS(cublasSetStream(cn->blas, st));
+  const bool custom = cn_custom_lu(cn);
   for (const CnLevel& L : cn->lv) {
-    if (L.getrf.count)
+    if (custom) {
+      // one CTA per odd-row block: LU (LAPACK layout, pivots, permutation,
+      // diagonal-block inverses), then D^-1 [L U] by W-column slabs
+      if (L.getrf.count) {
+        lb_getrf_kernel<kLuKB><<<L.getrf.count, kLuThreads, getrf_smem_bytes<kLuKB>(nb), st>>>(
+            nb, L.getrf.A, L.piv, L.perm, L.info, L.inv, pivot ? 1 : 0);
+        LB_CUDA(cudaGetLastError());
+      }
+      if (L.getrsL.count) {
+        const dim3 g(L.getrsL.count, (2 * nb + kLuW - 1) / kLuW);
+        lb_getrs_slab_kernel<kLuKB, kLuW><<<g, kLuThreads, getrs_smem_bytes<kLuKB, kLuW>(nb), st>>>(
+            nb, 2 * nb, L.getrsL.A, L.perm, L.inv, L.getrsL.B);
+        LB_CUDA(cudaGetLastError());
+      }
+    } else if (L.getrf.count) {
       LB_BLAS(cublasDgetrfBatched(cn->blas, nb, L.getrf.A, nb, pivot ? L.piv : nullptr, L.info,
                                   L.getrf.count));
+    }
     // L_l[k] and U_l[k] are adjacent in the pool, so [L U] is one nb x 2nb
     // column-major right-hand side: P = D^-1 [L U] in a single call (the
     // last odd row's U slot is unused scratch when it has no right neighbour)
-    if (L.getrsL.count) {
+    if (!custom && L.getrsL.count) {
       if (pivot) {
         LB_BLAS(cublasDgetrsBatched(cn->blas, CUBLAS_OP_N, nb, 2 * nb, L.getrsL.A, nb, L.piv, L.getrsL.B,
                                     nb, &hinfo, L.getrsL.count));
@@ -1779,6 +1806,11 @@ static int cn_plan(lb_cn* cn) {
     make(L.backU, bUA, bUx, bUy);
     if ((rc = cn_alloc(cn, (void**)&L.piv, sizeof(int) * std::max<size_t>(fA.size(), 1) * nb))) return rc;
     if ((rc = cn_alloc(cn, (void**)&L.info, sizeof(int) * std::max<size_t>(fA.size(), 1)))) return rc;
+    if (cn_custom_lu(cn)) {
+      const size_t cnt = std::max<size_t>(fA.size(), 1);
+      if ((rc = cn_alloc(cn, (void**)&L.perm, sizeof(int) * cnt * nb))) return rc;
+      if ((rc = cn_alloc(cn, (void**)&L.inv, sizeof(double) * cnt * lu_inv_stride<kLuKB>(nb)))) return rc;
+    }
   }
   double** dpool = nullptr;
   if ((rc = cn_alloc(cn, (void**)&dpool, sizeof(double*) * std::max<size_t>(pool.size(), 1)))) return rc;
@@ -1869,6 +1901,12 @@ int lb_cn_create(lb_ctx* ctx, const lb_mesh* m, int S, int n, const int* indptr,
       cudaFuncSetAttribute(lb_small_solve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)small_solve_smem_bytes(kSmallNb)) != cudaSuccess)
     return bail(fail(LB_ECUDA, "cudaFuncSetAttribute(lb_small_solve_kernel) failed"));
+  if (nb <= kLuMaxNb &&
+      (cudaFuncSetAttribute(lb_getrf_kernel<kLuKB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)getrf_smem_bytes<kLuKB>(kLuMaxNb)) != cudaSuccess ||
+       cudaFuncSetAttribute(lb_getrs_slab_kernel<kLuKB, kLuW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)getrs_smem_bytes<kLuKB, kLuW>(kLuMaxNb)) != cudaSuccess))
+    return bail(fail(LB_ECUDA, "cudaFuncSetAttribute(custom LU kernels) failed"));
   const size_t ws = size_t(32) << 20;
   if ((rc = cn_alloc(cn, &cn->blas_ws, ws))) return bail(rc);
   if (cublasSetWorkspace(cn->blas, cn->blas_ws, ws) != CUBLAS_STATUS_SUCCESS)
