@@ -34,7 +34,7 @@ constexpr int kLuThreads = 256;
 __device__ long long lu_prof[8];  // cycles per phase (block 0, thread 0), accumulated
 #define LU_T(k)                                                        \
   do {                                                                 \
-    if (blockIdx.x == 0 && threadIdx.x == 0) {                         \
+    if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) {      \
       const long long t1_ = clock64();                                 \
       lu_prof[k] += t1_ - t0_;                                         \
       t0_ = t1_;                                                       \
@@ -324,13 +324,30 @@ __global__ void __launch_bounds__(kLuThreads) lb_getrf_kernel(int n, double* con
 
 // X := A^-1 X for X = the n x m column-major block at Xs[b] (leading
 // dimension n), A the factors of lb_getrf_kernel.  CTA (b, s) owns columns
-// [s W, s W + W).  Shared memory: the slab [ld][W] (row-major: a row of W
-// columns is contiguous), one staged factor column block [KB][ld], the
-// diagonal inverse [KB][KB].
+// [s W, s W + W).  Shared memory: the slab X [ld][W] (row-major: a row of W
+// columns is contiguous), the factor column block of the current step in
+// two k-halves H0/H1 [KB/2][ld] (column-major), the diagonal-block inverse
+// (two buffers) and the scaled block Y [KB][W].
+//
+// 2 np block steps (forward p = 0..np-1 with L, backward p = np-1..0 with U).
+// Step q:   Y = Di(q) X[block]   (X rows of the block := Y)
+//           X[rows] -= F(q)[rows][0:KB/2] Y[0:KB/2]      (H0)
+//           X[rows] -= F(q)[rows][KB/2:KB] Y[KB/2:KB]   (H1)
+// The factor halves arrive by cp.async, each one phase ahead: H0 of step
+// q+1 streams in during the H1 pass of step q, H1 of step q+1 (and Di)
+// during the Di product of step q+1.
 template <int KB, int W>
 inline size_t getrs_smem_bytes(int n) {
-  return sizeof(double) * ((size_t)lu_ld<KB>(n) * W + (size_t)KB * lu_ld<KB>(n) + KB * KB);
+  return sizeof(double) * ((size_t)lu_ld<KB>(n) * W + (size_t)KB * lu_ld<KB>(n) + 2 * KB * KB + KB * W);
 }
+
+__device__ __forceinline__ void cp_async8(double* dst, const double* src) {
+  const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(d), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
 template <int KB, int W>
 __global__ void __launch_bounds__(kLuThreads) lb_getrs_slab_kernel(int n, int m, double* const* __restrict__ As,
@@ -338,11 +355,14 @@ __global__ void __launch_bounds__(kLuThreads) lb_getrs_slab_kernel(int n, int m,
                                                                    const double* __restrict__ inv_all,
                                                                    double* const* __restrict__ Xs) {
   static_assert(KB * W / 4 <= kLuThreads, "one diagonal-block output group per thread");
+  constexpr int KH = KB / 2, CG = W / 4;  // k-half, column groups of 4
+  constexpr int kMaxTiles = 3;           // row tiles per thread: ceil(ceil(383/4) CG / NT)
   extern __shared__ __align__(16) double lu_sm[];
   const int ld = lu_ld<KB>(n);
   double* X = lu_sm;                       // [ld][W]
-  double* F = X + (size_t)ld * W;          // [KB][ld]: factor columns, column-major
-  double* Di = F + (size_t)KB * ld;        // [KB][KB] diagonal-block inverse, column-major
+  double* H[2] = {X + (size_t)ld * W, X + (size_t)ld * W + (size_t)KH * ld};  // [KH][ld] each
+  double* Dib[2] = {H[1] + (size_t)KH * ld, H[1] + (size_t)KH * ld + KB * KB};  // [KB][KB]
+  double* Y = Dib[1] + KB * KB;            // [KB][W]
   const int b = blockIdx.x, s = blockIdx.y, tid = threadIdx.x;
   const int col0 = s * W, wc = min(W, m - col0);
   if (wc <= 0) return;
@@ -350,123 +370,128 @@ __global__ void __launch_bounds__(kLuThreads) lb_getrs_slab_kernel(int n, int m,
   double* Xg = Xs[b] + (size_t)col0 * n;
   const int* perm = perm_all ? perm_all + (size_t)b * n : nullptr;
   const double* inv = inv_all + (size_t)b * lu_inv_stride<KB>(n);
-  const int np = (n + KB - 1) / KB;
+  const int np = (n + KB - 1) / KB, nsteps = 2 * np;
+  auto geom = [&](int q, int& p, int& r0, int& kb, int& lo, int& hi) {
+    const bool fwd = q < np;
+    p = fwd ? q : nsteps - 1 - q;
+    r0 = p * KB;
+    kb = min(KB, n - r0);
+    lo = fwd ? r0 + kb : 0;  // rows the step updates: below the block (L) / above it (U)
+    hi = fwd ? n : r0;
+  };
+  // issue the copies of half h of step q's factor block (and its Di when h == 1)
+  auto issue = [&](int q, int h) {
+    int p, r0, kb, lo, hi;
+    geom(q, p, r0, kb, lo, hi);
+    const int rows = hi - lo;
+    double* dst = H[h];
+    for (int k = 0; k < KH; ++k) {
+      const int kk = h * KH + k;
+      if (kk >= kb) break;
+      const double* src = A + (size_t)(r0 + kk) * n;
+      for (int i = lo + tid; i < hi; i += kLuThreads) cp_async8(dst + (size_t)k * ld + i, src + i);
+    }
+    (void)rows;
+    if (h == 1) {
+      const double* di = inv + (size_t)(q < np ? 2 * p : 2 * p + 1) * KB * KB;
+      double* dd = Dib[q & 1];
+      for (int t = tid; t < KB * KB; t += kLuThreads) cp_async8(dd + t, di + t);
+    }
+    cp_async_commit();
+  };
+  issue(0, 0);
+  issue(0, 1);
   // gather P X into shared memory (zero rows n..ld, zero columns wc..W)
   for (int i = tid; i < ld; i += kLuThreads) {  // consecutive threads: consecutive rows of a column
     const int src = (i < n) ? (perm ? perm[i] : i) : 0;
-#pragma unroll 4
+#pragma unroll 8
     for (int c = 0; c < W; ++c) X[(size_t)i * W + c] = (i < n && c < wc) ? Xg[(size_t)c * n + src] : 0.0;
   }
-  // Per block step: Y = Di * X[r0:r0+KB] (KB x W, one thread per 4 outputs),
-  // then X[rows] -= F[rows][0:KB] * Y for the rows still to update.
-  auto step = [&](int r0, int kb, int u0, int u1) {
-    // X[r0:r0+kb] := Di X[r0:r0+kb]  (KB x KB times KB x W)
+  // this thread's output group of the Di product and its row tiles of the update
+  const int yi = tid / CG, yc = (tid - (tid / CG) * CG) * 4;
+  for (int q = 0; q < nsteps; ++q) {
+    int p, r0, kb, lo, hi;
+    geom(q, p, r0, kb, lo, hi);
+    cp_async_wait<0>();  // H1(q) and Di(q) (H0(q) landed earlier)
     __syncthreads();
-    double y[4];
-    const int nout = KB * W / 4;
-    int yi = -1, yc = 0;
-    for (int t = tid; t < nout; t += kLuThreads) {
-      const int i = t / (W / 4), c = (t - i * (W / 4)) * 4;
+    // Y = Di X[r0 : r0 + kb]
+    const double* Di = Dib[q & 1];
+    if (tid < KB * CG) {
       double a0 = 0, a1 = 0, a2 = 0, a3 = 0;
       for (int k = 0; k < kb; ++k) {
-        const double dk = Di[(size_t)k * KB + i];
-        const double* xr = X + (size_t)(r0 + k) * W + c;
-        a0 = fma(dk, xr[0], a0);
-        a1 = fma(dk, xr[1], a1);
-        a2 = fma(dk, xr[2], a2);
-        a3 = fma(dk, xr[3], a3);
+        const double dk = Di[(size_t)k * KB + yi];
+        const double2 x01 = *reinterpret_cast<const double2*>(X + (size_t)(r0 + k) * W + yc);
+        const double2 x23 = *reinterpret_cast<const double2*>(X + (size_t)(r0 + k) * W + yc + 2);
+        a0 = fma(dk, x01.x, a0);
+        a1 = fma(dk, x01.y, a1);
+        a2 = fma(dk, x23.x, a2);
+        a3 = fma(dk, x23.y, a3);
       }
-      y[0] = a0; y[1] = a1; y[2] = a2; y[3] = a3;
-      yi = i;
-      yc = c;
+      *reinterpret_cast<double2*>(Y + (size_t)yi * W + yc) = make_double2(a0, a1);
+      *reinterpret_cast<double2*>(Y + (size_t)yi * W + yc + 2) = make_double2(a2, a3);
     }
     __syncthreads();
-    if (yi >= 0 && yi < kb) {
-      double* xr = X + (size_t)(r0 + yi) * W + yc;
-      xr[0] = y[0]; xr[1] = y[1]; xr[2] = y[2]; xr[3] = y[3];
+    if (tid < KB * CG && yi < kb) {  // the block's rows of X become Y
+      *reinterpret_cast<double2*>(X + (size_t)(r0 + yi) * W + yc) =
+          *reinterpret_cast<const double2*>(Y + (size_t)yi * W + yc);
+      *reinterpret_cast<double2*>(X + (size_t)(r0 + yi) * W + yc + 2) =
+          *reinterpret_cast<const double2*>(Y + (size_t)yi * W + yc + 2);
     }
-    __syncthreads();
-    // X[u0:u1] -= F[u0:u1][0:kb] * X[r0:r0+kb]; 4 rows x 4 columns per thread
-    const int nr = u1 - u0;
-    if (nr <= 0) return;
-    const int tr = (nr + 3) >> 2;
-    for (int t = tid; t < tr * (W / 4); t += kLuThreads) {
-      const int ri = (t / (W / 4)) * 4, c = (t - (t / (W / 4)) * (W / 4)) * 4;
-      double acc[4][4] = {};
-      for (int k = 0; k < kb; ++k) {
-        const double* fp = F + (size_t)k * ld + u0 + ri;
-        const double* xr = X + (size_t)(r0 + k) * W + c;
-        const double2 x01 = *reinterpret_cast<const double2*>(xr);
-        const double2 x23 = *reinterpret_cast<const double2*>(xr + 2);
-        const double2 f01 = *reinterpret_cast<const double2*>(fp);
-        const double2 f23 = *reinterpret_cast<const double2*>(fp + 2);
-        const double xv[4] = {x01.x, x01.y, x23.x, x23.y};
-        const double fv[4] = {f01.x, f01.y, f23.x, f23.y};
+    // X[lo:hi] -= F Y in two k-halves; tiles of 4 rows x 4 columns
+    const int nr = hi - lo, ntile = ((nr + 3) >> 2) * CG;
+    double acc[kMaxTiles][4][4];
 #pragma unroll
-        for (int r = 0; r < 4; ++r) {
-          const double f = fv[r];
+    for (int u = 0; u < kMaxTiles; ++u)
 #pragma unroll
-          for (int q = 0; q < 4; ++q) acc[r][q] = fma(f, xv[q], acc[r][q]);
+      for (int r = 0; r < 4; ++r)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) acc[u][r][c] = 0.0;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int k0 = h * KH, k1 = min(kb, k0 + KH);
+      const double* Hh = H[h];
+#pragma unroll
+      for (int u = 0; u < kMaxTiles; ++u) {
+        const int t = tid + u * kLuThreads;
+        if (t >= ntile) break;
+        const int ri = (t / CG) * 4, c = (t - (t / CG) * CG) * 4;
+        for (int k = k0; k < k1; ++k) {
+          const double2 y01 = *reinterpret_cast<const double2*>(Y + (size_t)k * W + c);
+          const double2 y23 = *reinterpret_cast<const double2*>(Y + (size_t)k * W + c + 2);
+          const double2 f01 = *reinterpret_cast<const double2*>(Hh + (size_t)(k - k0) * ld + lo + ri);
+          const double2 f23 = *reinterpret_cast<const double2*>(Hh + (size_t)(k - k0) * ld + lo + ri + 2);
+          const double yv[4] = {y01.x, y01.y, y23.x, y23.y};
+          const double fv[4] = {f01.x, f01.y, f23.x, f23.y};
+#pragma unroll
+          for (int r = 0; r < 4; ++r)
+#pragma unroll
+            for (int cc = 0; cc < 4; ++cc) acc[u][r][cc] = fma(fv[r], yv[cc], acc[u][r][cc]);
         }
       }
+      if (h == 0) {
+        __syncthreads();  // H0 free: stream in the next step's first half
+        if (q + 1 < nsteps) issue(q + 1, 0);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kMaxTiles; ++u) {
+      const int t = tid + u * kLuThreads;
+      if (t >= ntile) break;
+      const int ri = (t / CG) * 4, c = (t - (t / CG) * CG) * 4;
 #pragma unroll
       for (int r = 0; r < 4; ++r) {
         if (ri + r >= nr) break;
-        double* xr = X + (size_t)(u0 + ri + r) * W + c;
-#pragma unroll
-        for (int q = 0; q < 4; ++q) xr[q] -= acc[r][q];
+        double* xr = X + (size_t)(lo + ri + r) * W + c;
+        const double2 x01 = *reinterpret_cast<const double2*>(xr);
+        const double2 x23 = *reinterpret_cast<const double2*>(xr + 2);
+        *reinterpret_cast<double2*>(xr) = make_double2(x01.x - acc[u][r][0], x01.y - acc[u][r][1]);
+        *reinterpret_cast<double2*>(xr + 2) = make_double2(x23.x - acc[u][r][2], x23.y - acc[u][r][3]);
       }
     }
-  };
-  // 2 np block steps: forward (L, unit lower) p = 0..np-1, then backward
-  // (U) p = np-1..0.  Step q's factor column block F and diagonal inverse
-  // Di are loaded into registers during step q-1 and stored after it.
-  constexpr int kPf = (KB * 384) / kLuThreads;  // per-thread share of F (n <= 384)
-  double fpf[kPf], dpf[KB * KB / kLuThreads];
-  // element t = tid + e NT of F is (k, i) = divmod(t, ld): stepped without divisions
-  const int k_0 = tid / ld, i_0 = tid - k_0 * ld, dk = kLuThreads / ld, di = kLuThreads - dk * ld;
-  auto fetch = [&](int q) {
-    const bool fwd = q < np;
-    const int p = fwd ? q : 2 * np - 1 - q;
-    const int r0 = p * KB, kb = min(KB, n - r0);
-    const int lo = fwd ? r0 + kb : 0, hi = fwd ? n : r0;
-    int k = k_0, i = i_0;
-#pragma unroll
-    for (int e = 0; e < kPf; ++e) {
-      const bool in = k < kb && i >= lo && i < hi;
-      fpf[e] = in ? A[(size_t)(r0 + k) * n + i] : 0.0;
-      i += di;
-      k += dk;
-      if (i >= ld) { i -= ld; ++k; }
-    }
-#pragma unroll
-    for (int e = 0; e < KB * KB / kLuThreads; ++e)
-      dpf[e] = inv[(size_t)(fwd ? 2 * p : 2 * p + 1) * KB * KB + tid + e * kLuThreads];
-  };
-  auto stash = [&]() {
-#pragma unroll
-    for (int e = 0; e < kPf; ++e) {
-      const int t = tid + e * kLuThreads;
-      if (t < KB * ld) F[t] = fpf[e];
-    }
-#pragma unroll
-    for (int e = 0; e < KB * KB / kLuThreads; ++e) Di[tid + e * kLuThreads] = dpf[e];
-  };
-  fetch(0);
-  __syncthreads();  // the gather above is complete
-  stash();
-  for (int q = 0; q < 2 * np; ++q) {
-    if (q + 1 < 2 * np) fetch(q + 1);
-    const bool fwd = q < np;
-    const int p = fwd ? q : 2 * np - 1 - q;
-    const int r0 = p * KB, kb = min(KB, n - r0);
-    if (fwd)
-      step(r0, kb, r0 + kb, n);
-    else
-      step(r0, kb, 0, r0);
-    __syncthreads();
-    if (q + 1 < 2 * np) stash();
+    __syncthreads();  // H1 and Y free
+    if (q + 1 < nsteps) issue(q + 1, 1);
   }
+  cp_async_wait<0>();
   __syncthreads();
   for (int c = 0; c < wc; ++c)
     for (int i = tid; i < n; i += kLuThreads) Xg[(size_t)c * n + i] = X[(size_t)i * W + c];

@@ -56,6 +56,23 @@ int main(int argc, char** argv) {
       for (int k = 0; k < 5; ++k) tot += h[k];
       printf("prof n=%d: load %lld factor %lld store+inv %lld swap+U12 %lld update %lld cycles (total %lld = %.1f us at 1.9 GHz)\n",
              n, h[0], h[1], h[2], h[3], h[4], tot, tot / 1.9e3);
+      // the slab solve of 2n right-hand sides with these factors
+      double* B;
+      cudaMalloc(&B, (size_t)n * 2 * n * 8);
+      cudaMemset(B, 0, (size_t)n * 2 * n * 8);
+      double** dB;
+      cudaMalloc(&dB, sizeof(double*));
+      cudaMemcpy(dB, &B, sizeof(double*), cudaMemcpyHostToDevice);
+      const size_t ss = getrs_smem_bytes<KB, W>(n);
+      cudaFuncSetAttribute(lb_getrs_slab_kernel<KB, W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ss);
+      cudaMemcpyToSymbol(lu_prof, z, sizeof(z));
+      lb_getrs_slab_kernel<KB, W><<<dim3(1, (2 * n + W - 1) / W), kLuThreads, ss>>>(n, 2 * n, dA, perm, inv, dB);
+      cudaDeviceSynchronize();
+      cudaMemcpyFromSymbol(h, lu_prof, sizeof(h));
+      printf("prof getrs n=%d: gather+first fetch %lld steps %lld stash %lld cycles (%.1f us)\n", n, h[5], h[6], h[7],
+             (h[5] + h[6] + h[7]) / 1.9e3);
+      cudaFree(B);
+      cudaFree(dB);
     }
   }
   return 0;
