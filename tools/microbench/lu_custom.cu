@@ -9,10 +9,13 @@
 #include <cstdio>
 #include <cstdlib>
 #include <vector>
+#ifndef LU_W
+#define LU_W 32
+#endif
 #include "landau_lu.cuh"
 
 using namespace lb;
-constexpr int KB = 32, W = 32;
+constexpr int KB = 32, W = LU_W;
 
 static double urand(unsigned long long& s) {
   s = s * 6364136223846793005ULL + 1442695040888963407ULL;
@@ -78,6 +81,10 @@ int main(int argc, char** argv) {
   return 0;
 #endif
   for (int n : {68, 260, 354}) {
+    if (getrs_smem_bytes<KB, W>(n) > 232448) {
+      printf("n=%3d: W=%d slab needs %zu B of shared memory, skipped\n", n, W, getrs_smem_bytes<KB, W>(n));
+      continue;
+    }
     for (int batch : {4, 64, 256}) {
       for (int kind = 0; kind < 2; ++kind) {  // 0: random (pivoting matters), 1: diagonally weighted
         const int m = 2 * n;
