@@ -31,18 +31,25 @@ namespace lb {
 
 constexpr int kLuThreads = 256;
 #ifdef LB_LU_PROF
-__device__ long long lu_prof[8];  // cycles per phase (block 0, thread 0), accumulated
+// cycles per phase (block 0, thread 0): accumulated in registers, written by LU_FLUSH
+__device__ long long lu_prof[8];
 #define LU_T(k)                                                        \
   do {                                                                 \
-    if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) {      \
-      const long long t1_ = clock64();                                 \
-      lu_prof[k] += t1_ - t0_;                                         \
-      t0_ = t1_;                                                       \
-    }                                                                  \
+    const long long t1_ = clock64();                                   \
+    pacc_[k] += t1_ - t0_;                                             \
+    t0_ = t1_;                                                         \
+  } while (0)
+#define LU_FLUSH()                                                                   \
+  do {                                                                               \
+    if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0)                      \
+      for (int k_ = 0; k_ < 8; ++k_) lu_prof[k_] += pacc_[k_];                       \
   } while (0)
 #else
 #define LU_T(k) \
   do {          \
+  } while (0)
+#define LU_FLUSH() \
+  do {             \
   } while (0)
 #endif
 
@@ -88,7 +95,7 @@ __global__ void __launch_bounds__(kLuThreads) lb_getrf_kernel(int n, double* con
   double* inv = inv_all + (size_t)b * lu_inv_stride<KB>(n);
   int info = 0;
 #ifdef LB_LU_PROF
-  long long t0_ = clock64();
+  long long t0_ = clock64(), pacc_[8] = {};
 #endif
 
   for (int c0 = 0, p = 0; c0 < n; c0 += KB, ++p) {
@@ -307,6 +314,7 @@ __global__ void __launch_bounds__(kLuThreads) lb_getrf_kernel(int n, double* con
     LU_T(4);
   }
   if (tid == 0) {
+    LU_FLUSH();
     if (info_all) info_all[b] = info;
     if (perm_all) {  // row i of P A is row perm[i] of A
       int* perm = perm_all + (size_t)b * n;
@@ -409,16 +417,22 @@ __global__ void __launch_bounds__(kLuThreads) lb_getrs_slab_kernel(int n, int m,
   }
   // this thread's output group of the Di product and its row tiles of the update
   const int yi = tid / CG, yc = (tid - (tid / CG) * CG) * 4;
+#ifdef LB_LU_PROF
+  long long t0_ = clock64(), pacc_[8] = {};
+#endif
   for (int q = 0; q < nsteps; ++q) {
     int p, r0, kb, lo, hi;
     geom(q, p, r0, kb, lo, hi);
     cp_async_wait<0>();  // H1(q) and Di(q) (H0(q) landed earlier)
     __syncthreads();
+    LU_T(1);
     // Y = Di X[r0 : r0 + kb]
     const double* Di = Dib[q & 1];
     if (tid < KB * CG) {
       double a0 = 0, a1 = 0, a2 = 0, a3 = 0;
-      for (int k = 0; k < kb; ++k) {
+#pragma unroll
+      for (int k = 0; k < KB; ++k) {
+        if (k >= kb) break;
         const double dk = Di[(size_t)k * KB + yi];
         const double2 x01 = *reinterpret_cast<const double2*>(X + (size_t)(r0 + k) * W + yc);
         const double2 x23 = *reinterpret_cast<const double2*>(X + (size_t)(r0 + k) * W + yc + 2);
@@ -437,6 +451,7 @@ __global__ void __launch_bounds__(kLuThreads) lb_getrs_slab_kernel(int n, int m,
       *reinterpret_cast<double2*>(X + (size_t)(r0 + yi) * W + yc + 2) =
           *reinterpret_cast<const double2*>(Y + (size_t)yi * W + yc + 2);
     }
+    LU_T(2);
     // X[lo:hi] -= F Y in two k-halves; tiles of 4 rows x 4 columns
     const int nr = hi - lo, ntile = ((nr + 3) >> 2) * CG;
     double acc[kMaxTiles][4][4];
@@ -455,7 +470,10 @@ __global__ void __launch_bounds__(kLuThreads) lb_getrs_slab_kernel(int n, int m,
         const int t = tid + u * kLuThreads;
         if (t >= ntile) break;
         const int ri = (t / CG) * 4, c = (t - (t / CG) * CG) * 4;
-        for (int k = k0; k < k1; ++k) {
+#pragma unroll
+        for (int kk = 0; kk < KH; ++kk) {
+          const int k = k0 + kk;
+          if (k >= k1) break;
           const double2 y01 = *reinterpret_cast<const double2*>(Y + (size_t)k * W + c);
           const double2 y23 = *reinterpret_cast<const double2*>(Y + (size_t)k * W + c + 2);
           const double2 f01 = *reinterpret_cast<const double2*>(Hh + (size_t)(k - k0) * ld + lo + ri);
@@ -473,6 +491,7 @@ __global__ void __launch_bounds__(kLuThreads) lb_getrs_slab_kernel(int n, int m,
         if (q + 1 < nsteps) issue(q + 1, 0);
       }
     }
+    LU_T(3);
 #pragma unroll
     for (int u = 0; u < kMaxTiles; ++u) {
       const int t = tid + u * kLuThreads;
@@ -488,9 +507,12 @@ __global__ void __launch_bounds__(kLuThreads) lb_getrs_slab_kernel(int n, int m,
         *reinterpret_cast<double2*>(xr + 2) = make_double2(x23.x - acc[u][r][2], x23.y - acc[u][r][3]);
       }
     }
+    LU_T(4);
     __syncthreads();  // H1 and Y free
     if (q + 1 < nsteps) issue(q + 1, 1);
+    LU_T(5);
   }
+  LU_FLUSH();
   cp_async_wait<0>();
   __syncthreads();
   for (int c = 0; c < wc; ++c)

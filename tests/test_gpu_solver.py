@@ -152,9 +152,10 @@ def test_newton_iterations_contract(gpu):
 @pytest.mark.parametrize("nr,nz", [(16, 32), (32, 64)])
 def test_config4_mesh_newton_step_matches_splu(gpu, nr, nz):
     """Uniform Q2 meshes with BASELINE config 4's four species -- 16x32
-    (2145 free nodes, 68-row blocks: the shared-memory block LU) and 32x64
-    (8385 free nodes, 132-row blocks in 64 block rows: cuBLAS, six reduction
-    levels): the device Newton step equals the host step done with SuperLU
+    (2145 free nodes, 68-row blocks) and 32x64 (8385 free nodes, 132-row
+    blocks in 64 block rows, six reduction levels), both through the
+    package's block-LU kernels (landau_lu.cuh): the device Newton step
+    equals the host step done with SuperLU
     on the same device operator, and the device mass matrix integrates r
     over the domain."""
     from paper_1702_08880_b200 import synthetic
@@ -254,3 +255,52 @@ def test_unpivoted_lu_falls_back_to_pivoting(gpu):
     stats = [s.stats() for s in S._LINEAR.values()]
     assert any(st["fallbacks"] >= 1 and st["pivoting"] for st in stats), stats
     assert min(st["rel_residual"] for st in stats) < 1e-12
+
+
+_CUBLAS_LU_SCRIPT = r"""
+import sys, numpy as np
+from types import SimpleNamespace
+sys.path.insert(0, sys.argv[1])
+import paper_1702_08880_b200 as gpu
+from paper_1702_08880_b200 import synthetic
+from paper_1702_08880_b200.solver import _mesh_solver
+import scipy.sparse as sp
+mesh, nodes = synthetic.uniform_q2_mesh(5.0, 32, 64)
+ref = synthetic.q2_reference()
+f0, nu, mro = synthetic.cfg4_state(nodes)
+params = gpu.CollisionParams(nu_hat=nu, mass_ratio_o=mro)
+s = _mesh_solver(mesh, ref, 4)
+s.set_mass(None)
+M = sp.csr_matrix((s.mass_values(), s.indices, s.indptr), shape=(s.n, s.n))
+cfg = SimpleNamespace(dt=0.1, eps_d=None)
+C_old = gpu.assemble_at(mesh, ref, f0, params)
+nxt, rnorm = gpu.newton_step(f0, f0, mesh, ref, params, cfg, M=M, C_old=C_old)
+np.save(sys.argv[2], nxt)
+"""
+
+
+def test_custom_block_lu_matches_cublas_path(gpu, tmp_path):
+    """The package's block LU + [L U] solve kernels and the cuBLAS
+    getrf/getrs/trsm path (LB_CN_CUBLAS_LU=1, read once per process, so it
+    runs in a subprocess) give the same Newton step on the 32x64 config-4
+    mesh (132-row blocks, four species): within the suite's 1e-10 bar (the
+    electron system is the ill-conditioned one that needs pivoting; there
+    both paths differ from SuperLU by ~3e-11 and from each other by ~2e-11,
+    the other species agree to ~1e-16)."""
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    root = Path(__file__).resolve().parents[1]
+    outs = {}
+    for name, extra in (("custom", {}), ("cublas", {"LB_CN_CUBLAS_LU": "1"})):
+        env = dict(os.environ, **extra)
+        out = tmp_path / f"{name}.npy"
+        subprocess.run([sys.executable, "-c", _CUBLAS_LU_SCRIPT, str(root), str(out)], env=env,
+                       check=True, timeout=600)
+        outs[name] = np.load(out)
+    for a in range(4):
+        err = _scaled(outs["custom"][a], outs["cublas"][a])
+        print("species", a, "custom LU vs cuBLAS LU", err)
+        assert err <= TOL

@@ -72,8 +72,8 @@ int main(int argc, char** argv) {
       lb_getrs_slab_kernel<KB, W><<<dim3(1, (2 * n + W - 1) / W), kLuThreads, ss>>>(n, 2 * n, dA, perm, inv, dB);
       cudaDeviceSynchronize();
       cudaMemcpyFromSymbol(h, lu_prof, sizeof(h));
-      printf("prof getrs n=%d: gather+first fetch %lld steps %lld stash %lld cycles (%.1f us)\n", n, h[5], h[6], h[7],
-             (h[5] + h[6] + h[7]) / 1.9e3);
+      printf("prof getrs n=%d: wait+sync %lld DiX %lld update %lld writeback %lld sync+issue %lld cycles (%.1f us)\n", n,
+             h[1], h[2], h[3], h[4], h[5], (h[1] + h[2] + h[3] + h[4] + h[5]) / 1.9e3);
       cudaFree(B);
       cudaFree(dB);
     }
