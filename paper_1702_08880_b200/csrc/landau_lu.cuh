@@ -353,6 +353,18 @@ __device__ __forceinline__ void cp_async8(double* dst, const double* src) {
   const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(d), "l"(src) : "memory");
 }
+// D += A B for one 8x8x4 FP64 tile (mma.sync, SASS DMMA): lane l holds
+// A[l/4][l%4], B[l%4][l/4] and D[l/4][2(l%4) + {0,1}]
+__device__ __forceinline__ void dmma_884(double (&d)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(d[0]), "+d"(d[1])
+               : "d"(a), "d"(b));
+}
+
+__device__ __forceinline__ void cp_async16(double* dst, const double* src) {
+  const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(src) : "memory");
+}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
@@ -364,14 +376,13 @@ __global__ void __launch_bounds__(kLuThreads) lb_getrs_slab_kernel(int n, int m,
                                                                    double* const* __restrict__ Xs) {
   static_assert(KB * W / 4 <= kLuThreads, "one diagonal-block output group per thread");
   constexpr int KH = KB / 2, CG = W / 4;  // k-half, column groups of 4
-  constexpr int kMaxTiles = 3;           // row tiles per thread: ceil(ceil(383/4) CG / NT)
   extern __shared__ __align__(16) double lu_sm[];
   const int ld = lu_ld<KB>(n);
   double* X = lu_sm;                       // [ld][W]
   double* H[2] = {X + (size_t)ld * W, X + (size_t)ld * W + (size_t)KH * ld};  // [KH][ld] each
   double* Dib[2] = {H[1] + (size_t)KH * ld, H[1] + (size_t)KH * ld + KB * KB};  // [KB][KB]
   double* Y = Dib[1] + KB * KB;            // [KB][W]
-  const int b = blockIdx.x, s = blockIdx.y, tid = threadIdx.x;
+  const int b = blockIdx.x, s = blockIdx.y, tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int col0 = s * W, wc = min(W, m - col0);
   if (wc <= 0) return;
   const double* A = As[b];
@@ -388,22 +399,30 @@ __global__ void __launch_bounds__(kLuThreads) lb_getrs_slab_kernel(int n, int m,
     hi = fwd ? n : r0;
   };
   // issue the copies of half h of step q's factor block (and its Di when h == 1)
+  // 16-byte copies of row pairs when every column start is 16-byte aligned
+  // (n even; the row ranges start at multiples of KB or at n - r0 = kb even)
+  const bool pairs = (n & 1) == 0 && (reinterpret_cast<uintptr_t>(A) & 15) == 0;
   auto issue = [&](int q, int h) {
     int p, r0, kb, lo, hi;
     geom(q, p, r0, kb, lo, hi);
-    const int rows = hi - lo;
     double* dst = H[h];
-    for (int k = 0; k < KH; ++k) {
-      const int kk = h * KH + k;
-      if (kk >= kb) break;
-      const double* src = A + (size_t)(r0 + kk) * n;
-      for (int i = lo + tid; i < hi; i += kLuThreads) cp_async8(dst + (size_t)k * ld + i, src + i);
+    const int k_end = min(KH, kb - h * KH);
+    if (pairs) {
+      const int np2 = (hi - lo) >> 1;  // row pairs (hi - lo is even)
+      for (int t = tid; t < k_end * np2; t += kLuThreads) {
+        const int k = t / np2, i = lo + 2 * (t - k * np2);
+        cp_async16(dst + (size_t)k * ld + i, A + (size_t)(r0 + h * KH + k) * n + i);
+      }
+    } else {
+      for (int k = 0; k < k_end; ++k) {
+        const double* src = A + (size_t)(r0 + h * KH + k) * n;
+        for (int i = lo + tid; i < hi; i += kLuThreads) cp_async8(dst + (size_t)k * ld + i, src + i);
+      }
     }
-    (void)rows;
     if (h == 1) {
       const double* di = inv + (size_t)(q < np ? 2 * p : 2 * p + 1) * KB * KB;
       double* dd = Dib[q & 1];
-      for (int t = tid; t < KB * KB; t += kLuThreads) cp_async8(dd + t, di + t);
+      for (int t = 2 * tid; t < KB * KB; t += 2 * kLuThreads) cp_async16(dd + t, di + t);
     }
     cp_async_commit();
   };
@@ -426,23 +445,27 @@ __global__ void __launch_bounds__(kLuThreads) lb_getrs_slab_kernel(int n, int m,
     cp_async_wait<0>();  // H1(q) and Di(q) (H0(q) landed earlier)
     __syncthreads();
     LU_T(1);
-    // Y = Di X[r0 : r0 + kb]
+    // Y = Di X[r0 : r0 + kb] on the FP64 tensor path (mma.m8n8k4.f64):
+    // 4 x (W/8) tiles of 8 x 8, two per warp
     const double* Di = Dib[q & 1];
-    if (tid < KB * CG) {
-      double a0 = 0, a1 = 0, a2 = 0, a3 = 0;
+    {
+      static_assert(KB == 32 && W == 32, "DMMA tiling assumes 32 x 32 blocks");
+      const int m = warp >> 1, n0 = (warp & 1) * 2, lr = lane >> 2, lk = lane & 3;
+      double d[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
 #pragma unroll
-      for (int k = 0; k < KB; ++k) {
-        if (k >= kb) break;
-        const double dk = Di[(size_t)k * KB + yi];
-        const double2 x01 = *reinterpret_cast<const double2*>(X + (size_t)(r0 + k) * W + yc);
-        const double2 x23 = *reinterpret_cast<const double2*>(X + (size_t)(r0 + k) * W + yc + 2);
-        a0 = fma(dk, x01.x, a0);
-        a1 = fma(dk, x01.y, a1);
-        a2 = fma(dk, x23.x, a2);
-        a3 = fma(dk, x23.y, a3);
+      for (int k0 = 0; k0 < KB; k0 += 4) {
+        const int k = k0 + lk;
+        const double av = Di[(size_t)k * KB + 8 * m + lr];
+#pragma unroll
+        for (int nn = 0; nn < 2; ++nn) {
+          const double bv = k < kb ? X[(size_t)(r0 + k) * W + 8 * (n0 + nn) + lr] : 0.0;
+          dmma_884(d[nn], av, bv);
+        }
       }
-      *reinterpret_cast<double2*>(Y + (size_t)yi * W + yc) = make_double2(a0, a1);
-      *reinterpret_cast<double2*>(Y + (size_t)yi * W + yc + 2) = make_double2(a2, a3);
+#pragma unroll
+      for (int nn = 0; nn < 2; ++nn)
+        *reinterpret_cast<double2*>(Y + (size_t)(8 * m + lr) * W + 8 * (n0 + nn) + 2 * lk) =
+            make_double2(d[nn][0], d[nn][1]);
     }
     __syncthreads();
     if (tid < KB * CG && yi < kb) {  // the block's rows of X become Y
@@ -452,38 +475,39 @@ __global__ void __launch_bounds__(kLuThreads) lb_getrs_slab_kernel(int n, int m,
           *reinterpret_cast<const double2*>(Y + (size_t)yi * W + yc + 2);
     }
     LU_T(2);
-    // X[lo:hi] -= F Y in two k-halves; tiles of 4 rows x 4 columns
-    const int nr = hi - lo, ntile = ((nr + 3) >> 2) * CG;
-    double acc[kMaxTiles][4][4];
+    // X[lo:hi] -= F Y in two k-halves on the FP64 tensor path: warp tiles of
+    // 16 rows x 32 columns (2 x 4 MMA tiles of 8 x 8), acc kept across halves
+    const int nr = hi - lo, nwt = (nr + 15) >> 4;
+    constexpr int kMaxWt = 3;  // ceil(ceil(383 / 16) / 8)
+    double acc[kMaxWt][2][4][2];
 #pragma unroll
-    for (int u = 0; u < kMaxTiles; ++u)
+    for (int u = 0; u < kMaxWt; ++u)
 #pragma unroll
-      for (int r = 0; r < 4; ++r)
+      for (int mm = 0; mm < 2; ++mm)
 #pragma unroll
-        for (int c = 0; c < 4; ++c) acc[u][r][c] = 0.0;
+        for (int nn = 0; nn < 4; ++nn) acc[u][mm][nn][0] = acc[u][mm][nn][1] = 0.0;
+    const int lr = lane >> 2, lk = lane & 3;
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
-      const int k0 = h * KH, k1 = min(kb, k0 + KH);
-      const double* Hh = H[h];
+      const int k1 = min(kb, (h + 1) * KH);
+      const double* Hh = H[h] + lo;
 #pragma unroll
-      for (int u = 0; u < kMaxTiles; ++u) {
-        const int t = tid + u * kLuThreads;
-        if (t >= ntile) break;
-        const int ri = (t / CG) * 4, c = (t - (t / CG) * CG) * 4;
+      for (int u = 0; u < kMaxWt; ++u) {
+        const int wt = warp + u * (kLuThreads / 32);
+        if (wt >= nwt) break;
 #pragma unroll
-        for (int kk = 0; kk < KH; ++kk) {
-          const int k = k0 + kk;
-          if (k >= k1) break;
-          const double2 y01 = *reinterpret_cast<const double2*>(Y + (size_t)k * W + c);
-          const double2 y23 = *reinterpret_cast<const double2*>(Y + (size_t)k * W + c + 2);
-          const double2 f01 = *reinterpret_cast<const double2*>(Hh + (size_t)(k - k0) * ld + lo + ri);
-          const double2 f23 = *reinterpret_cast<const double2*>(Hh + (size_t)(k - k0) * ld + lo + ri + 2);
-          const double yv[4] = {y01.x, y01.y, y23.x, y23.y};
-          const double fv[4] = {f01.x, f01.y, f23.x, f23.y};
+        for (int kq = 0; kq < KH; kq += 4) {
+          const int k = h * KH + kq + lk;
+          double av[2], bv[4];
 #pragma unroll
-          for (int r = 0; r < 4; ++r)
+          for (int mm = 0; mm < 2; ++mm)
+            av[mm] = k < k1 ? Hh[(size_t)(kq + lk) * ld + 16 * wt + 8 * mm + lr] : 0.0;
 #pragma unroll
-            for (int cc = 0; cc < 4; ++cc) acc[u][r][cc] = fma(fv[r], yv[cc], acc[u][r][cc]);
+          for (int nn = 0; nn < 4; ++nn) bv[nn] = Y[(size_t)k * W + 8 * nn + lr];
+#pragma unroll
+          for (int mm = 0; mm < 2; ++mm)
+#pragma unroll
+            for (int nn = 0; nn < 4; ++nn) dmma_884(acc[u][mm][nn], av[mm], bv[nn]);
         }
       }
       if (h == 0) {
@@ -493,18 +517,19 @@ __global__ void __launch_bounds__(kLuThreads) lb_getrs_slab_kernel(int n, int m,
     }
     LU_T(3);
 #pragma unroll
-    for (int u = 0; u < kMaxTiles; ++u) {
-      const int t = tid + u * kLuThreads;
-      if (t >= ntile) break;
-      const int ri = (t / CG) * 4, c = (t - (t / CG) * CG) * 4;
+    for (int u = 0; u < kMaxWt; ++u) {
+      const int wt = warp + u * (kLuThreads / 32);
+      if (wt >= nwt) break;
 #pragma unroll
-      for (int r = 0; r < 4; ++r) {
-        if (ri + r >= nr) break;
-        double* xr = X + (size_t)(lo + ri + r) * W + c;
-        const double2 x01 = *reinterpret_cast<const double2*>(xr);
-        const double2 x23 = *reinterpret_cast<const double2*>(xr + 2);
-        *reinterpret_cast<double2*>(xr) = make_double2(x01.x - acc[u][r][0], x01.y - acc[u][r][1]);
-        *reinterpret_cast<double2*>(xr + 2) = make_double2(x23.x - acc[u][r][2], x23.y - acc[u][r][3]);
+      for (int mm = 0; mm < 2; ++mm) {
+        const int R = 16 * wt + 8 * mm + lr;
+        if (R >= nr) continue;
+#pragma unroll
+        for (int nn = 0; nn < 4; ++nn) {
+          double* xr = X + (size_t)(lo + R) * W + 8 * nn + 2 * lk;
+          const double2 x2 = *reinterpret_cast<const double2*>(xr);
+          *reinterpret_cast<double2*>(xr) = make_double2(x2.x - acc[u][mm][nn][0], x2.y - acc[u][mm][nn][1]);
+        }
       }
     }
     LU_T(4);
