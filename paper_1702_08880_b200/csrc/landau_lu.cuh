@@ -61,7 +61,7 @@ __host__ __device__ constexpr int lu_ld(int n) {
 // shared memory of lb_getrf_kernel<KB>: panel [KB][ld] + U12 rows [KB][ld] + reduction scratch
 template <int KB>
 inline size_t getrf_smem_bytes(int n) {
-  return sizeof(double) * (2 * (size_t)KB * lu_ld<KB>(n) + 2 * 32) +
+  return sizeof(double) * (2 * (size_t)KB * lu_ld<KB>(n) + 2 * 32 + KB * KB) +
          sizeof(int) * (KB + 32 + lu_ld<KB>(n) + 4 * KB);
 }
 
@@ -70,6 +70,14 @@ inline size_t getrf_smem_bytes(int n) {
 template <int KB>
 __host__ __device__ inline int lu_inv_stride(int n) {
   return 2 * ((n + KB - 1) / KB) * KB * KB;
+}
+
+// D += A B for one 8x8x4 FP64 tile (mma.sync, SASS DMMA): lane l holds
+// A[l/4][l%4], B[l%4][l/4] and D[l/4][2(l%4) + {0,1}]
+__device__ __forceinline__ void dmma_884(double (&d)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(d[0]), "+d"(d[1])
+               : "d"(a), "d"(b));
 }
 
 template <int KB>
@@ -83,7 +91,8 @@ __global__ void __launch_bounds__(kLuThreads) lb_getrf_kernel(int n, double* con
   double* P = lu_sm;                   // panel, column-major [KB][ld] (row offset from c0)
   double* Ub = lu_sm + (size_t)KB * ld;  // U12 rows, row-major [KB][ld] (column offset from c0 + w)
   double* redv = Ub + (size_t)KB * ld;   // [32]
-  int* redi = reinterpret_cast<int*>(redv + 32);  // [32]
+  double* iLs = redv + 64;               // [KB][KB] L11^-1 of the current panel (column-major)
+  int* redi = reinterpret_cast<int*>(iLs + KB * KB);  // [32]
   int* pv_sh = redi + 32;                         // [KB]
   int* lp = pv_sh + KB;                           // [ld] panel-local row permutation
   int* tl_dst = lp + ld;                          // [2 KB] rows a panel's swaps touch
@@ -189,31 +198,35 @@ __global__ void __launch_bounds__(kLuThreads) lb_getrf_kernel(int n, double* con
     {
       double* iL = inv + (size_t)(2 * p) * KB * KB;
       double* iU = iL + KB * KB;
-      if (tid < KB) {  // column tid of L11^-1: forward substitution of e_tid
+      if (tid < KB) {  // column tid of L11^-1: right-looking forward substitution of e_tid
         const int c = tid;
         double x[KB];
 #pragma unroll
+        for (int i = 0; i < KB; ++i) x[i] = (i == c) ? 1.0 : 0.0;
+#pragma unroll
+        for (int k = 0; k < KB; ++k)  // x[k] is final; eliminate it from the rows below
+#pragma unroll
+          for (int i = k + 1; i < KB; ++i) x[i] = fma(-P[(size_t)k * ld + i], x[k], x[i]);
+#pragma unroll
         for (int i = 0; i < KB; ++i) {
-          double s = (i == c) ? 1.0 : 0.0;
-#pragma unroll
-          for (int k = 0; k < i; ++k) s = fma(-P[(size_t)k * ld + i], x[k], s);
-          x[i] = (i < w) ? s : 0.0;
+          const double v = (c < w && i < w) ? x[i] : 0.0;
+          iL[(size_t)c * KB + i] = v;
+          iLs[(size_t)c * KB + i] = v;
         }
-#pragma unroll
-        for (int i = 0; i < KB; ++i) iL[(size_t)c * KB + i] = (c < w) ? x[i] : 0.0;
-      } else if (tid >= 32 && tid < 32 + KB) {  // column c of U11^-1: back substitution of e_c
+      } else if (tid >= 32 && tid < 32 + KB) {  // column c of U11^-1: right-looking back substitution of e_c
         const int c = tid - 32;
         double x[KB];
 #pragma unroll
-        for (int i = KB - 1; i >= 0; --i) {
-          double s = (i == c) ? 1.0 : 0.0;
+        for (int i = 0; i < KB; ++i) x[i] = (i == c) ? 1.0 : 0.0;
 #pragma unroll
-          for (int k = i + 1; k < KB; ++k) s = fma(-P[(size_t)k * ld + i], x[k], s);
-          const double dii = (i < w) ? P[(size_t)i * ld + i] : 1.0;
-          x[i] = (i < w && c < w) ? s / dii : 0.0;
+        for (int k = KB - 1; k >= 0; --k) {
+          const double dkk = (k < w) ? P[(size_t)k * ld + k] : 1.0;
+          x[k] = x[k] / dkk;
+#pragma unroll
+          for (int i = 0; i < k; ++i) x[i] = fma(-P[(size_t)k * ld + i], x[k], x[i]);
         }
 #pragma unroll
-        for (int i = 0; i < KB; ++i) iU[(size_t)c * KB + i] = x[i];
+        for (int i = 0; i < KB; ++i) iU[(size_t)c * KB + i] = (c < w && i < w) ? x[i] : 0.0;
       }
     }
     LU_T(2);
@@ -224,91 +237,172 @@ __global__ void __launch_bounds__(kLuThreads) lb_getrf_kernel(int n, double* con
     // pivot row pv[j] when it lies below the panel's first w rows (first
     // occurrence only), its source lp[pv[j]] (always one of rows 0..w-1);
     // unused entries have source -1
-    if (tid < w) {
-      tl_dst[tid] = tid;
-      tl_src[tid] = lp[tid];
-      const int r = pv_sh[tid];
-      bool first = pivot && r >= w;
-      for (int q = 0; q < tid && first; ++q) first = pv_sh[q] != r;
-      tl_dst[w + tid] = r;
-      tl_src[w + tid] = first ? lp[r] : -1;
-    }
-    __syncthreads();
+    // (warps 0 and 1 are still computing the diagonal-block inverses: the
+    // list and the gather run on warps 2..7, synchronised by named barrier 1)
     const int cnt = 2 * w;
     const int n2 = n - c0 - w;
-    for (int k = tid; k < n - w; k += kLuThreads) {
-      const int col = k < c0 ? k : k + w;  // skip the panel's own columns
-      double* Ac = A + (size_t)col * n + c0;
-      double v[2 * KB];
-#pragma unroll
-      for (int q = 0; q < 2 * KB; ++q) {
-        const int sq = q < cnt ? tl_src[q] : -1;
-        v[q] = sq >= 0 ? Ac[sq] : 0.0;
+    constexpr int kGW = NW - 2;  // gather warps
+    if (warp >= 2) {
+      const int j = tid - 64;
+      if (j < w) {
+        tl_dst[j] = j;
+        tl_src[j] = lp[j];
+        const int r = pv_sh[j];
+        bool first = pivot && r >= w;
+        for (int q = 0; q < j && first; ++q) first = pv_sh[q] != r;
+        tl_dst[w + j] = r;
+        tl_src[w + j] = first ? lp[r] : -1;
       }
-      if (col >= c0 + w) {  // the first w entries are rows 0..w-1 in order
+      asm volatile("bar.sync 1, %0;" ::"n"(kGW * 32) : "memory");
+    // gather: one warp per column, lane q (and q + 32) owns list entry q:
+    // the column's touched rows are read together (one coalesced segment
+    // for rows c0..c0+w, a few sectors for the pivot rows), then written;
+    // the first w rows of a right column go to Ub for the U12 product
+    {
+      const int s0 = lane < cnt ? tl_src[lane] : -1, s1 = lane + 32 < cnt ? tl_src[lane + 32] : -1;
+      const int d0 = tl_dst[lane], d1 = tl_dst[lane + 32];
+      const int kbeg = pivot ? 0 : c0;  // left columns only need the swaps
+      constexpr int CB = 16;            // columns in flight per warp
+      for (int kb0 = kbeg + (warp - 2) * CB; kb0 < n - w; kb0 += kGW * CB) {
+        double v0[CB], v1[CB];
 #pragma unroll
-        for (int i = 0; i < KB; ++i) {
-          double sacc = v[i];
-#pragma unroll
-          for (int q = 0; q < i; ++q) sacc = fma(-P[(size_t)q * ld + i], v[q], sacc);
-          v[i] = (i < w) ? sacc : 0.0;
+        for (int u = 0; u < CB; ++u) {
+          const int k = kb0 + u;
+          const int col = k < c0 ? k : k + w;  // skip the panel's own columns
+          const double* Ac = A + (size_t)col * n + c0;
+          const bool ok = k < n - w;
+          v0[u] = (ok && s0 >= 0) ? Ac[s0] : 0.0;
+          v1[u] = (ok && s1 >= 0) ? Ac[s1] : 0.0;
         }
-        const int k2 = col - c0 - w;
+        __syncwarp();
 #pragma unroll
-        for (int i = 0; i < KB; ++i) Ub[(size_t)i * ld + k2] = v[i];
-      } else if (!pivot) {
-        continue;  // left columns: nothing to do without swaps
+        for (int u = 0; u < CB; ++u) {
+          const int k = kb0 + u;
+          if (k >= n - w) break;
+          const int col = k < c0 ? k : k + w;
+          double* Ac = A + (size_t)col * n + c0;
+          const bool right = col >= c0 + w;
+          if (s0 >= 0 && !(right && lane < w)) Ac[d0] = v0[u];
+          if (s1 >= 0 && !(right && lane + 32 < w)) Ac[d1] = v1[u];
+          if (right) Ub[(size_t)lane * ld + (col - c0 - w)] = (lane < w) ? v0[u] : 0.0;
+        }
       }
-#pragma unroll
-      for (int q = 0; q < 2 * KB; ++q)
-        if (q < cnt && tl_src[q] >= 0) Ac[tl_dst[q]] = v[q];
     }
-    // zero padding of Ub's columns n2..ld (8-column tiles read them)
-    for (int t = tid; t < KB * 8; t += kLuThreads) {
-      const int i = t >> 3, k2 = n2 + (t & 7);
+    }
+    __syncthreads();
+    LU_T(5);
+    // U12 = L11^-1 A12 on the FP64 tensor path: warp tiles of 32 rows x 16
+    // columns (4 x 2 MMA tiles), written to Ub and back to A's rows c0..c0+w
+    {
+      const int lk = lane & 3, lr = lane >> 2;
+      constexpr int kMaxU = 3;  // ceil(ceil(383 / 16) / NW)
+      double acc[kMaxU][4][2][2];
+      const int nwt = (n2 + 15) >> 4;
+#pragma unroll
+      for (int u = 0; u < kMaxU; ++u) {
+        const int t = warp + u * NW;
+        if (t >= nwt) break;
+        const int C0 = t * 16;
+#pragma unroll
+        for (int mm = 0; mm < 4; ++mm)
+#pragma unroll
+          for (int nn = 0; nn < 2; ++nn) acc[u][mm][nn][0] = acc[u][mm][nn][1] = 0.0;
+#pragma unroll
+        for (int k0 = 0; k0 < KB; k0 += 4) {
+          const int k = k0 + lk;
+          double av[4], bv[2];
+#pragma unroll
+          for (int mm = 0; mm < 4; ++mm) av[mm] = iLs[(size_t)k * KB + 8 * mm + lr];
+#pragma unroll
+          for (int nn = 0; nn < 2; ++nn) {
+            const int C = C0 + 8 * nn + lr;
+            bv[nn] = C < n2 ? Ub[(size_t)k * ld + C] : 0.0;
+          }
+#pragma unroll
+          for (int mm = 0; mm < 4; ++mm)
+#pragma unroll
+            for (int nn = 0; nn < 2; ++nn) dmma_884(acc[u][mm][nn], av[mm], bv[nn]);
+        }
+      }
+      __syncthreads();  // every Ub read done
+      LU_T(6);
+#pragma unroll
+      for (int u = 0; u < kMaxU; ++u) {
+        const int t = warp + u * NW;
+        if (t >= nwt) break;
+        const int C0 = t * 16;
+#pragma unroll
+        for (int mm = 0; mm < 4; ++mm) {
+          const int i = 8 * mm + lr;
+#pragma unroll
+          for (int nn = 0; nn < 2; ++nn)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+              const int C = C0 + 8 * nn + 2 * lk + e;
+              if (C < n2) {
+                Ub[(size_t)i * ld + C] = acc[u][mm][nn][e];
+                if (i < w) A[(size_t)(c0 + w + C) * n + c0 + i] = acc[u][mm][nn][e];
+              }
+            }
+        }
+      }
+    }
+    // zero padding of Ub's columns n2..n2+31 (32-column warp tiles read them)
+    for (int t = tid; t < KB * 32; t += kLuThreads) {
+      const int i = t >> 5, k2 = n2 + (t & 31);
       if (k2 < ld) Ub[(size_t)i * ld + k2] = 0.0;
     }
     __syncthreads();
     LU_T(3);
-    // 6. trailing update A22 -= L21 U12 (8 x 8 register tiles)
+    // 6. trailing update A22 -= L21 U12 on the FP64 tensor path
+    //    (mma.m8n8k4.f64): warp tiles of 16 rows x 32 columns (2 x 4 MMA
+    //    tiles), accumulators start from the tile's current values
     const int m2 = m - w;
     if (m2 > 0 && n2 > 0) {
-      const int tr = (m2 + 7) >> 3, tc = (n2 + 7) >> 3;
-      for (int t = tid; t < tr * tc; t += kLuThreads) {
-        const int ti = (t / tc) * 8, tk = (t - (t / tc) * tc) * 8;
-        // the tile's current values first (one round of independent loads)
-        double acc[8][8];
+      static_assert(KB % 4 == 0, "k steps of 4");
+      const int lr = lane & 31 ? lane >> 2 : 0, lk = lane & 3;
+      const int twr = (m2 + 15) >> 4, twc = (n2 + 31) >> 5;
+      for (int t = warp; t < twr * twc; t += NW) {
+        const int R0 = (t / twc) * 16, C0 = (t - (t / twc) * twc) * 32;
+        double acc[2][4][2];
 #pragma unroll
-        for (int c = 0; c < 8; ++c) {
-          const double* Ac = A + (size_t)(c0 + w + tk + c) * n + c0 + w + ti;
+        for (int mm = 0; mm < 2; ++mm) {
+          const int R = R0 + 8 * mm + (lane >> 2);
 #pragma unroll
-          for (int r = 0; r < 8; ++r) acc[c][r] = (tk + c < n2 && ti + r < m2) ? Ac[r] : 0.0;
-        }
-        for (int j = 0; j < w; ++j) {
-          const double* lp = P + (size_t)j * ld + w + ti;  // L21[ti..ti+8][j]
-          const double* up = Ub + (size_t)j * ld + tk;     // U12[j][tk..tk+8]
-          double lv[8], uv[8];
+          for (int nn = 0; nn < 4; ++nn)
 #pragma unroll
-          for (int q = 0; q < 8; q += 2) {
-            const double2 a2 = *reinterpret_cast<const double2*>(lp + q);
-            const double2 u2 = *reinterpret_cast<const double2*>(up + q);
-            lv[q] = a2.x; lv[q + 1] = a2.y;
-            uv[q] = u2.x; uv[q + 1] = u2.y;
-          }
-#pragma unroll
-          for (int c = 0; c < 8; ++c)
-#pragma unroll
-            for (int r = 0; r < 8; ++r) acc[c][r] = fma(-lv[r], uv[c], acc[c][r]);
+            for (int e = 0; e < 2; ++e) {
+              const int C = C0 + 8 * nn + 2 * lk + e;
+              acc[mm][nn][e] = (R < m2 && C < n2) ? A[(size_t)(c0 + w + C) * n + c0 + w + R] : 0.0;
+            }
         }
 #pragma unroll
-        for (int c = 0; c < 8; ++c) {
-          if (tk + c >= n2) break;
-          double* Ac = A + (size_t)(c0 + w + tk + c) * n + c0 + w + ti;
+        for (int k0 = 0; k0 < KB; k0 += 4) {
+          const int k = k0 + lk;
+          double av[2], bv[4];
 #pragma unroll
-          for (int r = 0; r < 8; ++r)
-            if (ti + r < m2) Ac[r] = acc[c][r];
+          for (int mm = 0; mm < 2; ++mm) av[mm] = -P[(size_t)k * ld + w + R0 + 8 * mm + (lane >> 2)];
+#pragma unroll
+          for (int nn = 0; nn < 4; ++nn) bv[nn] = Ub[(size_t)k * ld + C0 + 8 * nn + (lane >> 2)];
+#pragma unroll
+          for (int mm = 0; mm < 2; ++mm)
+#pragma unroll
+            for (int nn = 0; nn < 4; ++nn) dmma_884(acc[mm][nn], av[mm], bv[nn]);
+        }
+#pragma unroll
+        for (int mm = 0; mm < 2; ++mm) {
+          const int R = R0 + 8 * mm + (lane >> 2);
+          if (R >= m2) continue;
+#pragma unroll
+          for (int nn = 0; nn < 4; ++nn)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+              const int C = C0 + 8 * nn + 2 * lk + e;
+              if (C < n2) A[(size_t)(c0 + w + C) * n + c0 + w + R] = acc[mm][nn][e];
+            }
         }
       }
+      (void)lr;
     }
     __syncthreads();
     LU_T(4);
@@ -352,13 +446,6 @@ inline size_t getrs_smem_bytes(int n) {
 __device__ __forceinline__ void cp_async8(double* dst, const double* src) {
   const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(d), "l"(src) : "memory");
-}
-// D += A B for one 8x8x4 FP64 tile (mma.sync, SASS DMMA): lane l holds
-// A[l/4][l%4], B[l%4][l/4] and D[l/4][2(l%4) + {0,1}]
-__device__ __forceinline__ void dmma_884(double (&d)[2], double a, double b) {
-  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
-               : "+d"(d[0]), "+d"(d[1])
-               : "d"(a), "d"(b));
 }
 
 __device__ __forceinline__ void cp_async16(double* dst, const double* src) {

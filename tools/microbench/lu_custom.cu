@@ -57,8 +57,9 @@ int main(int argc, char** argv) {
       cudaMemcpyFromSymbol(h, lu_prof, sizeof(h));
       long long tot = 0;
       for (int k = 0; k < 5; ++k) tot += h[k];
-      printf("prof n=%d: load %lld factor %lld store+inv %lld swap+U12 %lld update %lld cycles (total %lld = %.1f us at 1.9 GHz)\n",
-             n, h[0], h[1], h[2], h[3], h[4], tot, tot / 1.9e3);
+      tot += h[5] + h[6];
+      printf("prof n=%d: load %lld factor %lld store+inv %lld gather %lld U12 %lld U12-store %lld update %lld cycles (total %lld = %.1f us at 1.9 GHz)\n",
+             n, h[0], h[1], h[2], h[5], h[6], h[3], h[4], tot, tot / 1.9e3);
       // the slab solve of 2n right-hand sides with these factors
       double* B;
       cudaMalloc(&B, (size_t)n * 2 * n * 8);
