@@ -1586,11 +1586,15 @@ static int cn_solve_issue(lb_cn* cn, cudaStream_t st, bool pivot) {
   const double one = 1.0, mone = -1.0;
   int hinfo = 0;
   LB_BLAS(cublasSetStream(cn->blas, st));
-  const bool small = cn_small(cn);
+  const bool small = cn_small(cn), custom = cn_custom_lu(cn);
   for (const CnLevel& L : cn->lv) {
-    if (small && L.solveY.count) {
+    if (small && L.solveY.count) {  // blocks of <= 96 rows: whole factor in shared memory
       lb_small_solve_kernel<<<L.solveY.count, kSmallThreads, small_solve_smem_bytes(nb), st>>>(
           nb, L.solveY.count, L.getrf.A, pivot ? L.piv : nullptr, L.solveY.B);
+      LB_CUDA(cudaGetLastError());
+    } else if (custom && L.solveY.count) {  // larger blocks with the custom LU's factors
+      lb_lu_vsolve_kernel<kLuKB><<<L.solveY.count, kLuThreads, sizeof(double) * nb, st>>>(
+          nb, L.solveY.count, L.getrf.A, L.perm, L.inv, L.solveY.B);
       LB_CUDA(cudaGetLastError());
     } else if (L.solveY.count && pivot) {
       LB_BLAS(cublasDgetrsBatched(cn->blas, CUBLAS_OP_N, nb, 1, L.getrf.A, nb, L.piv, L.solveY.B, nb, &hinfo,

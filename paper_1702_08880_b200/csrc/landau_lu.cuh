@@ -631,4 +631,73 @@ __global__ void __launch_bounds__(kLuThreads) lb_getrs_slab_kernel(int n, int m,
     for (int i = tid; i < n; i += kLuThreads) Xg[(size_t)c * n + i] = X[(size_t)i * W + c];
 }
 
+// v := A^-1 v for one vector per block (the cyclic reduction's vector
+// passes), A the factors of lb_getrf_kernel: permuted gather into shared
+// memory, then block forward / backward substitution -- per 32-row block a
+// warp-synchronous substitution with the block's triangle (lane r holds
+// x_r; the same operation order as LAPACK's trsv, divisions by the U
+// diagonal), then the rows still to update by one thread per row, the
+// block's 32 factor entries of that row read in one round of coalesced
+// loads.  (The explicit diagonal-block inverses of the many-column solve
+// are not used here: for the ill-conditioned electron systems of config 4
+// the vector pass needs the substitution's accuracy.)
+template <int KB>
+__global__ void __launch_bounds__(kLuThreads) lb_lu_vsolve_kernel(int n, int count, double* const* __restrict__ As,
+                                                                  const int* __restrict__ perm_all,
+                                                                  const double* __restrict__ inv_all,
+                                                                  double* const* __restrict__ Vs) {
+  extern __shared__ __align__(16) double lu_sm[];
+  double* x = lu_sm;  // [n]
+  const int b = blockIdx.x, tid = threadIdx.x;
+  if (b >= count) return;
+  const double* A = As[b];
+  const int* perm = perm_all + (size_t)b * n;
+  const double* inv = inv_all + (size_t)b * lu_inv_stride<KB>(n);
+  double* v = Vs[b];
+  for (int i = tid; i < n; i += kLuThreads) x[i] = v[perm[i]];
+  const int np = (n + KB - 1) / KB;
+  for (int q = 0; q < 2 * np; ++q) {
+    const bool fwd = q < np;
+    const int p = fwd ? q : 2 * np - 1 - q;
+    const int r0 = p * KB, kb = min(KB, n - r0);
+    const int lo = fwd ? r0 + kb : 0, hi = fwd ? n : r0;
+    __syncthreads();
+    if (tid < 32) {  // the diagonal block's triangle, warp 0
+      static_assert(KB == 32, "one lane per block row");
+      const int r = tid;
+      double xr = r < kb ? x[r0 + r] : 0.0;
+      double t[KB];  // column k of the block at row r
+#pragma unroll
+      for (int k = 0; k < KB; ++k) t[k] = (k < kb && r < kb) ? A[(size_t)(r0 + k) * n + r0 + r] : 0.0;
+      if (fwd) {
+#pragma unroll
+        for (int k = 0; k < KB; ++k) {
+          const double xk = __shfl_sync(0xffffffffu, xr, k);
+          if (r > k && k < kb) xr = fma(-t[k], xk, xr);
+        }
+      } else {
+#pragma unroll
+        for (int k = KB - 1; k >= 0; --k) {
+          if (r == k && k < kb) xr = xr / t[k];
+          const double xk = __shfl_sync(0xffffffffu, xr, k);
+          if (r < k && k < kb) xr = fma(-t[k], xk, xr);
+        }
+      }
+      if (r < kb) x[r0 + r] = xr;
+    }
+    __syncthreads();
+    for (int i = lo + tid; i < hi; i += kLuThreads) {
+      double f[KB];
+#pragma unroll
+      for (int k = 0; k < KB; ++k) f[k] = k < kb ? A[(size_t)(r0 + k) * n + i] : 0.0;
+      double acc = x[i];
+#pragma unroll
+      for (int k = 0; k < KB; ++k) acc = fma(-f[k], x[r0 + (k < kb ? k : 0)], acc);
+      x[i] = acc;
+    }
+  }
+  __syncthreads();
+  for (int i = tid; i < n; i += kLuThreads) v[i] = x[i];
+}
+
 }  // namespace lb
