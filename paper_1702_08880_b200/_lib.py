@@ -10,7 +10,10 @@ from __future__ import annotations
 
 import ctypes as C
 import os
+import atexit
+import sys
 import threading
+import weakref
 from pathlib import Path
 
 import numpy as np
@@ -141,6 +144,7 @@ class Context:
         self.handle = h
         self.device = int(device)
         self._lib = lib
+        register_native(self, 2)
 
     def close(self):
         if getattr(self, "handle", None):
@@ -148,6 +152,8 @@ class Context:
             self.handle = None
 
     def __del__(self):  # pragma: no cover - interpreter teardown order varies
+        if finalizing():
+            return
         try:
             self.close()
         except Exception:
@@ -155,6 +161,35 @@ class Context:
 
 
 _tls = threading.local()
+
+# Native objects are released in dependency order (CN solvers, then meshes,
+# then contexts) by an atexit hook, before interpreter finalization: a
+# __del__ during finalization can run after the context an object uses was
+# destroyed (garbage-collection order at shutdown is arbitrary), so __del__
+# does nothing once the interpreter is finalizing.
+_NATIVE: "list[weakref.WeakSet]" = []
+
+
+def register_native(obj, level: int) -> None:
+    """Track `obj` (with a close() method) for release at exit; lower levels
+    are released first (0 solvers, 1 meshes, 2 contexts)."""
+    while len(_NATIVE) <= level:
+        _NATIVE.append(weakref.WeakSet())
+    _NATIVE[level].add(obj)
+
+
+@atexit.register
+def _release_native() -> None:
+    for objs in _NATIVE:
+        for o in list(objs):
+            try:
+                o.close()
+            except Exception:
+                pass
+
+
+def finalizing() -> bool:
+    return sys.is_finalizing()
 
 
 def context(device: int | None = None) -> Context:

@@ -108,6 +108,7 @@ class DeviceMesh:
             _lib.iptr(gm.slot_ptr), int(gm.gather_idx.shape[0]), _lib.iptr(gm.gather_idx),
             _lib.dptr(gm.gather_w), _lib.C.byref(h)))
         self.handle = h
+        _lib.register_native(self, 1)
         self.n_free = gm.n_free
         self.has_geometry = all(hasattr(mesh, a) for a in ("origins",)) and all(
             hasattr(ref, a) for a in ("qpts", "qwts"))
@@ -129,6 +130,8 @@ class DeviceMesh:
             self.handle = None
 
     def __del__(self):  # pragma: no cover
+        if _lib.finalizing():
+            return
         try:
             self.close()
         except Exception:

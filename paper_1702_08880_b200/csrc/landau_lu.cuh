@@ -127,16 +127,21 @@ __global__ void __launch_bounds__(kLuThreads) lb_getrf_kernel(int n, double* con
     }
     __syncthreads();
     LU_T(0);
-    // 2. unblocked LU of the panel
+    // 2. unblocked LU of the panel.  The rank-1 update of column j and the
+    //    pivot search of column j+1 are one pass (each thread takes the
+    //    largest |a| of column j+1 over the rows it just updated), so a
+    //    column costs two barriers: after the warps' pivot candidates, and
+    //    after the row swap.
+    double best = -1.0;
+    int bi = m;
+    if (pivot)
+      for (int i = tid; i < m; i += kLuThreads) {
+        const double v = fabs(P[i]);
+        if (v > best) { best = v; bi = i; }  // rows visited in increasing order
+      }
     for (int j = 0; j < w; ++j) {
       int piv = j;
       if (pivot) {
-        double best = -1.0;
-        int bi = m;
-        for (int i = j + tid; i < m; i += kLuThreads) {
-          const double v = fabs(P[(size_t)j * ld + i]);
-          if (v > best) { best = v; bi = i; }  // rows visited in increasing order
-        }
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {
           const double ov = __shfl_xor_sync(0xffffffffu, best, o);
@@ -170,24 +175,33 @@ __global__ void __launch_bounds__(kLuThreads) lb_getrf_kernel(int n, double* con
       const double d = P[(size_t)j * ld + j];
       if (d == 0.0 && info == 0) info = c0 + j + 1;  // LAPACK info (first zero pivot)
       const double r = d != 0.0 ? 1.0 / d : 0.0;     // zero pivot: the column below is zero too
+      best = -1.0;
+      bi = m;
       for (int i = j + 1 + tid; i < m; i += kLuThreads) {
         const double l = P[(size_t)j * ld + i] * r;
         P[(size_t)j * ld + i] = l;
         int k = j + 1;
+        if (k < w) {  // column j+1 first: the next pivot candidate
+          const double v = fma(-l, P[(size_t)k * ld + j], P[(size_t)k * ld + i]);
+          P[(size_t)k * ld + i] = v;
+          if (fabs(v) > best) { best = fabs(v); bi = i; }
+          ++k;
+        }
         for (; k + 4 <= w; k += 4) {  // four independent read-modify-writes per round
-          double a[4], u[4];
+          double a4[4], u4[4];
 #pragma unroll
           for (int q = 0; q < 4; ++q) {
-            a[q] = P[(size_t)(k + q) * ld + i];
-            u[q] = P[(size_t)(k + q) * ld + j];
+            a4[q] = P[(size_t)(k + q) * ld + i];
+            u4[q] = P[(size_t)(k + q) * ld + j];
           }
 #pragma unroll
-          for (int q = 0; q < 4; ++q) P[(size_t)(k + q) * ld + i] = fma(-l, u[q], a[q]);
+          for (int q = 0; q < 4; ++q) P[(size_t)(k + q) * ld + i] = fma(-l, u4[q], a4[q]);
         }
         for (; k < w; ++k) P[(size_t)k * ld + i] = fma(-l, P[(size_t)k * ld + j], P[(size_t)k * ld + i]);
       }
-      __syncthreads();
+      if (!pivot) __syncthreads();  // (pivoting: the next column's first barrier orders these writes)
     }
+    __syncthreads();
     LU_T(1);
     // 3. panel back; pivots (1-based, global rows)
     for (int j = 0; j < w; ++j)

@@ -114,6 +114,7 @@ class CNSolver:
             _lib.iptr(self.perm), self.nb, _lib.C.byref(h)))
         self.handle = h
         self.dm = dm
+        _lib.register_native(self, 0)
         self._mass_key = None
         self._c_old_ref = None  # CollisionMatrix whose values are resident as C_old
 
@@ -152,6 +153,8 @@ class CNSolver:
             self.handle = None
 
     def __del__(self):  # pragma: no cover
+        if _lib.finalizing():
+            return
         try:
             self.close()
         except Exception:
