@@ -151,8 +151,8 @@ class Context:
             self._lib.lb_ctx_destroy(self.handle)
             self.handle = None
 
-    def __del__(self):  # pragma: no cover - interpreter teardown order varies
-        if finalizing():
+    def __del__(self, _finalizing=sys.is_finalizing):  # pragma: no cover - teardown order varies
+        if _finalizing():  # bound at definition: module globals may be gone at shutdown
             return
         try:
             self.close()

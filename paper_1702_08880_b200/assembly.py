@@ -20,6 +20,8 @@ import time
 from collections import OrderedDict
 from dataclasses import dataclass, field
 
+import sys
+
 import numpy as np
 import scipy.sparse as sp
 
@@ -129,8 +131,8 @@ class DeviceMesh:
             self._lib.lb_mesh_destroy(self.handle)
             self.handle = None
 
-    def __del__(self):  # pragma: no cover
-        if _lib.finalizing():
+    def __del__(self, _finalizing=sys.is_finalizing):  # pragma: no cover
+        if _finalizing():  # bound at definition: module globals may be gone at shutdown
             return
         try:
             self.close()

@@ -27,6 +27,8 @@ from __future__ import annotations
 
 from collections import OrderedDict
 
+import sys
+
 import numpy as np
 import scipy.sparse as sp
 from scipy.sparse.csgraph import reverse_cuthill_mckee
@@ -152,8 +154,8 @@ class CNSolver:
             self._lib.lb_cn_destroy(self.handle)
             self.handle = None
 
-    def __del__(self):  # pragma: no cover
-        if _lib.finalizing():
+    def __del__(self, _finalizing=sys.is_finalizing):  # pragma: no cover
+        if _finalizing():  # bound at definition: module globals may be gone at shutdown
             return
         try:
             self.close()
