@@ -8,9 +8,9 @@ library or the GPU is missing, every compute call fails loudly.
 
 from __future__ import annotations
 
+import atexit
 import ctypes as C
 import os
-import atexit
 import sys
 import threading
 import weakref

@@ -16,11 +16,10 @@ dB (fem.py:50-63).  `data` must come from sampling on the same mesh
 
 from __future__ import annotations
 
+import sys
 import time
 from collections import OrderedDict
 from dataclasses import dataclass, field
-
-import sys
 
 import numpy as np
 import scipy.sparse as sp

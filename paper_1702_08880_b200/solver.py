@@ -25,9 +25,8 @@ update); `install()` routes the reference's `advance` through them.
 
 from __future__ import annotations
 
-from collections import OrderedDict
-
 import sys
+from collections import OrderedDict
 
 import numpy as np
 import scipy.sparse as sp
