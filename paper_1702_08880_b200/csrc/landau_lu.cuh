@@ -1,29 +1,31 @@
-// landau_lu.cuh -- batched dense LU with partial pivoting and the
-// many-right-hand-side solve of the Crank-Nicolson block cyclic reduction
-// (landau_b200.cu, cn_factor_issue), replacing cuBLAS getrfBatched /
-// getrsBatched / trsmBatched at the solver's block sizes (nb = 68..354).
+// landau_lu.cuh -- batched dense LU with partial pivoting and the solves of
+// the Crank-Nicolson block cyclic reduction (landau_b200.cu, cn_factor_issue
+// / cn_solve_issue), replacing cuBLAS getrfBatched / getrsBatched /
+// trsmBatched at the solver's block sizes (nb <= 384; 68..354 here).
 //
 // cuBLAS's batched getrf is a latency-bound chain of small launches per
 // column panel (~4.6 us per column at nb = 260, 1.2 ms per call whatever
-// the batch), and its batched trsm + laswp with 2 nb right-hand sides runs
-// at ~4 TFLOP/s.  Here:
+// the batch), and its batched getrs with 2 nb right-hand sides runs at a few
+// TFLOP/s.  Here:
 //  * lb_getrf_kernel: one CTA per matrix, right-looking blocked LU with a
 //    KB-column panel in shared memory.  Panel: per column one CTA-wide
 //    pivot search (LAPACK idamax: first maximum of |a|), row swap, and a
-//    row-owned scale + rank-1 update (3 barriers per column).  Then the
-//    panel's swaps on the other columns, U12 = L11^-1 A12 (one column per
-//    thread, L11 broadcast from shared memory) and the trailing update
-//    A22 -= L21 U12 with 8x8 register tiles.  Output in LAPACK layout (unit
-//    L below the diagonal, U on and above it, 1-based ipiv) so the vector
-//    solves (lb_small_solve_kernel, getrs) consume it unchanged; also the
-//    row permutation and the inverses of the KB x KB diagonal blocks of L
-//    and U (for the solve below).
+//    row-owned scale + rank-1 update fused with the next column's pivot
+//    candidates (2 barriers per column).  Then the panel's swaps on the
+//    other columns (warp-per-column gather on six warps while two warps
+//    invert the diagonal blocks of L and U), U12 = L11^-1 A12 and the
+//    trailing update A22 -= L21 U12 on the FP64 tensor path
+//    (mma.sync.m8n8k4.f64).  Output in LAPACK layout (unit L below the
+//    diagonal, U on and above it, 1-based ipiv) so the vector solves
+//    (lb_small_solve_kernel, getrs) consume it unchanged; also the row
+//    permutation and the inverses of the KB x KB diagonal blocks.
 //  * lb_getrs_slab_kernel: X := A^-1 X for an n x m block of right-hand
 //    sides (the cyclic reduction's [L U], m = 2 nb), one CTA per (matrix,
 //    W-column slab): rows gathered through the permutation into shared
 //    memory, then block forward / backward substitution in which every
-//    step is a small GEMM (the diagonal block through its stored inverse,
-//    the off-diagonal column block staged in shared memory).
+//    step is two small DMMA GEMMs (the diagonal block through its stored
+//    inverse, then the factor column block streamed in by cp.async).
+//  * lb_lu_vsolve_kernel: one vector per matrix (blocks > 96 rows).
 #pragma once
 #include <cstdint>
 
@@ -374,7 +376,7 @@ __global__ void __launch_bounds__(kLuThreads) lb_getrf_kernel(int n, double* con
     const int m2 = m - w;
     if (m2 > 0 && n2 > 0) {
       static_assert(KB % 4 == 0, "k steps of 4");
-      const int lr = lane & 31 ? lane >> 2 : 0, lk = lane & 3;
+      const int lk = lane & 3;
       const int twr = (m2 + 15) >> 4, twc = (n2 + 31) >> 5;
       for (int t = warp; t < twr * twc; t += NW) {
         const int R0 = (t / twc) * 16, C0 = (t - (t / twc) * twc) * 32;
@@ -416,7 +418,6 @@ __global__ void __launch_bounds__(kLuThreads) lb_getrf_kernel(int n, double* con
             }
         }
       }
-      (void)lr;
     }
     __syncthreads();
     LU_T(4);
