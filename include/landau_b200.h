@@ -305,6 +305,11 @@ int lb_fp64_peak(lb_ctx *ctx, double *tflops, double *ms);
  *                  solve+download.
  * lb_cn_linear_step linear_cn_step (solver.py:137-150): (M - dt/2 C) f+ =
  *                  (M + dt/2 C) f with C (S, nslots) held fixed.
+ * lb_cn_theta_step the theta method with C held fixed: (M - theta dt C) f+ =
+ *                  (M + (1 - theta) dt C) f; theta = 1/2 is lb_cn_linear_step,
+ *                  theta = 1 the backward-Euler step BASELINE configs 1-2
+ *                  name (the reference has Crank-Nicolson only; SURVEY
+ *                  8(c)(iii) composes backward Euler from its pieces).
  * Every solve first uses the block LU WITHOUT pivoting (cheaper) and accepts
  * it only if the relative backward error is <= 1e-12; otherwise the solver
  * refactorises with partial pivoting inside the diagonal blocks, and keeps
@@ -319,6 +324,8 @@ int lb_cn_newton(lb_cn *cn, const double *coK, const double *coD, double eps_d, 
                  int c_old_mode, double *f_next, double *C_guess_out, double *rnorm,
                  double *phase_ms);
 int lb_cn_linear_step(lb_cn *cn, double dt, const double *C, const double *f, double *f_out);
+int lb_cn_theta_step(lb_cn *cn, double dt, double theta, const double *C, const double *f,
+                     double *f_out);
 /* Linear-solve diagnostics: relative backward error ||(M - dt/2 C) x - b|| /
  * ||b|| of the last solve, how often the unpivoted block LU was rejected
  * (then refactorised with pivoting), and whether the solver now pivots. */

@@ -24,7 +24,8 @@ from .assembly import (
     element_matrices,
     sample_state,
 )
-from .solver import CNSolver, StepFailure, linear_cn_step, newton_step
+from .solver import (CNSolver, StepFailure, backward_euler_step, linear_cn_step, newton_step,
+                     species_meshes_step, theta_step)
 from .kernel import (
     Accumulators,
     CollisionParams,
@@ -106,5 +107,6 @@ __all__ = [
     "QuadPointData", "assemble_at", "assemble_collision", "assemble_species_meshes", "sample_state", "axisym_tensor_pair", "axisym_tensor_pairs",
     "coupling", "default_eps_d", "element_matrices", "elliptic_KE", "flop_count", "fused_inner_loop",
     "fused_sweep", "install", "uninstall", "CNSolver", "StepFailure", "linear_cn_step",
+    "backward_euler_step", "theta_step", "species_meshes_step",
     "newton_step",
 ]

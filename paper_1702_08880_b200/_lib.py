@@ -78,6 +78,7 @@ SIGNATURES = {
     "lb_cn_get_mass": (_i, [_vp, _dp]),
     "lb_cn_newton": (_i, [_vp, _dp, _dp, _d, _d, _dp, _dp, _dp, _i, _dp, _dp, _dp, _dp]),
     "lb_cn_linear_step": (_i, [_vp, _d, _dp, _dp, _dp]),
+    "lb_cn_theta_step": (_i, [_vp, _d, _d, _dp, _dp, _dp]),
     "lb_cn_stats": (_i, [_vp, _dp, _ip, _ip]),
 }
 

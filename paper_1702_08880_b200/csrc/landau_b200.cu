@@ -2064,19 +2064,24 @@ int lb_cn_stats(lb_cn* cn, double* last_rel_residual, int* fallbacks, int* pivot
 }
 
 int lb_cn_linear_step(lb_cn* cn, double dt, const double* C, const double* f, double* f_out) {
+  return lb_cn_theta_step(cn, dt, 0.5, C, f, f_out);
+}
+
+int lb_cn_theta_step(lb_cn* cn, double dt, double theta, const double* C, const double* f, double* f_out) {
   if (!cn) return fail(LB_EINVAL, "null solver");
+  if (!(theta > 0.0 && theta <= 1.0)) return fail(LB_EINVAL, "theta must be in (0, 1]");
   int rc = use_ctx(cn->ctx);
   if (rc) return rc;
   if (!C || !f || !f_out) return fail(LB_EINVAL, "null argument");
   if (!cn->has_mass) return fail(LB_EINVAL, "mass matrix not set (lb_cn_set_mass)");
   const int S = cn->S, n = cn->n, nS = S * n;
   cudaStream_t st = cn->ctx->stream;
-  const double h = 0.5 * dt;
+  const double h = theta * dt, h_rhs = (1.0 - theta) * dt;  // CN: both dt/2 (solver.py:146)
   LB_CUDA(cudaMemcpyAsync(cn->Cg, C, sizeof(double) * S * cn->nnz, cudaMemcpyHostToDevice, st));
   LB_CUDA(cudaMemcpyAsync(cn->f, f, sizeof(double) * nS, cudaMemcpyHostToDevice, st));
-  // rhs = (M + dt/2 C) f (solver.py:146), then (M - dt/2 C) f+ = rhs
+  // rhs = (M + (1 - theta) dt C) f, then (M - theta dt C) f+ = rhs
   lb_cn_rhs_kernel<<<(nS + 127) / 128, 128, 0, st>>>(n, S, cn->indptr, cn->indices, cn->nnz, cn->Mv, cn->Cg,
-                                                     cn->f, h, cn->R);
+                                                     cn->f, h_rhs, cn->R);
   int bad = 0;
   if ((rc = cn_guarded_solve(cn, cn->Cg, h, cn->R, 1.0, nullptr, st, nullptr, nullptr, &bad))) return rc;
   LB_CUDA(cudaMemcpyAsync(f_out, cn->out, sizeof(double) * nS, cudaMemcpyDeviceToHost, st));

@@ -36,8 +36,8 @@ from . import _lib
 from .assembly import default_eps_d, device_mesh
 from .kernel import _n_species, coupling
 
-__all__ = ["CNSolver", "StepFailure", "band_order", "linear_cn_step", "newton_step",
-           "pattern_values"]
+__all__ = ["CNSolver", "StepFailure", "backward_euler_step", "band_order", "linear_cn_step",
+           "newton_step", "pattern_values", "species_meshes_step", "theta_step"]
 
 
 class StepFailure(RuntimeError):
@@ -245,6 +245,21 @@ _LINEAR: "OrderedDict[tuple, CNSolver]" = OrderedDict()
 def linear_cn_step(M, C, dt: float, state):
     """solver.linear_cn_step (solver.py:137-150) on the device: solves
     (M - dt/2 C_a) f+ = (M + dt/2 C_a) f per species with C held fixed."""
+    return theta_step(M, C, dt, state, 0.5)
+
+
+def backward_euler_step(M, C, dt: float, state):
+    """Backward-Euler step with C held fixed, (M - dt C_a) f+ = M f per
+    species -- the time step BASELINE configs 1-2 name; the reference has
+    Crank-Nicolson only, so this is the composition of its pieces (SURVEY
+    8(c)(iii)) on the device solver."""
+    return theta_step(M, C, dt, state, 1.0)
+
+
+def theta_step(M, C, dt: float, state, theta: float):
+    """(M - theta dt C_a) f+ = (M + (1 - theta) dt C_a) f per species with C
+    held fixed (lb_cn_theta_step): theta = 1/2 Crank-Nicolson, 1 backward
+    Euler."""
     f = _coeffs_of(state)
     S = f.shape[0]
     if len(C.blocks) != S:
@@ -269,8 +284,32 @@ def linear_cn_step(M, C, dt: float, state):
     Cv = solver.block_values(C.blocks)
     out = np.empty_like(f)
     try:
-        _lib.check(solver._lib.lb_cn_linear_step(solver.handle, float(dt), _lib.dptr(Cv),
-                                                 _lib.dptr(f), _lib.dptr(out)))
+        _lib.check(solver._lib.lb_cn_theta_step(solver.handle, float(dt), float(theta), _lib.dptr(Cv),
+                                                _lib.dptr(f), _lib.dptr(out)))
     except _lib.SingularSystem as err:
         raise _StepFailure(-1, f"linear solve failed: {err}") from err
     return _with_coeffs(state, out)
+
+
+def species_meshes_step(meshes, ref, states, params, dt: float, masses, theta: float = 1.0,
+                        eps_d: float | None = None):
+    """One time step with every species on its own mesh (PAPER.md section
+    3.0.2; BASELINE config 2 as worded): C_a at the current state from ONE
+    device sweep over the species-tagged union point set
+    (`assemble_species_meshes`; device sampling of each mesh), then per
+    species the theta step on its own mesh, (M_a - theta dt C_a) f_a+ =
+    (M_a + (1 - theta) dt C_a) f_a -- theta = 1 (default) is backward Euler.
+    `states[a]` is species a's coefficient vector on meshes[a], `masses[a]`
+    its mass matrix (CSR).  Returns the new list of coefficient vectors."""
+    from types import SimpleNamespace
+
+    from .assembly import assemble_species_meshes, sample_state
+
+    if not (len(meshes) == len(states) == len(masses)):
+        raise ValueError("need one mesh, state and mass matrix per species")
+    coeffs = [np.ascontiguousarray(np.asarray(getattr(c, "coeffs", c), dtype=np.float64).reshape(-1))
+              for c in states]
+    datas = [sample_state(mesh, ref, c[None, :]) for mesh, c in zip(meshes, coeffs)]
+    blocks, _ = assemble_species_meshes(meshes, ref, datas, params, eps_d=eps_d)
+    return [theta_step(M, SimpleNamespace(blocks=[blocks[a]]), dt, coeffs[a][None, :], theta)[0]
+            for a, M in enumerate(masses)]

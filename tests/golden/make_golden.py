@@ -438,6 +438,68 @@ def case_cfg2_meshes():
                          (16, 32))
 
 
+def case_cfg2_meshes_be(steps=10, dt=0.5):
+    """Config 2 as worded, time integration: e and D (m = 3670), T_e = 2 T_i,
+    each on its own 16x32 mesh scaled to its thermal speed; `steps`
+    backward-Euler steps of temperature relaxation, (M_a - dt C_a[f]) f_a+ =
+    M_a f_a with C_a at the old state (the reference has Crank-Nicolson
+    only: SURVEY 8(c)(iii) composes backward Euler from its pieces).  Each
+    step is the composed reference oracle of case_cfg2_meshes (reference
+    sample_state per mesh, ONE reference fused_sweep over the species-tagged
+    union, the pinned per-mesh contraction + condensation) and scipy splu.
+    Records every step's states and per-species moments."""
+    sys.path.insert(0, str(HERE.parents[1]))
+    from oracle import oracle as O
+
+    spec = [("e", 1.0, -1.0, 1.0, 0.5), ("D", 3670.0, 1.0, 1.0, 0.25)]
+    ref = ax.build_reference_element()
+    sp_ = [ax.Species(nm, m, q, T) for nm, m, q, _, T in spec]
+    params = ax.collision_params(sp_)
+    meshes, coeffs, Ms = [], [], []
+    for (nm, m, q, dens, T), s in zip(spec, sp_):
+        mesh = ax.cartesian_mesh(ax.DomainSpec(L=5.0 * math.sqrt(s.sigma2)), 16, 32)
+        st = ax.maxwellian_init(mesh, ref, [s], neutralize=False)
+        st.coeffs *= 2.0 * dens  # the reference prefactor is 1/2 (physics.py:97-100)
+        meshes.append(mesh)
+        coeffs.append(st.coeffs[0].copy())
+        Ms.append(ax.mass_matrix(mesh, ref))
+    S = len(spec)
+    eps_d = min(ax.assembly.default_eps_d(m) for m in meshes)
+    traj = [[c.copy() for c in coeffs]]
+    for _ in range(steps):
+        datas = [ax.sample_state(mesh, ref, ax.StateVector(c[None, :])) for mesh, c in zip(meshes, coeffs)]
+        ns = [d.N for d in datas]
+        off = np.concatenate([[0], np.cumsum(ns)])
+        n = int(off[-1])
+        f = np.zeros((S, n)); dfr = np.zeros((S, n)); dfz = np.zeros((S, n))
+        for a, d in enumerate(datas):
+            f[a, off[a]:off[a + 1]] = d.f[0]
+            dfr[a, off[a]:off[a + 1]] = d.df_r[0]
+            dfz[a, off[a]:off[a + 1]] = d.df_z[0]
+        union = ax.QuadPointData(N=n, r=np.concatenate([d.r for d in datas]),
+                                 z=np.concatenate([d.z for d in datas]),
+                                 w=np.concatenate([d.w for d in datas]), f=f, df_r=dfr, df_z=dfz)
+        K, D = ax.fused_sweep(union.r, union.z, union, params, eps_d=eps_d, workers=1)
+        new = []
+        for a, (mesh, d) in enumerate(zip(meshes, datas)):
+            sl = slice(off[a], off[a + 1])
+            elem = O.element_matrices(K[sl, a:a + 1], D[sl, a:a + 1], d.w, mesh.sizes, ref.B, ref.dB)
+            C = O.condense(elem, mesh.cell_nodes, mesh.n_nodes, mesh.prolongation)[0]
+            new.append(spla.splu((Ms[a] - dt * C).tocsc()).solve(Ms[a] @ coeffs[a]))
+        coeffs = new
+        traj.append([c.copy() for c in coeffs])
+    out = {"S": np.int64(S), "eps_d": np.float64(eps_d), "dt": np.float64(dt),
+           "steps": np.int64(steps), **params_parts(params),
+           "masses": np.array([s.mass for s in sp_])}
+    for a, mesh in enumerate(meshes):
+        for k, v in mesh_parts(mesh, ref).items():
+            out[f"s{a}_{k}"] = v
+        out.update(csr_parts(f"s{a}_M", Ms[a]))
+        out[f"s{a}_Wm"] = moment_matrix(mesh, ref)
+        out[f"s{a}_states"] = np.stack([t[a] for t in traj])
+    save("cfg2be", **out)
+
+
 def case_cfg4_meshes():
     """Config 4 as worded but on 8x16 meshes (the 64x128 union of 294,912
     points is beyond the reference's CPU budget): e, D, C6+, W10+ each on its
@@ -471,7 +533,7 @@ def main():
     cases = {"pairs": case_pairs, "sweep_small": case_sweep_small, "cfg1": case_cfg1,
              "hanging": case_hanging, "cons": case_cons, "cfg2": case_cfg2,
              "cfg3": case_cfg3, "cfg1adv": case_cfg1_advance, "cfg3adv": case_cfg3_advance, "cfg4s": case_cfg4_species, "cfg2m": case_cfg2_meshes,
-             "cfg4m": case_cfg4_meshes,
+             "cfg4m": case_cfg4_meshes, "cfg2be": case_cfg2_meshes_be,
              "cfg5_4096": lambda: case_cfg5(4096),
              "cfg5_65536": lambda: case_cfg5(65536, n_sub=192)}
     for name, fn in cases.items():

@@ -304,3 +304,67 @@ def test_custom_block_lu_matches_cublas_path(gpu, tmp_path):
         err = _scaled(outs["custom"][a], outs["cublas"][a])
         print("species", a, "custom LU vs cuBLAS LU", err)
         assert err <= TOL
+
+
+def test_species_meshes_backward_euler_trajectory(gpu):
+    """BASELINE config 2 as worded, time integration: electrons and deuterium
+    (m = 3670, T_e = 2 T_i) each on its own 16x32 mesh scaled to its thermal
+    speed, 10 backward-Euler steps of temperature relaxation.  The device
+    path (device sampling per mesh, one union sweep, per-mesh assembly,
+    lb_cn_theta_step with theta = 1) reproduces the composed reference
+    trajectory (tests/golden/make_golden.py case_cfg2_meshes_be: reference
+    sample_state + fused_sweep + pinned contraction, scipy splu): every
+    step's states to 1e-10 scaled, per-species density / momentum / energy
+    to 1e-10; each species' density is conserved (1e-13 relative) and the
+    energy moves from the electrons to the ions."""
+    from conftest import Prefixed
+
+    g = golden("cfg2be")
+    S, dt, steps = int(g["S"]), float(g["dt"]), int(g["steps"])
+    meshes = [mesh_from(Prefixed(g, f"s{a}_")) for a in range(S)]
+    ref = ref_from(Prefixed(g, "s0_"))
+    params = params_from(g)
+    Ms = [csr_from(g, f"s{a}_M") for a in range(S)]
+    masses = g["masses"]
+    states = [g[f"s{a}_states"][0].copy() for a in range(S)]
+    worst, worst_mom = 0.0, 0.0
+    for step in range(1, steps + 1):
+        states = gpu.species_meshes_step(meshes, ref, states, params, dt, Ms)
+        for a in range(S):
+            want = g[f"s{a}_states"][step]
+            worst = max(worst, _scaled(states[a], want))
+            scale = np.array([1.0, masses[a], masses[a], masses[a]])
+            mom = (g[f"s{a}_Wm"] @ states[a]) * scale
+            ref_mom = (g[f"s{a}_Wm"] @ want) * scale
+            worst_mom = max(worst_mom, abs(mom[0] - ref_mom[0]) / abs(ref_mom[0]),
+                            abs(mom[2] - ref_mom[2]) / abs(ref_mom[2]),
+                            abs(mom[1] - ref_mom[1]) / abs(ref_mom[0]))
+            n0 = (g[f"s{a}_Wm"] @ g[f"s{a}_states"][0])[0]
+            assert abs(mom[0] - n0) <= 1e-13 * abs(n0)
+    print("cfg2 per-species meshes, 10 BE steps: worst state", worst, "worst moment", worst_mom)
+    assert worst <= TOL and worst_mom <= TOL
+    E0 = [(g[f"s{a}_Wm"] @ g[f"s{a}_states"][0])[2] * masses[a] for a in range(S)]
+    E1 = [(g[f"s{a}_Wm"] @ states[a])[2] * masses[a] for a in range(S)]
+    assert E1[0] < E0[0] and E1[1] > E0[1]  # electrons cool, ions heat
+
+
+def test_theta_step_is_backward_euler_and_cn(gpu):
+    """lb_cn_theta_step: theta = 1 solves (M - dt C) f+ = M f and theta = 1/2
+    is linear_cn_step, both against scipy on the cfg1 fixture."""
+    g = golden("cfg1")
+    M = csr_from(g, "M")
+    C = SimpleNamespace(blocks=blocks_from(g, "C"))
+    f = np.atleast_2d(g["coeffs"])
+    dt = 0.1
+    be = gpu.backward_euler_step(M, C, dt, f)
+    cn = gpu.theta_step(M, C, dt, f, 0.5)
+    cn_ref = gpu.linear_cn_step(M, C, dt, f)
+    for a in range(f.shape[0]):
+        A = (M - dt * C.blocks[a]).tocsc()
+        want = spla.splu(A).solve(M @ f[a])
+        assert _scaled(be[a], want) <= 1e-12
+        want_cn = spla.splu((M - 0.5 * dt * C.blocks[a]).tocsc()).solve((M + 0.5 * dt * C.blocks[a]) @ f[a])
+        assert _scaled(cn[a], want_cn) <= 1e-12
+    assert np.array_equal(cn, cn_ref)
+    with pytest.raises(ValueError):
+        gpu.theta_step(M, C, dt, f, 0.0)
