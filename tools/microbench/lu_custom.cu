@@ -81,7 +81,7 @@ int main(int argc, char** argv) {
   }
   return 0;
 #endif
-  for (int n : {67, 68, 131, 260, 354, 383}) {
+  for (int n : {5, 17, 32, 33, 67, 68, 131, 260, 354, 383}) {
     if (getrs_smem_bytes<KB, W>(n) > 232448) {
       printf("n=%3d: W=%d slab needs %zu B of shared memory, skipped\n", n, W, getrs_smem_bytes<KB, W>(n));
       continue;
