@@ -1464,6 +1464,8 @@ static int cn_alloc(lb_cn* cn, void** p, size_t bytes) {
 // block LU + [L U] solve by the custom kernels of landau_lu.cuh (cuBLAS
 // getrf / getrs / trsm otherwise: blocks over 384 rows, or LB_CN_CUBLAS_LU set)
 constexpr int kLuKB = 32, kLuW = 32, kLuMaxNb = 384;
+constexpr int kLuWideMinCount = 48;       // blocks per level from which 64-column slabs pay
+constexpr size_t kLuSmemMax = 232448;     // opt-in shared memory per CTA (227 KB)
 static bool cn_custom_lu(const lb_cn* cn) {
   static const bool force_blas = std::getenv("LB_CN_CUBLAS_LU") != nullptr;
   return cn->nb <= kLuMaxNb && !force_blas;
@@ -1491,9 +1493,18 @@ static int cn_factor_issue(lb_cn* cn, cudaStream_t st, bool pivot) {
         LB_CUDA(cudaGetLastError());
       }
       if (L.getrsL.count) {
-        const dim3 g(L.getrsL.count, (2 * nb + kLuW - 1) / kLuW);
-        lb_getrs_slab_kernel<kLuKB, kLuW><<<g, kLuThreads, getrs_smem_bytes<kLuKB, kLuW>(nb), st>>>(
-            nb, 2 * nb, L.getrsL.A, L.perm, L.inv, L.getrsL.B);
+        // 64-column slabs where shared memory allows and the level has
+        // enough blocks to fill the GPU (fewer CTAs, less per-step overhead);
+        // 32-column slabs for the latency-bound small levels
+        if (L.getrsL.count >= kLuWideMinCount && getrs_smem_bytes<kLuKB, 2 * kLuW>(nb) <= kLuSmemMax) {
+          const dim3 g(L.getrsL.count, (2 * nb + 2 * kLuW - 1) / (2 * kLuW));
+          lb_getrs_slab_kernel<kLuKB, 2 * kLuW><<<g, kLuThreads, getrs_smem_bytes<kLuKB, 2 * kLuW>(nb), st>>>(
+              nb, 2 * nb, L.getrsL.A, L.perm, L.inv, L.getrsL.B);
+        } else {
+          const dim3 g(L.getrsL.count, (2 * nb + kLuW - 1) / kLuW);
+          lb_getrs_slab_kernel<kLuKB, kLuW><<<g, kLuThreads, getrs_smem_bytes<kLuKB, kLuW>(nb), st>>>(
+              nb, 2 * nb, L.getrsL.A, L.perm, L.inv, L.getrsL.B);
+        }
         LB_CUDA(cudaGetLastError());
       }
     } else if (L.getrf.count) {
@@ -1909,7 +1920,9 @@ int lb_cn_create(lb_ctx* ctx, const lb_mesh* m, int S, int n, const int* indptr,
       (cudaFuncSetAttribute(lb_getrf_kernel<kLuKB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             (int)getrf_smem_bytes<kLuKB>(kLuMaxNb)) != cudaSuccess ||
        cudaFuncSetAttribute(lb_getrs_slab_kernel<kLuKB, kLuW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            (int)getrs_smem_bytes<kLuKB, kLuW>(kLuMaxNb)) != cudaSuccess))
+                            (int)getrs_smem_bytes<kLuKB, kLuW>(kLuMaxNb)) != cudaSuccess ||
+       cudaFuncSetAttribute(lb_getrs_slab_kernel<kLuKB, 2 * kLuW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)kLuSmemMax) != cudaSuccess))
     return bail(fail(LB_ECUDA, "cudaFuncSetAttribute(custom LU kernels) failed"));
   const size_t ws = size_t(32) << 20;
   if ((rc = cn_alloc(cn, &cn->blas_ws, ws))) return bail(rc);

@@ -455,7 +455,7 @@ __global__ void __launch_bounds__(kLuThreads) lb_getrf_kernel(int n, double* con
 // during the Di product of step q+1.
 template <int KB, int W>
 inline size_t getrs_smem_bytes(int n) {
-  return sizeof(double) * ((size_t)lu_ld<KB>(n) * W + (size_t)KB * lu_ld<KB>(n) + 2 * KB * KB + KB * W);
+  return sizeof(double) * ((size_t)lu_ld<KB>(n) * W + (size_t)KB * lu_ld<KB>(n) + KB * KB + KB * W);
 }
 
 __device__ __forceinline__ void cp_async8(double* dst, const double* src) {
@@ -476,14 +476,13 @@ __global__ void __launch_bounds__(kLuThreads) lb_getrs_slab_kernel(int n, int m,
                                                                    const int* __restrict__ perm_all,
                                                                    const double* __restrict__ inv_all,
                                                                    double* const* __restrict__ Xs) {
-  static_assert(KB * W / 4 <= kLuThreads, "one diagonal-block output group per thread");
   constexpr int KH = KB / 2, CG = W / 4;  // k-half, column groups of 4
   extern __shared__ __align__(16) double lu_sm[];
   const int ld = lu_ld<KB>(n);
   double* X = lu_sm;                       // [ld][W]
   double* H[2] = {X + (size_t)ld * W, X + (size_t)ld * W + (size_t)KH * ld};  // [KH][ld] each
-  double* Dib[2] = {H[1] + (size_t)KH * ld, H[1] + (size_t)KH * ld + KB * KB};  // [KB][KB]
-  double* Y = Dib[1] + KB * KB;            // [KB][W]
+  double* Dis = H[1] + (size_t)KH * ld;    // [KB][KB] (streamed in with the first half)
+  double* Y = Dis + KB * KB;               // [KB][W]
   const int b = blockIdx.x, s = blockIdx.y, tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int col0 = s * W, wc = min(W, m - col0);
   if (wc <= 0) return;
@@ -521,10 +520,9 @@ __global__ void __launch_bounds__(kLuThreads) lb_getrs_slab_kernel(int n, int m,
         for (int i = lo + tid; i < hi; i += kLuThreads) cp_async8(dst + (size_t)k * ld + i, src + i);
       }
     }
-    if (h == 1) {
+    if (h == 0) {  // Di of step q: its buffer is free once step q-1's Di product is done
       const double* di = inv + (size_t)(q < np ? 2 * p : 2 * p + 1) * KB * KB;
-      double* dd = Dib[q & 1];
-      for (int t = 2 * tid; t < KB * KB; t += 2 * kLuThreads) cp_async16(dd + t, di + t);
+      for (int t = 2 * tid; t < KB * KB; t += 2 * kLuThreads) cp_async16(Dis + t, di + t);
     }
     cp_async_commit();
   };
@@ -536,8 +534,6 @@ __global__ void __launch_bounds__(kLuThreads) lb_getrs_slab_kernel(int n, int m,
 #pragma unroll 8
     for (int c = 0; c < W; ++c) X[(size_t)i * W + c] = (i < n && c < wc) ? Xg[(size_t)c * n + src] : 0.0;
   }
-  // this thread's output group of the Di product and its row tiles of the update
-  const int yi = tid / CG, yc = (tid - (tid / CG) * CG) * 4;
 #ifdef LB_LU_PROF
   long long t0_ = clock64(), pacc_[8] = {};
 #endif
@@ -548,39 +544,46 @@ __global__ void __launch_bounds__(kLuThreads) lb_getrs_slab_kernel(int n, int m,
     __syncthreads();
     LU_T(1);
     // Y = Di X[r0 : r0 + kb] on the FP64 tensor path (mma.m8n8k4.f64):
-    // 4 x (W/8) tiles of 8 x 8, two per warp
-    const double* Di = Dib[q & 1];
+    // 4 x (W/8) tiles of 8 x 8, W/16 per warp
+    const double* Di = Dis;
     {
-      static_assert(KB == 32 && W == 32, "DMMA tiling assumes 32 x 32 blocks");
-      const int m = warp >> 1, n0 = (warp & 1) * 2, lr = lane >> 2, lk = lane & 3;
-      double d[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+      static_assert(KB == 32 && (W == 32 || W == 64), "DMMA tiling assumes 32-row blocks, 32/64-column slabs");
+      constexpr int TPW = W / 16;
+      const int m = warp >> 1, n0 = (warp & 1) * TPW, lr = lane >> 2, lk = lane & 3;
+      double d[TPW][2];
+#pragma unroll
+      for (int nn = 0; nn < TPW; ++nn) d[nn][0] = d[nn][1] = 0.0;
 #pragma unroll
       for (int k0 = 0; k0 < KB; k0 += 4) {
         const int k = k0 + lk;
         const double av = Di[(size_t)k * KB + 8 * m + lr];
 #pragma unroll
-        for (int nn = 0; nn < 2; ++nn) {
+        for (int nn = 0; nn < TPW; ++nn) {
           const double bv = k < kb ? X[(size_t)(r0 + k) * W + 8 * (n0 + nn) + lr] : 0.0;
           dmma_884(d[nn], av, bv);
         }
       }
 #pragma unroll
-      for (int nn = 0; nn < 2; ++nn)
+      for (int nn = 0; nn < TPW; ++nn)
         *reinterpret_cast<double2*>(Y + (size_t)(8 * m + lr) * W + 8 * (n0 + nn) + 2 * lk) =
             make_double2(d[nn][0], d[nn][1]);
     }
     __syncthreads();
-    if (tid < KB * CG && yi < kb) {  // the block's rows of X become Y
-      *reinterpret_cast<double2*>(X + (size_t)(r0 + yi) * W + yc) =
-          *reinterpret_cast<const double2*>(Y + (size_t)yi * W + yc);
-      *reinterpret_cast<double2*>(X + (size_t)(r0 + yi) * W + yc + 2) =
-          *reinterpret_cast<const double2*>(Y + (size_t)yi * W + yc + 2);
+    for (int t = tid; t < KB * CG; t += kLuThreads) {  // the block's rows of X become Y
+      const int yi = t / CG, yc = (t - (t / CG) * CG) * 4;
+      if (yi < kb) {
+        *reinterpret_cast<double2*>(X + (size_t)(r0 + yi) * W + yc) =
+            *reinterpret_cast<const double2*>(Y + (size_t)yi * W + yc);
+        *reinterpret_cast<double2*>(X + (size_t)(r0 + yi) * W + yc + 2) =
+            *reinterpret_cast<const double2*>(Y + (size_t)yi * W + yc + 2);
+      }
     }
     LU_T(2);
     // X[lo:hi] -= F Y in two k-halves on the FP64 tensor path: warp tiles of
     // 16 rows x 32 columns (2 x 4 MMA tiles of 8 x 8), acc kept across halves
-    const int nr = hi - lo, nwt = (nr + 15) >> 4;
-    constexpr int kMaxWt = 3;  // ceil(ceil(383 / 16) / 8)
+    constexpr int CGW = W / 32;            // 32-column groups
+    const int nr = hi - lo, nwt = ((nr + 15) >> 4) * CGW;
+    constexpr int kMaxWt = 3 * CGW;        // ceil(ceil(383 / 16) CGW / 8)
     double acc[kMaxWt][2][4][2];
 #pragma unroll
     for (int u = 0; u < kMaxWt; ++u)
@@ -595,8 +598,9 @@ __global__ void __launch_bounds__(kLuThreads) lb_getrs_slab_kernel(int n, int m,
       const double* Hh = H[h] + lo;
 #pragma unroll
       for (int u = 0; u < kMaxWt; ++u) {
-        const int wt = warp + u * (kLuThreads / 32);
-        if (wt >= nwt) break;
+        const int t = warp + u * (kLuThreads / 32);
+        if (t >= nwt) break;
+        const int wt = t / CGW, cg = t - (t / CGW) * CGW;
 #pragma unroll
         for (int kq = 0; kq < KH; kq += 4) {
           const int k = h * KH + kq + lk;
@@ -605,7 +609,7 @@ __global__ void __launch_bounds__(kLuThreads) lb_getrs_slab_kernel(int n, int m,
           for (int mm = 0; mm < 2; ++mm)
             av[mm] = k < k1 ? Hh[(size_t)(kq + lk) * ld + 16 * wt + 8 * mm + lr] : 0.0;
 #pragma unroll
-          for (int nn = 0; nn < 4; ++nn) bv[nn] = Y[(size_t)k * W + 8 * nn + lr];
+          for (int nn = 0; nn < 4; ++nn) bv[nn] = Y[(size_t)k * W + 32 * cg + 8 * nn + lr];
 #pragma unroll
           for (int mm = 0; mm < 2; ++mm)
 #pragma unroll
@@ -620,15 +624,16 @@ __global__ void __launch_bounds__(kLuThreads) lb_getrs_slab_kernel(int n, int m,
     LU_T(3);
 #pragma unroll
     for (int u = 0; u < kMaxWt; ++u) {
-      const int wt = warp + u * (kLuThreads / 32);
-      if (wt >= nwt) break;
+      const int t = warp + u * (kLuThreads / 32);
+      if (t >= nwt) break;
+      const int wt = t / CGW, cg = t - (t / CGW) * CGW;
 #pragma unroll
       for (int mm = 0; mm < 2; ++mm) {
         const int R = 16 * wt + 8 * mm + lr;
         if (R >= nr) continue;
 #pragma unroll
         for (int nn = 0; nn < 4; ++nn) {
-          double* xr = X + (size_t)(lo + R) * W + 8 * nn + 2 * lk;
+          double* xr = X + (size_t)(lo + R) * W + 32 * cg + 8 * nn + 2 * lk;
           const double2 x2 = *reinterpret_cast<const double2*>(xr);
           *reinterpret_cast<double2*>(xr) = make_double2(x2.x - acc[u][mm][nn][0], x2.y - acc[u][mm][nn][1]);
         }
