@@ -682,6 +682,15 @@ __global__ void __launch_bounds__(kLuThreads) lb_lu_vsolve_kernel(int n, int cou
     const int r0 = p * KB, kb = min(KB, n - r0);
     const int lo = fwd ? r0 + kb : 0, hi = fwd ? n : r0;
     __syncthreads();
+    // this thread's rows of the update (<= 2 for n <= 384): their 32 factor
+    // entries are loaded first, so the load latency overlaps the triangle
+    const int i0 = lo + tid, i1 = i0 + kLuThreads;
+    double f0[KB], f1[KB];
+#pragma unroll
+    for (int k = 0; k < KB; ++k) {
+      f0[k] = (k < kb && i0 < hi) ? A[(size_t)(r0 + k) * n + i0] : 0.0;
+      f1[k] = (k < kb && i1 < hi) ? A[(size_t)(r0 + k) * n + i1] : 0.0;
+    }
     if (tid < 32) {  // the diagonal block's triangle, warp 0
       static_assert(KB == 32, "one lane per block row");
       const int r = tid;
@@ -706,14 +715,17 @@ __global__ void __launch_bounds__(kLuThreads) lb_lu_vsolve_kernel(int n, int cou
       if (r < kb) x[r0 + r] = xr;
     }
     __syncthreads();
-    for (int i = lo + tid; i < hi; i += kLuThreads) {
-      double f[KB];
+    if (i0 < hi) {
+      double acc = x[i0];
 #pragma unroll
-      for (int k = 0; k < KB; ++k) f[k] = k < kb ? A[(size_t)(r0 + k) * n + i] : 0.0;
-      double acc = x[i];
+      for (int k = 0; k < KB; ++k) acc = fma(-f0[k], x[r0 + (k < kb ? k : 0)], acc);
+      x[i0] = acc;
+    }
+    if (i1 < hi) {
+      double acc = x[i1];
 #pragma unroll
-      for (int k = 0; k < KB; ++k) acc = fma(-f[k], x[r0 + (k < kb ? k : 0)], acc);
-      x[i] = acc;
+      for (int k = 0; k < KB; ++k) acc = fma(-f1[k], x[r0 + (k < kb ? k : 0)], acc);
+      x[i1] = acc;
     }
   }
   __syncthreads();
