@@ -279,6 +279,45 @@ np.save(sys.argv[2], nxt)
 """
 
 
+_CUBLAS_LU_CFG3_SCRIPT = r"""
+import sys, numpy as np
+from types import SimpleNamespace
+sys.path.insert(0, sys.argv[1])
+sys.path.insert(0, sys.argv[1] + "/tests")
+import paper_1702_08880_b200 as gpu
+from conftest import csr_from, golden, mesh_from, params_from, ref_from
+g = golden("cfg3")
+cfg = SimpleNamespace(dt=float(g["dt"]), eps_d=None)
+nxt, rnorm = gpu.newton_step(g["coeffs"], g["coeffs"], mesh_from(g), ref_from(g), params_from(g), cfg,
+                             M=csr_from(g, "M"))
+np.save(sys.argv[2], nxt)
+"""
+
+
+def test_custom_block_lu_matches_cublas_path_cfg3(gpu, tmp_path):
+    """Config 3 (hanging nodes, 354-row blocks, the unpivoted path): the
+    package's block-LU kernels and the cuBLAS path (LB_CN_CUBLAS_LU=1, in a
+    subprocess) give the same Newton step, and both the reference's."""
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    root = Path(__file__).resolve().parents[1]
+    outs = {}
+    for name, extra in (("custom", {}), ("cublas", {"LB_CN_CUBLAS_LU": "1"})):
+        out = tmp_path / f"{name}.npy"
+        subprocess.run([sys.executable, "-c", _CUBLAS_LU_CFG3_SCRIPT, str(root), str(out)],
+                       env=dict(os.environ, **extra), check=True, timeout=600)
+        outs[name] = np.load(out)
+    g = golden("cfg3")
+    err = _scaled(outs["custom"], outs["cublas"])
+    print("cfg3 custom LU vs cuBLAS LU", err)
+    assert err <= 1e-12
+    for v in outs.values():
+        assert _scaled(v, g["newton_coeffs"]) <= TOL
+
+
 def test_custom_block_lu_matches_cublas_path(gpu, tmp_path):
     """The package's block LU + [L U] solve kernels and the cuBLAS
     getrf/getrs/trsm path (LB_CN_CUBLAS_LU=1, read once per process, so it

@@ -238,6 +238,19 @@ def test_elliptic_domain_errors_before_the_device():
             pkg.elliptic_KE([bad])
 
 
+def test_species_meshes_step_argument_errors_before_the_device():
+    """species_meshes_step needs one mesh, state and mass matrix per species;
+    a mismatch is a ValueError before any device work."""
+    import pytest
+
+    import paper_1702_08880_b200 as pkg
+
+    with pytest.raises(ValueError):
+        pkg.species_meshes_step([object()], None, [np.zeros(3), np.zeros(3)], None, 0.1, [None])
+    with pytest.raises(ValueError):
+        pkg.species_meshes_step([object(), object()], None, [np.zeros(3), np.zeros(3)], None, 0.1, [None])
+
+
 def test_bench_reference_arm_contract():
     """`bench.py --impl reference` (the reference algorithm on the host cores)
     prints one JSON line with the contract's keys: impl, cpu_baseline,
