@@ -218,6 +218,7 @@ def ours_arm(args):
     params = pkg.CollisionParams(nu_hat=wl.nu_hat, mass_ratio_o=wl.mass_ratio_o)
     sh = ShardedSweep(N, S, params, wl.eps_d, dev, align=1, p2p=args.p2p)
     nloc = sh.hi - sh.lo
+    nacc = sh.nacc  # accumulator species sets (1: rank-one species collapse)
     host = local_fields(wl, sh.lo, sh.hi)
     d_fields = [torch.from_numpy(a).to(dev) for a in host]
     lib = _lib.load()
@@ -264,6 +265,12 @@ def ours_arm(args):
         sampler.start()
     E = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
     sh.launches = 0
+    # execution counters of the symmetric sweep (thread-steps by kind) over
+    # the timed steps: with the per-step FP64 counts of this library's SASS
+    # they give the executed FP64 work (tools/sass_fp64.py)
+    counting = sh.symmetric and nacc == 1
+    if counting:
+        _lib.check(lib.lb_sym_counters(sh._ctx.handle, 1, None))
     barrier()
     for k in range(args.steps):
         flush.fill_(float(k))  # evict L2 between timed steps (outside the step events)
@@ -278,13 +285,50 @@ def ours_arm(args):
     tot_ms, tot_sweep_ms = allmax([sum(step_ms), sum(sweep_ms)])
     pairs_step = N * N
     value = pairs_step * args.steps / (tot_ms * 1e-3)
-    # roofline of the dominant kernel on this rank: model flops per launch / launch time
+    counts = None
+    if counting:
+        cbuf = (_lib.C.c_ulonglong * 3)()
+        _lib.check(lib.lb_sym_counters(sh._ctx.handle, 0, cbuf))
+        counts = [int(c) for c in cbuf]
+    # roofline of the dominant kernel on this rank: executed FP64 flops per
+    # launch / launch time (the hardware fraction), and the reference's flop
+    # model per ordered pair delivered (model_frac, can exceed 1: the
+    # symmetric path evaluates each unordered pair once and the species
+    # collapse makes S = 2 cost what S = 1 costs)
     sweep_avg_s = sum(sweep_ms) / len(sweep_ms) * 1e-3
-    nacc = sh.nacc  # accumulator species sets (1: rank-one species collapse)
     # ordered pairs this rank's sweep delivers: its outer points x N (general
     # path) or its 1/world share of the tile pairs, each feeding both points
     flops_launch = pkg.flop_count(N, S, N / world if sh.symmetric else nloc)
-    achieved_tf = flops_launch / sweep_avg_s / 1e12
+    model_tf = flops_launch / sweep_avg_s / 1e12
+    executed = None
+    if counts is not None:
+        from tools import sass_fp64
+
+        try:
+            sass = sass_fp64.analyse(Path(lib._name))
+            ex = sass_fp64.executed(counts, sass)
+            executed = {
+                "flops_per_launch": ex["flops"] / args.steps,
+                "fp64_instr_per_launch": ex["instr"] / args.steps,
+                "pairs_per_launch": ex["pairs"] / args.steps,
+                "thread_steps": {"off_diagonal": counts[0], "diagonal": counts[1],
+                                 "series_branch": counts[2], "over_steps": args.steps},
+                "sass_per_thread_step": {"instr": sass["instr"], "flops": sass["flops"],
+                                         "pairs": sass["pairs_per_thread_step"]},
+                "fp64_instr_per_unordered_pair": ex["instr"] / max(ex["pairs"], 1),
+                "derivation": "kernel execution counters (lb_sym_counters) x FP64 "
+                              "instructions per thread-step counted in this library's "
+                              "SASS (tools/sass_fp64.py: DFMA = 2 flops, DMUL/DADD = 1); "
+                              "FP64 work outside the pair loop (< 1 %) not counted",
+            }
+        except (RuntimeError, OSError, subprocess.CalledProcessError) as err:
+            executed = {"error": str(err)}
+    if executed and "flops_per_launch" in executed:
+        achieved_tf = executed["flops_per_launch"] / sweep_avg_s / 1e12
+        bound_note = "executed FP64 flops (in-run counters x SASS)"
+    else:  # general path / uncollapsed kernels: the model figure only
+        achieved_tf = model_tf
+        bound_note = "model flops (no execution counters for this kernel)"
 
     # e2e through the public API with pinned host buffers (copies inside the timed region)
     e2e = None
@@ -302,7 +346,9 @@ def ours_arm(args):
             t0 = time.perf_counter()
             K, D = pkg.fused_sweep(hp[0], hp[1], data, params, eps_d=wl.eps_d)
             ts.append(time.perf_counter() - t0)
-        h2d = 8 * ((3 + 3 * S) * N + 2 * N)
+        # the all-points call (outer == inner) uploads r, z, w, f, df_r, df_z
+        # once (kernel.py:504 called as in assembly.py:148); no outer copies
+        h2d = 8 * (3 + 3 * S) * N
         d2h = 8 * 6 * S * N
         e2e = {"value": pairs_step * len(ts) / sum(ts), "unit": UNIT,
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
@@ -349,6 +395,7 @@ def ours_arm(args):
         cpu["single_core_value"] = k1 * N / t1
 
     check = None
+    bitwise = None
     if args.check:  # every rank's own rows vs the oracle on a sample (functional check)
         from oracle import oracle as O
 
@@ -358,14 +405,24 @@ def ours_arm(args):
                                wl.nu_hat, wl.mass_ratio_o, eps_d=wl.eps_d)
         err = O.per_component_scaled_error(Kh_[idx - sh.lo], Dh_[idx - sh.lo], Kr, Dr)
         check = allmax([err])[0]
-    traffic = None
-    executed = None
+        # this rank's rows vs the single-GPU all-points call on its device
+        data1 = pkg.QuadPointData(N=N, r=wl.r, z=wl.z, w=wl.w, f=wl.f, df_r=wl.df_r,
+                                  df_z=wl.df_z)
+        K1, D1 = pkg.fused_sweep(wl.r, wl.z, data1, params, eps_d=wl.eps_d)
+        same = (np.array_equal(Kh_, K1[sh.lo:sh.hi]) and np.array_equal(Dh_, D1[sh.lo:sh.hi]))
+        bitwise = allmax([0.0 if same else 1.0])[0] == 0.0
+    # DRAM traffic of the sweep launch: not measurable without a profiler;
+    # taken from the committed ncu --set full capture, labelled with the
+    # kernel version it was measured on
+    traffic, traffic_src = None, None
     tf_file = ROOT / "profiles" / "sweep_traffic.json"
-    if tf_file.exists():  # committed ncu capture of the same kernel (profiles/)
+    if tf_file.exists() and sh.symmetric and nacc == 1:
         try:
             prof = json.loads(tf_file.read_text())
             traffic = prof.get("bytes_per_launch")
-            executed = prof.get("executed_fp64_ncu")
+            traffic_src = {"source": prof.get("source"), "kernel_version": prof.get("version"),
+                           "measured": "ncu --set full (dram__bytes_read.sum + "
+                                       "dram__bytes_write.sum), one launch, committed profile"}
         except (OSError, ValueError):
             traffic = None
 
@@ -379,26 +436,26 @@ def ours_arm(args):
                        "N": N, "S": S, "outer_per_gpu": nloc, "pairs_per_step": pairs_step,
                        "parallelism": f"outer-point shards x{world}" + (
                            f" + {args.backend} all-gather of packed field state"
-                           + ((" + peer-memory (CUDA IPC) reduction fused with the combine"
-                              if sh.p2p else " + all-reduce of partial sums") if sh.symmetric else "")
+                           + ((" + row-group split, peer-memory (CUDA IPC) read of the group "
+                               "sums fused with the combine" if sh.p2p else
+                               " + row-group split, all-gather of the group sums")
+                              if sh.symmetric else "")
                            if world > 1 else ""),
                        "l2": "flushed between timed steps (256 MiB write, outside step events)"},
             "roofline": {"bound": "fp64", "achieved": achieved_tf, "peak": fp64_sustained,
                          "unit": "TFLOP/s", "frac": achieved_tf / fp64_sustained,
-                         "traffic": traffic,
+                         "traffic": traffic, "traffic_source": traffic_src,
+                         "achieved_is": bound_note,
                          "kernel": ((f"lb_symsweep_ib_kernel<1>" if nacc == 1 else f"lb_symsweep_kernel<{nacc}>")
                                     + " + lb_symreduce_kernel" if sh.symmetric
                                     else f"lb_sweep_kernel<{nacc}> (+ lb_combine_kernel, <1%)"),
+                         "executed_fp64": executed,
+                         "model_achieved": model_tf, "model_frac": model_tf / fp64_sustained,
+                         "model_flops": "165+20*S^2 per ordered pair delivered (kernel.py:560-574)",
                          "species_collapsed": nacc == 1 and S > 1,
-                         "flops": "model 165+20*S^2 per ordered pair (kernel.py:560-574)"
-                                  + ("; symmetric path evaluates each unordered pair once, "
-                                     "so model flops per executed flop is ~1.7 and frac may "
-                                     "exceed 1 (see executed-flop fraction from ncu in "
-                                     "profiles/)" if sh.symmetric else ""),
                          "peak_source": "measured DFMA microbenchmark on this GPU "
-                                        "(lb_fp64_peak, median of the last half of 1 s)",
-                         "peak_burst": fp64_burst, "frac_of_nominal_37.2": achieved_tf / 37.2,
-                         "executed_fp64_ncu": executed},
+                                        "(lb_fp64_peak, median of the last half of the probe)",
+                         "peak_burst": fp64_burst, "frac_of_nominal_37.2": achieved_tf / 37.2},
             "e2e": e2e,
             "gpu_launches": launches,
             "clocks": clocks,
@@ -410,6 +467,7 @@ def ours_arm(args):
             line["parity_scaled_err_vs_oracle"] = parity
         if check is not None:
             line["check_all_ranks_scaled_err_vs_oracle"] = check
+            line["check_all_ranks_bitwise_equal_single"] = bitwise
         if args.backend != "nccl" and world > 1:
             line["note"] = f"functional run over {args.backend} (ranks may share a GPU): not a timing"
 

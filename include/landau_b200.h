@@ -223,19 +223,32 @@ int lb_elements_dev(lb_ctx *ctx, int ncell, int S, const double *cell_sizes,
                     const double *B, const double *dB, double *elem_out, void *stream);
 
 /* Symmetric all-points sweep in three device steps, for the multi-GPU
- * layer (the per-rank partial sums are added across ranks by the caller,
- * e.g. an NCCL all-reduce, between steps 2 and 3):
+ * layer:
  *  1 lb_sym_prepare_dev  Morton-order the n packed records (all points, the
  *                        same on every rank) into the context;
- *  2 lb_sym_partial_dev  this rank's share of the unordered tile pairs ->
- *                        tot[5S][lb_sym_npad(n)] partial accumulators (sorted
- *                        point order; zero where the rank contributed none);
- *  3 lb_sym_combine_dev  K/D for original points [q0, q1) from the summed tot
- *                        (K_out/D_out hold q1-q0 rows).
+ *  2 lb_sym_partial_dev  this rank's share of the unordered tile pairs: the
+ *                        row groups [g0, g1) of lb_sym_groups(rank, world)
+ *                        -> tot, (g1 - g0) group sums of [5S][lb_sym_npad(n)]
+ *                        doubles each (sorted point order);
+ *  3 lb_sym_combine_dev  K/D for original points [q0, q1) from all eight
+ *                        group sums held in one buffer (world = 1, or after
+ *                        an all-gather of every rank's group sums), or
+ *    lb_sym_combine_groups_dev  the same from a HOST array of eight device
+ *                        pointers, one per group in group order -- e.g.
+ *                        peers' buffers mapped with lb_ipc_open, which makes
+ *                        it the cross-rank reduction and the combine in one
+ *                        kernel, reading only this rank's points.
+ * The summation order is fixed by n alone: a point's total is the eight
+ * group sums added in group order, each group summed by increasing row.  So
+ * K and D are bitwise identical for every world size <= 8 (the reference
+ * promises bitwise invariance to `workers`, kernel.py:508-511,
+ * test_kernel.py:197-212).
  * lb_sym_supported(S, coK, coD) is 1 when this path implements the
- * coupling (any S with a rank-one coupling, else S <= 3). */
+ * coupling (any S with a rank-one coupling, else S <= 3).
+ * lb_sym_groups returns the group count (8) and this rank's [g0, g1). */
 int lb_sym_supported(int S, const double *coK, const double *coD);
 int lb_sym_npad(int n);
+int lb_sym_groups(int rank, int world, int *g0, int *g1);
 int lb_sym_prepare_dev(lb_ctx *ctx, int n, int S, const double *coK, const double *coD,
                        const double *rec, void *stream);
 int lb_sym_partial_dev(lb_ctx *ctx, int S, double eps_d, int rank, int world, double *tot,
@@ -243,23 +256,30 @@ int lb_sym_partial_dev(lb_ctx *ctx, int S, double eps_d, int rank, int world, do
 int lb_sym_combine_dev(lb_ctx *ctx, int S, const double *tot, const double *coK,
                        const double *coD, int q0, int q1, double *K_out, double *D_out,
                        void *stream);
+int lb_sym_combine_groups_dev(lb_ctx *ctx, int S, const double *const *group_ptrs,
+                              const double *coK, const double *coD, int q0, int q1,
+                              double *K_out, double *D_out, void *stream);
+
+/* Execution counters of the species-collapsed symmetric sweep (the
+ * benchmark's executed-FP64 count): out (3, may be NULL) receives the
+ * counts since the last call -- off-diagonal thread-steps, diagonal
+ * thread-steps, thread-steps that took the m < 0.01 series branch (each
+ * thread-step evaluates 4 pairs: 2 outer points x 2 partners) -- then the
+ * counters are zeroed and counting is switched on (enable != 0) or off.
+ * Synchronises the device. */
+int lb_sym_counters(lb_ctx *ctx, int enable, unsigned long long *out);
 
 /* elliptic_KE (kernel.py:93-113): K(m), E(m) for n parameters in [0, 1)
  * (LB_EINVAL outside), with the device's table log and Horner chains. */
 int lb_elliptic_ke(lb_ctx *ctx, int n, const double *m, double *K, double *E);
 
-/* Peer-memory reduction for the symmetric multi-GPU path: every rank
- * allocates its partial-sum buffer with lb_ipc_alloc (cudaMalloc + a
- * 64-byte CUDA IPC handle), the handles are exchanged out of band, and each
- * rank maps its peers' buffers with lb_ipc_open (peer access over NVLink).
- * lb_sym_combine_peers_dev is lb_sym_combine_dev reading the G ranks'
- * partial sums (tots: a DEVICE array of G pointers, rank order) and adding
- * them for points [q0, q1) only -- the all-reduce and the combine in one
- * kernel.  The caller orders it after every rank's lb_sym_partial_dev and
- * before any rank's next one (e.g. a stream-ordered barrier). */
-int lb_sym_combine_peers_dev(lb_ctx *ctx, int S, const double *const *tots, int G,
-                             const double *coK, const double *coD, int q0, int q1,
-                             double *K_out, double *D_out, void *stream);
+/* Peer memory for the symmetric multi-GPU path: every rank allocates its
+ * group-sum buffer with lb_ipc_alloc (cudaMalloc + a 64-byte CUDA IPC
+ * handle), the handles are exchanged out of band, and each rank maps its
+ * peers' buffers with lb_ipc_open (peer access over NVLink); the mapped
+ * pointers feed lb_sym_combine_groups_dev.  The caller orders the combine
+ * after every rank's lb_sym_partial_dev and before any rank's next one
+ * (e.g. a stream-ordered barrier). */
 int lb_ipc_alloc(lb_ctx *ctx, size_t bytes, void **dptr, unsigned char *handle);
 int lb_ipc_open(lb_ctx *ctx, const unsigned char *handle, void **dptr);
 int lb_ipc_close(lb_ctx *ctx, void *dptr);

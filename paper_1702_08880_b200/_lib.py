@@ -67,7 +67,9 @@ SIGNATURES = {
     "lb_last_launch_count": (_i, [_vp]),
     "lb_fp64_peak": (_i, [_vp, _dp, _dp]),
     "lb_elliptic_ke": (_i, [_vp, _i, _dp, _dp, _dp]),
-    "lb_sym_combine_peers_dev": (_i, [_vp, _i, _vp, _i, _dp, _dp, _i, _i, _vp, _vp, _vp]),
+    "lb_sym_combine_groups_dev": (_i, [_vp, _i, C.POINTER(_vp), _dp, _dp, _i, _i, _vp, _vp, _vp]),
+    "lb_sym_groups": (_i, [_i, _i, _ip, _ip]),
+    "lb_sym_counters": (_i, [_vp, _i, C.POINTER(C.c_ulonglong)]),
     "lb_ipc_alloc": (_i, [_vp, C.c_size_t, C.POINTER(_vp), C.c_char_p]),
     "lb_ipc_open": (_i, [_vp, C.c_char_p, C.POINTER(_vp)]),
     "lb_ipc_close": (_i, [_vp, _vp]),

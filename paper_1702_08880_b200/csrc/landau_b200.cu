@@ -69,7 +69,8 @@ struct lb_ctx {
   // grow-only scratch
   lb::DevBuf in, rec, partial, out, elem, outer, aux, order;
   // symmetric all-points sweep state (lb_sym_*): sorted records, order, partials
-  lb::DevBuf symord, symrec, syminv, symi, symj, symtot, symctr, sweepctr;
+  lb::DevBuf symord, symrec, syminv, symi, symj, symtot, symctr, sweepctr, symstats;
+  bool sym_count = false;  // lb_sym_counters: execution counters of the symmetric sweep on
   int sym_n = -1, sym_S = 0, sym_Se = 0, sym_nt = 0;
   // CUDA graph of the state-level operator's device work (lb_assemble_state):
   // captured on the second call with an unchanged key, replayed after
@@ -347,11 +348,18 @@ template <int S>
 int sym_partial(lb_ctx* ctx, long long gthr, int rank, int world, double* tot, cudaStream_t st) {
   const int nt = ctx->sym_nt;
   const int npad = nt * kSymTile;
-  const int R0 = (int)((long long)nt * rank / world), R1 = (int)((long long)nt * (rank + 1) / world);
+  // this rank's whole row groups (landau_sym.cuh: summation order)
+  int g0, g1;
+  sym_rank_groups(rank, world, g0, g1);
+  const int R0 = sym_group_row(g0, nt), R1 = sym_group_row(g1, nt);
   const int nseg = sym_nseg(nt), hmax = sym_hmax(nt);
+  const size_t slot = (size_t)5 * S * npad;
   int launches = 0;
+  // groups without rows contribute exact zeros
+  for (int g = g0; g < g1; ++g)
+    if (sym_group_row(g, nt) == sym_group_row(g + 1, nt))
+      LB_CUDA(cudaMemsetAsync(tot + (size_t)(g - g0) * slot, 0, sizeof(double) * slot, st));
   if (R0 >= R1) {
-    LB_CUDA(cudaMemsetAsync(tot, 0, sizeof(double) * 5 * S * npad, st));
     ctx->last_launches = 0;
     return LB_OK;
   }
@@ -375,6 +383,11 @@ int sym_partial(lb_ctx* ctx, long long gthr, int rank, int world, double* tot, c
   if ((rc = ensure(ctx->symctr, sizeof(int) * nbatch))) return rc;
   int* ctr = static_cast<int*>(ctx->symctr.p);
   LB_CUDA(cudaMemsetAsync(ctr, 0, sizeof(int) * nbatch, st));
+  unsigned long long* stats = nullptr;
+  if (ctx->sym_count && S == 1 && LB_SYM_IB) {
+    if ((rc = ensure(ctx->symstats, 4 * sizeof(unsigned long long)))) return rc;
+    stats = static_cast<unsigned long long*>(ctx->symstats.p);
+  }
   for (int b0 = R0; b0 < R1; b0 += RB) {
     const int b1 = std::min(R1, b0 + RB);
     SymArgs a;
@@ -382,6 +395,7 @@ int sym_partial(lb_ctx* ctx, long long gthr, int rank, int world, double* tot, c
     a.iside = static_cast<double*>(ctx->symi.p);
     a.jside = static_cast<double*>(ctx->symj.p);
     a.next_item = ctr + (b0 - R0) / RB;
+    a.stats = stats;
     a.nt = nt;
     a.row0 = b0;
     a.row1 = b1;
@@ -393,7 +407,7 @@ int sym_partial(lb_ctx* ctx, long long gthr, int rank, int world, double* tot, c
     sym_kernel<S>()<<<grid, sym_threads<S>(), smem, st>>>(a);
     LB_CUDA(cudaGetLastError());
     lb_symreduce_kernel<S><<<(npad + 127) / 128, 128, 0, st>>>(a.iside, a.jside, nt, b0, b1, nseg,
-                                                               hmax, b0 == R0 ? 1 : 0, tot);
+                                                               hmax, g0, tot);
     LB_CUDA(cudaGetLastError());
     launches += 2;
   }
@@ -402,15 +416,22 @@ int sym_partial(lb_ctx* ctx, long long gthr, int rank, int world, double* tot, c
 }
 
 template <int S>
-int sym_combine(lb_ctx* ctx, const double* tot, const Coupling& cp, int q0, int q1, double* K,
+int sym_combine(lb_ctx* ctx, const SymGroupPtrs& gp, const Coupling& cp, int q0, int q1, double* K,
                 double* D, cudaStream_t st) {
   if (q1 <= q0) return LB_OK;
   const int npad = ctx->sym_nt * kSymTile;
   lb_sym_combine_kernel<S><<<(q1 - q0 + 127) / 128, 128, 0, st>>>(
-      tot, npad, static_cast<const int*>(ctx->syminv.p), q0, q1, cp, K, D);
+      gp, npad, static_cast<const int*>(ctx->syminv.p), q0, q1, cp, K, D);
   LB_CUDA(cudaGetLastError());
   ctx->last_launches = 1;
   return LB_OK;
+}
+
+// group pointers of a single buffer holding all eight group sums
+SymGroupPtrs sym_local_groups(const double* tot, int Se, int npad) {
+  SymGroupPtrs gp;
+  for (int g = 0; g < kSymGroups; ++g) gp.p[g] = tot + (size_t)g * 5 * Se * npad;
+  return gp;
 }
 
 int sym_partial_dispatch(lb_ctx* ctx, int S, long long gthr, int rank, int world, double* tot,
@@ -425,13 +446,13 @@ int sym_partial_dispatch(lb_ctx* ctx, int S, long long gthr, int rank, int world
   }
 }
 
-int sym_combine_dispatch(lb_ctx* ctx, int S, const double* tot, const Coupling& cp, int q0, int q1,
-                         double* K, double* D, cudaStream_t st) {
+int sym_combine_dispatch(lb_ctx* ctx, int S, const SymGroupPtrs& gp, const Coupling& cp, int q0,
+                         int q1, double* K, double* D, cudaStream_t st) {
   switch (S) {
-    case 1: return sym_combine<1>(ctx, tot, cp, q0, q1, K, D, st);
-    case 2: return sym_combine<2>(ctx, tot, cp, q0, q1, K, D, st);
+    case 1: return sym_combine<1>(ctx, gp, cp, q0, q1, K, D, st);
+    case 2: return sym_combine<2>(ctx, gp, cp, q0, q1, K, D, st);
 #if LB_SYM_MAXS >= 3
-    case 3: return sym_combine<3>(ctx, tot, cp, q0, q1, K, D, st);
+    case 3: return sym_combine<3>(ctx, gp, cp, q0, q1, K, D, st);
 #endif
     default: return fail(LB_EINVAL, "symmetric sweep supports S <= " + std::to_string(kSymMaxS));
   }
@@ -446,11 +467,11 @@ int all_points_sweep(lb_ctx* ctx, int n, const double* rec, const double* r, con
   int rc = sym_prepare(ctx, n, cp, rec, st);
   if (rc) return rc;
   const int npad = ctx->sym_nt * kSymTile;
-  if ((rc = ensure(ctx->symtot, (size_t)5 * cp.Se * npad * sizeof(double)))) return rc;
+  if ((rc = ensure(ctx->symtot, (size_t)kSymGroups * 5 * cp.Se * npad * sizeof(double)))) return rc;
   double* tot = static_cast<double*>(ctx->symtot.p);
   if ((rc = sym_partial_dispatch(ctx, cp.Se, gthr, 0, 1, tot, st))) return rc;
   const int l = ctx->last_launches;  // sweep + reduce launches
-  rc = sym_combine_dispatch(ctx, cp.Se, tot, cp, 0, n, K, D, st);
+  rc = sym_combine_dispatch(ctx, cp.Se, sym_local_groups(tot, cp.Se, npad), cp, 0, n, K, D, st);
   ctx->last_launches += l + 5;        // + combine (set above) + 5 ordering kernels
   return rc;
 }
@@ -542,7 +563,7 @@ int lb_ctx_destroy(lb_ctx* ctx) {
   cudaSetDevice(ctx->device);
   for (DevBuf* b : {&ctx->in, &ctx->rec, &ctx->partial, &ctx->out, &ctx->elem, &ctx->outer, &ctx->aux,
                     &ctx->order, &ctx->symord, &ctx->symrec, &ctx->syminv, &ctx->symi, &ctx->symj,
-                    &ctx->symtot, &ctx->symctr, &ctx->sweepctr})
+                    &ctx->symtot, &ctx->symctr, &ctx->sweepctr, &ctx->symstats})
     if (b->p) cudaFree(b->p);
   for (auto& ev : ctx->ev)
     if (ev) cudaEventDestroy(ev);
@@ -810,45 +831,63 @@ int lb_sym_partial_dev(lb_ctx* ctx, int S, double eps_d, int rank, int world, do
                               (cudaStream_t)stream);
 }
 
-int lb_sym_combine_dev(lb_ctx* ctx, int S, const double* tot, const double* coK, const double* coD,
-                       int q0, int q1, double* K_out, double* D_out, void* stream) {
+int lb_sym_groups(int rank, int world, int* g0, int* g1) {
+  if (world < 1 || rank < 0 || rank >= world) return fail(LB_EINVAL, "bad rank / world");
+  int a, b;
+  sym_rank_groups(rank, world, a, b);
+  if (g0) *g0 = a;
+  if (g1) *g1 = b;
+  return kSymGroups;
+}
+
+static int sym_combine_checked(lb_ctx* ctx, int S, const SymGroupPtrs& gp, const double* coK,
+                               const double* coD, int q0, int q1, double* K_out, double* D_out,
+                               void* stream) {
   int rc = use_ctx(ctx);
   if (rc) return rc;
   if (ctx->sym_n < 0 || ctx->sym_S != S) return fail(LB_EINVAL, "lb_sym_prepare_dev not called for this S");
   if (q0 < 0 || q1 > ctx->sym_n || q0 > q1) return fail(LB_EINVAL, "bad point range");
   if (!coK || !coD) return fail(LB_EINVAL, "null coupling table");
+  for (int g = 0; g < kSymGroups; ++g)
+    if (!gp.p[g]) return fail(LB_EINVAL, "null group-sum pointer");
   Coupling cp;
   make_coupling(S, coK, coD, cp);
   if (cp.Se != ctx->sym_Se) return fail(LB_EINVAL, "coupling differs from lb_sym_prepare_dev's");
-  return sym_combine_dispatch(ctx, cp.Se, tot, cp, q0, q1, K_out, D_out, (cudaStream_t)stream);
+  return sym_combine_dispatch(ctx, cp.Se, gp, cp, q0, q1, K_out, D_out, (cudaStream_t)stream);
 }
 
-int lb_sym_combine_peers_dev(lb_ctx* ctx, int S, const double* const* tots, int G, const double* coK,
-                             const double* coD, int q0, int q1, double* K_out, double* D_out,
-                             void* stream) {
+int lb_sym_combine_dev(lb_ctx* ctx, int S, const double* tot, const double* coK, const double* coD,
+                       int q0, int q1, double* K_out, double* D_out, void* stream) {
+  if (!tot) return fail(LB_EINVAL, "null group sums");
+  if (!ctx || ctx->sym_n < 0) return fail(LB_EINVAL, "lb_sym_prepare_dev not called");
+  return sym_combine_checked(ctx, S, sym_local_groups(tot, ctx->sym_Se, ctx->sym_nt * kSymTile), coK,
+                             coD, q0, q1, K_out, D_out, stream);
+}
+
+int lb_sym_combine_groups_dev(lb_ctx* ctx, int S, const double* const* group_ptrs, const double* coK,
+                              const double* coD, int q0, int q1, double* K_out, double* D_out,
+                              void* stream) {
+  if (!group_ptrs) return fail(LB_EINVAL, "null group pointer array");
+  SymGroupPtrs gp;
+  for (int g = 0; g < kSymGroups; ++g) gp.p[g] = group_ptrs[g];
+  return sym_combine_checked(ctx, S, gp, coK, coD, q0, q1, K_out, D_out, stream);
+}
+
+int lb_sym_counters(lb_ctx* ctx, int enable, unsigned long long* out) {
   int rc = use_ctx(ctx);
   if (rc) return rc;
-  if (ctx->sym_n < 0 || ctx->sym_S != S) return fail(LB_EINVAL, "lb_sym_prepare_dev not called for this S");
-  if (q0 < 0 || q1 > ctx->sym_n || q0 > q1) return fail(LB_EINVAL, "bad point range");
-  if (!coK || !coD || !tots || G < 1) return fail(LB_EINVAL, "null argument or no ranks");
-  Coupling cp;
-  make_coupling(S, coK, coD, cp);
-  if (cp.Se != ctx->sym_Se) return fail(LB_EINVAL, "coupling differs from lb_sym_prepare_dev's");
-  if (q1 == q0) return LB_OK;
-  const int npad = ctx->sym_nt * kSymTile;
-  const int* inv = static_cast<const int*>(ctx->syminv.p);
-  cudaStream_t st = (cudaStream_t)stream;
-  const int grid = (q1 - q0 + 127) / 128;
-  switch (cp.Se) {
-    case 1: lb_sym_combine_peers_kernel<1><<<grid, 128, 0, st>>>(tots, G, npad, inv, q0, q1, cp, K_out, D_out); break;
-    case 2: lb_sym_combine_peers_kernel<2><<<grid, 128, 0, st>>>(tots, G, npad, inv, q0, q1, cp, K_out, D_out); break;
-#if LB_SYM_MAXS >= 3
-    case 3: lb_sym_combine_peers_kernel<3><<<grid, 128, 0, st>>>(tots, G, npad, inv, q0, q1, cp, K_out, D_out); break;
-#endif
-    default: return fail(LB_EINVAL, "symmetric sweep supports S <= " + std::to_string(kSymMaxS));
+  if (out) {
+    unsigned long long h[4] = {0, 0, 0, 0};
+    if (ctx->symstats.p) {
+      LB_CUDA(cudaDeviceSynchronize());
+      LB_CUDA(cudaMemcpy(h, ctx->symstats.p, sizeof(h), cudaMemcpyDeviceToHost));
+    }
+    for (int k = 0; k < 3; ++k) out[k] = h[k];
   }
-  LB_CUDA(cudaGetLastError());
-  ctx->last_launches = 1;
+  if ((rc = ensure(ctx->symstats, 4 * sizeof(unsigned long long)))) return rc;
+  LB_CUDA(cudaDeviceSynchronize());
+  LB_CUDA(cudaMemset(ctx->symstats.p, 0, 4 * sizeof(unsigned long long)));
+  ctx->sym_count = enable != 0;
   return LB_OK;
 }
 

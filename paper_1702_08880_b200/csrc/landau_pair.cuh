@@ -346,13 +346,14 @@ __device__ __forceinline__ double pair_tensor_sym(const Outer& o, double rn, dou
 // coefficient is loaded once for U fused multiply-adds and the U dependency
 // chains overlap.  The closed form for S2/S3 is evaluated for every pair and
 // replaced by the series where m < 0.01 (kernel.py:366-378 likewise computes
-// both and selects).
+// both and selects).  `nser` counts the calls that took the series branch
+// (the benchmark's executed-instruction count; callers may ignore it).
 template <int U>
 __device__ __forceinline__ void pair_tensor_sym_x(const Outer (&oo)[U], const double (&rn)[U],
                                                   const double (&zn)[U], const double (&rn2)[U],
                                                   const double (&rcpr)[U], long long gthr,
                                                   const double2* __restrict__ logt, T5 (&t)[U],
-                                                  double (&txx2)[U]) {
+                                                  double (&txx2)[U], unsigned& nser) {
   PairS1 s[U];
   double lx[U], x[U];
 #pragma unroll
@@ -424,6 +425,7 @@ __device__ __forceinline__ void pair_tensor_sym_x(const Outer (&oo)[U], const do
     any |= ser[u];
   }
   if (any) {
+    ++nser;
     double m[U], s2[U], s3[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {

@@ -202,7 +202,8 @@ __global__ void __launch_bounds__(kTI, kMinBlocks) lb_sweep_kernel(const SweepAr
         const double rn2[2] = {ax0.x, ax1.x}, rcpr[2] = {ax0.y, ax1.y};
         T5 t[2];
         double txx2[2];  // (unused: the general path has no swapped pair)
-        pair_tensor_sym_x<2>(oo, rn, zn, rn2, rcpr, a.gthr, logt, t, txx2);
+        unsigned nser_unused = 0;
+        pair_tensor_sym_x<2>(oo, rn, zn, rn2, rcpr, a.gthr, logt, t, txx2, nser_unused);
         accumulate(t[0], rp0);
         accumulate(t[1], rp1);
       }

@@ -27,6 +27,17 @@
 //  * a reduction kernel adds, per point and in a fixed order, its i-side
 //    segments and the j-side blocks of every row that has its tile as a
 //    partner.  No atomics: results are bitwise reproducible.
+//
+// Summation order (independent of the GPU count): the rows are cut into
+// kSymGroups = 8 fixed row groups (boundaries nt*g/8).  A point's total is
+// ((T_0 + T_1) + ...) + T_7 in group order, where T_g adds, by increasing row
+// I of group g, the j-side block of row I (if the point's tile is one of its
+// partners) or, at I = the point's own row, its i-side segments.  A rank of a
+// G-GPU split owns whole groups (groups 8r/G .. 8(r+1)/G - 1, the same rows
+// as an even split when G divides 8), computes their T_g, and the owner of a
+// point adds all eight in group order -- so every bit of K and D is the same
+// for G = 1, 2, 4, 8 (and any G <= 8), as the reference promises for its
+// `workers` (kernel.py:508-511, test_kernel.py:197-212).
 #pragma once
 #include "landau_sweep.cuh"
 
@@ -76,6 +87,21 @@ __host__ __device__ __forceinline__ int sym_nseg(int nt) {
   return (sym_hmax(nt) + 1 + L - 1) / L;
 }
 
+// fixed row groups: the outer level of every point's summation order
+constexpr int kSymGroups = 8;
+__host__ __device__ __forceinline__ int sym_group_row(int g, int nt) {
+  return (int)((long long)nt * g / kSymGroups);
+}
+// groups [g0, g1) of rank `rank` among `world` (contiguous, whole groups)
+__host__ __device__ __forceinline__ void sym_rank_groups(int rank, int world, int& g0, int& g1) {
+  g0 = (int)((long long)kSymGroups * rank / world);
+  g1 = (int)((long long)kSymGroups * (rank + 1) / world);
+}
+// device pointers of the eight group sums T_g ([5S][npad] each), in group order
+struct SymGroupPtrs {
+  const double* p[kSymGroups];
+};
+
 #ifndef LB_SYM_IB
 #define LB_SYM_IB 1  // species-collapsed sweep: two outer points per thread (lb_symsweep_ib_kernel)
 #endif
@@ -102,6 +128,12 @@ struct SymArgs {
   double* iside;      // [row - row0][nseg][5S][128]
   double* jside;      // [row - row0][hmax][5S][128]
   int* next_item;     // work counter (zero at launch): items past the first wave
+  // optional execution counters (species-collapsed kernel; NULL: off):
+  // [0] off-diagonal thread-steps, [1] diagonal thread-steps, [2] thread-steps
+  // that took the m < 0.01 series branch -- with the per-step FP64
+  // instruction counts read from this kernel's SASS they give the executed
+  // FP64 work of a launch (bench.py, tools/sass_fp64.py)
+  unsigned long long* stats;
   int nt, row0, row1, nseg, hmax;
   long long gthr;
 };
@@ -371,6 +403,7 @@ __global__ void __launch_bounds__(kIbThreads, LB_IB_MINB) lb_symsweep_ib_kernel(
   double gi[2][S][3];
   double acc[2][S][5];
   int cur = -1, I = 0;
+  unsigned n_off = 0, n_diag = 0, n_ser = 0;  // thread-steps (execution counters)
   auto pidx = [&](int ib) { return warp * 64 + ib * 32 + lane; };
   auto flush_iside = [&]() {
 #pragma unroll
@@ -455,7 +488,7 @@ __global__ void __launch_bounds__(kIbThreads, LB_IB_MINB) lb_symsweep_ib_kernel(
         }
         T5 t[P2];
         double txx2[P2];
-        pair_tensor_sym_x<P2>(oo, rn, zn, rn2, rcpr, a.gthr, logt, t, txx2);
+        pair_tensor_sym_x<P2>(oo, rn, zn, rn2, rcpr, a.gthr, logt, t, txx2, n_ser);
 #pragma unroll
         for (int u = 0; u < JU; ++u)
 #pragma unroll
@@ -523,6 +556,7 @@ __global__ void __launch_bounds__(kIbThreads, LB_IB_MINB) lb_symsweep_ib_kernel(
 #pragma unroll
           for (int q = 0; q < 5; ++q) ju[u][b][q] = __shfl_sync(0xffffffffu, ju[u][b][q], (lane + 1) & 31);
 #endif
+      if (diag) n_diag += L; else n_off += L;
       // lane l holds accumulator u of j = l + (u+1)L: gather j = l in u order
       double jacc[S][5];
 #pragma unroll
@@ -561,78 +595,115 @@ __global__ void __launch_bounds__(kIbThreads, LB_IB_MINB) lb_symsweep_ib_kernel(
     if (lane == 0) mbar_arrive(&empty[s]);
   }
   if (cur >= 0) flush_iside();
+  if (a.stats) {
+    unsigned long long c0 = n_off, c1 = n_diag, c2 = n_ser;
+#pragma unroll
+    for (int o2 = 16; o2 > 0; o2 >>= 1) {
+      c0 += __shfl_xor_sync(0xffffffffu, c0, o2);
+      c1 += __shfl_xor_sync(0xffffffffu, c1, o2);
+      c2 += __shfl_xor_sync(0xffffffffu, c2, o2);
+    }
+    if (lane == 0) {
+      atomicAdd(a.stats + 0, c0);
+      atomicAdd(a.stats + 1, c1);
+      atomicAdd(a.stats + 2, c2);
+    }
+  }
 }
 
-// Fixed-order reduction of one row batch [row0, row1) into the running
-// totals tot[5S][nt*128] (SoA): per point, its own row's i-side segments (if
-// the row is in the batch), then the j-side block of every batch row I that
-// has this tile as a partner (d = P - I mod nt in 1..H(I)), by increasing I.
-// Batches are processed in increasing row order, so each point's sum order
-// is a function of n (and the row-batch size) only.
+// Fixed-order reduction of one row batch [row0, row1) into the group sums
+// T_g (tot + (g - gbase) [5S][npad], SoA) of every group the batch touches:
+// per point, by increasing row I within the group, the j-side block of row
+// I when the point's tile P is one of its partners (d = P - I mod nt in
+// 1..H(I)) or, at I = P, the sum of the point's own i-side segments (added
+// among themselves in segment order).  A group's first
+// batch starts its sums from zero.  The order depends only on n, never on
+// the batching or on which rank runs the group (landau_sym.cuh header).
 template <int S>
 __global__ void lb_symreduce_kernel(const double* __restrict__ iside, const double* __restrict__ jside,
-                                    int nt, int row0, int row1, int nseg, int hmax, int first,
+                                    int nt, int row0, int row1, int nseg, int hmax, int gbase,
                                     double* __restrict__ tot) {
   const int p = blockIdx.x * blockDim.x + threadIdx.x;
   const int npad = nt * kSymTile;
   if (p >= npad) return;
   const int P = p / kSymTile, t = p % kSymTile;
-  double v[5 * S];
-#pragma unroll
-  for (int c = 0; c < 5 * S; ++c) v[c] = first ? 0.0 : tot[(size_t)c * npad + p];
 #ifndef LB_RED_G
 #define LB_RED_G 8
 #endif
   constexpr int G = LB_RED_G;
-  if (P >= row0 && P < row1) {
-    // own row's segments, in groups of G loads ahead of their ordered adds
+  // the point's own i-side segments (its row's partners, in segment order),
+  // added into the group sum at I = P
+  double own[5 * S];
+  const bool has_own = P >= row0 && P < row1;
+  if (has_own) {
     const int nsg = min(nseg, sym_h(P, nt) / sym_seglen(nt) + 1);
-    for (int s0 = 0; s0 < nsg; s0 += G) {
+    const double* src = iside + (size_t)(P - row0) * nseg * (5 * S) * kSymTile + t;
+#pragma unroll
+    for (int c = 0; c < 5 * S; ++c) own[c] = src[(size_t)c * kSymTile];
+#pragma unroll 1
+    for (int s1 = 1; s1 < nsg; s1 += G) {
       double x[G][5 * S];
 #pragma unroll
-      for (int g = 0; g < G; ++g)
-        if (s0 + g < nsg) {
-          const double* src = iside + ((size_t)(P - row0) * nseg + s0 + g) * (5 * S) * kSymTile + t;
+      for (int k = 0; k < G; ++k)
+        if (s1 + k < nsg) {
+          const double* sp = src + (size_t)(s1 + k) * (5 * S) * kSymTile;
 #pragma unroll
-          for (int c = 0; c < 5 * S; ++c) x[g][c] = src[(size_t)c * kSymTile];
+          for (int c = 0; c < 5 * S; ++c) x[k][c] = sp[(size_t)c * kSymTile];
         }
 #pragma unroll
-      for (int g = 0; g < G; ++g)
-        if (s0 + g < nsg) {
+      for (int k = 0; k < G; ++k)
+        if (s1 + k < nsg) {
 #pragma unroll
-          for (int c = 0; c < 5 * S; ++c) v[c] = __dadd_rn(v[c], x[g][c]);
+          for (int c = 0; c < 5 * S; ++c) own[c] = __dadd_rn(own[c], x[k][c]);
         }
     }
   }
-  // d = (P - I) mod nt, stepped down with I (no integer division per row);
-  // rows in groups of G: the group's loads are issued before its adds, which
-  // stay in increasing-I order (the condition is uniform across the block)
-  int d = (P - row0) % nt;
-  if (d < 0) d += nt;
-  for (int I0 = row0; I0 < row1; I0 += G) {
-    double x[G][5 * S];
-    bool on[G];
+#pragma unroll 1
+  for (int g = 0; g < kSymGroups; ++g) {
+    const int gb0 = sym_group_row(g, nt), gb1 = sym_group_row(g + 1, nt);
+    const int lo = max(row0, gb0), hi = min(row1, gb1);
+    if (lo >= hi) continue;
+    LB_DCHECK(g >= gbase);
+    double* T = tot + (size_t)(g - gbase) * (5 * S) * npad;
+    double v[5 * S];
 #pragma unroll
-    for (int g = 0; g < G; ++g) {
-      const int I = I0 + g;
-      on[g] = I < row1 && d >= 1 && d <= sym_h(I, nt);
-      if (on[g]) {
-        LB_DCHECK(d >= 1 && d <= hmax);
-        const double* src = jside + ((size_t)(I - row0) * hmax + (d - 1)) * (5 * S) * kSymTile + t;
+    for (int c = 0; c < 5 * S; ++c) v[c] = lo == gb0 ? 0.0 : T[(size_t)c * npad + p];
+    // d = (P - I) mod nt, stepped down with I (no integer division per row);
+    // rows in groups of G: the group's loads are issued before its adds, which
+    // stay in increasing-I order (the conditions are uniform across the block)
+    int d = (P - lo) % nt;
+    if (d < 0) d += nt;
+#pragma unroll 1
+    for (int I0 = lo; I0 < hi; I0 += G) {
+      double x[G][5 * S];
+      bool on[G];
 #pragma unroll
-        for (int c = 0; c < 5 * S; ++c) x[g][c] = src[(size_t)c * kSymTile];
+      for (int k = 0; k < G; ++k) {
+        const int I = I0 + k;
+        on[k] = I < hi && d >= 1 && d <= sym_h(I, nt);
+        if (on[k]) {
+          LB_DCHECK(d >= 1 && d <= hmax);
+          const double* src = jside + ((size_t)(I - row0) * hmax + (d - 1)) * (5 * S) * kSymTile + t;
+#pragma unroll
+          for (int c = 0; c < 5 * S; ++c) x[k][c] = src[(size_t)c * kSymTile];
+        }
+        d = d == 0 ? nt - 1 : d - 1;
       }
-      d = d == 0 ? nt - 1 : d - 1;
+#pragma unroll
+      for (int k = 0; k < G; ++k) {
+        if (has_own && I0 + k == P && P < hi) {
+#pragma unroll
+          for (int c = 0; c < 5 * S; ++c) v[c] = __dadd_rn(v[c], own[c]);
+        }
+        if (on[k]) {
+#pragma unroll
+          for (int c = 0; c < 5 * S; ++c) v[c] = __dadd_rn(v[c], x[k][c]);
+        }
+      }
     }
 #pragma unroll
-    for (int g = 0; g < G; ++g)
-      if (on[g]) {
-#pragma unroll
-        for (int c = 0; c < 5 * S; ++c) v[c] = __dadd_rn(v[c], x[g][c]);
-      }
+    for (int c = 0; c < 5 * S; ++c) T[(size_t)c * npad + p] = v[c];
   }
-#pragma unroll
-  for (int c = 0; c < 5 * S; ++c) tot[(size_t)c * npad + p] = v[c];
 }
 
 // Sorted, padded records: rec_s[p] = rec[perm[p]] for p < n, inert records
@@ -654,33 +725,15 @@ __global__ void lb_sym_gather_kernel(int n, int npad, int RS, const int* __restr
   }
 }
 
-// K/D for original points [q0, q1) from the totals (sorted order) through
-// the inverse permutation; coupling as _combine (kernel.py:419-440).
+// K/D for original points [q0, q1) from the eight group sums (sorted point
+// order, through the inverse permutation), added in group order; coupling as
+// _combine (kernel.py:419-440).  The group sums may live on other GPUs: with
+// peer pointers (CUDA IPC over NVLink) this kernel is the cross-rank
+// reduction and the combine in one, reading only this rank's points.
 template <int Se>
-__global__ void lb_sym_combine_kernel(const double* __restrict__ tot, int npad,
-                                      const int* __restrict__ inv, int q0, int q1, const Coupling cp,
-                                      double* __restrict__ K, double* __restrict__ D) {
-  const int q = q0 + blockIdx.x * blockDim.x + threadIdx.x;
-  if (q >= q1) return;
-  const int p = inv[q];
-  double A[Se][5];
-#pragma unroll
-  for (int b = 0; b < Se; ++b)
-#pragma unroll
-    for (int c = 0; c < 5; ++c) A[b][c] = tot[(size_t)(b * 5 + c) * npad + p];
-  write_kd<Se>(A, cp, (size_t)(q - q0), K, D);
-}
-
-// Peer-memory variant fused with the cross-rank reduction: the partial
-// sums of all G ranks are read directly (tots[g] are peer pointers mapped
-// over NVLink with CUDA IPC) for this rank's own points only and added in
-// rank order before the coupling -- the all-reduce + combine of the NCCL
-// path as one kernel, moving only this rank's share of every rank's sums.
-template <int Se>
-__global__ void lb_sym_combine_peers_kernel(const double* const* __restrict__ tots, int G, int npad,
-                                            const int* __restrict__ inv, int q0, int q1,
-                                            const Coupling cp, double* __restrict__ K,
-                                            double* __restrict__ D) {
+__global__ void lb_sym_combine_kernel(const SymGroupPtrs gp, int npad, const int* __restrict__ inv,
+                                      int q0, int q1, const Coupling cp, double* __restrict__ K,
+                                      double* __restrict__ D) {
   const int q = q0 + blockIdx.x * blockDim.x + threadIdx.x;
   if (q >= q1) return;
   const int p = inv[q];
@@ -689,8 +742,10 @@ __global__ void lb_sym_combine_peers_kernel(const double* const* __restrict__ to
   for (int b = 0; b < Se; ++b)
 #pragma unroll
     for (int c = 0; c < 5; ++c) {
-      double v = tots[0][(size_t)(b * 5 + c) * npad + p];
-      for (int g = 1; g < G; ++g) v = __dadd_rn(v, tots[g][(size_t)(b * 5 + c) * npad + p]);
+      const size_t off = (size_t)(b * 5 + c) * npad + p;
+      double v = gp.p[0][off];
+#pragma unroll
+      for (int g = 1; g < kSymGroups; ++g) v = __dadd_rn(v, gp.p[g][off]);
       A[b][c] = v;
     }
   write_kd<Se>(A, cp, (size_t)(q - q0), K, D);

@@ -8,11 +8,16 @@ fields of its own points, packs them into inner records on its device
 replicates the packed records of every point to every rank -- the paper's
 per-point field state (w f, w grad f) plus coordinates, 10 doubles per point
 at S = 2, 5.2 MB at N = 2^16.  Then, either
- * symmetric path (S <= 2, outer set == inner set, the default here): every
-   rank Morton-orders all records identically, evaluates its share of the
-   unordered tile pairs (each pair once, feeding both points), and one
-   all-reduce adds the ranks' 5S partial sums per point (5.2 MB); each rank
-   applies the coupling to its own points; or
+ * symmetric path (outer set == inner set, the default here): every rank
+   Morton-orders all records identically and evaluates its share of the
+   unordered tile pairs (each pair once, feeding both points): whole row
+   groups of the fixed 8-group split (`lb_sym_groups`), one sum per group and
+   point.  One all-gather replicates the group sums (2.6 MB per group at
+   N = 2^16), and each rank adds, for its own points only, all eight in group
+   order and applies the coupling -- so K and D are bitwise the same for any
+   GPU count <= 8 (the reference promises bitwise invariance to `workers`,
+   kernel.py:508-511).  In peer-memory mode the owner reads the peers' group
+   sums directly over NVLink instead of the all-gather; or
  * general path: each rank sweeps its own outer points against all inner
    points (`lb_sweep_dev`); no collective follows.  Because the inner
    chunking depends only on the global inner count, every rank's K/D rows
@@ -34,7 +39,14 @@ from . import _lib
 from .kernel import coupling
 from .synthetic import shard_bounds
 
-__all__ = ["ShardPlan", "ShardedSweep"]
+__all__ = ["ShardPlan", "ShardedSweep", "SYM_GROUPS", "sym_rank_groups"]
+
+SYM_GROUPS = 8  # kSymGroups of landau_sym.cuh (lb_sym_groups)
+
+
+def sym_rank_groups(rank: int, world: int):
+    """Row groups [g0, g1) of `rank` among `world` (lb_sym_groups)."""
+    return SYM_GROUPS * rank // world, SYM_GROUPS * (rank + 1) // world
 
 
 @dataclass(frozen=True)
@@ -61,6 +73,16 @@ class ShardPlan:
         return len(set(self.counts)) == 1
 
 
+def _device_index(device) -> int:
+    """CUDA ordinal of a torch device; torch.device("cuda") means the current
+    device (under torchrun: the rank's own GPU), not GPU 0."""
+    import torch
+
+    if device.index is not None:
+        return int(device.index)
+    return int(torch.cuda.current_device()) if torch.cuda.is_available() else 0
+
+
 def _dist():
     import torch.distributed as dist
 
@@ -80,10 +102,13 @@ class ShardedSweep:
     align : shard alignment in points (9 = whole Q2 cells; 1 for point clouds)
     pack_fn, sweep_fn : injectable for CPU testing; default to the CUDA
              library (lb_pack_records_dev / lb_sweep_dev on torch tensors)
-    p2p : symmetric path only -- replace the all-reduce of the partial sums
-             and the combine by one kernel that reads every rank's partial
-             sums for this rank's own points through CUDA IPC peer mappings
-             (NVLink), ordered by stream-level barriers
+    p2p : symmetric path only -- replace the all-gather of the group sums
+             by one kernel that reads every rank's group sums for this
+             rank's own points through CUDA IPC peer mappings (NVLink),
+             ordered by stream-level barriers
+    sym_fns : injectable (prepare(rec), partial(tot), combine(groups, q0, q1,
+             K, D)) for CPU testing of the symmetric host logic; `groups` is
+             the list of the eight group-sum arrays in group order
     """
 
     def __init__(self, n: int, S: int, params, eps_d: float, device, align: int = 9,
@@ -105,7 +130,10 @@ class ShardedSweep:
         if pack_fn is None or sweep_fn is None:
             lib = _lib.load()
             self._lib = lib
-            self._ctx = _lib.context(self.device.index or 0)
+            # a context of its own: its stream-ordered scratch (sorted records,
+            # partial sums) is used on torch's stream, so it must not be shared
+            # with the host entry points' cached context and its stream
+            self._ctx = _lib.Context(_device_index(self.device))
             p = _lib.dptr
             self.RS = lib.lb_record_stride(self.S, p(self.coK), p(self.coD))
             self.nacc = lib.lb_accumulator_sets(self.S, p(self.coK), p(self.coD))
@@ -132,13 +160,20 @@ class ShardedSweep:
         self._p2p_pending = False
         self._opened = []
         self._ipc_ptr = None
-        if self.symmetric:  # partial sums: 5 per accumulator set (1 set when collapsed)
-            npad = -(-self.n // 128) * 128
-            shape = (5 * max(self.nacc, 1), npad)
+        if self.symmetric:
+            # group sums: 5 per accumulator set (1 set when collapsed) and point,
+            # one slot per row group this rank owns (lb_sym_groups)
+            self.npad = -(-self.n // 128) * 128
+            self.g0, self.g1 = sym_rank_groups(self.rank, self.world)
+            self.ngmax = max(b - a for a, b in (sym_rank_groups(r, self.world)
+                                                 for r in range(self.world)))
+            shape = (max(self.ngmax, 1), 5 * max(self.nacc, 1), self.npad)
             if self.p2p:
                 self.tot = self._init_p2p(shape)
             else:
                 self.tot = torch.zeros(shape, dtype=torch.float64, device=self.device)
+            self.gathered = (self.tot if self.world == 1 or self.p2p else torch.zeros(
+                (self.world * shape[0],) + shape[1:], dtype=torch.float64, device=self.device))
         mc = self.plan.max_count
         f64 = torch.float64
         self.send = torch.zeros((mc, self.RS), dtype=f64, device=self.device)
@@ -177,7 +212,7 @@ class ShardedSweep:
             _lib.check(lib.lb_ipc_open(ctx, h, C.byref(q)))
             self._opened.append(q.value)
             peers.append(q.value)
-        self._peer_ptrs = torch.tensor(peers, dtype=torch.int64, device=self.device)
+        self._peers = peers
         self._flag = torch.zeros(1, dtype=torch.float64, device=self.device)
 
         class _View:  # torch view of the IPC allocation (__cuda_array_interface__)
@@ -252,11 +287,44 @@ class ShardedSweep:
                                                 self.world, tot.data_ptr(), self._stream()))
         self.launches += self._lib.lb_last_launch_count(self._ctx.handle)
 
-    def _sym_combine_cuda(self, tot, q0, q1, K, D):
+    def _group_owner(self, g: int):
+        """(rank, slot) holding row group g's sums."""
+        for r in range(self.world):
+            a, b = sym_rank_groups(r, self.world)
+            if a <= g < b:
+                return r, g - a
+        raise AssertionError(g)
+
+    def _group_ptrs(self):
+        """Device pointers of the eight group sums in group order: the local
+        buffer (one rank), the all-gathered copy, or the peers' buffers."""
+        slot = 8 * 5 * max(self.nacc, 1) * self.npad
+        out = []
+        for g in range(SYM_GROUPS):
+            r, k = self._group_owner(g)
+            if self.p2p:
+                base = self._peers[r]
+            else:
+                base = self.gathered.data_ptr() + r * self.tot.shape[0] * slot
+            out.append(base + k * slot)
+        return out
+
+    def _group_views(self):
+        """The eight group-sum arrays in group order (non-peer modes)."""
+        views = []
+        for g in range(SYM_GROUPS):
+            r, k = self._group_owner(g)
+            views.append(self.gathered[r * self.tot.shape[0] + k])
+        return views
+
+    def _sym_combine_cuda(self, groups, q0, q1, K, D):
+        import ctypes as C
+
         p = _lib.dptr
-        _lib.check(self._lib.lb_sym_combine_dev(self._ctx.handle, self.S, tot.data_ptr(),
-                                                p(self.coK), p(self.coD), q0, q1, K.data_ptr(),
-                                                D.data_ptr(), self._stream()))
+        arr = (C.c_void_p * SYM_GROUPS)(*self._group_ptrs())
+        _lib.check(self._lib.lb_sym_combine_groups_dev(
+            self._ctx.handle, self.S, arr, p(self.coK), p(self.coD), q0, q1, K.data_ptr(),
+            D.data_ptr(), self._stream()))
         self.launches += self._lib.lb_last_launch_count(self._ctx.handle)
 
     # ---------------------------------------------------------------- steps
@@ -288,34 +356,31 @@ class ShardedSweep:
         self._sym_prepare(self.rec[:self.n])
 
     def sym_partial(self):
-        """Step 2: this rank's share of the unordered tile pairs -> tot."""
+        """Step 2: this rank's row groups of the unordered tile pairs -> its
+        group sums (tot)."""
         if self.p2p and self._p2p_pending:  # peers may still read our last sums
             self._barrier()
             self._p2p_pending = False
         self._sym_partial(self.tot)
 
     def sym_reduce(self):
-        """Step 3: add the ranks' partial sums (one all-reduce of 5S doubles
-        per point, 5.2 MB at N = 2^16, S = 2); peer-memory mode: only order
-        every rank's partial sums before the fused combine."""
+        """Step 3: replicate every rank's group sums (one all-gather, 2.6 MB
+        per group at N = 2^16, S = 2); peer-memory mode: only order every
+        rank's group sums before the fused combine."""
         if self.p2p:
             self._barrier()
         elif self.world > 1:
-            _dist().all_reduce(self.tot, group=self.group)
+            _dist().all_gather_into_tensor(self.gathered, self.tot, group=self.group)
 
     def sym_finish(self):
-        """Step 4: coupling -> K, D for this rank's own points (peer-memory
-        mode: the cross-rank sum for these points, fused)."""
+        """Step 4: the eight group sums of this rank's own points, added in
+        group order, and the coupling -> K, D (peer-memory mode: read from
+        the peers' buffers)."""
         if self.p2p:
-            p = _lib.dptr
-            _lib.check(self._lib.lb_sym_combine_peers_dev(
-                self._ctx.handle, self.S, self._peer_ptrs.data_ptr(), self.world, p(self.coK),
-                p(self.coD), self.lo, self.hi, self.K.data_ptr(), self.D.data_ptr(),
-                self._stream()))
-            self.launches += self._lib.lb_last_launch_count(self._ctx.handle)
+            self._sym_combine(None, self.lo, self.hi, self.K, self.D)
             self._p2p_pending = True
             return self.K, self.D
-        self._sym_combine(self.tot, self.lo, self.hi, self.K, self.D)
+        self._sym_combine(self._group_views(), self.lo, self.hi, self.K, self.D)
         return self.K, self.D
 
     def step(self, r, z, w, f, dfr, dfz):
@@ -348,12 +413,16 @@ class ShardedOperator:
          small replicated vector -- and samples ITS cells on the device
          (`lb_sample_state_dev`, K4);
       2. packs its points and all-gathers the packed field state (NCCL);
-      3. evaluates its share of the unordered tile pairs (symmetric sweep),
-         one all-reduce of the per-point partial sums, coupling for its own
-         points (K, D of its cells);
-      4. contracts its cells' element matrices and gathers them into a
-         partial CSR value array (`lb_operator_partial_dev`, K2 + K3);
-      5. one all-reduce of the CSR values (S x nnz) gives every rank C.
+      3. evaluates its row groups of the unordered tile pairs (symmetric
+         sweep), one all-gather of the per-group sums, the group-ordered sum
+         and the coupling for its own points (K, D of its cells);
+      4. one all-gather of every point's (w, K, D) -- 1 + 6S doubles per
+         point, 14.7 MB at config 4 -- and every rank contracts all cells'
+         element matrices and gathers them into the CSR values
+         (`lb_operator_partial_dev` over all cells, K2 + K3: ~0.3 ms at config
+         4).  Every rank thus holds C, bitwise the single-GPU operator for
+         any GPU count (an all-reduce of per-rank partial CSR values would
+         re-associate the sums with G).
     """
 
     def __init__(self, mesh, ref, params, device, eps_d: float | None = None, group=None):
@@ -364,7 +433,7 @@ class ShardedOperator:
         self.device = torch.device(device)
         self.group = group
         self.S = int(np.asarray(params.mass_ratio_o).shape[0])
-        self.dm = device_mesh(mesh, ref, self.device.index or 0)
+        self.dm = device_mesh(mesh, ref, _device_index(self.device))
         if not self.dm.has_geometry:
             raise ValueError("mesh/ref lack origins/qpts/qwts needed for device sampling")
         self.ncell = self.dm.ncell
@@ -377,8 +446,18 @@ class ShardedOperator:
         self.coeffs = torch.empty((self.S, self.dm.n_free), dtype=f64, device=self.device)
         self.fields = torch.empty((3 + 3 * self.S, max(nl, 1)), dtype=f64, device=self.device)
         self.csr = torch.empty((self.S, self.dm.map.nnz), dtype=f64, device=self.device)
+        # all-gather buffers of (w, K, D) per point: 1 + 6S doubles
+        W = self.sweep.world
+        self._wkd_w = 1 + 6 * self.S
+        mc = self.sweep.plan.max_count
+        self._wkd_send = torch.zeros((mc, self._wkd_w), dtype=f64, device=self.device)
+        self._wkd_recv = (self._wkd_send if W == 1 else
+                          torch.zeros((W * mc, self._wkd_w), dtype=f64, device=self.device))
+        self._w_all = torch.empty(n, dtype=f64, device=self.device)
+        self._K_all = torch.empty((n, self.S, 2), dtype=f64, device=self.device)
+        self._D_all = torch.empty((n, self.S, 2, 2), dtype=f64, device=self.device)
         self._lib = _lib.load()
-        self._ctx = _lib.context(self.device.index or 0)
+        self._ctx = self.sweep._ctx  # the sweep's own context (not the cached one)
 
     def _stream(self):
         import torch
@@ -410,11 +489,27 @@ class ShardedOperator:
             o + 2 * row, o + 3 * row, o + (3 + self.S) * row, o + (3 + 2 * self.S) * row, st))
         r, z, w, f, dfr, dfz = (t.contiguous() for t in self.local_fields())
         K, D = self.sweep.step(r, z, w, f, dfr, dfz)
+        sw, S = self.sweep, self.S
+        if sw.world == 1:
+            w_all, K_all, D_all = w, K, D
+        else:  # replicate (w, K, D) of every point: one all-gather
+            nl = sw.hi - sw.lo
+            snd = self._wkd_send
+            snd[:nl, 0] = w
+            snd[:nl, 1:1 + 2 * S] = K.reshape(nl, 2 * S)
+            snd[:nl, 1 + 2 * S:] = D.reshape(nl, 4 * S)
+            _dist().all_gather_into_tensor(self._wkd_recv, snd, group=self.group)
+            mc = sw.plan.max_count
+            for k in range(sw.world):
+                lo, hi = sw.plan.bounds(k)
+                blk = self._wkd_recv[k * mc:k * mc + (hi - lo)]
+                self._w_all[lo:hi] = blk[:, 0]
+                self._K_all[lo:hi] = blk[:, 1:1 + 2 * S].reshape(hi - lo, S, 2)
+                self._D_all[lo:hi] = blk[:, 1 + 2 * S:].reshape(hi - lo, S, 2, 2)
+            w_all, K_all, D_all = self._w_all, self._K_all, self._D_all
         _lib.check(lib.lb_operator_partial_dev(
-            h, self.dm.handle, self.S, self.c0, self.c1, w.data_ptr(), K.data_ptr(), D.data_ptr(),
-            self.csr.data_ptr(), st))
-        if self.sweep.world > 1:
-            _dist().all_reduce(self.csr, group=self.group)
+            h, self.dm.handle, S, 0, self.ncell, w_all.data_ptr(), K_all.data_ptr(),
+            D_all.data_ptr(), self.csr.data_ptr(), st))
         vals = self.csr.cpu().numpy()
         gm = self.dm.map
         return [sp.csr_matrix((vals[a], gm.indices, gm.indptr), shape=(gm.n_free, gm.n_free))

@@ -122,8 +122,9 @@ class CNSolver:
     def set_mass(self, M=None):
         """Mass values: the caller's matrix mapped onto the pattern, or (None)
         assembled on the device (fem.py:152-167).  Re-uploaded only when M
-        changes (by identity)."""
-        key = ("device",) if M is None else ("host", id(M))
+        changes: by identity plus a content fingerprint, so in-place edits of
+        M are picked up."""
+        key = ("device",) if M is None else ("host", id(M), _fingerprint(M))
         if key == self._mass_key:
             return
         vals = None if M is None else pattern_values(M, self.indptr, self.indices, self.n)
@@ -160,6 +161,19 @@ class CNSolver:
             self.close()
         except Exception:
             pass
+
+
+def _fingerprint(M) -> tuple:
+    """Cheap content key of a sparse (or dense) matrix: shape, nnz and the
+    XOR of the bit patterns of its values and indices."""
+    data = np.ascontiguousarray(getattr(M, "data", M), dtype=np.float64).ravel()
+    key = (getattr(M, "shape", None), data.size,
+           int(np.bitwise_xor.reduce(data.view(np.int64))) if data.size else 0,
+           float(np.add.reduce(data)) if data.size else 0.0)
+    idx = getattr(M, "indices", None)
+    if idx is not None and idx.size:
+        key += (int(np.bitwise_xor.reduce(idx.astype(np.int64) * np.arange(1, idx.size + 1))),)
+    return key
 
 
 _SOLVERS: "OrderedDict[tuple, tuple]" = OrderedDict()
@@ -222,13 +236,15 @@ def newton_step(f_guess, f_old, mesh, ref, params, cfg, M=None, C_old=None):
     out = np.empty_like(g)
     rnorm = np.zeros(1)
     phase = np.zeros(4)
+    # the device C_old is overwritten (mode 0/1) before anything can fail, so
+    # the resident-copy marker is cleared first and set again only on success
+    solver._c_old_ref = None
     try:
         _lib.check(solver._lib.lb_cn_newton(
             solver.handle, _lib.dptr(coK), _lib.dptr(coD), eps, float(cfg.dt), _lib.dptr(g),
             _lib.dptr(f), _lib.dptr(Cv) if Cv is not None else None, mode, _lib.dptr(out), None,
             _lib.dptr(rnorm), _lib.dptr(phase)))
     except _lib.SingularSystem as err:
-        solver._c_old_ref = None
         raise _StepFailure(-1, f"linear solve failed: {err}") from err
     solver._c_old_ref = C_old  # held: its identity marks the resident copy
     # device phase times (ms) of the last call: assembly, residual + band

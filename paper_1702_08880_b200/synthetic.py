@@ -180,3 +180,52 @@ def cfg4_state(nodes: np.ndarray, species=CFG4_SPECIES, seed: int = 4):
     e = np.array([q for _, q, _, _ in species])
     nu = np.outer(e**2, e**2)
     return coeffs, nu / nu[0, 0], np.array([1.0 / m for m, _, _, _ in species])
+
+
+# ---------------------------------------------------------------- config 3, Q3
+# BASELINE config 3 as worded uses Q3 elements with 4x4 Gauss points; the
+# reference implements Q2 / 3x3 only (fem.py:33-36).  Its pair sweep
+# (`fused_sweep`, kernel.py:504-536) does not care which point set it gets,
+# so D/K on the Q3 point set of the refined mesh is pinned against it
+# (tests/golden/make_golden.py case_cfg3_q3); the Q3 element contraction has
+# no reference ("parity unpinned") and is not built.
+def gauss_points(origins, sizes, qpts, qwts):
+    """Quadrature points of every axis-aligned cell for a tensor rule on
+    [-1, 1]^2 (qpts (Nq, 2), qwts (Nq,)), in the reference's operation order
+    (fem.py:103-113): r, z (coords) and w = qwt * detJ * r, point n = Nq *
+    cell + q."""
+    origins = np.asarray(origins, dtype=np.float64)
+    sizes = np.asarray(sizes, dtype=np.float64)
+    nq = qpts.shape[0]
+    dr, dz = sizes[:, 0], sizes[:, 1]
+    detJ = np.broadcast_to((dr * dz / 4.0)[:, None], (sizes.shape[0], nq))
+    coords = origins[:, None, :] + (qpts[None, :, :] + 1.0) * 0.5 * sizes[:, None, :]
+    w = qwts[None, :] * detJ * coords[:, :, 0]
+    return (np.ascontiguousarray(coords[:, :, 0].ravel()),
+            np.ascontiguousarray(coords[:, :, 1].ravel()), np.ascontiguousarray(w.ravel()))
+
+
+def q3_points(origins, sizes):
+    """4x4 Gauss-Legendre points of every cell (z-major q = 4 kz + kr)."""
+    xi, wi = np.polynomial.legendre.leggauss(4)
+    qr, qz = np.meshgrid(xi, xi, indexing="xy")
+    return gauss_points(origins, sizes, np.stack([qr.ravel(), qz.ravel()], 1),
+                        (wi[None, :] * wi[:, None]).ravel())
+
+
+def cfg3_state_values(r, z):
+    """Config 3's distributions at arbitrary points, analytically: electrons
+    bi-Maxwellian (sigma_perp^2 = 0.8, sigma_par^2 = 1.2, T_par = 1.5 T_perp,
+    prefactor 1/2 like physics.py:97-100), ions Maxwellian (m = 4, T = 0.2,
+    physics.maxwellian_values); returns f, df_r, df_z of shape (2, n) and the
+    (nu_hat, mass_ratio_o) of collision_params (e^2 e^2 coupling, m_o = 1)."""
+    r = np.asarray(r, dtype=np.float64)
+    z = np.asarray(z, dtype=np.float64)
+    s_perp, s_par = 2.0 * 0.4, 2.0 * 0.6
+    fe = 0.5 * (math.pi ** 1.5 * s_perp * math.sqrt(s_par)) ** -1 * np.exp(-r * r / s_perp - z * z / s_par)
+    s2 = 2.0 * 0.2 / 4.0
+    fi = 0.5 * (np.pi * s2) ** -1.5 * np.exp(-(r ** 2 + z ** 2) / s2)
+    f = np.stack([fe, fi])
+    dfr = np.stack([-2.0 * r / s_perp * fe, -2.0 * r / s2 * fi])
+    dfz = np.stack([-2.0 * z / s_par * fe, -2.0 * z / s2 * fi])
+    return f, dfr, dfz, np.ones((2, 2)), np.array([1.0, 0.25])

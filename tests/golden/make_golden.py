@@ -509,6 +509,197 @@ def case_cfg4_meshes():
                                    ("W", 335000.0, 10.0, 0.001, 0.5)], (8, 16), seed=4)
 
 
+def _closest_owners(r, z, k=64):
+    from scipy.spatial import cKDTree
+
+    pts = np.stack([r, z], 1)
+    dist, _ = cKDTree(pts).query(pts, k=2)
+    return np.argsort(dist[:, 1], kind="stable")[:k]
+
+
+def _cfg4_species():
+    spec = [("e", 1.0, -1.0, 1.0, 1.0), ("D", 3670.0, 1.0, 0.8, 1.0),
+            ("C", 21900.0, 6.0, 0.02, 0.5), ("W", 335000.0, 10.0, 0.001, 0.5)]
+    return spec, [ax.Species(nm, m, q, T) for nm, m, q, _, T in spec]
+
+
+def case_cfg4_full():
+    """BASELINE config 4 at its stated size, shared mesh (reference-native):
+    cartesian_mesh(L=5, 64, 128), N = 73,728, S = 4 (e, D, C6+, W10+,
+    n = 1/0.8/0.02/0.001, T = 1/1/0.5/0.5, non-neutral, seeded 1 % noise --
+    the state of case_cfg4_species on the full mesh).  The FULL reference
+    assemble_collision (fused_sweep workers=1 over all 5.4e9 ordered pairs,
+    then the reference's transform + scatter), with the sweep's K/D captured:
+    stored are K/D at 128 evenly spaced whole cells + the 64 closest-pair
+    owners, those cells' element matrices (pinned restatement, oracle/), 256
+    evenly spaced rows of every species' C and each block's max |C|."""
+    import time
+
+    sys.path.insert(0, str(HERE.parents[1]))
+    from oracle import oracle as O
+
+    domain = ax.DomainSpec(L=5.0)
+    ref = ax.build_reference_element()
+    mesh = ax.cartesian_mesh(domain, 64, 128)
+    spec, sp_ = _cfg4_species()
+    r = mesh.nodes[mesh.free_nodes, 0]
+    z = mesh.nodes[mesh.free_nodes, 1]
+    rng = np.random.default_rng(4)
+    coeffs = []
+    for (nm, m, q, dens, T), s in zip(spec, sp_):
+        s2 = s.sigma2
+        vals = dens * (math.pi * s2) ** -1.5 * np.exp(-(r * r + z * z) / s2)
+        coeffs.append(vals * (1.0 + 0.01 * rng.standard_normal(vals.shape)))
+    state = ax.StateVector(np.stack(coeffs))
+    data = ax.sample_state(mesh, ref, state)
+    params = ax.collision_params(sp_)
+    eps_d = ax.assembly.default_eps_d(mesh)
+    seen = {}
+    sweep = ax.assembly.fused_sweep
+
+    def capture(*a, **k):  # assembly.py imports fused_sweep by value (assembly.py:38-43)
+        k["workers"] = 1
+        seen["KD"] = sweep(*a, **k)
+        return seen["KD"]
+
+    ax.assembly.fused_sweep = capture
+    t0 = time.time()
+    try:
+        cm = ax.assemble_collision(mesh, ref, data, params, eps_d=eps_d)
+    finally:
+        ax.assembly.fused_sweep = sweep
+    print(f"cfg4full: reference assemble_collision {time.time() - t0:.0f} s")
+    K, D = seen["KD"]
+    cells = np.unique(np.linspace(0, mesh.n_cells - 1, 128).astype(np.int64))
+    pts = (9 * cells[:, None] + np.arange(9)[None, :]).ravel()
+    idx = np.unique(np.concatenate([pts, _closest_owners(data.r, data.z)]))
+    elem = O.element_matrices(K[pts], D[pts], data.w[pts], mesh.sizes[cells], ref.B, ref.dB)
+    rows = np.unique(np.linspace(0, mesh.n_free - 1, 256).astype(np.int64))
+    out = {**mesh_parts(mesh, ref), **params_parts(params), "eps_d": np.float64(eps_d),
+           "coeffs": state.coeffs, "masses": np.array([s.mass for s in sp_]),
+           "idx": idx, "K": K[idx], "D": D[idx], "r_idx": data.r[idx], "z_idx": data.z[idx],
+           "w_idx": data.w[idx], "cells": cells, "elem": elem, "rows": rows,
+           "C_max": np.array([np.abs(b.data).max() for b in cm.blocks]),
+           "timings": np.array([cm.timings[k] for k in ("kernel", "fe_transform", "scatter")])}
+    for a, b in enumerate(cm.blocks):
+        out.update(csr_parts(f"R{a}", b[rows]))
+    save("cfg4full", **out)
+
+
+def case_cfg4_meshes_full():
+    """BASELINE config 4 as worded at its stated size: e, D, C6+, W10+ each
+    on its OWN 64x128 mesh over L_a = 5 sigma_a (294,912 union points, 8.7e10
+    ordered pairs), densities 1/0.8/0.02/0.001, T 1/1/0.5/0.5, 1 % seeded
+    noise.  Composed reference oracle on patches: per
+    species four 4x4-cell patches; the reference fused_sweep (workers=1) of
+    their points + the 64 closest-pair owners of the union against ALL union
+    points; each patch's element matrices (pinned restatement) condensed on
+    the species' mesh, keeping the rows of the 49 nodes interior to each
+    patch (those rows see only patch cells, so they are the full operator's
+    rows)."""
+    import time
+
+    sys.path.insert(0, str(HERE.parents[1]))
+    from oracle import oracle as O
+
+    spec, sp_ = _cfg4_species()
+    ref = ax.build_reference_element()
+    params = ax.collision_params(sp_)
+    rng = np.random.default_rng(4)
+    nr, nz = 64, 128
+    meshes, datas, coeffs = [], [], []
+    for (nm, m, q, dens, T), s in zip(spec, sp_):
+        mesh = ax.cartesian_mesh(ax.DomainSpec(L=5.0 * math.sqrt(s.sigma2)), nr, nz)
+        st = ax.maxwellian_init(mesh, ref, [s], neutralize=False)
+        st.coeffs *= 2.0 * dens  # the reference prefactor is 1/2 (physics.py:97-100)
+        st.coeffs *= 1.0 + 0.01 * rng.standard_normal(st.coeffs.shape)
+        meshes.append(mesh)
+        coeffs.append(st.coeffs[0])
+        datas.append(ax.sample_state(mesh, ref, st))
+    S = len(spec)
+    off = np.concatenate([[0], np.cumsum([d.N for d in datas])])
+    n = int(off[-1])
+    f = np.zeros((S, n)); dfr = np.zeros((S, n)); dfz = np.zeros((S, n))
+    for a, d in enumerate(datas):
+        f[a, off[a]:off[a + 1]] = d.f[0]
+        dfr[a, off[a]:off[a + 1]] = d.df_r[0]
+        dfz[a, off[a]:off[a + 1]] = d.df_z[0]
+    union = ax.QuadPointData(N=n, r=np.concatenate([d.r for d in datas]),
+                             z=np.concatenate([d.z for d in datas]),
+                             w=np.concatenate([d.w for d in datas]), f=f, df_r=dfr, df_z=dfz)
+    eps_d = min(ax.assembly.default_eps_d(m) for m in meshes)
+    # four 4x4-cell patches per species mesh (cells are z-major: cell = j nr + i)
+    corners = [(3, 10), (20, 60), (40, 100), (58, 120)]
+    patch_cells = np.array(sorted(j * nr + i for (i0, j0) in corners
+                                  for j in range(j0, j0 + 4) for i in range(i0, i0 + 4)))
+    pts_local = (9 * patch_cells[:, None] + np.arange(9)[None, :]).ravel()
+    pts = np.concatenate([off[a] + pts_local for a in range(S)])
+    idx = np.unique(np.concatenate([pts, _closest_owners(union.r, union.z)]))
+    t0 = time.time()
+    K, D = ax.fused_sweep(union.r[idx], union.z[idx], union, params, eps_d=eps_d, workers=1)
+    print(f"cfg4mfull: reference fused_sweep {idx.size} x {n} in {time.time() - t0:.0f} s")
+    pos = {int(p): k for k, p in enumerate(idx)}
+    out = {"S": np.int64(S), "eps_d": np.float64(eps_d), "offsets": off, "idx": idx, "K": K,
+           "D": D, **params_parts(params), "masses": np.array([s.mass for s in sp_]),
+           "patch_cells": patch_cells}
+    for a, (mesh, d) in enumerate(zip(meshes, datas)):
+        sel = np.array([pos[int(off[a] + p)] for p in pts_local])
+        elem = np.zeros((1, mesh.n_cells, 9, 9))
+        elem[:, patch_cells] = O.element_matrices(K[sel, a:a + 1], D[sel, a:a + 1], d.w[pts_local],
+                                                  mesh.sizes[patch_cells], ref.B, ref.dB)
+        blk = O.condense(elem, mesh.cell_nodes, mesh.n_nodes, mesh.prolongation)[0]
+        # nodes interior to a patch: on no cell outside the patch
+        outside = np.setdiff1d(np.arange(mesh.n_cells), patch_cells)
+        inner_nodes = np.setdiff1d(np.unique(mesh.cell_nodes[patch_cells]),
+                                   np.unique(mesh.cell_nodes[outside]))
+        free_pos = {int(v): k for k, v in enumerate(mesh.free_nodes)}
+        rows = np.array(sorted(free_pos[int(v)] for v in inner_nodes if int(v) in free_pos))
+        assert rows.size == 4 * 49, rows.size
+        for k, v in mesh_parts(mesh, ref).items():
+            # the meshes differ only in scale: the topology (cell_nodes,
+            # prolongation) and reference tables are stored once, with s0
+            if a and (k.startswith("mesh_P") or k in ("mesh_cell_nodes", "ref_B", "ref_dB",
+                                                      "ref_qpts", "ref_qwts")):
+                assert np.array_equal(v, out[f"s0_{k}"])
+                continue
+            out[f"s{a}_{k}"] = v
+        out[f"s{a}_coeffs"] = coeffs[a]
+        out[f"s{a}_rows"] = rows
+        out[f"s{a}_r_idx"] = d.r[pts_local]
+        out[f"s{a}_w_idx"] = d.w[pts_local]
+        out.update(csr_parts(f"s{a}_R", blk[rows]))
+    save("cfg4mfull", **out)
+
+
+def case_cfg3_q3():
+    """BASELINE config 3 as worded, D/K parity: the 4x4
+    Gauss points of Q3 elements on the config-3 refined mesh (8x16 base, 3
+    refinement rounds toward the origin and the thermal shell: 950 cells,
+    N = 15,200 points) with the config-3 state evaluated analytically there
+    (synthetic.q3_points / cfg3_state_values, pinned here against the
+    reference's element_geometry operation order and maxwellian_values).
+    The reference's point-set-agnostic fused_sweep (workers=1) gives D/K of
+    2048 evenly spaced points + the 64 closest-pair owners against all N.
+    The Q3 Jacobian has no reference ("parity unpinned")."""
+    mesh, ref, sp_, state = _cfg3_setup()
+    r, z, w = synthetic.q3_points(mesh.origins, mesh.sizes)
+    f, dfr, dfz, nu, mro = synthetic.cfg3_state_values(r, z)
+    params = ax.collision_params(sp_)
+    assert np.array_equal(params.nu_hat, nu) and np.array_equal(params.mass_ratio_o, mro)
+    assert np.array_equal(f[1], ax.physics.maxwellian_values(sp_[1], r, z))
+    # the geometry restatement reproduces the reference's own Q2 points bitwise
+    r2, z2, w2 = synthetic.gauss_points(mesh.origins, mesh.sizes, ref.qpts, ref.qwts)
+    g2 = ax.fem.element_geometry(mesh, ref)
+    assert np.array_equal(r2, g2.coords[:, :, 0].ravel()) and np.array_equal(w2, g2.weights.ravel())
+    data = ax.QuadPointData(N=r.size, r=r, z=z, w=w, f=f, df_r=dfr, df_z=dfz)
+    eps_d = ax.assembly.default_eps_d(mesh)
+    idx = np.unique(np.concatenate([np.linspace(0, r.size - 1, 2048).astype(np.int64),
+                                    _closest_owners(r, z)]))
+    K, D = ax.fused_sweep(r[idx], z[idx], data, params, eps_d=eps_d, workers=1)
+    save("cfg3q3", origins=mesh.origins, sizes=mesh.sizes, eps_d=np.float64(eps_d), idx=idx,
+         K=K, D=D, r_idx=r[idx], z_idx=z[idx], w_idx=w[idx], **params_parts(params))
+
+
 def case_cfg5(N, n_sub=None):
     """BASELINE config 5 recipe (paper_1702_08880_b200/synthetic.py).  Full
     N^2 when n_sub is None, else n_sub evenly spaced outer points plus the 64
@@ -534,6 +725,7 @@ def main():
              "hanging": case_hanging, "cons": case_cons, "cfg2": case_cfg2,
              "cfg3": case_cfg3, "cfg1adv": case_cfg1_advance, "cfg3adv": case_cfg3_advance, "cfg4s": case_cfg4_species, "cfg2m": case_cfg2_meshes,
              "cfg4m": case_cfg4_meshes, "cfg2be": case_cfg2_meshes_be,
+             "cfg4full": case_cfg4_full, "cfg3q3": case_cfg3_q3, "cfg4mfull": case_cfg4_meshes_full,
              "cfg5_4096": lambda: case_cfg5(4096),
              "cfg5_65536": lambda: case_cfg5(65536, n_sub=192)}
     for name, fn in cases.items():

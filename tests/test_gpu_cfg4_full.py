@@ -1,0 +1,114 @@
+"""BASELINE config 4 at its stated size, pinned to the reference.
+
+* Shared mesh (reference-native): cartesian_mesh(L=5, 64, 128), N = 73,728
+  quadrature points, S = 4 (e, D, C6+, W10+, non-neutral densities).  The
+  fixture holds the reference's FULL assemble_collision run
+  (tests/golden/make_golden.py case_cfg4_full): D/K at 128 whole cells + the
+  64 closest-pair owners, those cells' element matrices and 256 rows of
+  every species block.  The device path runs the state-level operator
+  (`assemble_at`: device sampling, symmetric species-collapsed sweep,
+  element contraction, CSR scatter) on the reference's mesh and state.
+* Per-species meshes (config 4 as worded): each species on its own 64x128
+  mesh over 5 sigma_a, 294,912 union points (8.7e10 ordered pairs); the
+  composed reference oracle on 4x4-cell patches gives D/K
+  of the patch points + the union's 64 closest-pair owners against all union
+  points, and the operator rows of the nodes interior to each patch.
+
+Bar (BASELINE north_star): 1e-10 per species/component scaled; mass
+conserved at full size.
+"""
+
+import numpy as np
+import pytest
+
+from conftest import csr_from, golden, mesh_from, params_from, ref_from, worst_component
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-10
+
+
+class _Species:
+    """Fixture view of species a's mesh with the shared topology from s0."""
+
+    SHARED = ("mesh_cell_nodes", "mesh_P_data", "mesh_P_indices", "mesh_P_indptr",
+              "mesh_P_shape", "ref_B", "ref_dB", "ref_qpts", "ref_qwts")
+
+    def __init__(self, g, a):
+        self.g, self.a = g, a
+
+    def __getitem__(self, k):
+        key = f"s{self.a}_{k}"
+        if key not in self.g and k in self.SHARED:
+            key = f"s0_{k}"
+        return self.g[key]
+
+    def __contains__(self, k):
+        return f"s{self.a}_{k}" in self.g or (k in self.SHARED and f"s0_{k}" in self.g)
+
+
+def test_cfg4_shared_mesh_full_size(gpu):
+    g = golden("cfg4full")
+    mesh, ref, params = mesh_from(g), ref_from(g), params_from(g)
+    eps = float(g["eps_d"])
+    assert mesh.n_cells == 64 * 128 and np.asarray(g["coeffs"]).shape[0] == 4
+    cm, data = gpu.assemble_at(mesh, ref, g["coeffs"], params, eps_d=eps, return_data=True)
+    idx = g["idx"]
+    # device sampling reproduces the reference's point set bitwise
+    assert data.N == 73728
+    assert np.array_equal(data.r[idx], g["r_idx"]) and np.array_equal(data.z[idx], g["z_idx"])
+    assert np.array_equal(data.w[idx], g["w_idx"])
+    # D/K: the all-points (symmetric, species-collapsed) call, subset rows
+    K, D = gpu.fused_sweep(data.r, data.z, data, params, eps_d=eps)
+    err_kd = worst_component(K[idx], D[idx], g["K"], g["D"])
+    # element matrices of the stored cells (same sweep inside: bitwise K/D)
+    elem, _, K2, D2 = gpu.element_matrices(mesh, ref, data, params, eps_d=eps, return_kd=True)
+    assert np.array_equal(K2, K) and np.array_equal(D2, D)
+    e, er = elem[:, g["cells"]], g["elem"]
+    err_el = max(np.abs(e[a] - er[a]).max() / np.abs(er[a]).max() for a in range(4))
+    # Jacobian rows against the reference's assembled blocks
+    err_c = 0.0
+    for a in range(4):
+        got = cm.blocks[a][g["rows"]].toarray()
+        want = csr_from(g, f"R{a}").toarray()
+        err_c = max(err_c, np.abs(got - want).max() / float(g["C_max"][a]))
+        assert np.abs(cm.blocks[a].data).max() == pytest.approx(float(g["C_max"][a]), rel=1e-10)
+    print(f"cfg4 shared 64x128 (N=73728, S=4): D/K {err_kd:.2e}, elements {err_el:.2e}, "
+          f"jacobian rows {err_c:.2e}")
+    assert err_kd < TOL and err_el < TOL and err_c < TOL
+    # mass conservation of every species' operator at full size (test_assembly.py:64-76)
+    rate = cm.apply(g["coeffs"])
+    scale = max(np.abs(rate[a]).max() for a in range(4))
+    for a in range(4):
+        assert abs(rate[a].sum()) <= 1e-11 * max(scale, 1.0)
+
+
+def test_cfg4_species_meshes_full_size(gpu):
+    g = golden("cfg4mfull")
+    S = int(g["S"])
+    views = [_Species(g, a) for a in range(S)]
+    meshes = [mesh_from(v) for v in views]
+    ref = ref_from(views[0])
+    params = params_from(g)
+    eps = float(g["eps_d"])
+    cells = g["patch_cells"]
+    pts = (9 * cells[:, None] + np.arange(9)[None, :]).ravel()
+    # device sampling per species mesh
+    datas = [gpu.sample_state(m, ref, g[f"s{a}_coeffs"][None, :]) for a, m in enumerate(meshes)]
+    for a, d in enumerate(datas):
+        assert d.N == 73728
+        assert np.array_equal(d.r[pts], g[f"s{a}_r_idx"]) and np.array_equal(d.w[pts], g[f"s{a}_w_idx"])
+    blocks, (K, D) = gpu.assemble_species_meshes(meshes, ref, datas, params, eps_d=eps)
+    assert K.shape[0] == 4 * 73728
+    err_kd = worst_component(K[g["idx"]], D[g["idx"]], g["K"], g["D"])
+    err_c = 0.0
+    for a in range(S):
+        got = blocks[a][g[f"s{a}_rows"]].toarray()
+        want = csr_from(g, f"s{a}_R").toarray()
+        err_c = max(err_c, np.abs(got - want).max() / np.abs(want).max())
+    print(f"cfg4 per-species meshes (294,912 union points): D/K {err_kd:.2e}, "
+          f"jacobian rows {err_c:.2e}")
+    assert err_kd < TOL and err_c < TOL
+    for a in range(S):
+        rate = blocks[a] @ g[f"s{a}_coeffs"]
+        assert abs(rate.sum()) <= 1e-11 * max(np.abs(rate).max(), 1.0)

@@ -83,43 +83,51 @@ def test_symmetric_dev_path_matches_general(gpu, oracle):
     assert np.array_equal(Kh, Ks) and np.array_equal(Dh, Ds)
 
 
-@pytest.mark.parametrize("world", [2, 3, 8])
-def test_symmetric_rank_partials_sum_to_single(gpu, world):
-    """Emulate `world` ranks on one GPU one after another: each rank's partial
-    sums (its share of tile pairs) added on the host reproduce the
-    single-rank totals (the all-reduce the multi-GPU path performs)."""
+@pytest.mark.parametrize("world", [2, 3, 5, 8])
+def test_symmetric_ranks_bitwise_equal_single(gpu, world):
+    """Emulate `world` ranks on one GPU one after another: each rank's row
+    groups (lb_sym_groups) -> its group sums; the eight group sums combined in
+    group order reproduce the single-rank K and D BITWISE, as the reference
+    promises for `workers` (kernel.py:508-511, test_kernel.py:197-212)."""
+    import ctypes
+
     torch, pkg, wl, params, data = _setup(4096 + 77)
     from paper_1702_08880_b200 import _lib
-    from paper_1702_08880_b200.shard import ShardedSweep, local_fields
+    from paper_1702_08880_b200.shard import SYM_GROUPS, ShardedSweep, local_fields, sym_rank_groups
 
     dev = torch.device("cuda", 0)
     f = [torch.from_numpy(a).to(dev) for a in local_fields(wl, 0, wl.N)]
     sh = ShardedSweep(wl.N, wl.S, params, wl.eps_d, dev, align=1)
-    sh.pack_local(*f)
-    sh.all_gather()
-    sh.sym_prepare()
-    sh.sym_partial()
-    full = sh.tot.clone()
-    acc = torch.zeros_like(full)
-    lib, ctx = _lib.load(), _lib.context(0)
+    K0, D0 = (t.cpu().numpy() for t in sh.step(*f))
+    lib, h = _lib.load(), sh._ctx.handle
     st = torch.cuda.current_stream().cuda_stream
-    part = torch.empty_like(full)
+    groups = torch.full((SYM_GROUPS,) + tuple(sh.tot.shape[1:]), float("nan"), dtype=torch.float64,
+                        device=dev)
     for r in range(world):
-        _lib.check(lib.lb_sym_partial_dev(ctx.handle, wl.S, wl.eps_d, r, world, part.data_ptr(), st))
-        acc += part
+        g0, g1 = sym_rank_groups(r, world)
+        a, b = ctypes.c_int(-1), ctypes.c_int(-1)
+        assert lib.lb_sym_groups(r, world, ctypes.byref(a), ctypes.byref(b)) == SYM_GROUPS
+        assert (a.value, b.value) == (g0, g1)
+        part = torch.full((max(g1 - g0, 1),) + tuple(sh.tot.shape[1:]), float("nan"),
+                          dtype=torch.float64, device=dev)
+        _lib.check(lib.lb_sym_partial_dev(h, wl.S, wl.eps_d, r, world, part.data_ptr(), st))
+        groups[g0:g1] = part[:g1 - g0]
+    K = torch.empty_like(sh.K)
+    D = torch.empty_like(sh.D)
+    p = _lib.dptr
+    _lib.check(lib.lb_sym_combine_dev(h, wl.S, groups.data_ptr(), p(sh.coK), p(sh.coD), 0, wl.N,
+                                      K.data_ptr(), D.data_ptr(), st))
     torch.cuda.synchronize()
-    scale = full.abs().max(dim=1).values.clamp_min(1e-300)
-    err = ((acc - full).abs().max(dim=1).values / scale).max().item()
-    print(f"world={world} rank-sum vs single", err)
-    assert err < 1e-13
+    assert np.array_equal(K.cpu().numpy(), K0) and np.array_equal(D.cpu().numpy(), D0)
 
 
 @pytest.mark.parametrize("world", [2, 3])
 def test_multirank_bench_functional(gpu, world):
     """The multi-GPU bench path end to end with `world` ranks over gloo on
     one GPU (ranks time-share the device; no kernel waits on another rank):
-    all-gather of packed records, symmetric tile-pair split, all-reduce of
-    partial sums, per-rank combine -- every rank's rows vs the oracle."""
+    all-gather of packed records, symmetric row-group split, all-gather of
+    the group sums, per-rank combine -- every rank's rows vs the oracle, and
+    bitwise equal to the single-GPU all-points call."""
     import json
     import socket
     import subprocess
@@ -140,14 +148,15 @@ def test_multirank_bench_functional(gpu, world):
     assert line["n_gpus"] == world
     print("multi-rank", world, "check", line["check_all_ranks_scaled_err_vs_oracle"])
     assert line["check_all_ranks_scaled_err_vs_oracle"] < 1e-10
+    assert line["check_all_ranks_bitwise_equal_single"] is True
 
 
 @pytest.mark.parametrize("world", [2, 3])
 def test_multirank_bench_p2p(gpu, world):
-    """The peer-memory reduction (CUDA IPC mappings of every rank's partial
+    """The peer-memory reduction (CUDA IPC mappings of every rank's group
     sums, read by one fused reduce + combine kernel) with `world` ranks over
     gloo on one GPU (ordering by host barriers; no kernel waits on another
-    rank): every rank's rows vs the oracle."""
+    rank): every rank's rows vs the oracle and bitwise equal to one GPU."""
     import json
     import socket
     import subprocess
@@ -168,13 +177,15 @@ def test_multirank_bench_p2p(gpu, world):
     assert "peer-memory" in line["config"]["parallelism"]
     print("p2p multi-rank", world, "check", line["check_all_ranks_scaled_err_vs_oracle"])
     assert line["check_all_ranks_scaled_err_vs_oracle"] < 1e-10
+    assert line["check_all_ranks_bitwise_equal_single"] is True
 
 
 @pytest.mark.parametrize("world,case", [(1, "cfg3"), (2, "cfg3"), (3, "hanging"), (2, "cfg2")])
 def test_sharded_operator(gpu, tmp_path, world, case):
     """Multi-GPU state-level operator (cells sharded, device sampling,
-    all-gather, symmetric sweep split, per-rank element contraction, CSR
-    all-reduce), `world` ranks over gloo on one GPU, vs the reference blocks."""
+    all-gather, symmetric row-group split, all-gather of (w, K, D), element
+    contraction + CSR gather), `world` ranks over gloo on one GPU, vs the
+    reference blocks -- and bitwise equal to the single-GPU operator."""
     import socket
     import subprocess
     import sys
@@ -197,6 +208,7 @@ def test_sharded_operator(gpu, tmp_path, world, case):
         worst = max(worst, np.abs(d[f"b{a}"] - r).max() / np.abs(r).max())
     print(f"sharded operator {case} world={world}", worst)
     assert worst < 1e-10
+    assert bool(d["bitwise_single"])
 
 
 def test_bench_json_contract(gpu):

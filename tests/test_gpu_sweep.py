@@ -113,6 +113,26 @@ def test_mesh_sweeps(gpu, case):
     assert err < TOL
 
 
+def test_cfg3_q3_point_set(gpu):
+    """BASELINE config 3 as worded: Q3 elements / 4x4 Gauss points on the
+    refined mesh (950 cells, N = 15,200, two species, bi-Maxwellian
+    electrons).  The all-points device call on the committed point set vs
+    the reference's fused_sweep (2048 points + the 64 closest-pair owners).
+    The Q3 element contraction has no reference (parity unpinned, not built)."""
+    from paper_1702_08880_b200 import QuadPointData, synthetic
+
+    g = golden("cfg3q3")
+    r, z, w = synthetic.q3_points(g["origins"], g["sizes"])
+    idx = g["idx"]
+    assert np.array_equal(r[idx], g["r_idx"]) and np.array_equal(w[idx], g["w_idx"])
+    f, dfr, dfz, nu, mro = synthetic.cfg3_state_values(r, z)
+    data = QuadPointData(N=r.size, r=r, z=z, w=w, f=f, df_r=dfr, df_z=dfz)
+    K, D = gpu.fused_sweep(r, z, data, params_from(g), eps_d=float(g["eps_d"]))
+    err = worst_component(K[idx], D[idx], g["K"], g["D"])
+    print("cfg3 Q3 / 4x4 point set (N=%d)" % r.size, err)
+    assert err < TOL
+
+
 def test_four_species(gpu):
     g = golden("cfg4s")
     idx = g["idx"]
@@ -145,15 +165,21 @@ def test_cfg5_4096_full(gpu):
 
 
 def test_cfg5_headline_subset_with_closest_pairs(gpu):
-    """N = 2^16: evenly spaced outer points + the 64 closest-pair owners."""
+    """N = 2^16, the benchmarked configuration: the all-points call (the
+    symmetric, species-collapsed path bench.py times) indexed at 192 evenly
+    spaced points + the 64 closest-pair owners, against the reference's
+    fused_sweep rows; the general (ordered-pair) path on the same outer
+    subset as well."""
     g = golden("cfg5_65536")
     wl, data, params = _cfg5(65536)
     assert wl.checksum() == float(g["checksum"])
     idx = g["idx"]
-    K, D = gpu.fused_sweep(wl.r[idx], wl.z[idx], data, params, eps_d=wl.eps_d)
-    err = worst_component(K, D, g["K"], g["D"])
-    print("cfg5 N=65536 subset", err)
-    assert err < TOL
+    K, D = gpu.fused_sweep(wl.r, wl.z, data, params, eps_d=wl.eps_d)
+    err = worst_component(K[idx], D[idx], g["K"], g["D"])
+    Kg, Dg = gpu.fused_sweep(wl.r[idx], wl.z[idx], data, params, eps_d=wl.eps_d)
+    err_g = worst_component(Kg, Dg, g["K"], g["D"])
+    print("cfg5 N=65536 subset: symmetric (benchmarked) path", err, "general path", err_g)
+    assert err < TOL and err_g < TOL
 
 
 def test_cfg5_headline_full_properties(gpu):

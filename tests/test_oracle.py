@@ -199,3 +199,87 @@ def _union_fields(g):
         dfr[a, off[a]:off[a + 1]] = g[f"s{a}_df_r"][0]
         dfz[a, off[a]:off[a + 1]] = g[f"s{a}_df_z"][0]
     return r, z, w, f, dfr, dfz
+
+
+def _sample(oracle, g, coeffs):
+    from conftest import csr_from
+
+    return oracle.sample_state(g["mesh_origins"], g["mesh_sizes"], g["mesh_cell_nodes"],
+                               csr_from(g, "mesh_P"), g["ref_qpts"], g["ref_qwts"], g["ref_B"],
+                               g["ref_dB"], coeffs)
+
+
+def test_cfg4_full_size_subset(oracle):
+    """BASELINE config 4 at its stated size (shared 64x128 mesh, N = 73,728,
+    S = 4): the oracle's sampling + sweep reproduce the reference's full
+    assemble_collision run at the stored points, and the element
+    restatement its stored cells."""
+    g = golden("cfg4full")
+    r, z, w, f, dfr, dfz = _sample(oracle, g, g["coeffs"])
+    idx = g["idx"]
+    assert r.size == 73728
+    assert np.array_equal(r[idx], g["r_idx"]) and np.array_equal(w[idx], g["w_idx"])
+    K, D = oracle.fused_sweep(r[idx], z[idx], r, z, w, f, dfr, dfz, g["nu_hat"],
+                              g["mass_ratio_o"], eps_d=float(g["eps_d"]))
+    assert worst_component(K, D, g["K"], g["D"]) < 1e-11
+    cells = g["cells"]
+    pts = (9 * cells[:, None] + np.arange(9)[None, :]).ravel()
+    pos = np.searchsorted(idx, pts)
+    elem = oracle.element_matrices(K[pos], D[pos], w[pts], g["mesh_sizes"][cells], g["ref_B"],
+                                   g["ref_dB"])
+    for a in range(4):
+        assert np.abs(elem[a] - g["elem"][a]).max() <= 1e-11 * np.abs(g["elem"][a]).max()
+
+
+def test_cfg4_species_meshes_full_size_subset(oracle):
+    """Config 4 as worded at its stated size (294,912 union points): the
+    oracle's per-mesh sampling + union sweep reproduce the composed reference
+    oracle's D/K at the patch points and the closest-pair owners."""
+    g = golden("cfg4mfull")
+    S = int(g["S"])
+    shared = ("mesh_cell_nodes", "mesh_P_data", "mesh_P_indices", "mesh_P_indptr",
+              "mesh_P_shape", "ref_B", "ref_dB", "ref_qpts", "ref_qwts")
+
+    class V:
+        def __init__(self, a):
+            self.a = a
+
+        def __getitem__(self, k):
+            key = f"s{self.a}_{k}"
+            return g[key] if key in g else g[f"s0_{k}"] if k in shared else g[key]
+
+    parts = [_sample(oracle, V(a), g[f"s{a}_coeffs"]) for a in range(S)]
+    off = g["offsets"]
+    n = int(off[-1])
+    r = np.concatenate([p[0] for p in parts])
+    z = np.concatenate([p[1] for p in parts])
+    w = np.concatenate([p[2] for p in parts])
+    f, dfr, dfz = np.zeros((S, n)), np.zeros((S, n)), np.zeros((S, n))
+    for a, p in enumerate(parts):
+        f[a, off[a]:off[a + 1]], dfr[a, off[a]:off[a + 1]], dfz[a, off[a]:off[a + 1]] = p[3][0], p[4][0], p[5][0]
+    idx = g["idx"]
+    K, D = oracle.fused_sweep(r[idx], z[idx], r, z, w, f, dfr, dfz, g["nu_hat"], g["mass_ratio_o"],
+                              eps_d=float(g["eps_d"]))
+    # 2.1e-11 worst: D_rr of one closest-pair owner on the tungsten mesh
+    # (sigma_W = 1.7e-3: Gauss points ~1e-5 apart, the UD_xx cancellation of
+    # ~r^2/d^2 terms); every other component <= 3e-13.  Bar: north_star's 1e-10
+    assert worst_component(K, D, g["K"], g["D"]) < 1e-10
+
+
+def test_cfg3_q3_point_set(oracle):
+    """Config 3 as worded (Q3 / 4x4 Gauss point set of the refined mesh):
+    the committed point-set generator + analytic state, swept by the oracle,
+    reproduce the reference's fused_sweep on that point set."""
+    from paper_1702_08880_b200 import synthetic
+
+    g = golden("cfg3q3")
+    r, z, w = synthetic.q3_points(g["origins"], g["sizes"])
+    idx = g["idx"]
+    assert r.size == 16 * g["sizes"].shape[0]
+    assert np.array_equal(r[idx], g["r_idx"]) and np.array_equal(z[idx], g["z_idx"])
+    assert np.array_equal(w[idx], g["w_idx"])
+    f, dfr, dfz, nu, mro = synthetic.cfg3_state_values(r, z)
+    assert np.array_equal(nu, g["nu_hat"]) and np.array_equal(mro, g["mass_ratio_o"])
+    K, D = oracle.fused_sweep(r[idx], z[idx], r, z, w, f, dfr, dfz, nu, mro,
+                              eps_d=float(g["eps_d"]))
+    assert worst_component(K, D, g["K"], g["D"]) < TOL_SWEEP

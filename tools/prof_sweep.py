@@ -28,6 +28,7 @@ def main():
     params = pkg.CollisionParams(nu_hat=wl.nu_hat, mass_ratio_o=wl.mass_ratio_o)
     sym = "--general" not in sys.argv
     world = int(next((a.split("=")[1] for a in sys.argv if a.startswith("--world=")), 1))
+    rank = int(next((a.split("=")[1] for a in sys.argv if a.startswith("--rank=")), 0))
     sh = ShardedSweep(n, wl.S, params, wl.eps_d, dev, align=1, symmetric=sym)
     f = [torch.from_numpy(a).to(dev) for a in local_fields(wl, 0, n)]
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -37,9 +38,9 @@ def main():
         if sh.symmetric:
             sh.sym_prepare()
             e0.record()
-            if world > 1:  # rank 0's share of a `world`-GPU split (per-rank kernel time)
+            if world > 1:  # one rank's row groups of a `world`-GPU split (per-rank kernel time)
                 _lib.check(_lib.load().lb_sym_partial_dev(
-                    _lib.context(0).handle, wl.S, wl.eps_d, 0, world, sh.tot.data_ptr(),
+                    sh._ctx.handle, wl.S, wl.eps_d, rank, world, sh.tot.data_ptr(),
                     torch.cuda.current_stream().cuda_stream))
             else:
                 sh.sym_partial()
@@ -52,7 +53,7 @@ def main():
         torch.cuda.synchronize()
         ms = e0.elapsed_time(e1)
         if world > 1:
-            print(f"rep {k}: rank 0 of {world}: {ms:.3f} ms (x{world} = {ms * world:.2f} ms single-GPU equiv.)")
+            print(f"rep {k}: rank {rank} of {world}: {ms:.3f} ms (x{world} = {ms * world:.2f} ms single-GPU equiv.)")
             continue
         print(f"rep {k}: sweep {ms:.3f} ms, {n * n / ms / 1e6:.3e} Gpairs/s... "
               f"model {pkg.flop_count(n, wl.S, n) / ms / 1e9:.2f} TFLOP/s, S={wl.S}, "

@@ -35,8 +35,16 @@ def main():
     blocks = op.step(g["coeffs"])
     blocks = op.step(g["coeffs"])  # second evaluation reuses every buffer
     if not dist.is_initialized() or dist.get_rank() == 0:
+        # the single-GPU state-level operator (assemble_at = lb_assemble_state)
+        # on this rank's device: the sharded blocks must equal it bitwise
+        from paper_1702_08880_b200.assembly import assemble_at
+
+        single = assemble_at(mesh_from(g), ref_from(g), g["coeffs"], params_from(g)).blocks
+        same = all(np.array_equal(a.data, b.data) and np.array_equal(a.indices, b.indices)
+                   for a, b in zip(blocks, single))
         np.savez(out, **{f"b{a}": b.toarray() for a, b in enumerate(blocks)},
-                 world=dist.get_world_size() if dist.is_initialized() else 1)
+                 world=dist.get_world_size() if dist.is_initialized() else 1,
+                 bitwise_single=same)
     if dist.is_initialized():
         dist.destroy_process_group()
 
