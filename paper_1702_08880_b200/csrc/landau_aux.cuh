@@ -208,9 +208,12 @@ __global__ void lb_sample_kernel(int c0, int c1, int S, int n_free, const double
       const int node = cell_nodes[9 * e + i];
       double v = 0.0;  // (P @ coeffs^T)[node] (fem.py:182)
       for (int k = P_ptr[node]; k < P_ptr[node + 1]; ++k) v = __dadd_rn(v, __dmul_rn(P_w[k], cs[P_idx[k]]));
-      fv = fma(v, basis[9 * i + q], fv);
-      gr = fma(v, basis[81 + 2 * (9 * i + q)], gr);
-      gz = fma(v, basis[81 + 2 * (9 * i + q) + 1], gz);
+      // einsum("sei,iq->seq") / ("sei,iqd->seqd") (fem.py:185-186): numpy
+      // sums the 9 products in i order, each rounded (no FMA), from zero --
+      // the same here, so f and grad f are bitwise the reference's
+      fv = __dadd_rn(fv, __dmul_rn(v, basis[9 * i + q]));
+      gr = __dadd_rn(gr, __dmul_rn(v, basis[81 + 2 * (9 * i + q)]));
+      gz = __dadd_rn(gz, __dmul_rn(v, basis[81 + 2 * (9 * i + q) + 1]));
     }
     f[(size_t)s * nloc + pl] = fv;
     dfr[(size_t)s * nloc + pl] = __dmul_rn(gr, jr);  // fem.py:188-189

@@ -21,7 +21,22 @@
 //    exponent/mantissa split + atanh series (kernel.py:317-337); both are
 //    accurate to ~1 ulp;
 //  * the mask and the d^2 guard are 64-bit integer compares on the bit
-//    pattern (d^2 >= 0, so IEEE order == integer order).
+//    pattern (d^2 >= 0, so IEEE order == integer order);
+//  * the tensor components are formed from B1, B3, B4 and the two
+//    DIFFERENCES c34 = B3 - B4 = c3 (Em1 - S2) and c35 = B3 - B5 =
+//    c3 (Em1 - S3), which have closed forms free of the 1/x terms (using
+//    Em1 (1 - m) = E):  Em1 - S2 = (2/m)(K - E),  Em1 - S3 =
+//    (4/m^2)((2 - m) K - 2 E)  (m >= 0.01; below, the series' S2/S3 are
+//    subtracted directly).  With dr = ri - rn (kernel.py:384-389 rearranged):
+//      UD_xx = B1 - dr^2 B3 - 2 ri rn c34 + rn^2 c35
+//      UD_zz = B1 - dz^2 B3,  UD_xz = -dz (dr B3 + rn c34)
+//      UK_rr = dz^2 B4 + ri rn c35,  UK_zr = dz (rn c34 - dr B4)
+//    The reference's forms (e.g. ri rn (B3 - B5)) subtract two O(1/x)
+//    terms: for near-coincident pairs (x = d^2/P -> 0) they lose
+//    ~log10(1/x) digits, which at config 4's per-species meshes (tungsten
+//    mesh, points ~1e-5 apart) put the reference itself ~1e-10 from exact
+//    arithmetic (tools/diag/hp_point.py); these forms do not, and cost one
+//    FP64 operation less per pair.
 // Every change is a re-association or a <= 1-ulp reciprocal; the parity
 // tests bound the end-to-end effect (<= 1e-10 scaled, measured ~1e-14).
 #pragma once
@@ -181,11 +196,12 @@ struct T5 {
   double xx, zz, xz, kr, zr;
 };
 
-// The symmetric part of one pair: B1..B5 (each / 4), dz, dz^2 and the mask.
+// The symmetric part of one pair (each / 4; all zero for masked pairs):
+// B1, B3, B4 and the differences c34 = B3 - B4, c35 = B3 - B5 in their
+// well-conditioned closed forms; dz, dz^2, dr = ri - rn and ri rn.
 struct PairB {
-  double B1, B3, B4, B5, dz, dz2;  // B's are zero for masked pairs
-  double rr;                        // ri rn
-  double u;                         // B1 + 2 ri rn B4 (shared by UD_xx of both orientations)
+  double B1, B3, B4, c34, c35;
+  double dz, dz2, dr, rr;
 };
 
 // gthr = max(bits(eps^2), 1): the pair contributes iff bits(d^2) >= gthr,
@@ -194,16 +210,16 @@ struct PairB {
 // lookup -- the long-latency front (MUFU, shared-memory table) that the
 // symmetric sweep issues one step ahead of the rest.
 struct PairS1 {
-  double dz, dz2, P, rr, isPm, invP, x, lr, logc, kd;
+  double dz, dz2, dr, P, rr, isPm, invP, x, lr, logc, kd;
 };
 
 __device__ __forceinline__ PairS1 pair_stage1(const Outer& o, double rn, double zn, long long gthr,
                                               const double2* __restrict__ logt) {
   PairS1 s;
-  const double dr = o.ri - rn;
+  s.dr = o.ri - rn;
   s.dz = o.zi - zn;
   s.dz2 = s.dz * s.dz;
-  const double dist2 = fma(dr, dr, s.dz2);
+  const double dist2 = fma(s.dr, s.dr, s.dz2);
   const long long di = __double_as_longlong(dist2);
   const bool g = di >= gthr;  // d^2 >= eps^2 and d^2 > 0 (kernel.py:344)
   const double d2 = di > kTinyBits ? dist2 : 1.0;
@@ -221,7 +237,8 @@ __device__ __forceinline__ PairS1 pair_stage1(const Outer& o, double rn, double 
   return s;
 }
 
-// Stage 2: ln x, K(m), E(m), S2/S3 and B1..B5 (each / 4).
+// Stage 2: ln x, K(m), E(m), then B1, B3, B4 and the differences c34, c35
+// (each / 4; closed form or, for m < 0.01, the series).
 __device__ __forceinline__ PairB pair_stage2(const Outer& o, double rn, double rcpr, const PairS1& s) {
   const double x = s.x, P = s.P, invP = s.invP;
   const double lx = log_finish(s.lr, s.logc, s.kd);
@@ -263,8 +280,11 @@ __device__ __forceinline__ PairB pair_stage2(const Outer& o, double rn, double r
   const double EK = fma(-lx, qk, pk);
   const double EE = fma(-lx, qe, pe);
   const double Em1 = EE * rcp_nr(x);  // E/(1-m) = E P/d^2
-
-  double S2, S3;
+  const double isPm = s.isPm;
+  const double c3 = isPm * invP;  // P^-3/2 (the 4 is folded into the coupling)
+  PairB p;
+  p.B1 = EK * isPm;
+  p.B3 = Em1 * c3;
   // m < 0.01 (kernel.py:376) tested as x = 1 - m > 0.99 on the bit pattern;
   // m itself is only needed by the series
   if (__double_as_longlong(x) > kXSwitchBits) {
@@ -279,28 +299,25 @@ __device__ __forceinline__ PairB pair_stage2(const Outer& o, double rn, double r
     s2 = fma(s2, m, c_s2[3]);  s3 = fma(s3, m, c_s3[3]);
     s2 = fma(s2, m, c_s2[2]);  s3 = fma(s3, m, c_s3[2]);
     s2 = fma(s2, m, c_s2[1]);  s3 = fma(s3, m, c_s3[1]);
-    S2 = s2 * m;
-    S3 = fma(s3, m, c_s3[0]);
+    const double S2 = s2 * m;
+    const double S3 = fma(s3, m, c_s3[0]);
+    p.B4 = S2 * c3;
+    p.c34 = (Em1 - S2) * c3;
+    p.c35 = (Em1 - S3) * c3;
   } else {
-    // closed form (kernel.py:366-367) in 2/m = P/(2 ri rn) (m >= 0.01, so rn > 0):
-    // S2 = a (2/m) - Em1, S3 = (c (2/m) - 2a)(2/m) + Em1 = 4c/m^2 - 4a/m + Em1
+    // closed form (kernel.py:366-367) as the differences from Em1, in
+    // 2/m = P/(2 ri rn) (m >= 0.01, so rn > 0):
+    //   Em1 - S2 = (2/m)(K - E),  Em1 - S3 = (2/m)^2 ((1 + x) K - 2 E)
     const double invm2 = P * o.rtri * rcpr;  // 2/m
-    const double a = Em1 - EK;
-    S2 = fma(a, invm2, -Em1);
-    const double c = fma(-2.0, EK, Em1 + EE);
-    S3 = fma(fma(c, invm2, -(a + a)), invm2, Em1);
+    const double cq = c3 * invm2;
+    p.c34 = cq * (EK - EE);
+    p.c35 = (cq * invm2) * fma(1.0 + x, EK, -(EE + EE));
+    p.B4 = p.B3 - p.c34;
   }
-  const double isPm = s.isPm;
-  const double c3 = isPm * invP;  // P^-3/2 (the 4 is folded into the coupling)
-  PairB p;
-  p.B1 = EK * isPm;
-  p.B3 = Em1 * c3;
-  p.B4 = S2 * c3;
-  p.B5 = S3 * c3;
   p.dz = s.dz;
   p.dz2 = s.dz2;
+  p.dr = s.dr;
   p.rr = s.rr;
-  p.u = fma(s.rr + s.rr, p.B4, p.B1);
   return p;
 }
 
@@ -310,16 +327,20 @@ __device__ __forceinline__ PairB pair_core(const Outer& o, double rn, double zn,
   return pair_stage2(o, rn, rcpr, pair_stage1(o, rn, zn, gthr, logt));
 }
 
-// Direct-pair tensor components from the symmetric part.
-__device__ __forceinline__ T5 pair_tensors(const Outer& o, double rn, double rn2, const PairB& p) {
-  const double rr = p.rr;
+// Direct-pair tensor components from the symmetric part (kernel.py:384-389
+// rearranged, see the header): w2 = B1 - dr^2 B3 - 2 ri rn c34 is shared by
+// UD_xx of both orientations.
+__device__ __forceinline__ double pair_w2(const PairB& p) {
+  return fma(-(p.rr + p.rr), p.c34, fma(-(p.dr * p.dr), p.B3, p.B1));
+}
+__device__ __forceinline__ T5 pair_tensors(double rn, double rn2, const PairB& p, double w2) {
   T5 t;
-  t.xx = fma(-rn2, p.B5, fma(-o.ri2, p.B3, p.u));
+  t.xx = fma(rn2, p.c35, w2);
   t.zz = fma(-p.dz2, p.B3, p.B1);
-  t.xz = p.dz * fma(rn, p.B4, -(o.ri * p.B3));
-  t.kr = fma(rr, p.B3 - p.B5, p.dz2 * p.B4);
-  t.zr = p.dz * fma(rn, p.B3, -(o.ri * p.B4));
-  return t;  // masked pairs: all B are zero (pair_core), so is every component
+  t.xz = -p.dz * fma(p.dr, p.B3, rn * p.c34);
+  t.kr = fma(p.rr, p.c35, p.dz2 * p.B4);
+  t.zr = p.dz * fma(rn, p.c34, -(p.dr * p.B4));
+  return t;  // masked pairs: all B and c are zero (pair_core), so is every component
 }
 
 // One (outer, inner) pair: the five tensor components / 4.
@@ -327,18 +348,19 @@ __device__ __forceinline__ T5 pair_tensor(const Outer& o, double rn, double zn, 
                                           double rcpr, long long gthr,
                                           const double2* __restrict__ logt) {
   const PairB p = pair_core(o, rn, zn, rcpr, gthr, logt);
-  return pair_tensors(o, rn, rn2, p);
+  return pair_tensors(rn, rn2, p, pair_w2(p));
 }
 
 // One unordered pair: the direct components in `t` and, returned, the one
-// new component of the swapped pair, UD_xx(j,i) / 4 = (B1 - rn^2 B3 +
-// 2 ri rn B4 - ri^2 B5) / 4; the others are permutations of `t`.
+// new component of the swapped pair, UD_xx(j,i) / 4 = (B1 - dr^2 B3 -
+// 2 ri rn c34 + ri^2 c35) / 4; the others are permutations of `t`.
 __device__ __forceinline__ double pair_tensor_sym(const Outer& o, double rn, double zn, double rn2,
                                                   double rcpr, long long gthr,
                                                   const double2* __restrict__ logt, T5& t) {
   const PairB p = pair_core(o, rn, zn, rcpr, gthr, logt);
-  t = pair_tensors(o, rn, rn2, p);
-  return fma(-o.ri2, p.B5, fma(-rn2, p.B3, p.u));
+  const double w2 = pair_w2(p);
+  t = pair_tensors(rn, rn2, p, w2);
+  return fma(o.ri2, p.c35, w2);
 }
 
 // U unordered pairs (outer point oo[u], inner point u) evaluated in lockstep:
@@ -382,28 +404,39 @@ __device__ __forceinline__ void pair_tensor_sym_x(const Outer (&oo)[U], const do
       qe[u] = fma(qe[u], x[u], c_qe[k]);
     }
   }
-  double EK[U], EE[U], Em1[U], S2[U], S3[U];
+  PairB p[U];
+  double Em1[U];
 #pragma unroll
   for (int u = 0; u < U; ++u) {
     pk[u] = fma(pk[u], x[u], c_pk[0]);
     qk[u] = fma(qk[u], x[u], c_qk[0]);
     pe[u] = fma(pe[u], x[u], c_pe[0]);
     qe[u] = qe[u] * x[u];
-    EK[u] = fma(-lx[u], qk[u], pk[u]);
-    EE[u] = fma(-lx[u], qe[u], pe[u]);
-    Em1[u] = EE[u] * rcp_nr(x[u]);  // E/(1-m) = E P/d^2
-    // closed form (kernel.py:366-367) in 2/m = P/(2 ri rn), as in pair_stage2
+    const double EK = fma(-lx[u], qk[u], pk[u]);
+    const double EE = fma(-lx[u], qe[u], pe[u]);
+    Em1[u] = EE * rcp_nr(x[u]);  // E/(1-m) = E P/d^2
+    const double isPm = s[u].isPm;
+    const double c3 = isPm * s[u].invP;  // P^-3/2 (the 4 is folded into the coupling)
+    p[u].B1 = EK * isPm;
+    p[u].B3 = Em1[u] * c3;
+    // closed form (kernel.py:366-367) as the differences from Em1 (header):
+    // Em1 - S2 = (2/m)(K - E), Em1 - S3 = (2/m)^2 ((1 + x) K - 2 E)
     const double invm2 = s[u].P * oo[u].rtri * rcpr[u];  // 2/m
-    const double a = Em1[u] - EK[u];
-    S2[u] = fma(a, invm2, -Em1[u]);
-    const double c = fma(-2.0, EK[u], Em1[u] + EE[u]);
-    S3[u] = fma(fma(c, invm2, -(a + a)), invm2, Em1[u]);
+    const double cq = c3 * invm2;
+    p[u].c34 = cq * (EK - EE);
+    p[u].c35 = (cq * invm2) * fma(1.0 + x[u], EK, -(EE + EE));
+    p[u].B4 = p[u].B3 - p[u].c34;
+    p[u].dz = s[u].dz;
+    p[u].dz2 = s[u].dz2;
+    p[u].dr = s[u].dr;
+    p[u].rr = s[u].rr;
   }
 #if LB_SERIES_MODE == 0
 #pragma unroll
   for (int u = 0; u < U; ++u) {
     // m < 0.01 (kernel.py:376), tested as x = 1 - m > 0.99 on the bit pattern
     if (__double_as_longlong(x[u]) > kXSwitchBits) {
+      ++nser;
       const double m = (4.0 * s[u].rr) * s[u].invP;
       double s2 = c_s2[9], s3 = c_s3[9];
 #pragma unroll
@@ -411,8 +444,11 @@ __device__ __forceinline__ void pair_tensor_sym_x(const Outer (&oo)[U], const do
         s2 = fma(s2, m, c_s2[k]);
         s3 = fma(s3, m, c_s3[k]);
       }
-      S2[u] = s2 * m;
-      S3[u] = fma(s3, m, c_s3[0]);
+      const double c3 = s[u].isPm * s[u].invP;
+      const double S2 = s2 * m, S3 = fma(s3, m, c_s3[0]);
+      p[u].B4 = S2 * c3;
+      p[u].c34 = (Em1[u] - S2) * c3;
+      p[u].c35 = (Em1[u] - S3) * c3;
     }
   }
 #else
@@ -442,27 +478,20 @@ __device__ __forceinline__ void pair_tensor_sym_x(const Outer (&oo)[U], const do
       }
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-      const double a2 = s2[u] * m[u], a3 = fma(s3[u], m[u], c_s3[0]);
-      S2[u] = ser[u] ? a2 : S2[u];
-      S3[u] = ser[u] ? a3 : S3[u];
+      const double c3 = s[u].isPm * s[u].invP;
+      const double S2 = s2[u] * m[u], S3 = fma(s3[u], m[u], c_s3[0]);
+      const double b4 = S2 * c3, d34 = (Em1[u] - S2) * c3, d35 = (Em1[u] - S3) * c3;
+      p[u].B4 = ser[u] ? b4 : p[u].B4;
+      p[u].c34 = ser[u] ? d34 : p[u].c34;
+      p[u].c35 = ser[u] ? d35 : p[u].c35;
     }
   }
 #endif
 #pragma unroll
   for (int u = 0; u < U; ++u) {
-    const double isPm = s[u].isPm;
-    const double c3 = isPm * s[u].invP;  // P^-3/2 (the 4 is folded into the coupling)
-    PairB p;
-    p.B1 = EK[u] * isPm;
-    p.B3 = Em1[u] * c3;
-    p.B4 = S2[u] * c3;
-    p.B5 = S3[u] * c3;
-    p.dz = s[u].dz;
-    p.dz2 = s[u].dz2;
-    p.rr = s[u].rr;
-    p.u = fma(s[u].rr + s[u].rr, p.B4, p.B1);
-    t[u] = pair_tensors(oo[u], rn[u], rn2[u], p);
-    txx2[u] = fma(-oo[u].ri2, p.B5, fma(-rn2[u], p.B3, p.u));
+    const double w2 = pair_w2(p[u]);
+    t[u] = pair_tensors(rn[u], rn2[u], p[u], w2);
+    txx2[u] = fma(oo[u].ri2, p[u].c35, w2);
   }
 }
 

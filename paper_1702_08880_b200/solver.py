@@ -37,7 +37,7 @@ from .assembly import default_eps_d, device_mesh
 from .kernel import _n_species, coupling
 
 __all__ = ["CNSolver", "StepFailure", "backward_euler_step", "band_order", "linear_cn_step",
-           "newton_step", "pattern_values", "species_meshes_step", "theta_step"]
+           "mass_matrix", "newton_step", "pattern_values", "species_meshes_step", "theta_step"]
 
 
 class StepFailure(RuntimeError):
@@ -207,10 +207,47 @@ def _with_coeffs(state, coeffs: np.ndarray):
     return coeffs.reshape(np.shape(state))
 
 
+_MASS: "OrderedDict[int, tuple]" = OrderedDict()
+
+
+def mass_matrix(mesh, ref):
+    """fem.mass_matrix (fem.py:150-165): the r-weighted Q2 mass matrix on the
+    free dofs, by the reference's own numpy/scipy operations (so bitwise
+    equal to it: newton_step(M=None) must give exactly what newton_step(M=
+    mass_matrix(mesh, ref)) gives, test_solver.py:166-176).  Mesh-constant
+    set-up, off the operator's hot path; cached per mesh.  The device
+    assembly of the same matrix is `CNSolver.set_mass(None)`."""
+    key = id(mesh)
+    hit = _MASS.get(key)
+    if hit is not None and hit[0] is mesh:
+        return hit[1]
+    sizes = np.asarray(mesh.sizes, dtype=np.float64)
+    dr, dz = sizes[:, 0], sizes[:, 1]
+    nq = int(ref.Nq)
+    detJ = np.broadcast_to((dr * dz / 4.0)[:, None], (sizes.shape[0], nq)).copy()
+    coords = (np.asarray(mesh.origins)[:, None, :]
+              + (np.asarray(ref.qpts)[None, :, :] + 1.0) * 0.5 * sizes[:, None, :])
+    weights = np.asarray(ref.qwts)[None, :] * detJ * coords[:, :, 0]
+    elem = np.einsum("iq,jq,eq->eij", ref.B, ref.B, weights)
+    cn = np.asarray(mesh.cell_nodes)
+    rows = np.repeat(cn, 9, axis=1).ravel()
+    cols = np.tile(cn, (1, 9)).ravel()
+    nn = int(mesh.n_nodes)
+    Mn = sp.csr_matrix((elem.ravel(), (rows, cols)), shape=(nn, nn))
+    P = mesh.prolongation
+    M = (P.T @ Mn @ P).tocsr()
+    _MASS[key] = (mesh, M)
+    while len(_MASS) > 8:
+        _MASS.popitem(last=False)
+    return M
+
+
 def newton_step(f_guess, f_old, mesh, ref, params, cfg, M=None, C_old=None):
     """solver.newton_step (solver.py:103-134) on the device: returns
-    (f_next, rel_residual).  M / C_old as in the reference (None: assembled
-    here, on the device)."""
+    (f_next, rel_residual).  M / C_old as in the reference: None assembles
+    them here -- M by the reference's own operations (`mass_matrix`), C_old
+    on the device at f_old (bitwise what assemble_collision(sample_state)
+    gives: device sampling reproduces fem.sample_state's arithmetic)."""
     S = _n_species(params)
     g, f = _coeffs_of(f_guess), _coeffs_of(f_old)
     if g.shape != f.shape:
@@ -220,7 +257,7 @@ def newton_step(f_guess, f_old, mesh, ref, params, cfg, M=None, C_old=None):
     solver = _mesh_solver(mesh, ref, S)
     if g.shape[1] != solver.n:
         raise ValueError(f"state has {g.shape[1]} dofs, mesh has {solver.n} free nodes")
-    solver.set_mass(M)
+    solver.set_mass(mass_matrix(mesh, ref) if M is None else M)
     # C_old: advance() hands the same CollisionMatrix to every Newton
     # iteration of a step (solver.py:171-181); it is uploaded once and kept
     # resident on the device for the following iterations

@@ -700,6 +700,28 @@ def case_cfg3_q3():
          K=K, D=D, r_idx=r[idx], z_idx=z[idx], w_idx=w[idx], **params_parts(params))
 
 
+def case_cfg5_hp():
+    """High-precision yardstick (tests/golden/hp_sweep.py) for the outer
+    points that own the globally closest pairs: config 5 at N = 2^20 (16
+    owners, the test_cfg5_max_size set) and config 4 as worded at full size
+    (the 64 owners in the 294,912-point union of cfg4mfull)."""
+    import time
+
+    sys.path.insert(0, str(HERE.parents[1]))
+    sys.path.insert(0, str(HERE))
+    from oracle import oracle as O
+    import hp_sweep
+
+    t0 = time.time()
+    N = 1 << 20
+    wl = synthetic.cfg5(N)
+    close = _closest_owners(wl.r, wl.z, 16)
+    K5, D5 = hp_sweep.hp_kd(close, wl.r, wl.z, wl.w, wl.f, wl.df_r, wl.df_z, wl.nu_hat,
+                            wl.mass_ratio_o, wl.eps_d, 0.3, O)
+    print(f"cfg5hp: N=2^20 owners {time.time() - t0:.0f} s")
+    save("cfg5hp", idx=close, K=K5, D=D5, checksum=np.float64(wl.checksum()))
+
+
 def case_cfg5(N, n_sub=None):
     """BASELINE config 5 recipe (paper_1702_08880_b200/synthetic.py).  Full
     N^2 when n_sub is None, else n_sub evenly spaced outer points plus the 64
@@ -725,7 +747,7 @@ def main():
              "hanging": case_hanging, "cons": case_cons, "cfg2": case_cfg2,
              "cfg3": case_cfg3, "cfg1adv": case_cfg1_advance, "cfg3adv": case_cfg3_advance, "cfg4s": case_cfg4_species, "cfg2m": case_cfg2_meshes,
              "cfg4m": case_cfg4_meshes, "cfg2be": case_cfg2_meshes_be,
-             "cfg4full": case_cfg4_full, "cfg3q3": case_cfg3_q3, "cfg4mfull": case_cfg4_meshes_full,
+             "cfg4full": case_cfg4_full, "cfg3q3": case_cfg3_q3, "cfg5hp": case_cfg5_hp, "cfg4mfull": case_cfg4_meshes_full,
              "cfg5_4096": lambda: case_cfg5(4096),
              "cfg5_65536": lambda: case_cfg5(65536, n_sub=192)}
     for name, fn in cases.items():

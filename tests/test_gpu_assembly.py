@@ -118,16 +118,13 @@ def test_assembly_deterministic(gpu):
 
 @pytest.mark.parametrize("case", ["cfg1", "hanging", "cfg2", "cons", "cfg3"])
 def test_device_sampling_matches_reference(gpu, case):
-    """Device sample_state (fem.py:170-199): r, z, w bitwise the reference's,
-    f and grad f to rounding."""
+    """Device sample_state (fem.py:170-199): r, z, w, f and grad f bitwise
+    the reference's (the kernel reproduces numpy's einsum order: the nine
+    products summed in basis order, each rounded)."""
     g = golden(case)
     qd = gpu.sample_state(mesh_from(g), ref_from(g), g["coeffs"])
-    for k in ("r", "z", "w"):
+    for k in ("r", "z", "w", "f", "df_r", "df_z"):
         assert np.array_equal(getattr(qd, k), g[k]), k
-    for k in ("f", "df_r", "df_z"):
-        ref = g[k]
-        err = np.abs(getattr(qd, k) - ref).max() / np.abs(ref).max()
-        assert err < 1e-14, (k, err)
 
 
 @pytest.mark.parametrize("case", ["cfg1", "hanging", "cfg2"])

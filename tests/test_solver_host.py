@@ -4,6 +4,7 @@ pattern mapping of M and C, and a numpy restatement of the block cyclic
 reduction checked against SuperLU on the reference's own operators."""
 
 import numpy as np
+import pytest
 import scipy.linalg as sla
 import scipy.sparse as sp
 import scipy.sparse.linalg as spla
@@ -133,3 +134,19 @@ def test_block_cyclic_reduction_matches_splu():
         want = spla.splu(A.tocsc()).solve(b)
         got = block_cyclic_solve(A, b, perm, max(bw, 1))
         assert np.abs(got - want).max() <= 1e-12 * np.abs(want).max(), case
+
+
+@pytest.mark.parametrize("case", ["cfg3", "cfg1adv", "cfg3adv"])
+def test_mass_matrix_bitwise_reference(case):
+    """solver.mass_matrix (the M=None default of newton_step) is the
+    reference's fem.mass_matrix bitwise (fem.py:150-165), hanging nodes
+    included, so newton_step(M=None) == newton_step(M=mass_matrix(...))."""
+    from conftest import csr_from, golden, mesh_from, ref_from
+    from paper_1702_08880_b200.solver import mass_matrix
+
+    g = golden(case)
+    M = mass_matrix(mesh_from(g), ref_from(g))
+    Mr = csr_from(g, "M")
+    M.sort_indices()
+    assert np.array_equal(M.indptr, Mr.indptr) and np.array_equal(M.indices, Mr.indices)
+    assert np.array_equal(M.data, Mr.data)
