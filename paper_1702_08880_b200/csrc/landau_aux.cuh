@@ -88,66 +88,76 @@ __global__ void lb_gather_kernel(int n, const int* __restrict__ perm, const doub
 }
 
 // ------------------------------------------------------------------ K2 elements
-// One warp per (species a, cell e).  G2 = K Jinv w, G3 = Jinv D Jinv w
-// (assembly.py:159-160), then
+// One warp per cell, all S species.  The cell's K (9 x S x 2), D (9 x S x 4)
+// and w (9) are contiguous in HBM and read with coalesced loads; then per
+// species G2 = K Jinv w, G3 = Jinv D Jinv w (assembly.py:159-160, same
+// factor grouping) and
 //   elem[a,e,i,j] = sum_q dB[i,q,:].G2[q] B[j,q] + sum_q dB[i,q,:].G3[q].dB[j,q,:]
-// computed as u[i,q] = dB[i,q,:].G2[q], v[i,q,:] = dB[i,q,:].G3[q] followed
-// by a 27-term dot product per entry.
+// as u[i,q] = dB[i,q,:].G2[q], v[i,q,:] = dB[i,q,:].G3[q] followed by a
+// 27-term dot product per entry; each species' 81 entries are one
+// contiguous store.  Per (cell, species): 9 x 48 + 72 B in, 648 B out.
 constexpr int kElemWarps = 4;
+constexpr int kElemMaxS = 8;
 __global__ void __launch_bounds__(32 * kElemWarps) lb_elements_kernel(
     int ncell, int S, const double* __restrict__ sizes, const double* __restrict__ w,
     const double* __restrict__ K, const double* __restrict__ D, const double* __restrict__ Bt,
     const double* __restrict__ dBt, double* __restrict__ elem, int ncell_out, int c_out) {
   // cells e of this launch land at cell c_out + e of an (S, ncell_out, 81) buffer
   __shared__ double sB[81], sdB[162];
-  __shared__ double sG[kElemWarps][9][6];  // G2 r,z ; G3 rr, rz, zr, zz
+  __shared__ double sKD[kElemWarps][9 * kElemMaxS * 6 + 9];  // K (9 S 2), D (9 S 4), w (9)
   __shared__ double su[kElemWarps][81], sv[kElemWarps][162];
+  __shared__ double sG[kElemWarps][9][6];  // G2 r,z ; G3 rr, rz, zr, zz
   for (int t = threadIdx.x; t < 81; t += blockDim.x) sB[t] = Bt[t];
   for (int t = threadIdx.x; t < 162; t += blockDim.x) sdB[t] = dBt[t];
   __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const long long nwork = (long long)ncell * S;
-  for (long long wk = (long long)blockIdx.x * kElemWarps + warp; wk < nwork;
-       wk += (long long)gridDim.x * kElemWarps) {
-    const int a = (int)(wk / ncell);
-    const int e = (int)(wk % ncell);
+  double* kd = sKD[warp];
+  const int nK = 18 * S, nD = 36 * S;
+  for (int e = blockIdx.x * kElemWarps + warp; e < ncell; e += gridDim.x * kElemWarps) {
+    const double* Kc = K + (size_t)e * nK;
+    const double* Dc = D + (size_t)e * nD;
+    for (int t = lane; t < nK; t += 32) kd[t] = Kc[t];
+    for (int t = lane; t < nD; t += 32) kd[nK + t] = Dc[t];
+    if (lane < 9) kd[nK + nD + lane] = w[9 * (size_t)e + lane];
     const double jr = 2.0 / sizes[2 * e], jz = 2.0 / sizes[2 * e + 1];
-    if (lane < 9) {
-      const int pnt = 9 * e + lane;
-      const double wp = w[pnt];
-      const double* Kp = K + ((size_t)pnt * S + a) * 2;
-      const double* Dp = D + ((size_t)pnt * S + a) * 4;
-      // same factor grouping as assembly.py:159-160
-      sG[warp][lane][0] = Kp[0] * (jr * wp);
-      sG[warp][lane][1] = Kp[1] * (jz * wp);
-      sG[warp][lane][2] = Dp[0] * ((jr * jr) * wp);
-      sG[warp][lane][3] = Dp[1] * ((jr * jz) * wp);
-      sG[warp][lane][4] = Dp[2] * ((jz * jr) * wp);
-      sG[warp][lane][5] = Dp[3] * ((jz * jz) * wp);
-    }
     __syncwarp();
-    for (int t = lane; t < 81; t += 32) {  // t = 9*i + q
-      const int q = t % 9;
-      const double* g = sG[warp][q];
-      const double b0 = sdB[2 * t], b1 = sdB[2 * t + 1];
-      su[warp][t] = fma(b1, g[1], b0 * g[0]);
-      sv[warp][2 * t] = fma(b1, g[4], b0 * g[2]);
-      sv[warp][2 * t + 1] = fma(b1, g[5], b0 * g[3]);
-    }
-    __syncwarp();
-    double* out = elem + ((size_t)a * ncell_out + c_out + e) * 81;
-    for (int t = lane; t < 81; t += 32) {  // t = 9*i + j
-      const int ii = t / 9, jj = t % 9;
-      double s = 0.0;
-#pragma unroll
-      for (int q = 0; q < 9; ++q) {
-        s = fma(su[warp][9 * ii + q], sB[9 * jj + q], s);
-        s = fma(sv[warp][2 * (9 * ii + q)], sdB[2 * (9 * jj + q)], s);
-        s = fma(sv[warp][2 * (9 * ii + q) + 1], sdB[2 * (9 * jj + q) + 1], s);
+    for (int a = 0; a < S; ++a) {
+      if (lane < 9) {
+        const double wp = kd[nK + nD + lane];
+        const double* Kp = kd + (lane * S + a) * 2;
+        const double* Dp = kd + nK + (lane * S + a) * 4;
+        // same factor grouping as assembly.py:159-160
+        sG[warp][lane][0] = Kp[0] * (jr * wp);
+        sG[warp][lane][1] = Kp[1] * (jz * wp);
+        sG[warp][lane][2] = Dp[0] * ((jr * jr) * wp);
+        sG[warp][lane][3] = Dp[1] * ((jr * jz) * wp);
+        sG[warp][lane][4] = Dp[2] * ((jz * jr) * wp);
+        sG[warp][lane][5] = Dp[3] * ((jz * jz) * wp);
       }
-      out[t] = s;
+      __syncwarp();
+      for (int t = lane; t < 81; t += 32) {  // t = 9*i + q
+        const int q = t % 9;
+        const double* g = sG[warp][q];
+        const double b0 = sdB[2 * t], b1 = sdB[2 * t + 1];
+        su[warp][t] = fma(b1, g[1], b0 * g[0]);
+        sv[warp][2 * t] = fma(b1, g[4], b0 * g[2]);
+        sv[warp][2 * t + 1] = fma(b1, g[5], b0 * g[3]);
+      }
+      __syncwarp();
+      double* out = elem + ((size_t)a * ncell_out + c_out + e) * 81;
+      for (int t = lane; t < 81; t += 32) {  // t = 9*i + j
+        const int ii = t / 9, jj = t % 9;
+        double s = 0.0;
+#pragma unroll
+        for (int q = 0; q < 9; ++q) {
+          s = fma(su[warp][9 * ii + q], sB[9 * jj + q], s);
+          s = fma(sv[warp][2 * (9 * ii + q)], sdB[2 * (9 * jj + q)], s);
+          s = fma(sv[warp][2 * (9 * ii + q) + 1], sdB[2 * (9 * jj + q) + 1], s);
+        }
+        out[t] = s;
+      }
+      __syncwarp();
     }
-    __syncwarp();
   }
 }
 

@@ -32,6 +32,7 @@
 #include "landau_common.cuh"
 #include "landau_sweep.cuh"
 #include "landau_sym.cuh"
+#include "landau_blas.cuh"
 #include "landau_aux.cuh"
 #include "landau_cn.cuh"
 #include "landau_lu.cuh"
@@ -498,9 +499,8 @@ int launch_elements(lb_ctx* ctx, int ncell, int S, const double* sizes, const do
                     double* elem, cudaStream_t st, int ncell_out = -1, int c_out = 0) {
   if (ncell_out < 0) ncell_out = ncell;
   if (ncell == 0) return LB_OK;
-  const long long nwork = (long long)ncell * S;
-  const int blocks =
-      (int)std::min<long long>((nwork + kElemWarps - 1) / kElemWarps, (long long)ctx->num_sms * 16);
+  if (S > kElemMaxS) return fail(LB_EINVAL, "element contraction supports S <= 8");
+  const int blocks = (int)std::min<long long>((ncell + kElemWarps - 1) / kElemWarps, (long long)ctx->num_sms * 16);
   lb_elements_kernel<<<blocks, 32 * kElemWarps, 0, st>>>(ncell, S, sizes, w, K, D, B, dB, elem,
                                                          ncell_out, c_out);
   LB_CUDA(cudaGetLastError());
@@ -1566,16 +1566,21 @@ static int cn_factor_issue(lb_cn* cn, cudaStream_t st, bool pivot) {
                                    L.getrsL.count));
       }
     }
+    // Schur updates D_even -= A B and new couplings C = -A B: this
+    // package's batched DMMA GEMM (landau_blas.cuh)
+    const int gt = (nb + kGemmTile - 1) / kGemmTile;
     const CnBatch* acc[2] = {&L.gemmE, &L.gemmF};
     for (const CnBatch* b : acc)
-      if (b->count)
-        LB_BLAS(cublasDgemmBatched(cn->blas, CUBLAS_OP_N, CUBLAS_OP_N, nb, nb, nb, &mone, b->A, nb, b->B, nb,
-                                   &one, b->C, nb, b->count));
+      if (b->count) {
+        lb_bgemm_kernel<<<dim3(gt * gt, b->count), kGemmThreads, 0, st>>>(nb, b->A, b->B, b->C, 1);
+        LB_CUDA(cudaGetLastError());
+      }
     const CnBatch* fresh[2] = {&L.gemmG, &L.gemmH};
     for (const CnBatch* b : fresh)
-      if (b->count)
-        LB_BLAS(cublasDgemmBatched(cn->blas, CUBLAS_OP_N, CUBLAS_OP_N, nb, nb, nb, &mone, b->A, nb, b->B, nb,
-                                   &zero, b->C, nb, b->count));
+      if (b->count) {
+        lb_bgemm_kernel<<<dim3(gt * gt, b->count), kGemmThreads, 0, st>>>(nb, b->A, b->B, b->C, 0);
+        LB_CUDA(cudaGetLastError());
+      }
   }
   return LB_OK;
 }
@@ -1658,17 +1663,21 @@ static int cn_solve_issue(lb_cn* cn, cudaStream_t st, bool pivot) {
     }
     const CnBatch* fw[2] = {&L.fwdL, &L.fwdU};
     for (const CnBatch* b : fw)
-      if (b->count)
-        LB_BLAS(cublasDgemvBatched(cn->blas, CUBLAS_OP_N, nb, nb, &mone, b->A, nb, b->B, 1, &one, b->C, 1,
-                                   b->count));
+      if (b->count) {
+        lb_bgemv_kernel<<<dim3((nb + kGemvRows - 1) / kGemvRows, b->count), kGemvThreads, 0, st>>>(
+            nb, b->A, b->B, b->C);
+        LB_CUDA(cudaGetLastError());
+      }
   }
   for (int l = (int)cn->lv.size() - 1; l >= 0; --l) {
     const CnLevel& L = cn->lv[l];
     const CnBatch* bk[2] = {&L.backL, &L.backU};
     for (const CnBatch* b : bk)
-      if (b->count)
-        LB_BLAS(cublasDgemvBatched(cn->blas, CUBLAS_OP_N, nb, nb, &mone, b->A, nb, b->B, 1, &one, b->C, 1,
-                                   b->count));
+      if (b->count) {
+        lb_bgemv_kernel<<<dim3((nb + kGemvRows - 1) / kGemvRows, b->count), kGemvThreads, 0, st>>>(
+            nb, b->A, b->B, b->C);
+        LB_CUDA(cudaGetLastError());
+      }
   }
   return LB_OK;
 }

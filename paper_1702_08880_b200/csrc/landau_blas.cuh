@@ -10,8 +10,9 @@
 //    32 x 32 sub-tile of 4 x 4 FP64 MMA tiles (mma.sync.m8n8k4.f64, SASS
 //    DMMA) with the accumulators in registers.  Edge tiles are zero-padded.
 //  * lb_bgemv_kernel: y_b -= A_b x_b (the level passes of the block
-//    substitution): one CTA per matrix, x in shared memory, each thread a
-//    row, the k loop reading A's columns coalesced.
+//    substitution): one CTA per (32-row strip, matrix), eight column groups
+//    per row reading A's columns coalesced, partial sums added in fixed
+//    order.
 #pragma once
 #include "landau_lu.cuh"
 
@@ -130,30 +131,36 @@ __global__ void __launch_bounds__(kGemmThreads) lb_bgemm_kernel(int n, double* c
   }
 }
 
-constexpr int kGemvThreads = 256;
-
-// y_b -= A_b x_b, n x n column-major; x staged in shared memory (n doubles)
+// y_b -= A_b x_b, n x n column-major.  One CTA per (32-row strip, matrix):
+// 32 rows x 8 column groups; thread (row, g) sums the columns k = g mod 8
+// (reads of a column's 32 rows are one 256-byte segment per warp), the 8
+// partial sums meet in shared memory in fixed order.
+constexpr int kGemvRows = 32, kGemvGroups = 8, kGemvThreads = kGemvRows * kGemvGroups;
 __global__ void __launch_bounds__(kGemvThreads) lb_bgemv_kernel(int n, double* const* __restrict__ As_,
                                                                 double* const* __restrict__ xs_,
                                                                 double* const* __restrict__ ys_) {
-  extern __shared__ double xsh[];
-  const double* __restrict__ A = As_[blockIdx.x];
-  const double* __restrict__ x = xs_[blockIdx.x];
-  double* __restrict__ y = ys_[blockIdx.x];
-  for (int k = threadIdx.x; k < n; k += kGemvThreads) xsh[k] = x[k];
-  __syncthreads();
-  for (int i = threadIdx.x; i < n; i += kGemvThreads) {
-    // four independent partial sums over interleaved columns (latency)
-    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
-    int k = 0;
-    for (; k + 3 < n; k += 4) {
-      s0 = fma(A[(size_t)k * n + i], xsh[k], s0);
-      s1 = fma(A[(size_t)(k + 1) * n + i], xsh[k + 1], s1);
-      s2 = fma(A[(size_t)(k + 2) * n + i], xsh[k + 2], s2);
-      s3 = fma(A[(size_t)(k + 3) * n + i], xsh[k + 3], s3);
+  __shared__ double part[kGemvGroups][kGemvRows];
+  const double* __restrict__ A = As_[blockIdx.y];
+  const double* __restrict__ x = xs_[blockIdx.y];
+  double* __restrict__ y = ys_[blockIdx.y];
+  const int r = threadIdx.x & (kGemvRows - 1), g = threadIdx.x / kGemvRows;
+  const int i = blockIdx.x * kGemvRows + r;
+  double s0 = 0.0, s1 = 0.0;
+  if (i < n) {
+    int k = g;
+    for (; k + kGemvGroups < n; k += 2 * kGemvGroups) {
+      s0 = fma(A[(size_t)k * n + i], x[k], s0);
+      s1 = fma(A[(size_t)(k + kGemvGroups) * n + i], x[k + kGemvGroups], s1);
     }
-    for (; k < n; ++k) s0 = fma(A[(size_t)k * n + i], xsh[k], s0);
-    y[i] -= (s0 + s1) + (s2 + s3);
+    if (k < n) s0 = fma(A[(size_t)k * n + i], x[k], s0);
+  }
+  part[g][r] = s0 + s1;
+  __syncthreads();
+  if (g == 0 && i < n) {
+    double s = part[0][r];
+#pragma unroll
+    for (int q = 1; q < kGemvGroups; ++q) s += part[q][r];
+    y[i] -= s;
   }
 }
 

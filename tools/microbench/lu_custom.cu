@@ -12,10 +12,13 @@
 #ifndef LU_W
 #define LU_W 32
 #endif
+#ifndef LU_KB
+#define LU_KB 32
+#endif
 #include "landau_lu.cuh"
 
 using namespace lb;
-constexpr int KB = 32, W = LU_W;
+constexpr int KB = LU_KB, W = LU_W;
 
 static double urand(unsigned long long& s) {
   s = s * 6364136223846793005ULL + 1442695040888963407ULL;
@@ -81,7 +84,12 @@ int main(int argc, char** argv) {
   }
   return 0;
 #endif
-  for (int n : {5, 17, 32, 33, 67, 68, 131, 260, 354, 383}) {
+  std::vector<int> sizes = {5, 17, 32, 33, 67, 68, 131, 260, 354, 383};
+  if (argc > 1) {  // explicit sizes: lu_custom n1 n2 ...
+    sizes.clear();
+    for (int a = 1; a < argc; ++a) sizes.push_back(std::atoi(argv[a]));
+  }
+  for (int n : sizes) {
     if (getrs_smem_bytes<KB, W>(n) > 232448) {
       printf("n=%3d: W=%d slab needs %zu B of shared memory, skipped\n", n, W, getrs_smem_bytes<KB, W>(n));
       continue;
