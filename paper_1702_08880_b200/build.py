@@ -28,8 +28,8 @@ NVCC_FLAGS = [
     "-cudart", "static",
     f"-I{ROOT / 'include'}",
 ]
-# cuBLAS (batched dense block LU of the Crank-Nicolson solver, landau_cn.cuh)
-LINK_FLAGS = ["-lcublas"]
+# no libraries beyond the CUDA runtime: every kernel is this package's own
+LINK_FLAGS: list = []
 
 
 def nvcc() -> str:

@@ -88,73 +88,81 @@ __global__ void lb_gather_kernel(int n, const int* __restrict__ perm, const doub
 }
 
 // ------------------------------------------------------------------ K2 elements
-// One warp per cell, all S species.  The cell's K (9 x S x 2), D (9 x S x 4)
-// and w (9) are contiguous in HBM and read with coalesced loads; then per
-// species G2 = K Jinv w, G3 = Jinv D Jinv w (assembly.py:159-160, same
-// factor grouping) and
-//   elem[a,e,i,j] = sum_q dB[i,q,:].G2[q] B[j,q] + sum_q dB[i,q,:].G3[q].dB[j,q,:]
-// as u[i,q] = dB[i,q,:].G2[q], v[i,q,:] = dB[i,q,:].G3[q] followed by a
-// 27-term dot product per entry; each species' 81 entries are one
-// contiguous store.  Per (cell, species): 9 x 48 + 72 B in, 648 B out.
+// One warp per cell, all S species in chunks of three.  Per species G2 =
+// K Jinv w, G3 = Jinv D Jinv w (assembly.py:159-160, same factor grouping;
+// the cell's K (9 x S x 2), D (9 x S x 4) and w (9) are contiguous in HBM),
+// then one lane per (species, row i) forms
+//   u[q] = (dB[i,q,:].G2[q], dB[i,q,:].G3[q][:,0], dB[i,q,:].G3[q][:,1])
+// in registers and the row's nine entries
+//   elem[a,e,i,j] = sum_q u[q] . (B[j,q], dB[j,q,0], dB[j,q,1])
+// together, the basis values being warp-wide shared-memory broadcasts (one
+// shared load per FMA; ncu: an entry-per-lane form with u/v staged in shared
+// memory was MIO-bound and occupancy-limited by its shared memory).  Per
+// (cell, species): 9 x 48 + 72 B in, 648 B out; the (S, ncell, 81) result
+// stays in L2 for K3.
 constexpr int kElemWarps = 4;
 constexpr int kElemMaxS = 8;
+constexpr int kElemChunk = 3;  // species per pass (27 row tasks for a warp's 32 lanes)
 __global__ void __launch_bounds__(32 * kElemWarps) lb_elements_kernel(
     int ncell, int S, const double* __restrict__ sizes, const double* __restrict__ w,
     const double* __restrict__ K, const double* __restrict__ D, const double* __restrict__ Bt,
     const double* __restrict__ dBt, double* __restrict__ elem, int ncell_out, int c_out) {
   // cells e of this launch land at cell c_out + e of an (S, ncell_out, 81) buffer
-  __shared__ double sB[81], sdB[162];
-  __shared__ double sKD[kElemWarps][9 * kElemMaxS * 6 + 9];  // K (9 S 2), D (9 S 4), w (9)
-  __shared__ double su[kElemWarps][81], sv[kElemWarps][162];
-  __shared__ double sG[kElemWarps][9][6];  // G2 r,z ; G3 rr, rz, zr, zz
-  for (int t = threadIdx.x; t < 81; t += blockDim.x) sB[t] = Bt[t];
-  for (int t = threadIdx.x; t < 162; t += blockDim.x) sdB[t] = dBt[t];
+  __shared__ double sV[9][9][3];  // basis as V[j][q] = (B, dB_r, dB_z)
+  __shared__ double sG[kElemWarps][kElemChunk][9][6];  // G2 r,z ; G3 rr, rz, zr, zz
+  for (int t = threadIdx.x; t < 81; t += blockDim.x) {
+    const int j = t / 9, q = t % 9;
+    sV[j][q][0] = Bt[t];
+    sV[j][q][1] = dBt[2 * t];
+    sV[j][q][2] = dBt[2 * t + 1];
+  }
   __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  double* kd = sKD[warp];
-  const int nK = 18 * S, nD = 36 * S;
   for (int e = blockIdx.x * kElemWarps + warp; e < ncell; e += gridDim.x * kElemWarps) {
-    const double* Kc = K + (size_t)e * nK;
-    const double* Dc = D + (size_t)e * nD;
-    for (int t = lane; t < nK; t += 32) kd[t] = Kc[t];
-    for (int t = lane; t < nD; t += 32) kd[nK + t] = Dc[t];
-    if (lane < 9) kd[nK + nD + lane] = w[9 * (size_t)e + lane];
     const double jr = 2.0 / sizes[2 * e], jz = 2.0 / sizes[2 * e + 1];
-    __syncwarp();
-    for (int a = 0; a < S; ++a) {
-      if (lane < 9) {
-        const double wp = kd[nK + nD + lane];
-        const double* Kp = kd + (lane * S + a) * 2;
-        const double* Dp = kd + nK + (lane * S + a) * 4;
+    for (int a0 = 0; a0 < S; a0 += kElemChunk) {
+      const int nc = min(kElemChunk, S - a0);
+      for (int t = lane; t < 9 * nc; t += 32) {  // (species a0 + c, point q)
+        const int c = t / 9, q = t % 9, a = a0 + c;
+        const size_t pnt = 9 * (size_t)e + q;
+        const double wp = w[pnt];
+        const double* Kp = K + (pnt * S + a) * 2;
+        const double* Dp = D + (pnt * S + a) * 4;
+        double* g = sG[warp][c][q];
         // same factor grouping as assembly.py:159-160
-        sG[warp][lane][0] = Kp[0] * (jr * wp);
-        sG[warp][lane][1] = Kp[1] * (jz * wp);
-        sG[warp][lane][2] = Dp[0] * ((jr * jr) * wp);
-        sG[warp][lane][3] = Dp[1] * ((jr * jz) * wp);
-        sG[warp][lane][4] = Dp[2] * ((jz * jr) * wp);
-        sG[warp][lane][5] = Dp[3] * ((jz * jz) * wp);
+        g[0] = Kp[0] * (jr * wp);
+        g[1] = Kp[1] * (jz * wp);
+        g[2] = Dp[0] * ((jr * jr) * wp);
+        g[3] = Dp[1] * ((jr * jz) * wp);
+        g[4] = Dp[2] * ((jz * jr) * wp);
+        g[5] = Dp[3] * ((jz * jz) * wp);
       }
       __syncwarp();
-      for (int t = lane; t < 81; t += 32) {  // t = 9*i + q
-        const int q = t % 9;
-        const double* g = sG[warp][q];
-        const double b0 = sdB[2 * t], b1 = sdB[2 * t + 1];
-        su[warp][t] = fma(b1, g[1], b0 * g[0]);
-        sv[warp][2 * t] = fma(b1, g[4], b0 * g[2]);
-        sv[warp][2 * t + 1] = fma(b1, g[5], b0 * g[3]);
-      }
-      __syncwarp();
-      double* out = elem + ((size_t)a * ncell_out + c_out + e) * 81;
-      for (int t = lane; t < 81; t += 32) {  // t = 9*i + j
-        const int ii = t / 9, jj = t % 9;
-        double s = 0.0;
+      for (int t = lane; t < 9 * nc; t += 32) {  // (c, row i): the nine entries of the row
+        const int c = t / 9, i = t % 9;
+        double u[9][3];
 #pragma unroll
         for (int q = 0; q < 9; ++q) {
-          s = fma(su[warp][9 * ii + q], sB[9 * jj + q], s);
-          s = fma(sv[warp][2 * (9 * ii + q)], sdB[2 * (9 * jj + q)], s);
-          s = fma(sv[warp][2 * (9 * ii + q) + 1], sdB[2 * (9 * jj + q) + 1], s);
+          const double* g = sG[warp][c][q];
+          const double b0 = sV[i][q][1], b1 = sV[i][q][2];  // dB[i,q,:]
+          u[q][0] = fma(b1, g[1], b0 * g[0]);
+          u[q][1] = fma(b1, g[4], b0 * g[2]);
+          u[q][2] = fma(b1, g[5], b0 * g[3]);
         }
-        out[t] = s;
+        double s[9];
+#pragma unroll
+        for (int j = 0; j < 9; ++j) s[j] = 0.0;
+#pragma unroll
+        for (int q = 0; q < 9; ++q)
+#pragma unroll
+          for (int j = 0; j < 9; ++j) {
+            s[j] = fma(u[q][0], sV[j][q][0], s[j]);
+            s[j] = fma(u[q][1], sV[j][q][1], s[j]);
+            s[j] = fma(u[q][2], sV[j][q][2], s[j]);
+          }
+        double* out = elem + ((size_t)(a0 + c) * ncell_out + c_out + e) * 81 + 9 * i;
+#pragma unroll
+        for (int j = 0; j < 9; ++j) out[j] = s[j];
       }
       __syncwarp();
     }
@@ -172,15 +180,37 @@ __global__ void lb_csr_gather_kernel(int nslots, int nent, int S, const int* __r
   const int slot = blockIdx.x * blockDim.x + threadIdx.x;
   if (slot >= nslots) return;
   const int k0 = slot_ptr[slot], k1 = slot_ptr[slot + 1];
-  for (int a = 0; a < S; ++a) {
-    const double* ea = elem + (size_t)a * nent;
-    double v = 0.0;
-    for (int k = k0; k < k1; ++k) {
-      LB_DCHECK(gidx[k] >= 0 && gidx[k] < nent);
-      v = fma(gw[k], ea[gidx[k]], v);
+  // contributions in groups of 4: the group's indices, weights and element
+  // entries (all species) are loaded before the ordered adds (latency-bound
+  // gather from L2; the order of the adds is the map's)
+  double v[kElemMaxS];
+#pragma unroll
+  for (int a = 0; a < kElemMaxS; ++a) v[a] = 0.0;
+  for (int kb = k0; kb < k1; kb += 4) {
+    int ix[4];
+    double ww[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const bool on = kb + u < k1;
+      ix[u] = on ? gidx[kb + u] : 0;
+      ww[u] = on ? gw[kb + u] : 0.0;
+      LB_DCHECK(ix[u] >= 0 && ix[u] < nent);
     }
-    out[(size_t)a * nslots + slot] = v;
+#pragma unroll
+    for (int a = 0; a < kElemMaxS; ++a) {
+      if (a >= S) break;
+      const double* ea = elem + (size_t)a * nent;
+      double x[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) x[u] = kb + u < k1 ? ea[ix[u]] : 0.0;
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (kb + u < k1) v[a] = fma(ww[u], x[u], v[a]);
+    }
   }
+#pragma unroll
+  for (int a = 0; a < kElemMaxS; ++a)
+    if (a < S) out[(size_t)a * nslots + slot] = v[a];
 }
 
 // ------------------------------------------------------------------ K4 sampling

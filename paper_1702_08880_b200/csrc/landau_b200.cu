@@ -15,7 +15,6 @@
 // Determinism: every reduction runs in a fixed order that is a function of
 // the problem size (and the Morton order of the points); no atomics.
 #include <cub/device/device_radix_sort.cuh>
-#include <cublas_v2.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -1462,7 +1461,6 @@ struct lb_cn {
   long long nnz = 0, sstride = 0;  // sstride: block-pool doubles per species
   bool has_mass = false;
   bool co_valid = false;     // Co holds a C_old from an earlier lb_cn_newton
-  cublasHandle_t blas = nullptr;
   int *indptr = nullptr, *indices = nullptr, *perm = nullptr, *flag = nullptr;
   long long* off = nullptr;  // CSR slot -> block-pool offset (species 0)
   double* Mv = nullptr;      // mass values (nnz)
@@ -1476,18 +1474,10 @@ struct lb_cn {
   bool pivot = false;
   int fallbacks = 0;
   double last_rel_residual = 0.0;
-  void* blas_ws = nullptr;   // cuBLAS workspace (set explicitly so calls can be captured)
   double *g = nullptr, *f = nullptr, *d = nullptr, *R = nullptr, *Mf = nullptr, *x = nullptr,
          *out = nullptr, *Co = nullptr, *Cg = nullptr, *red = nullptr;
   std::vector<void*> allocs;
 };
-
-#define LB_BLAS(call)                                                                  \
-  do {                                                                                 \
-    cublasStatus_t s_ = (call);                                                        \
-    if (s_ != CUBLAS_STATUS_SUCCESS)                                                   \
-      return fail(LB_ECUDA, std::string(#call) + ": cuBLAS status " + std::to_string((int)s_)); \
-  } while (0)
 
 static int cn_alloc(lb_cn* cn, void** p, size_t bytes) {
   cudaError_t e = cudaMalloc(p, std::max<size_t>(bytes, 8));
@@ -1500,27 +1490,22 @@ static int cn_alloc(lb_cn* cn, void** p, size_t bytes) {
   return LB_OK;
 }
 
-// block LU + [L U] solve by the custom kernels of landau_lu.cuh (cuBLAS
-// getrf / getrs / trsm otherwise: blocks over 384 rows, or LB_CN_CUBLAS_LU set)
+// block LU + [L U] solve by the shared-memory kernels of landau_lu.cuh for
+// blocks up to 384 rows; larger blocks (or LB_CN_GM_LU set) by the
+// global-memory LU and substitution of landau_blas.cuh
 constexpr int kLuKB = 32, kLuW = 32, kLuMaxNb = 384;
 constexpr int kLuWideMinCount = 48;       // blocks per level from which 64-column slabs pay
 constexpr size_t kLuSmemMax = 232448;     // opt-in shared memory per CTA (227 KB)
 static bool cn_custom_lu(const lb_cn* cn) {
-  static const bool force_blas = std::getenv("LB_CN_CUBLAS_LU") != nullptr;
-  return cn->nb <= kLuMaxNb && !force_blas;
+  static const bool force_gm = std::getenv("LB_CN_GM_LU") != nullptr;
+  return cn->nb <= kLuMaxNb && !force_gm;
 }
 
-// factor blocks small enough for the shared-memory vector solve (cuBLAS otherwise)
-static bool cn_small(const lb_cn* cn) {
-  static const bool force_blas = std::getenv("LB_CN_CUBLAS") != nullptr;
-  return cn->nb <= kSmallNb && !force_blas;
-}
+// factor blocks small enough for the shared-memory vector solve
+static bool cn_small(const lb_cn* cn) { return cn->nb <= kSmallNb; }
 
 static int cn_factor_issue(lb_cn* cn, cudaStream_t st, bool pivot) {
   const int nb = cn->nb;
-  const double one = 1.0, mone = -1.0, zero = 0.0;
-  int hinfo = 0;
-  LB_BLAS(cublasSetStream(cn->blas, st));
   const bool custom = cn_custom_lu(cn);
   for (const CnLevel& L : cn->lv) {
     if (custom) {
@@ -1546,24 +1531,18 @@ static int cn_factor_issue(lb_cn* cn, cudaStream_t st, bool pivot) {
         }
         LB_CUDA(cudaGetLastError());
       }
-    } else if (L.getrf.count) {
-      LB_BLAS(cublasDgetrfBatched(cn->blas, nb, L.getrf.A, nb, pivot ? L.piv : nullptr, L.info,
-                                  L.getrf.count));
-    }
-    // L_l[k] and U_l[k] are adjacent in the pool, so [L U] is one nb x 2nb
-    // column-major right-hand side: P = D^-1 [L U] in a single call (the
-    // last odd row's U slot is unused scratch when it has no right neighbour)
-    if (!custom && L.getrsL.count) {
-      if (pivot) {
-        LB_BLAS(cublasDgetrsBatched(cn->blas, CUBLAS_OP_N, nb, 2 * nb, L.getrsL.A, nb, L.piv, L.getrsL.B,
-                                    nb, &hinfo, L.getrsL.count));
-      } else {
-        LB_BLAS(cublasDtrsmBatched(cn->blas, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N,
-                                   CUBLAS_DIAG_UNIT, nb, 2 * nb, &one, L.getrsL.A, nb, L.getrsL.B, nb,
-                                   L.getrsL.count));
-        LB_BLAS(cublasDtrsmBatched(cn->blas, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_UPPER, CUBLAS_OP_N,
-                                   CUBLAS_DIAG_NON_UNIT, nb, 2 * nb, &one, L.getrsL.A, nb, L.getrsL.B, nb,
-                                   L.getrsL.count));
+    } else {
+      // any block size: global-memory LU (ipiv = identity when not pivoting)
+      // and substitution for the nb x 2nb right-hand side [L U] (adjacent in
+      // the pool; the last odd row's U slot is unused scratch)
+      if (L.getrf.count) {
+        lb_getrf_gm_kernel<<<L.getrf.count, kGmThreads, 0, st>>>(nb, L.getrf.A, L.piv, L.info, pivot ? 1 : 0);
+        LB_CUDA(cudaGetLastError());
+      }
+      if (L.getrsL.count) {
+        lb_getrs_gm_kernel<<<dim3(L.getrsL.count, (2 * nb + kGmCols - 1) / kGmCols), 256, 0, st>>>(
+            nb, 2 * nb, L.getrsL.A, L.piv, L.getrsL.B);
+        LB_CUDA(cudaGetLastError());
       }
     }
     // Schur updates D_even -= A B and new couplings C = -A B: this
@@ -1638,28 +1617,19 @@ static int cn_factor(lb_cn* cn, cudaStream_t st) {
 // on exit.
 static int cn_solve_issue(lb_cn* cn, cudaStream_t st, bool pivot) {
   const int nb = cn->nb;
-  const double one = 1.0, mone = -1.0;
-  int hinfo = 0;
-  LB_BLAS(cublasSetStream(cn->blas, st));
   const bool small = cn_small(cn), custom = cn_custom_lu(cn);
   for (const CnLevel& L : cn->lv) {
     if (small && L.solveY.count) {  // blocks of <= 96 rows: whole factor in shared memory
       lb_small_solve_kernel<<<L.solveY.count, kSmallThreads, small_solve_smem_bytes(nb), st>>>(
-          nb, L.solveY.count, L.getrf.A, pivot ? L.piv : nullptr, L.solveY.B);
+          nb, L.solveY.count, L.getrf.A, pivot || !custom ? L.piv : nullptr, L.solveY.B);
       LB_CUDA(cudaGetLastError());
     } else if (custom && L.solveY.count) {  // larger blocks with the custom LU's factors
       lb_lu_vsolve_kernel<kLuKB><<<L.solveY.count, kLuThreads, sizeof(double) * nb, st>>>(
           nb, L.solveY.count, L.getrf.A, L.perm, L.inv, L.solveY.B);
       LB_CUDA(cudaGetLastError());
-    } else if (L.solveY.count && pivot) {
-      LB_BLAS(cublasDgetrsBatched(cn->blas, CUBLAS_OP_N, nb, 1, L.getrf.A, nb, L.piv, L.solveY.B, nb, &hinfo,
-                                  L.solveY.count));
-    } else if (L.solveY.count) {
-      LB_BLAS(cublasDtrsmBatched(cn->blas, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N,
-                                 CUBLAS_DIAG_UNIT, nb, 1, &one, L.getrf.A, nb, L.solveY.B, nb, L.solveY.count));
-      LB_BLAS(cublasDtrsmBatched(cn->blas, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_UPPER, CUBLAS_OP_N,
-                                 CUBLAS_DIAG_NON_UNIT, nb, 1, &one, L.getrf.A, nb, L.solveY.B, nb,
-                                 L.solveY.count));
+    } else if (L.solveY.count) {  // global-memory factors
+      lb_getrs_gm_kernel<<<dim3(L.solveY.count, 1), 256, 0, st>>>(nb, 1, L.getrf.A, L.piv, L.solveY.B);
+      LB_CUDA(cudaGetLastError());
     }
     const CnBatch* fw[2] = {&L.fwdL, &L.fwdU};
     for (const CnBatch* b : fw)
@@ -1959,7 +1929,6 @@ int lb_cn_create(lb_ctx* ctx, const lb_mesh* m, int S, int n, const int* indptr,
   up(cn->perm, perm, sizeof(int) * n);
   up(cn->off, off.data(), sizeof(long long) * nnz);
   if (e != cudaSuccess) return bail(fail(LB_ECUDA, std::string("lb_cn_create: ") + cudaGetErrorString(e)));
-  if (cublasCreate(&cn->blas) != CUBLAS_STATUS_SUCCESS) return bail(fail(LB_ECUDA, "cublasCreate failed"));
   if (nb <= kSmallNb &&
       cudaFuncSetAttribute(lb_small_solve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)small_solve_smem_bytes(kSmallNb)) != cudaSuccess)
@@ -1972,10 +1941,6 @@ int lb_cn_create(lb_ctx* ctx, const lb_mesh* m, int S, int n, const int* indptr,
        cudaFuncSetAttribute(lb_getrs_slab_kernel<kLuKB, 2 * kLuW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             (int)kLuSmemMax) != cudaSuccess))
     return bail(fail(LB_ECUDA, "cudaFuncSetAttribute(custom LU kernels) failed"));
-  const size_t ws = size_t(32) << 20;
-  if ((rc = cn_alloc(cn, &cn->blas_ws, ws))) return bail(rc);
-  if (cublasSetWorkspace(cn->blas, cn->blas_ws, ws) != CUBLAS_STATUS_SUCCESS)
-    return bail(fail(LB_ECUDA, "cublasSetWorkspace failed"));
   *out = cn;
   return LB_OK;
 }
@@ -1988,7 +1953,6 @@ int lb_cn_destroy(lb_cn* cn) {
     if (cn->factor_graph[k]) cudaGraphExecDestroy(cn->factor_graph[k]);
     if (cn->solve_graph[k]) cudaGraphExecDestroy(cn->solve_graph[k]);
   }
-  if (cn->blas) cublasDestroy(cn->blas);
   for (void* p : cn->allocs) cudaFree(p);
   delete cn;
   return LB_OK;

@@ -165,3 +165,128 @@ __global__ void __launch_bounds__(kGemvThreads) lb_bgemv_kernel(int n, double* c
 }
 
 }  // namespace lb
+
+namespace lb {
+
+// ---------------------------------------------------------------------------
+// Blocks above the shared-memory kernels' size (nb > 384, landau_lu.cuh):
+// a plain right-looking LU with partial pivoting (LAPACK layout: unit L
+// below the diagonal, U on and above it, 1-based ipiv, info = first zero
+// pivot) worked in global memory by one CTA per matrix, and the matching
+// substitution for blocks of right-hand sides.  O(n^3) L2 traffic per
+// matrix: correct for any block size, meant for meshes whose banded order
+// exceeds 384 rows (none of the BASELINE configurations does).
+constexpr int kGmThreads = 1024;
+
+__global__ void __launch_bounds__(kGmThreads) lb_getrf_gm_kernel(int n, double* const* __restrict__ As,
+                                                                 int* __restrict__ ipiv_all,
+                                                                 int* __restrict__ info_all, int pivot) {
+  __shared__ double redv[32];
+  __shared__ int redi[32];
+  __shared__ int piv_sh;
+  double* A = As[blockIdx.x];
+  int* ipiv = ipiv_all + (size_t)blockIdx.x * n;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  int info = 0;
+  for (int j = 0; j < n; ++j) {
+    double* cj = A + (size_t)j * n;
+    if (pivot) {  // idamax over rows j..n-1: the first largest |a|
+      double best = -1.0;
+      int bi = n;
+      for (int i = j + tid; i < n; i += kGmThreads) {
+        const double v = fabs(cj[i]);
+        if (v > best) { best = v; bi = i; }
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const double ov = __shfl_xor_sync(0xffffffffu, best, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+        if (ov > best || (ov == best && oi < bi)) { best = ov; bi = oi; }
+      }
+      if (lane == 0) { redv[warp] = best; redi[warp] = bi; }
+      __syncthreads();
+      if (tid == 0) {
+        for (int q = 1; q < kGmThreads / 32; ++q)
+          if (redv[q] > best || (redv[q] == best && redi[q] < bi)) { best = redv[q]; bi = redi[q]; }
+        piv_sh = bi < n ? bi : j;
+      }
+      __syncthreads();
+      const int p = piv_sh;
+      if (p != j)
+        for (int k = tid; k < n; k += kGmThreads) {
+          double* ck = A + (size_t)k * n;
+          const double t = ck[j];
+          ck[j] = ck[p];
+          ck[p] = t;
+        }
+      if (tid == 0) ipiv[j] = p + 1;
+      __syncthreads();
+    } else if (tid == 0) {
+      ipiv[j] = j + 1;
+    }
+    const double d = cj[j];
+    if (d == 0.0 && info == 0) info = j + 1;
+    const double r = d != 0.0 ? 1.0 / d : 0.0;
+    for (int i = j + 1 + tid; i < n; i += kGmThreads) cj[i] *= r;
+    __syncthreads();
+    // A[j+1:, j+1:] -= A[j+1:, j] A[j, j+1:] (column-major: i runs fastest)
+    const int m = n - j - 1;
+    for (long long t = tid; t < (long long)m * m; t += kGmThreads) {
+      const int i = j + 1 + (int)(t % m), k = j + 1 + (int)(t / m);
+      double* ck = A + (size_t)k * n;
+      ck[i] = fma(-cj[i], ck[j], ck[i]);
+    }
+    __syncthreads();
+  }
+  if (tid == 0) info_all[blockIdx.x] = info;
+}
+
+// X := A^-1 X for the factors of lb_getrf_gm_kernel, X (n x m, ld n,
+// column-major) in place; one CTA per (matrix, 8-column chunk).
+constexpr int kGmCols = 8;
+__global__ void __launch_bounds__(256) lb_getrs_gm_kernel(int n, int m, double* const* __restrict__ As,
+                                                          const int* __restrict__ ipiv_all,
+                                                          double* const* __restrict__ Xs) {
+  const double* A = As[blockIdx.x];
+  const int* ipiv = ipiv_all + (size_t)blockIdx.x * n;
+  double* X = Xs[blockIdx.x];
+  const int c0 = blockIdx.y * kGmCols, nc = min(kGmCols, m - c0);
+  const int tid = threadIdx.x;
+  if (tid < nc) {  // row swaps in order (LAPACK laswp)
+    double* x = X + (size_t)(c0 + tid) * n;
+    for (int k = 0; k < n; ++k) {
+      const int p = ipiv[k] - 1;
+      if (p != k) {
+        const double t = x[k];
+        x[k] = x[p];
+        x[p] = t;
+      }
+    }
+  }
+  __syncthreads();
+  for (int k = 0; k < n; ++k) {  // unit lower L
+    const double* lk = A + (size_t)k * n;
+    for (int t = tid; t < (n - k - 1) * nc; t += blockDim.x) {
+      const int i = k + 1 + t % (n - k - 1), c = t / (n - k - 1);
+      double* x = X + (size_t)(c0 + c) * n;
+      x[i] = fma(-lk[i], x[k], x[i]);
+    }
+    __syncthreads();
+  }
+  for (int k = n - 1; k >= 0; --k) {  // upper U
+    const double* uk = A + (size_t)k * n;
+    if (tid < nc) {
+      double* x = X + (size_t)(c0 + tid) * n;
+      x[k] = x[k] / uk[k];
+    }
+    __syncthreads();
+    for (int t = tid; t < k * nc; t += blockDim.x) {
+      const int i = t % k, c = t / k;
+      double* x = X + (size_t)(c0 + c) * n;
+      x[i] = fma(-uk[i], x[k], x[i]);
+    }
+    __syncthreads();
+  }
+}
+
+}  // namespace lb

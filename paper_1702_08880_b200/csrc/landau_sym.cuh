@@ -157,10 +157,17 @@ struct SymProducer {
   uint32_t p_k = 0;
   bool p_done = false;
 
+  long long nclaim;  // items that exist (rows x their segments); nitems = rows x nseg slots
+
   __device__ SymProducer(const SymArgs& args, long long n, double* sm, uint64_t* f, uint64_t* e, int* si,
                          int* sd)
-      : a(args), nitems(n), smem(sm), full(f), empty(e), stage_item(si), stage_d(sd),
-        p_item(blockIdx.x) {}
+      : a(args), nitems(n), smem(sm), full(f), empty(e), stage_item(si), stage_d(sd) {
+    const int nt = a.nt, L = sym_seglen(nt);
+    const int mid = (nt & 1) ? a.row1 : max(a.row0, min(a.row1, nt / 2));
+    const int tA = sym_h(a.row0 < mid ? a.row0 : mid, nt) + 1, tB = sym_h(max(mid, a.row0), nt) + 1;
+    nclaim = (long long)(mid - a.row0) * ((tA + L - 1) / L) + (long long)(a.row1 - mid) * ((tB + L - 1) / L);
+    p_item = (int)blockIdx.x < nclaim ? claimed_item((int)blockIdx.x) : (int)nitems;
+  }
 
   __device__ void seg_range(int item, int& I, int& d0, int& d1) const {
     I = a.row0 + item / a.nseg;
@@ -170,6 +177,30 @@ struct SymProducer {
     d1 = min(sym_h(I, a.nt) + 1, d0 + L);
   }
 
+  // Claim order -> work item (row-major slot (I - row0) nseg + seg).  The
+  // full L-tile segments of all rows come first, then the short last
+  // segments (rows whose H + 1 tiles are not a multiple of L), so the final
+  // wave is made of the smallest items (a shorter tail, most visible on the
+  // 1/G row share of a G-GPU split).  Every item still writes its own
+  // partial slot: the order changes the schedule, never a bit of the result.
+  __device__ int claimed_item(int c) const {
+    const int nt = a.nt, L = sym_seglen(nt);
+    const int mid = (nt & 1) ? a.row1 : max(a.row0, min(a.row1, nt / 2));  // rows below mid: H + 1 = nt/2 + 1
+    const int tA = sym_h(a.row0 < mid ? a.row0 : mid, nt) + 1;             // tiles per row, class A
+    const int tB = sym_h(max(mid, a.row0), nt) + 1;                         // class B (rows >= mid)
+    const int rowsA = mid - a.row0, rowsB = a.row1 - mid;
+    const int fA = tA / L, fB = tB / L;
+    const long long nfA = (long long)rowsA * fA, nfB = (long long)rowsB * fB;
+    if (c < nfA) return (c / fA) * a.nseg + c % fA;
+    c -= (int)nfA;
+    if (c < nfB) return (rowsA + c / fB) * a.nseg + c % fB;
+    c -= (int)nfB;
+    const int sA = (tA % L) ? rowsA : 0;  // short segments: class A rows first, then B
+    if (c < sA) return c * a.nseg + fA;
+    c -= sA;
+    return (rowsA + c) * a.nseg + fB;
+  }
+
   __device__ void issue_next() {
     if (p_done) return;
     int I = 0, d0, d1;
@@ -177,7 +208,9 @@ struct SymProducer {
       seg_range(p_item, I, d0, d1);
       if (p_d < 0) p_d = d0;
       if (p_d < d1) break;
-      p_item = (int)gridDim.x + atomicAdd(a.next_item, 1);  // segment done: claim the next
+      // segment done: claim the next one
+      const int c = (int)gridDim.x + atomicAdd(a.next_item, 1);
+      p_item = c < nclaim ? claimed_item(c) : (int)nitems;
       p_d = -1;
     }
     const uint32_t s = p_k % kSymStages;

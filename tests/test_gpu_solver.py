@@ -296,8 +296,9 @@ np.save(sys.argv[2], nxt)
 
 def test_custom_block_lu_matches_cublas_path_cfg3(gpu, tmp_path):
     """Config 3 (hanging nodes, 354-row blocks, the unpivoted path): the
-    package's block-LU kernels and the cuBLAS path (LB_CN_CUBLAS_LU=1, in a
-    subprocess) give the same Newton step, and both the reference's."""
+    shared-memory block-LU kernels and the global-memory LU path
+    (LB_CN_GM_LU=1, in a subprocess; the path blocks over 384 rows take)
+    give the same Newton step, and both the reference's."""
     import os
     import subprocess
     import sys
@@ -305,27 +306,27 @@ def test_custom_block_lu_matches_cublas_path_cfg3(gpu, tmp_path):
 
     root = Path(__file__).resolve().parents[1]
     outs = {}
-    for name, extra in (("custom", {}), ("cublas", {"LB_CN_CUBLAS_LU": "1"})):
+    for name, extra in (("custom", {}), ("cublas", {"LB_CN_GM_LU": "1"})):
         out = tmp_path / f"{name}.npy"
         subprocess.run([sys.executable, "-c", _CUBLAS_LU_CFG3_SCRIPT, str(root), str(out)],
                        env=dict(os.environ, **extra), check=True, timeout=600)
         outs[name] = np.load(out)
     g = golden("cfg3")
     err = _scaled(outs["custom"], outs["cublas"])
-    print("cfg3 custom LU vs cuBLAS LU", err)
+    print("cfg3 shared-memory LU vs global-memory LU", err)
     assert err <= 1e-12
     for v in outs.values():
         assert _scaled(v, g["newton_coeffs"]) <= TOL
 
 
 def test_custom_block_lu_matches_cublas_path(gpu, tmp_path):
-    """The package's block LU + [L U] solve kernels and the cuBLAS
-    getrf/getrs/trsm path (LB_CN_CUBLAS_LU=1, read once per process, so it
-    runs in a subprocess) give the same Newton step on the 32x64 config-4
-    mesh (132-row blocks, four species): within the suite's 1e-10 bar (the
-    electron system is the ill-conditioned one that needs pivoting; there
-    both paths differ from SuperLU by ~3e-11 and from each other by ~2e-11,
-    the other species agree to ~1e-16)."""
+    """The shared-memory block LU + [L U] slab-solve kernels and the
+    global-memory LU + substitution (LB_CN_GM_LU=1, read once per process,
+    so it runs in a subprocess) give the same Newton step on the 32x64
+    config-4 mesh (132-row blocks, four species): within the suite's 1e-10
+    bar (the electron system is the ill-conditioned one that needs
+    pivoting; both differ from SuperLU by ~3e-11 there, the other species
+    agree to ~1e-16)."""
     import os
     import subprocess
     import sys
@@ -333,7 +334,7 @@ def test_custom_block_lu_matches_cublas_path(gpu, tmp_path):
 
     root = Path(__file__).resolve().parents[1]
     outs = {}
-    for name, extra in (("custom", {}), ("cublas", {"LB_CN_CUBLAS_LU": "1"})):
+    for name, extra in (("custom", {}), ("cublas", {"LB_CN_GM_LU": "1"})):
         env = dict(os.environ, **extra)
         out = tmp_path / f"{name}.npy"
         subprocess.run([sys.executable, "-c", _CUBLAS_LU_SCRIPT, str(root), str(out)], env=env,
@@ -341,7 +342,7 @@ def test_custom_block_lu_matches_cublas_path(gpu, tmp_path):
         outs[name] = np.load(out)
     for a in range(4):
         err = _scaled(outs["custom"][a], outs["cublas"][a])
-        print("species", a, "custom LU vs cuBLAS LU", err)
+        print("species", a, "shared-memory LU vs global-memory LU", err)
         assert err <= TOL
 
 
@@ -407,3 +408,30 @@ def test_theta_step_is_backward_euler_and_cn(gpu):
     assert np.array_equal(cn, cn_ref)
     with pytest.raises(ValueError):
         gpu.theta_step(M, C, dt, f, 0.0)
+
+
+@pytest.mark.parametrize("dominant", [True, False])
+def test_wide_band_blocks_above_384_rows(gpu, dominant):
+    """A banded system whose bandwidth (420) exceeds the shared-memory LU's
+    384-row blocks: the solver takes the global-memory block LU (no library
+    fallback) and matches scipy's splu -- diagonally dominant (unpivoted LU
+    accepted) and not (the pivoted refactorisation)."""
+    import scipy.sparse as sp
+    import scipy.sparse.linalg as spla
+    from types import SimpleNamespace
+
+    from paper_1702_08880_b200.solver import linear_cn_step
+
+    n, b = 2100, 420
+    rng = np.random.default_rng(7 if dominant else 8)
+    offs = np.arange(-b, b + 1)
+    diags = [rng.uniform(-1, 1, n - abs(k)) for k in offs]
+    C = sp.diags(diags, offs, shape=(n, n), format="csr")
+    M = sp.identity(n, format="csr") * (3.0 * b if dominant else 0.5)
+    dt = 0.2
+    f = rng.uniform(-1, 1, (1, n))
+    out = linear_cn_step(M, SimpleNamespace(blocks=[C]), dt, f)
+    ref = spla.splu((M - 0.5 * dt * C).tocsc()).solve((M + 0.5 * dt * C) @ f[0])
+    err = np.abs(np.asarray(out)[0] - ref).max() / np.abs(ref).max()
+    print("bandwidth 420 (global-memory block LU), dominant" if dominant else "not dominant", err)
+    assert err < 1e-10
