@@ -1436,6 +1436,7 @@ struct CnBatch {  // one batched call: pointer arrays (device) and their count
   double** A = nullptr;
   double** B = nullptr;
   double** C = nullptr;
+  double** C2 = nullptr;  // second output (fused GEMMs), may be absent
   int count = 0;
 };
 
@@ -1447,8 +1448,8 @@ struct CnLevel {
   double* inv = nullptr;   // inverses of the factors' diagonal blocks (custom LU)
   CnBatch getrf;        // A = D (odd rows)
   CnBatch getrsL;       // A = D, B = [L U] (odd rows; adjacent blocks, one nb x 2nb right-hand side)
-  CnBatch gemmE, gemmF;    // C = D_even -= A B
-  CnBatch gemmG, gemmH;    // C = next level's L / U = -A B
+  CnBatch gemmEG;          // A = L_k, B = [P^L P^U]_{k-1}: C = L_{l+1}[k/2] = -A P^L, C2 = D_k -= A P^U
+  CnBatch gemmFH;          // A = U_k, B = [P^L P^U]_{k+1}: C = D_k -= A P^L, C2 = U_{l+1}[k/2] = -A P^U (if any)
   CnBatch solveY;          // B = v (odd rows): v := D^-1 v
   CnBatch fwdL, fwdU;      // even rows: v_k -= A x (A = L_k / U_k, x = v of the neighbour)
   CnBatch backL, backU;    // odd rows:  v_k -= A x (A = P^L / P^U)
@@ -1545,21 +1546,20 @@ static int cn_factor_issue(lb_cn* cn, cudaStream_t st, bool pivot) {
         LB_CUDA(cudaGetLastError());
       }
     }
-    // Schur updates D_even -= A B and new couplings C = -A B: this
-    // package's batched DMMA GEMM (landau_blas.cuh)
-    const int gt = (nb + kGemmTile - 1) / kGemmTile;
-    const CnBatch* acc[2] = {&L.gemmE, &L.gemmF};
-    for (const CnBatch* b : acc)
-      if (b->count) {
-        lb_bgemm_kernel<<<dim3(gt * gt, b->count), kGemmThreads, 0, st>>>(nb, b->A, b->B, b->C, 1);
-        LB_CUDA(cudaGetLastError());
-      }
-    const CnBatch* fresh[2] = {&L.gemmG, &L.gemmH};
-    for (const CnBatch* b : fresh)
-      if (b->count) {
-        lb_bgemm_kernel<<<dim3(gt * gt, b->count), kGemmThreads, 0, st>>>(nb, b->A, b->B, b->C, 0);
-        LB_CUDA(cudaGetLastError());
-      }
+    // Schur updates of the even rows' D and the next level's couplings:
+    // this package's batched DMMA GEMM (landau_blas.cuh), the two products
+    // that share an A in one launch (EG before FH: both update D_k)
+    const int gt = (nb + kGemmTile - 1) / kGemmTile, gt2 = (2 * nb + kGemmTile - 1) / kGemmTile;
+    if (L.gemmEG.count) {
+      lb_bgemm_kernel<<<dim3(gt * gt2, L.gemmEG.count), kGemmThreads, 0, st>>>(
+          nb, L.gemmEG.A, L.gemmEG.B, L.gemmEG.C, 0, L.gemmEG.C2, 1);
+      LB_CUDA(cudaGetLastError());
+    }
+    if (L.gemmFH.count) {
+      lb_bgemm_kernel<<<dim3(gt * gt2, L.gemmFH.count), kGemmThreads, 0, st>>>(
+          nb, L.gemmFH.A, L.gemmFH.B, L.gemmFH.C, 1, L.gemmFH.C2, 0);
+      LB_CUDA(cudaGetLastError());
+    }
   }
   return LB_OK;
 }
@@ -1758,18 +1758,21 @@ static int cn_plan(lb_cn* cn) {
   std::vector<double*> pool;
   struct Pending {
     CnBatch* b;
-    size_t a0, b0, c0;
+    size_t a0, b0, c0, c20;
+    bool has_c2;
   };
   std::vector<Pending> pend;
   auto make = [&](CnBatch& b, const std::vector<double*>& A, const std::vector<double*>& B,
-                  const std::vector<double*>& C) {
+                  const std::vector<double*>& C, const std::vector<double*>& C2 = {}) {
     b.count = (int)std::max(A.size(), std::max(B.size(), C.size()));
-    Pending p{&b, pool.size(), 0, 0};
+    Pending p{&b, pool.size(), 0, 0, 0, !C2.empty()};
     pool.insert(pool.end(), A.begin(), A.end());
     p.b0 = pool.size();
     pool.insert(pool.end(), B.begin(), B.end());
     p.c0 = pool.size();
     pool.insert(pool.end(), C.begin(), C.end());
+    p.c20 = pool.size();
+    pool.insert(pool.end(), C2.begin(), C2.end());
     pend.push_back(p);
   };
   cn->lv.resize(Ns.size());
@@ -1778,7 +1781,7 @@ static int cn_plan(lb_cn* cn) {
     const int Nl = Ns[l], step = 1 << l;
     L.N = Nl;
     std::vector<double*> fA, lB, yB, bLA, bLx, bLy, bUA, bUx, bUy;
-    std::vector<double*> eA, eB, eC, fA2, fB2, fC2, gA, gB, gC, hA, hB, hC;
+    std::vector<double*> egA, egB, egC, egC2, fhA, fhB, fhC, fhC2;
     std::vector<double*> wLA, wLx, wLy, wUA, wUx, wUy;
     // odd rows (or the single row of the last level)
     for (int k = (Nl == 1 ? 0 : 1); k < Nl; k += 2)
@@ -1801,37 +1804,29 @@ static int cn_plan(lb_cn* cn) {
     if (Nl > 1)
       for (int k = 0; k < Nl; k += 2)  // even rows
         for (int a = 0; a < S; ++a) {
-          if (k >= 2) {
-            eA.push_back(Lb(l, k, a));
-            eB.push_back(Ub(l, k - 1, a));
-            eC.push_back(D(k * step, a));
-            gA.push_back(Lb(l, k, a));
-            gB.push_back(Lb(l, k - 1, a));
-            gC.push_back(Lb(l + 1, k / 2, a));
+          if (k >= 2) {  // L_k [P^L P^U]_{k-1}: -> L_{l+1}[k/2] (beta 0), D_k -= (beta 1)
+            egA.push_back(Lb(l, k, a));
+            egB.push_back(Lb(l, k - 1, a));
+            egC.push_back(Lb(l + 1, k / 2, a));
+            egC2.push_back(D(k * step, a));
             wLA.push_back(Lb(l, k, a));
             wLx.push_back(V((k - 1) * step, a));
             wLy.push_back(V(k * step, a));
           }
-          if (k + 1 < Nl) {
-            fA2.push_back(Ub(l, k, a));
-            fB2.push_back(Lb(l, k + 1, a));
-            fC2.push_back(D(k * step, a));
+          if (k + 1 < Nl) {  // U_k [P^L P^U]_{k+1}: D_k -= (beta 1), -> U_{l+1}[k/2] (beta 0) if it exists
+            fhA.push_back(Ub(l, k, a));
+            fhB.push_back(Lb(l, k + 1, a));
+            fhC.push_back(D(k * step, a));
+            fhC2.push_back(k + 2 < Nl ? Ub(l + 1, k / 2, a) : nullptr);
             wUA.push_back(Ub(l, k, a));
             wUx.push_back(V((k + 1) * step, a));
             wUy.push_back(V(k * step, a));
           }
-          if (k + 2 < Nl) {
-            hA.push_back(Ub(l, k, a));
-            hB.push_back(Ub(l, k + 1, a));
-            hC.push_back(Ub(l + 1, k / 2, a));
-          }
         }
     make(L.getrf, fA, {}, {});
     make(L.getrsL, fA.size() && Nl > 1 ? fA : std::vector<double*>{}, lB, {});
-    make(L.gemmE, eA, eB, eC);
-    make(L.gemmF, fA2, fB2, fC2);
-    make(L.gemmG, gA, gB, gC);
-    make(L.gemmH, hA, hB, hC);
+    make(L.gemmEG, egA, egB, egC, egC2);
+    make(L.gemmFH, fhA, fhB, fhC, fhC2);
     make(L.solveY, {}, yB, {});
     make(L.fwdL, wLA, wLx, wLy);
     make(L.fwdU, wUA, wUx, wUy);
@@ -1852,6 +1847,7 @@ static int cn_plan(lb_cn* cn) {
     p.b->A = dpool + p.a0;
     p.b->B = dpool + p.b0;
     p.b->C = dpool + p.c0;
+    p.b->C2 = p.has_c2 ? dpool + p.c20 : nullptr;
   }
   return LB_OK;
 }

@@ -2,10 +2,12 @@
 // cyclic reduction (landau_b200.cu, cn_factor_issue / cn_solve_issue) on
 // this package's own kernels, replacing cuBLAS gemmBatched / gemvBatched:
 //
-//  * lb_bgemm_kernel: C_b = beta C_b - A_b B_b for a batch of n x n
-//    column-major blocks given by pointer arrays (the reduction's Schur
-//    updates D -= L P^U + U P^L and its new couplings -L P^L, -U P^U).  One
-//    CTA per (64 x 64 tile of C, matrix); A and B tiles of 16 k-columns are
+//  * lb_bgemm_kernel: [C0 | C1] = [b0 C0 | b1 C1] - A [B | B'] for a batch
+//    of n x n column-major blocks given by pointer arrays, B' the block
+//    after B (the reduction's products sharing A: L_k [P^L P^U]_{k-1} gives
+//    the next level's coupling -L P^L and the Schur update D_k -= L P^U;
+//    U_k [P^L P^U]_{k+1} gives D_k -= U P^L and -U P^U).  One CTA per
+//    (64 x 64 tile of the product, matrix); A and B tiles of 16 k-columns are
 //    double-buffered into shared memory by cp.async; four warps, each a
 //    32 x 32 sub-tile of 4 x 4 FP64 MMA tiles (mma.sync.m8n8k4.f64, SASS
 //    DMMA) with the accumulators in registers.  Edge tiles are zero-padded.
@@ -24,7 +26,8 @@ constexpr int kGemmLdB = kGemmKT + 4;     // B tile [64][KT + 4] (column-major)
 
 __device__ __forceinline__ void gemm_load_tile(double* __restrict__ As, double* __restrict__ Bs,
                                                const double* __restrict__ A, const double* __restrict__ B,
-                                               int n, int i0, int j0, int k0, bool even, int tid) {
+                                               int n, int nc, int i0, int j0, int k0, bool even, int tid) {
+  // A: n x n; B: n x nc (nc = n or 2n), both column-major with ld n
   // A[i0 .. i0+64, k0 .. k0+16]: per k, 64 contiguous rows
   if (even) {
     for (int t = tid; t < kGemmKT * (kGemmTile / 2); t += kGemmThreads) {
@@ -43,10 +46,10 @@ __device__ __forceinline__ void gemm_load_tile(double* __restrict__ As, double* 
       const int jj = t / (kGemmKT / 2), kk = 2 * (t % (kGemmKT / 2));
       const int j = j0 + jj, k = k0 + kk;
       double* dst = Bs + jj * kGemmLdB + kk;
-      if (j < n && k + 1 < n) {
+      if (j < nc && k + 1 < n) {
         cp_async16(dst, B + (size_t)j * n + k);
       } else {
-        dst[0] = (j < n && k < n) ? B[(size_t)j * n + k] : 0.0;
+        dst[0] = (j < nc && k < n) ? B[(size_t)j * n + k] : 0.0;
         dst[1] = 0.0;
       }
     }
@@ -62,24 +65,34 @@ __device__ __forceinline__ void gemm_load_tile(double* __restrict__ As, double* 
       const int jj = t / kGemmKT, kk = t % kGemmKT;
       const int j = j0 + jj, k = k0 + kk;
       double* dst = Bs + jj * kGemmLdB + kk;
-      if (j < n && k < n) cp_async8(dst, B + (size_t)j * n + k);
+      if (j < nc && k < n) cp_async8(dst, B + (size_t)j * n + k);
       else *dst = 0.0;
     }
   }
   cp_async_commit();
 }
 
+// [C0_b | C1_b] = [beta0 C0_b | beta1 C1_b] - A_b [B_b | B_b + n^2]: A n x n,
+// B the n x 2n pair of adjacent blocks (column-major, ld n), the product's
+// first n columns into C0, the last n into C1 (C1 null: those columns are
+// skipped).  The cyclic reduction's two products that share an A -- e.g.
+// L_k P^L (the next level's coupling, beta 0) and L_k P^U (the Schur update
+// of D_k, beta 1) -- are one launch reading A once.
 __global__ void __launch_bounds__(kGemmThreads) lb_bgemm_kernel(int n, double* const* __restrict__ As_,
                                                                 double* const* __restrict__ Bs_,
-                                                                double* const* __restrict__ Cs_, int beta) {
+                                                                double* const* __restrict__ C0s_, int beta0,
+                                                                double* const* __restrict__ C1s_, int beta1) {
   __shared__ __align__(16) double As[2][kGemmKT * kGemmLdA];
   __shared__ __align__(16) double Bs[2][kGemmTile * kGemmLdB];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int tiles = (n + kGemmTile - 1) / kGemmTile;
   const int i0 = (blockIdx.x % tiles) * kGemmTile, j0 = (blockIdx.x / tiles) * kGemmTile;
+  double* __restrict__ C0 = C0s_[blockIdx.y];
+  double* __restrict__ C1 = C1s_ ? C1s_[blockIdx.y] : nullptr;
+  if (j0 >= n && !C1) return;
+  const int nc = C1 ? 2 * n : n;  // product columns computed
   const double* __restrict__ A = As_[blockIdx.y];
   const double* __restrict__ B = Bs_[blockIdx.y];
-  double* __restrict__ C = Cs_[blockIdx.y];
   const bool even = (n & 1) == 0;
   const int wr = (warp & 1) * 32, wc = (warp >> 1) * 32;  // warp sub-tile
   const int lr = lane >> 2, lk = lane & 3;
@@ -89,10 +102,10 @@ __global__ void __launch_bounds__(kGemmThreads) lb_bgemm_kernel(int n, double* c
 #pragma unroll
     for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
   const int nk = (n + kGemmKT - 1) / kGemmKT;
-  gemm_load_tile(As[0], Bs[0], A, B, n, i0, j0, 0, even, tid);
+  gemm_load_tile(As[0], Bs[0], A, B, n, nc, i0, j0, 0, even, tid);
   for (int s = 0; s < nk; ++s) {
     if (s + 1 < nk) {
-      gemm_load_tile(As[(s + 1) & 1], Bs[(s + 1) & 1], A, B, n, i0, j0, (s + 1) * kGemmKT, even, tid);
+      gemm_load_tile(As[(s + 1) & 1], Bs[(s + 1) & 1], A, B, n, nc, i0, j0, (s + 1) * kGemmKT, even, tid);
       cp_async_wait<1>();
     } else {
       cp_async_wait<0>();
@@ -123,10 +136,11 @@ __global__ void __launch_bounds__(kGemmThreads) lb_bgemm_kernel(int n, double* c
     for (int b = 0; b < 4; ++b)
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
-        const int j = j0 + wc + 8 * b + 2 * lk + e;
-        if (j >= n) continue;
-        double* c = C + (size_t)j * n + i;
-        *c = beta ? *c - acc[a][b][e] : -acc[a][b][e];
+        int j = j0 + wc + 8 * b + 2 * lk + e;
+        if (j >= nc) continue;
+        const bool second = j >= n;
+        double* c = (second ? C1 : C0) + (size_t)(second ? j - n : j) * n + i;
+        *c = (second ? beta1 : beta0) ? *c - acc[a][b][e] : -acc[a][b][e];
       }
   }
 }

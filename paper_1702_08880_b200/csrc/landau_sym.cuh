@@ -52,6 +52,9 @@ constexpr int kSymStages = LB_SYM_STAGES;  // TMA ring depth (one J tile per sta
 #define LB_SEGLEN 2
 #endif
 constexpr int kSegLenMax = LB_SEGLEN;  // partner tiles per work item (large n)
+#ifndef LB_CLAIM_FULL_FIRST
+#define LB_CLAIM_FULL_FIRST 0  // 1: claim full segments of every row before the short last ones (measured: 17.09 vs 16.92 ms, and no better G = 8 share)
+#endif
 #ifndef LB_SYM_MINB
 #define LB_SYM_MINB 5  // CTAs per SM of lb_symsweep_kernel<1> (LB_SYM_IB=0; 94 registers)
 #endif
@@ -184,6 +187,17 @@ struct SymProducer {
   // 1/G row share of a G-GPU split).  Every item still writes its own
   // partial slot: the order changes the schedule, never a bit of the result.
   __device__ int claimed_item(int c) const {
+#if !LB_CLAIM_FULL_FIRST
+    {  // row-major claim order (the item's own slot order)
+      const int nt = a.nt, L = sym_seglen(nt);
+      const int mid = (nt & 1) ? a.row1 : max(a.row0, min(a.row1, nt / 2));
+      const int tA = sym_h(a.row0 < mid ? a.row0 : mid, nt) + 1, tB = sym_h(max(mid, a.row0), nt) + 1;
+      const int sA = (tA + L - 1) / L, sB = (tB + L - 1) / L, rowsA = mid - a.row0;
+      if (c < rowsA * sA) return (c / sA) * a.nseg + c % sA;
+      c -= rowsA * sA;
+      return (rowsA + c / sB) * a.nseg + c % sB;
+    }
+#endif
     const int nt = a.nt, L = sym_seglen(nt);
     const int mid = (nt & 1) ? a.row1 : max(a.row0, min(a.row1, nt / 2));  // rows below mid: H + 1 = nt/2 + 1
     const int tA = sym_h(a.row0 < mid ? a.row0 : mid, nt) + 1;             // tiles per row, class A
