@@ -12,9 +12,10 @@ device-timed step durations).
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
 `--impl reference` times the reference algorithm's CPU implementation (the
-C restatement in oracle/, all host threads; the reference itself is Python +
-numba and is not installable on the GPU box) on a bounded outer sample of
-the same workload, rank 0 only.
+C restatement in oracle/, all host threads) on a bounded outer sample of the
+same workload, rank 0 only: the reference's own numba fused_sweep when the
+unmodified reference is installed in baseline/_ref
+(tools/install_reference.sh), else the C restatement in oracle/.
 """
 
 from __future__ import annotations
@@ -140,7 +141,28 @@ def cpu_sample(wl, seconds: float, threads: int, min_outer: int = 128):
     return k, run
 
 
+def _import_reference():
+    """The unmodified reference (axlandau, numba) installed in baseline/_ref
+    by tools/install_reference.sh, or None."""
+    ref = ROOT / "baseline" / "_ref"
+    if not (ref / "axlandau").is_dir():
+        return None
+    os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/lb_numba_cache")
+    if str(ref) not in sys.path:
+        sys.path.insert(0, str(ref))
+    try:
+        import axlandau
+    except Exception:  # numba missing or incompatible
+        return None
+    return axlandau
+
+
 def reference_arm(args):
+    """The reference's own CPU implementation of the path on this host: its
+    numba fused_sweep (kernel.py:504-536, all host threads) when the
+    unmodified reference is installed in baseline/_ref, else the C
+    restatement in oracle/ (OpenMP); a bounded sample of outer points x all
+    N inner points per step, rank 0 only."""
     rank = env_int("RANK", 0)
     if rank != 0:
         return 0
@@ -152,7 +174,35 @@ def reference_arm(args):
     threads = O.max_threads()
     # each step is a bounded sample sized so the whole run stays ~2 minutes
     per_step = min(args.ref_step_seconds, 120.0 / max(args.steps + args.warmup, 1))
-    k, run = cpu_sample(wl, per_step, threads, min_outer=16)
+    ax = _import_reference()
+    port = None
+    if ax is not None:
+        data = ax.QuadPointData(N=wl.N, r=wl.r, z=wl.z, w=wl.w, f=wl.f, df_r=wl.df_r, df_z=wl.df_z)
+        params = ax.kernel.CollisionParams(nu_hat=wl.nu_hat, mass_ratio_o=wl.mass_ratio_o)
+
+        def run(k):
+            idx = np.linspace(0, wl.N - 1, k).astype(np.int64)
+            t0 = time.perf_counter()
+            ax.fused_sweep(wl.r[idx], wl.z[idx], data, params, eps_d=wl.eps_d, workers=threads)
+            return time.perf_counter() - t0, idx, None, None
+
+        run(16)  # JIT compile + thread pool
+        t, *_ = run(64)
+        k = int(min(wl.N, max(64, 64 * per_step / max(t, 1e-9))))
+        kind = "reference"
+        sample = (f"{{k}} evenly spaced outer points x all {wl.N} inner points per step "
+                  f"(the reference's own numba fused_sweep, kernel.py:504-536, workers={threads}; "
+                  f"unmodified install in baseline/_ref)")
+        kp, runp = cpu_sample(wl, min(per_step, 4.0), threads, min_outer=16)
+        tp, *_ = runp(kp)
+        port = {"value": kp * wl.N / tp, "unit": UNIT, "cores": threads,
+                "sample": f"{kp} outer points x all {wl.N} inner points (oracle/ C restatement)"}
+    else:
+        k, run = cpu_sample(wl, per_step, threads, min_outer=16)
+        kind = "port"
+        sample = (f"{{k}} evenly spaced outer points x all {wl.N} inner points per step "
+                  f"(oracle/ C restatement of kernel.py:306-493, OpenMP {threads} threads; the "
+                  f"reference itself is not installed in baseline/_ref)")
     for _ in range(args.warmup):
         run(k)
     times = [run(k)[0] for _ in range(args.steps)]
@@ -165,13 +215,13 @@ def reference_arm(args):
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": f"cfg5 pure kernel sweep N={wl.N} S={wl.S} (BASELINE configs[4])",
                    "N": wl.N, "S": wl.S, "sample_outer_points": k},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
-                         "sample": f"{k} evenly spaced outer points x all {wl.N} inner points "
-                                   f"per step (oracle/ C restatement of kernel.py:306-493, "
-                                   f"OpenMP {threads} threads)"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": kind,
+                         "sample": sample.format(k=k)},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "model_gflops": value * flops_per_pair(wl.S) / 1e9,
     }
+    if port:
+        line["oracle_port"] = port
     print(json.dumps(line), flush=True)
     return 0
 
