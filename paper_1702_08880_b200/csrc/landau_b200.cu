@@ -348,19 +348,18 @@ template <int S>
 int sym_partial(lb_ctx* ctx, long long gthr, int rank, int world, double* tot, cudaStream_t st) {
   const int nt = ctx->sym_nt;
   const int npad = nt * kSymTile;
-  // this rank's whole row groups (landau_sym.cuh: summation order): rows
-  // I with I mod 8 in [g0, g1), local index k in increasing I
+  // this rank's whole row groups (landau_sym.cuh: summation order)
   int g0, g1;
   sym_rank_groups(rank, world, g0, g1);
-  const int ng = g1 - g0;
-  const int nrows = ng > 0 ? sym_rank_rows(nt, g0, ng) : 0;
+  const int R0 = sym_group_row(g0, nt), R1 = sym_group_row(g1, nt);
   const int nseg = sym_nseg(nt), hmax = sym_hmax(nt);
   const size_t slot = (size_t)5 * S * npad;
   int launches = 0;
   // groups without rows contribute exact zeros
   for (int g = g0; g < g1; ++g)
-    if (g >= nt) LB_CUDA(cudaMemsetAsync(tot + (size_t)(g - g0) * slot, 0, sizeof(double) * slot, st));
-  if (nrows == 0) {
+    if (sym_group_row(g, nt) == sym_group_row(g + 1, nt))
+      LB_CUDA(cudaMemsetAsync(tot + (size_t)(g - g0) * slot, 0, sizeof(double) * slot, st));
+  if (R0 >= R1) {
     ctx->last_launches = 0;
     return LB_OK;
   }
@@ -376,11 +375,11 @@ int sym_partial(lb_ctx* ctx, long long gthr, int rank, int world, double* tot, c
   per_sm = std::max(per_sm, 1);
   const size_t row_i = (size_t)nseg * 5 * S * kSymTile * sizeof(double);
   const size_t row_j = (size_t)std::max(hmax, 1) * 5 * S * kSymTile * sizeof(double);
-  const int RB = (int)std::max<size_t>(1, std::min<size_t>(nrows, partial_budget() / (row_i + row_j)));
+  const int RB = (int)std::max<size_t>(1, std::min<size_t>(R1 - R0, partial_budget() / (row_i + row_j)));
   int rc;
   if ((rc = ensure(ctx->symi, row_i * RB))) return rc;
   if ((rc = ensure(ctx->symj, row_j * RB))) return rc;
-  const int nbatch = (nrows + RB - 1) / RB;
+  const int nbatch = (R1 - R0 + RB - 1) / RB;
   if ((rc = ensure(ctx->symctr, sizeof(int) * nbatch))) return rc;
   int* ctr = static_cast<int*>(ctx->symctr.p);
   LB_CUDA(cudaMemsetAsync(ctr, 0, sizeof(int) * nbatch, st));
@@ -389,28 +388,26 @@ int sym_partial(lb_ctx* ctx, long long gthr, int rank, int world, double* tot, c
     if ((rc = ensure(ctx->symstats, 4 * sizeof(unsigned long long)))) return rc;
     stats = static_cast<unsigned long long*>(ctx->symstats.p);
   }
-  for (int k0 = 0; k0 < nrows; k0 += RB) {
-    const int k1 = std::min(nrows, k0 + RB);
+  for (int b0 = R0; b0 < R1; b0 += RB) {
+    const int b1 = std::min(R1, b0 + RB);
     SymArgs a;
     a.rec = static_cast<const double*>(ctx->symrec.p);
     a.iside = static_cast<double*>(ctx->symi.p);
     a.jside = static_cast<double*>(ctx->symj.p);
-    a.next_item = ctr + k0 / RB;
+    a.next_item = ctr + (b0 - R0) / RB;
     a.stats = stats;
     a.nt = nt;
-    a.k0 = k0;
-    a.k1 = k1;
-    a.g0 = g0;
-    a.ng = ng;
+    a.row0 = b0;
+    a.row1 = b1;
     a.nseg = nseg;
     a.hmax = hmax;
     a.gthr = gthr;
-    const long long nitems = (long long)(k1 - k0) * nseg;
+    const long long nitems = (long long)(b1 - b0) * nseg;
     const int grid = (int)std::min<long long>(nitems, (long long)ctx->num_sms * per_sm);
     sym_kernel<S>()<<<grid, sym_threads<S>(), smem, st>>>(a);
     LB_CUDA(cudaGetLastError());
-    lb_symreduce_kernel<S><<<(npad + 127) / 128, 128, 0, st>>>(a.iside, a.jside, nt, k0, k1, g0, ng, nseg,
-                                                               hmax, tot);
+    lb_symreduce_kernel<S><<<(npad + 127) / 128, 128, 0, st>>>(a.iside, a.jside, nt, b0, b1, nseg,
+                                                               hmax, g0, tot);
     LB_CUDA(cudaGetLastError());
     launches += 2;
   }

@@ -28,18 +28,16 @@
 //    segments and the j-side blocks of every row that has its tile as a
 //    partner.  No atomics: results are bitwise reproducible.
 //
-// Summation order (independent of the GPU count): the rows are dealt into
-// kSymGroups = 8 fixed row groups, row I into group I mod 8 (interleaved, so
-// every group -- hence every rank of a split -- gets an even share of the
-// data-dependent work, e.g. the near-axis rows that take the m < 0.01
-// series).  A point's total is ((T_0 + T_1) + ...) + T_7 in group order,
-// where T_g adds, by increasing row I of group g, the j-side block of row I
-// (if the point's tile is one of its partners) or, at I = the point's own
-// row, the sum of its i-side segments.  A rank of a G-GPU split owns whole
-// groups (groups 8r/G .. 8(r+1)/G - 1), computes their T_g, and the owner
-// of a point adds all eight in group order -- so every bit of K and D is
-// the same for G = 1, 2, 4, 8 (and any G <= 8), as the reference promises
-// for its `workers` (kernel.py:508-511, test_kernel.py:197-212).
+// Summation order (independent of the GPU count): the rows are cut into
+// kSymGroups = 8 fixed row groups (boundaries nt*g/8).  A point's total is
+// ((T_0 + T_1) + ...) + T_7 in group order, where T_g adds, by increasing row
+// I of group g, the j-side block of row I (if the point's tile is one of its
+// partners) or, at I = the point's own row, its i-side segments.  A rank of a
+// G-GPU split owns whole groups (groups 8r/G .. 8(r+1)/G - 1, the same rows
+// as an even split when G divides 8), computes their T_g, and the owner of a
+// point adds all eight in group order -- so every bit of K and D is the same
+// for G = 1, 2, 4, 8 (and any G <= 8), as the reference promises for its
+// `workers` (kernel.py:508-511, test_kernel.py:197-212).
 #pragma once
 #include "landau_sweep.cuh"
 
@@ -54,6 +52,9 @@ constexpr int kSymStages = LB_SYM_STAGES;  // TMA ring depth (one J tile per sta
 #define LB_SEGLEN 2
 #endif
 constexpr int kSegLenMax = LB_SEGLEN;  // partner tiles per work item (large n)
+#ifndef LB_CLAIM_FULL_FIRST
+#define LB_CLAIM_FULL_FIRST 0  // 1: claim full segments of every row before the short last ones (measured: 17.09 vs 16.92 ms, and no better G = 8 share)
+#endif
 #ifndef LB_SYM_MINB
 #define LB_SYM_MINB 5  // CTAs per SM of lb_symsweep_kernel<1> (LB_SYM_IB=0; 94 registers)
 #endif
@@ -89,23 +90,15 @@ __host__ __device__ __forceinline__ int sym_nseg(int nt) {
   return (sym_hmax(nt) + 1 + L - 1) / L;
 }
 
-// fixed row groups (row I -> group I mod 8): the outer level of every
-// point's summation order
+// fixed row groups: the outer level of every point's summation order
 constexpr int kSymGroups = 8;
+__host__ __device__ __forceinline__ int sym_group_row(int g, int nt) {
+  return (int)((long long)nt * g / kSymGroups);
+}
 // groups [g0, g1) of rank `rank` among `world` (contiguous, whole groups)
 __host__ __device__ __forceinline__ void sym_rank_groups(int rank, int world, int& g0, int& g1) {
   g0 = (int)((long long)kSymGroups * rank / world);
   g1 = (int)((long long)kSymGroups * (rank + 1) / world);
-}
-// a rank's rows in increasing order: local row k -> row I (groups [g0, g0+ng))
-__host__ __device__ __forceinline__ int sym_row(int k, int g0, int ng) {
-  return kSymGroups * (k / ng) + g0 + k % ng;
-}
-// number of rows (< nt) in groups [g0, g0+ng)
-__host__ __device__ __forceinline__ int sym_rank_rows(int nt, int g0, int ng) {
-  int c = 0;
-  for (int g = g0; g < g0 + ng; ++g) c += g < nt ? (nt - g + kSymGroups - 1) / kSymGroups : 0;
-  return c;
 }
 // device pointers of the eight group sums T_g ([5S][npad] each), in group order
 struct SymGroupPtrs {
@@ -135,8 +128,8 @@ constexpr size_t sym_smem_bytes() {
 
 struct SymArgs {
   const double* rec;  // sorted records, nt*128 x RS (padding records are inert)
-  double* iside;      // [k - k0][nseg][5S][128]   (k: the rank's local row index)
-  double* jside;      // [k - k0][hmax][5S][128]
+  double* iside;      // [row - row0][nseg][5S][128]
+  double* jside;      // [row - row0][hmax][5S][128]
   int* next_item;     // work counter (zero at launch): items past the first wave
   // optional execution counters (species-collapsed kernel; NULL: off):
   // [0] off-diagonal thread-steps, [1] diagonal thread-steps, [2] thread-steps
@@ -144,11 +137,8 @@ struct SymArgs {
   // instruction counts read from this kernel's SASS they give the executed
   // FP64 work of a launch (bench.py, tools/sass_fp64.py)
   unsigned long long* stats;
-  int nt, k0, k1;     // this batch: the rank's local rows [k0, k1)
-  int g0, ng;         // the rank's groups [g0, g0 + ng): row I = sym_row(k, g0, ng)
-  int nseg, hmax;
+  int nt, row0, row1, nseg, hmax;
   long long gthr;
-  __device__ int row(int item) const { return sym_row(k0 + item / nseg, g0, ng); }
 };
 
 // Producer of both symmetric sweeps (thread 0 of the CTA): walks the (item,
@@ -170,18 +160,59 @@ struct SymProducer {
   uint32_t p_k = 0;
   bool p_done = false;
 
+  long long nclaim;  // items that exist (rows x their segments); nitems = rows x nseg slots
+
   __device__ SymProducer(const SymArgs& args, long long n, double* sm, uint64_t* f, uint64_t* e, int* si,
                          int* sd)
-      : a(args), nitems(n), smem(sm), full(f), empty(e), stage_item(si), stage_d(sd),
-        p_item(blockIdx.x) {}
+      : a(args), nitems(n), smem(sm), full(f), empty(e), stage_item(si), stage_d(sd) {
+    const int nt = a.nt, L = sym_seglen(nt);
+    const int mid = (nt & 1) ? a.row1 : max(a.row0, min(a.row1, nt / 2));
+    const int tA = sym_h(a.row0 < mid ? a.row0 : mid, nt) + 1, tB = sym_h(max(mid, a.row0), nt) + 1;
+    nclaim = (long long)(mid - a.row0) * ((tA + L - 1) / L) + (long long)(a.row1 - mid) * ((tB + L - 1) / L);
+    p_item = (int)blockIdx.x < nclaim ? claimed_item((int)blockIdx.x) : (int)nitems;
+  }
 
-  // item = (local row) nseg + segment; segments past a row's partners are empty
   __device__ void seg_range(int item, int& I, int& d0, int& d1) const {
-    I = a.row(item);
+    I = a.row0 + item / a.nseg;
     const int seg = item % a.nseg;
     const int L = sym_seglen(a.nt);
     d0 = seg * L;
     d1 = min(sym_h(I, a.nt) + 1, d0 + L);
+  }
+
+  // Claim order -> work item (row-major slot (I - row0) nseg + seg).  The
+  // full L-tile segments of all rows come first, then the short last
+  // segments (rows whose H + 1 tiles are not a multiple of L), so the final
+  // wave is made of the smallest items (a shorter tail, most visible on the
+  // 1/G row share of a G-GPU split).  Every item still writes its own
+  // partial slot: the order changes the schedule, never a bit of the result.
+  __device__ int claimed_item(int c) const {
+#if !LB_CLAIM_FULL_FIRST
+    {  // row-major claim order (the item's own slot order)
+      const int nt = a.nt, L = sym_seglen(nt);
+      const int mid = (nt & 1) ? a.row1 : max(a.row0, min(a.row1, nt / 2));
+      const int tA = sym_h(a.row0 < mid ? a.row0 : mid, nt) + 1, tB = sym_h(max(mid, a.row0), nt) + 1;
+      const int sA = (tA + L - 1) / L, sB = (tB + L - 1) / L, rowsA = mid - a.row0;
+      if (c < rowsA * sA) return (c / sA) * a.nseg + c % sA;
+      c -= rowsA * sA;
+      return (rowsA + c / sB) * a.nseg + c % sB;
+    }
+#endif
+    const int nt = a.nt, L = sym_seglen(nt);
+    const int mid = (nt & 1) ? a.row1 : max(a.row0, min(a.row1, nt / 2));  // rows below mid: H + 1 = nt/2 + 1
+    const int tA = sym_h(a.row0 < mid ? a.row0 : mid, nt) + 1;             // tiles per row, class A
+    const int tB = sym_h(max(mid, a.row0), nt) + 1;                         // class B (rows >= mid)
+    const int rowsA = mid - a.row0, rowsB = a.row1 - mid;
+    const int fA = tA / L, fB = tB / L;
+    const long long nfA = (long long)rowsA * fA, nfB = (long long)rowsB * fB;
+    if (c < nfA) return (c / fA) * a.nseg + c % fA;
+    c -= (int)nfA;
+    if (c < nfB) return (rowsA + c / fB) * a.nseg + c % fB;
+    c -= (int)nfB;
+    const int sA = (tA % L) ? rowsA : 0;  // short segments: class A rows first, then B
+    if (c < sA) return c * a.nseg + fA;
+    c -= sA;
+    return (rowsA + c) * a.nseg + fB;
   }
 
   __device__ void issue_next() {
@@ -191,7 +222,9 @@ struct SymProducer {
       seg_range(p_item, I, d0, d1);
       if (p_d < 0) p_d = d0;
       if (p_d < d1) break;
-      p_item = (int)gridDim.x + atomicAdd(a.next_item, 1);  // segment done: claim the next
+      // segment done: claim the next one
+      const int c = (int)gridDim.x + atomicAdd(a.next_item, 1);
+      p_item = c < nclaim ? claimed_item(c) : (int)nitems;
       p_d = -1;
     }
     const uint32_t s = p_k % kSymStages;
@@ -206,7 +239,7 @@ struct SymProducer {
     stage_item[s] = p_item;
     stage_d[s] = p_d;
     const int J = (I + p_d) % a.nt;
-    LB_DCHECK(I >= 0 && I < a.nt && p_d >= 0 && p_d <= sym_h(I, a.nt) && J >= 0 && J < a.nt);
+    LB_DCHECK(I >= a.row0 && I < a.row1 && p_d >= 0 && p_d <= sym_h(I, a.nt) && J >= 0 && J < a.nt);
     const uint32_t bytes = kSymTile * RS * sizeof(double);
     mbar_expect_tx(&full[s], bytes);
     bulk_g2s(smem + s * (kSymTile * RS), a.rec + (size_t)J * kSymTile * RS, bytes, &full[s]);
@@ -236,7 +269,8 @@ __global__ void __launch_bounds__(kSymTile, sym_min_blocks(S)) lb_symsweep_kerne
   double* jred = lb_smem + kSymStages * kSymTile * RS + (2 << LB_LOGT_BITS);  // [2][NW][32][5S]
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const long long nitems = (long long)(a.k1 - a.k0) * a.nseg;
+  const int nrows = a.row1 - a.row0;
+  const long long nitems = (long long)nrows * a.nseg;
 
   for (int t = tid; t < (2 << LB_LOGT_BITS); t += kSymTile)
     lb_smem[kSymStages * kSymTile * RS + t] = c_logt[t];
@@ -258,7 +292,7 @@ __global__ void __launch_bounds__(kSymTile, sym_min_blocks(S)) lb_symsweep_kerne
   double acc[S][5];
   int cur = -1, I = 0;
   auto flush_iside = [&]() {
-    double* dst = a.iside + (size_t)cur * (5 * S) * kSymTile + tid;  // slot = item
+    double* dst = a.iside + ((size_t)(I - a.row0) * a.nseg + (cur % a.nseg)) * (5 * S) * kSymTile + tid;
 #pragma unroll
     for (int b = 0; b < S; ++b)
 #pragma unroll
@@ -273,7 +307,7 @@ __global__ void __launch_bounds__(kSymTile, sym_min_blocks(S)) lb_symsweep_kerne
     if (item != cur) {
       if (cur >= 0) flush_iside();
       cur = item;
-      I = a.row(item);
+      I = a.row0 + item / a.nseg;
       load_point<S>(a.rec + ((size_t)I * kSymTile + tid) * RS, o, gi);
 #pragma unroll
       for (int b = 0; b < S; ++b)
@@ -343,7 +377,7 @@ __global__ void __launch_bounds__(kSymTile, sym_min_blocks(S)) lb_symsweep_kerne
             for (int q = 0; q < 5; ++q) dst[b * 5 + q] = jacc[b][q];
           __syncthreads();
           LB_DCHECK(d >= 1 && d <= a.hmax);
-          double* out = a.jside + ((size_t)(cur / a.nseg) * a.hmax + (d - 1)) * (5 * S) * kSymTile +
+          double* out = a.jside + ((size_t)(I - a.row0) * a.hmax + (d - 1)) * (5 * S) * kSymTile +
                         jb * 32;
           for (int v = tid; v < 32 * 5 * S; v += kSymTile) {
             const int c = v >> 5, jj = v & 31;
@@ -395,7 +429,8 @@ __global__ void __launch_bounds__(kIbThreads, LB_IB_MINB) lb_symsweep_ib_kernel(
 #endif
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const long long nitems = (long long)(a.k1 - a.k0) * a.nseg;
+  const int nrows = a.row1 - a.row0;
+  const long long nitems = (long long)nrows * a.nseg;
   for (int t = tid; t < (2 << LB_LOGT_BITS); t += kIbThreads)
     lb_smem[kSymStages * kSymTile * RS + t] = c_logt[t];
   if (tid == 0) {
@@ -420,8 +455,8 @@ __global__ void __launch_bounds__(kIbThreads, LB_IB_MINB) lb_symsweep_ib_kernel(
   auto flush_iside = [&]() {
 #pragma unroll
     for (int ib = 0; ib < 2; ++ib) {
-      LB_DCHECK(pidx(ib) < kSymTile && I >= 0 && I < a.nt);
-      double* dst = a.iside + (size_t)cur * (5 * S) * kSymTile + pidx(ib);  // slot = item
+      LB_DCHECK(pidx(ib) < kSymTile && I >= a.row0 && I < a.row1);
+      double* dst = a.iside + ((size_t)(I - a.row0) * a.nseg + (cur % a.nseg)) * (5 * S) * kSymTile + pidx(ib);
 #pragma unroll
       for (int b = 0; b < S; ++b)
 #pragma unroll
@@ -437,7 +472,7 @@ __global__ void __launch_bounds__(kIbThreads, LB_IB_MINB) lb_symsweep_ib_kernel(
     if (item != cur) {
       if (cur >= 0) flush_iside();
       cur = item;
-      I = a.row(item);
+      I = a.row0 + item / a.nseg;
 #pragma unroll
       for (int ib = 0; ib < 2; ++ib) {
         load_point<S>(a.rec + ((size_t)I * kSymTile + pidx(ib)) * RS, o[ib], gi[ib]);
@@ -593,7 +628,7 @@ __global__ void __launch_bounds__(kIbThreads, LB_IB_MINB) lb_symsweep_ib_kernel(
           for (int q = 0; q < 5; ++q) dst[b * 5 + q] = jacc[b][q];
         __syncthreads();
         LB_DCHECK(d >= 1 && d <= a.hmax);
-        double* out = a.jside + ((size_t)(cur / a.nseg) * a.hmax + (d - 1)) * (5 * S) * kSymTile + jb * 32;
+        double* out = a.jside + ((size_t)(I - a.row0) * a.hmax + (d - 1)) * (5 * S) * kSymTile + jb * 32;
         for (int v = tid; v < 32 * 5 * S; v += kIbThreads) {
           const int c = v >> 5, jj = v & 31;
           double x = slot[(size_t)jj * (5 * S) + c];
@@ -623,17 +658,17 @@ __global__ void __launch_bounds__(kIbThreads, LB_IB_MINB) lb_symsweep_ib_kernel(
   }
 }
 
-// Fixed-order reduction of one batch (the rank's local rows [k0, k1)) into
-// the group sums T_g (tot + (g - g0) [5S][npad], SoA) of the rank's groups:
-// per point, by increasing row I of group g, the j-side block of row I when
-// the point's tile P is one of its partners (d = P - I mod nt in 1..H(I))
-// or, at I = P, the sum of the point's own i-side segments (added among
-// themselves in segment order).  A group's sums start from zero in the batch
-// holding its first row.  The order depends only on n, never on the
-// batching or on which rank runs the group (landau_sym.cuh header).
+// Fixed-order reduction of one row batch [row0, row1) into the group sums
+// T_g (tot + (g - gbase) [5S][npad], SoA) of every group the batch touches:
+// per point, by increasing row I within the group, the j-side block of row
+// I when the point's tile P is one of its partners (d = P - I mod nt in
+// 1..H(I)) or, at I = P, the sum of the point's own i-side segments (added
+// among themselves in segment order).  A group's first
+// batch starts its sums from zero.  The order depends only on n, never on
+// the batching or on which rank runs the group (landau_sym.cuh header).
 template <int S>
 __global__ void lb_symreduce_kernel(const double* __restrict__ iside, const double* __restrict__ jside,
-                                    int nt, int k0, int k1, int g0, int ng, int nseg, int hmax,
+                                    int nt, int row0, int row1, int nseg, int hmax, int gbase,
                                     double* __restrict__ tot) {
   const int p = blockIdx.x * blockDim.x + threadIdx.x;
   const int npad = nt * kSymTile;
@@ -643,14 +678,13 @@ __global__ void lb_symreduce_kernel(const double* __restrict__ iside, const doub
 #define LB_RED_G 8
 #endif
   constexpr int G = LB_RED_G;
-  // the point's own row: local index kp when its group is this rank's
-  const int gP = P % kSymGroups;
-  const int kp = (gP >= g0 && gP < g0 + ng) ? (P / kSymGroups) * ng + (gP - g0) : -1;
-  const bool has_own = kp >= k0 && kp < k1;
+  // the point's own i-side segments (its row's partners, in segment order),
+  // added into the group sum at I = P
   double own[5 * S];
+  const bool has_own = P >= row0 && P < row1;
   if (has_own) {
     const int nsg = min(nseg, sym_h(P, nt) / sym_seglen(nt) + 1);
-    const double* src = iside + (size_t)(kp - k0) * nseg * (5 * S) * kSymTile + t;
+    const double* src = iside + (size_t)(P - row0) * nseg * (5 * S) * kSymTile + t;
 #pragma unroll
     for (int c = 0; c < 5 * S; ++c) own[c] = src[(size_t)c * kSymTile];
 #pragma unroll 1
@@ -672,54 +706,47 @@ __global__ void lb_symreduce_kernel(const double* __restrict__ iside, const doub
     }
   }
 #pragma unroll 1
-  for (int gl = 0; gl < ng; ++gl) {
-    // the group's first local row in the batch (local rows of group gl: k = gl mod ng)
-    const int kstart = k0 + ((gl - k0 % ng) % ng + ng) % ng;
-    if (kstart >= k1) continue;
-    double* T = tot + (size_t)gl * (5 * S) * npad;
+  for (int g = 0; g < kSymGroups; ++g) {
+    const int gb0 = sym_group_row(g, nt), gb1 = sym_group_row(g + 1, nt);
+    const int lo = max(row0, gb0), hi = min(row1, gb1);
+    if (lo >= hi) continue;
+    LB_DCHECK(g >= gbase);
+    double* T = tot + (size_t)(g - gbase) * (5 * S) * npad;
     double v[5 * S];
 #pragma unroll
-    for (int c = 0; c < 5 * S; ++c) v[c] = kstart == gl ? 0.0 : T[(size_t)c * npad + p];
-    // rows I = sym_row(k), k = kstart, kstart + ng, ...: I steps by 8 and
-    // d = (P - I) mod nt by -8; rows in groups of G: the loads are issued
-    // before the ordered adds (conditions uniform across the block)
-    int I = sym_row(kstart, g0, ng);
-    int d = (P - I) % nt;
+    for (int c = 0; c < 5 * S; ++c) v[c] = lo == gb0 ? 0.0 : T[(size_t)c * npad + p];
+    // d = (P - I) mod nt, stepped down with I (no integer division per row);
+    // rows in groups of G: the group's loads are issued before its adds, which
+    // stay in increasing-I order (the conditions are uniform across the block)
+    int d = (P - lo) % nt;
     if (d < 0) d += nt;
 #pragma unroll 1
-    for (int kb = kstart; kb < k1; kb += G * ng) {
+    for (int I0 = lo; I0 < hi; I0 += G) {
       double x[G][5 * S];
-      bool on[G], me[G];
+      bool on[G];
 #pragma unroll
-      for (int q = 0; q < G; ++q) {
-        const int k = kb + q * ng;
-        const int Iq = I + q * kSymGroups;
-        int dq = d - q * kSymGroups;
-        dq %= nt;
-        if (dq < 0) dq += nt;
-        on[q] = k < k1 && dq >= 1 && dq <= sym_h(Iq, nt);
-        me[q] = has_own && k < k1 && Iq == P;
-        if (on[q]) {
-          LB_DCHECK(dq >= 1 && dq <= hmax);
-          const double* src = jside + ((size_t)(k - k0) * hmax + (dq - 1)) * (5 * S) * kSymTile + t;
+      for (int k = 0; k < G; ++k) {
+        const int I = I0 + k;
+        on[k] = I < hi && d >= 1 && d <= sym_h(I, nt);
+        if (on[k]) {
+          LB_DCHECK(d >= 1 && d <= hmax);
+          const double* src = jside + ((size_t)(I - row0) * hmax + (d - 1)) * (5 * S) * kSymTile + t;
 #pragma unroll
-          for (int c = 0; c < 5 * S; ++c) x[q][c] = src[(size_t)c * kSymTile];
+          for (int c = 0; c < 5 * S; ++c) x[k][c] = src[(size_t)c * kSymTile];
         }
+        d = d == 0 ? nt - 1 : d - 1;
       }
 #pragma unroll
-      for (int q = 0; q < G; ++q) {
-        if (me[q]) {
+      for (int k = 0; k < G; ++k) {
+        if (has_own && I0 + k == P && P < hi) {
 #pragma unroll
           for (int c = 0; c < 5 * S; ++c) v[c] = __dadd_rn(v[c], own[c]);
         }
-        if (on[q]) {
+        if (on[k]) {
 #pragma unroll
-          for (int c = 0; c < 5 * S; ++c) v[c] = __dadd_rn(v[c], x[q][c]);
+          for (int c = 0; c < 5 * S; ++c) v[c] = __dadd_rn(v[c], x[k][c]);
         }
       }
-      I += G * kSymGroups;
-      d = (d - G * kSymGroups) % nt;
-      if (d < 0) d += nt;
     }
 #pragma unroll
     for (int c = 0; c < 5 * S; ++c) T[(size_t)c * npad + p] = v[c];

@@ -11,8 +11,8 @@ at S = 2, 5.2 MB at N = 2^16.  Then, either
  * symmetric path (outer set == inner set, the default here): every rank
    Morton-orders all records identically and evaluates its share of the
    unordered tile pairs (each pair once, feeding both points): whole row
-   groups of the fixed 8-group split (row I in group I mod 8, `lb_sym_groups`),
-   one sum per group and point.  One all-gather replicates the group sums (2.6 MB per group at
+   groups of the fixed 8-group split (`lb_sym_groups`), one sum per group and
+   point.  One all-gather replicates the group sums (2.6 MB per group at
    N = 2^16), and each rank adds, for its own points only, all eight in group
    order and applies the coupling -- so K and D are bitwise the same for any
    GPU count <= 8 (the reference promises bitwise invariance to `workers`,

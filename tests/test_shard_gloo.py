@@ -98,14 +98,15 @@ def test_sharded_equals_single(tmp_path, world, n, align):
 # ---------------------------------------------------------------- symmetric path
 def _sym_fns(wl):
     """numpy stand-ins for the symmetric path's three device steps: the sum of
-    row group g (the points of the 128-point tiles I with I mod 8 == g as
-    inner points) is the oracle sweep of every point against that inner
-    subset, stored as the 5S accumulators (K_r, K_z, D_rr, D_rz, D_zz per
-    species); the combine adds the eight groups in group order."""
+    row group g (points [128 B(g), 128 B(g+1)) as inner points, B(g) =
+    nt g / 8) is the oracle sweep of every point against that inner subset,
+    stored as the 5S accumulators (K_r, K_z, D_rr, D_rz, D_zz per species);
+    the combine adds the eight groups in group order."""
     from oracle import oracle as O
     from paper_1702_08880_b200.shard import SYM_GROUPS, sym_rank_groups
 
     n, S = wl.N, wl.S
+    nt = -(-n // 128)
 
     def prepare(rec):
         pass
@@ -114,14 +115,14 @@ def _sym_fns(wl):
         rank, world = dist.get_rank(), dist.get_world_size()
         g0, g1 = sym_rank_groups(rank, world)
         for g in range(g0, g1):
-            sel = np.nonzero((np.arange(n) // 128) % SYM_GROUPS == g)[0]
+            lo, hi = 128 * (nt * g // SYM_GROUPS), min(n, 128 * (nt * (g + 1) // SYM_GROUPS))
             tot[g - g0].zero_()
-            if sel.size == 0:
+            if lo >= hi:
                 continue
-            K, D = O.fused_sweep(wl.r, wl.z, wl.r[sel], wl.z[sel], wl.w[sel],
-                                 np.ascontiguousarray(wl.f[:, sel]),
-                                 np.ascontiguousarray(wl.df_r[:, sel]),
-                                 np.ascontiguousarray(wl.df_z[:, sel]), wl.nu_hat,
+            K, D = O.fused_sweep(wl.r, wl.z, wl.r[lo:hi], wl.z[lo:hi], wl.w[lo:hi],
+                                 np.ascontiguousarray(wl.f[:, lo:hi]),
+                                 np.ascontiguousarray(wl.df_r[:, lo:hi]),
+                                 np.ascontiguousarray(wl.df_z[:, lo:hi]), wl.nu_hat,
                                  wl.mass_ratio_o, eps_d=wl.eps_d, threads=1)
             acc = np.concatenate([K, D.reshape(n, S, 4)[:, :, [0, 1, 3]]], axis=2)  # (n, S, 5)
             tot[g - g0, :, :n] = torch.from_numpy(acc.reshape(n, 5 * S).T.copy())
