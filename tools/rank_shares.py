@@ -54,7 +54,10 @@ def main():
                         "share": single / G / slow, "groups": [sym_rank_groups(r, G) for r in range(G)]}
         print(f"G={G}: slowest rank {slow:.3f} ms vs ideal {single / G:.3f} ms -> "
               f"{100 * single / G / slow:.1f} % ({', '.join(f'{t:.3f}' for t in times)})")
-    print(json.dumps(out))
+    try:
+        print(json.dumps(out), flush=True)
+    except BrokenPipeError:  # output piped into head
+        pass
 
 
 if __name__ == "__main__":
