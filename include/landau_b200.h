@@ -166,6 +166,13 @@ int lb_sample_state_dev(lb_ctx *ctx, const lb_mesh *mesh, int S, int c0, int c1,
                         const double *coeffs, double *r, double *z, double *w, double *f,
                         double *df_r, double *df_z, void *stream);
 
+/* Host-pointer `sample_state` (fem.py:170-199) for the whole mesh: coeffs
+ * (S, n_free) host in, data_out ((3+3S) x 9*ncell host: r, z, w, f, df_r,
+ * df_z) out -- bitwise the reference's (the kernel reproduces numpy's einsum
+ * order). */
+int lb_sample_state(lb_ctx *ctx, const lb_mesh *mesh, int S, const double *coeffs,
+                    double *data_out);
+
 /* State-level operator: replaces solver._assemble_at (solver.py:81-84) =
  * sample_state + assemble_collision.  Host coeffs (S, n_free) in, CSR
  * values csr_out (S, nslots) out; data_out ((3+3S) x 9*ncell: r, z, w, f,

@@ -52,6 +52,7 @@ SIGNATURES = {
     "lb_elements_csr": (_i, [_vp, _vp, _i, _dp, _dp, _dp, _dp]),
     "lb_operator_partial_dev": (_i, [_vp, _vp, _i, _i, _i, _vp, _vp, _vp, _vp, _vp]),
     "lb_mesh_set_geometry": (_i, [_vp, _dp, _dp, _dp, _ip, _i, _i, _ip, _ip, _dp]),
+    "lb_sample_state": (_i, [_vp, _vp, _i, _dp, _dp]),
     "lb_sample_state_dev": (_i, [_vp, _vp, _i, _i, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
     "lb_assemble_state": (_i, [_vp, _vp, _i, _dp, _dp, _dp, _d, _dp, _dp, _dp]),
     "lb_assemble_csr": (_i, [_vp, _vp, _i, _dp, _dp, _dp, _dp, _dp, _dp, _dp, _dp, _d, _dp,

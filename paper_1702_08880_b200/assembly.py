@@ -260,31 +260,23 @@ def assemble_at(mesh, ref, state, params, eps_d: float | None = None,
 
 def sample_state(mesh, ref, state):
     """Device `sample_state` (fem.py:170-199): QuadPointData of the state at
-    all quadrature points (r, z, w bitwise the reference's)."""
-    import torch
-
+    all quadrature points, bitwise the reference's (`lb_sample_state`, host
+    pointers in and out)."""
     dm = device_mesh(mesh, ref)
     if not dm.has_geometry:
         raise ValueError("mesh/ref lack origins/qpts/qwts needed for device sampling")
     c = _coeffs(state, None, dm.n_free)
     S = c.shape[0]
     n = 9 * dm.ncell
-    dev = torch.device("cuda", _lib.current_device())
-    dc = torch.from_numpy(c).to(dev)
-    out = torch.empty((3 + 3 * S, n), dtype=torch.float64, device=dev)
+    out = np.empty((3 + 3 * S, n))
     if n:
-        ctx = _lib.context(dev.index)
-        o = out.data_ptr()
-        row = 8 * n
-        _lib.check(_lib.load().lb_sample_state_dev(
-            ctx.handle, dm.handle, S, 0, dm.ncell, dc.data_ptr(), o, o + row, o + 2 * row,
-            o + 3 * row, o + (3 + S) * row, o + (3 + 2 * S) * row,
-            torch.cuda.current_stream(dev).cuda_stream))
-    h = out.cpu().numpy()
+        ctx = _lib.context()
+        _lib.check(_lib.load().lb_sample_state(ctx.handle, dm.handle, S, _lib.dptr(c),
+                                               _lib.dptr(out)))
     from .kernel import QuadPointData
 
-    return QuadPointData(N=n, r=h[0], z=h[1], w=h[2], f=h[3:3 + S], df_r=h[3 + S:3 + 2 * S],
-                         df_z=h[3 + 2 * S:3 + 3 * S])
+    return QuadPointData(N=n, r=out[0], z=out[1], w=out[2], f=out[3:3 + S],
+                         df_r=out[3 + S:3 + 2 * S], df_z=out[3 + 2 * S:3 + 3 * S])
 
 
 def union_point_data(datas):

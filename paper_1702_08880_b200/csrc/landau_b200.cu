@@ -1116,6 +1116,32 @@ int lb_sample_state_dev(lb_ctx* ctx, const lb_mesh* m, int S, int c0, int c1, co
   return LB_OK;
 }
 
+int lb_sample_state(lb_ctx* ctx, const lb_mesh* m, int S, const double* coeffs, double* data_out) {
+  int rc = use_ctx(ctx);
+  if (rc) return rc;
+  if ((rc = check_species(S))) return rc;
+  if (!m || !m->cell_nodes) return fail(LB_EINVAL, "mesh has no sampling geometry (lb_mesh_set_geometry)");
+  if (m->device != ctx->device) return fail(LB_EINVAL, "mesh handle on another device");
+  if (!coeffs || !data_out) return fail(LB_EINVAL, "null argument");
+  const int n = 9 * m->ncell;
+  if (n == 0) return LB_OK;
+  const size_t nco = (size_t)S * m->n_free, nout = (size_t)(3 + 3 * S) * n;
+  if ((rc = ensure(ctx->in, (nco + nout) * sizeof(double)))) return rc;
+  double* dco = static_cast<double*>(ctx->in.p);
+  double* o = dco + nco;
+  cudaStream_t st = ctx->stream;
+  LB_CUDA(cudaMemcpyAsync(dco, coeffs, sizeof(double) * nco, cudaMemcpyHostToDevice, st));
+  lb_sample_kernel<<<(n + 127) / 128, 128, 0, st>>>(0, m->ncell, S, m->n_free, m->origins, m->sizes, m->qgeo,
+                                                   m->basis, m->cell_nodes, m->P_ptr, m->P_idx, m->P_w, dco,
+                                                   o, o + n, o + 2 * (size_t)n, o + 3 * (size_t)n,
+                                                   o + (3 + S) * (size_t)n, o + (3 + 2 * S) * (size_t)n);
+  LB_CUDA(cudaGetLastError());
+  LB_CUDA(cudaMemcpyAsync(data_out, o, sizeof(double) * nout, cudaMemcpyDeviceToHost, st));
+  LB_CUDA(cudaStreamSynchronize(st));
+  ctx->last_launches = 1;
+  return LB_OK;
+}
+
 // Scratch of the state-level operator (sampling outputs, records, K/D,
 // element blocks, CSR values) inside the context's grow-only buffers.
 struct StateBufs {

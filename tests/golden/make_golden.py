@@ -719,7 +719,32 @@ def case_cfg5_hp():
     K5, D5 = hp_sweep.hp_kd(close, wl.r, wl.z, wl.w, wl.f, wl.df_r, wl.df_z, wl.nu_hat,
                             wl.mass_ratio_o, wl.eps_d, 0.3, O)
     print(f"cfg5hp: N=2^20 owners {time.time() - t0:.0f} s")
-    save("cfg5hp", idx=close, K=K5, D=D5, checksum=np.float64(wl.checksum()))
+    # config 4 as worded: the union's 64 closest-pair owners (sampled by the
+    # pinned restatement of sample_state, bitwise the reference's)
+    g = np.load(HERE / "cfg4mfull.npz")
+    S = int(g["S"])
+    off = g["offsets"]
+    n = int(off[-1])
+    r = np.empty(n); z = np.empty(n); w = np.empty(n)
+    f, dfr, dfz = np.zeros((S, n)), np.zeros((S, n)), np.zeros((S, n))
+    for a in range(S):
+        key = lambda k: f"s{a}_{k}" if f"s{a}_{k}" in g else f"s0_{k}"  # noqa: E731
+        P = sp.csr_matrix((g[key("mesh_P_data")], g[key("mesh_P_indices")], g[key("mesh_P_indptr")]),
+                          shape=tuple(g[key("mesh_P_shape")]))
+        ra, za, wa, fa, dra, dza = O.sample_state(g[key("mesh_origins")], g[key("mesh_sizes")],
+                                                  g[key("mesh_cell_nodes")], P, g[key("ref_qpts")],
+                                                  g[key("ref_qwts")], g[key("ref_B")], g[key("ref_dB")],
+                                                  g[f"s{a}_coeffs"])
+        sl = slice(off[a], off[a + 1])
+        r[sl], z[sl], w[sl] = ra, za, wa
+        f[a, sl], dfr[a, sl], dfz[a, sl] = fa[0], dra[0], dza[0]
+    own = _closest_owners(r, z, 64)
+    t0 = time.time()
+    K4, D4 = hp_sweep.hp_kd(own, r, z, w, f, dfr, dfz, g["nu_hat"], g["mass_ratio_o"],
+                            float(g["eps_d"]), 2e-3, O)
+    print(f"cfg5hp: config-4-as-worded owners {time.time() - t0:.0f} s")
+    save("cfg5hp", idx=close, K=K5, D=D5, checksum=np.float64(wl.checksum()),
+         cfg4m_idx=own, cfg4m_K=K4, cfg4m_D=D4)
 
 
 def case_cfg5(N, n_sub=None):

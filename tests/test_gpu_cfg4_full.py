@@ -106,9 +106,16 @@ def test_cfg4_species_meshes_full_size(gpu):
         got = blocks[a][g[f"s{a}_rows"]].toarray()
         want = csr_from(g, f"s{a}_R").toarray()
         err_c = max(err_c, np.abs(got - want).max() / np.abs(want).max())
-    print(f"cfg4 per-species meshes (294,912 union points): D/K {err_kd:.2e}, "
-          f"jacobian rows {err_c:.2e}")
-    assert err_kd < TOL and err_c < TOL
+    # the union's 64 closest-pair owners against the reference's formulas in
+    # 40-digit arithmetic (tests/golden/hp_sweep.py): there the reference's
+    # own double-precision result is up to 8e-11 off; this kernel's
+    # cancellation-free tensor forms are expected far closer
+    hp = golden("cfg5hp")
+    own = hp["cfg4m_idx"]
+    err_hp = worst_component(K[own], D[own], hp["cfg4m_K"], hp["cfg4m_D"])
+    print(f"cfg4 per-species meshes (294,912 union points): D/K {err_kd:.2e} vs reference, "
+          f"closest-pair owners {err_hp:.2e} vs 40-digit, jacobian rows {err_c:.2e}")
+    assert err_kd < TOL and err_c < TOL and err_hp < 1e-12
     for a in range(S):
         rate = blocks[a] @ g[f"s{a}_coeffs"]
         assert abs(rate.sum()) <= 1e-11 * max(np.abs(rate).max(), 1.0)
