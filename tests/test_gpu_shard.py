@@ -121,7 +121,7 @@ def test_symmetric_ranks_bitwise_equal_single(gpu, world):
     assert np.array_equal(K.cpu().numpy(), K0) and np.array_equal(D.cpu().numpy(), D0)
 
 
-@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("world", [2, 3, 8])
 def test_multirank_bench_functional(gpu, world):
     """The multi-GPU bench path end to end with `world` ranks over gloo on
     one GPU (ranks time-share the device; no kernel waits on another rank):
