@@ -747,6 +747,26 @@ def case_cfg5_hp():
          cfg4m_idx=own, cfg4m_K=K4, cfg4m_D=D4)
 
 
+def case_pairs_hp():
+    """The 1000 tensor-pair inputs of pairs.npz evaluated with the
+    reference's formulas (kernel.py:306-389) in 40-digit arithmetic
+    (hp_sweep.pair_hp): the yardstick for pairs whose double-precision
+    closed form is ill-conditioned (near-coincident points, where UD_xx /
+    UK_rr cancel O(r^2/d^2) terms)."""
+    sys.path.insert(0, str(HERE))
+    import hp_sweep
+
+    P = np.load(HERE / "pairs.npz")["pairs"]
+    tab = hp_sweep._tables()
+    UK = np.empty((P.shape[0], 2, 2))
+    UD = np.empty((P.shape[0], 2, 2))
+    for k, (r, z, rb, zb) in enumerate(P):
+        tkr, tzr, txx, txz, tzz = (float(v) for v in hp_sweep.pair_hp(r, z, rb, zb, tab))
+        UK[k] = [[tkr, txz], [tzr, tzz]]
+        UD[k] = [[txx, txz], [txz, tzz]]
+    save("pairs_hp", UK=UK, UD=UD)
+
+
 def case_cfg5(N, n_sub=None):
     """BASELINE config 5 recipe (paper_1702_08880_b200/synthetic.py).  Full
     N^2 when n_sub is None, else n_sub evenly spaced outer points plus the 64
@@ -772,7 +792,7 @@ def main():
              "hanging": case_hanging, "cons": case_cons, "cfg2": case_cfg2,
              "cfg3": case_cfg3, "cfg1adv": case_cfg1_advance, "cfg3adv": case_cfg3_advance, "cfg4s": case_cfg4_species, "cfg2m": case_cfg2_meshes,
              "cfg4m": case_cfg4_meshes, "cfg2be": case_cfg2_meshes_be,
-             "cfg4full": case_cfg4_full, "cfg3q3": case_cfg3_q3, "cfg5hp": case_cfg5_hp, "cfg4mfull": case_cfg4_meshes_full,
+             "cfg4full": case_cfg4_full, "cfg3q3": case_cfg3_q3, "cfg5hp": case_cfg5_hp, "pairshp": case_pairs_hp, "cfg4mfull": case_cfg4_meshes_full,
              "cfg5_4096": lambda: case_cfg5(4096),
              "cfg5_65536": lambda: case_cfg5(65536, n_sub=192)}
     for name, fn in cases.items():

@@ -283,3 +283,20 @@ def test_cfg3_q3_point_set(oracle):
     K, D = oracle.fused_sweep(r[idx], z[idx], r, z, w, f, dfr, dfz, nu, mro,
                               eps_d=float(g["eps_d"]))
     assert worst_component(K, D, g["K"], g["D"]) < TOL_SWEEP
+
+
+def test_pairs_hp_fixture_consistent_with_reference():
+    """The 40-digit pair values (pairs_hp.npz, hp_sweep.pair_hp) agree with
+    the reference's own double results within the reference's conditioning
+    64 eps (1 + r^2/d^2 + [m >= 0.01]/m^2): they are the same formulas, the
+    reference's rounding amplified by its cancellations."""
+    g, h = golden("pairs"), golden("pairs_hp")
+    P = g["pairs"]
+    s = np.maximum(np.abs(h["UK"]).reshape(-1, 4).max(1), np.abs(h["UD"]).reshape(-1, 4).max(1))
+    e = np.maximum(np.abs(g["UK"] - h["UK"]).reshape(-1, 4).max(1),
+                   np.abs(g["UD"] - h["UD"]).reshape(-1, 4).max(1)) / s
+    d2 = (P[:, 0] - P[:, 2]) ** 2 + (P[:, 1] - P[:, 3]) ** 2
+    m = 4 * P[:, 0] * P[:, 2] / (d2 + 4 * P[:, 0] * P[:, 2])
+    amp = 1.0 + np.maximum(P[:, 0], P[:, 2]) ** 2 / d2 + np.where(m >= 0.01, 1.0 / m**2, 0.0)
+    assert np.all(e <= 64 * np.finfo(float).eps * amp)
+    assert np.median(e) < 1e-15
