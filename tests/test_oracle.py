@@ -297,6 +297,7 @@ def test_pairs_hp_fixture_consistent_with_reference():
                    np.abs(g["UD"] - h["UD"]).reshape(-1, 4).max(1)) / s
     d2 = (P[:, 0] - P[:, 2]) ** 2 + (P[:, 1] - P[:, 3]) ** 2
     m = 4 * P[:, 0] * P[:, 2] / (d2 + 4 * P[:, 0] * P[:, 2])
-    amp = 1.0 + np.maximum(P[:, 0], P[:, 2]) ** 2 / d2 + np.where(m >= 0.01, 1.0 / m**2, 0.0)
+    with np.errstate(divide="ignore"):
+        amp = 1.0 + np.maximum(P[:, 0], P[:, 2]) ** 2 / d2 + np.where(m >= 0.01, 1.0 / m**2, 0.0)
     assert np.all(e <= 64 * np.finfo(float).eps * amp)
     assert np.median(e) < 1e-15
