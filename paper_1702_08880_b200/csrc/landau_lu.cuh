@@ -160,7 +160,10 @@ __global__ void __launch_bounds__(kLuThreads) lb_getrf_kernel(int n, double* con
           const int oi = redi[q];
           if (ov > best || (ov == best && oi < bi)) { best = ov; bi = oi; }
         }
-        piv = bi;  // idamax: the first index of the largest |a|
+        // idamax: the first index of the largest |a|; a column with no
+        // comparable entry (all NaN, after a singular block upstream) keeps
+        // row j -- never the sentinel m, which would index past the block
+        piv = bi < m ? bi : j;
         if (piv != j && tid < w) {
           const double t0 = P[(size_t)tid * ld + j];
           P[(size_t)tid * ld + j] = P[(size_t)tid * ld + piv];

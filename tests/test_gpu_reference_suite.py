@@ -10,8 +10,8 @@ by-value import of the hot path (kernel.fused_sweep / fused_inner_loop,
 assembly.assemble_collision, solver._assemble_at / newton_step /
 linear_cn_step, cli) before the test modules import them, and counts the
 calls that reach this package.  Suites: test_kernel.py,
-test_assembly.py, test_solver.py, and acceptance criteria 3-4
-(test_acceptance.py:108-192).
+test_assembly.py, test_solver.py, test_cli.py, and acceptance criteria 3-4
+(test_acceptance.py:108-192); plus the reference's own advance() loop.
 """
 
 import json
@@ -77,6 +77,14 @@ def test_reference_assembly_suite(gpu, tmp_path):
 def test_reference_solver_suite(gpu, tmp_path):
     counts, log = _run_suite(tmp_path, ["test_solver.py"])
     assert counts["axlandau.solver.newton_step"] + counts["axlandau.solver._assemble_at"] > 0
+
+
+def test_reference_cli_suite(gpu, tmp_path):
+    """test_cli.py: the reference's command layer (run / converge / bench /
+    mesh, exit codes) over the installed B200 path -- cli.py imports
+    assemble_collision and fused_sweep by value (cli.py:27-29)."""
+    counts, log = _run_suite(tmp_path, ["test_cli.py"])
+    assert sum(counts.values()) > 0
 
 
 def test_reference_acceptance_criteria_3_4(gpu, tmp_path):
