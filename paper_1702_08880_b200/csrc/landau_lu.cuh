@@ -164,6 +164,7 @@ __global__ void __launch_bounds__(kLuThreads) lb_getrf_kernel(int n, double* con
         // comparable entry (all NaN, after a singular block upstream) keeps
         // row j -- never the sentinel m, which would index past the block
         piv = bi < m ? bi : j;
+        LB_DCHECK(piv >= j && piv < m);
         if (piv != j && tid < w) {
           const double t0 = P[(size_t)tid * ld + j];
           P[(size_t)tid * ld + j] = P[(size_t)tid * ld + piv];
