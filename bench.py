@@ -355,7 +355,9 @@ def ours_arm(args):
         from tools import sass_fp64
 
         try:
-            sass = sass_fp64.analyse(Path(lib._name))
+            # the kernel variant this eps_d selects (merged mask/guard compare
+            # when eps_d^2 > 1e-300, landau_pair.cuh pair_stage1)
+            sass = sass_fp64.analyse(Path(lib._name), sass_fp64.KERNELS[wl.eps_d ** 2 > 1e-300])
             ex = sass_fp64.executed(counts, sass)
             executed = {
                 "flops_per_launch": ex["flops"] / args.steps,

@@ -338,9 +338,12 @@ int sym_prepare(lb_ctx* ctx, int n, const Coupling& cp, const double* rec, cudaS
   return LB_OK;
 }
 
+// the symmetric sweep kernel for S accumulator sets; the species-collapsed
+// one has a merged-guard variant (landau_pair.cuh pair_stage1) used when the
+// mask threshold is above the d^2 guard
 template <int S>
-auto sym_kernel() {
-  if constexpr (S == 1 && LB_SYM_IB) return lb_symsweep_ib_kernel<S>;
+auto sym_kernel(bool merged_guard) {
+  if constexpr (S == 1 && LB_SYM_IB) return merged_guard ? lb_symsweep_ib_kernel<S, true> : lb_symsweep_ib_kernel<S, false>;
   else return lb_symsweep_kernel<S>;
 }
 
@@ -366,12 +369,15 @@ int sym_partial(lb_ctx* ctx, long long gthr, int rank, int world, double* tot, c
   const size_t smem = sym_smem_bytes<S>();
   static bool attr_done[64] = {};
   if (!attr_done[ctx->device & 63]) {
-    LB_CUDA(cudaFuncSetAttribute(sym_kernel<S>(), cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)smem));
+    for (bool mg : {false, true})
+      LB_CUDA(cudaFuncSetAttribute(sym_kernel<S>(mg), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)smem));
     attr_done[ctx->device & 63] = true;
   }
+  const bool merged_guard = gthr > kTinyBits;  // every guarded pair is masked
+  const auto kern = sym_kernel<S>(merged_guard);
   int per_sm = 0;
-  LB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sym_kernel<S>(), sym_threads<S>(), smem));
+  LB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, sym_threads<S>(), smem));
   per_sm = std::max(per_sm, 1);
   const size_t row_i = (size_t)nseg * 5 * S * kSymTile * sizeof(double);
   const size_t row_j = (size_t)std::max(hmax, 1) * 5 * S * kSymTile * sizeof(double);
@@ -404,7 +410,7 @@ int sym_partial(lb_ctx* ctx, long long gthr, int rank, int world, double* tot, c
     a.gthr = gthr;
     const long long nitems = (long long)(b1 - b0) * nseg;
     const int grid = (int)std::min<long long>(nitems, (long long)ctx->num_sms * per_sm);
-    sym_kernel<S>()<<<grid, sym_threads<S>(), smem, st>>>(a);
+    kern<<<grid, sym_threads<S>(), smem, st>>>(a);
     LB_CUDA(cudaGetLastError());
     lb_symreduce_kernel<S><<<(npad + 127) / 128, 128, 0, st>>>(a.iside, a.jside, nt, b0, b1, nseg,
                                                                hmax, g0, tot);

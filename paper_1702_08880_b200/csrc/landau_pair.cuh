@@ -213,6 +213,12 @@ struct PairS1 {
   double dz, dz2, dr, P, rr, isPm, invP, x, lr, logc, kd;
 };
 
+// MG ("merged guard"): when the mask threshold is above the d^2 guard
+// (eps_d^2 > 1e-300, e.g. assemble_collision's 1e-14 L), every pair the
+// guard would touch is masked anyway, so one compare serves both; the host
+// picks the variant (sym_partial), the general form keeps the reference's
+// semantics for eps_d ~ 0 (kernel.py:315,344-345).
+template <bool MG = false>
 __device__ __forceinline__ PairS1 pair_stage1(const Outer& o, double rn, double zn, long long gthr,
                                               const double2* __restrict__ logt) {
   PairS1 s;
@@ -222,7 +228,7 @@ __device__ __forceinline__ PairS1 pair_stage1(const Outer& o, double rn, double 
   const double dist2 = fma(s.dr, s.dr, s.dz2);
   const long long di = __double_as_longlong(dist2);
   const bool g = di >= gthr;  // d^2 >= eps^2 and d^2 > 0 (kernel.py:344)
-  const double d2 = di > kTinyBits ? dist2 : 1.0;
+  const double d2 = (MG ? g : di > kTinyBits) ? dist2 : 1.0;
   // ri rn; 4 ri rn and 2 ri rn below are exact scalings of it, so P, m and
   // u round exactly as with (4 ri) rn and (2 ri) rn
   s.rr = o.ri * rn;
@@ -311,7 +317,7 @@ __device__ __forceinline__ PairB pair_stage2(const Outer& o, double rn, double r
     const double invm2 = P * o.rtri * rcpr;  // 2/m
     const double cq = c3 * invm2;
     p.c34 = cq * (EK - EE);
-    p.c35 = (cq * invm2) * fma(1.0 + x, EK, -(EE + EE));
+    p.c35 = (cq * invm2) * fma(x, EK, fma(-2.0, EE, EK));  // ((1 + x) K - 2 E)
     p.B4 = p.B3 - p.c34;
   }
   p.dz = s.dz;
@@ -370,7 +376,7 @@ __device__ __forceinline__ double pair_tensor_sym(const Outer& o, double rn, dou
 // replaced by the series where m < 0.01 (kernel.py:366-378 likewise computes
 // both and selects).  `nser` counts the calls that took the series branch
 // (the benchmark's executed-instruction count; callers may ignore it).
-template <int U>
+template <int U, bool MG = false>
 __device__ __forceinline__ void pair_tensor_sym_x(const Outer (&oo)[U], const double (&rn)[U],
                                                   const double (&zn)[U], const double (&rn2)[U],
                                                   const double (&rcpr)[U], long long gthr,
@@ -380,7 +386,7 @@ __device__ __forceinline__ void pair_tensor_sym_x(const Outer (&oo)[U], const do
   double lx[U], x[U];
 #pragma unroll
   for (int u = 0; u < U; ++u) {
-    s[u] = pair_stage1(oo[u], rn[u], zn[u], gthr, logt);
+    s[u] = pair_stage1<MG>(oo[u], rn[u], zn[u], gthr, logt);
     x[u] = s[u].x;
   }
 #pragma unroll
@@ -424,7 +430,7 @@ __device__ __forceinline__ void pair_tensor_sym_x(const Outer (&oo)[U], const do
     const double invm2 = s[u].P * oo[u].rtri * rcpr[u];  // 2/m
     const double cq = c3 * invm2;
     p[u].c34 = cq * (EK - EE);
-    p[u].c35 = (cq * invm2) * fma(1.0 + x[u], EK, -(EE + EE));
+    p[u].c35 = (cq * invm2) * fma(x[u], EK, fma(-2.0, EE, EK));  // ((1 + x) K - 2 E)
     p[u].B4 = p[u].B3 - p[u].c34;
     p[u].dz = s[u].dz;
     p[u].dz2 = s[u].dz2;

@@ -411,7 +411,7 @@ __global__ void __launch_bounds__(kSymTile, sym_min_blocks(S)) lb_symsweep_kerne
 #define LB_IB_MINB (LB_IB_PAIRS == 2 ? 4 : 6)  // CTAs per SM (240 / 168 registers)
 #endif
 
-template <int S>
+template <int S, bool MG>
 #ifdef LB_IB_MAXNREG
 __global__ void __maxnreg__(LB_IB_MAXNREG) lb_symsweep_ib_kernel(const SymArgs a) {
 #else
@@ -535,7 +535,7 @@ __global__ void __launch_bounds__(kIbThreads, LB_IB_MINB) lb_symsweep_ib_kernel(
         }
         T5 t[P2];
         double txx2[P2];
-        pair_tensor_sym_x<P2>(oo, rn, zn, rn2, rcpr, a.gthr, logt, t, txx2, n_ser);
+        pair_tensor_sym_x<P2, MG>(oo, rn, zn, rn2, rcpr, a.gthr, logt, t, txx2, n_ser);
 #pragma unroll
         for (int u = 0; u < JU; ++u)
 #pragma unroll

@@ -34,7 +34,10 @@ from pathlib import Path
 
 ROOT = Path(__file__).resolve().parents[1]
 LIB = ROOT / "paper_1702_08880_b200" / "liblandau_b200.so"
-KERNEL = "_ZN2lb21lb_symsweep_ib_kernelILi1EEEvNS_7SymArgsE"
+# lb_symsweep_ib_kernel<1, merged_guard>: the benchmark's eps_d takes the merged-guard variant
+KERNELS = {True: "_ZN2lb21lb_symsweep_ib_kernelILi1ELb1EEEvNS_7SymArgsE",
+           False: "_ZN2lb21lb_symsweep_ib_kernelILi1ELb0EEEvNS_7SymArgsE"}
+KERNEL = KERNELS[True]
 FP64 = ("DFMA", "DMUL", "DADD")
 _LINE = re.compile(r"/\*([0-9a-f]{4,})\*/\s+(@!?U?P\w+\s+)?([A-Z0-9_.]+)\s*([^;]*);")
 
