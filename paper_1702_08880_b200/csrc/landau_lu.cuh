@@ -29,6 +29,12 @@
 #pragma once
 #include <cstdint>
 
+#ifndef LB_DCHECK  // standalone use (tools/microbench): bounds checks off
+#define LB_DCHECK(cond) \
+  do {                  \
+  } while (0)
+#endif
+
 namespace lb {
 
 constexpr int kLuThreads = 256;
