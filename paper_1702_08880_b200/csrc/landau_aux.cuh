@@ -88,85 +88,120 @@ __global__ void lb_gather_kernel(int n, const int* __restrict__ perm, const doub
 }
 
 // ------------------------------------------------------------------ K2 elements
-// One warp per cell, all S species in chunks of three.  Per species G2 =
-// K Jinv w, G3 = Jinv D Jinv w (assembly.py:159-160, same factor grouping;
-// the cell's K (9 x S x 2), D (9 x S x 4) and w (9) are contiguous in HBM),
-// then one lane per (species, row i) forms
-//   u[q] = (dB[i,q,:].G2[q], dB[i,q,:].G3[q][:,0], dB[i,q,:].G3[q][:,1])
-// in registers and the row's nine entries
-//   elem[a,e,i,j] = sum_q u[q] . (B[j,q], dB[j,q,0], dB[j,q,1])
-// together, the basis values being warp-wide shared-memory broadcasts (one
-// shared load per FMA; ncu: an entry-per-lane form with u/v staged in shared
-// memory was MIO-bound and occupancy-limited by its shared memory).  Per
-// (cell, species): 9 x 48 + 72 B in, 648 B out; the (S, ncell, 81) result
-// stays in L2 for K3.
-constexpr int kElemWarps = 4;
+// One thread per row i of two (cell e, species a) pairs of the element
+// matrices: the nine entries of row i,
+//   elem[a,e,i,j] = sum_q u[q] . (B[j,q], dB[j,q,0], dB[j,q,1]),
+//   u[q] = (dB[i,q,:].G2[q], dB[i,q,:].G3[q][:,0], dB[i,q,:].G3[q][:,1]),
+// with G2 = K Jinv w, G3 = Jinv D Jinv w (assembly.py:159-160, same factor
+// grouping).  The 243 basis values (B, dB at the nine Gauss points) are a
+// by-value kernel parameter: the row loop is fully unrolled with warp-uniform
+// indices, so every one of the 243 DFMAs of a row takes its basis operand
+// from the constant bank (uniform registers), not from a shared-memory load
+// per FMA as the round-1 warp-per-cell form did (MIO-bound, 36 us at config
+// 4).  A block takes 32 consecutive (e, a) pairs (tasks in (e, a, i) order:
+// the cells' K/D/w are read contiguously); stage 1 forms G for its 288
+// (e, a, q) in shared memory, stage 2 gives each of 144 threads row i of two
+// pairs (c, c + 16), so each basis operand feeds two FMA chains (measured at
+// config 4 under ncu's cache flush: 1 / 2 / 3 / 4 rows per thread 37 / 25 /
+// 27 / 31 us -- fewer, fatter threads lose to latency: the kernel has ~2 waves
+// of work).  Per (cell, species): 9 x 56 B in, 648 B out, 2772 FP64 ops; the
+// (S, ncell, 81) result stays in L2 for K3.  Products and sums keep the
+// round-1 kernel's order, so every entry is bitwise unchanged.
 constexpr int kElemMaxS = 8;
-constexpr int kElemChunk = 3;  // species per pass (27 row tasks for a warp's 32 lanes)
-__global__ void __launch_bounds__(32 * kElemWarps) lb_elements_kernel(
+#ifndef LB_ELEM_RPT
+#define LB_ELEM_RPT 2  // rows per thread (pairs c and c + 16 of the block): the basis operands serve both
+#endif
+constexpr int kElemRpt = LB_ELEM_RPT;
+constexpr int kElemPairs = 16 * kElemRpt;  // (cell, species) pairs per block
+constexpr int kElemThreads = 144;          // row i of RPT pairs each
+struct ElemBasis {
+  double v[9][9][3];  // v[j][q] = (B[j,q], dB[j,q,0], dB[j,q,1])
+};
+__global__ void __launch_bounds__(kElemThreads) lb_elements_kernel(
     int ncell, int S, const double* __restrict__ sizes, const double* __restrict__ w,
-    const double* __restrict__ K, const double* __restrict__ D, const double* __restrict__ Bt,
+    const double* __restrict__ K, const double* __restrict__ D, const ElemBasis V,
     const double* __restrict__ dBt, double* __restrict__ elem, int ncell_out, int c_out) {
   // cells e of this launch land at cell c_out + e of an (S, ncell_out, 81) buffer
-  __shared__ double sV[9][9][3];  // basis as V[j][q] = (B, dB_r, dB_z)
-  __shared__ double sG[kElemWarps][kElemChunk][9][6];  // G2 r,z ; G3 rr, rz, zr, zz
-  for (int t = threadIdx.x; t < 81; t += blockDim.x) {
-    const int j = t / 9, q = t % 9;
-    sV[j][q][0] = Bt[t];
-    sV[j][q][1] = dBt[2 * t];
-    sV[j][q][2] = dBt[2 * t + 1];
-  }
-  __syncthreads();
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  for (int e = blockIdx.x * kElemWarps + warp; e < ncell; e += gridDim.x * kElemWarps) {
-    const double jr = 2.0 / sizes[2 * e], jz = 2.0 / sizes[2 * e + 1];
-    for (int a0 = 0; a0 < S; a0 += kElemChunk) {
-      const int nc = min(kElemChunk, S - a0);
-      for (int t = lane; t < 9 * nc; t += 32) {  // (species a0 + c, point q)
-        const int c = t / 9, q = t % 9, a = a0 + c;
-        const size_t pnt = 9 * (size_t)e + q;
-        const double wp = w[pnt];
-        const double* Kp = K + (pnt * S + a) * 2;
-        const double* Dp = D + (pnt * S + a) * 4;
-        double* g = sG[warp][c][q];
-        // same factor grouping as assembly.py:159-160
-        g[0] = Kp[0] * (jr * wp);
-        g[1] = Kp[1] * (jz * wp);
-        g[2] = Dp[0] * ((jr * jr) * wp);
-        g[3] = Dp[1] * ((jr * jz) * wp);
-        g[4] = Dp[2] * ((jz * jr) * wp);
-        g[5] = Dp[3] * ((jz * jz) * wp);
-      }
-      __syncwarp();
-      for (int t = lane; t < 9 * nc; t += 32) {  // (c, row i): the nine entries of the row
-        const int c = t / 9, i = t % 9;
-        double u[9][3];
+  __shared__ double sG[kElemPairs][9][6];  // G2 r,z ; G3 rr, rz, zr, zz
+  __shared__ double sdB[9][9][2];          // dB[i][q][:] (row-dependent, not uniform)
+  const int t = threadIdx.x;
+  const long long npair = (long long)ncell * S;
+  const long long pr0 = (long long)blockIdx.x * kElemPairs;
+  for (int k = t; k < 162; k += kElemThreads) (&sdB[0][0][0])[k] = dBt[k];
+  // stage 1: G of pair pr0 + c at point q, (c, q) = divmod(task, 9)
 #pragma unroll
-        for (int q = 0; q < 9; ++q) {
-          const double* g = sG[warp][c][q];
-          const double b0 = sV[i][q][1], b1 = sV[i][q][2];  // dB[i,q,:]
-          u[q][0] = fma(b1, g[1], b0 * g[0]);
-          u[q][1] = fma(b1, g[4], b0 * g[2]);
-          u[q][2] = fma(b1, g[5], b0 * g[3]);
-        }
-        double s[9];
-#pragma unroll
-        for (int j = 0; j < 9; ++j) s[j] = 0.0;
-#pragma unroll
-        for (int q = 0; q < 9; ++q)
-#pragma unroll
-          for (int j = 0; j < 9; ++j) {
-            s[j] = fma(u[q][0], sV[j][q][0], s[j]);
-            s[j] = fma(u[q][1], sV[j][q][1], s[j]);
-            s[j] = fma(u[q][2], sV[j][q][2], s[j]);
-          }
-        double* out = elem + ((size_t)(a0 + c) * ncell_out + c_out + e) * 81 + 9 * i;
-#pragma unroll
-        for (int j = 0; j < 9; ++j) out[j] = s[j];
-      }
-      __syncwarp();
+  for (int r = 0; r < kElemRpt; ++r) {
+    const int task = t + r * kElemThreads, c = task / 9, q = task % 9;
+    const long long pr = pr0 + c;
+    if (pr < npair) {
+      const int e = (int)(pr / S), a = (int)(pr % S);
+      const double jr = 2.0 / sizes[2 * e], jz = 2.0 / sizes[2 * e + 1];
+      const size_t pnt = 9 * (size_t)e + q;
+      const double wp = w[pnt];
+      const double* Kp = K + (pnt * S + a) * 2;  // (caller pointers: no alignment assumed)
+      const double* Dp = D + (pnt * S + a) * 4;
+      double* g = sG[c][q];
+      g[0] = Kp[0] * (jr * wp);
+      g[1] = Kp[1] * (jz * wp);
+      g[2] = Dp[0] * ((jr * jr) * wp);
+      g[3] = Dp[1] * ((jr * jz) * wp);
+      g[4] = Dp[2] * ((jz * jr) * wp);
+      g[5] = Dp[3] * ((jz * jz) * wp);
     }
   }
+  __syncthreads();
+  // stage 2: row i of pairs c0 + 16 r; u[q] formed per q (registers: the
+  // RPT x 9 row sums and one q's u)
+  const int c0 = t / 9, i = t % 9;
+  constexpr int kStep = kElemPairs / kElemRpt;
+  double s[kElemRpt][9];
+#pragma unroll
+  for (int r = 0; r < kElemRpt; ++r)
+#pragma unroll
+    for (int j = 0; j < 9; ++j) s[r][j] = 0.0;
+#pragma unroll
+  for (int q = 0; q < 9; ++q) {
+    const double2 b = *reinterpret_cast<const double2*>(sdB[i][q]);  // dB[i,q,:]
+    double u[kElemRpt][3];
+#pragma unroll
+    for (int r = 0; r < kElemRpt; ++r) {
+      const double* g = sG[c0 + r * kStep][q];
+      u[r][0] = fma(b.y, g[1], b.x * g[0]);
+      u[r][1] = fma(b.y, g[4], b.x * g[2]);
+      u[r][2] = fma(b.y, g[5], b.x * g[3]);
+    }
+#pragma unroll
+    for (int j = 0; j < 9; ++j)
+#pragma unroll
+      for (int r = 0; r < kElemRpt; ++r) {
+        s[r][j] = fma(u[r][0], V.v[j][q][0], s[r][j]);
+        s[r][j] = fma(u[r][1], V.v[j][q][1], s[r][j]);
+        s[r][j] = fma(u[r][2], V.v[j][q][2], s[r][j]);
+      }
+  }
+#pragma unroll
+  for (int r = 0; r < kElemRpt; ++r) {
+    const long long pr = pr0 + c0 + r * kStep;
+    if (pr < npair) {
+      const int e = (int)(pr / S), a = (int)(pr % S);
+      double* out = elem + ((size_t)a * ncell_out + c_out + e) * 81 + 9 * i;
+#pragma unroll
+      for (int j = 0; j < 9; ++j) out[j] = s[r][j];
+    }
+  }
+}
+
+// host: the by-value basis parameter from host copies of B (9 x 9, [j][q])
+// and dB (9 x 9 x 2)
+inline ElemBasis make_elem_basis(const double* hB, const double* hdB) {
+  ElemBasis V;
+  for (int t = 0; t < 81; ++t) {
+    const int j = t / 9, q = t % 9;
+    V.v[j][q][0] = hB[t];
+    V.v[j][q][1] = hdB[2 * t];
+    V.v[j][q][2] = hdB[2 * t + 1];
+  }
+  return V;
 }
 
 // ------------------------------------------------------------------ K3 CSR gather

@@ -18,6 +18,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <climits>
 #include <cmath>
 #include <atomic>
 #include <cstdint>
@@ -92,6 +93,7 @@ struct lb_mesh {
   int ncell = 0, nslots = 0, ncontrib = 0;
   double* sizes = nullptr;    // (ncell, 2)
   double* basis = nullptr;    // B (81) then dB (162)
+  double hbasis[243] = {};    // host copy (the element kernel takes the basis by value)
   int* slot_ptr = nullptr;    // (nslots + 1)
   int* gidx = nullptr;        // (ncontrib)
   double* gw = nullptr;       // (ncontrib)
@@ -499,15 +501,19 @@ int launch_pack(lb_ctx* ctx, int n, int S, const double* r, const double* z, con
   return LB_OK;
 }
 
+// hB / hdB: host copies of the basis (kernel parameter); ddB: the device dB
 int launch_elements(lb_ctx* ctx, int ncell, int S, const double* sizes, const double* w,
-                    const double* K, const double* D, const double* B, const double* dB,
-                    double* elem, cudaStream_t st, int ncell_out = -1, int c_out = 0) {
+                    const double* K, const double* D, const double* hB, const double* hdB,
+                    const double* ddB, double* elem, cudaStream_t st, int ncell_out = -1,
+                    int c_out = 0) {
   if (ncell_out < 0) ncell_out = ncell;
   if (ncell == 0) return LB_OK;
   if (S > kElemMaxS) return fail(LB_EINVAL, "element contraction supports S <= 8");
-  const int blocks = (int)std::min<long long>((ncell + kElemWarps - 1) / kElemWarps, (long long)ctx->num_sms * 16);
-  lb_elements_kernel<<<blocks, 32 * kElemWarps, 0, st>>>(ncell, S, sizes, w, K, D, B, dB, elem,
-                                                         ncell_out, c_out);
+  const long long blocks = ((long long)ncell * S + kElemPairs - 1) / kElemPairs;
+  if (blocks > INT_MAX) return fail(LB_EINVAL, "too many cells");
+  lb_elements_kernel<<<(int)blocks, kElemThreads, 0, st>>>(ncell, S, sizes, w, K, D,
+                                                           make_elem_basis(hB, hdB), ddB, elem,
+                                                           ncell_out, c_out);
   LB_CUDA(cudaGetLastError());
   return LB_OK;
 }
@@ -645,7 +651,13 @@ int lb_elements_dev(lb_ctx* ctx, int ncell, int S, const double* cell_sizes, con
   if ((rc = check_species(S))) return rc;
   if (ncell < 0) return fail(LB_EINVAL, "negative cell count");
   cudaStream_t st = (cudaStream_t)stream;  // NULL = legacy default stream
-  rc = launch_elements(ctx, ncell, S, cell_sizes, w, K, D, B, dB, elem_out, st);
+  double hb[243];
+  if (ncell > 0) {  // the basis becomes a kernel parameter: read its 243 values once
+    LB_CUDA(cudaMemcpyAsync(hb, B, sizeof(double) * 81, cudaMemcpyDeviceToHost, st));
+    LB_CUDA(cudaMemcpyAsync(hb + 81, dB, sizeof(double) * 162, cudaMemcpyDeviceToHost, st));
+    LB_CUDA(cudaStreamSynchronize(st));
+  }
+  rc = launch_elements(ctx, ncell, S, cell_sizes, w, K, D, hb, hb + 81, dB, elem_out, st);
   ctx->last_launches = ncell > 0 ? 1 : 0;
   return rc;
 }
@@ -746,7 +758,7 @@ int lb_assemble_elements(lb_ctx* ctx, int ncell, const double* cell_sizes, int S
   if ((rc = all_points_sweep(ctx, n, drec, dr, dz, cp, mask_threshold(eps_d), dK, dD, st)))
     return rc;
   LB_CUDA(cudaEventRecord(ctx->ev[2], st));
-  if ((rc = launch_elements(ctx, ncell, S, dsz, dw, dK, dD, dB_, ddB, delem, st))) return rc;
+  if ((rc = launch_elements(ctx, ncell, S, dsz, dw, dK, dD, B, dB, ddB, delem, st))) return rc;
   if (K_out) LB_CUDA(cudaMemcpyAsync(K_out, dK, sizeof(double) * 2 * S * n, cudaMemcpyDeviceToHost, st));
   if (D_out) LB_CUDA(cudaMemcpyAsync(D_out, dD, sizeof(double) * 4 * S * n, cudaMemcpyDeviceToHost, st));
   LB_CUDA(cudaMemcpyAsync(elem_out, delem, sizeof(double) * 81 * S * ncell, cudaMemcpyDeviceToHost, st));
@@ -974,6 +986,8 @@ int lb_mesh_create(lb_ctx* ctx, int ncell, const double* cell_sizes, const doubl
   if (e == cudaSuccess) e = cudaMemcpy(m->sizes, cell_sizes, sizeof(double) * 2 * ncell, cudaMemcpyHostToDevice);
   if (e == cudaSuccess) e = cudaMemcpy(m->basis, B, sizeof(double) * 81, cudaMemcpyHostToDevice);
   if (e == cudaSuccess) e = cudaMemcpy(m->basis + 81, dB, sizeof(double) * 162, cudaMemcpyHostToDevice);
+  std::memcpy(m->hbasis, B, sizeof(double) * 81);
+  std::memcpy(m->hbasis + 81, dB, sizeof(double) * 162);
   if (e == cudaSuccess) e = cudaMemcpy(m->slot_ptr, slot_ptr, sizeof(int) * (nslots + 1), cudaMemcpyHostToDevice);
   if (e == cudaSuccess && ncontrib) e = cudaMemcpy(m->gidx, gather_idx, sizeof(int) * ncontrib, cudaMemcpyHostToDevice);
   if (e == cudaSuccess && ncontrib) e = cudaMemcpy(m->gw, gather_w, sizeof(double) * ncontrib, cudaMemcpyHostToDevice);
@@ -1040,8 +1054,8 @@ int lb_assemble_csr(lb_ctx* ctx, const lb_mesh* mesh, int S, const double* r, co
   if ((rc = all_points_sweep(ctx, n, drec, dr, dz, cp, mask_threshold(eps_d), dK, dD, st)))
     return rc;
   LB_CUDA(cudaEventRecord(ctx->ev[2], st));
-  if ((rc = launch_elements(ctx, ncell, S, mesh->sizes, dw, dK, dD, mesh->basis, mesh->basis + 81,
-                            delem, st)))
+  if ((rc = launch_elements(ctx, ncell, S, mesh->sizes, dw, dK, dD, mesh->hbasis, mesh->hbasis + 81,
+                            mesh->basis + 81, delem, st)))
     return rc;
   if (mesh->nslots) {
     lb_csr_gather_kernel<<<(mesh->nslots + 255) / 256, 256, 0, st>>>(
@@ -1193,8 +1207,8 @@ static int state_issue(lb_ctx* ctx, const lb_mesh* m, int S, const Coupling& cp,
   int r = launch_pack(ctx, n, S, b.dr, b.dz, b.dw, b.df, b.dfr, b.dfz, cp, b.drec, st);
   if (r) return r;
   if ((r = all_points_sweep(ctx, n, b.drec, b.dr, b.dz, cp, gthr, b.dK, b.dD, st))) return r;
-  if ((r = launch_elements(ctx, ncell, S, m->sizes, b.dw, b.dK, b.dD, m->basis, m->basis + 81,
-                           b.delem, st)))
+  if ((r = launch_elements(ctx, ncell, S, m->sizes, b.dw, b.dK, b.dD, m->hbasis, m->hbasis + 81,
+                           m->basis + 81, b.delem, st)))
     return r;
   if (m->nslots) {
     lb_csr_gather_kernel<<<(m->nslots + 255) / 256, 256, 0, st>>>(m->nslots, 81 * ncell, S,
@@ -1325,7 +1339,8 @@ int lb_elements_csr(lb_ctx* ctx, const lb_mesh* m, int S, const double* w, const
   LB_CUDA(cudaMemcpyAsync(dw, w, sizeof(double) * n, cudaMemcpyHostToDevice, st));
   LB_CUDA(cudaMemcpyAsync(dK, K, sizeof(double) * 2 * S * n, cudaMemcpyHostToDevice, st));
   LB_CUDA(cudaMemcpyAsync(dD, D, sizeof(double) * 4 * S * n, cudaMemcpyHostToDevice, st));
-  if ((rc = launch_elements(ctx, ncell, S, m->sizes, dw, dK, dD, m->basis, m->basis + 81, delem, st)))
+  if ((rc = launch_elements(ctx, ncell, S, m->sizes, dw, dK, dD, m->hbasis, m->hbasis + 81, m->basis + 81,
+                            delem, st)))
     return rc;
   if (m->nslots) {
     lb_csr_gather_kernel<<<(m->nslots + 255) / 256, 256, 0, st>>>(m->nslots, 81 * ncell, S, m->slot_ptr,
@@ -1351,8 +1366,8 @@ int lb_operator_partial_dev(lb_ctx* ctx, const lb_mesh* m, int S, int c0, int c1
   LB_CUDA(cudaMemsetAsync(delem, 0, nel * sizeof(double), st));
   int launches = 0;
   if (c1 > c0) {
-    if ((rc = launch_elements(ctx, c1 - c0, S, m->sizes + 2 * (size_t)c0, w, K, D, m->basis,
-                              m->basis + 81, delem, st, m->ncell, c0)))
+    if ((rc = launch_elements(ctx, c1 - c0, S, m->sizes + 2 * (size_t)c0, w, K, D, m->hbasis,
+                              m->hbasis + 81, m->basis + 81, delem, st, m->ncell, c0)))
       return rc;
     ++launches;
   }
