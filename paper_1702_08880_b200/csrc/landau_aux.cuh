@@ -124,29 +124,49 @@ __global__ void __launch_bounds__(kElemThreads) lb_elements_kernel(
   // cells e of this launch land at cell c_out + e of an (S, ncell_out, 81) buffer
   __shared__ double sG[kElemPairs][9][6];  // G2 r,z ; G3 rr, rz, zr, zz
   __shared__ double sdB[9][9][2];          // dB[i][q][:] (row-dependent, not uniform)
+  __shared__ double sJ[kElemPairs + 1][2];  // 2 / sizes of the block's cells (fem.py:107-108)
   const int t = threadIdx.x;
-  const long long npair = (long long)ncell * S;
-  const long long pr0 = (long long)blockIdx.x * kElemPairs;
-  for (int k = t; k < 162; k += kElemThreads) (&sdB[0][0][0])[k] = dBt[k];
-  // stage 1: G of pair pr0 + c at point q, (c, q) = divmod(task, 9)
+  const int npair = ncell * S;  // host-checked < 2^31
+  const int pr0 = blockIdx.x * kElemPairs, e_lo = pr0 / S;
+  // stage 1 loads first (K, D, w of the thread's (pair, q) tasks in flight
+  // while the block forms its cells' inverse sizes), then G
+  double ld[kElemRpt][7];
 #pragma unroll
   for (int r = 0; r < kElemRpt; ++r) {
-    const int task = t + r * kElemThreads, c = task / 9, q = task % 9;
-    const long long pr = pr0 + c;
+    const int task = t + r * kElemThreads, c = task / 9, q = task % 9, pr = pr0 + c;
     if (pr < npair) {
-      const int e = (int)(pr / S), a = (int)(pr % S);
-      const double jr = 2.0 / sizes[2 * e], jz = 2.0 / sizes[2 * e + 1];
+      const int e = pr / S, a = pr - e * S;
       const size_t pnt = 9 * (size_t)e + q;
-      const double wp = w[pnt];
       const double* Kp = K + (pnt * S + a) * 2;  // (caller pointers: no alignment assumed)
       const double* Dp = D + (pnt * S + a) * 4;
+      ld[r][0] = Kp[0];
+      ld[r][1] = Kp[1];
+      ld[r][2] = Dp[0];
+      ld[r][3] = Dp[1];
+      ld[r][4] = Dp[2];
+      ld[r][5] = Dp[3];
+      ld[r][6] = w[pnt];
+    }
+  }
+  for (int k = t; k < 162; k += kElemThreads) (&sdB[0][0][0])[k] = dBt[k];
+  for (int k = t; k < 2 * (kElemPairs + 1); k += kElemThreads) {
+    const int e = e_lo + (k >> 1);
+    if (e < ncell) sJ[k >> 1][k & 1] = 2.0 / sizes[2 * e + (k & 1)];
+  }
+  __syncthreads();
+#pragma unroll
+  for (int r = 0; r < kElemRpt; ++r) {
+    const int task = t + r * kElemThreads, c = task / 9, q = task % 9, pr = pr0 + c;
+    if (pr < npair) {
+      const int e = pr / S;
+      const double jr = sJ[e - e_lo][0], jz = sJ[e - e_lo][1], wp = ld[r][6];
       double* g = sG[c][q];
-      g[0] = Kp[0] * (jr * wp);
-      g[1] = Kp[1] * (jz * wp);
-      g[2] = Dp[0] * ((jr * jr) * wp);
-      g[3] = Dp[1] * ((jr * jz) * wp);
-      g[4] = Dp[2] * ((jz * jr) * wp);
-      g[5] = Dp[3] * ((jz * jz) * wp);
+      g[0] = ld[r][0] * (jr * wp);
+      g[1] = ld[r][1] * (jz * wp);
+      g[2] = ld[r][2] * ((jr * jr) * wp);
+      g[3] = ld[r][3] * ((jr * jz) * wp);
+      g[4] = ld[r][4] * ((jz * jr) * wp);
+      g[5] = ld[r][5] * ((jz * jz) * wp);
     }
   }
   __syncthreads();
@@ -181,9 +201,9 @@ __global__ void __launch_bounds__(kElemThreads) lb_elements_kernel(
   }
 #pragma unroll
   for (int r = 0; r < kElemRpt; ++r) {
-    const long long pr = pr0 + c0 + r * kStep;
+    const int pr = pr0 + c0 + r * kStep;
     if (pr < npair) {
-      const int e = (int)(pr / S), a = (int)(pr % S);
+      const int e = pr / S, a = pr - e * S;
       double* out = elem + ((size_t)a * ncell_out + c_out + e) * 81 + 9 * i;
 #pragma unroll
       for (int j = 0; j < 9; ++j) out[j] = s[r][j];
@@ -209,18 +229,28 @@ inline ElemBasis make_elem_basis(const double* hB, const double* hdB) {
 // element-matrix entries that land on it, in the map's fixed order
 // (scatter.py builds the map once per mesh; assembly.py:115-129 is the
 // reference's scipy COO->CSR + condensation).  HBM-bound gather.
-__global__ void lb_csr_gather_kernel(int nslots, int nent, int S, const int* __restrict__ slot_ptr,
-                                     const int* __restrict__ gidx, const double* __restrict__ gw,
-                                     const double* __restrict__ elem, double* __restrict__ out) {
+// MAXS bounds S at compile time (2, 4 or 8: registers for the S running
+// sums; fewer registers -> more resident warps -> more gathers in flight,
+// which is what a latency-bound gather needs).
+#ifndef LB_GATHER_MINB
+#define LB_GATHER_MINB 8  // 32 registers, 8 blocks per SM (measured at config 4: 14.1 vs 17.7 us with 45 registers)
+#endif
+template <int MAXS>
+__global__ void __launch_bounds__(256, LB_GATHER_MINB) lb_csr_gather_kernel(int nslots, int nent, int S,
+                                                            const int* __restrict__ slot_ptr,
+                                                            const int* __restrict__ gidx,
+                                                            const double* __restrict__ gw,
+                                                            const double* __restrict__ elem,
+                                                            double* __restrict__ out) {
   const int slot = blockIdx.x * blockDim.x + threadIdx.x;
   if (slot >= nslots) return;
   const int k0 = slot_ptr[slot], k1 = slot_ptr[slot + 1];
   // contributions in groups of 4: the group's indices, weights and element
   // entries (all species) are loaded before the ordered adds (latency-bound
   // gather from L2; the order of the adds is the map's)
-  double v[kElemMaxS];
+  double v[MAXS];
 #pragma unroll
-  for (int a = 0; a < kElemMaxS; ++a) v[a] = 0.0;
+  for (int a = 0; a < MAXS; ++a) v[a] = 0.0;
   for (int kb = k0; kb < k1; kb += 4) {
     int ix[4];
     double ww[4];
@@ -232,7 +262,7 @@ __global__ void lb_csr_gather_kernel(int nslots, int nent, int S, const int* __r
       LB_DCHECK(ix[u] >= 0 && ix[u] < nent);
     }
 #pragma unroll
-    for (int a = 0; a < kElemMaxS; ++a) {
+    for (int a = 0; a < MAXS; ++a) {
       if (a >= S) break;
       const double* ea = elem + (size_t)a * nent;
       double x[4];
@@ -244,8 +274,20 @@ __global__ void lb_csr_gather_kernel(int nslots, int nent, int S, const int* __r
     }
   }
 #pragma unroll
-  for (int a = 0; a < kElemMaxS; ++a)
+  for (int a = 0; a < MAXS; ++a)
     if (a < S) out[(size_t)a * nslots + slot] = v[a];
+}
+
+// host launcher of the gather (the S-bound instantiation)
+inline void launch_csr_gather(int nslots, int nent, int S, const int* slot_ptr, const int* gidx,
+                              const double* gw, const double* elem, double* out, cudaStream_t st) {
+  const int blocks = (nslots + 255) / 256;
+  if (S <= 2)
+    lb_csr_gather_kernel<2><<<blocks, 256, 0, st>>>(nslots, nent, S, slot_ptr, gidx, gw, elem, out);
+  else if (S <= 4)
+    lb_csr_gather_kernel<4><<<blocks, 256, 0, st>>>(nslots, nent, S, slot_ptr, gidx, gw, elem, out);
+  else
+    lb_csr_gather_kernel<kElemMaxS><<<blocks, 256, 0, st>>>(nslots, nent, S, slot_ptr, gidx, gw, elem, out);
 }
 
 // ------------------------------------------------------------------ K4 sampling

@@ -509,9 +509,9 @@ int launch_elements(lb_ctx* ctx, int ncell, int S, const double* sizes, const do
   if (ncell_out < 0) ncell_out = ncell;
   if (ncell == 0) return LB_OK;
   if (S > kElemMaxS) return fail(LB_EINVAL, "element contraction supports S <= 8");
-  const long long blocks = ((long long)ncell * S + kElemPairs - 1) / kElemPairs;
-  if (blocks > INT_MAX) return fail(LB_EINVAL, "too many cells");
-  lb_elements_kernel<<<(int)blocks, kElemThreads, 0, st>>>(ncell, S, sizes, w, K, D,
+  if ((long long)ncell * S + kElemPairs > INT_MAX) return fail(LB_EINVAL, "too many cells");
+  const int blocks = (ncell * S + kElemPairs - 1) / kElemPairs;
+  lb_elements_kernel<<<blocks, kElemThreads, 0, st>>>(ncell, S, sizes, w, K, D,
                                                            make_elem_basis(hB, hdB), ddB, elem,
                                                            ncell_out, c_out);
   LB_CUDA(cudaGetLastError());
@@ -1058,8 +1058,7 @@ int lb_assemble_csr(lb_ctx* ctx, const lb_mesh* mesh, int S, const double* r, co
                             mesh->basis + 81, delem, st)))
     return rc;
   if (mesh->nslots) {
-    lb_csr_gather_kernel<<<(mesh->nslots + 255) / 256, 256, 0, st>>>(
-        mesh->nslots, 81 * ncell, S, mesh->slot_ptr, mesh->gidx, mesh->gw, delem, dcsr);
+    launch_csr_gather(mesh->nslots, 81 * ncell, S, mesh->slot_ptr, mesh->gidx, mesh->gw, delem, dcsr, st);
     LB_CUDA(cudaGetLastError());
   }
   LB_CUDA(cudaMemcpyAsync(csr_out, dcsr, sizeof(double) * S * mesh->nslots, cudaMemcpyDeviceToHost, st));
@@ -1211,9 +1210,7 @@ static int state_issue(lb_ctx* ctx, const lb_mesh* m, int S, const Coupling& cp,
                            m->basis + 81, b.delem, st)))
     return r;
   if (m->nslots) {
-    lb_csr_gather_kernel<<<(m->nslots + 255) / 256, 256, 0, st>>>(m->nslots, 81 * ncell, S,
-                                                                   m->slot_ptr, m->gidx, m->gw,
-                                                                   b.delem, dcsr);
+    launch_csr_gather(m->nslots, 81 * ncell, S, m->slot_ptr, m->gidx, m->gw, b.delem, dcsr, st);
     LB_CUDA(cudaGetLastError());
   }
   return LB_OK;
@@ -1343,8 +1340,7 @@ int lb_elements_csr(lb_ctx* ctx, const lb_mesh* m, int S, const double* w, const
                             delem, st)))
     return rc;
   if (m->nslots) {
-    lb_csr_gather_kernel<<<(m->nslots + 255) / 256, 256, 0, st>>>(m->nslots, 81 * ncell, S, m->slot_ptr,
-                                                                   m->gidx, m->gw, delem, dcsr);
+    launch_csr_gather(m->nslots, 81 * ncell, S, m->slot_ptr, m->gidx, m->gw, delem, dcsr, st);
     LB_CUDA(cudaGetLastError());
   }
   LB_CUDA(cudaMemcpyAsync(csr_out, dcsr, sizeof(double) * S * m->nslots, cudaMemcpyDeviceToHost, st));
@@ -1372,9 +1368,7 @@ int lb_operator_partial_dev(lb_ctx* ctx, const lb_mesh* m, int S, int c0, int c1
     ++launches;
   }
   if (m->nslots) {
-    lb_csr_gather_kernel<<<(m->nslots + 255) / 256, 256, 0, st>>>(m->nslots, 81 * m->ncell, S,
-                                                                   m->slot_ptr, m->gidx, m->gw, delem,
-                                                                   csr_out);
+    launch_csr_gather(m->nslots, 81 * m->ncell, S, m->slot_ptr, m->gidx, m->gw, delem, csr_out, st);
     LB_CUDA(cudaGetLastError());
     ++launches;
   }
@@ -2027,8 +2021,7 @@ int lb_cn_set_mass(lb_cn* cn, const double* M_vals) {
                                                        sb.df, sb.dfr, sb.dfz);
     lb_mass_elements_kernel<<<(81 * ncell + 255) / 256, 256, 0, st>>>(ncell, sb.dw, m->basis, sb.delem);
     if (m->nslots)
-      lb_csr_gather_kernel<<<(m->nslots + 255) / 256, 256, 0, st>>>(m->nslots, 81 * ncell, 1, m->slot_ptr,
-                                                                     m->gidx, m->gw, sb.delem, cn->Mv);
+      launch_csr_gather(m->nslots, 81 * ncell, 1, m->slot_ptr, m->gidx, m->gw, sb.delem, cn->Mv, st);
     LB_CUDA(cudaGetLastError());
   }
   LB_CUDA(cudaStreamSynchronize(st));
