@@ -330,7 +330,7 @@ int sym_prepare(lb_ctx* ctx, int n, const Coupling& cp, const double* rec, cudaS
   if ((rc = ensure(ctx->syminv, (size_t)n * sizeof(int)))) return rc;
   lb_sym_gather_kernel<<<(npad + 255) / 256, 256, 0, st>>>(n, npad, RS, perm, rec,
                                                           static_cast<double*>(ctx->symrec.p));
-  lb_invert_perm_kernel<<<(n + 255) / 256, 256, 0, st>>>(n, perm, static_cast<int*>(ctx->syminv.p));
+  lb_invert_perm_kernel<<<(n + 255) / 256, 256, 0, st>>>(n, nt, perm, static_cast<int*>(ctx->syminv.p));
   LB_CUDA(cudaGetLastError());
   ctx->sym_n = n;
   ctx->sym_S = cp.S;

@@ -753,13 +753,42 @@ __global__ void lb_symreduce_kernel(const double* __restrict__ iside, const doub
   }
 }
 
-// Sorted, padded records: rec_s[p] = rec[perm[p]] for p < n, inert records
-// beyond (far away on the axis side, zero fields: they add exact zeros).
+// Tile interleave.  The Morton order keeps each 128-point tile spatially
+// coherent (warp-coherent series branch), but consecutive tiles -- hence a
+// row group, hence a rank's share of a G-GPU split -- would cover one region
+// of velocity space, and regions differ in work (rows near the axis take the
+// m < 0.01 series more often: groups 0, 1, 4, 5 ran 4 % slower than 2, 3, 6,
+// 7).  So the sorted order deals the Morton tiles to the tile positions by
+// residue class: position T holds Morton tile c + 8 k, classes c = 0..7 in
+// turn (class c at positions off(c) .. off(c) + cnt(c) - 1).  Every row group
+// then draws its tiles evenly from the whole curve.  A function of nt alone:
+// the summation order, hence every bit of K and D, stays GPU-count invariant.
+__host__ __device__ __forceinline__ int sym_class_off(int c, int nt) {
+  return c * (nt / kSymGroups) + min(c, nt % kSymGroups);
+}
+// Morton tile -> sorted tile position
+__host__ __device__ __forceinline__ int sym_tile_pos(int To, int nt) {
+  return sym_class_off(To % kSymGroups, nt) + To / kSymGroups;
+}
+// sorted tile position -> Morton tile
+__host__ __device__ __forceinline__ int sym_tile_src(int Tn, int nt) {
+  int c = 0;
+#pragma unroll 1
+  while (c + 1 < kSymGroups && sym_class_off(c + 1, nt) <= Tn) ++c;
+  return c + kSymGroups * (Tn - sym_class_off(c, nt));
+}
+
+// Sorted, padded records: rec_s[p'] = rec[perm[p]] where p is the Morton
+// position of sorted position p' (tile interleave above) and p < n; inert
+// records for the padding positions p >= n (far away on the axis side, zero
+// fields: they add exact zeros).
 __global__ void lb_sym_gather_kernel(int n, int npad, int RS, const int* __restrict__ perm,
                                      const double* __restrict__ rec, double* __restrict__ rec_s) {
-  const int p = blockIdx.x * blockDim.x + threadIdx.x;
-  if (p >= npad) return;
-  double* o = rec_s + (size_t)p * RS;
+  const int pn = blockIdx.x * blockDim.x + threadIdx.x;
+  if (pn >= npad) return;
+  const int nt = npad / kSymTile;
+  const int p = sym_tile_src(pn / kSymTile, nt) * kSymTile + pn % kSymTile;
+  double* o = rec_s + (size_t)pn * RS;
   if (p < n) {
     const double* src = rec + (size_t)perm[p] * RS;
     for (int c = 0; c < RS; ++c) o[c] = src[c];
@@ -798,9 +827,11 @@ __global__ void lb_sym_combine_kernel(const SymGroupPtrs gp, int npad, const int
   write_kd<Se>(A, cp, (size_t)(q - q0), K, D);
 }
 
-__global__ void lb_invert_perm_kernel(int n, const int* __restrict__ perm, int* __restrict__ inv) {
+// inv[q] = sorted position of original point q (Morton position perm^-1[q]
+// through the tile interleave)
+__global__ void lb_invert_perm_kernel(int n, int nt, const int* __restrict__ perm, int* __restrict__ inv) {
   const int p = blockIdx.x * blockDim.x + threadIdx.x;
-  if (p < n) inv[perm[p]] = p;
+  if (p < n) inv[perm[p]] = sym_tile_pos(p / kSymTile, nt) * kSymTile + p % kSymTile;
 }
 
 }  // namespace lb
