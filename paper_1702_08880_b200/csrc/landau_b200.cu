@@ -1554,7 +1554,7 @@ static int cn_factor_issue(lb_cn* cn, cudaStream_t st, bool pivot) {
       // one CTA per odd-row block: LU (LAPACK layout, pivots, permutation,
       // diagonal-block inverses), then D^-1 [L U] by W-column slabs
       if (L.getrf.count) {
-        lb_getrf_kernel<kLuKB><<<L.getrf.count, kLuThreads, getrf_smem_bytes<kLuKB>(nb), st>>>(
+        lb_getrf_kernel<kLuKB><<<L.getrf.count, kGetrfThreads, getrf_smem_bytes<kLuKB>(nb), st>>>(
             nb, L.getrf.A, L.piv, L.perm, L.info, L.inv, pivot ? 1 : 0);
         LB_CUDA(cudaGetLastError());
       }

@@ -27,6 +27,7 @@
 //    inverse, then the factor column block streamed in by cp.async).
 //  * lb_lu_vsolve_kernel: one vector per matrix (blocks > 96 rows).
 #pragma once
+#include <climits>
 #include <cstdint>
 
 #ifndef LB_DCHECK  // standalone use (tools/microbench): bounds checks off
@@ -38,6 +39,11 @@
 namespace lb {
 
 constexpr int kLuThreads = 256;
+#ifndef LB_LU_REGPANEL
+#define LB_LU_REGPANEL 1  // panel factorisation in registers (one row per thread); 0: shared-memory panel
+#endif
+// lb_getrf_kernel: one thread per panel row (n <= 384) with the register panel
+constexpr int kGetrfThreads = LB_LU_REGPANEL ? 384 : kLuThreads;
 #ifdef LB_LU_PROF
 // cycles per phase (block 0, thread 0): accumulated in registers, written by LU_FLUSH
 __device__ long long lu_prof[8];
@@ -49,8 +55,18 @@ __device__ long long lu_prof[8];
   } while (0)
 #define LU_FLUSH()                                                                   \
   do {                                                                               \
-    if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0)                      \
+    if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) {                    \
       for (int k_ = 0; k_ < 8; ++k_) lu_prof[k_] += pacc_[k_];                       \
+      for (int k_ = 0; k_ < 4; ++k_) lu_prof2[k_] += pcol_[k_];                      \
+    }                                                                                \
+  } while (0)
+// column-loop breakdown of the register panel (reduction, pivot row, update)
+__device__ long long lu_prof2[4];
+#define LU_TC(k)                                                       \
+  do {                                                                 \
+    const long long t1_ = clock64();                                   \
+    pcol_[k] += t1_ - t0_;                                             \
+    t0_ = t1_;                                                         \
   } while (0)
 #else
 #define LU_T(k) \
@@ -58,6 +74,9 @@ __device__ long long lu_prof[8];
   } while (0)
 #define LU_FLUSH() \
   do {             \
+  } while (0)
+#define LU_TC(k) \
+  do {           \
   } while (0)
 #endif
 
@@ -69,8 +88,9 @@ __host__ __device__ constexpr int lu_ld(int n) {
 // shared memory of lb_getrf_kernel<KB>: panel [KB][ld] + U12 rows [KB][ld] + reduction scratch
 template <int KB>
 inline size_t getrf_smem_bytes(int n) {
-  return sizeof(double) * (2 * (size_t)KB * lu_ld<KB>(n) + 2 * 32 + KB * KB) +
-         sizeof(int) * (KB + 32 + lu_ld<KB>(n) + 4 * KB);
+  constexpr int NW = kGetrfThreads / 32;
+  return sizeof(double) * (2 * (size_t)KB * lu_ld<KB>(n) + 2 * 32 + KB * KB + 2 * NW * (KB + 2)) +
+         sizeof(int) * (KB + 32 + lu_ld<KB>(n) + 4 * KB + 4 * NW);
 }
 
 // Inverse diagonal blocks: per matrix, per panel p, invL[p] (KB x KB, unit
@@ -89,7 +109,7 @@ __device__ __forceinline__ void dmma_884(double (&d)[2], double a, double b) {
 }
 
 template <int KB>
-__global__ void __launch_bounds__(kLuThreads) lb_getrf_kernel(int n, double* const* __restrict__ As,
+__global__ void __launch_bounds__(kGetrfThreads) lb_getrf_kernel(int n, double* const* __restrict__ As,
                                                               int* __restrict__ ipiv_all,
                                                               int* __restrict__ perm_all,
                                                               int* __restrict__ info_all,
@@ -100,28 +120,166 @@ __global__ void __launch_bounds__(kLuThreads) lb_getrf_kernel(int n, double* con
   double* Ub = lu_sm + (size_t)KB * ld;  // U12 rows, row-major [KB][ld] (column offset from c0 + w)
   double* redv = Ub + (size_t)KB * ld;   // [32]
   double* iLs = redv + 64;               // [KB][KB] L11^-1 of the current panel (column-major)
-  int* redi = reinterpret_cast<int*>(iLs + KB * KB);  // [32]
+  // register panel: the warps' pivot candidates, double-buffered by column parity
+  constexpr int NT = kGetrfThreads;
+  constexpr int NW = NT / 32;
+  double* pr_rows = iLs + KB * KB;                            // [2][NW][KB] candidate rows
+  double* pr_rcp = pr_rows + 2 * NW * KB;                     // [2][NW] 1 / a of the candidates
+  unsigned long long* pr_key = reinterpret_cast<unsigned long long*>(pr_rcp + 2 * NW);  // [2][NW]
+  int* pr_slot = reinterpret_cast<int*>(pr_key + 2 * NW);     // [2][NW]
+  int* pr_thr = pr_slot + 2 * NW;                             // [2][NW]
+  int* redi = pr_thr + 2 * NW;                                // [32]
   int* pv_sh = redi + 32;                         // [KB]
   int* lp = pv_sh + KB;                           // [ld] panel-local row permutation
   int* tl_dst = lp + ld;                          // [2 KB] rows a panel's swaps touch
   int* tl_src = tl_dst + 2 * KB;                  // [2 KB] and where their values come from
   const int b = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  constexpr int NW = kLuThreads / 32;
   double* A = As[b];
   int* ipiv = ipiv_all ? ipiv_all + (size_t)b * n : nullptr;
   double* inv = inv_all + (size_t)b * lu_inv_stride<KB>(n);
   int info = 0;
 #ifdef LB_LU_PROF
-  long long t0_ = clock64(), pacc_[8] = {};
+  long long t0_ = clock64(), pacc_[8] = {}, pcol_[4] = {};
 #endif
 
   for (int c0 = 0, p = 0; c0 < n; c0 += KB, ++p) {
     const int w = min(KB, n - c0), m = n - c0;
+#if LB_LU_REGPANEL
+    // 1-3. Panel in registers: thread t holds panel row t (its KB columns,
+    //    compile-time indexed: the column loop is unrolled).  Rows never
+    //    move during the panel: the row chosen as pivot of column j retires
+    //    (it is row j of U); every other row takes l = a_j / d and its
+    //    rank-1 update in registers.  The LAPACK view is bookkeeping: each
+    //    thread tracks its row's slot, and the pivot is the largest |a| among
+    //    the live rows, ties to the smallest slot (idamax's first maximum
+    //    over slots j..m-1), so pivots and factors (the same operations in
+    //    the same order) are those of the shared-memory panel.  ONE barrier
+    //    per column, over the warps that own rows (named barrier 1): every
+    //    warp publishes its best candidate -- key, slot, thread, 1/a and the
+    //    row itself -- double-buffered by column parity, and after the
+    //    barrier every warp picks the winner among them.  Warp-level picks
+    //    are three redux.sync (max |a| as the high and low words of its bit
+    //    pattern, then the smallest slot) instead of shuffle trees.
+    const bool own = tid < m;
+    double v[KB];
+    {
+      const double* src = A + (size_t)c0 * n + c0 + tid;
+#pragma unroll
+      for (int k = 0; k < KB; ++k) v[k] = (own && k < w) ? src[(size_t)k * n] : 0.0;
+    }
+    for (int i = tid; i < ld; i += NT) lp[i] = i;  // slot -> panel-local row (after the panel)
+    int slot = tid;
+    bool done = false;  // this row is a pivot (a row of U) already
+    // every live row's 1 / a_j, computed as soon as a_j is final (the IEEE
+    // division overlaps the pivot search; the winner's is published)
+    double rcp = v[0] != 0.0 ? 1.0 / v[0] : 0.0;
+    // only the warps that own panel rows take part: the per-column overhead
+    // is issue- and latency-bound, and the panel shrinks by 32 rows a step
+    const int nact = (m + 31) >> 5;
+    __syncthreads();
+    LU_T(0);
+#pragma unroll
+    for (int j = 0; j < KB; ++j) {
+      if (j >= w || warp >= nact) break;
+      const int buf = j & 1;
+      double* rows = pr_rows + (size_t)buf * NW * KB;  // [NW][KB]
+      int wq = 0;  // entry of the pivot row
+      bool pub;    // this thread publishes its row
+      if (pivot) {
+        // key: live non-NaN rows by |a| (bit pattern, top bit set); the row
+        // holding slot j is the fallback when no row has a comparable |a|
+        const double av = fabs(v[j]);
+        const bool live = own && !done;
+        const unsigned long long key =
+            (live && av >= 0.0) ? (__double_as_longlong(av) | (1ull << 63)) : ((live && slot == j) ? 1ull : 0ull);
+        const unsigned hi = (unsigned)(key >> 32), lo = (unsigned)key;
+        const unsigned m1 = __reduce_max_sync(0xffffffffu, hi);
+        const unsigned m2 = __reduce_max_sync(0xffffffffu, hi == m1 ? lo : 0u);
+        const bool top = hi == m1 && lo == m2;
+        const unsigned ms = __reduce_min_sync(0xffffffffu, top ? (unsigned)slot : 0xffffffffu);
+        pub = top && (unsigned)slot == ms;  // this warp's candidate (one lane: slots are distinct)
+        if (pub) pr_key[buf * NW + warp] = key;
+      } else {
+        pub = tid == j;  // no pivoting: the row at slot j (thread j) is the pivot
+      }
+      if (pub) {
+        const int e = pivot ? warp : 0;
+        pr_slot[buf * NW + e] = slot;
+        pr_thr[buf * NW + e] = tid;
+        pr_rcp[buf * NW + e] = rcp;
+        double2* dst = reinterpret_cast<double2*>(rows + e * KB);
+#pragma unroll
+        for (int k = 2 * (j / 2); k < KB; k += 2) dst[k / 2] = make_double2(v[k], v[k + 1]);
+      }
+      asm volatile("bar.sync 1, %0;" ::"r"(nact * 32) : "memory");
+      if (pivot) {  // the winner among the warps' candidates (every warp, same answer)
+        const unsigned long long kq = lane < nact ? pr_key[buf * NW + lane] : 0ull;
+        const int sq = lane < nact ? pr_slot[buf * NW + lane] : INT_MAX;
+        const unsigned qh = (unsigned)(kq >> 32), ql = (unsigned)kq;
+        const unsigned g1 = __reduce_max_sync(0xffffffffu, qh);
+        const unsigned g2 = __reduce_max_sync(0xffffffffu, qh == g1 ? ql : 0u);
+        const bool gt = lane < nact && qh == g1 && ql == g2;
+        const unsigned gs = __reduce_min_sync(0xffffffffu, gt ? (unsigned)sq : 0xffffffffu);
+        wq = __ffs(__ballot_sync(0xffffffffu, gt && (unsigned)sq == gs)) - 1;
+      }
+      const int ps = pr_slot[buf * NW + wq], ph = pr_thr[buf * NW + wq];
+      LB_DCHECK(ps >= j && ps < m && ph >= 0 && ph < m);
+      const double* ur = rows + wq * KB;  // the pivot row: U row j
+      const double r = pr_rcp[buf * NW + wq];
+      LU_TC(0);
+      if (tid == 0) {
+        if (ur[j] == 0.0 && info == 0) info = c0 + j + 1;  // LAPACK info (first zero pivot)
+        pv_sh[j] = ps;
+      }
+      if (tid == ph) {
+        slot = j;
+        done = true;
+      } else if (slot == j) {
+        slot = ps;
+      }
+      if (own && !done) {  // zero pivot: r = 0, the column below is zero too
+        const double l = v[j] * r;
+        v[j] = l;
+#pragma unroll
+        for (int k = j + 1; k < KB; ++k) v[k] = fma(-l, ur[k], v[k]);
+        if (j + 1 < KB) rcp = v[j + 1] != 0.0 ? 1.0 / v[j + 1] : 0.0;
+      }
+      LU_TC(2);
+    }
+    __syncthreads();
+    // the factored panel by LAPACK slot in P (zero padding: rows m..ld,
+    // columns w..KB are zero in v)
+    if (own) {
+#pragma unroll
+      for (int k = 0; k < KB; ++k) P[(size_t)k * ld + slot] = v[k];
+    } else if (tid < ld) {
+#pragma unroll
+      for (int k = 0; k < KB; ++k) P[(size_t)k * ld + tid] = 0.0;
+    }
+    // slot -> panel-local row (the LAPACK swaps j <-> pv[j] in order) for
+    // the gather list below
+    if (tid == 0) {
+      for (int j = 0; j < w; ++j) {
+        const int q = pv_sh[j], t0 = lp[j];
+        lp[j] = lp[q];
+        lp[q] = t0;
+      }
+    }
+    __syncthreads();  // pv_sh / lp final
+    LU_T(1);
+    // the factored panel back to A (LAPACK layout)
+    for (int t = tid; t < w * m; t += NT) {
+      const int k = t / m, i = t - k * m;
+      A[(size_t)(c0 + k) * n + c0 + i] = P[(size_t)k * ld + i];
+    }
+    if (ipiv && tid < w) ipiv[c0 + tid] = c0 + pv_sh[tid] + 1;
+    __syncthreads();
+#else
     // 1. panel rows c0..n, columns c0..c0+w -> P (zero padding to ld rows /
     //    KB columns); rows tid + 256 h, eight columns of loads in flight
-    for (int i = tid; i < ld; i += kLuThreads) lp[i] = i;  // panel-local row permutation
-    for (int h = 0; h * kLuThreads < ld; ++h) {
-      const int i = tid + h * kLuThreads;
+    for (int i = tid; i < ld; i += NT) lp[i] = i;  // panel-local row permutation
+    for (int h = 0; h * NT < ld; ++h) {
+      const int i = tid + h * NT;
       if (i >= ld) break;
       const double* src = A + (size_t)c0 * n + c0 + i;
 #pragma unroll
@@ -143,7 +301,7 @@ __global__ void __launch_bounds__(kLuThreads) lb_getrf_kernel(int n, double* con
     double best = -1.0;
     int bi = m;
     if (pivot)
-      for (int i = tid; i < m; i += kLuThreads) {
+      for (int i = tid; i < m; i += NT) {
         const double v = fabs(P[i]);
         if (v > best) { best = v; bi = i; }  // rows visited in increasing order
       }
@@ -189,7 +347,7 @@ __global__ void __launch_bounds__(kLuThreads) lb_getrf_kernel(int n, double* con
       const double r = d != 0.0 ? 1.0 / d : 0.0;     // zero pivot: the column below is zero too
       best = -1.0;
       bi = m;
-      for (int i = j + 1 + tid; i < m; i += kLuThreads) {
+      for (int i = j + 1 + tid; i < m; i += NT) {
         const double l = P[(size_t)j * ld + i] * r;
         P[(size_t)j * ld + i] = l;
         int k = j + 1;
@@ -217,8 +375,9 @@ __global__ void __launch_bounds__(kLuThreads) lb_getrf_kernel(int n, double* con
     LU_T(1);
     // 3. panel back; pivots (1-based, global rows)
     for (int j = 0; j < w; ++j)
-      for (int i = tid; i < m; i += kLuThreads) A[(size_t)(c0 + j) * n + c0 + i] = P[(size_t)j * ld + i];
+      for (int i = tid; i < m; i += NT) A[(size_t)(c0 + j) * n + c0 + i] = P[(size_t)j * ld + i];
     if (ipiv && tid < w) ipiv[c0 + tid] = c0 + pv_sh[tid] + 1;
+#endif
     // 4. inverses of the diagonal blocks: unit lower L11 and upper U11 (one
     //    column of each inverse per thread)
     {
@@ -321,7 +480,7 @@ __global__ void __launch_bounds__(kLuThreads) lb_getrf_kernel(int n, double* con
     // columns (4 x 2 MMA tiles), written to Ub and back to A's rows c0..c0+w
     {
       const int lk = lane & 3, lr = lane >> 2;
-      constexpr int kMaxU = 3;  // ceil(ceil(383 / 16) / NW)
+      constexpr int kMaxU = (24 + NW - 1) / NW;  // ceil(ceil(383 / 16) / NW)
       double acc[kMaxU][4][2][2];
       const int nwt = (n2 + 15) >> 4;
 #pragma unroll
@@ -374,7 +533,7 @@ __global__ void __launch_bounds__(kLuThreads) lb_getrf_kernel(int n, double* con
       }
     }
     // zero padding of Ub's columns n2..n2+31 (32-column warp tiles read them)
-    for (int t = tid; t < KB * 32; t += kLuThreads) {
+    for (int t = tid; t < KB * 32; t += NT) {
       const int i = t >> 5, k2 = n2 + (t & 31);
       if (k2 < ld) Ub[(size_t)i * ld + k2] = 0.0;
     }
@@ -545,7 +704,7 @@ __global__ void __launch_bounds__(kLuThreads) lb_getrs_slab_kernel(int n, int m,
     for (int c = 0; c < W; ++c) X[(size_t)i * W + c] = (i < n && c < wc) ? Xg[(size_t)c * n + src] : 0.0;
   }
 #ifdef LB_LU_PROF
-  long long t0_ = clock64(), pacc_[8] = {};
+  long long t0_ = clock64(), pacc_[8] = {}, pcol_[4] = {};
 #endif
   for (int q = 0; q < nsteps; ++q) {
     int p, r0, kb, lo, hi;

@@ -50,14 +50,20 @@ int main(int argc, char** argv) {
     cudaMemcpy(dA, &A, sizeof(double*), cudaMemcpyHostToDevice);
     const size_t sf = getrf_smem_bytes<KB>(n);
     cudaFuncSetAttribute(lb_getrf_kernel<KB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sf);
-    for (int rep = 0; rep < 2; ++rep) {
+    for (int i = 0; i < n; ++i) hA[(size_t)i * n + i] += 4.0;  // (unpivoted rep stays stable)
+    for (int rep = 0; rep < 4; ++rep) {
+      const int pv = rep < 2;  // reps 0, 1 pivoted; 2, 3 unpivoted
+      if (rep == 2) printf("(unpivoted)\n");
       cudaMemcpy(A, hA.data(), nn * 8, cudaMemcpyHostToDevice);
       long long z[8] = {};
       cudaMemcpyToSymbol(lu_prof, z, sizeof(z));
-      lb_getrf_kernel<KB><<<1, kLuThreads, sf>>>(n, dA, piv, perm, info, inv, 1);
+      cudaMemcpyToSymbol(lu_prof2, z, 4 * sizeof(long long));
+      lb_getrf_kernel<KB><<<1, kGetrfThreads, sf>>>(n, dA, piv, perm, info, inv, pv);
       cudaDeviceSynchronize();
-      long long h[8];
+      long long h[8], h2[4];
       cudaMemcpyFromSymbol(h, lu_prof, sizeof(h));
+      cudaMemcpyFromSymbol(h2, lu_prof2, sizeof(h2));
+      printf("  column loop (thread 0): reduction %lld, pivot row %lld, update %lld cycles\n", h2[0], h2[1], h2[2]);
       long long tot = 0;
       for (int k = 0; k < 5; ++k) tot += h[k];
       tot += h[5] + h[6];
@@ -138,7 +144,7 @@ int main(int argc, char** argv) {
           cudaMemcpy(A, A0, nn * batch * 8, cudaMemcpyDeviceToDevice);
           cudaMemcpy(B, B0, nm * batch * 8, cudaMemcpyDeviceToDevice);
           cudaEventRecord(e0);
-          lb_getrf_kernel<KB><<<batch, kLuThreads, sf>>>(n, dA, piv, perm, info, inv, 1);
+          lb_getrf_kernel<KB><<<batch, kGetrfThreads, sf>>>(n, dA, piv, perm, info, inv, 1);
           cudaEventRecord(e1);
           cudaEventSynchronize(e1);
           cudaEventElapsedTime(&tc_f, e0, e1);
