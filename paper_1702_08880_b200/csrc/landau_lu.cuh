@@ -211,7 +211,9 @@ __global__ void __launch_bounds__(kGetrfThreads) lb_getrf_kernel(int n, double* 
 #pragma unroll
         for (int k = 2 * (j / 2); k < KB; k += 2) dst[k / 2] = make_double2(v[k], v[k + 1]);
       }
+      LU_TC(1);
       asm volatile("bar.sync 1, %0;" ::"r"(nact * 32) : "memory");
+      LU_TC(3);
       if (pivot) {  // the winner among the warps' candidates (every warp, same answer)
         const unsigned long long kq = lane < nact ? pr_key[buf * NW + lane] : 0ull;
         const int sq = lane < nact ? pr_slot[buf * NW + lane] : INT_MAX;

@@ -63,7 +63,7 @@ int main(int argc, char** argv) {
       long long h[8], h2[4];
       cudaMemcpyFromSymbol(h, lu_prof, sizeof(h));
       cudaMemcpyFromSymbol(h2, lu_prof2, sizeof(h2));
-      printf("  column loop (thread 0): reduction %lld, pivot row %lld, update %lld cycles\n", h2[0], h2[1], h2[2]);
+      printf("  column loop (thread 0): candidates+publish %lld, barrier issue %lld, winner+loads %lld, update %lld cycles\n", h2[1], h2[3], h2[0], h2[2]);
       long long tot = 0;
       for (int k = 0; k < 5; ++k) tot += h[k];
       tot += h[5] + h[6];
