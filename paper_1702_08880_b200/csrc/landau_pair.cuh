@@ -339,13 +339,22 @@ __device__ __forceinline__ PairB pair_core(const Outer& o, double rn, double zn,
 __device__ __forceinline__ double pair_w2(const PairB& p) {
   return fma(-(p.rr + p.rr), p.c34, fma(-(p.dr * p.dr), p.B3, p.B1));
 }
+#ifndef LB_SHARED_U
+#define LB_SHARED_U 1  // UD_xz and UK_zr share rn c34 (one FP64 operation fewer per pair)
+#endif
 __device__ __forceinline__ T5 pair_tensors(double rn, double rn2, const PairB& p, double w2) {
   T5 t;
   t.xx = fma(rn2, p.c35, w2);
   t.zz = fma(-p.dz2, p.B3, p.B1);
+#if LB_SHARED_U
+  const double u = rn * p.c34;
+  t.xz = -p.dz * fma(p.dr, p.B3, u);
+  t.zr = p.dz * fma(-p.dr, p.B4, u);
+#else
   t.xz = -p.dz * fma(p.dr, p.B3, rn * p.c34);
-  t.kr = fma(p.rr, p.c35, p.dz2 * p.B4);
   t.zr = p.dz * fma(rn, p.c34, -(p.dr * p.B4));
+#endif
+  t.kr = fma(p.rr, p.c35, p.dz2 * p.B4);
   return t;  // masked pairs: all B and c are zero (pair_core), so is every component
 }
 

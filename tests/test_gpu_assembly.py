@@ -56,6 +56,40 @@ def test_element_kernel_matches_restatement(gpu, oracle):
     assert np.all(phase >= 0)
 
 
+def test_elements_dev_entry(gpu):
+    """lb_elements_dev (device pointers; the basis becomes a by-value kernel
+    parameter, read back once): bitwise the host entry's element matrices,
+    also with K/D at an 8-byte (not 16-byte) aligned address."""
+    import ctypes as C
+
+    import torch
+
+    from paper_1702_08880_b200 import _lib
+
+    g = golden("cfg2")
+    mesh, ref = mesh_from(g), ref_from(g)
+    elem, _, K, D = gpu.element_matrices(mesh, ref, data_from(g), params_from(g), return_kd=True)
+    S, ncell = elem.shape[0], mesh.n_cells
+    dev = torch.device("cuda", 0)
+    t = lambda a: torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64)).to(dev)  # noqa: E731
+    sizes, w = t(mesh.sizes), t(g["w"])
+    B, dB = t(ref.B), t(ref.dB)
+    for off in (0, 1):  # off = 1: K and D one double into their buffers
+        Kb = torch.zeros(K.size + off, dtype=torch.float64, device=dev)
+        Db = torch.zeros(D.size + off, dtype=torch.float64, device=dev)
+        Kb[off:] = t(K.ravel())
+        Db[off:] = t(D.ravel())
+        out = torch.full((S * ncell * 81,), np.nan, dtype=torch.float64, device=dev)
+        p = lambda x, o=0: C.c_void_p(x.data_ptr() + 8 * o)  # noqa: E731
+        stream = torch.cuda.current_stream(dev)
+        ctx = _lib.context(0)
+        _lib.check(_lib.load().lb_elements_dev(ctx.handle, ncell, S, p(sizes), p(w), p(Kb, off), p(Db, off),
+                                               p(B), p(dB), p(out), C.c_void_p(stream.cuda_stream)))
+        torch.cuda.synchronize(dev)
+        got = out.cpu().numpy().reshape(elem.shape)
+        assert np.array_equal(got, elem), f"offset {off}"
+
+
 def test_mass_identity(gpu):
     """1^T (C_a f_a) = 0 (test_assembly.py:64-76) on the reference fixtures."""
     for case in ("cfg1", "hanging", "cfg2"):
