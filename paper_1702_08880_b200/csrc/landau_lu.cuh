@@ -642,8 +642,8 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
-template <int KB, int W>
-__global__ void __launch_bounds__(kLuThreads) lb_getrs_slab_kernel(int n, int m, double* const* __restrict__ As,
+template <int KB, int W, int NT = kLuThreads>
+__global__ void __launch_bounds__(NT) lb_getrs_slab_kernel(int n, int m, double* const* __restrict__ As,
                                                                    const int* __restrict__ perm_all,
                                                                    const double* __restrict__ inv_all,
                                                                    double* const* __restrict__ Xs) {
@@ -681,26 +681,26 @@ __global__ void __launch_bounds__(kLuThreads) lb_getrs_slab_kernel(int n, int m,
     const int k_end = min(KH, kb - h * KH);
     if (pairs) {
       const int np2 = (hi - lo) >> 1;  // row pairs (hi - lo is even)
-      for (int t = tid; t < k_end * np2; t += kLuThreads) {
+      for (int t = tid; t < k_end * np2; t += NT) {
         const int k = t / np2, i = lo + 2 * (t - k * np2);
         cp_async16(dst + (size_t)k * ld + i, A + (size_t)(r0 + h * KH + k) * n + i);
       }
     } else {
       for (int k = 0; k < k_end; ++k) {
         const double* src = A + (size_t)(r0 + h * KH + k) * n;
-        for (int i = lo + tid; i < hi; i += kLuThreads) cp_async8(dst + (size_t)k * ld + i, src + i);
+        for (int i = lo + tid; i < hi; i += NT) cp_async8(dst + (size_t)k * ld + i, src + i);
       }
     }
     if (h == 0) {  // Di of step q: its buffer is free once step q-1's Di product is done
       const double* di = inv + (size_t)(q < np ? 2 * p : 2 * p + 1) * KB * KB;
-      for (int t = 2 * tid; t < KB * KB; t += 2 * kLuThreads) cp_async16(Dis + t, di + t);
+      for (int t = 2 * tid; t < KB * KB; t += 2 * NT) cp_async16(Dis + t, di + t);
     }
     cp_async_commit();
   };
   issue(0, 0);
   issue(0, 1);
   // gather P X into shared memory (zero rows n..ld, zero columns wc..W)
-  for (int i = tid; i < ld; i += kLuThreads) {  // consecutive threads: consecutive rows of a column
+  for (int i = tid; i < ld; i += NT) {  // consecutive threads: consecutive rows of a column
     const int src = (i < n) ? (perm ? perm[i] : i) : 0;
 #pragma unroll 8
     for (int c = 0; c < W; ++c) X[(size_t)i * W + c] = (i < n && c < wc) ? Xg[(size_t)c * n + src] : 0.0;
@@ -719,8 +719,10 @@ __global__ void __launch_bounds__(kLuThreads) lb_getrs_slab_kernel(int n, int m,
     const double* Di = Dis;
     {
       static_assert(KB == 32 && (W == 32 || W == 64), "DMMA tiling assumes 32-row blocks, 32/64-column slabs");
-      constexpr int TPW = W / 16;
-      const int m = warp >> 1, n0 = (warp & 1) * TPW, lr = lane >> 2, lk = lane & 3;
+      constexpr int NWS = NT / 32;
+      static_assert(NWS % 4 == 0 && (W / 8) % (NWS / 4) == 0, "4 row tiles x (W/8) column tiles over the warps");
+      constexpr int TPW = (W / 8) / (NWS / 4);  // column tiles per warp
+      const int m = warp & 3, n0 = (warp >> 2) * TPW, lr = lane >> 2, lk = lane & 3;
       double d[TPW][2];
 #pragma unroll
       for (int nn = 0; nn < TPW; ++nn) d[nn][0] = d[nn][1] = 0.0;
@@ -740,7 +742,7 @@ __global__ void __launch_bounds__(kLuThreads) lb_getrs_slab_kernel(int n, int m,
             make_double2(d[nn][0], d[nn][1]);
     }
     __syncthreads();
-    for (int t = tid; t < KB * CG; t += kLuThreads) {  // the block's rows of X become Y
+    for (int t = tid; t < KB * CG; t += NT) {  // the block's rows of X become Y
       const int yi = t / CG, yc = (t - (t / CG) * CG) * 4;
       if (yi < kb) {
         *reinterpret_cast<double2*>(X + (size_t)(r0 + yi) * W + yc) =
@@ -754,7 +756,7 @@ __global__ void __launch_bounds__(kLuThreads) lb_getrs_slab_kernel(int n, int m,
     // 16 rows x 32 columns (2 x 4 MMA tiles of 8 x 8), acc kept across halves
     constexpr int CGW = W / 32;            // 32-column groups
     const int nr = hi - lo, nwt = ((nr + 15) >> 4) * CGW;
-    constexpr int kMaxWt = 3 * CGW;        // ceil(ceil(383 / 16) CGW / 8)
+    constexpr int kMaxWt = (24 * CGW + NT / 32 - 1) / (NT / 32);  // ceil(ceil(383 / 16) CGW / warps)
     double acc[kMaxWt][2][4][2];
 #pragma unroll
     for (int u = 0; u < kMaxWt; ++u)
@@ -769,7 +771,7 @@ __global__ void __launch_bounds__(kLuThreads) lb_getrs_slab_kernel(int n, int m,
       const double* Hh = H[h] + lo;
 #pragma unroll
       for (int u = 0; u < kMaxWt; ++u) {
-        const int t = warp + u * (kLuThreads / 32);
+        const int t = warp + u * (NT / 32);
         if (t >= nwt) break;
         const int wt = t / CGW, cg = t - (t / CGW) * CGW;
 #pragma unroll
@@ -795,7 +797,7 @@ __global__ void __launch_bounds__(kLuThreads) lb_getrs_slab_kernel(int n, int m,
     LU_T(3);
 #pragma unroll
     for (int u = 0; u < kMaxWt; ++u) {
-      const int t = warp + u * (kLuThreads / 32);
+      const int t = warp + u * (NT / 32);
       if (t >= nwt) break;
       const int wt = t / CGW, cg = t - (t / CGW) * CGW;
 #pragma unroll
@@ -819,7 +821,7 @@ __global__ void __launch_bounds__(kLuThreads) lb_getrs_slab_kernel(int n, int m,
   cp_async_wait<0>();
   __syncthreads();
   for (int c = 0; c < wc; ++c)
-    for (int i = tid; i < n; i += kLuThreads) Xg[(size_t)c * n + i] = X[(size_t)i * W + c];
+    for (int i = tid; i < n; i += NT) Xg[(size_t)c * n + i] = X[(size_t)i * W + c];
 }
 
 // v := A^-1 v for one vector per block (the cyclic reduction's vector

@@ -210,8 +210,11 @@ struct PairB {
 // lookup -- the long-latency front (MUFU, shared-memory table) that the
 // symmetric sweep issues one step ahead of the rest.
 struct PairS1 {
-  double dz, dz2, dr, P, rr, isPm, invP, x, lr, logc, kd;
+  double dz, dz2, dr, d2, P, rr, isPm, invP, x, lr, logc, kd;
 };
+#ifndef LB_B3_RD2
+#define LB_B3_RD2 1  // B3 from 1/d^2 (one FP64 operation fewer per pair than from 1/x and P^-3/2)
+#endif
 
 // MG ("merged guard"): when the mask threshold is above the d^2 guard
 // (eps_d^2 > 1e-300, e.g. assemble_collision's 1e-14 L), every pair the
@@ -229,6 +232,7 @@ __device__ __forceinline__ PairS1 pair_stage1(const Outer& o, double rn, double 
   const long long di = __double_as_longlong(dist2);
   const bool g = di >= gthr;  // d^2 >= eps^2 and d^2 > 0 (kernel.py:344)
   const double d2 = (MG ? g : di > kTinyBits) ? dist2 : 1.0;
+  s.d2 = d2;
   // ri rn; 4 ri rn and 2 ri rn below are exact scalings of it, so P, m and
   // u round exactly as with (4 ri) rn and (2 ri) rn
   s.rr = o.ri * rn;
@@ -285,12 +289,17 @@ __device__ __forceinline__ PairB pair_stage2(const Outer& o, double rn, double r
 #endif
   const double EK = fma(-lx, qk, pk);
   const double EE = fma(-lx, qe, pe);
-  const double Em1 = EE * rcp_nr(x);  // E/(1-m) = E P/d^2
   const double isPm = s.isPm;
-  const double c3 = isPm * invP;  // P^-3/2 (the 4 is folded into the coupling)
   PairB p;
   p.B1 = EK * isPm;
-  p.B3 = Em1 * c3;
+#if LB_B3_RD2
+  // B3 = Em1 c3 = E (P/d^2) P^-3/2 = E P^-1/2 / d^2: one reciprocal of d^2
+  // instead of 1/x and P^-3/2 (c3 is only needed by the rare series branch)
+  p.B3 = EE * (isPm * rcp_nr(s.d2));
+#else
+  const double Em1 = EE * rcp_nr(x);  // E/(1-m) = E P/d^2
+  p.B3 = Em1 * (isPm * invP);
+#endif
   // m < 0.01 (kernel.py:376) tested as x = 1 - m > 0.99 on the bit pattern;
   // m itself is only needed by the series
   if (__double_as_longlong(x) > kXSwitchBits) {
@@ -307,17 +316,19 @@ __device__ __forceinline__ PairB pair_stage2(const Outer& o, double rn, double r
     s2 = fma(s2, m, c_s2[1]);  s3 = fma(s3, m, c_s3[1]);
     const double S2 = s2 * m;
     const double S3 = fma(s3, m, c_s3[0]);
+    const double c3 = isPm * invP;  // P^-3/2 (the 4 is folded into the coupling)
     p.B4 = S2 * c3;
-    p.c34 = (Em1 - S2) * c3;
-    p.c35 = (Em1 - S3) * c3;
+    p.c34 = fma(-S2, c3, p.B3);  // (Em1 - S2) c3
+    p.c35 = fma(-S3, c3, p.B3);  // (Em1 - S3) c3
   } else {
     // closed form (kernel.py:366-367) as the differences from Em1, in
     // 2/m = P/(2 ri rn) (m >= 0.01, so rn > 0):
     //   Em1 - S2 = (2/m)(K - E),  Em1 - S3 = (2/m)^2 ((1 + x) K - 2 E)
-    const double invm2 = P * o.rtri * rcpr;  // 2/m
-    const double cq = c3 * invm2;
+    // with c3 (2/m) = P^-1/2 / (2 ri rn)
+    const double a = o.rtri * rcpr;  // 1/(2 ri rn)
+    const double cq = isPm * a;      // c3 2/m
     p.c34 = cq * (EK - EE);
-    p.c35 = (cq * invm2) * fma(x, EK, fma(-2.0, EE, EK));  // ((1 + x) K - 2 E)
+    p.c35 = (cq * (P * a)) * fma(x, EK, fma(-2.0, EE, EK));  // ((1 + x) K - 2 E)
     p.B4 = p.B3 - p.c34;
   }
   p.dz = s.dz;
@@ -420,7 +431,9 @@ __device__ __forceinline__ void pair_tensor_sym_x(const Outer (&oo)[U], const do
     }
   }
   PairB p[U];
+#if !LB_B3_RD2
   double Em1[U];
+#endif
 #pragma unroll
   for (int u = 0; u < U; ++u) {
     pk[u] = fma(pk[u], x[u], c_pk[0]);
@@ -429,10 +442,20 @@ __device__ __forceinline__ void pair_tensor_sym_x(const Outer (&oo)[U], const do
     qe[u] = qe[u] * x[u];
     const double EK = fma(-lx[u], qk[u], pk[u]);
     const double EE = fma(-lx[u], qe[u], pe[u]);
-    Em1[u] = EE * rcp_nr(x[u]);  // E/(1-m) = E P/d^2
     const double isPm = s[u].isPm;
-    const double c3 = isPm * s[u].invP;  // P^-3/2 (the 4 is folded into the coupling)
     p[u].B1 = EK * isPm;
+#if LB_B3_RD2
+    p[u].B3 = EE * (isPm * rcp_nr(s[u].d2));  // E P^-1/2 / d^2 = Em1 c3
+    // closed form (kernel.py:366-367) as the differences from Em1 (header):
+    // Em1 - S2 = (2/m)(K - E), Em1 - S3 = (2/m)^2 ((1 + x) K - 2 E);
+    // c3 (2/m) = P^-1/2 / (2 ri rn)
+    const double a = oo[u].rtri * rcpr[u];  // 1/(2 ri rn)
+    const double cq = isPm * a;
+    p[u].c34 = cq * (EK - EE);
+    p[u].c35 = (cq * (s[u].P * a)) * fma(x[u], EK, fma(-2.0, EE, EK));  // ((1 + x) K - 2 E)
+#else
+    Em1[u] = EE * rcp_nr(x[u]);  // E/(1-m) = E P/d^2
+    const double c3 = isPm * s[u].invP;  // P^-3/2 (the 4 is folded into the coupling)
     p[u].B3 = Em1[u] * c3;
     // closed form (kernel.py:366-367) as the differences from Em1 (header):
     // Em1 - S2 = (2/m)(K - E), Em1 - S3 = (2/m)^2 ((1 + x) K - 2 E)
@@ -440,6 +463,7 @@ __device__ __forceinline__ void pair_tensor_sym_x(const Outer (&oo)[U], const do
     const double cq = c3 * invm2;
     p[u].c34 = cq * (EK - EE);
     p[u].c35 = (cq * invm2) * fma(x[u], EK, fma(-2.0, EE, EK));  // ((1 + x) K - 2 E)
+#endif
     p[u].B4 = p[u].B3 - p[u].c34;
     p[u].dz = s[u].dz;
     p[u].dz2 = s[u].dz2;
@@ -462,8 +486,8 @@ __device__ __forceinline__ void pair_tensor_sym_x(const Outer (&oo)[U], const do
       const double c3 = s[u].isPm * s[u].invP;
       const double S2 = s2 * m, S3 = fma(s3, m, c_s3[0]);
       p[u].B4 = S2 * c3;
-      p[u].c34 = (Em1[u] - S2) * c3;
-      p[u].c35 = (Em1[u] - S3) * c3;
+      p[u].c34 = fma(-S2, c3, p[u].B3);  // (Em1 - S2) c3
+      p[u].c35 = fma(-S3, c3, p[u].B3);  // (Em1 - S3) c3
     }
   }
 #else
@@ -495,7 +519,7 @@ __device__ __forceinline__ void pair_tensor_sym_x(const Outer (&oo)[U], const do
     for (int u = 0; u < U; ++u) {
       const double c3 = s[u].isPm * s[u].invP;
       const double S2 = s2[u] * m[u], S3 = fma(s3[u], m[u], c_s3[0]);
-      const double b4 = S2 * c3, d34 = (Em1[u] - S2) * c3, d35 = (Em1[u] - S3) * c3;
+      const double b4 = S2 * c3, d34 = fma(-S2, c3, p[u].B3), d35 = fma(-S3, c3, p[u].B3);  // (Em1 - S.) c3
       p[u].B4 = ser[u] ? b4 : p[u].B4;
       p[u].c34 = ser[u] ? d34 : p[u].c34;
       p[u].c35 = ser[u] ? d35 : p[u].c35;
