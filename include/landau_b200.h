@@ -224,7 +224,10 @@ int lb_sweep_dev(lb_ctx *ctx, int nout, const double *outer_r, const double *out
                  double eps_d, double *K_out, double *D_out, void *stream);
 
 /* Outer-point transform + element contraction from device K/D
- * (assembly.py:151-165).  w (9*ncell) outer weights, cell_sizes (ncell,2). */
+ * (assembly.py:151-165).  w (9*ncell) outer weights, cell_sizes (ncell,2).
+ * The 243 basis values B/dB become a by-value kernel parameter: this entry
+ * reads them back from the device once (a synchronisation of `stream`);
+ * the mesh entries (lb_mesh_create) keep a host copy instead. */
 int lb_elements_dev(lb_ctx *ctx, int ncell, int S, const double *cell_sizes,
                     const double *w, const double *K, const double *D,
                     const double *B, const double *dB, double *elem_out, void *stream);
