@@ -350,7 +350,7 @@ __global__ void lb_pairs_kernel(int npair, const double* __restrict__ r, const d
   if (p >= npair) return;
   const Outer o = make_outer(r[p], z[p]);
   const double rn = rb[p];
-  const T5 t = pair_tensor(o, rn, zb[p], rn * rn, rn > 0.0 ? 1.0 / rn : 0.0, 1LL, logt);
+  const T5 t = pair_tensor(o, rn, zb[p], 4.0 * (rn * rn), rn > 0.0 ? 1.0 / rn : 0.0, 1LL, logt);
   // restore the pulled-out factor 4 (exact) and lay out as kernel.py:227-234
   UD[4 * p + 0] = 4.0 * t.xx;
   UD[4 * p + 1] = 4.0 * t.xz;

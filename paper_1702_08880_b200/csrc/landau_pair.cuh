@@ -173,22 +173,34 @@ __device__ __forceinline__ double log_table(double x, const double2* __restrict_
   return log_finish(r, logc, kd);
 }
 
-// Per-outer-point invariants (hoisted out of the pair loop).
+// Per-outer-point invariants (hoisted out of the pair loop).  Scaled by
+// exact powers of two (see "Scaled pair quantities" below).
 struct Outer {
   double ri, zi;
-  double ri2;   // ri*ri
-  double rtri;  // 1/(2 ri), 0 when ri == 0 (then m == 0 and the series runs)
+  double ri2;   // 4 ri^2
+  double rtri;  // 1/(4 ri), 0 when ri == 0 (then m == 0 and the series runs)
+  double ri4;   // 4 ri
 };
 
 __device__ __forceinline__ Outer make_outer(double ri, double zi) {
   Outer o;
   o.ri = ri;
   o.zi = zi;
-  o.ri2 = ri * ri;
-  o.rtri = ri > 0.0 ? 1.0 / (2.0 * ri) : 0.0;
+  o.ri2 = 4.0 * (ri * ri);
+  o.rtri = ri > 0.0 ? 1.0 / (4.0 * ri) : 0.0;
+  o.ri4 = 4.0 * ri;
   return o;
 }
 
+// Scaled pair quantities.  Every factor below is an exact power of two, so
+// each rounded value is the unscaled one times that power and the tensor
+// components are bitwise those of the unscaled formulas; the scalings only
+// let the products meet without extra multiplications:
+//   rq = 4 ri rn (P = rq + d^2, m = rq / P),
+//   c34' = c34 / 2 and c35' = c35 / 4 (from 1/(4 ri rn) instead of 1/(2 ri rn)),
+//   records carry 4 rn^2 and 2 rn, outer points 4 ri^2:
+//   2 ri rn c34 = rq c34',  ri rn c35 = rq c35',  rn^2 c35 = (4 rn^2) c35',
+//   rn c34 = (2 rn) c34',  ri^2 c35 = (4 ri^2) c35',  B4 = B3 - 2 c34'.
 // The five distinct tensor components, each scaled by 1/4:
 //   xx = UD_xx, zz = UD_zz = UK_zz, xz = UD_xz = UD_zx = UK_rz,
 //   kr = UK_rr, zr = UK_zr                                   (kernel.py:384-389)
@@ -200,8 +212,8 @@ struct T5 {
 // B1, B3, B4 and the differences c34 = B3 - B4, c35 = B3 - B5 in their
 // well-conditioned closed forms; dz, dz^2, dr = ri - rn and ri rn.
 struct PairB {
-  double B1, B3, B4, c34, c35;
-  double dz, dz2, dr, rr;
+  double B1, B3, B4, c34, c35;  // c34 = (B3 - B4) / 2, c35 = (B3 - B5) / 4 (scaled)
+  double dz, dz2, dr, rr;       // rr = 4 ri rn
 };
 
 // gthr = max(bits(eps^2), 1): the pair contributes iff bits(d^2) >= gthr,
@@ -212,9 +224,7 @@ struct PairB {
 struct PairS1 {
   double dz, dz2, dr, d2, P, rr, isPm, invP, x, lr, logc, kd;
 };
-#ifndef LB_B3_RD2
-#define LB_B3_RD2 1  // B3 from 1/d^2 (one FP64 operation fewer per pair than from 1/x and P^-3/2)
-#endif
+
 
 // MG ("merged guard"): when the mask threshold is above the d^2 guard
 // (eps_d^2 > 1e-300, e.g. assemble_collision's 1e-14 L), every pair the
@@ -235,8 +245,8 @@ __device__ __forceinline__ PairS1 pair_stage1(const Outer& o, double rn, double 
   s.d2 = d2;
   // ri rn; 4 ri rn and 2 ri rn below are exact scalings of it, so P, m and
   // u round exactly as with (4 ri) rn and (2 ri) rn
-  s.rr = o.ri * rn;
-  s.P = fma(4.0, s.rr, d2);
+  s.rr = o.ri4 * rn;  // 4 ri rn (exactly 4 (ri rn))
+  s.P = s.rr + d2;
   const double isP = rsqrt_nr(s.P);
   s.invP = isP * isP;
   s.x = d2 * s.invP;
@@ -292,19 +302,14 @@ __device__ __forceinline__ PairB pair_stage2(const Outer& o, double rn, double r
   const double isPm = s.isPm;
   PairB p;
   p.B1 = EK * isPm;
-#if LB_B3_RD2
   // B3 = Em1 c3 = E (P/d^2) P^-3/2 = E P^-1/2 / d^2: one reciprocal of d^2
   // instead of 1/x and P^-3/2 (c3 is only needed by the rare series branch)
   p.B3 = EE * (isPm * rcp_nr(s.d2));
-#else
-  const double Em1 = EE * rcp_nr(x);  // E/(1-m) = E P/d^2
-  p.B3 = Em1 * (isPm * invP);
-#endif
   // m < 0.01 (kernel.py:376) tested as x = 1 - m > 0.99 on the bit pattern;
   // m itself is only needed by the series
   if (__double_as_longlong(x) > kXSwitchBits) {
     // hypergeometric series (kernel.py:369-375)
-    const double m = (4.0 * s.rr) * invP;
+    const double m = s.rr * invP;
     double s2 = c_s2[9], s3 = c_s3[9];
     s2 = fma(s2, m, c_s2[8]);  s3 = fma(s3, m, c_s3[8]);
     s2 = fma(s2, m, c_s2[7]);  s3 = fma(s3, m, c_s3[7]);
@@ -318,18 +323,18 @@ __device__ __forceinline__ PairB pair_stage2(const Outer& o, double rn, double r
     const double S3 = fma(s3, m, c_s3[0]);
     const double c3 = isPm * invP;  // P^-3/2 (the 4 is folded into the coupling)
     p.B4 = S2 * c3;
-    p.c34 = fma(-S2, c3, p.B3);  // (Em1 - S2) c3
-    p.c35 = fma(-S3, c3, p.B3);  // (Em1 - S3) c3
+    p.c34 = 0.5 * fma(-S2, c3, p.B3);   // (Em1 - S2) c3 / 2
+    p.c35 = 0.25 * fma(-S3, c3, p.B3);  // (Em1 - S3) c3 / 4
   } else {
     // closed form (kernel.py:366-367) as the differences from Em1, in
     // 2/m = P/(2 ri rn) (m >= 0.01, so rn > 0):
     //   Em1 - S2 = (2/m)(K - E),  Em1 - S3 = (2/m)^2 ((1 + x) K - 2 E)
-    // with c3 (2/m) = P^-1/2 / (2 ri rn)
-    const double a = o.rtri * rcpr;  // 1/(2 ri rn)
-    const double cq = isPm * a;      // c3 2/m
+    // with c3 (2/m) = P^-1/2 / (2 ri rn); scaled: a = 1/(4 ri rn)
+    const double a = o.rtri * rcpr;  // 1/(4 ri rn)
+    const double cq = isPm * a;      // c3 (2/m) / 2
     p.c34 = cq * (EK - EE);
-    p.c35 = (cq * (P * a)) * fma(x, EK, fma(-2.0, EE, EK));  // ((1 + x) K - 2 E)
-    p.B4 = p.B3 - p.c34;
+    p.c35 = (cq * (P * a)) * fma(x, EK, fma(-2.0, EE, EK));  // ((1 + x) K - 2 E) / 4
+    p.B4 = fma(-2.0, p.c34, p.B3);
   }
   p.dz = s.dz;
   p.dz2 = s.dz2;
@@ -348,22 +353,24 @@ __device__ __forceinline__ PairB pair_core(const Outer& o, double rn, double zn,
 // rearranged, see the header): w2 = B1 - dr^2 B3 - 2 ri rn c34 is shared by
 // UD_xx of both orientations.
 __device__ __forceinline__ double pair_w2(const PairB& p) {
-  return fma(-(p.rr + p.rr), p.c34, fma(-(p.dr * p.dr), p.B3, p.B1));
+  return fma(-p.rr, p.c34, fma(-(p.dr * p.dr), p.B3, p.B1));  // 2 ri rn c34 = rq c34'
+
 }
 #ifndef LB_SHARED_U
 #define LB_SHARED_U 1  // UD_xz and UK_zr share rn c34 (one FP64 operation fewer per pair)
 #endif
-__device__ __forceinline__ T5 pair_tensors(double rn, double rn2, const PairB& p, double w2) {
+// rnx = 2 rn, rn2 = 4 rn^2 (the record's scaled fields)
+__device__ __forceinline__ T5 pair_tensors(double rnx, double rn2, const PairB& p, double w2) {
   T5 t;
   t.xx = fma(rn2, p.c35, w2);
   t.zz = fma(-p.dz2, p.B3, p.B1);
 #if LB_SHARED_U
-  const double u = rn * p.c34;
+  const double u = rnx * p.c34;  // rn c34
   t.xz = -p.dz * fma(p.dr, p.B3, u);
   t.zr = p.dz * fma(-p.dr, p.B4, u);
 #else
-  t.xz = -p.dz * fma(p.dr, p.B3, rn * p.c34);
-  t.zr = p.dz * fma(rn, p.c34, -(p.dr * p.B4));
+  t.xz = -p.dz * fma(p.dr, p.B3, rnx * p.c34);
+  t.zr = p.dz * fma(rnx, p.c34, -(p.dr * p.B4));
 #endif
   t.kr = fma(p.rr, p.c35, p.dz2 * p.B4);
   return t;  // masked pairs: all B and c are zero (pair_core), so is every component
@@ -374,7 +381,7 @@ __device__ __forceinline__ T5 pair_tensor(const Outer& o, double rn, double zn, 
                                           double rcpr, long long gthr,
                                           const double2* __restrict__ logt) {
   const PairB p = pair_core(o, rn, zn, rcpr, gthr, logt);
-  return pair_tensors(rn, rn2, p, pair_w2(p));
+  return pair_tensors(rn + rn, rn2, p, pair_w2(p));  // rn2: the record's 4 rn^2
 }
 
 // One unordered pair: the direct components in `t` and, returned, the one
@@ -385,7 +392,7 @@ __device__ __forceinline__ double pair_tensor_sym(const Outer& o, double rn, dou
                                                   const double2* __restrict__ logt, T5& t) {
   const PairB p = pair_core(o, rn, zn, rcpr, gthr, logt);
   const double w2 = pair_w2(p);
-  t = pair_tensors(rn, rn2, p, w2);
+  t = pair_tensors(rn + rn, rn2, p, w2);  // rn2: the record's 4 rn^2
   return fma(o.ri2, p.c35, w2);
 }
 
@@ -399,6 +406,7 @@ __device__ __forceinline__ double pair_tensor_sym(const Outer& o, double rn, dou
 template <int U, bool MG = false>
 __device__ __forceinline__ void pair_tensor_sym_x(const Outer (&oo)[U], const double (&rn)[U],
                                                   const double (&zn)[U], const double (&rn2)[U],
+                                                  const double (&rnx)[U],
                                                   const double (&rcpr)[U], long long gthr,
                                                   const double2* __restrict__ logt, T5 (&t)[U],
                                                   double (&txx2)[U], unsigned& nser) {
@@ -431,9 +439,6 @@ __device__ __forceinline__ void pair_tensor_sym_x(const Outer (&oo)[U], const do
     }
   }
   PairB p[U];
-#if !LB_B3_RD2
-  double Em1[U];
-#endif
 #pragma unroll
   for (int u = 0; u < U; ++u) {
     pk[u] = fma(pk[u], x[u], c_pk[0]);
@@ -444,27 +449,15 @@ __device__ __forceinline__ void pair_tensor_sym_x(const Outer (&oo)[U], const do
     const double EE = fma(-lx[u], qe[u], pe[u]);
     const double isPm = s[u].isPm;
     p[u].B1 = EK * isPm;
-#if LB_B3_RD2
     p[u].B3 = EE * (isPm * rcp_nr(s[u].d2));  // E P^-1/2 / d^2 = Em1 c3
     // closed form (kernel.py:366-367) as the differences from Em1 (header):
     // Em1 - S2 = (2/m)(K - E), Em1 - S3 = (2/m)^2 ((1 + x) K - 2 E);
-    // c3 (2/m) = P^-1/2 / (2 ri rn)
-    const double a = oo[u].rtri * rcpr[u];  // 1/(2 ri rn)
+    // c3 (2/m) = P^-1/2 / (2 ri rn); scaled (header): a = 1/(4 ri rn), c34 / 2, c35 / 4
+    const double a = oo[u].rtri * rcpr[u];  // 1/(4 ri rn)
     const double cq = isPm * a;
     p[u].c34 = cq * (EK - EE);
-    p[u].c35 = (cq * (s[u].P * a)) * fma(x[u], EK, fma(-2.0, EE, EK));  // ((1 + x) K - 2 E)
-#else
-    Em1[u] = EE * rcp_nr(x[u]);  // E/(1-m) = E P/d^2
-    const double c3 = isPm * s[u].invP;  // P^-3/2 (the 4 is folded into the coupling)
-    p[u].B3 = Em1[u] * c3;
-    // closed form (kernel.py:366-367) as the differences from Em1 (header):
-    // Em1 - S2 = (2/m)(K - E), Em1 - S3 = (2/m)^2 ((1 + x) K - 2 E)
-    const double invm2 = s[u].P * oo[u].rtri * rcpr[u];  // 2/m
-    const double cq = c3 * invm2;
-    p[u].c34 = cq * (EK - EE);
-    p[u].c35 = (cq * invm2) * fma(x[u], EK, fma(-2.0, EE, EK));  // ((1 + x) K - 2 E)
-#endif
-    p[u].B4 = p[u].B3 - p[u].c34;
+    p[u].c35 = (cq * (s[u].P * a)) * fma(x[u], EK, fma(-2.0, EE, EK));  // ((1 + x) K - 2 E) / 4
+    p[u].B4 = fma(-2.0, p[u].c34, p[u].B3);
     p[u].dz = s[u].dz;
     p[u].dz2 = s[u].dz2;
     p[u].dr = s[u].dr;
@@ -476,7 +469,7 @@ __device__ __forceinline__ void pair_tensor_sym_x(const Outer (&oo)[U], const do
     // m < 0.01 (kernel.py:376), tested as x = 1 - m > 0.99 on the bit pattern
     if (__double_as_longlong(x[u]) > kXSwitchBits) {
       ++nser;
-      const double m = (4.0 * s[u].rr) * s[u].invP;
+      const double m = s[u].rr * s[u].invP;
       double s2 = c_s2[9], s3 = c_s3[9];
 #pragma unroll
       for (int k = 8; k >= 1; --k) {
@@ -486,8 +479,8 @@ __device__ __forceinline__ void pair_tensor_sym_x(const Outer (&oo)[U], const do
       const double c3 = s[u].isPm * s[u].invP;
       const double S2 = s2 * m, S3 = fma(s3, m, c_s3[0]);
       p[u].B4 = S2 * c3;
-      p[u].c34 = fma(-S2, c3, p[u].B3);  // (Em1 - S2) c3
-      p[u].c35 = fma(-S3, c3, p[u].B3);  // (Em1 - S3) c3
+      p[u].c34 = 0.5 * fma(-S2, c3, p[u].B3);   // (Em1 - S2) c3 / 2
+      p[u].c35 = 0.25 * fma(-S3, c3, p[u].B3);  // (Em1 - S3) c3 / 4
     }
   }
 #else
@@ -504,7 +497,7 @@ __device__ __forceinline__ void pair_tensor_sym_x(const Outer (&oo)[U], const do
     double m[U], s2[U], s3[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-      m[u] = (4.0 * s[u].rr) * s[u].invP;
+      m[u] = s[u].rr * s[u].invP;
       s2[u] = c_s2[9];
       s3[u] = c_s3[9];
     }
@@ -519,7 +512,8 @@ __device__ __forceinline__ void pair_tensor_sym_x(const Outer (&oo)[U], const do
     for (int u = 0; u < U; ++u) {
       const double c3 = s[u].isPm * s[u].invP;
       const double S2 = s2[u] * m[u], S3 = fma(s3[u], m[u], c_s3[0]);
-      const double b4 = S2 * c3, d34 = fma(-S2, c3, p[u].B3), d35 = fma(-S3, c3, p[u].B3);  // (Em1 - S.) c3
+      const double b4 = S2 * c3, d34 = 0.5 * fma(-S2, c3, p[u].B3),
+                   d35 = 0.25 * fma(-S3, c3, p[u].B3);  // (Em1 - S2) c3 / 2, (Em1 - S3) c3 / 4
       p[u].B4 = ser[u] ? b4 : p[u].B4;
       p[u].c34 = ser[u] ? d34 : p[u].c34;
       p[u].c35 = ser[u] ? d35 : p[u].c35;
@@ -529,7 +523,7 @@ __device__ __forceinline__ void pair_tensor_sym_x(const Outer (&oo)[U], const do
 #pragma unroll
   for (int u = 0; u < U; ++u) {
     const double w2 = pair_w2(p[u]);
-    t[u] = pair_tensors(rn[u], rn2[u], p[u], w2);
+    t[u] = pair_tensors(rnx[u], rn2[u], p[u], w2);
     txx2[u] = fma(oo[u].ri2, p[u].c35, w2);
   }
 }

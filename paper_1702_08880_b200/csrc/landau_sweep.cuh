@@ -21,7 +21,7 @@ __global__ void lb_pack_kernel(int n, int S, int RS, const double* __restrict__ 
     double* o = rec + (size_t)p * RS;
     o[0] = rn;
     o[1] = z[p];
-    o[2] = rn * rn;
+    o[2] = 4.0 * (rn * rn);  // scaled (landau_pair.cuh): exactly 4 (rn rn)
     o[3] = rn > 0.0 ? 1.0 / rn : 0.0;
     if (pw.collapsed) {  // species-collapsed record (see Coupling)
       double gr = 0.0, gz = 0.0, fw = 0.0;
@@ -43,6 +43,9 @@ __global__ void lb_pack_kernel(int n, int S, int RS, const double* __restrict__ 
       }
       for (int k = 4 + 3 * S; k < RS; ++k) o[k] = 0.0;
     }
+    // one accumulator set (collapsed, or S = 1): slot 7 is free and carries
+    // 2 rn for the species-collapsed symmetric sweep's tensor forms
+    if ((pw.collapsed || S == 1) && RS > 7) o[7] = rn + rn;
   }
 }
 
@@ -200,10 +203,11 @@ __global__ void __launch_bounds__(kTI, kMinBlocks) lb_sweep_kernel(const SweepAr
         const double2 ax1 = *reinterpret_cast<const double2*>(rp1 + 2);
         const double rn[2] = {rz0.x, rz1.x}, zn[2] = {rz0.y, rz1.y};
         const double rn2[2] = {ax0.x, ax1.x}, rcpr[2] = {ax0.y, ax1.y};
+        const double rnx[2] = {rz0.x + rz0.x, rz1.x + rz1.x};
         T5 t[2];
         double txx2[2];  // (unused: the general path has no swapped pair)
         unsigned nser_unused = 0;
-        pair_tensor_sym_x<2>(oo, rn, zn, rn2, rcpr, a.gthr, logt, t, txx2, nser_unused);
+        pair_tensor_sym_x<2>(oo, rn, zn, rn2, rnx, rcpr, a.gthr, logt, t, txx2, nser_unused);
         accumulate(t[0], rp0);
         accumulate(t[1], rp1);
       }

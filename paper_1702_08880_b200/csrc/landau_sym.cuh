@@ -516,7 +516,7 @@ __global__ void __launch_bounds__(kIbThreads, LB_IB_MINB) lb_symsweep_ib_kernel(
 #endif
         const double* rp[JU];
         Outer oo[P2];
-        double rn[P2], zn[P2], rn2[P2], rcpr[P2];
+        double rn[P2], zn[P2], rn2[P2], rcpr[P2], rnx[P2];
 #pragma unroll
         for (int u = 0; u < JU; ++u) {
           const int jl = (lane + st + u * L) & 31;
@@ -524,6 +524,7 @@ __global__ void __launch_bounds__(kIbThreads, LB_IB_MINB) lb_symsweep_ib_kernel(
           const double2 rz = rzn[u];
           rzn[u] = *reinterpret_cast<const double2*>(tile + (jb * 32 + ((jl + 1) & 31)) * RS);
           const double2 aux = *reinterpret_cast<const double2*>(rp[u] + 2);
+          const double r2x = rp[u][7];  // 2 rn (species-collapsed record)
 #pragma unroll
           for (int ib = 0; ib < 2; ++ib) {
             oo[2 * u + ib] = o[ib];
@@ -531,11 +532,12 @@ __global__ void __launch_bounds__(kIbThreads, LB_IB_MINB) lb_symsweep_ib_kernel(
             zn[2 * u + ib] = rz.y;
             rn2[2 * u + ib] = aux.x;
             rcpr[2 * u + ib] = aux.y;
+            rnx[2 * u + ib] = r2x;
           }
         }
         T5 t[P2];
         double txx2[P2];
-        pair_tensor_sym_x<P2, MG>(oo, rn, zn, rn2, rcpr, a.gthr, logt, t, txx2, n_ser);
+        pair_tensor_sym_x<P2, MG>(oo, rn, zn, rn2, rnx, rcpr, a.gthr, logt, t, txx2, n_ser);
 #pragma unroll
         for (int u = 0; u < JU; ++u)
 #pragma unroll
@@ -792,12 +794,12 @@ __global__ void lb_sym_gather_kernel(int n, int npad, int RS, const int* __restr
   if (p < n) {
     const double* src = rec + (size_t)perm[p] * RS;
     for (int c = 0; c < RS; ++c) o[c] = src[c];
-  } else {
+  } else {  // r = 1: r, z, 4 r^2, 1/r, zero fields (and 2 r in a collapsed record's slot 7)
     o[0] = 1.0;
     o[1] = 1.0e6;
-    o[2] = 1.0;
+    o[2] = 4.0;
     o[3] = 1.0;
-    for (int c = 4; c < RS; ++c) o[c] = 0.0;
+    for (int c = 4; c < RS; ++c) o[c] = c == 7 ? 2.0 : 0.0;
   }
 }
 
