@@ -699,12 +699,21 @@ __global__ void __launch_bounds__(NT) lb_getrs_slab_kernel(int n, int m, double*
   };
   issue(0, 0);
   issue(0, 1);
-  // gather P X into shared memory (zero rows n..ld, zero columns wc..W)
+  // gather P X into shared memory (zero rows n..ld, zero columns wc..W) by
+  // cp.async: the whole slab is in flight at once (a register-staged gather
+  // of 8 columns at a time left each CTA -- one per SM -- waiting on 8
+  // successive HBM round trips, 16 % of the kernel at 256 blocks); the first
+  // step's wait covers this group
   for (int i = tid; i < ld; i += NT) {  // consecutive threads: consecutive rows of a column
     const int src = (i < n) ? (perm ? perm[i] : i) : 0;
-#pragma unroll 8
-    for (int c = 0; c < W; ++c) X[(size_t)i * W + c] = (i < n && c < wc) ? Xg[(size_t)c * n + src] : 0.0;
+    for (int c = 0; c < W; ++c) {
+      if (i < n && c < wc)
+        cp_async8(X + (size_t)i * W + c, Xg + (size_t)c * n + src);
+      else
+        X[(size_t)i * W + c] = 0.0;
+    }
   }
+  cp_async_commit();
 #ifdef LB_LU_PROF
   long long t0_ = clock64(), pacc_[8] = {}, pcol_[4] = {};
 #endif
