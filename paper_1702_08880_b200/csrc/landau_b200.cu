@@ -1536,7 +1536,7 @@ static int cn_alloc(lb_cn* cn, void** p, size_t bytes) {
 // blocks up to 384 rows; larger blocks (or LB_CN_GM_LU set) by the
 // global-memory LU and substitution of landau_blas.cuh
 constexpr int kLuKB = 32, kLuW = 32, kLuMaxNb = 384;
-constexpr int kLuWideMinCount = 48;       // blocks per level from which 64-column slabs pay
+constexpr int kLuWideMinCount = 12;       // blocks per level from which 64-column slabs pay (measured at 260 rows: 16 blocks 0.157 vs 0.194 ms, 4 blocks 0.155 vs 0.102)
 constexpr size_t kLuSmemMax = 232448;     // opt-in shared memory per CTA (227 KB)
 static bool cn_custom_lu(const lb_cn* cn) {
   static const bool force_gm = std::getenv("LB_CN_GM_LU") != nullptr;

@@ -103,7 +103,16 @@ int main(int argc, char** argv) {
       printf("n=%3d: W=%d slab needs %zu B of shared memory, skipped\n", n, W, getrs_smem_bytes<KB, W>(n));
       continue;
     }
-    for (int batch : {4, 64, 256}) {
+    std::vector<int> batches = {4, 64, 256};
+    if (const char* e = std::getenv("LU_BATCHES")) {  // e.g. LU_BATCHES=8,16,32
+      batches.clear();
+      for (const char* q = e; *q;) {
+        batches.push_back(std::atoi(q));
+        while (*q && *q != ',') ++q;
+        if (*q == ',') ++q;
+      }
+    }
+    for (int batch : batches) {
       for (int kind = 0; kind < 2; ++kind) {  // 0: random (pivoting matters), 1: diagonally weighted
         const int m = 2 * n;
         const size_t nn = (size_t)n * n, nm = (size_t)n * m;
