@@ -195,7 +195,7 @@ def assemble_collision(mesh, ref, data, params, eps_d: float | None = None,
             float(eps_d), p(csr), None, None, p(phase)))
     t2 = time.perf_counter()
     n_free = gm.n_free
-    blocks = [sp.csr_matrix((csr[a], gm.indices, gm.indptr), shape=(n_free, n_free))
+    blocks = [gm.csr_block(csr[a])
               for a in range(S)]
     t3 = time.perf_counter()
     host = max(t2 - t1 - float(phase.sum()) * 1e-3, 0.0)
@@ -242,7 +242,7 @@ def assemble_at(mesh, ref, state, params, eps_d: float | None = None,
             ctx.handle, dm.handle, S, p(c), p(coK), p(coD), float(eps_d), p(csr),
             p(data) if return_data else None, p(phase)))
     t1 = time.perf_counter()
-    blocks = [sp.csr_matrix((csr[a], gm.indices, gm.indptr), shape=(gm.n_free, gm.n_free))
+    blocks = [gm.csr_block(csr[a])
               for a in range(S)]
     t2 = time.perf_counter()
     host = max(t1 - t0 - float(phase.sum()) * 1e-3, 0.0)
@@ -339,5 +339,5 @@ def assemble_species_meshes(meshes, ref, datas, params, eps_d: float | None = No
             p = _lib.dptr
             _lib.check(_lib.load().lb_elements_csr(ctx.handle, dm.handle, 1, p(w), p(Ka), p(Da),
                                                    p(csr)))
-        blocks.append(sp.csr_matrix((csr[0], gm.indices, gm.indptr), shape=(gm.n_free, gm.n_free)))
+        blocks.append(gm.csr_block(csr[0]))
     return blocks, (K, D)

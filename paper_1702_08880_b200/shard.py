@@ -512,5 +512,5 @@ class ShardedOperator:
             D_all.data_ptr(), self.csr.data_ptr(), st))
         vals = self.csr.cpu().numpy()
         gm = self.dm.map
-        return [sp.csr_matrix((vals[a], gm.indices, gm.indptr), shape=(gm.n_free, gm.n_free))
+        return [gm.csr_block(vals[a])
                 for a in range(self.S)]
