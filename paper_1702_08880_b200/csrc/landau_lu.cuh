@@ -45,7 +45,10 @@ constexpr int kLuThreads = 256;
 // lb_getrf_kernel: one thread per panel row (n <= 384) with the register panel
 constexpr int kGetrfThreads = LB_LU_REGPANEL ? 384 : kLuThreads;
 #ifdef LB_LU_PROF
-// cycles per phase (block 0, thread 0): accumulated in registers, written by LU_FLUSH
+#ifndef LB_LU_PROF_TID
+#define LB_LU_PROF_TID 0  // the thread whose phase cycles are recorded
+#endif
+// cycles per phase (block 0, thread LB_LU_PROF_TID): accumulated in registers, written by LU_FLUSH
 __device__ long long lu_prof[8];
 #define LU_T(k)                                                        \
   do {                                                                 \
@@ -55,7 +58,7 @@ __device__ long long lu_prof[8];
   } while (0)
 #define LU_FLUSH()                                                                   \
   do {                                                                               \
-    if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) {                    \
+    if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == LB_LU_PROF_TID) {       \
       for (int k_ = 0; k_ < 8; ++k_) lu_prof[k_] += pacc_[k_];                       \
       for (int k_ = 0; k_ < 4; ++k_) lu_prof2[k_] += pcol_[k_];                      \
     }                                                                                \
@@ -593,8 +596,8 @@ __global__ void __launch_bounds__(kGetrfThreads) lb_getrf_kernel(int n, double* 
     __syncthreads();
     LU_T(4);
   }
+  LU_FLUSH();
   if (tid == 0) {
-    LU_FLUSH();
     if (info_all) info_all[b] = info;
     if (perm_all) {  // row i of P A is row perm[i] of A
       int* perm = perm_all + (size_t)b * n;
