@@ -170,7 +170,6 @@ __global__ void __launch_bounds__(kGetrfThreads) lb_getrf_kernel(int n, double* 
 #pragma unroll
       for (int k = 0; k < KB; ++k) v[k] = (own && k < w) ? src[(size_t)k * n] : 0.0;
     }
-    for (int i = tid; i < ld; i += NT) lp[i] = i;  // slot -> panel-local row (after the panel)
     int slot = tid;
     bool done = false;  // this row is a pivot (a row of U) already
     // every live row's 1 / a_j, computed as soon as a_j is final (the IEEE
@@ -257,18 +256,11 @@ __global__ void __launch_bounds__(kGetrfThreads) lb_getrf_kernel(int n, double* 
     if (own) {
 #pragma unroll
       for (int k = 0; k < KB; ++k) P[(size_t)k * ld + slot] = v[k];
+      lp[slot] = tid;  // slot -> panel-local row: each row knows where the LAPACK swaps took it
     } else if (tid < ld) {
 #pragma unroll
       for (int k = 0; k < KB; ++k) P[(size_t)k * ld + tid] = 0.0;
-    }
-    // slot -> panel-local row (the LAPACK swaps j <-> pv[j] in order) for
-    // the gather list below
-    if (tid == 0) {
-      for (int j = 0; j < w; ++j) {
-        const int q = pv_sh[j], t0 = lp[j];
-        lp[j] = lp[q];
-        lp[q] = t0;
-      }
+      lp[tid] = tid;
     }
     __syncthreads();  // pv_sh / lp final
     LU_T(1);
@@ -405,13 +397,16 @@ __global__ void __launch_bounds__(kGetrfThreads) lb_getrf_kernel(int n, double* 
         }
       } else if (tid >= 32 && tid < 32 + KB) {  // column c of U11^-1: right-looking back substitution of e_c
         const int c = tid - 32;
+        // 1/u_kk: lane k divides once, the substitution multiplies (a
+        // 32-step chain of IEEE divisions was the longest path of the
+        // panel's tail: the other warps waited for it at the next barrier)
+        const double rme = 1.0 / ((c < w) ? P[(size_t)c * ld + c] : 1.0);
         double x[KB];
 #pragma unroll
         for (int i = 0; i < KB; ++i) x[i] = (i == c) ? 1.0 : 0.0;
 #pragma unroll
         for (int k = KB - 1; k >= 0; --k) {
-          const double dkk = (k < w) ? P[(size_t)k * ld + k] : 1.0;
-          x[k] = x[k] / dkk;
+          x[k] = x[k] * __shfl_sync(0xffffffffu, rme, k);
 #pragma unroll
           for (int i = 0; i < k; ++i) x[i] = fma(-P[(size_t)k * ld + i], x[k], x[i]);
         }
@@ -497,6 +492,9 @@ __global__ void __launch_bounds__(kGetrfThreads) lb_getrf_kernel(int n, double* 
         for (int mm = 0; mm < 4; ++mm)
 #pragma unroll
           for (int nn = 0; nn < 2; ++nn) acc[u][mm][nn][0] = acc[u][mm][nn][1] = 0.0;
+#ifdef LB_LU_PROF_SKIP_U12  // profiling experiment only (wrong results)
+        continue;
+#endif
 #pragma unroll
         for (int k0 = 0; k0 < KB; k0 += 4) {
           const int k = k0 + lk;
