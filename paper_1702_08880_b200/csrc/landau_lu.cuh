@@ -93,7 +93,7 @@ template <int KB>
 inline size_t getrf_smem_bytes(int n) {
   constexpr int NW = kGetrfThreads / 32;
   return sizeof(double) * (2 * (size_t)KB * lu_ld<KB>(n) + 2 * 32 + KB * KB + 2 * NW * (KB + 2)) +
-         sizeof(int) * (KB + 32 + lu_ld<KB>(n) + 4 * KB + 4 * NW);
+         sizeof(int) * (KB + 32 + 2 * lu_ld<KB>(n) + 4 * KB + 4 * NW);
 }
 
 // Inverse diagonal blocks: per matrix, per panel p, invL[p] (KB x KB, unit
@@ -136,6 +136,7 @@ __global__ void __launch_bounds__(kGetrfThreads) lb_getrf_kernel(int n, double* 
   int* lp = pv_sh + KB;                           // [ld] panel-local row permutation
   int* tl_dst = lp + ld;                          // [2 KB] rows a panel's swaps touch
   int* tl_src = tl_dst + 2 * KB;                  // [2 KB] and where their values come from
+  int* perm_s = tl_src + 2 * KB;                  // [ld] cumulative row permutation (register panel)
   const int b = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   double* A = As[b];
   int* ipiv = ipiv_all ? ipiv_all + (size_t)b * n : nullptr;
@@ -145,6 +146,9 @@ __global__ void __launch_bounds__(kGetrfThreads) lb_getrf_kernel(int n, double* 
   long long t0_ = clock64(), pacc_[8] = {}, pcol_[4] = {};
 #endif
 
+#if LB_LU_REGPANEL
+  for (int i = tid; i < ld; i += NT) perm_s[i] = i;  // (ordered before use by the first panel's barriers)
+#endif
   for (int c0 = 0, p = 0; c0 < n; c0 += KB, ++p) {
     const int w = min(KB, n - c0), m = n - c0;
 #if LB_LU_REGPANEL
@@ -264,6 +268,9 @@ __global__ void __launch_bounds__(kGetrfThreads) lb_getrf_kernel(int n, double* 
     }
     __syncthreads();  // pv_sh / lp final
     LU_T(1);
+    // cumulative row permutation: row c0 + s of P A is row c0 + lp[s] before
+    // this panel's swaps
+    const int perm_new = own ? perm_s[c0 + lp[tid]] : 0;
     // the factored panel back to A (LAPACK layout)
     for (int t = tid; t < w * m; t += NT) {
       const int k = t / m, i = t - k * m;
@@ -271,6 +278,7 @@ __global__ void __launch_bounds__(kGetrfThreads) lb_getrf_kernel(int n, double* 
     }
     if (ipiv && tid < w) ipiv[c0 + tid] = c0 + pv_sh[tid] + 1;
     __syncthreads();
+    if (own) perm_s[c0 + tid] = perm_new;
 #else
     // 1. panel rows c0..n, columns c0..c0+w -> P (zero padding to ld rows /
     //    KB columns); rows tid + 256 h, eight columns of loads in flight
@@ -597,6 +605,7 @@ __global__ void __launch_bounds__(kGetrfThreads) lb_getrf_kernel(int n, double* 
   LU_FLUSH();
   if (tid == 0) {
     if (info_all) info_all[b] = info;
+#if !LB_LU_REGPANEL
     if (perm_all) {  // row i of P A is row perm[i] of A
       int* perm = perm_all + (size_t)b * n;
       for (int i = 0; i < n; ++i) perm[i] = i;
@@ -608,7 +617,15 @@ __global__ void __launch_bounds__(kGetrfThreads) lb_getrf_kernel(int n, double* 
           perm[q] = t0;
         }
     }
+#endif
   }
+#if LB_LU_REGPANEL
+  if (perm_all) {  // row i of P A is row perm[i] of A (built per panel in shared memory)
+    __syncthreads();
+    int* perm = perm_all + (size_t)b * n;
+    for (int i = tid; i < n; i += NT) perm[i] = perm_s[i];
+  }
+#endif
 }
 
 // X := A^-1 X for X = the n x m column-major block at Xs[b] (leading
