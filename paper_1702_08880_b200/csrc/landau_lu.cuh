@@ -905,9 +905,12 @@ __global__ void __launch_bounds__(kLuThreads) lb_lu_vsolve_kernel(int n, int cou
           if (r > k && k < kb) xr = fma(-t[k], xk, xr);
         }
       } else {
+        // 1/u_rr per lane up front (overlapping the loads): the chain then
+        // multiplies instead of running 32 dependent IEEE divisions
+        const double rinv = 1.0 / (r < kb ? A[(size_t)(r0 + r) * n + r0 + r] : 1.0);
 #pragma unroll
         for (int k = KB - 1; k >= 0; --k) {
-          if (r == k && k < kb) xr = xr / t[k];
+          if (r == k && k < kb) xr = xr * rinv;
           const double xk = __shfl_sync(0xffffffffu, xr, k);
           if (r < k && k < kb) xr = fma(-t[k], xk, xr);
         }
