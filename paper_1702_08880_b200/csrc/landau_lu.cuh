@@ -388,7 +388,11 @@ __global__ void __launch_bounds__(kGetrfThreads) lb_getrf_kernel(int n, double* 
     {
       double* iL = inv + (size_t)(2 * p) * KB * KB;
       double* iU = iL + KB * KB;
-      if (tid < KB) {  // column tid of L11^-1: right-looking forward substitution of e_tid
+#ifdef LB_LU_PROF_SKIP_INV  // profiling experiment only (wrong results)
+      if (false) {
+#else
+      if (tid < KB) {  // column tid of L11^-1
+#endif: right-looking forward substitution of e_tid
         const int c = tid;
         double x[KB];
 #pragma unroll
@@ -456,7 +460,11 @@ __global__ void __launch_bounds__(kGetrfThreads) lb_getrf_kernel(int n, double* 
       const int d0 = tl_dst[lane], d1 = tl_dst[lane + 32];
       const int kbeg = pivot ? 0 : c0;  // left columns only need the swaps
       constexpr int CB = 16;            // columns in flight per warp
+#ifdef LB_LU_PROF_SKIP_GATHER  // profiling experiment only (wrong results)
+      for (int kb0 = n; kb0 < n - w; kb0 += kGW * CB) {
+#else
       for (int kb0 = kbeg + (warp - 2) * CB; kb0 < n - w; kb0 += kGW * CB) {
+#endif
         double v0[CB], v1[CB];
 #pragma unroll
         for (int u = 0; u < CB; ++u) {
@@ -484,40 +492,47 @@ __global__ void __launch_bounds__(kGetrfThreads) lb_getrf_kernel(int n, double* 
     }
     __syncthreads();
     LU_T(5);
-    // U12 = L11^-1 A12 on the FP64 tensor path: warp tiles of 32 rows x 16
-    // columns (4 x 2 MMA tiles), written to Ub and back to A's rows c0..c0+w
+    // U12 = L11^-1 A12 on the FP64 tensor path: warp tiles of 32 rows x TN
+    // columns (4 x TN/8 MMA tiles), written to Ub and back to A's rows c0..c0+w.
+    // TN = 32: 16 independent accumulators per warp, so consecutive MMAs of a
+    // k-step do not wait on each other (with 4 x 2 tiles ptxas grouped them
+    // into 4 chains and the loop ran at a third of the pipe in place)
     {
+#ifndef LB_U12_TN
+#define LB_U12_TN 32
+#endif
+      constexpr int TN = LB_U12_TN, NNT = TN / 8;
       const int lk = lane & 3, lr = lane >> 2;
-      constexpr int kMaxU = (24 + NW - 1) / NW;  // ceil(ceil(383 / 16) / NW)
-      double acc[kMaxU][4][2][2];
-      const int nwt = (n2 + 15) >> 4;
+      constexpr int kMaxU = ((383 + TN - 1) / TN + NW - 1) / NW;
+      double acc[kMaxU][4][NNT][2];
+      const int nwt = (n2 + TN - 1) / TN;
 #pragma unroll
       for (int u = 0; u < kMaxU; ++u) {
         const int t = warp + u * NW;
         if (t >= nwt) break;
-        const int C0 = t * 16;
+        const int C0 = t * TN;
 #pragma unroll
         for (int mm = 0; mm < 4; ++mm)
 #pragma unroll
-          for (int nn = 0; nn < 2; ++nn) acc[u][mm][nn][0] = acc[u][mm][nn][1] = 0.0;
+          for (int nn = 0; nn < NNT; ++nn) acc[u][mm][nn][0] = acc[u][mm][nn][1] = 0.0;
 #ifdef LB_LU_PROF_SKIP_U12  // profiling experiment only (wrong results)
         continue;
 #endif
 #pragma unroll
         for (int k0 = 0; k0 < KB; k0 += 4) {
           const int k = k0 + lk;
-          double av[4], bv[2];
+          double av[4], bv[NNT];
 #pragma unroll
           for (int mm = 0; mm < 4; ++mm) av[mm] = iLs[(size_t)k * KB + 8 * mm + lr];
 #pragma unroll
-          for (int nn = 0; nn < 2; ++nn) {
+          for (int nn = 0; nn < NNT; ++nn) {
             const int C = C0 + 8 * nn + lr;
             bv[nn] = C < n2 ? Ub[(size_t)k * ld + C] : 0.0;
           }
 #pragma unroll
           for (int mm = 0; mm < 4; ++mm)
 #pragma unroll
-            for (int nn = 0; nn < 2; ++nn) dmma_884(acc[u][mm][nn], av[mm], bv[nn]);
+            for (int nn = 0; nn < NNT; ++nn) dmma_884(acc[u][mm][nn], av[mm], bv[nn]);
         }
       }
       __syncthreads();  // every Ub read done
@@ -526,12 +541,12 @@ __global__ void __launch_bounds__(kGetrfThreads) lb_getrf_kernel(int n, double* 
       for (int u = 0; u < kMaxU; ++u) {
         const int t = warp + u * NW;
         if (t >= nwt) break;
-        const int C0 = t * 16;
+        const int C0 = t * TN;
 #pragma unroll
         for (int mm = 0; mm < 4; ++mm) {
           const int i = 8 * mm + lr;
 #pragma unroll
-          for (int nn = 0; nn < 2; ++nn)
+          for (int nn = 0; nn < NNT; ++nn)
 #pragma unroll
             for (int e = 0; e < 2; ++e) {
               const int C = C0 + 8 * nn + 2 * lk + e;
@@ -554,7 +569,11 @@ __global__ void __launch_bounds__(kGetrfThreads) lb_getrf_kernel(int n, double* 
     //    (mma.m8n8k4.f64): warp tiles of 16 rows x 32 columns (2 x 4 MMA
     //    tiles), accumulators start from the tile's current values
     const int m2 = m - w;
+#ifdef LB_LU_PROF_SKIP_UPD  // profiling experiment only (wrong results)
+    if (false) {
+#else
     if (m2 > 0 && n2 > 0) {
+#endif
       static_assert(KB % 4 == 0, "k steps of 4");
       const int lk = lane & 3;
       const int twr = (m2 + 15) >> 4, twc = (n2 + 31) >> 5;

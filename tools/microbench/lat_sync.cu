@@ -43,6 +43,25 @@ __global__ void k_div(double* out, int iters, long long* cyc) {
   long long t1 = clock64();
   out[threadIdx.x] = x; if (threadIdx.x == 0) *cyc = t1 - t0;
 }
+__global__ void k_dmma(double* out, int iters, long long* cyc, int chains) {
+  double d[8][2];
+  for (int c = 0; c < 8; ++c) d[c][0] = d[c][1] = threadIdx.x * 1e-3 + c;
+  const double a = 0.999, b = 1e-3;
+  long long t0 = clock64();
+  for (int i = 0; i < iters; ++i) {
+    if (chains == 1) {
+      asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};" : "+d"(d[0][0]), "+d"(d[0][1]) : "d"(a), "d"(b));
+    } else {
+#pragma unroll
+      for (int c = 0; c < 8; ++c)
+        asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};" : "+d"(d[c][0]), "+d"(d[c][1]) : "d"(a), "d"(b));
+    }
+  }
+  long long t1 = clock64();
+  double s = 0; for (int c = 0; c < 8; ++c) s += d[c][0] + d[c][1];
+  if (s == 1234.5) out[0] = s;
+  if (threadIdx.x == 0) *cyc = t1 - t0;
+}
 int main() {
   unsigned* o; double* od; long long* c; cudaMalloc(&o, 4096); cudaMalloc(&od, 8192); cudaMalloc(&c, 8);
   const int it = 10000; long long h;
@@ -50,6 +69,9 @@ int main() {
   k_shfl<<<1, 32>>>(o, it, c); cudaMemcpy(&h, c, 8, cudaMemcpyDeviceToHost); printf("shfl dependent: %.1f cyc\n", (double)h / it);
   k_lds<<<1, 32>>>(o, it, c); cudaMemcpy(&h, c, 8, cudaMemcpyDeviceToHost); printf("lds dependent: %.1f cyc\n", (double)h / it);
   for (int nt : {64, 288, 384}) { k_bar<<<1, nt>>>(o, it, c); cudaMemcpy(&h, c, 8, cudaMemcpyDeviceToHost); printf("sts+bar+lds (%d thr): %.1f cyc\n", nt, (double)h / it); }
+  k_dmma<<<1, 32>>>(od, it, c, 1); cudaMemcpy(&h, c, 8, cudaMemcpyDeviceToHost); printf("dmma m8n8k4 dependent: %.1f cyc\n", (double)h / it);
+  k_dmma<<<1, 32>>>(od, it, c, 8); cudaMemcpy(&h, c, 8, cudaMemcpyDeviceToHost); printf("dmma m8n8k4, 8 chains, 1 warp: %.1f cyc per mma\n", (double)h / it / 8);
+  k_dmma<<<1, 128>>>(od, it, c, 8); cudaMemcpy(&h, c, 8, cudaMemcpyDeviceToHost); printf("dmma m8n8k4, 8 chains, 4 warps: %.1f cyc per mma per warp\n", (double)h / it / 8);
   k_div<<<1, 32>>>(od, it, c); cudaMemcpy(&h, c, 8, cudaMemcpyDeviceToHost); printf("ddiv+dadd dependent: %.1f cyc\n", (double)h / it);
   return 0;
 }
