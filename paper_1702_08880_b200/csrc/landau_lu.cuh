@@ -391,8 +391,8 @@ __global__ void __launch_bounds__(kGetrfThreads) lb_getrf_kernel(int n, double* 
 #ifdef LB_LU_PROF_SKIP_INV  // profiling experiment only (wrong results)
       if (false) {
 #else
-      if (tid < KB) {  // column tid of L11^-1
-#endif: right-looking forward substitution of e_tid
+      if (tid < KB) {  // column tid of L11^-1: right-looking forward substitution of e_tid
+#endif
         const int c = tid;
         double x[KB];
 #pragma unroll
