@@ -159,16 +159,21 @@ __global__ void __launch_bounds__(kGemvThreads) lb_bgemv_kernel(int n, double* c
   double* __restrict__ y = ys_[blockIdx.y];
   const int r = threadIdx.x & (kGemvRows - 1), g = threadIdx.x / kGemvRows;
   const int i = blockIdx.x * kGemvRows + r;
-  double s0 = 0.0, s1 = 0.0;
+  // four running sums (columns g + 8 (4 j + u)), loop unrolled twice: eight
+  // independent column loads in flight per thread (a latency-bound pass:
+  // the two-sum form waited out an L2 round trip every two columns)
+  double s[4] = {0.0, 0.0, 0.0, 0.0};
   if (i < n) {
     int k = g;
-    for (; k + kGemvGroups < n; k += 2 * kGemvGroups) {
-      s0 = fma(A[(size_t)k * n + i], x[k], s0);
-      s1 = fma(A[(size_t)(k + kGemvGroups) * n + i], x[k + kGemvGroups], s1);
+#pragma unroll 2
+    for (; k + 3 * kGemvGroups < n; k += 4 * kGemvGroups) {
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        s[u] = fma(A[(size_t)(k + u * kGemvGroups) * n + i], x[k + u * kGemvGroups], s[u]);
     }
-    if (k < n) s0 = fma(A[(size_t)k * n + i], x[k], s0);
+    for (; k < n; k += kGemvGroups) s[0] = fma(A[(size_t)k * n + i], x[k], s[0]);
   }
-  part[g][r] = s0 + s1;
+  part[g][r] = (s[0] + s[1]) + (s[2] + s[3]);
   __syncthreads();
   if (g == 0 && i < n) {
     double s = part[0][r];
