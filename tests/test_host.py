@@ -127,6 +127,22 @@ def test_gather_map_reproduces_scipy_condensation(case):
         assert np.abs(x.toarray() - z.toarray()).max() <= 1e-13 * np.abs(z.toarray()).max()
     assert gm.slot_ptr[-1] == gm.gather_idx.shape[0]
     assert gm.gather_idx.max() < elem[0].size
+    # csr_block flags its matrices canonical without scipy's re-validation:
+    # the pattern must really be canonical, and the blocks independent
+    import scipy.sparse as sp
+
+    assert np.all(np.diff(gm.indptr) >= 0) and gm.indptr[-1] == gm.nnz
+    for r in range(gm.n_free):  # columns sorted and unique within every row
+        row = gm.indices[gm.indptr[r]:gm.indptr[r + 1]]
+        assert np.all(np.diff(row) > 0)
+    chk = sp.csr_matrix((np.ones(gm.nnz), gm.indices, gm.indptr), shape=(gm.n_free, gm.n_free))
+    chk.sum_duplicates()  # scipy's canonicalisation changes nothing
+    assert chk.nnz == gm.nnz and np.array_equal(chk.indices, gm.indices)
+    b0, b1 = gm.csr_block(np.arange(gm.nnz, dtype=float)), gm.csr_block(np.ones(gm.nnz))
+    assert b0.indices is not b1.indices and b0.indptr is not b1.indptr
+    b0.eliminate_zeros()  # in place on b0's own arrays only
+    assert b1.nnz == gm.nnz and np.array_equal(b1.indices, gm.indices)
+    assert np.array_equal((b1 @ np.ones(gm.n_free)), np.diff(gm.indptr).astype(float))
 
 
 def test_coefficient_header_is_generated():
