@@ -44,6 +44,10 @@ constexpr int kLuThreads = 256;
 #endif
 // lb_getrf_kernel: one thread per panel row (n <= 384) with the register panel
 constexpr int kGetrfThreads = LB_LU_REGPANEL ? 384 : kLuThreads;
+#ifndef LB_LU_LOOKAHEAD_WARPS
+#define LB_LU_LOOKAHEAD_WARPS 4  // idle warps needed to run a deferred trailing update beside a panel
+#endif
+constexpr int kLookAheadWarps = LB_LU_LOOKAHEAD_WARPS;
 #ifdef LB_LU_PROF
 #ifndef LB_LU_PROF_TID
 #define LB_LU_PROF_TID 0  // the thread whose phase cycles are recorded
@@ -149,6 +153,57 @@ __global__ void __launch_bounds__(kGetrfThreads) lb_getrf_kernel(int n, double* 
 #if LB_LU_REGPANEL
   for (int i = tid; i < ld; i += NT) perm_s[i] = i;  // (ordered before use by the first panel's barriers)
 #endif
+  // trailing update A22 -= L21 U12 of the panel at (uc0, uw) for the warp
+  // tiles (16 rows x 32 columns) in tile columns [tc0, tc1), distributed over
+  // warps [wb, wb + nwk); L21 from P, U12 from Ub (shared memory)
+  auto trailing_update = [&](int uc0, int uw, int um2, int un2, int tc0, int tc1, int wb, int nwk) {
+    const int lk = lane & 3;
+    const int twr = (um2 + 15) >> 4, twc = tc1 - tc0;
+    for (int t = warp - wb; t < twr * twc; t += nwk) {
+      const int R0 = (t / twc) * 16, C0 = (tc0 + t - (t / twc) * twc) * 32;
+      double acc[2][4][2];
+#pragma unroll
+      for (int mm = 0; mm < 2; ++mm) {
+        const int R = R0 + 8 * mm + (lane >> 2);
+#pragma unroll
+        for (int nn = 0; nn < 4; ++nn)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int C = C0 + 8 * nn + 2 * lk + e;
+            acc[mm][nn][e] = (R < um2 && C < un2) ? A[(size_t)(uc0 + uw + C) * n + uc0 + uw + R] : 0.0;
+          }
+      }
+#pragma unroll
+      for (int k0 = 0; k0 < KB; k0 += 4) {
+        const int k = k0 + lk;
+        double av[2], bv[4];
+#pragma unroll
+        for (int mm = 0; mm < 2; ++mm) av[mm] = -P[(size_t)k * ld + uw + R0 + 8 * mm + (lane >> 2)];
+#pragma unroll
+        for (int nn = 0; nn < 4; ++nn) bv[nn] = Ub[(size_t)k * ld + C0 + 8 * nn + (lane >> 2)];
+#pragma unroll
+        for (int mm = 0; mm < 2; ++mm)
+#pragma unroll
+          for (int nn = 0; nn < 4; ++nn) dmma_884(acc[mm][nn], av[mm], bv[nn]);
+      }
+#pragma unroll
+      for (int mm = 0; mm < 2; ++mm) {
+        const int R = R0 + 8 * mm + (lane >> 2);
+        if (R >= um2) continue;
+#pragma unroll
+        for (int nn = 0; nn < 4; ++nn)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int C = C0 + 8 * nn + 2 * lk + e;
+            if (C < un2) A[(size_t)(uc0 + uw + C) * n + uc0 + uw + R] = acc[mm][nn][e];
+          }
+      }
+    }
+  };
+  // look-ahead: the previous panel's update of the columns right of the
+  // current panel (tile columns 1..), deferred so that the warps the current
+  // panel leaves idle (those past its rows) run it during the factorisation
+  int def_c0 = 0, def_w = 0, def_m2 = 0, def_n2 = 0, def_twc = 0;
   for (int c0 = 0, p = 0; c0 < n; c0 += KB, ++p) {
     const int w = min(KB, n - c0), m = n - c0;
 #if LB_LU_REGPANEL
@@ -168,25 +223,39 @@ __global__ void __launch_bounds__(kGetrfThreads) lb_getrf_kernel(int n, double* 
     //    are three redux.sync (max |a| as the high and low words of its bit
     //    pattern, then the smallest slot) instead of shuffle trees.
     const bool own = tid < m;
-    double v[KB];
-    {
-      const double* src = A + (size_t)c0 * n + c0 + tid;
-#pragma unroll
-      for (int k = 0; k < KB; ++k) v[k] = (own && k < w) ? src[(size_t)k * n] : 0.0;
-    }
     int slot = tid;
     bool done = false;  // this row is a pivot (a row of U) already
-    // every live row's 1 / a_j, computed as soon as a_j is final (the IEEE
-    // division overlaps the pivot search; the winner's is published)
-    double rcp = v[0] != 0.0 ? 1.0 / v[0] : 0.0;
     // only the warps that own panel rows take part: the per-column overhead
     // is issue- and latency-bound, and the panel shrinks by 32 rows a step
     const int nact = (m + 31) >> 5;
     __syncthreads();
     LU_T(0);
+    // the previous panel's deferred update (tile columns 1.., columns right
+    // of this panel): beside the panel on its idle warps, or -- too few of
+    // them -- by everyone first
+    const bool lookahead = def_twc > 1 && NW - nact >= kLookAheadWarps;
+    if (def_twc > 1 && !lookahead) {
+      trailing_update(def_c0, def_w, def_m2, def_n2, 1, def_twc, 0, NW);
+      __syncthreads();
+    }
+    double v[KB];
+    if (warp >= nact) {  // (no panel rows; separate branch: v and the update's
+                         // accumulators are never live together)
+#pragma unroll
+      for (int k = 0; k < KB; ++k) v[k] = 0.0;
+      if (lookahead) trailing_update(def_c0, def_w, def_m2, def_n2, 1, def_twc, nact, NW - nact);
+    } else {
+    {
+      const double* src = A + (size_t)c0 * n + c0 + tid;
+#pragma unroll
+      for (int k = 0; k < KB; ++k) v[k] = (own && k < w) ? src[(size_t)k * n] : 0.0;
+    }
+    // every live row's 1 / a_j, computed as soon as a_j is final (the IEEE
+    // division overlaps the pivot search; the winner's is published)
+    double rcp = v[0] != 0.0 ? 1.0 / v[0] : 0.0;
 #pragma unroll
     for (int j = 0; j < KB; ++j) {
-      if (j >= w || warp >= nact) break;
+      if (j >= w) break;
       const int buf = j & 1;
       double* rows = pr_rows + (size_t)buf * NW * KB;  // [NW][KB]
       int wq = 0;  // entry of the pivot row
@@ -254,6 +323,7 @@ __global__ void __launch_bounds__(kGetrfThreads) lb_getrf_kernel(int n, double* 
       }
       LU_TC(2);
     }
+    }  // warp < nact
     __syncthreads();
     // the factored panel by LAPACK slot in P (zero padding: rows m..ld,
     // columns w..KB are zero in v)
@@ -566,56 +636,28 @@ __global__ void __launch_bounds__(kGetrfThreads) lb_getrf_kernel(int n, double* 
     __syncthreads();
     LU_T(3);
     // 6. trailing update A22 -= L21 U12 on the FP64 tensor path
-    //    (mma.m8n8k4.f64): warp tiles of 16 rows x 32 columns (2 x 4 MMA
-    //    tiles), accumulators start from the tile's current values
+    //    (mma.m8n8k4.f64): warp tiles of 16 rows x 32 columns, accumulators
+    //    start from the tile's current values.  Tile column 0 is the next
+    //    panel: updated now by every warp; the rest is deferred to the next
+    //    panel's idle warps (look-ahead) -- or done now on the last panel /
+    //    the shared-memory-panel build
     const int m2 = m - w;
+    def_twc = 0;
 #ifdef LB_LU_PROF_SKIP_UPD  // profiling experiment only (wrong results)
     if (false) {
 #else
     if (m2 > 0 && n2 > 0) {
 #endif
       static_assert(KB % 4 == 0, "k steps of 4");
-      const int lk = lane & 3;
-      const int twr = (m2 + 15) >> 4, twc = (n2 + 31) >> 5;
-      for (int t = warp; t < twr * twc; t += NW) {
-        const int R0 = (t / twc) * 16, C0 = (t - (t / twc) * twc) * 32;
-        double acc[2][4][2];
-#pragma unroll
-        for (int mm = 0; mm < 2; ++mm) {
-          const int R = R0 + 8 * mm + (lane >> 2);
-#pragma unroll
-          for (int nn = 0; nn < 4; ++nn)
-#pragma unroll
-            for (int e = 0; e < 2; ++e) {
-              const int C = C0 + 8 * nn + 2 * lk + e;
-              acc[mm][nn][e] = (R < m2 && C < n2) ? A[(size_t)(c0 + w + C) * n + c0 + w + R] : 0.0;
-            }
-        }
-#pragma unroll
-        for (int k0 = 0; k0 < KB; k0 += 4) {
-          const int k = k0 + lk;
-          double av[2], bv[4];
-#pragma unroll
-          for (int mm = 0; mm < 2; ++mm) av[mm] = -P[(size_t)k * ld + w + R0 + 8 * mm + (lane >> 2)];
-#pragma unroll
-          for (int nn = 0; nn < 4; ++nn) bv[nn] = Ub[(size_t)k * ld + C0 + 8 * nn + (lane >> 2)];
-#pragma unroll
-          for (int mm = 0; mm < 2; ++mm)
-#pragma unroll
-            for (int nn = 0; nn < 4; ++nn) dmma_884(acc[mm][nn], av[mm], bv[nn]);
-        }
-#pragma unroll
-        for (int mm = 0; mm < 2; ++mm) {
-          const int R = R0 + 8 * mm + (lane >> 2);
-          if (R >= m2) continue;
-#pragma unroll
-          for (int nn = 0; nn < 4; ++nn)
-#pragma unroll
-            for (int e = 0; e < 2; ++e) {
-              const int C = C0 + 8 * nn + 2 * lk + e;
-              if (C < n2) A[(size_t)(c0 + w + C) * n + c0 + w + R] = acc[mm][nn][e];
-            }
-        }
+      const int twc = (n2 + 31) >> 5;
+      const bool defer = LB_LU_REGPANEL && c0 + KB < n && twc > 1;
+      trailing_update(c0, w, m2, n2, 0, defer ? 1 : twc, 0, NW);
+      if (defer) {
+        def_c0 = c0;
+        def_w = w;
+        def_m2 = m2;
+        def_n2 = n2;
+        def_twc = twc;
       }
     }
     __syncthreads();
