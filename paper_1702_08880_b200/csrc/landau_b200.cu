@@ -1564,8 +1564,14 @@ static int cn_factor_issue(lb_cn* cn, cudaStream_t st, bool pivot) {
         // 32-column slabs for the latency-bound small levels
         if (L.getrsL.count >= kLuWideMinCount && getrs_smem_bytes<kLuKB, 2 * kLuW>(nb) <= kLuSmemMax) {
           const dim3 g(L.getrsL.count, (2 * nb + 2 * kLuW - 1) / (2 * kLuW));
-          lb_getrs_slab_kernel<kLuKB, 2 * kLuW><<<g, kLuThreads, getrs_smem_bytes<kLuKB, 2 * kLuW>(nb), st>>>(
-              nb, 2 * nb, L.getrsL.A, L.perm, L.inv, L.getrsL.B);
+          // 16 warps when two update tiles per warp cover the block (nb <= 288:
+          // 64 accumulator registers instead of 192), else 8 warps
+          if (slab_mwt<kLuKB, 2 * kLuW, 512>(nb) <= 2)
+            lb_getrs_slab_kernel<kLuKB, 2 * kLuW, 512, 2><<<g, 512, getrs_smem_bytes<kLuKB, 2 * kLuW>(nb), st>>>(
+                nb, 2 * nb, L.getrsL.A, L.perm, L.inv, L.getrsL.B);
+          else
+            lb_getrs_slab_kernel<kLuKB, 2 * kLuW><<<g, kLuThreads, getrs_smem_bytes<kLuKB, 2 * kLuW>(nb), st>>>(
+                nb, 2 * nb, L.getrsL.A, L.perm, L.inv, L.getrsL.B);
         } else {
           const dim3 g(L.getrsL.count, (2 * nb + kLuW - 1) / kLuW);
           lb_getrs_slab_kernel<kLuKB, kLuW><<<g, kLuThreads, getrs_smem_bytes<kLuKB, kLuW>(nb), st>>>(
@@ -1976,7 +1982,9 @@ int lb_cn_create(lb_ctx* ctx, const lb_mesh* m, int S, int n, const int* indptr,
        cudaFuncSetAttribute(lb_getrs_slab_kernel<kLuKB, kLuW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             (int)getrs_smem_bytes<kLuKB, kLuW>(kLuMaxNb)) != cudaSuccess ||
        cudaFuncSetAttribute(lb_getrs_slab_kernel<kLuKB, 2 * kLuW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            (int)kLuSmemMax) != cudaSuccess))
+                            (int)kLuSmemMax) != cudaSuccess ||
+       cudaFuncSetAttribute(lb_getrs_slab_kernel<kLuKB, 2 * kLuW, 512, 2>,
+                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kLuSmemMax) != cudaSuccess))
     return bail(fail(LB_ECUDA, "cudaFuncSetAttribute(custom LU kernels) failed"));
   *out = cn;
   return LB_OK;

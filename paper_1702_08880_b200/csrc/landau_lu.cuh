@@ -691,10 +691,11 @@ __global__ void __launch_bounds__(kGetrfThreads) lb_getrf_kernel(int n, double* 
 
 // X := A^-1 X for X = the n x m column-major block at Xs[b] (leading
 // dimension n), A the factors of lb_getrf_kernel.  CTA (b, s) owns columns
-// [s W, s W + W).  Shared memory: the slab X [ld][W] (row-major: a row of W
-// columns is contiguous), the factor column block of the current step in
-// two k-halves H0/H1 [KB/2][ld] (column-major), the diagonal-block inverse
-// (two buffers) and the scaled block Y [KB][W].
+// [s W, s W + W).  Shared memory: the slab X [ld][W + 4] (row-major: a row
+// of W columns is contiguous), the factor column block of the current step
+// in two k-halves H0/H1 [KB/2][ldh] (column-major, only the rows the step
+// updates) and the diagonal-block inverse; the scaled block Y replaces the
+// block's rows of X in place.
 //
 // 2 np block steps (forward p = 0..np-1 with L, backward p = np-1..0 with U).
 // Step q:   Y = Di(q) X[block]   (X rows of the block := Y)
@@ -703,9 +704,24 @@ __global__ void __launch_bounds__(kGetrfThreads) lb_getrf_kernel(int n, double* 
 // The factor halves arrive by cp.async, each one phase ahead: H0 of step
 // q+1 streams in during the H1 pass of step q, H1 of step q+1 (and Di)
 // during the Di product of step q+1.
+// Shared-memory strides chosen so that the FP64 MMA fragment loads are bank
+// conflict free (a half-warp reads 4 k x 4 rows/columns of 8 bytes: the
+// k-stride must be 4 or 12 mod 16 doubles): X and Y rows of W + 4, the
+// diagonal-block inverse in columns of KB + 4, and the factor halves in
+// columns of slab_ldh(n) holding only the rows a step updates (at most
+// n - KB of them, stored from row 0).  (Strides of W, KB and lu_ld(n) made
+// the Di product and the update 4-way / 4-way / 2-way conflicted: 64 k + 125 k
+// of a 260-row slab's 252 k cycles.)
+template <int KB>
+__host__ __device__ constexpr int slab_ldh(int n) {
+  int r = ((n + KB - 1) / KB - 1) * KB;  // most rows a step updates: above the last (ragged) block
+  r = r < 16 ? 16 : r;
+  r = (r + 3) & ~3;              // even (16-byte copies of row pairs), multiple of 4
+  return (r & 7) == 4 ? r : r + 4;  // 4 or 12 mod 16
+}
 template <int KB, int W>
 inline size_t getrs_smem_bytes(int n) {
-  return sizeof(double) * ((size_t)lu_ld<KB>(n) * W + (size_t)KB * lu_ld<KB>(n) + KB * KB + KB * W);
+  return sizeof(double) * ((size_t)lu_ld<KB>(n) * (W + 4) + (size_t)KB * slab_ldh<KB>(n) + 16 + KB * (KB + 4));
 }
 
 __device__ __forceinline__ void cp_async8(double* dst, const double* src) {
@@ -721,18 +737,25 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
-template <int KB, int W, int NT = kLuThreads>
+// MWT: warp tiles (16 rows x 32 columns) of the update a warp may hold --
+// 0: sized for 383 rows; the host passes slab_mwt() when the block is small
+// enough for fewer (fewer accumulator registers).
+template <int KB, int W, int NT>
+__host__ __device__ constexpr int slab_mwt(int n) {
+  return ((((n + KB - 1) / KB - 1) * KB + 15) / 16 * (W / 32) + NT / 32 - 1) / (NT / 32);
+}
+template <int KB, int W, int NT = kLuThreads, int MWT = 0>
 __global__ void __launch_bounds__(NT) lb_getrs_slab_kernel(int n, int m, double* const* __restrict__ As,
                                                                    const int* __restrict__ perm_all,
                                                                    const double* __restrict__ inv_all,
                                                                    double* const* __restrict__ Xs) {
-  constexpr int KH = KB / 2, CG = W / 4;  // k-half, column groups of 4
+  constexpr int KH = KB / 2;  // k-half
   extern __shared__ __align__(16) double lu_sm[];
-  const int ld = lu_ld<KB>(n);
-  double* X = lu_sm;                       // [ld][W]
-  double* H[2] = {X + (size_t)ld * W, X + (size_t)ld * W + (size_t)KH * ld};  // [KH][ld] each
-  double* Dis = H[1] + (size_t)KH * ld;    // [KB][KB] (streamed in with the first half)
-  double* Y = Dis + KB * KB;               // [KB][W]
+  constexpr int XS = W + 4, DS = KB + 4;   // row stride of X and Y, column stride of Di (conflict-free)
+  const int ld = lu_ld<KB>(n), ldh = slab_ldh<KB>(n);
+  double* X = lu_sm;                       // [ld][XS]
+  double* H[2] = {X + (size_t)ld * XS, X + (size_t)ld * XS + (size_t)KH * ldh};  // [KH][ldh] each, rows from lo
+  double* Dis = H[1] + (size_t)KH * ldh + 16;  // [KB][DS] (streamed in with the first half; 16: tile reads past the last row)
   const int b = blockIdx.x, s = blockIdx.y, tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int col0 = s * W, wc = min(W, m - col0);
   if (wc <= 0) return;
@@ -762,17 +785,17 @@ __global__ void __launch_bounds__(NT) lb_getrs_slab_kernel(int n, int m, double*
       const int np2 = (hi - lo) >> 1;  // row pairs (hi - lo is even)
       for (int t = tid; t < k_end * np2; t += NT) {
         const int k = t / np2, i = lo + 2 * (t - k * np2);
-        cp_async16(dst + (size_t)k * ld + i, A + (size_t)(r0 + h * KH + k) * n + i);
+        cp_async16(dst + (size_t)k * ldh + (i - lo), A + (size_t)(r0 + h * KH + k) * n + i);
       }
     } else {
       for (int k = 0; k < k_end; ++k) {
         const double* src = A + (size_t)(r0 + h * KH + k) * n;
-        for (int i = lo + tid; i < hi; i += NT) cp_async8(dst + (size_t)k * ld + i, src + i);
+        for (int i = lo + tid; i < hi; i += NT) cp_async8(dst + (size_t)k * ldh + (i - lo), src + i);
       }
     }
     if (h == 0) {  // Di of step q: its buffer is free once step q-1's Di product is done
       const double* di = inv + (size_t)(q < np ? 2 * p : 2 * p + 1) * KB * KB;
-      for (int t = 2 * tid; t < KB * KB; t += 2 * NT) cp_async16(Dis + t, di + t);
+      for (int t = 2 * tid; t < KB * KB; t += 2 * NT) cp_async16(Dis + (t / KB) * DS + (t % KB), di + t);
     }
     cp_async_commit();
   };
@@ -787,9 +810,9 @@ __global__ void __launch_bounds__(NT) lb_getrs_slab_kernel(int n, int m, double*
     const int src = (i < n) ? (perm ? perm[i] : i) : 0;
     for (int c = 0; c < W; ++c) {
       if (i < n && c < wc)
-        cp_async8(X + (size_t)i * W + c, Xg + (size_t)c * n + src);
+        cp_async8(X + (size_t)i * XS + c, Xg + (size_t)c * n + src);
       else
-        X[(size_t)i * W + c] = 0.0;
+        X[(size_t)i * XS + c] = 0.0;
     }
   }
   cp_async_commit();
@@ -817,34 +840,30 @@ __global__ void __launch_bounds__(NT) lb_getrs_slab_kernel(int n, int m, double*
 #pragma unroll
       for (int k0 = 0; k0 < KB; k0 += 4) {
         const int k = k0 + lk;
-        const double av = Di[(size_t)k * KB + 8 * m + lr];
+        const double av = Di[(size_t)k * DS + 8 * m + lr];
 #pragma unroll
         for (int nn = 0; nn < TPW; ++nn) {
-          const double bv = k < kb ? X[(size_t)(r0 + k) * W + 8 * (n0 + nn) + lr] : 0.0;
+          const double bv = k < kb ? X[(size_t)(r0 + k) * XS + 8 * (n0 + nn) + lr] : 0.0;
           dmma_884(d[nn], av, bv);
         }
       }
+      __syncthreads();  // every warp has read the block's rows of X: they become Y in place
+      if (8 * m + lr < kb) {
 #pragma unroll
-      for (int nn = 0; nn < TPW; ++nn)
-        *reinterpret_cast<double2*>(Y + (size_t)(8 * m + lr) * W + 8 * (n0 + nn) + 2 * lk) =
-            make_double2(d[nn][0], d[nn][1]);
-    }
-    __syncthreads();
-    for (int t = tid; t < KB * CG; t += NT) {  // the block's rows of X become Y
-      const int yi = t / CG, yc = (t - (t / CG) * CG) * 4;
-      if (yi < kb) {
-        *reinterpret_cast<double2*>(X + (size_t)(r0 + yi) * W + yc) =
-            *reinterpret_cast<const double2*>(Y + (size_t)yi * W + yc);
-        *reinterpret_cast<double2*>(X + (size_t)(r0 + yi) * W + yc + 2) =
-            *reinterpret_cast<const double2*>(Y + (size_t)yi * W + yc + 2);
+        for (int nn = 0; nn < TPW; ++nn)
+          *reinterpret_cast<double2*>(X + (size_t)(r0 + 8 * m + lr) * XS + 8 * (n0 + nn) + 2 * lk) =
+              make_double2(d[nn][0], d[nn][1]);
       }
     }
+    __syncthreads();
+    const double* Y = X + (size_t)r0 * XS;  // [kb][XS]
     LU_T(2);
     // X[lo:hi] -= F Y in two k-halves on the FP64 tensor path: warp tiles of
     // 16 rows x 32 columns (2 x 4 MMA tiles of 8 x 8), acc kept across halves
     constexpr int CGW = W / 32;            // 32-column groups
     const int nr = hi - lo, nwt = ((nr + 15) >> 4) * CGW;
-    constexpr int kMaxWt = (24 * CGW + NT / 32 - 1) / (NT / 32);  // ceil(ceil(383 / 16) CGW / warps)
+    constexpr int kMaxWt = MWT ? MWT : (24 * CGW + NT / 32 - 1) / (NT / 32);  // ceil(ceil(383 / 16) CGW / warps)
+    LB_DCHECK(nwt <= kMaxWt * (NT / 32));
     double acc[kMaxWt][2][4][2];
 #pragma unroll
     for (int u = 0; u < kMaxWt; ++u)
@@ -856,7 +875,7 @@ __global__ void __launch_bounds__(NT) lb_getrs_slab_kernel(int n, int m, double*
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       const int k1 = min(kb, (h + 1) * KH);
-      const double* Hh = H[h] + lo;
+      const double* Hh = H[h];  // rows stored from lo
 #pragma unroll
       for (int u = 0; u < kMaxWt; ++u) {
         const int t = warp + u * (NT / 32);
@@ -868,9 +887,9 @@ __global__ void __launch_bounds__(NT) lb_getrs_slab_kernel(int n, int m, double*
           double av[2], bv[4];
 #pragma unroll
           for (int mm = 0; mm < 2; ++mm)
-            av[mm] = k < k1 ? Hh[(size_t)(kq + lk) * ld + 16 * wt + 8 * mm + lr] : 0.0;
+            av[mm] = k < k1 ? Hh[(size_t)(kq + lk) * ldh + 16 * wt + 8 * mm + lr] : 0.0;
 #pragma unroll
-          for (int nn = 0; nn < 4; ++nn) bv[nn] = Y[(size_t)k * W + 32 * cg + 8 * nn + lr];
+          for (int nn = 0; nn < 4; ++nn) bv[nn] = k < k1 ? Y[(size_t)k * XS + 32 * cg + 8 * nn + lr] : 0.0;
 #pragma unroll
           for (int mm = 0; mm < 2; ++mm)
 #pragma unroll
@@ -894,7 +913,7 @@ __global__ void __launch_bounds__(NT) lb_getrs_slab_kernel(int n, int m, double*
         if (R >= nr) continue;
 #pragma unroll
         for (int nn = 0; nn < 4; ++nn) {
-          double* xr = X + (size_t)(lo + R) * W + 32 * cg + 8 * nn + 2 * lk;
+          double* xr = X + (size_t)(lo + R) * XS + 32 * cg + 8 * nn + 2 * lk;
           const double2 x2 = *reinterpret_cast<const double2*>(xr);
           *reinterpret_cast<double2*>(xr) = make_double2(x2.x - acc[u][mm][nn][0], x2.y - acc[u][mm][nn][1]);
         }
@@ -909,7 +928,7 @@ __global__ void __launch_bounds__(NT) lb_getrs_slab_kernel(int n, int m, double*
   cp_async_wait<0>();
   __syncthreads();
   for (int c = 0; c < wc; ++c)
-    for (int i = tid; i < n; i += NT) Xg[(size_t)c * n + i] = X[(size_t)i * W + c];
+    for (int i = tid; i < n; i += NT) Xg[(size_t)c * n + i] = X[(size_t)i * XS + c];
 }
 
 // v := A^-1 v for one vector per block (the cyclic reduction's vector

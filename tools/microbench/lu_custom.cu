@@ -18,6 +18,9 @@
 #ifndef LU_NT
 #define LU_NT 256  // slab-solve threads
 #endif
+#ifndef LU_MWT
+#define LU_MWT 0  // slab-solve warp tiles per warp (0: sized for 383 rows)
+#endif
 #include "landau_lu.cuh"
 
 using namespace lb;
@@ -80,9 +83,9 @@ int main(int argc, char** argv) {
       cudaMalloc(&dB, sizeof(double*));
       cudaMemcpy(dB, &B, sizeof(double*), cudaMemcpyHostToDevice);
       const size_t ss = getrs_smem_bytes<KB, W>(n);
-      cudaFuncSetAttribute(lb_getrs_slab_kernel<KB, W, LU_NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ss);
+      cudaFuncSetAttribute(lb_getrs_slab_kernel<KB, W, LU_NT, LU_MWT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ss);
       cudaMemcpyToSymbol(lu_prof, z, sizeof(z));
-      lb_getrs_slab_kernel<KB, W, LU_NT><<<dim3(1, (2 * n + W - 1) / W), LU_NT, ss>>>(n, 2 * n, dA, perm, inv, dB);
+      lb_getrs_slab_kernel<KB, W, LU_NT, LU_MWT><<<dim3(1, (2 * n + W - 1) / W), LU_NT, ss>>>(n, 2 * n, dA, perm, inv, dB);
       cudaDeviceSynchronize();
       cudaMemcpyFromSymbol(h, lu_prof, sizeof(h));
       printf("prof getrs n=%d: wait+sync %lld DiX %lld update %lld writeback %lld sync+issue %lld cycles (%.1f us)\n", n,
@@ -147,7 +150,7 @@ int main(int argc, char** argv) {
         cudaMemcpy(dB, pb.data(), sizeof(double*) * batch, cudaMemcpyHostToDevice);
         const size_t sf = getrf_smem_bytes<KB>(n), ss = getrs_smem_bytes<KB, W>(n);
         cudaFuncSetAttribute(lb_getrf_kernel<KB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sf);
-        cudaFuncSetAttribute(lb_getrs_slab_kernel<KB, W, LU_NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ss);
+        cudaFuncSetAttribute(lb_getrs_slab_kernel<KB, W, LU_NT, LU_MWT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ss);
         const dim3 gs(batch, (m + W - 1) / W);
         float tc_f = 0, tc_s = 0, tb_f = 0, tb_s = 0;
         int hinfo = 0;
@@ -161,7 +164,7 @@ int main(int argc, char** argv) {
           cudaEventSynchronize(e1);
           cudaEventElapsedTime(&tc_f, e0, e1);
           cudaEventRecord(e0);
-          lb_getrs_slab_kernel<KB, W, LU_NT><<<gs, LU_NT, ss>>>(n, m, dA, perm, inv, dB);
+          lb_getrs_slab_kernel<KB, W, LU_NT, LU_MWT><<<gs, LU_NT, ss>>>(n, m, dA, perm, inv, dB);
           cudaEventRecord(e1);
           cudaEventSynchronize(e1);
           cudaEventElapsedTime(&tc_s, e0, e1);
