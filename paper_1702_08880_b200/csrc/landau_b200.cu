@@ -1500,6 +1500,7 @@ struct lb_cn {
   lb_ctx* ctx = nullptr;
   const lb_mesh* m = nullptr;
   int S = 0, n = 0, nb = 0, nblk = 0, npad = 0;
+  bool tri0 = false;       // level-0 L blocks upper, U blocks lower triangular (lb_bgemm_kernel's tri)
   long long nnz = 0, sstride = 0;  // sstride: block-pool doubles per species
   bool has_mass = false;
   bool co_valid = false;     // Co holds a C_old from an earlier lb_cn_newton
@@ -1550,6 +1551,9 @@ static int cn_factor_issue(lb_cn* cn, cudaStream_t st, bool pivot) {
   const int nb = cn->nb;
   const bool custom = cn_custom_lu(cn);
   for (const CnLevel& L : cn->lv) {
+    // level 0's couplings are the band's own blocks: triangular when every
+    // entry lies on its block's near side of the diagonal (cn->tri0)
+    const bool tri = cn->tri0 && &L == &cn->lv[0];
     if (custom) {
       // one CTA per odd-row block: LU (LAPACK layout, pivots, permutation,
       // diagonal-block inverses), then D^-1 [L U] by W-column slabs
@@ -1599,12 +1603,12 @@ static int cn_factor_issue(lb_cn* cn, cudaStream_t st, bool pivot) {
     const int gt = (nb + kGemmTile - 1) / kGemmTile, gt2 = (2 * nb + kGemmTile - 1) / kGemmTile;
     if (L.gemmEG.count) {
       lb_bgemm_kernel<<<dim3(gt * gt2, L.gemmEG.count), kGemmThreads, 0, st>>>(
-          nb, L.gemmEG.A, L.gemmEG.B, L.gemmEG.C, 0, L.gemmEG.C2, 1);
+          nb, L.gemmEG.A, L.gemmEG.B, L.gemmEG.C, 0, L.gemmEG.C2, 1, tri ? 1 : 0);
       LB_CUDA(cudaGetLastError());
     }
     if (L.gemmFH.count) {
       lb_bgemm_kernel<<<dim3(gt * gt2, L.gemmFH.count), kGemmThreads, 0, st>>>(
-          nb, L.gemmFH.A, L.gemmFH.B, L.gemmFH.C, 1, L.gemmFH.C2, 0);
+          nb, L.gemmFH.A, L.gemmFH.B, L.gemmFH.C, 1, L.gemmFH.C2, 0, tri ? 2 : 0);
       LB_CUDA(cudaGetLastError());
     }
   }
@@ -1922,6 +1926,7 @@ int lb_cn_create(lb_ctx* ctx, const lb_mesh* m, int S, int n, const int* indptr,
   // slot -> block pool offset (species 0): D[I] = block I, level-0 L_I / U_I
   // = blocks nblk + 2 I / + 1, column-major inside the block
   std::vector<long long> off(nnz);
+  bool tri0 = std::getenv("LB_CN_NO_TRI") == nullptr;
   for (int row = 0; row < n; ++row)
     for (int k = indptr[row]; k < indptr[row + 1]; ++k) {
       const int col = indices[k];
@@ -1930,8 +1935,8 @@ int lb_cn_create(lb_ctx* ctx, const lb_mesh* m, int S, int n, const int* indptr,
       const int I = pi / nb, J = pj / nb;
       long long id;
       if (J == I) id = I;
-      else if (J == I - 1) id = nblk + 2LL * I;
-      else if (J == I + 1) id = nblk + 2LL * I + 1;
+      else if (J == I - 1) id = nblk + 2LL * I, tri0 = tri0 && (pi % nb) <= (pj % nb);
+      else if (J == I + 1) id = nblk + 2LL * I + 1, tri0 = tri0 && (pj % nb) <= (pi % nb);
       else return fail(LB_EINVAL, "block size " + std::to_string(nb) + " is below the permuted bandwidth");
       off[k] = id * (long long)bsz + (long long)(pj % nb) * nb + (pi % nb);
     }
@@ -1942,6 +1947,7 @@ int lb_cn_create(lb_ctx* ctx, const lb_mesh* m, int S, int n, const int* indptr,
   cn->n = n;
   cn->nnz = nnz;
   cn->nb = nb;
+  cn->tri0 = tri0;
   cn->nblk = nblk;
   cn->npad = nb * nblk;
   auto bail = [&](int r) {

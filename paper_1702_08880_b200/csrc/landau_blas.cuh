@@ -78,10 +78,17 @@ __device__ __forceinline__ void gemm_load_tile(double* __restrict__ As, double* 
 // skipped).  The cyclic reduction's two products that share an A -- e.g.
 // L_k P^L (the next level's coupling, beta 0) and L_k P^U (the Schur update
 // of D_k, beta 1) -- are one launch reading A once.
+// tri: the structure of A the caller vouches for -- 0 dense, 1 upper
+// triangular (A[p][q] = 0 for p > q), 2 lower triangular (0 for q > p): the
+// couplings of the reduction's level 0 are the band's own off-diagonal
+// blocks, triangular when the block size covers the bandwidth.  The k-steps
+// that only meet A's zeros are skipped; the sums that remain are formed in
+// the same order, so the product is bitwise the dense one.
 __global__ void __launch_bounds__(kGemmThreads) lb_bgemm_kernel(int n, double* const* __restrict__ As_,
                                                                 double* const* __restrict__ Bs_,
                                                                 double* const* __restrict__ C0s_, int beta0,
-                                                                double* const* __restrict__ C1s_, int beta1) {
+                                                                double* const* __restrict__ C1s_, int beta1,
+                                                                int tri) {
   __shared__ __align__(16) double As[2][kGemmKT * kGemmLdA];
   __shared__ __align__(16) double Bs[2][kGemmTile * kGemmLdB];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -101,18 +108,23 @@ __global__ void __launch_bounds__(kGemmThreads) lb_bgemm_kernel(int n, double* c
   for (int a = 0; a < 4; ++a)
 #pragma unroll
     for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
-  const int nk = (n + kGemmKT - 1) / kGemmKT;
-  gemm_load_tile(As[0], Bs[0], A, B, n, nc, i0, j0, 0, even, tid);
-  for (int s = 0; s < nk; ++s) {
+  int ks = 0, nk = (n + kGemmKT - 1) / kGemmKT;
+  // rows i0 .. i0+63 of an upper triangular A are zero left of column i0,
+  // of a lower triangular one right of column i0+63
+  if (tri == 1) ks = i0 / kGemmKT;
+  else if (tri == 2) nk = min(nk, (i0 + kGemmTile + kGemmKT - 1) / kGemmKT);
+  gemm_load_tile(As[0], Bs[0], A, B, n, nc, i0, j0, ks * kGemmKT, even, tid);
+  for (int s = ks; s < nk; ++s) {
+    const int cur = (s - ks) & 1;
     if (s + 1 < nk) {
-      gemm_load_tile(As[(s + 1) & 1], Bs[(s + 1) & 1], A, B, n, nc, i0, j0, (s + 1) * kGemmKT, even, tid);
+      gemm_load_tile(As[cur ^ 1], Bs[cur ^ 1], A, B, n, nc, i0, j0, (s + 1) * kGemmKT, even, tid);
       cp_async_wait<1>();
     } else {
       cp_async_wait<0>();
     }
     __syncthreads();
-    const double* a_s = As[s & 1];
-    const double* b_s = Bs[s & 1];
+    const double* a_s = As[cur];
+    const double* b_s = Bs[cur];
 #pragma unroll
     for (int k4 = 0; k4 < kGemmKT; k4 += 4) {
       double av[4], bv[4];

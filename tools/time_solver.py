@@ -6,6 +6,7 @@ config 4 shared 64x128 Q2 mesh with four species.
 
     python tools/time_solver.py [cfg1 cfg3 cfg4]
 """
+import hashlib
 import sys
 import time
 from pathlib import Path
@@ -79,7 +80,7 @@ def main():
               f"device newton_step {min(td) * 1e3:.2f} ms  host (device assembly + splu) "
               f"{min(th) * 1e3:.2f} ms  x{min(th) / min(td):.1f}  rel diff {err:.1e}  rnorm {rnorm:.3e}"
               f"  device phases (assemble, residual+fill, LU, solve) {np.round(ph, 2).tolist()} ms"
-              f"  solver {s.stats()}")
+              f"  solver {s.stats()}  sha1(f_next) {hashlib.sha1(np.ascontiguousarray(dev).tobytes()).hexdigest()[:12]}")
 
 
 if __name__ == "__main__":
