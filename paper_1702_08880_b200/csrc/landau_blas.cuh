@@ -108,6 +108,11 @@ __global__ void __launch_bounds__(kGemmThreads) lb_bgemm_kernel(int n, double* c
   for (int a = 0; a < 4; ++a)
 #pragma unroll
     for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+  // 8 x 8 MMA tiles of this warp's 32 x 32 sub-tile that hold rows / columns
+  // of the product (a prefix of the four; edge tiles of a 260-row block are
+  // 4 rows of 64: the all-padding MMA tiles are skipped, warp-uniformly)
+  const int na = min(4, max(0, (n - (i0 + wr) + 7) >> 3));
+  const int nbt = min(4, max(0, (nc - (j0 + wc) + 7) >> 3));
   int ks = 0, nk = (n + kGemmKT - 1) / kGemmKT;
   // rows i0 .. i0+63 of an upper triangular A are zero left of column i0,
   // of a lower triangular one right of column i0+63
@@ -125,17 +130,22 @@ __global__ void __launch_bounds__(kGemmThreads) lb_bgemm_kernel(int n, double* c
     __syncthreads();
     const double* a_s = As[cur];
     const double* b_s = Bs[cur];
+    const int kv = min(kGemmKT, n - s * kGemmKT);  // k-columns of this step inside the matrix
 #pragma unroll
     for (int k4 = 0; k4 < kGemmKT; k4 += 4) {
+      if (k4 >= kv) break;  // zero padding only
       double av[4], bv[4];
 #pragma unroll
       for (int a = 0; a < 4; ++a) av[a] = a_s[(k4 + lk) * kGemmLdA + wr + 8 * a + lr];
 #pragma unroll
       for (int b = 0; b < 4; ++b) bv[b] = b_s[(wc + 8 * b + lr) * kGemmLdB + k4 + lk];
 #pragma unroll
-      for (int a = 0; a < 4; ++a)
+      for (int a = 0; a < 4; ++a) {
+        if (a >= na) break;
 #pragma unroll
-        for (int b = 0; b < 4; ++b) dmma_884(acc[a][b], av[a], bv[b]);
+        for (int b = 0; b < 4; ++b)
+          if (b < nbt) dmma_884(acc[a][b], av[a], bv[b]);
+      }
     }
     __syncthreads();
   }
