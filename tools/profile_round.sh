@@ -25,5 +25,8 @@ python tools/time_solver.py > $O/${TAG}_solver.log 2>&1 && \
       python tools/time_solver.py cfg4 > $O/${TAG}_solver_ncu.log 2>&1 && \
   ncu --set full --clock-control none --import-source on -k 'regex:lb_getrf_kernel|lb_getrs_slab_kernel|lb_bgemm_kernel' \
       -s 20 -c 3 -o $O/${TAG}_lu -f python tools/time_solver.py cfg4 > $O/${TAG}_lu_ncu.log 2>&1
+# the reduction's level-0 launches (256 blocks at config 4): the first four LU-phase kernels
+ncu --set full --clock-control none --import-source on -k 'regex:lb_getrf_kernel|lb_getrs_slab_kernel|lb_bgemm_kernel' \
+    -s 0 -c 4 -o $O/${TAG}_lu_level0 -f python tools/time_solver.py cfg4 > $O/${TAG}_lu_level0_ncu.log 2>&1
 python tools/rank_shares.py 65536 5 > $O/${TAG}_rank_shares.log 2>&1
 echo done
