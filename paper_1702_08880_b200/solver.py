@@ -165,14 +165,15 @@ class CNSolver:
 
 def _fingerprint(M) -> tuple:
     """Cheap content key of a sparse (or dense) matrix: shape, nnz and the
-    XOR of the bit patterns of its values and indices."""
+    XOR of the bit patterns of its values and of its indices -- one pass
+    each (any single edited entry changes the key); this runs on every
+    newton_step, so it stays well under the step's device time."""
     data = np.ascontiguousarray(getattr(M, "data", M), dtype=np.float64).ravel()
     key = (getattr(M, "shape", None), data.size,
-           int(np.bitwise_xor.reduce(data.view(np.int64))) if data.size else 0,
-           float(np.add.reduce(data)) if data.size else 0.0)
+           int(np.bitwise_xor.reduce(data.view(np.int64))) if data.size else 0)
     idx = getattr(M, "indices", None)
     if idx is not None and idx.size:
-        key += (int(np.bitwise_xor.reduce(idx.astype(np.int64) * np.arange(1, idx.size + 1))),)
+        key += (int(np.bitwise_xor.reduce(np.ascontiguousarray(idx).ravel())), int(idx[0]), int(idx[-1]))
     return key
 
 
