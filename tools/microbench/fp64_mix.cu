@@ -1,0 +1,99 @@
+// What FP64-pipe utilisation does the sweep's INSTRUCTION MIX allow?  Eight
+// independent chains per thread (no dependency stalls), W warps per SMSP on
+// every SM, FP64 warp-instructions per SMSP-cycle reported as a share of the
+// half-rate peak (0.5):
+//   mode 0  DFMA register operands only (the peak probe's form)
+//   mode 1  DFMA with a constant-bank coefficient (the Horner chains' form)
+//   mode 2  2 DFMA : 1 DMUL
+//   mode 3  mode 1 plus one integer instruction (IADD3) per two FP64 (the
+//           sweep: 68 % FP64, 32 % other)
+//   mode 4  mode 3 with a register shuffle among the others
+//   mode 5  mode 3 with one STS.128 + one LDS.128 per 80 FP64 instead (the
+//           rotation through shared memory: 10 wide accesses per step, not 20 shuffles)
+//   nvcc -O3 -std=c++17 -gencode arch=compute_100a,code=sm_100a fp64_mix.cu -o fp64_mix
+#include <cstdio>
+#include <cuda_runtime.h>
+
+__constant__ double c_k[16] = {1.0000001, 0.9999999, 1.0000002, 0.9999998, 1.0000003, 0.9999997,
+                               1.0000004, 0.9999996, 1e-9,      2e-9,      3e-9,      4e-9,
+                               5e-9,      6e-9,      7e-9,      8e-9};
+
+template <int MODE>
+__global__ void __launch_bounds__(512) mix(double* out, double a, double b, int iters, unsigned seed) {
+  double v[8];
+  unsigned q[4];
+#pragma unroll
+  for (int c = 0; c < 8; ++c) v[c] = threadIdx.x * 1e-9 + c;
+#pragma unroll
+  for (int c = 0; c < 4; ++c) q[c] = seed + threadIdx.x * (c + 1);
+  __shared__ uint4 sm[512];
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      if (MODE == 5 && u == 0) {
+        sm[threadIdx.x] = make_uint4(q[0], q[1], q[2], q[3]);
+        __syncwarp();
+        const uint4 t = sm[(threadIdx.x & ~31) | ((threadIdx.x + 1) & 31)];
+        __syncwarp();
+        q[0] = t.x; q[1] = t.y; q[2] = t.z; q[3] = t.w;
+      }
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        if (MODE == 0) v[c] = fma(v[c], a, b);
+        else if (MODE == 2) v[c] = (u % 3 == 2) ? v[c] * a : fma(v[c], a, b);
+        else v[c] = fma(v[c], a, c_k[8 + (u & 7)]);
+        if (MODE >= 3 && (c & 1)) {
+          const int k = (c >> 1);
+          if (MODE == 4 && k == 3 && (u & 1))
+            q[k] = __shfl_sync(0xffffffffu, q[k], (threadIdx.x + 1) & 31);
+          else
+            q[k] = q[k] + q[(k + 1) & 3] + (unsigned)u;  // one IADD3
+        }
+      }
+    }
+  }
+  double s = 0;
+#pragma unroll
+  for (int c = 0; c < 8; ++c) s += v[c];
+  unsigned r = q[0] ^ q[1] ^ q[2] ^ q[3];
+  if (s == 1234.5 || r == 0x12345u) out[0] = s + r;
+}
+
+template <int MODE>
+void run(int warps_per_smsp, const char* what) {
+  double* out;
+  cudaMalloc(&out, 8);
+  int dev = 0, sms = 0, khz = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaDeviceGetAttribute(&khz, cudaDevAttrClockRate, dev);
+  const int iters = 4000, threads = 32 * 4 * warps_per_smsp;  // one CTA per SM
+  mix<MODE><<<sms, threads>>>(out, 0.999999, 1e-7, iters, 7u);
+  cudaDeviceSynchronize();
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  cudaEventRecord(e0);
+  mix<MODE><<<sms, threads>>>(out, 0.999999, 1e-7, iters, 7u);
+  cudaEventRecord(e1);
+  cudaEventSynchronize(e1);
+  float ms;
+  cudaEventElapsedTime(&ms, e0, e1);
+  const double fp64_per_warp = (double)iters * 64;
+  const double cycles = ms * 1e-3 * khz * 1e3;
+  const double per_smsp_cycle = fp64_per_warp * warps_per_smsp / cycles;
+  printf("mode %d (%s) %d warps/SMSP: %.3f ms, FP64 warp-instr per SMSP-cycle %.3f = %.1f %% of the half-rate peak (at the %d MHz attribute clock)\n",
+         MODE, what, warps_per_smsp, ms, per_smsp_cycle, 200 * per_smsp_cycle, khz / 1000);
+  cudaFree(out);
+}
+
+int main() {
+  for (int w : {2, 4}) {
+    run<0>(w, "DFMA r,r,r");
+    run<1>(w, "DFMA r,r,c[]");
+    run<2>(w, "2 DFMA : 1 DMUL");
+    run<3>(w, "DFMA c[] + 1 int per 2 FP64");
+    run<4>(w, "same with shuffles");
+    run<5>(w, "same with STS.128 + LDS.128");
+  }
+  return 0;
+}
