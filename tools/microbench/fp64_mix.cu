@@ -8,6 +8,9 @@
 //   mode 3  mode 1 plus one integer instruction (IADD3) per two FP64 (the
 //           sweep: 68 % FP64, 32 % other)
 //   mode 4  mode 3 with a register shuffle among the others
+//   mode 6  mode 3 plus 4 shuffles per 80 FP64 whose results are first used a
+//           whole loop iteration later (no exposed shuffle latency: the sweep's
+//           rotated sums are next touched at the end of the following step)
 //   mode 5  mode 3 with one STS.128 + one LDS.128 per 80 FP64 instead (the
 //           rotation through shared memory: 10 wide accesses per step, not 20 shuffles)
 //   nvcc -O3 -std=c++17 -gencode arch=compute_100a,code=sm_100a fp64_mix.cu -o fp64_mix
@@ -27,9 +30,13 @@ __global__ void __launch_bounds__(512) mix(double* out, double a, double b, int 
 #pragma unroll
   for (int c = 0; c < 4; ++c) q[c] = seed + threadIdx.x * (c + 1);
   __shared__ uint4 sm[512];
+  unsigned w4[4] = {seed, seed + 1, seed + 2, seed + 3}, w4n[4] = {0, 0, 0, 0};
   for (int i = 0; i < iters; ++i) {
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
+      if (MODE == 6 && (u & 1)) {  // 4 shuffles per 8 u-iterations, consumed at the loop's end
+        w4n[u >> 1] = __shfl_sync(0xffffffffu, w4[u >> 1], (threadIdx.x + 1) & 31);
+      }
       if (MODE == 5 && u == 0) {
         sm[threadIdx.x] = make_uint4(q[0], q[1], q[2], q[3]);
         __syncwarp();
@@ -51,10 +58,15 @@ __global__ void __launch_bounds__(512) mix(double* out, double a, double b, int 
         }
       }
     }
+    if (MODE == 6) {
+#pragma unroll
+      for (int k = 0; k < 4; ++k) w4[k] = w4n[k] + 1u;
+    }
   }
   double s = 0;
 #pragma unroll
   for (int c = 0; c < 8; ++c) s += v[c];
+  q[0] ^= w4[0] ^ w4[1] ^ w4[2] ^ w4[3];
   unsigned r = q[0] ^ q[1] ^ q[2] ^ q[3];
   if (s == 1234.5 || r == 0x12345u) out[0] = s + r;
 }
@@ -94,6 +106,7 @@ int main() {
     run<3>(w, "DFMA c[] + 1 int per 2 FP64");
     run<4>(w, "same with shuffles");
     run<5>(w, "same with STS.128 + LDS.128");
+    run<6>(w, "mode 3 + 4 shuffles consumed a loop later");
   }
   return 0;
 }
